@@ -1,0 +1,426 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (-m "not gpu").
+
+Every oracle function is pinned by at least one of: a value the paper/spec prints
+(tests/golden/*), a closed form, an invariant, a special case that reduces to a
+library routine (torch SDPA in float64), or brute force on tiny inputs written
+as plain Python loops (an independent implementation, not a re-call).
+"""
+import json
+import math
+import os
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import kvtier_oracle as O
+from paper_2605_09490_b200.synth import synth as S
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+# ------------------------------------------------------------ Eq. 2 / Eq. 3
+def test_single_key_weight_is_one():
+    assert O.attention_weights([0.3, -1.0], [[5.0, 2.0]]).tolist() == [1.0]
+
+
+def test_identical_keys_uniform():
+    w = O.attention_weights([1.0, 2.0, 3.0], [[0.5, 0.1, 0.2]] * 4)
+    assert np.allclose(w, 0.25, rtol=0, atol=1e-15)
+
+
+def test_d2_hand_softmax():
+    # q=(1,0), keys (1,0),(0,1): logits 1/sqrt2 and 0; weight_0 = logistic(1/sqrt2)
+    w = O.attention_weights([1.0, 0.0], [[1.0, 0.0], [0.0, 1.0]])
+    x = 1.0 / math.sqrt(2.0)
+    w0 = 0.5 * (1.0 + math.tanh(x / 2.0))                  # logistic via tanh (independent form)
+    assert abs(w[0] - w0) < 1e-15 and abs(w[1] - (1.0 - w0)) < 1e-15
+    assert abs(w0 - 0.6697615493266569) < 1e-12             # hand-evaluated value
+
+
+def test_one_pair_and_identical_values():
+    v = [0.25, -1.5, 3.0]
+    assert O.attention_output([1.0, 1.0, 1.0], [[0.1, 0.2, 0.3]], [v]).tolist() == v
+    rng = np.random.default_rng(0)
+    out = O.attention_output(rng.normal(size=3), rng.normal(size=(7, 3)), [v] * 7)
+    assert np.allclose(out, v, rtol=0, atol=1e-14)
+
+
+def _brute_attention(q, K, V, skip=()):
+    """Plain double loop (independent implementation)."""
+    d = len(q)
+    idx = [i for i in range(len(K)) if i not in skip]
+    logits = {}
+    for i in idx:
+        s = 0.0
+        for k in range(d):
+            s += q[k] * K[i][k]
+        logits[i] = s / math.sqrt(d)
+    m = max(logits.values())
+    Z = sum(math.exp(logits[i] - m) for i in idx)
+    out = [0.0] * len(V[0])
+    for i in idx:
+        a = math.exp(logits[i] - m) / Z
+        for k in range(len(out)):
+            out[k] += a * V[i][k]
+    return out
+
+
+def test_attention_bruteforce_5_tokens():
+    rng = random.Random(5)
+    q = [rng.uniform(-2, 2) for _ in range(4)]
+    K = [[rng.uniform(-2, 2) for _ in range(4)] for _ in range(5)]
+    V = [[rng.uniform(-2, 2) for _ in range(3)] for _ in range(5)]
+    assert np.allclose(O.attention_output(q, K, V), _brute_attention(q, K, V), rtol=0, atol=1e-13)
+
+
+def test_eq3_empty_eviction_is_bitwise_eq2():
+    rng = np.random.default_rng(1)
+    q, K, V = rng.normal(size=8), rng.normal(size=(9, 8)), rng.normal(size=(9, 8))
+    assert np.array_equal(O.evicted_attention_output(q, K, V, []), O.attention_output(q, K, V))
+
+
+def test_eq3_single_survivor_and_bruteforce():
+    rng = np.random.default_rng(2)
+    q, K, V = rng.normal(size=4), rng.normal(size=(6, 4)), rng.normal(size=(6, 3))
+    out = O.evicted_attention_output(q, K, V, [0, 1, 2, 4, 5])
+    assert np.allclose(out, V[3], rtol=0, atol=1e-15)
+    out = O.evicted_attention_output(q, K, V, [1, 4])   # "evict {2,5}" 1-based
+    ref = _brute_attention(q.tolist(), K.tolist(), V.tolist(), skip=(1, 4))
+    assert np.allclose(out, ref, rtol=0, atol=1e-13)
+    with pytest.raises(ValueError):
+        O.evicted_attention_output(q, K, V, range(6))
+
+
+def test_eq4_bound_sound_equal_norms_1000_instances():
+    """Eq. 4 as printed holds when every value row has the same norm (then
+    ||o_hat|| <= ||v||), and the always-valid triangle bound holds everywhere."""
+    rng = np.random.default_rng(3)
+    worst = 0.0
+    for _ in range(1000):
+        n, d = rng.integers(2, 64), rng.integers(1, 16)
+        q, K = rng.normal(size=d) * 2, rng.normal(size=(n, d))
+        V = rng.normal(size=(n, d))
+        V /= np.linalg.norm(V, axis=1, keepdims=True)
+        ev = [i for i in range(n) if rng.random() < 0.3][: n - 1]
+        a = O.attention_weights(q, K)
+        err = np.linalg.norm(O.evicted_attention_output(q, K, V, ev) - a @ V)
+        bound = O.eviction_error_bound(a, V, ev)
+        assert err <= bound + 1e-12
+        assert err <= O.eviction_error_bound_triangle(a, V, ev) + 1e-12
+        worst = max(worst, err / bound if bound > 0 else 0)
+    assert worst > 0.05          # the bound is exercised, not vacuous
+
+
+def test_eq4_counterexample_and_triangle_bound():               # reading R-EQ4
+    """Eq. 4 is not a bound for arbitrary values: golden counterexample (3 tokens)."""
+    g = _golden("eq4_counterexample.json")
+    q, K, V, ev = (np.array(g[k], dtype=np.float64) for k in ("q", "K", "V", "evicted"))
+    ev = ev.astype(int).tolist()
+    a = O.attention_weights(q, K)
+    err = np.linalg.norm(O.evicted_attention_output(q, K, V, ev) - a @ V)
+    assert err > O.eviction_error_bound(a, V, ev) * 1.5          # Eq. 4 violated
+    assert err <= O.eviction_error_bound_triangle(a, V, ev) + 1e-12
+    rng = np.random.default_rng(33)
+    for _ in range(1000):                                        # triangle bound: always
+        n, d = rng.integers(2, 64), rng.integers(1, 16)
+        q, K, V = rng.normal(size=d) * 2, rng.normal(size=(n, d)), rng.normal(size=(n, d)) * rng.uniform(0.1, 3, size=(n, 1))
+        ev = [i for i in range(n) if rng.random() < 0.3][: n - 1]
+        a = O.attention_weights(q, K)
+        err = np.linalg.norm(O.evicted_attention_output(q, K, V, ev) - a @ V)
+        assert err <= O.eviction_error_bound_triangle(a, V, ev) + 1e-12
+
+
+def test_eq4_single_eviction_instantiation():
+    rng = np.random.default_rng(4)
+    q, K, V = rng.normal(size=5), rng.normal(size=(7, 5)), rng.normal(size=(7, 5))
+    a = O.attention_weights(q, K)
+    assert O.eviction_error_bound(a, V, [3]) == pytest.approx(2 * a[3] * np.linalg.norm(V[3]), rel=1e-15)
+    assert O.eviction_error_bound(a, V, []) == 0.0
+
+
+def test_masked_attention_matches_torch_sdpa_float64():       # library routine (SDPA)
+    rng = np.random.default_rng(5)
+    q, K, V = rng.normal(size=(1, 64)), rng.normal(size=(40, 64)), rng.normal(size=(40, 64))
+    ev = [2, 7, 8, 30]
+    mask = torch.ones(1, 40, dtype=torch.bool)
+    mask[0, ev] = False
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.from_numpy(q)[None], torch.from_numpy(K)[None], torch.from_numpy(V)[None],
+        attn_mask=mask[None])[0, 0].numpy()
+    assert np.allclose(O.evicted_attention_output(q[0], K, V, ev), ref, rtol=0, atol=1e-13)
+
+
+# ------------------------------------------------------------ LSE merge
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 8])
+def test_lse_merge_equals_unsplit(k):
+    rng = np.random.default_rng(10 + k)
+    q, K, V = rng.normal(size=16) * 3, rng.normal(size=(97, 16)), rng.normal(size=(97, 16))
+    cuts = np.linspace(0, 97, k + 1).astype(int)
+    parts = [O.partial_softmax(q, K[a:b], V[a:b]) for a, b in zip(cuts[:-1], cuts[1:])]
+    assert np.allclose(O.lse_merge(parts), O.attention_output(q, K, V), rtol=0, atol=1e-13)
+
+
+# ------------------------------------------------------------ T2 codec (AMB-12)
+def test_int8_zero_row_exact():
+    c, s = O.quantize_int8(np.zeros(16, np.float32))
+    assert s == np.float32(1.0) and not c.any()
+    assert not O.dequantize_int8(c, s).any()
+
+
+def test_int8_absmax_maps_to_127_and_exact_grid():
+    x = np.array([127.0, -3.0, 64.0, -127.0, 0.0], np.float32)
+    c, s = O.quantize_int8(x)
+    assert s == np.float32(1.0)
+    assert c.tolist() == [127, -3, 64, -127, 0]
+    assert np.array_equal(O.dequantize_int8(c, s), x)
+
+
+def test_int8_round_trip_bound_half_scale():                 # S:94 (tighter: scale/2)
+    rng = np.random.default_rng(6)
+    for _ in range(200):
+        x = S.bf16_bits_to_f32(S.f32_to_bf16_bits(rng.normal(size=128).astype(np.float32) * rng.uniform(0.01, 10)))
+        c, s = O.quantize_int8(x)
+        assert np.max(np.abs(c.astype(int))) == 127
+        err = np.abs(O.dequantize_int8(c, s).astype(np.float64) - x.astype(np.float64))
+        assert np.all(err <= float(s) * (0.5 + 2e-5))        # + fp32 rounding of x/scale and code*scale
+
+
+def test_bf16_rounding_matches_torch():                      # library routine
+    rng = np.random.default_rng(7)
+    x = (rng.normal(size=100000) * np.exp(rng.normal(size=100000) * 3)).astype(np.float32)
+    ref = torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(O.f32_to_bf16_value(x), ref)
+    assert np.array_equal(S.bf16_bits_to_f32(S.f32_to_bf16_bits(x)), ref)
+
+
+# ------------------------------------------------------------ protected set / counts
+def test_protected_set_spec_example():                       # S:261 (AMB-6)
+    g = _golden("protected_set.json")
+    for case in g["cases"]:
+        m = O.protected_mask(case["n"], case["P"], case["k_s"], case["k_w"])
+        assert int(m.sum()) == case["size"], case
+        if "ranges" in case:
+            want = np.zeros(case["n"], bool)
+            for a, b in case["ranges"]:
+                want[a:b] = True
+            assert np.array_equal(m, want)
+
+
+def test_tier_counts_golden():                                # S:270, SURVEY §8d table, AMB-8
+    g = _golden("tier_counts.json")
+    for c in g["cases"]:
+        got = O.tier_counts(c["n_protected"], c["n_live"], c["n_t3"], c["hbm_bp"],
+                            c["evict_bp"], c.get("t2_bp", 0), c.get("mode", 0))
+        assert list(got) == c["expect"], c
+
+
+def test_floor_is_exact_integer_not_float():                  # AMB-8: 0.7*90 = 62.999.. in double
+    assert math.floor(0.7 * 90) == 62
+    assert O.tier_counts(0, 90, 0, 7000, 0, 0)[1] == 63
+
+
+def _brute_classify(S_list, tier_old, n, P, ks, kw, hbm_bp, evict_bp, t2_bp, mode):
+    """Independent loop implementation of Alg. 1 lines P:189-197 + AMB rules."""
+    prot = set(range(min(P, n))) | set(range(P, min(P + ks, n))) | set(range(max(0, n - kw), n))
+    t3_old = [i for i in range(n) if tier_old[i] == 3]
+    live = [i for i in range(n) if i not in prot and tier_old[i] != 3]
+    live.sort(key=lambda i: (S_list[i], i))     # float order == bit order for S >= 0
+    if mode == 0:
+        n_new = max(0, (evict_bp * (len(live) + len(t3_old))) // 10000 - len(t3_old))
+    else:
+        n_new = (evict_bp * len(live)) // 10000
+    surv = live[n_new:]
+    n_hbm = (hbm_bp * len(surv)) // 10000
+    n_t2 = (t2_bp * (len(surv) - n_hbm)) // 10000
+    out = [0] * n
+    for i in t3_old + live[:n_new]:
+        out[i] = 3
+    for j, i in enumerate(surv):
+        if j < n_t2:
+            out[i] = 2
+        elif j < len(surv) - n_hbm:
+            out[i] = 1
+        else:
+            out[i] = 0
+    return out
+
+
+@pytest.mark.parametrize("kind", ["ties", "cont"])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_classify_matches_bruteforce(kind, mode):
+    cfg = O.OracleConfig(B=3, L=1, Hq=4, Hkv=2, d=8, prompt_len=16, hbm_bp=5000,
+                         evict_bp=1000, t2_bp=5000, evict_mode=mode)
+    Sp = S.gen_scores(11, 3, 2, 600, kind)
+    for b in range(3):
+        tier = np.zeros(600, np.uint8)
+        for n in (150, 420, 600):                       # three successive events
+            new = O.classify_request(Sp[b], tier, n, cfg)
+            S_tot = [float(np.float32(Sp[b, 0, i]) + np.float32(Sp[b, 1, i])) for i in range(n)]
+            ref = _brute_classify(S_tot, tier[:n].tolist(), n, 16, 4, 128, 5000, 1000, 5000, mode)
+            assert new.tolist() == ref
+            # permanence: old T3 stays T3
+            assert np.all(new[tier[:n] == 3] == 3)
+            tier[:n] = new
+            Sp[b] += np.float32(0.5)     # scores evolve between events
+
+
+def test_classify_invariants_and_budget():
+    cfg = O.OracleConfig(B=1, L=1, Hq=2, Hkv=1, d=8, prompt_len=64, hbm_bp=3000, evict_bp=300)
+    Sp = S.gen_scores(12, 1, 1, 2000, "cont")
+    new = O.classify_request(Sp[0], np.zeros(2000, np.uint8), 2000, cfg)
+    prot = O.protected_mask(2000, 64, 4, 128)
+    assert np.all(new[prot] == 0)
+    cnt = np.bincount(new, minlength=4)
+    # SURVEY §8d 7B r=3% beta=30%: |P|=196 |U|=1804 n_evict=54 n_hbm=525 T1=1225
+    assert cnt.tolist() == [196 + 525, 1225, 0, 54]
+    # evicted are the lowest-scored non-protected tokens
+    S_tot = Sp[0, 0]
+    assert S_tot[new == 3].max() <= S_tot[(new != 3) & ~prot].min()
+    assert S_tot[(new == 0) & ~prot].min() >= S_tot[new == 1].max()
+
+
+def test_r0_beta100_all_t0():
+    cfg = O.OracleConfig(B=1, L=1, Hq=2, Hkv=1, d=8, prompt_len=8, hbm_bp=10000, evict_bp=0)
+    new = O.classify_request(S.gen_scores(3, 1, 1, 500)[0], np.zeros(500, np.uint8), 500, cfg)
+    assert np.all(new == 0)
+
+
+# ------------------------------------------------------------ full decode loop
+def _tiny_run(hbm_bp=5000, evict_bp=500, t2_bp=0, interval=64, steps=32, mode=0, L=1):
+    w = S.WORKLOADS["tiny"]
+    n0 = w["N"] - 1
+    K = S.gen_kv(w["seed"], "k", L, w["B"], w["Hkv"], w["d"], 0, n0 + steps, w["P"], 4)
+    V = S.gen_kv(w["seed"], "v", L, w["B"], w["Hkv"], w["d"], 0, n0 + steps, w["P"], 4)
+    Q = S.gen_q(w["seed"], 0, steps, L, w["B"], w["Hq"], w["Hkv"], w["d"])
+    cfg = O.OracleConfig(B=w["B"], L=L, Hq=w["Hq"], Hkv=w["Hkv"], d=w["d"], prompt_len=w["P"],
+                         manage_interval=interval, hbm_bp=hbm_bp, evict_bp=evict_bp,
+                         t2_bp=t2_bp, evict_mode=mode)
+    st = O.init_state(cfg, K, V, n0)
+    outs, t3s = [], []
+    for t in range(steps):
+        outs.append(O.decode_step(st, Q[t]))
+        t3s.append(O.export_index(st, 0, 3))
+    return st, outs, t3s, (K, V, Q)
+
+
+def test_tiny_first_event_counts():                           # SURVEY §8d tiny row
+    st, _, _, _ = _tiny_run(steps=1)
+    assert O.census(st, 0).tolist() == [148 + 51, 52, 0, 5]
+
+
+def test_prop1_bitwise_over_beta():                           # Prop. 1
+    runs = [_tiny_run(hbm_bp=b, interval=8, steps=32) for b in (3000, 5000, 7000)]
+    for st, outs, t3s, _ in runs[1:]:
+        for a, b in zip(outs, runs[0][1]):
+            assert np.array_equal(a, b)
+        for a, b in zip(t3s, runs[0][2]):
+            assert np.array_equal(a, b)
+    # the T0/T1 split really differs between the runs
+    assert O.census(runs[0][0], 0)[1] != O.census(runs[2][0], 0)[1]
+
+
+def test_r0_equals_full_attention_sdpa():                     # Prop. 1 + north star pin
+    st, outs, _, (K, V, Q) = _tiny_run(hbm_bp=3000, evict_bp=0, interval=8, steps=20)
+    n0 = 255
+    for t in (0, 9, 19):
+        n = n0 + t + 1
+        k = torch.from_numpy(S.bf16_bits_to_f32(K[0, 0, :, :n]).astype(np.float64))   # [Hkv][n][d]
+        v = torch.from_numpy(S.bf16_bits_to_f32(V[0, 0, :, :n]).astype(np.float64))
+        q = torch.from_numpy(S.bf16_bits_to_f32(Q[t, 0, 0]).astype(np.float64))       # [Hq][d]
+        G = 2
+        ref = torch.nn.functional.scaled_dot_product_attention(
+            q[:, None, :], k.repeat_interleave(G, 0), v.repeat_interleave(G, 0))[:, 0].numpy()
+        assert np.allclose(outs[t][0, 0], ref, rtol=0, atol=1e-12)
+
+
+def test_score_mass_and_monotone():                            # north star "sum = steps x heads"
+    st, _, _, _ = _tiny_run(interval=8, steps=32)
+    total = float(np.sum(st.S_part[0].astype(np.float64)))
+    assert abs(total - 32 * 4 * 1) <= 1e-5 * 32 * 4            # t * H_q * L
+    st2, _, _, _ = _tiny_run(interval=8, steps=31)
+    assert np.all(st.S_part[0][:, :st2.n] >= st2.S_part[0][:, :st2.n])
+
+
+def test_score_update_bruteforce_tiny():                        # S:151 brute force
+    """Nested-loop Eq. 1 (S = sum over layers, heads of alpha) on a 2-layer run with
+    no eviction; compares the fp32 scores within 1e-6 rel."""
+    w = S.WORKLOADS["tiny"]
+    L, steps, n0 = 2, 3, 40
+    K = S.gen_kv(7, "k", L, 1, 2, 64, 0, n0 + steps, 16, 4)
+    V = S.gen_kv(7, "v", L, 1, 2, 64, 0, n0 + steps, 16, 4)
+    Q = S.gen_q(7, 0, steps, L, 1, 4, 2, 64)
+    cfg = O.OracleConfig(B=1, L=L, Hq=4, Hkv=2, d=64, prompt_len=16, hbm_bp=5000, evict_bp=0)
+    st = O.init_state(cfg, K, V, n0)
+    for t in range(steps):
+        O.decode_step(st, Q[t], manage=False)
+    Kf, Qf = S.bf16_bits_to_f32(K), S.bf16_bits_to_f32(Q)
+    ref = [0.0] * (n0 + steps)
+    for t in range(steps):
+        n = n0 + t + 1
+        for l in range(L):
+            for h in range(4):
+                g = h // 2
+                z = [sum(float(Qf[t, l, 0, h, k]) * float(Kf[l, 0, g, i, k]) for k in range(64)) / 8.0
+                     for i in range(n)]
+                m = max(z)
+                Z = sum(math.exp(x - m) for x in z)
+                for i in range(n):
+                    ref[i] += math.exp(z[i] - m) / Z
+    got = O.total_score_fp32(st.S_part[0])[: n0 + steps].astype(np.float64)
+    assert np.allclose(got, ref, rtol=1e-6, atol=0)
+    assert abs(sum(ref) - steps * L * 4) < 1e-9
+
+
+def test_t2_variant_rows_and_codec():                           # AMB-11/12 stores
+    st, outs, _, (K, V, Q) = _tiny_run(t2_bp=5000, interval=8, steps=32)
+    cnt = O.census(st, 0)
+    assert cnt[2] > 0
+    Kf = S.bf16_bits_to_f32(K)
+    for p in O.export_index(st, 0, 2):
+        for g in range(2):
+            c, s = O.quantize_int8(st.rowK[0, 0, g, p])
+            assert np.array_equal(c, st.codeK[0, 0, g, p]) and s == st.scaleK[0, 0, g, p]
+    # T0/T1 rows: the original generator bytes, or (token passed through T2) the
+    # bf16 of a dequantised row -- one to three codec round trips (AMB-12)
+    for tier in (0, 1):
+        for p in O.export_index(st, 0, tier):
+            for g in range(2):
+                x, ok = Kf[0, 0, g, p], False
+                for _ in range(4):
+                    if np.array_equal(st.rowK[0, 0, g, p], x):
+                        ok = True
+                        break
+                    x = O.f32_to_bf16_value(O.dequantize_int8(*O.quantize_int8(x)))
+                assert ok, (tier, p, g)
+    assert np.isfinite(outs[-1]).all()
+
+
+def test_migration_rows_equal_generator_when_f2_zero():         # "migration is a copy"
+    st, _, _, (K, V, Q) = _tiny_run(interval=8, steps=32)
+    Kf, Vf = S.bf16_bits_to_f32(K), S.bf16_bits_to_f32(V)
+    for tier in (0, 1):
+        idx = O.export_index(st, 0, tier)
+        assert np.array_equal(st.rowK[:, 0, :, idx], Kf[:, 0, :, idx])
+        assert np.array_equal(st.rowV[:, 0, :, idx], Vf[:, 0, :, idx])
+
+
+def test_generator_long_tail_calibration():                     # P:76 (top-20% -> 56.5%)
+    """Recipe calibration: 7B head shapes, 2 layers, 64 steps, r=0."""
+    L, steps, n0 = 2, 24, 1999
+    K = S.gen_kv(2, "k", L, 1, 4, 128, 0, n0 + steps, 64, 4)
+    V = S.gen_kv(2, "v", L, 1, 4, 128, 0, n0 + steps, 64, 4)
+    Q = S.gen_q(2, 0, steps, L, 1, 28, 4, 128)
+    cfg = O.OracleConfig(B=1, L=L, Hq=28, Hkv=4, d=128, prompt_len=64, evict_bp=0)
+    st = O.init_state(cfg, K, V, n0)
+    for t in range(steps):
+        O.decode_step(st, Q[t], manage=False)
+    s = np.sort(O.total_score_fp32(st.S_part[0][:, :st.n]))[::-1]
+    share = s[: len(s) // 5].sum() / s.sum()
+    assert 0.50 < share < 0.66, share
