@@ -1,0 +1,216 @@
+/*
+ * kv_tier.h -- C ABI of the B200 (sm_100a) tiered-KV decode hot path of
+ * arXiv 2605.09490, "Semantics-aware four-tier KV memory hierarchy".
+ *
+ * Citations: P:n = PAPER.md line n (section / equation / algorithm named),
+ * AMB-k = the reading of an ambiguous passage adopted in DESIGN.md.
+ *
+ * The per-decode-step path (Alg. 1):
+ *   kv_tier_begin_step            new position n joins T0 (window)
+ *   kv_tier_append      (layer)   its K/V row of layer l -> T0 store           (a1)
+ *   kv_tier_prefetch    (layer)   T1 rows -> HBM staging (stream mode)         (a2)
+ *   kv_tier_decode_attention (l)  GQA attention over T0+T1+T2 (Eq. 3, Prop. 1) (a3)
+ *                                 + fused cumulative score update (Eq. 1)      (a4)
+ *   kv_tier_end_step              t += 1
+ *   kv_tier_classify              every Delta steps: tiers T0..T3              (a5)
+ *   kv_tier_migrate               apply tier transitions to the stores         (a6)
+ *
+ * Conventions (all functions):
+ *   - Return kv_tier_status: 0 = OK, < 0 = error.  No aborts, no exceptions.
+ *     Argument errors are detected synchronously (E_INVAL / E_STATE / E_CAPACITY).
+ *     Asynchronous CUDA errors and the device-side numeric flag (non-finite
+ *     probability or score, AMB-2) surface at the next call that synchronises
+ *     (kv_tier_sync / census / export) as E_CUDA / E_NUMERIC.
+ *     kv_tier_last_error() returns a message for the last failure.
+ *   - Every device call is asynchronous and stream-ordered on the stream passed
+ *     (a cudaStream_t, passed as void*; NULL = legacy default stream).
+ *   - Pointers marked "device" must be device-accessible, 16-byte aligned,
+ *     contiguous, and are owned by the caller; the library never frees them.
+ *   - bf16 = IEEE bfloat16 bit patterns (uint16).  Positions are 0-based (AMB-6).
+ *   - One ctx per (process, device); a ctx is not thread-safe.
+ */
+#ifndef KV_TIER_H_
+#define KV_TIER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define KV_TIER_API __attribute__((visibility("default")))
+#else
+#define KV_TIER_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KV_TIER_OK = 0,
+  KV_TIER_E_INVAL = -1,     /* bad argument / shape mismatch, empty visible set */
+  KV_TIER_E_CUDA = -2,      /* CUDA runtime error (possibly from an earlier async launch) */
+  KV_TIER_E_NCCL = -3,      /* reserved: collective failure */
+  KV_TIER_E_STATE = -4,     /* call out of order (e.g. migrate without classify) */
+  KV_TIER_E_CAPACITY = -5,  /* a tier store would overflow its capacity */
+  KV_TIER_E_OOM = -6,       /* host pinned allocation failed */
+  KV_TIER_E_NUMERIC = -7    /* non-finite probability or score seen on device (AMB-2) */
+} kv_tier_status;
+
+/* Eviction budget semantics (AMB-9). TOTAL: |T3| = floor(r * |U_all|) over the run;
+ * PER_EVENT: literal Alg. 1, n_evict = floor(r * |U|) at every event. */
+typedef enum { KV_TIER_EVICT_TOTAL = 0, KV_TIER_EVICT_PER_EVENT = 1 } kv_tier_evict_mode;
+
+/* Multi-GPU partitioning.  REQUEST: each rank owns B requests (no
+ * collective in the step).  KVHEAD / SEQUENCE are reserved for later rounds. */
+typedef enum { KV_TIER_SHARD_REQUEST = 0, KV_TIER_SHARD_KVHEAD = 1, KV_TIER_SHARD_SEQUENCE = 2 } kv_tier_shard;
+
+#define KV_TIER_STAGING_ALL 0xFFFFFFFFu   /* differential mode: staging holds all of T1 (§3.4) */
+
+typedef struct {
+  int32_t  num_requests;     /* B  (this rank's requests)                            */
+  int32_t  num_layers;       /* L                                                     */
+  int32_t  num_q_heads;      /* H_q                                                   */
+  int32_t  num_kv_heads;     /* H_kv; q head h reads kv head h / (H_q/H_kv) (AMB-4)   */
+  int32_t  head_dim;         /* d in {64, 128}                                        */
+  int32_t  max_tokens;       /* N_max per request: positions [0, N_max)               */
+  int32_t  prompt_len;       /* P (protected)                                  */
+  int32_t  sink_size;        /* k_s = 4                              */
+  int32_t  window_size;      /* k_w = 128                             */
+  int32_t  manage_interval;  /* Delta = 64; informative, the caller schedules */
+  uint32_t hbm_ratio_bp;     /* beta in basis points (AMB-8)                   */
+  uint32_t evict_ratio_bp;   /* r in basis points                              */
+  uint32_t t2_fraction_bp;   /* f2: share of offloaded survivors placed in T2 (AMB-11) */
+  int32_t  evict_mode;       /* kv_tier_evict_mode                                    */
+  uint32_t staging_tokens;   /* KV_TIER_STAGING_ALL = differential (paper §3.4);
+                                0 = stream mode: T1 rows re-fetched from pinned host
+                                memory every step (strict DDR residency, AMB-13)      */
+  int32_t  device;           /* CUDA device ordinal                                   */
+  int32_t  rank, world, shard;
+  int32_t  out_fp32;         /* 1: o is fp32 [B][H_q][d]; 0: bf16                      */
+  int32_t  split;            /* CTAs per (request, kv head) cluster; 0 = auto          */
+} kv_tier_config;
+
+typedef struct kv_tier_ctx kv_tier_ctx;
+
+typedef struct {
+  size_t device_arena;       /* bytes of device memory the caller must provide         */
+  size_t t0_store, t1_staging, t2_store, scores, meta;   /* breakdown (informative)    */
+  size_t host_t1, host_t2;   /* pinned host bytes the library allocates                */
+  int32_t cap_t0, cap_t1, cap_t2;                        /* rows per (l, b, g)          */
+} kv_tier_sizes;
+
+typedef struct {
+  void* device_arena;        /* device, >= sizes.device_arena bytes, 256-B aligned     */
+} kv_tier_buffers;
+
+/* Validate cfg and report the memory it needs.  Capacities (rows per layer, request and
+ * kv head): T0 = N_max (the prefill prefix starts all-T0); T1 staging and the T2
+ * store = the offloaded share ceil((1-beta) N_max) (+ f2 share for T2).  Stores are
+ * double-buffered: migrate rebuilds the next buffer from the current one. */
+KV_TIER_API kv_tier_status kv_tier_query_sizes(const kv_tier_config* cfg, kv_tier_sizes* out);
+
+/* Create a ctx over caller-owned device memory; pins host T1/T2 stores
+ * (cudaHostAlloc, mapped).  nccl_unique_id must be NULL (request sharding has
+ * no collective on the step). */
+KV_TIER_API kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* buf,
+                            const void* nccl_unique_id, kv_tier_ctx** out);
+KV_TIER_API kv_tier_status kv_tier_destroy(kv_tier_ctx* ctx);
+
+/* Initial chain (prefill result, Alg. 1): positions [0, n0) of layer `layer`
+ * all enter T0 with score 0.  k, v: device bf16 [B][H_kv][n0][d].  Must be called
+ * for every layer with the same n0 before the first begin_step. */
+KV_TIER_API kv_tier_status kv_tier_load_prefix(kv_tier_ctx* ctx, int32_t layer, const void* k, const void* v,
+                                   int32_t n0, void* stream);
+
+/* Start decode step t: position n (the new token, Alg. 1) joins T0 and the
+ * window (protected).  E_CAPACITY if T0 or N_max would overflow. */
+KV_TIER_API kv_tier_status kv_tier_begin_step(kv_tier_ctx* ctx, void* stream);
+
+/* a1: write the new token's K/V of layer `layer`.  k_new, v_new: device bf16 [B][H_kv][d]. */
+KV_TIER_API kv_tier_status kv_tier_append(kv_tier_ctx* ctx, int32_t layer, const void* k_new, const void* v_new,
+                              void* stream);
+
+/* a2 (stream mode only; no-op in differential mode): gather layer `layer`'s T1 rows
+ * from pinned host memory into a 2-slot HBM staging ring on `side` (zero-copy
+ * reads over the host link), layer-ahead.  decode_attention(layer) waits on it. */
+KV_TIER_API kv_tier_status kv_tier_prefetch(kv_tier_ctx* ctx, int32_t layer, void* side);
+
+/* a3 + a4: o[b][h] = sum_{i visible} softmax_i(q[b][h].k_i / sqrt d) v_i with
+ * visible = T0 u T1 u T2 (T3 masked, Eq. 3; T2 rows dequantised,
+ * AMB-12), and, if fuse_score_update, S_part[b][g][i] += sum_{h in g} p_{b,h,i}
+ * from the exact, globally normalised probabilities (Eq. 1, AMB-1/14/15).
+ * q: device bf16 [B][H_q][d]; o: device [B][H_q][d] fp32 (out_fp32) or bf16. */
+KV_TIER_API kv_tier_status kv_tier_decode_attention(kv_tier_ctx* ctx, int32_t layer, const void* q, void* o,
+                                        int32_t fuse_score_update, void* stream);
+
+/* a4 standalone (external probabilities, e.g. from another attention kernel):
+ * probs: device fp32 [B][H_q][n_vis] over the visible tokens in ascending position
+ * order; S_part[b][g][i] += fp32(sum_{h in g} probs[b][h][j(i)]).  n_vis is
+ * returned by kv_tier_visible_count. */
+KV_TIER_API kv_tier_status kv_tier_score_update(kv_tier_ctx* ctx, int32_t layer, const float* probs, void* stream);
+KV_TIER_API kv_tier_status kv_tier_visible_count(const kv_tier_ctx* ctx, int32_t* n_vis);
+
+KV_TIER_API kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream);
+
+/* One whole decode step: begin_step; for every layer l: [prefetch], append, decode_attention;
+ * end_step.  q: device bf16 [L][B][H_q][d]; k_new, v_new: device bf16 [L][B][H_kv][d];
+ * o: device [L][B][H_q][d] (fp32 or bf16 per out_fp32).  `side` carries stream-mode prefetch. */
+KV_TIER_API kv_tier_status kv_tier_step(kv_tier_ctx* ctx, const void* q, const void* k_new, const void* v_new,
+                                        void* o, int32_t fuse_score_update, void* stream, void* side);
+/* Capture kv_tier_step over fixed buffers as a CUDA graph (stream must not be the legacy
+ * default stream); kv_tier_step_graph_launch replays it as one decode step.  Kernels read
+ * the step/tier counters from device memory, so one graph serves every step; the caller
+ * refills q / k_new / v_new before each launch and runs classify/migrate outside it. */
+KV_TIER_API kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const void* k_new,
+                                                      const void* v_new, void* o, int32_t fuse_score_update,
+                                                      void* stream, void* side);
+KV_TIER_API kv_tier_status kv_tier_step_graph_launch(kv_tier_ctx* ctx, void* stream);
+
+/* a5: per request, protected set P = [0,P) u [P,P+k_s) u [n-k_w,n); the live
+ * non-protected tokens ordered by the unique key (fp32 bits of S_i, i) ascending
+ * (AMB-7); n_new = bottom -> T3 (AMB-8/9), top floor(beta|surv|) -> T0, lowest
+ * floor(f2 * rest) -> T2, remainder -> T1 (Alg. 1).  Idempotent until migrate. */
+KV_TIER_API kv_tier_status kv_tier_classify(kv_tier_ctx* ctx, void* stream);
+
+/* a6: apply the transitions of the last classify: T0<->T1 copies, ->T2 int8
+ * quantisation (AMB-12), T2-> bf16 of the dequantised row, ->T3 dropped.
+ * Newly offloaded rows are written to the pinned host store on `side`.  E_STATE
+ * without a preceding classify. */
+KV_TIER_API kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side);
+
+/* Synchronise the device and report async errors (E_CUDA, E_NUMERIC). */
+KV_TIER_API kv_tier_status kv_tier_sync(kv_tier_ctx* ctx);
+
+/* counts: host int32 [B][4] = |T0|,|T1|,|T2|,|T3| over positions [0, n) (App. D);
+ * d2h_rows: host int64, rows written to the host stores so far (may be NULL). Synchronises. */
+KV_TIER_API kv_tier_status kv_tier_census(kv_tier_ctx* ctx, int32_t* counts, int64_t* d2h_rows);
+
+/* Host-side state (no sync): current sequence length n and step t. */
+KV_TIER_API kv_tier_status kv_tier_position(const kv_tier_ctx* ctx, int32_t* n, int32_t* t);
+
+/* ---- test hooks: canonical, layout-independent exports (synchronise) -------- */
+enum {
+  KV_TIER_X_SCORES = 0,     /* fp32 [B][H_kv][n]   S_part (AMB-1)                        */
+  KV_TIER_X_TIERS = 1,      /* u8   [B][n]                                                */
+  KV_TIER_X_IDX_T0 = 2,     /* i32  [B][|T0|] positions in store order (ascending)         */
+  KV_TIER_X_IDX_T1 = 3,     /* i32  [B][|T1|]                                              */
+  KV_TIER_X_IDX_T2 = 4,     /* i32  [B][|T2|]                                              */
+  KV_TIER_X_T0_ROWS = 5,    /* bf16 [B][H_kv][|T0|][2][d]  (K,V) in idx order, layer       */
+  KV_TIER_X_T1_ROWS = 6,    /* bf16 [B][H_kv][|T1|][2][d]  from the pinned host store      */
+  KV_TIER_X_STAGING = 7,    /* bf16 [B][H_kv][|T1|][2][d]  HBM staging (differential mode) */
+  KV_TIER_X_T2_CODES = 8,   /* i8   [B][H_kv][|T2|][2][d]                                  */
+  KV_TIER_X_T2_SCALES = 9   /* f32  [B][H_kv][|T2|][2]                                     */
+};
+/* Bytes `what` needs (counts are uniform across requests). */
+KV_TIER_API kv_tier_status kv_tier_export_size(kv_tier_ctx* ctx, int32_t what, size_t* bytes);
+KV_TIER_API kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, void* host_dst, size_t bytes);
+/* Overwrite S_part with host fp32 [B][H_kv][n] (classify cross-feed, AMB-18). Synchronises. */
+KV_TIER_API kv_tier_status kv_tier_import_scores(kv_tier_ctx* ctx, const float* host_S, size_t bytes);
+
+KV_TIER_API const char* kv_tier_last_error(const kv_tier_ctx* ctx);
+KV_TIER_API const char* kv_tier_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KV_TIER_H_ */

@@ -295,6 +295,24 @@ def decode_layer(st, l, qbits_l):
     return o
 
 
+def visible_positions(st, b):
+    """Ascending positions of request b that attention sees: tier != T3 (Eq. 3)."""
+    return np.nonzero(st.tier[b, :st.n] != T3)[0]
+
+
+def score_update_external(S_part_b, vis, probs_b, G):
+    """Eq. 1 with externally supplied probabilities (Alg. 1, AMB-14):
+    S_part[g][vis[j]] = fp32(S_part[g][vis[j]] + fp32(sum_{h in g} probs[h][j])).
+    S_part_b: [H_kv][N] fp32 (updated in place); probs_b: [H_q][len(vis)]."""
+    Hkv = S_part_b.shape[0]
+    for g in range(Hkv):
+        inc = np.zeros(len(vis), dtype=np.float64)
+        for h in range(g * G, (g + 1) * G):
+            inc += np.asarray(probs_b[h], dtype=np.float64)
+        S_part_b[g, vis] = (S_part_b[g, vis] + inc.astype(np.float32)).astype(np.float32)
+    return S_part_b
+
+
 def manage_event(st):
     """Classify every request then migrate its rows (Alg. 1, AMB-11/12).
 

@@ -1,0 +1,44 @@
+"""Build the in-tree CUDA libraries for sm_100a (called by __graft_entry__.build()).
+
+    libkvtier.so  -- the product: C-ABI tiered-KV decode path (include/kv_tier.h)
+    libkvsynth.so -- seeded synthetic-input generator (include/kv_synth.h), test plumbing
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(HERE, "lib")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-Xcompiler", "-fvisibility=hidden"]
+
+TARGETS = {
+    "libkvtier.so": ["csrc/ctx.cu", "csrc/attn.cu", "csrc/tiers.cu"],
+    "libkvsynth.so": ["synth/synth.cu"],
+}
+DEPS = ["csrc/kv_internal.cuh", "../include/kv_tier.h", "../include/kv_synth.h"]
+
+
+def _stale(out, srcs):
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(os.path.join(HERE, s)) > t for s in srcs + DEPS)
+
+
+def build(force=False, verbose=False):
+    os.makedirs(LIB_DIR, exist_ok=True)
+    for name, srcs in TARGETS.items():
+        out = os.path.join(LIB_DIR, name)
+        if not force and not _stale(out, srcs):
+            continue
+        cmd = [NVCC, *ARCH, *FLAGS, "-o", out, *[os.path.join(HERE, s) for s in srcs]]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+    return LIB_DIR
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

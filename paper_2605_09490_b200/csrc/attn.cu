@@ -1,0 +1,448 @@
+// a3 + a4: GQA decode attention over the visible tiers with the fused cumulative
+// score update (Eq. 1, Eq. 3, Prop. 1).
+//
+// One thread-block cluster of C CTAs per (request b, kv head g); CTA r of the cluster
+// owns a contiguous chunk of the visible tokens [T0 rows | T1 staging rows | T2 rows].
+//
+//   phase A  K tiles (cp.async 4-stage ring, XOR-swizzled SMEM) -> S^T = K q^T on the
+//            tensor cores (mma.sync m16n8k16 bf16, swap-AB: tokens = M, heads = N = 8);
+//            logits (log2 domain) kept in SMEM for the whole chunk, running max.
+//   phase B  V tiles -> p = exp2(z - m_local) -> o^T += V^T p^T on the tensor cores
+//            (P moved C-fragment -> B-fragment with movmatrix.trans).
+//   merge    (m, l, o) of the C CTAs exchanged through distributed shared memory
+//            (no HBM round trip); each CTA writes a 1/C slice of o.
+//   score    exact globally-normalised p_i = exp2(z_i - M)/L re-derived from the SMEM
+//            logits; S_part[b][g][pos_i] += sum_{h in g} p_{h,i}  (one fp32 add per
+//            layer, AMB-14).  Every (b, g, pos) is owned by exactly one CTA: no atomics.
+//
+// HBM traffic per launch = the algorithmic bytes: every visible K/V row once,
+// q, o, and 8 B of score RMW per visible token per kv head.
+#include "kv_internal.cuh"
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
+
+namespace kvt {
+
+constexpr int ATT_THREADS = 128;   // 4 warps, 16 tokens each per tile
+constexpr int TILE = 64;           // tokens per pipeline stage
+constexpr int NST = 4;             // pipeline depth
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int nbytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(nbytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);   // .x (low 16 bits) = lo
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ uint32_t i8pair_to_bf16x2(uint32_t word, int k) {
+  // bytes 2k, 2k+1 of `word` (signed) -> bf16x2 (exact: |code| <= 127)
+  const float lo = (float)(int8_t)((word >> (16 * k)) & 0xFF);
+  const float hi = (float)(int8_t)((word >> (16 * k + 8)) & 0xFF);
+  return pack_bf16(lo, hi);
+}
+
+template <int D>
+struct AttnSmem {
+  static constexpr int ROWB = D * 2;
+  static constexpr int TILEB = TILE * ROWB;
+};
+
+template <int D>
+__global__ void __launch_bounds__(ATT_THREADS, 2)
+    k_decode_attn(const DevView v, const int layer, const __nv_bfloat16* __restrict__ q,
+                  void* __restrict__ o, const int fuse) {
+  constexpr int ROWB = AttnSmem<D>::ROWB;
+  constexpr int TILEB = AttnSmem<D>::TILEB;
+  constexpr int KS = D / 16;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int r = (int)cluster.block_rank();
+  const int unit = blockIdx.y;
+  const int b = unit / v.Hkv, g = unit - b * v.Hkv;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int G = v.G;
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* ring = smem;
+  float* zs = reinterpret_cast<float*>(smem + NST * TILEB);   // [chunk_max][8]
+  float* xo = zs + (size_t)v.chunk_max * 8;                   // [8][D]   exchange: o partial
+  float* xm = xo + 8 * D;                                      // [8]      exchange: max (log2)
+  float* xl = xm + 8;                                          // [8]      exchange: sum
+  float* red = xl + 8;                                         // [2][4][8] warp max / warp l
+  float* sML = red + 64;                                       // [16] merged M, 1/L
+  float* t2sc = sML + 16;                                      // [TILE] T2 row scales
+  unsigned char* t2buf = reinterpret_cast<unsigned char*>(t2sc + TILE);   // [TILE][D] bf16 (T2 only)
+
+  const int cur = v.st->cur;
+  const int* cn = v.cnt[cur] + b * CNT_STRIDE;
+  const int n0 = cn[0], n1 = cn[1], n2 = cn[2];
+  const int n01 = n0 + n1, nvis = n01 + n2;
+  const int chunk = (nvis + C - 1) / C;
+  const int vbeg = min(r * chunk, nvis), vend = min(vbeg + chunk, nvis);
+  const int aend = min(vend, n01);                  // bf16 segment [vbeg, aend)
+  const int t2beg = max(vbeg, n01);                 // int8 segment [t2beg, vend)
+  const int nb = max(0, aend - vbeg);
+  const int nt = (nb + TILE - 1) / TILE;
+
+  const size_t grp = grp_of(v, layer, b, g);
+  const __nv_bfloat16* K0 = v.k0[cur] + grp * v.cap0 * D;
+  const __nv_bfloat16* V0 = v.v0[cur] + grp * v.cap0 * D;
+  const __nv_bfloat16* K1;
+  const __nv_bfloat16* V1;
+  if (v.stream_mode) {
+    const size_t sg = ((size_t)(layer & 1) * v.B + b) * v.Hkv + g;
+    K1 = v.k1[0] + sg * v.cap1 * D;
+    V1 = v.v1[0] + sg * v.cap1 * D;
+  } else {
+    K1 = v.k1[cur] + grp * v.cap1 * D;
+    V1 = v.v1[cur] + grp * v.cap1 * D;
+  }
+
+  // ---- stage the first tiles while q is loaded
+  auto load_tile = [&](int i) {
+    const bool isV = i >= nt;
+    const int tv0 = vbeg + (isV ? i - nt : i) * TILE;
+    const __nv_bfloat16* S0 = isV ? V0 : K0;
+    const __nv_bfloat16* S1 = isV ? V1 : K1;
+    const uint32_t sbase = smem_u32(ring + (i % NST) * TILEB);
+    constexpr int CPR = D / 8;                // 16-B chunks per row
+    constexpr int RPP = ATT_THREADS / CPR;    // rows per pass
+    const int c = tid % CPR, r0 = tid / CPR;
+#pragma unroll
+    for (int p = 0; p < TILE / RPP; ++p) {
+      const int row = r0 + p * RPP;
+      const int tok = tv0 + row;
+      const __nv_bfloat16* src = S0;
+      int nbytes = 0;
+      if (tok < aend) {
+        nbytes = 16;
+        src = tok < n0 ? S0 + (size_t)tok * D : S1 + (size_t)(tok - n0) * D;
+      }
+      cp_async16(sbase + row * ROWB + ((c ^ (row & 7)) << 4), src + c * 8, nbytes);
+    }
+  };
+  const int total = 2 * nt;
+#pragma unroll
+  for (int s = 0; s < NST - 1; ++s) {
+    if (s < total) load_tile(s);
+    cp_commit();
+  }
+
+  uint32_t qf[KS][2];
+  {
+    const __nv_bfloat16* qh = q + ((size_t)b * v.Hq + g * G + gq) * D;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      if (gq < G) {
+        qf[ks][0] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 2 * tq);
+        qf[ks][1] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 8 + 2 * tq);
+      } else {
+        qf[ks][0] = 0u;
+        qf[ks][1] = 0u;
+      }
+    }
+  }
+  const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));   // log2(e)/sqrt(d)
+
+  float mx0 = -INFINITY, mx1 = -INFINITY;    // running max, heads 2tq, 2tq+1
+  float l0 = 0.f, l1 = 0.f;
+  float oacc[KS][4];
+#pragma unroll
+  for (int mt = 0; mt < KS; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
+
+  // QK^T for one warp's 16 tokens of a tile staged at sbase; row scale `rs` (T2) or 1
+  auto qk_warp = [&](uint32_t sbase, int tv0, int tend, const float* rsc) {
+    if (tv0 + w * 16 >= tend) return;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int mi = lane >> 3, ii = lane & 7;
+    const int row = w * 16 + ii + ((mi & 1) << 3);
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int ch = 2 * ks + (mi >> 1);
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4(a0, a1, a2, a3, sbase + row * ROWB + ((ch ^ (row & 7)) << 4));
+      mma16816(acc, a0, a1, a2, a3, qf[ks][0], qf[ks][1]);
+    }
+    const int r0 = w * 16 + gq, r1 = r0 + 8;
+    const int t0 = tv0 + r0, t1 = tv0 + r1;
+    if (t0 < tend) {
+      const float f = rsc ? rsc[r0] * sl2 : sl2;
+      const float z0 = acc[0] * f, z1 = acc[1] * f;
+      *reinterpret_cast<float2*>(&zs[(t0 - vbeg) * 8 + 2 * tq]) = make_float2(z0, z1);
+      mx0 = fmaxf(mx0, z0);
+      mx1 = fmaxf(mx1, z1);
+    }
+    if (t1 < tend) {
+      const float f = rsc ? rsc[r1] * sl2 : sl2;
+      const float z0 = acc[2] * f, z1 = acc[3] * f;
+      *reinterpret_cast<float2*>(&zs[(t1 - vbeg) * 8 + 2 * tq]) = make_float2(z0, z1);
+      mx0 = fmaxf(mx0, z0);
+      mx1 = fmaxf(mx1, z1);
+    }
+  };
+  float m2a = 0.f, m2b = 0.f;   // CTA max for heads 2tq, 2tq+1
+  auto pv_warp = [&](uint32_t sbase, int tv0, int tend, const float* rsc) {
+    if (tv0 + w * 16 >= tend) return;
+    const int r0 = w * 16 + gq, r1 = r0 + 8;
+    const int t0 = tv0 + r0, t1 = tv0 + r1;
+    float p00 = 0.f, p01 = 0.f, p10 = 0.f, p11 = 0.f;
+    if (t0 < tend) {
+      const float2 z = *reinterpret_cast<const float2*>(&zs[(t0 - vbeg) * 8 + 2 * tq]);
+      p00 = exp2f(z.x - m2a);
+      p01 = exp2f(z.y - m2b);
+    }
+    if (t1 < tend) {
+      const float2 z = *reinterpret_cast<const float2*>(&zs[(t1 - vbeg) * 8 + 2 * tq]);
+      p10 = exp2f(z.x - m2a);
+      p11 = exp2f(z.y - m2b);
+    }
+    l0 += p00 + p10;
+    l1 += p01 + p11;
+    if (rsc) {   // T2: o += p * scale_v * code  (codes are exact in bf16)
+      p00 *= rsc[r0]; p01 *= rsc[r0];
+      p10 *= rsc[r1]; p11 *= rsc[r1];
+    }
+    const uint32_t b0 = movm_t(pack_bf16(p00, p01));
+    const uint32_t b1 = movm_t(pack_bf16(p10, p11));
+    const int mi = lane >> 3, ii = lane & 7;
+    const int row = w * 16 + ii + ((mi >> 1) << 3);
+#pragma unroll
+    for (int mt = 0; mt < KS; ++mt) {
+      const int ch = 2 * mt + (mi & 1);
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4_t(a0, a1, a2, a3, sbase + row * ROWB + ((ch ^ (row & 7)) << 4));
+      mma16816(oacc[mt], a0, a1, a2, a3, b0, b1);
+    }
+  };
+  // int8 T2 rows: codes -> bf16 (exact) into the swizzled t2buf, scales -> t2sc
+  auto stage_t2 = [&](int tv0, bool isV) {
+    const int8_t* C2 = (isV ? v.c2v[cur] : v.c2k[cur]) + grp * v.cap2 * D;
+    const float* S2 = (isV ? v.s2v[cur] : v.s2k[cur]) + grp * v.cap2;
+    for (int e = tid; e < TILE * (D / 16); e += ATT_THREADS) {
+      const int row = e / (D / 16), j = e % (D / 16);
+      const int tok = tv0 + row;
+      uint4 cw = make_uint4(0u, 0u, 0u, 0u);
+      if (tok < vend) cw = *reinterpret_cast<const uint4*>(C2 + (size_t)(tok - n01) * D + 16 * j);
+      uint4 lo, hi;
+      lo.x = i8pair_to_bf16x2(cw.x, 0); lo.y = i8pair_to_bf16x2(cw.x, 1);
+      lo.z = i8pair_to_bf16x2(cw.y, 0); lo.w = i8pair_to_bf16x2(cw.y, 1);
+      hi.x = i8pair_to_bf16x2(cw.z, 0); hi.y = i8pair_to_bf16x2(cw.z, 1);
+      hi.z = i8pair_to_bf16x2(cw.w, 0); hi.w = i8pair_to_bf16x2(cw.w, 1);
+      *reinterpret_cast<uint4*>(t2buf + row * ROWB + (((2 * j) ^ (row & 7)) << 4)) = lo;
+      *reinterpret_cast<uint4*>(t2buf + row * ROWB + (((2 * j + 1) ^ (row & 7)) << 4)) = hi;
+    }
+    for (int row = tid; row < TILE; row += ATT_THREADS) {
+      const int tok = tv0 + row;
+      t2sc[row] = tok < vend ? S2[tok - n01] : 0.f;
+    }
+  };
+
+  // ---- phase A on T2 rows (rare; synchronous)
+  for (int tv0 = t2beg; tv0 < vend; tv0 += TILE) {
+    stage_t2(tv0, false);
+    __syncthreads();
+    qk_warp(smem_u32(t2buf), tv0, vend, t2sc);
+    __syncthreads();
+  }
+
+  auto reduce_max = [&]() {   // all threads: CTA max of the two heads this lane owns
+    m2a = fmaxf(fmaxf(red[0 * 8 + 2 * tq], red[1 * 8 + 2 * tq]), fmaxf(red[2 * 8 + 2 * tq], red[3 * 8 + 2 * tq]));
+    m2b = fmaxf(fmaxf(red[0 * 8 + 2 * tq + 1], red[1 * 8 + 2 * tq + 1]),
+                fmaxf(red[2 * 8 + 2 * tq + 1], red[3 * 8 + 2 * tq + 1]));
+    if (tid < 8) xm[tid] = fmaxf(fmaxf(red[tid], red[8 + tid]), fmaxf(red[16 + tid], red[24 + tid]));
+    if (m2a == -INFINITY) m2a = 0.f;
+    if (m2b == -INFINITY) m2b = 0.f;
+  };
+  auto write_warp_max = [&]() {
+    float a = mx0, c = mx1;
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, off));
+      c = fmaxf(c, __shfl_xor_sync(0xffffffffu, c, off));
+    }
+    if (lane < 4) {
+      red[w * 8 + 2 * lane] = a;
+      red[w * 8 + 2 * lane + 1] = c;
+    }
+  };
+
+  // ---- phases A (K tiles) and B (V tiles) through the cp.async ring
+  for (int i = 0; i < total; ++i) {
+    cp_wait<NST - 2>();
+    __syncthreads();
+    if (i + NST - 1 < total) load_tile(i + NST - 1);
+    cp_commit();
+    if (i == nt) reduce_max();
+    const uint32_t sbase = smem_u32(ring + (i % NST) * TILEB);
+    if (i < nt) {
+      qk_warp(sbase, vbeg + i * TILE, aend, nullptr);
+      if (i == nt - 1) write_warp_max();
+    } else {
+      pv_warp(sbase, vbeg + (i - nt) * TILE, aend, nullptr);
+    }
+  }
+  cp_wait<0>();
+  if (nt == 0) {
+    write_warp_max();
+    __syncthreads();
+    reduce_max();
+  }
+
+  // ---- phase B on T2 rows
+  for (int tv0 = t2beg; tv0 < vend; tv0 += TILE) {
+    __syncthreads();
+    stage_t2(tv0, true);
+    __syncthreads();
+    pv_warp(smem_u32(t2buf), tv0, vend, t2sc);
+  }
+
+  // ---- CTA reduction of l and o (ring reused as [4 warps][8 heads][D] fp32)
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+  }
+  __syncthreads();
+  float* ow = reinterpret_cast<float*>(ring);
+  if (lane < 4) {
+    red[32 + w * 8 + 2 * lane] = l0;
+    red[32 + w * 8 + 2 * lane + 1] = l1;
+  }
+#pragma unroll
+  for (int mt = 0; mt < KS; ++mt) {
+    float* o0 = ow + (w * 8 + 2 * tq) * D + mt * 16 + gq;
+    float* o1 = ow + (w * 8 + 2 * tq + 1) * D + mt * 16 + gq;
+    o0[0] = oacc[mt][0];
+    o1[0] = oacc[mt][1];
+    o0[8] = oacc[mt][2];
+    o1[8] = oacc[mt][3];
+  }
+  __syncthreads();
+  for (int e = tid; e < 8 * D; e += ATT_THREADS)
+    xo[e] = (ow[e] + ow[8 * D + e]) + (ow[16 * D + e] + ow[24 * D + e]);
+  if (tid < 8) xl[tid] = (red[32 + tid] + red[40 + tid]) + (red[48 + tid] + red[56 + tid]);
+
+  // ---- cluster merge through distributed shared memory
+  cluster.sync();
+  if (tid < 8) {
+    float M = -INFINITY;
+    for (int c = 0; c < C; ++c) M = fmaxf(M, cluster.map_shared_rank(xm, c)[tid]);
+    float Ls = 0.f;
+    for (int c = 0; c < C; ++c) {
+      const float mc = cluster.map_shared_rank(xm, c)[tid];
+      if (mc != -INFINITY) Ls += cluster.map_shared_rank(xl, c)[tid] * exp2f(mc - M);
+    }
+    sML[tid] = M;
+    sML[8 + tid] = 1.0f / Ls;
+  }
+  __syncthreads();
+  {
+    const int tot = G * D;
+    const int per = (tot + C - 1) / C;
+    const int e1 = min(tot, (r + 1) * per);
+    for (int e = r * per + tid; e < e1; e += ATT_THREADS) {
+      const int h = e / D, dd = e - h * D;
+      float acc = 0.f;
+      for (int c = 0; c < C; ++c) {
+        const float mc = cluster.map_shared_rank(xm, c)[h];
+        if (mc != -INFINITY) acc += exp2f(mc - sML[h]) * cluster.map_shared_rank(xo, c)[h * D + dd];
+      }
+      const float val = acc * sML[8 + h];
+      const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
+      if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = val;
+      else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(val);
+    }
+  }
+  if (fuse) {
+    const int* I0 = v.idx[cur][0] + (size_t)b * v.cap0;
+    const int* I1 = v.idx[cur][1] + (size_t)b * v.cap1;
+    const int* I2 = v.idx[cur][2] + (size_t)b * v.cap2;
+    float* Sg = v.S + ((size_t)b * v.Hkv + g) * v.Nmax;
+    bool bad = false;
+    for (int j = tid; j < vend - vbeg; j += ATT_THREADS) {
+      const int tok = vbeg + j;
+      const float* zr = zs + j * 8;
+      float inc = 0.f;
+      for (int h = 0; h < G; ++h) inc += exp2f(zr[h] - sML[h]) * sML[8 + h];
+      const int pos = tok < n0 ? I0[tok] : (tok < n01 ? I1[tok - n0] : I2[tok - n01]);
+      Sg[pos] = Sg[pos] + inc;
+      bad |= !isfinite(inc);
+    }
+    if (bad) atomicOr(&v.st->err, 1);
+  }
+  cluster.sync();   // keep this CTA's shared memory alive until every peer has read it
+}
+
+size_t attn_smem_bytes(const DevView& v) {
+  const size_t ringb = (size_t)NST * TILE * v.D * 2;
+  const size_t zsb = (size_t)v.chunk_max * 8 * 4;
+  const size_t xob = (size_t)8 * v.D * 4;
+  const size_t misc = (size_t)(8 + 8 + 64 + 16 + TILE) * 4;
+  const size_t t2 = (v.cap2 > 0) ? (size_t)TILE * v.D * 2 : 0;
+  return ringb + zsb + xob + misc + t2;
+}
+
+template <int D>
+static cudaError_t configure_d(const DevView& v) {
+  cudaError_t e = cudaFuncSetAttribute(k_decode_attn<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)attn_smem_bytes(v));
+  if (e != cudaSuccess) return e;
+  if (v.split > 8) e = cudaFuncSetAttribute(k_decode_attn<D>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return e;
+}
+
+cudaError_t attn_configure(const DevView& v) {
+  return v.D == 128 ? configure_d<128>(v) : configure_d<64>(v);
+}
+
+cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, void* o, int fuse, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(v.split, v.B * v.Hkv, 1);
+  cfg.blockDim = dim3(ATT_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = attn_smem_bytes(v);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = v.split;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const __nv_bfloat16* qq = reinterpret_cast<const __nv_bfloat16*>(q);
+  if (v.D == 128) return cudaLaunchKernelEx(&cfg, k_decode_attn<128>, v, layer, qq, o, fuse);
+  return cudaLaunchKernelEx(&cfg, k_decode_attn<64>, v, layer, qq, o, fuse);
+}
+
+}  // namespace kvt

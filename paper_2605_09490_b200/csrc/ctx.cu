@@ -1,0 +1,696 @@
+// Host side of libkvtier.so: config validation, memory carving, host-side state
+// machine of Alg. 1, stream/event ordering, and the C ABI entry points.
+#include "../../include/kv_tier.h"
+#include "kv_internal.cuh"
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace kvt;
+
+struct kv_tier_ctx {
+  kv_tier_config cfg;
+  kv_tier_sizes sz;
+  DevView v;
+  // host mirror of the uniform-per-request state (all requests share n and P)
+  int n = 0, t = 0, cur = 0, n0 = -1;
+  int c[4] = {0, 0, 0, 0};            // |T0| |T1| |T2| |T3|
+  int pend[4] = {0, 0, 0, 0};         // counts computed by the last classify
+  int n_event = 0, nvis_event = 0;
+  bool classified = false, step_open = false, loaded = false;
+  std::vector<int> loaded_layers;
+  void* host_t1 = nullptr;            // cudaHostAlloc base (K then V)
+  void* host_t2 = nullptr;            // codes K, codes V, scales K, scales V
+  cudaEvent_t ev_step_begin = nullptr, ev_migrated = nullptr, ev_offload_done = nullptr;
+  cudaEvent_t ev_slot_free[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> ev_prefetched;
+  std::vector<int> prefetched_step;
+  bool offload_pending = false;
+  bool capturing = false;
+  bool slot_recorded[2] = {false, false};   // ev_slot_free[x] recorded within the open step
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+kv_tier_status fail(kv_tier_ctx* ctx, kv_tier_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  g_err = buf;
+  return st;
+}
+
+kv_tier_status cuda_check(kv_tier_ctx* ctx, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return KV_TIER_OK;
+  return fail(ctx, KV_TIER_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+int round16(long long x) { return (int)((x + 15) / 16 * 16); }
+
+int auto_split(const kv_tier_config& c) {
+  if (c.split > 0) return c.split;
+  const int units = c.num_requests * c.num_kv_heads;
+  int s = (2 * 148 + units - 1) / units;
+  s = std::max(1, std::min(8, s));
+  while (s < 16 && (c.max_tokens + s - 1) / s > 2048) ++s;   // logits of a chunk stay in SMEM
+  return s;
+}
+
+kv_tier_status validate(const kv_tier_config* c) {
+  if (!c) return fail(nullptr, KV_TIER_E_INVAL, "null config");
+  if (c->num_requests < 1 || c->num_requests > 1024) return fail(nullptr, KV_TIER_E_INVAL, "num_requests out of range");
+  if (c->num_layers < 1) return fail(nullptr, KV_TIER_E_INVAL, "num_layers < 1");
+  if (c->num_kv_heads < 1 || c->num_q_heads % c->num_kv_heads != 0)
+    return fail(nullptr, KV_TIER_E_INVAL, "num_q_heads must be a multiple of num_kv_heads");
+  if (c->num_q_heads / c->num_kv_heads > 8) return fail(nullptr, KV_TIER_E_INVAL, "GQA group > 8 not supported");
+  if (c->head_dim != 64 && c->head_dim != 128) return fail(nullptr, KV_TIER_E_INVAL, "head_dim must be 64 or 128");
+  if (c->max_tokens < 2) return fail(nullptr, KV_TIER_E_INVAL, "max_tokens < 2");
+  if (c->prompt_len < 0 || c->sink_size < 0 || c->window_size < 1)
+    return fail(nullptr, KV_TIER_E_INVAL, "window_size must be >= 1 (AMB-20) and P, k_s >= 0");
+  if (c->hbm_ratio_bp > 10000 || c->evict_ratio_bp > 10000 || c->t2_fraction_bp > 10000)
+    return fail(nullptr, KV_TIER_E_INVAL, "ratios are basis points in [0, 10000]");
+  if (c->evict_mode != 0 && c->evict_mode != 1) return fail(nullptr, KV_TIER_E_INVAL, "bad evict_mode");
+  if (c->staging_tokens != 0 && c->staging_tokens != KV_TIER_STAGING_ALL)
+    return fail(nullptr, KV_TIER_E_INVAL, "staging_tokens must be 0 (stream) or KV_TIER_STAGING_ALL (differential)");
+  if (c->shard != KV_TIER_SHARD_REQUEST) return fail(nullptr, KV_TIER_E_INVAL, "only request sharding is implemented");
+  if (c->split < 0 || c->split > 16) return fail(nullptr, KV_TIER_E_INVAL, "split must be in [0, 16]");
+  return KV_TIER_OK;
+}
+
+// Capacities (rows per (l, b, g)).  T0 must hold the initial prefix (all T0 until the
+// first event) and, after an event, P u top-n_hbm plus Delta appends (AMB-25).
+void capacities(const kv_tier_config& c, int* cap0, int* cap1, int* cap2) {
+  const long long N = c.max_tokens;
+  const long long prot = (long long)c.prompt_len + c.sink_size + c.window_size;
+  const long long hbm = ((long long)c.hbm_ratio_bp * N + 9999) / 10000;
+  (void)prot; (void)hbm;   // v1: T0 sized for the whole chain (the prefix starts all-T0)
+  long long c0 = N;
+  const long long off = ((long long)(10000 - c.hbm_ratio_bp) * N + 9999) / 10000 + 2;
+  long long c1 = std::min<long long>(N, off);
+  long long c2 = c.t2_fraction_bp ? std::min<long long>(N, (off * c.t2_fraction_bp + 9999) / 10000 + 2) : 0;
+  *cap0 = round16(c0);
+  *cap1 = round16(c1);
+  *cap2 = round16(c2);
+}
+
+struct Layout {
+  size_t off_k0[2], off_v0[2], off_k1[2], off_v1[2], off_c2k[2], off_c2v[2], off_s2k[2], off_s2v[2];
+  size_t off_idx[2][3], off_vis[2], off_tier[2], off_row[2], off_cnt[2], off_S, off_fS, off_st, total;
+  size_t b_t0, b_t1, b_t2, b_scores, b_meta;
+};
+
+Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
+  Layout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes); return r; };
+  const size_t LBH = (size_t)c.num_layers * c.num_requests * c.num_kv_heads;
+  const size_t BH = (size_t)c.num_requests * c.num_kv_heads;
+  const size_t D = c.head_dim, B = c.num_requests, N = c.max_tokens;
+  const bool stream = c.staging_tokens == 0;
+  size_t s0 = o;
+  for (int i = 0; i < 2; ++i) { L.off_k0[i] = take(LBH * cap0 * D * 2); L.off_v0[i] = take(LBH * cap0 * D * 2); }
+  L.b_t0 = o - s0; s0 = o;
+  if (stream) {
+    L.off_k1[0] = L.off_k1[1] = take(2 * BH * cap1 * D * 2);
+    L.off_v1[0] = L.off_v1[1] = take(2 * BH * cap1 * D * 2);
+  } else {
+    for (int i = 0; i < 2; ++i) { L.off_k1[i] = take(LBH * cap1 * D * 2); L.off_v1[i] = take(LBH * cap1 * D * 2); }
+  }
+  L.b_t1 = o - s0; s0 = o;
+  for (int i = 0; i < 2; ++i) {
+    L.off_c2k[i] = take(LBH * cap2 * D); L.off_c2v[i] = take(LBH * cap2 * D);
+    L.off_s2k[i] = take(LBH * cap2 * 4); L.off_s2v[i] = take(LBH * cap2 * 4);
+  }
+  L.b_t2 = o - s0; s0 = o;
+  L.off_S = take(BH * N * 4);
+  L.b_scores = o - s0; s0 = o;
+  for (int i = 0; i < 2; ++i) {
+    L.off_idx[i][0] = take(B * cap0 * 4);
+    L.off_idx[i][1] = take(B * std::max(cap1, 1) * 4);
+    L.off_idx[i][2] = take(B * std::max(cap2, 1) * 4);
+    L.off_vis[i] = take(B * N * 4);
+    L.off_tier[i] = take(B * N);
+    L.off_row[i] = take(B * N * 4);
+    L.off_cnt[i] = take(B * CNT_STRIDE * 4);
+  }
+  L.off_fS = take(B * N * 4);
+  L.off_st = take(sizeof(DevState));
+  L.b_meta = o - s0;
+  L.total = o;
+  return L;
+}
+
+int n_protected(const kv_tier_config& c, int n) {
+  const int a = std::min(c.prompt_len + c.sink_size, n);
+  const int w0 = std::max(0, n - c.window_size);
+  return a + (n - std::max(w0, a));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kv_tier_version(void) { return "kvtier-b200 0.1 (sm_100a, mma.sync+cluster decode)"; }
+
+const char* kv_tier_last_error(const kv_tier_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_err.c_str();
+}
+
+kv_tier_status kv_tier_query_sizes(const kv_tier_config* cfg, kv_tier_sizes* out) {
+  kv_tier_status st = validate(cfg);
+  if (st != KV_TIER_OK) return st;
+  if (!out) return fail(nullptr, KV_TIER_E_INVAL, "null sizes");
+  int cap0, cap1, cap2;
+  capacities(*cfg, &cap0, &cap1, &cap2);
+  Layout L = make_layout(*cfg, cap0, cap1, cap2);
+  memset(out, 0, sizeof(*out));
+  out->device_arena = L.total;
+  out->t0_store = L.b_t0;
+  out->t1_staging = L.b_t1;
+  out->t2_store = L.b_t2;
+  out->scores = L.b_scores;
+  out->meta = L.b_meta;
+  const size_t rows = (size_t)cfg->num_layers * cfg->num_requests * cfg->num_kv_heads * cfg->max_tokens;
+  out->host_t1 = cfg->hbm_ratio_bp < 10000 ? rows * cfg->head_dim * 2 * 2 : 0;
+  out->host_t2 = cfg->t2_fraction_bp ? rows * (cfg->head_dim + 4) * 2 : 0;
+  out->cap_t0 = cap0;
+  out->cap_t1 = cap1;
+  out->cap_t2 = cap2;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* buf, const void* nccl_unique_id,
+                            kv_tier_ctx** out) {
+  kv_tier_status st = validate(cfg);
+  if (st != KV_TIER_OK) return st;
+  if (!buf || !buf->device_arena || !out) return fail(nullptr, KV_TIER_E_INVAL, "null buffers/out");
+  if (nccl_unique_id) return fail(nullptr, KV_TIER_E_INVAL, "request sharding has no collective: pass NULL");
+  if (((uintptr_t)buf->device_arena) & 255) return fail(nullptr, KV_TIER_E_INVAL, "device_arena must be 256-B aligned");
+  cudaError_t e = cudaSetDevice(cfg->device);
+  if (e != cudaSuccess) return fail(nullptr, KV_TIER_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+  kv_tier_ctx* ctx = new kv_tier_ctx();
+  ctx->cfg = *cfg;
+  kv_tier_query_sizes(cfg, &ctx->sz);
+  int cap0 = ctx->sz.cap_t0, cap1 = ctx->sz.cap_t1, cap2 = ctx->sz.cap_t2;
+  Layout L = make_layout(*cfg, cap0, cap1, cap2);
+  char* A = reinterpret_cast<char*>(buf->device_arena);
+  DevView& v = ctx->v;
+  memset(&v, 0, sizeof(v));
+  v.B = cfg->num_requests; v.L = cfg->num_layers; v.Hq = cfg->num_q_heads; v.Hkv = cfg->num_kv_heads;
+  v.G = v.Hq / v.Hkv; v.D = cfg->head_dim; v.Nmax = cfg->max_tokens;
+  v.cap0 = cap0; v.cap1 = cap1; v.cap2 = cap2;
+  v.P = cfg->prompt_len; v.ks = cfg->sink_size; v.kw = cfg->window_size;
+  v.hbm_bp = (int)cfg->hbm_ratio_bp; v.evict_bp = (int)cfg->evict_ratio_bp; v.t2_bp = (int)cfg->t2_fraction_bp;
+  v.evict_mode = cfg->evict_mode;
+  v.stream_mode = cfg->staging_tokens == 0;
+  v.out_fp32 = cfg->out_fp32;
+  v.split = auto_split(*cfg);
+  v.chunk_max = round16((cfg->max_tokens + v.split - 1) / v.split);
+  for (int i = 0; i < 2; ++i) {
+    v.k0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_k0[i]);
+    v.v0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_v0[i]);
+    v.k1[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_k1[i]);
+    v.v1[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_v1[i]);
+    v.c2k[i] = reinterpret_cast<int8_t*>(A + L.off_c2k[i]);
+    v.c2v[i] = reinterpret_cast<int8_t*>(A + L.off_c2v[i]);
+    v.s2k[i] = reinterpret_cast<float*>(A + L.off_s2k[i]);
+    v.s2v[i] = reinterpret_cast<float*>(A + L.off_s2v[i]);
+    for (int T = 0; T < 3; ++T) v.idx[i][T] = reinterpret_cast<int*>(A + L.off_idx[i][T]);
+    v.idxvis[i] = reinterpret_cast<int*>(A + L.off_vis[i]);
+    v.tier[i] = reinterpret_cast<uint8_t*>(A + L.off_tier[i]);
+    v.rowof[i] = reinterpret_cast<int*>(A + L.off_row[i]);
+    v.cnt[i] = reinterpret_cast<int*>(A + L.off_cnt[i]);
+  }
+  v.S = reinterpret_cast<float*>(A + L.off_S);
+  v.fS = reinterpret_cast<float*>(A + L.off_fS);
+  v.st = reinterpret_cast<DevState*>(A + L.off_st);
+  // pinned, mapped host stores (NUMA placement follows the calling thread's node)
+  const size_t rows = (size_t)v.L * v.B * v.Hkv * v.Nmax;
+  if (ctx->sz.host_t1) {
+    e = cudaHostAlloc(&ctx->host_t1, ctx->sz.host_t1, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) { delete ctx; return fail(nullptr, KV_TIER_E_OOM, "cudaHostAlloc(T1 %zu B): %s", (size_t)0, cudaGetErrorString(e)); }
+    void* dptr = nullptr;
+    cudaHostGetDevicePointer(&dptr, ctx->host_t1, 0);
+    v.hk1 = reinterpret_cast<__nv_bfloat16*>(dptr);
+    v.hv1 = v.hk1 + rows * v.D;
+  }
+  if (ctx->sz.host_t2) {
+    e = cudaHostAlloc(&ctx->host_t2, ctx->sz.host_t2, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) { if (ctx->host_t1) cudaFreeHost(ctx->host_t1); delete ctx; return fail(nullptr, KV_TIER_E_OOM, "cudaHostAlloc(T2): %s", cudaGetErrorString(e)); }
+    void* dptr = nullptr;
+    cudaHostGetDevicePointer(&dptr, ctx->host_t2, 0);
+    char* h = reinterpret_cast<char*>(dptr);
+    v.hc2k = reinterpret_cast<int8_t*>(h);
+    v.hc2v = reinterpret_cast<int8_t*>(h + rows * v.D);
+    v.hs2k = reinterpret_cast<float*>(h + 2 * rows * v.D);
+    v.hs2v = reinterpret_cast<float*>(h + 2 * rows * v.D + rows * 4);
+  }
+  e = attn_configure(v);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_step_begin, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_migrated, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_offload_done, cudaEventDisableTiming);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ctx->ev_slot_free[i], cudaEventDisableTiming);
+  ctx->ev_prefetched.assign(v.L, nullptr);
+  for (int l = 0; l < v.L && e == cudaSuccess; ++l) e = cudaEventCreateWithFlags(&ctx->ev_prefetched[l], cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    kv_tier_status s2 = fail(nullptr, KV_TIER_E_CUDA, "init: %s", cudaGetErrorString(e));
+    kv_tier_destroy(ctx);
+    return s2;
+  }
+  ctx->loaded_layers.assign(v.L, 0);
+  ctx->prefetched_step.assign(v.L, -1);
+  *out = ctx;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_destroy(kv_tier_ctx* ctx) {
+  if (!ctx) return KV_TIER_OK;
+  cudaDeviceSynchronize();
+  if (ctx->host_t1) cudaFreeHost(ctx->host_t1);
+  if (ctx->host_t2) cudaFreeHost(ctx->host_t2);
+  if (ctx->ev_step_begin) cudaEventDestroy(ctx->ev_step_begin);
+  if (ctx->ev_migrated) cudaEventDestroy(ctx->ev_migrated);
+  if (ctx->ev_offload_done) cudaEventDestroy(ctx->ev_offload_done);
+  for (auto& ev : ctx->ev_slot_free) if (ev) cudaEventDestroy(ev);
+  for (auto& ev : ctx->ev_prefetched) if (ev) cudaEventDestroy(ev);
+  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  delete ctx;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_load_prefix(kv_tier_ctx* ctx, int32_t layer, const void* k, const void* v, int32_t n0,
+                                   void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
+  if (!k || !v) return fail(ctx, KV_TIER_E_INVAL, "null k/v");
+  if (ctx->t > 0 || ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "load_prefix after decoding started");
+  if (n0 < 0 || n0 + 1 > ctx->v.cap0 || n0 + 1 > ctx->v.Nmax)
+    return fail(ctx, KV_TIER_E_CAPACITY, "prefix of %d tokens exceeds T0 capacity %d / N_max %d", n0, ctx->v.cap0, ctx->v.Nmax);
+  if (ctx->n0 >= 0 && ctx->n0 != n0) return fail(ctx, KV_TIER_E_INVAL, "n0 differs between layers");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (ctx->n0 < 0) {
+    kv_tier_status st = cuda_check(ctx, launch_init_meta(ctx->v, n0, s), "init_meta");
+    if (st) return st;
+    ctx->n0 = n0;
+    ctx->n = n0;
+    ctx->c[0] = n0; ctx->c[1] = ctx->c[2] = ctx->c[3] = 0;
+    ctx->n_event = n0;
+    ctx->nvis_event = n0;
+  }
+  if (n0 > 0) {
+    kv_tier_status st = cuda_check(ctx, launch_load_prefix(ctx->v, layer, k, v, n0, s), "load_prefix");
+    if (st) return st;
+  }
+  ctx->loaded_layers[layer] = 1;
+  ctx->loaded = std::all_of(ctx->loaded_layers.begin(), ctx->loaded_layers.end(), [](int x) { return x != 0; });
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_begin_step(kv_tier_ctx* ctx, void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!ctx->loaded) return fail(ctx, KV_TIER_E_STATE, "load_prefix not called for every layer");
+  if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "begin_step twice without end_step");
+  if (ctx->n + 1 > ctx->v.Nmax) return fail(ctx, KV_TIER_E_CAPACITY, "N_max=%d reached", ctx->v.Nmax);
+  if (ctx->c[0] + 1 > ctx->v.cap0)
+    return fail(ctx, KV_TIER_E_CAPACITY, "T0 store full (%d rows): call classify/migrate every Delta steps", ctx->v.cap0);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  kv_tier_status st = cuda_check(ctx, launch_begin_step(ctx->v, s), "begin_step");
+  if (st) return st;
+  st = cuda_check(ctx, cudaEventRecord(ctx->ev_step_begin, s), "event");
+  if (st) return st;
+  ctx->n += 1;
+  ctx->c[0] += 1;
+  ctx->step_open = true;
+  ctx->classified = false;
+  ctx->slot_recorded[0] = ctx->slot_recorded[1] = false;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_append(kv_tier_ctx* ctx, int32_t layer, const void* k_new, const void* v_new, void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "append outside begin_step/end_step");
+  if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
+  if (!k_new || !v_new) return fail(ctx, KV_TIER_E_INVAL, "null k/v");
+  return cuda_check(ctx, launch_append(ctx->v, layer, k_new, v_new, reinterpret_cast<cudaStream_t>(stream)), "append");
+}
+
+kv_tier_status kv_tier_prefetch(kv_tier_ctx* ctx, int32_t layer, void* side) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
+  if (!ctx->v.stream_mode) return KV_TIER_OK;     // differential: staging already holds T1
+  if (!ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "prefetch outside a step");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(side);
+  // ev_step_begin orders this after all earlier main-stream work (incl. the previous
+  // step's attention on both ring slots); slot reuse within the step waits on the
+  // attention that last read the slot.
+  cudaError_t e = cudaStreamWaitEvent(s, ctx->ev_step_begin, 0);
+  if (e == cudaSuccess && ctx->slot_recorded[layer & 1]) e = cudaStreamWaitEvent(s, ctx->ev_slot_free[layer & 1], 0);
+  if (e == cudaSuccess && ctx->offload_pending && !ctx->capturing) e = cudaStreamWaitEvent(s, ctx->ev_offload_done, 0);
+  if (e == cudaSuccess) e = launch_prefetch(ctx->v, layer, s);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_prefetched[layer], s);
+  if (e == cudaSuccess) ctx->prefetched_step[layer] = ctx->t;
+  return cuda_check(ctx, e, "prefetch");
+}
+
+kv_tier_status kv_tier_decode_attention(kv_tier_ctx* ctx, int32_t layer, const void* q, void* o,
+                                        int32_t fuse_score_update, void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
+  if (!q || !o) return fail(ctx, KV_TIER_E_INVAL, "null q/o");
+  if (((uintptr_t)q & 15) || ((uintptr_t)o & 15)) return fail(ctx, KV_TIER_E_INVAL, "q/o must be 16-B aligned");
+  if (!ctx->loaded) return fail(ctx, KV_TIER_E_STATE, "no prefix loaded");
+  if (ctx->v.stream_mode && (!ctx->step_open || ctx->prefetched_step[layer] != ctx->t))
+    return fail(ctx, KV_TIER_E_STATE, "stream mode: kv_tier_prefetch(layer %d) must precede decode_attention in every step", layer);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  if (ctx->v.stream_mode) e = cudaStreamWaitEvent(s, ctx->ev_prefetched[layer], 0);
+  if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, o, fuse_score_update, s);
+  if (e == cudaSuccess && ctx->v.stream_mode) {
+    e = cudaEventRecord(ctx->ev_slot_free[layer & 1], s);
+    ctx->slot_recorded[layer & 1] = true;
+  }
+  return cuda_check(ctx, e, "decode_attention");
+}
+
+kv_tier_status kv_tier_visible_count(const kv_tier_ctx* ctx, int32_t* n_vis) {
+  if (!ctx || !n_vis) return fail(nullptr, KV_TIER_E_INVAL, "null arg");
+  *n_vis = ctx->nvis_event + (ctx->n - ctx->n_event);
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_score_update(kv_tier_ctx* ctx, int32_t layer, const float* probs, void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!probs) return fail(ctx, KV_TIER_E_INVAL, "null probs");
+  if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
+  return cuda_check(ctx, launch_score_update(ctx->v, layer, probs, reinterpret_cast<cudaStream_t>(stream)), "score_update");
+}
+
+kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "end_step without begin_step");
+  kv_tier_status st = cuda_check(ctx, launch_end_step(ctx->v, reinterpret_cast<cudaStream_t>(stream)), "end_step");
+  if (st) return st;
+  ctx->step_open = false;
+  ctx->t += 1;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_classify(kv_tier_ctx* ctx, void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!ctx->loaded) return fail(ctx, KV_TIER_E_STATE, "no prefix loaded");
+  if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "classify inside a step (call after the last layer's score update)");
+  const kv_tier_config& c = ctx->cfg;
+  const long long n = ctx->n, np = n_protected(c, ctx->n), n3 = ctx->c[3];
+  const long long nl = n - np - n3;
+  long long n_new = c.evict_mode == 0 ? std::max(0LL, ((long long)c.evict_ratio_bp * (nl + n3)) / 10000 - n3)
+                                      : ((long long)c.evict_ratio_bp * nl) / 10000;
+  const long long surv = nl - n_new;
+  const long long n_hbm = ((long long)c.hbm_ratio_bp * surv) / 10000;
+  const long long n_t2 = ((long long)c.t2_fraction_bp * (surv - n_hbm)) / 10000;
+  const int p0 = (int)(np + n_hbm), p1 = (int)(surv - n_hbm - n_t2), p2 = (int)n_t2, p3 = (int)(n3 + n_new);
+  if (p0 > ctx->v.cap0 || p1 > ctx->v.cap1 || p2 > ctx->v.cap2)
+    return fail(ctx, KV_TIER_E_CAPACITY, "tier counts %d/%d/%d exceed capacities %d/%d/%d", p0, p1, p2,
+                ctx->v.cap0, ctx->v.cap1, ctx->v.cap2);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  if (ctx->offload_pending) e = cudaStreamWaitEvent(s, ctx->ev_offload_done, 0);
+  if (e == cudaSuccess) e = launch_classify(ctx->v, s);
+  kv_tier_status st = cuda_check(ctx, e, "classify");
+  if (st) return st;
+  ctx->pend[0] = p0; ctx->pend[1] = p1; ctx->pend[2] = p2; ctx->pend[3] = p3;
+  ctx->classified = true;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!ctx->classified) return fail(ctx, KV_TIER_E_STATE, "migrate without a preceding classify");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(main_stream);
+  cudaStream_t sd = reinterpret_cast<cudaStream_t>(side);
+  cudaError_t e = launch_migrate(ctx->v, ctx->cur, s);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_migrated, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, ctx->ev_migrated, 0);
+  if (e == cudaSuccess) e = launch_offload_host(ctx->v, ctx->cur, sd);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_offload_done, sd);
+  if (e == cudaSuccess) e = launch_commit(ctx->v, s);
+  kv_tier_status st = cuda_check(ctx, e, "migrate");
+  if (st) return st;
+  ctx->offload_pending = true;
+  for (int i = 0; i < 4; ++i) ctx->c[i] = ctx->pend[i];
+  ctx->cur ^= 1;
+  ctx->n_event = ctx->n;
+  ctx->nvis_event = ctx->n - ctx->c[3];
+  ctx->classified = false;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_step(kv_tier_ctx* ctx, const void* q, const void* k_new, const void* v_new, void* o,
+                            int32_t fuse_score_update, void* stream, void* side) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!q || !k_new || !v_new || !o) return fail(ctx, KV_TIER_E_INVAL, "null step buffer");
+  const DevView& v = ctx->v;
+  const size_t qs = (size_t)v.B * v.Hq * v.D, ks = (size_t)v.B * v.Hkv * v.D;
+  const size_t os = qs * (v.out_fp32 ? 4 : 2);
+  const char* qb = reinterpret_cast<const char*>(q);
+  const char* kb = reinterpret_cast<const char*>(k_new);
+  const char* vb = reinterpret_cast<const char*>(v_new);
+  char* ob = reinterpret_cast<char*>(o);
+  kv_tier_status st = kv_tier_begin_step(ctx, stream);
+  if (st) return st;
+  if (v.stream_mode)
+    for (int l = 0; l < std::min(2, v.L) && !st; ++l) st = kv_tier_prefetch(ctx, l, side);
+  for (int l = 0; l < v.L && !st; ++l) {
+    st = kv_tier_append(ctx, l, kb + l * ks * 2, vb + l * ks * 2, stream);
+    if (!st) st = kv_tier_decode_attention(ctx, l, qb + l * qs * 2, ob + l * os, fuse_score_update, stream);
+    if (!st && v.stream_mode && l + 2 < v.L) st = kv_tier_prefetch(ctx, l + 2, side);
+  }
+  if (st) return st;
+  return kv_tier_end_step(ctx, stream);
+}
+
+kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const void* k_new, const void* v_new,
+                                          void* o, int32_t fuse_score_update, void* stream, void* side) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "capture inside a step");
+  if (!ctx->loaded) return fail(ctx, KV_TIER_E_STATE, "no prefix loaded");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (s == nullptr) return fail(ctx, KV_TIER_E_INVAL, "capture needs a non-default stream");
+  if (ctx->graph_exec) { cudaGraphExecDestroy(ctx->graph_exec); ctx->graph_exec = nullptr; }
+  if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
+  // the capture runs the host state machine once; restore it afterwards
+  const int n = ctx->n, t = ctx->t, c0 = ctx->c[0];
+  const bool classified = ctx->classified;
+  const std::vector<int> pstep = ctx->prefetched_step;
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return cuda_check(ctx, e, "begin capture");
+  ctx->capturing = true;
+  kv_tier_status st = kv_tier_step(ctx, q, k_new, v_new, o, fuse_score_update, stream, side);
+  ctx->capturing = false;
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(s, &g);
+  ctx->n = n; ctx->t = t; ctx->c[0] = c0; ctx->classified = classified; ctx->step_open = false;
+  ctx->prefetched_step = pstep;
+  if (st) { if (g) cudaGraphDestroy(g); return st; }
+  if (e != cudaSuccess) return cuda_check(ctx, e, "end capture");
+  e = cudaGraphInstantiate(&ctx->graph_exec, g, 0);
+  if (e != cudaSuccess) { cudaGraphDestroy(g); return cuda_check(ctx, e, "graph instantiate"); }
+  ctx->graph = g;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_step_graph_launch(kv_tier_ctx* ctx, void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!ctx->graph_exec) return fail(ctx, KV_TIER_E_STATE, "no step graph captured");
+  if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "graph launch inside a step");
+  if (ctx->n + 1 > ctx->v.Nmax) return fail(ctx, KV_TIER_E_CAPACITY, "N_max=%d reached", ctx->v.Nmax);
+  if (ctx->c[0] + 1 > ctx->v.cap0) return fail(ctx, KV_TIER_E_CAPACITY, "T0 store full (%d rows)", ctx->v.cap0);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  if (ctx->offload_pending && ctx->v.stream_mode) e = cudaStreamWaitEvent(s, ctx->ev_offload_done, 0);
+  if (e == cudaSuccess) e = cudaGraphLaunch(ctx->graph_exec, s);
+  kv_tier_status st = cuda_check(ctx, e, "graph launch");
+  if (st) return st;
+  ctx->n += 1;
+  ctx->c[0] += 1;
+  ctx->t += 1;
+  ctx->classified = false;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_sync(kv_tier_ctx* ctx) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return fail(ctx, KV_TIER_E_CUDA, "async CUDA error: %s", cudaGetErrorString(e));
+  DevState h;
+  e = cudaMemcpy(&h, ctx->v.st, sizeof(h), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return fail(ctx, KV_TIER_E_CUDA, "state read: %s", cudaGetErrorString(e));
+  if (h.err) return fail(ctx, KV_TIER_E_NUMERIC, "non-finite probability or score detected on device");
+  if (h.n != ctx->n || h.cur != ctx->cur)
+    return fail(ctx, KV_TIER_E_STATE, "device/host state diverged (n %d/%d cur %d/%d)", h.n, ctx->n, h.cur, ctx->cur);
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_census(kv_tier_ctx* ctx, int32_t* counts, int64_t* d2h_rows) {
+  kv_tier_status st = kv_tier_sync(ctx);
+  if (st) return st;
+  if (counts) {
+    std::vector<int> cn((size_t)ctx->v.B * CNT_STRIDE);
+    cudaError_t e = cudaMemcpy(cn.data(), ctx->v.cnt[ctx->cur], cn.size() * 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_check(ctx, e, "census");
+    for (int b = 0; b < ctx->v.B; ++b) {
+      // counts over [0, n): T3 is n - |visible| (positions appended since the event are T0)
+      for (int i = 0; i < 3; ++i) counts[b * 4 + i] = cn[b * CNT_STRIDE + i];
+      counts[b * 4 + 3] = ctx->n - cn[b * CNT_STRIDE + 0] - cn[b * CNT_STRIDE + 1] - cn[b * CNT_STRIDE + 2];
+    }
+  }
+  if (d2h_rows) {
+    DevState h;
+    cudaMemcpy(&h, ctx->v.st, sizeof(h), cudaMemcpyDeviceToHost);
+    *d2h_rows = (int64_t)h.d2h_rows;
+  }
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_position(const kv_tier_ctx* ctx, int32_t* n, int32_t* t) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (n) *n = ctx->n;
+  if (t) *t = ctx->t;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_export_size(kv_tier_ctx* ctx, int32_t what, size_t* bytes) {
+  if (!ctx || !bytes) return fail(nullptr, KV_TIER_E_INVAL, "null arg");
+  const size_t B = ctx->v.B, H = ctx->v.Hkv, D = ctx->v.D, n = ctx->n;
+  const size_t c0 = ctx->c[0], c1 = ctx->c[1], c2 = ctx->c[2];
+  switch (what) {
+    case KV_TIER_X_SCORES: *bytes = B * H * n * 4; break;
+    case KV_TIER_X_TIERS: *bytes = B * n; break;
+    case KV_TIER_X_IDX_T0: *bytes = B * c0 * 4; break;
+    case KV_TIER_X_IDX_T1: *bytes = B * c1 * 4; break;
+    case KV_TIER_X_IDX_T2: *bytes = B * c2 * 4; break;
+    case KV_TIER_X_T0_ROWS: *bytes = B * H * c0 * 2 * D * 2; break;
+    case KV_TIER_X_T1_ROWS: case KV_TIER_X_STAGING: *bytes = B * H * c1 * 2 * D * 2; break;
+    case KV_TIER_X_T2_CODES: *bytes = B * H * c2 * 2 * D; break;
+    case KV_TIER_X_T2_SCALES: *bytes = B * H * c2 * 2 * 4; break;
+    default: return fail(ctx, KV_TIER_E_INVAL, "unknown export %d", what);
+  }
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, void* host_dst, size_t bytes) {
+  size_t need = 0;
+  kv_tier_status st = kv_tier_export_size(ctx, what, &need);
+  if (st) return st;
+  if (!host_dst || bytes != need) return fail(ctx, KV_TIER_E_INVAL, "export %d needs %zu bytes, got %zu", what, need, bytes);
+  if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
+  if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "export inside a step");
+  st = kv_tier_sync(ctx);
+  if (st) return st;
+  const DevView& v = ctx->v;
+  const int cur = ctx->cur;
+  const size_t B = v.B, H = v.Hkv, D = v.D, N = v.Nmax, n = ctx->n;
+  char* out = reinterpret_cast<char*>(host_dst);
+  auto d2h = [&](void* dst, const void* src, size_t nbytes) {
+    return cudaMemcpy(dst, src, nbytes, cudaMemcpyDeviceToHost);
+  };
+  cudaError_t e = cudaSuccess;
+  const int cnts[3] = {ctx->c[0], ctx->c[1], ctx->c[2]};
+  const int caps[3] = {v.cap0, v.cap1, v.cap2};
+  if (what == KV_TIER_X_SCORES) {
+    for (size_t bg = 0; bg < B * H && e == cudaSuccess; ++bg) e = d2h(out + bg * n * 4, v.S + bg * N, n * 4);
+  } else if (what == KV_TIER_X_TIERS) {
+    for (size_t b = 0; b < B && e == cudaSuccess; ++b) e = d2h(out + b * n, v.tier[cur] + b * N, n);
+  } else if (what >= KV_TIER_X_IDX_T0 && what <= KV_TIER_X_IDX_T2) {
+    const int T = what - KV_TIER_X_IDX_T0;
+    for (size_t b = 0; b < B && e == cudaSuccess; ++b)
+      e = d2h(out + b * cnts[T] * 4, v.idx[cur][T] + b * caps[T], (size_t)cnts[T] * 4);
+  } else if (what == KV_TIER_X_T0_ROWS || what == KV_TIER_X_STAGING) {
+    const bool t0 = what == KV_TIER_X_T0_ROWS;
+    if (!t0 && v.stream_mode) return fail(ctx, KV_TIER_E_STATE, "no persistent staging in stream mode");
+    const int cnt = t0 ? cnts[0] : cnts[1];
+    const int cap = t0 ? v.cap0 : v.cap1;
+    const __nv_bfloat16* Ks = t0 ? v.k0[cur] : v.k1[cur];
+    const __nv_bfloat16* Vs = t0 ? v.v0[cur] : v.v1[cur];
+    std::vector<uint16_t> tk((size_t)cnt * D), tv((size_t)cnt * D);
+    for (size_t b = 0; b < B && e == cudaSuccess; ++b)
+      for (size_t g = 0; g < H && e == cudaSuccess; ++g) {
+        const size_t grp = ((size_t)layer * B + b) * H + g;
+        e = d2h(tk.data(), Ks + grp * cap * D, tk.size() * 2);
+        if (e == cudaSuccess) e = d2h(tv.data(), Vs + grp * cap * D, tv.size() * 2);
+        uint16_t* o16 = reinterpret_cast<uint16_t*>(out) + ((b * H + g) * cnt) * 2 * D;
+        for (int j = 0; j < cnt; ++j) {
+          memcpy(o16 + (size_t)j * 2 * D, tk.data() + (size_t)j * D, D * 2);
+          memcpy(o16 + (size_t)j * 2 * D + D, tv.data() + (size_t)j * D, D * 2);
+        }
+      }
+  } else if (what == KV_TIER_X_T1_ROWS) {
+    const int cnt = cnts[1];
+    std::vector<int> idx((size_t)std::max(cnt, 1));
+    const size_t rows = (size_t)v.L * B * H * N;
+    const uint16_t* hk = reinterpret_cast<const uint16_t*>(ctx->host_t1);
+    const uint16_t* hv = hk ? hk + rows * D : nullptr;
+    if (cnt > 0 && !hk) return fail(ctx, KV_TIER_E_STATE, "no host T1 store");
+    for (size_t b = 0; b < B && e == cudaSuccess; ++b) {
+      e = d2h(idx.data(), v.idx[cur][1] + b * v.cap1, (size_t)cnt * 4);
+      for (size_t g = 0; g < H && e == cudaSuccess; ++g) {
+        const size_t grp = ((size_t)layer * B + b) * H + g;
+        uint16_t* o16 = reinterpret_cast<uint16_t*>(out) + ((b * H + g) * cnt) * 2 * D;
+        for (int j = 0; j < cnt; ++j) {
+          memcpy(o16 + (size_t)j * 2 * D, hk + (grp * N + idx[j]) * D, D * 2);
+          memcpy(o16 + (size_t)j * 2 * D + D, hv + (grp * N + idx[j]) * D, D * 2);
+        }
+      }
+    }
+  } else if (what == KV_TIER_X_T2_CODES || what == KV_TIER_X_T2_SCALES) {
+    const int cnt = cnts[2];
+    const bool codes = what == KV_TIER_X_T2_CODES;
+    std::vector<int8_t> ck((size_t)cnt * D + 1), cv((size_t)cnt * D + 1);
+    std::vector<float> sk((size_t)cnt + 1), sv((size_t)cnt + 1);
+    for (size_t b = 0; b < B && e == cudaSuccess; ++b)
+      for (size_t g = 0; g < H && e == cudaSuccess; ++g) {
+        const size_t grp = ((size_t)layer * B + b) * H + g;
+        if (codes) {
+          e = d2h(ck.data(), v.c2k[cur] + grp * v.cap2 * D, (size_t)cnt * D);
+          if (e == cudaSuccess) e = d2h(cv.data(), v.c2v[cur] + grp * v.cap2 * D, (size_t)cnt * D);
+          int8_t* o8 = reinterpret_cast<int8_t*>(out) + ((b * H + g) * cnt) * 2 * D;
+          for (int j = 0; j < cnt; ++j) {
+            memcpy(o8 + (size_t)j * 2 * D, ck.data() + (size_t)j * D, D);
+            memcpy(o8 + (size_t)j * 2 * D + D, cv.data() + (size_t)j * D, D);
+          }
+        } else {
+          e = d2h(sk.data(), v.s2k[cur] + grp * v.cap2, (size_t)cnt * 4);
+          if (e == cudaSuccess) e = d2h(sv.data(), v.s2v[cur] + grp * v.cap2, (size_t)cnt * 4);
+          float* of = reinterpret_cast<float*>(out) + ((b * H + g) * cnt) * 2;
+          for (int j = 0; j < cnt; ++j) { of[2 * j] = sk[j]; of[2 * j + 1] = sv[j]; }
+        }
+      }
+  }
+  return cuda_check(ctx, e, "export");
+}
+
+kv_tier_status kv_tier_import_scores(kv_tier_ctx* ctx, const float* host_S, size_t bytes) {
+  if (!ctx || !host_S) return fail(ctx, KV_TIER_E_INVAL, "null arg");
+  const size_t B = ctx->v.B, H = ctx->v.Hkv, N = ctx->v.Nmax, n = ctx->n;
+  if (bytes != B * H * n * 4) return fail(ctx, KV_TIER_E_INVAL, "import_scores needs %zu bytes", B * H * n * 4);
+  if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "import inside a step");
+  cudaError_t e = cudaDeviceSynchronize();
+  for (size_t bg = 0; bg < B * H && e == cudaSuccess; ++bg)
+    e = cudaMemcpy(ctx->v.S + bg * N, host_S + bg * n, n * 4, cudaMemcpyHostToDevice);
+  return cuda_check(ctx, e, "import_scores");
+}
+
+}  // extern "C"

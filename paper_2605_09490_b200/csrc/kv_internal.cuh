@@ -1,0 +1,79 @@
+// Internal device-side view of a kv_tier ctx (shared by the kernels of libkvtier.so).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace kvt {
+
+constexpr int T0 = 0, T1 = 1, T2 = 2, T3 = 3;
+constexpr int CNT_STRIDE = 8;   // cnt[buf][b][8]: |T0| |T1| |T2| |T3| |visible at event| pad..
+
+// Mutable device state (graph-static kernels read it instead of taking args).
+struct DevState {
+  int n;            // current sequence length: positions [0, n)
+  int t;            // decode step
+  int cur;          // ping-pong buffer holding the live stores / lists
+  int n_event;      // n at the last committed manage event
+  int err;          // sticky error bits: 1 = non-finite probability/score
+  int pad[3];
+  unsigned long long d2h_rows;   // rows written to the pinned host stores
+};
+
+struct DevView {
+  int B, L, Hq, Hkv, G, D, Nmax;
+  int cap0, cap1, cap2;
+  int P, ks, kw;
+  int hbm_bp, evict_bp, t2_bp, evict_mode;
+  int stream_mode;      // staging_tokens == 0
+  int out_fp32;
+  int split;            // CTAs per (b, g) cluster
+  int chunk_max;        // max tokens per CTA (logit buffer rows)
+  __nv_bfloat16* k0[2]; __nv_bfloat16* v0[2];        // T0 store  [L][B][Hkv][cap0][D]
+  __nv_bfloat16* k1[2]; __nv_bfloat16* v1[2];        // T1 staging [L][B][Hkv][cap1][D] (stream: [2][B][Hkv][cap1][D] in k1[0]/v1[0])
+  int8_t* c2k[2]; int8_t* c2v[2];                      // T2 codes  [L][B][Hkv][cap2][D]
+  float* s2k[2]; float* s2v[2];                        // T2 scales [L][B][Hkv][cap2]
+  int* idx[2][3];                                      // [buf][tier] -> [B][cap_tier] ascending positions
+  int* idxvis[2];                                      // [buf] -> [B][Nmax] ascending visible positions at event
+  uint8_t* tier[2];                                    // [buf] -> [B][Nmax]
+  int* rowof[2];                                       // [buf] -> [B][Nmax] row within the tier store
+  int* cnt[2];                                         // [buf] -> [B][CNT_STRIDE]
+  float* S;                                            // S_part [B][Hkv][Nmax]
+  float* fS;                                           // scratch [B][Nmax]
+  DevState* st;
+  __nv_bfloat16* hk1; __nv_bfloat16* hv1;            // pinned host T1 [L][B][Hkv][Nmax][D] (mapped)
+  int8_t* hc2k; int8_t* hc2v; float* hs2k; float* hs2v;   // pinned host T2 (mapped, may be null)
+};
+
+__device__ __forceinline__ size_t grp_of(const DevView& v, int l, int b, int g) {
+  return ((size_t)l * v.B + b) * v.Hkv + g;
+}
+
+__device__ __forceinline__ float bf16_bits_to_f(uint16_t h) { return __uint_as_float(((uint32_t)h) << 16); }
+
+// fp32 -> bf16 round-to-nearest-even on the bit pattern (finite inputs)
+__device__ __forceinline__ uint16_t f_to_bf16_bits(float x) {
+  uint32_t u = __float_as_uint(x);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+}  // namespace kvt
+
+// Launchers (defined in the .cu files, called by ctx.cu)
+namespace kvt {
+cudaError_t launch_begin_step(const DevView& v, cudaStream_t s);
+cudaError_t launch_append(const DevView& v, int layer, const void* k, const void* vv, cudaStream_t s);
+cudaError_t launch_load_prefix(const DevView& v, int layer, const void* k, const void* vv, int n0, cudaStream_t s);
+cudaError_t launch_init_meta(const DevView& v, int n0, cudaStream_t s);
+cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, void* o, int fuse, cudaStream_t s);
+cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s);
+cudaError_t launch_end_step(const DevView& v, cudaStream_t s);
+cudaError_t launch_classify(const DevView& v, cudaStream_t s);
+cudaError_t launch_migrate(const DevView& v, int cur, cudaStream_t s);
+cudaError_t launch_offload_host(const DevView& v, int cur, cudaStream_t s);
+cudaError_t launch_commit(const DevView& v, cudaStream_t s);
+cudaError_t launch_prefetch(const DevView& v, int layer, cudaStream_t s);
+size_t attn_smem_bytes(const DevView& v);
+cudaError_t attn_configure(const DevView& v);
+}  // namespace kvt

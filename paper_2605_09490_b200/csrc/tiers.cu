@@ -1,0 +1,556 @@
+// Tier management kernels of libkvtier.so:
+//   a1 append / step bookkeeping, a4 standalone score update, a5 classify
+//   (radix select + compaction), a6 migrate (gather / quantise / offload), a2 stream
+//   prefetch.  Citations: PAPER.md Alg. 1, §3.2-3.4 P:143-211.
+#include "kv_internal.cuh"
+
+namespace kvt {
+
+// ------------------------------------------------------------------ step bookkeeping
+// New position n joins T0 at the end of the T0 list (ascending order is kept since
+// n exceeds every stored position); it is inside the window, hence protected.
+__global__ void k_begin_step(const DevView v) {
+  const int b = threadIdx.x;
+  const int cur = v.st->cur;
+  const int n = v.st->n;
+  if (b < v.B) {
+    int* cn = v.cnt[cur] + b * CNT_STRIDE;
+    const int r = cn[0];
+    v.idx[cur][0][(size_t)b * v.cap0 + r] = n;
+    v.tier[cur][(size_t)b * v.Nmax + n] = T0;
+    v.rowof[cur][(size_t)b * v.Nmax + n] = r;
+    cn[0] = r + 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) v.st->n = n + 1;
+}
+
+__global__ void k_end_step(const DevView v) {
+  if (threadIdx.x == 0) v.st->t += 1;
+}
+
+// a1: K/V row of the new token for one layer -> T0 store row |T0|-1.
+__global__ void k_append(const DevView v, const int layer, const uint16_t* __restrict__ k,
+                         const uint16_t* __restrict__ vv) {
+  const int unit = blockIdx.x;               // b * Hkv + g
+  const int b = unit / v.Hkv, g = unit % v.Hkv;
+  const int cur = v.st->cur;
+  const int row = v.cnt[cur][b * CNT_STRIDE + 0] - 1;
+  const size_t dst = (grp_of(v, layer, b, g) * v.cap0 + row) * v.D;
+  uint16_t* K = reinterpret_cast<uint16_t*>(v.k0[cur]);
+  uint16_t* V = reinterpret_cast<uint16_t*>(v.v0[cur]);
+  for (int e = threadIdx.x; e < v.D; e += blockDim.x) {
+    K[dst + e] = k[(size_t)unit * v.D + e];
+    V[dst + e] = vv[(size_t)unit * v.D + e];
+  }
+}
+
+// Prefill rows [0, n0) of one layer into T0 (Alg. 1).
+__global__ void k_load_prefix(const DevView v, const int layer, const uint16_t* __restrict__ k,
+                              const uint16_t* __restrict__ vv, const int n0) {
+  const int unit = blockIdx.y;
+  const int b = unit / v.Hkv, g = unit % v.Hkv;
+  const size_t base = grp_of(v, layer, b, g) * v.cap0 * v.D;
+  uint16_t* K = reinterpret_cast<uint16_t*>(v.k0[0]);
+  uint16_t* V = reinterpret_cast<uint16_t*>(v.v0[0]);
+  const size_t tot = (size_t)n0 * v.D;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+    K[base + e] = k[(size_t)unit * tot + e];
+    V[base + e] = vv[(size_t)unit * tot + e];
+  }
+}
+
+// All n0 prefix tokens in T0 with S = 0 (Alg. 1).
+__global__ void k_init_meta(const DevView v, const int n0) {
+  const int b = blockIdx.y;
+  for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < v.Nmax; pos += gridDim.x * blockDim.x) {
+    for (int buf = 0; buf < 2; ++buf) {
+      v.tier[buf][(size_t)b * v.Nmax + pos] = pos < n0 ? T0 : T3;
+      v.rowof[buf][(size_t)b * v.Nmax + pos] = pos < n0 ? pos : -1;
+      v.idxvis[buf][(size_t)b * v.Nmax + pos] = pos;
+    }
+    if (pos < n0) v.idx[0][0][(size_t)b * v.cap0 + pos] = pos;
+    for (int g = 0; g < v.Hkv; ++g) v.S[((size_t)b * v.Hkv + g) * v.Nmax + pos] = 0.f;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int buf = 0; buf < 2; ++buf) {
+      int* cn = v.cnt[buf] + b * CNT_STRIDE;
+      cn[0] = buf == 0 ? n0 : 0;
+      cn[1] = cn[2] = cn[3] = 0;
+      cn[4] = buf == 0 ? n0 : 0;
+      cn[5] = cn[6] = cn[7] = 0;
+    }
+    if (b == 0) {
+      v.st->n = n0;
+      v.st->t = 0;
+      v.st->cur = 0;
+      v.st->n_event = n0;
+      v.st->err = 0;
+      v.st->d2h_rows = 0ull;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a4 standalone
+// probs [B][Hq][n_vis] in ascending visible order; visible list = idxvis at the last
+// event followed by the positions appended since (all T0, ascending).
+__global__ void k_score_update(const DevView v, const float* __restrict__ probs) {
+  const int unit = blockIdx.y;
+  const int b = unit / v.Hkv, g = unit % v.Hkv;
+  const int cur = v.st->cur;
+  const int nve = v.cnt[cur][b * CNT_STRIDE + 4];
+  const int n_event = v.st->n_event;
+  const int nvis = nve + (v.st->n - n_event);
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nvis) return;
+  const int pos = j < nve ? v.idxvis[cur][(size_t)b * v.Nmax + j] : n_event + (j - nve);
+  float inc = 0.f;
+  for (int h = g * v.G; h < (g + 1) * v.G; ++h) inc += probs[((size_t)b * v.Hq + h) * nvis + j];
+  float* S = v.S + ((size_t)b * v.Hkv + g) * v.Nmax + pos;
+  *S = *S + inc;
+  if (!isfinite(inc)) atomicOr(&v.st->err, 1);
+}
+
+// ------------------------------------------------------------------ a5 classify
+// One 1024-thread CTA per request.  Keys (bits(S_i) << 32 | i) are unique, so the
+// tier of every live token is decided by comparing its key with the keys at three
+// ranks, found by an 8-pass MSB radix select (histograms in shared memory).
+constexpr int CLS_THREADS = 1024;
+
+__global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v) {
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int cur = v.st->cur, nxt = cur ^ 1, n = v.st->n;
+  const uint8_t* told = v.tier[cur] + (size_t)b * v.Nmax;
+  float* fS = v.fS + (size_t)b * v.Nmax;
+  const int prot_lo = v.P + v.ks;          // [0,P) u [P,P+k_s)  (positions < n)
+  const int prot_hi = n - v.kw;            // window [n-k_w, n)
+
+  __shared__ int s_cnt[2];
+  __shared__ unsigned int hist[3][256];
+  __shared__ unsigned long long s_prefix[3];
+  __shared__ long long s_rank[3];
+  __shared__ int s_active[3];
+  __shared__ int s_wsum[4][32];
+  __shared__ int s_tot[4];
+  __shared__ int s_base[4];
+
+  if (tid < 2) s_cnt[tid] = 0;
+  __syncthreads();
+  // S_i = fp32 sum over kv heads in ascending order (AMB-1/14)
+  int c_live = 0, c_t3 = 0;
+  bool bad = false;
+  for (int pos = tid; pos < n; pos += CLS_THREADS) {
+    float s = v.S[((size_t)b * v.Hkv) * v.Nmax + pos];
+    for (int g = 1; g < v.Hkv; ++g) s = __fadd_rn(s, v.S[((size_t)b * v.Hkv + g) * v.Nmax + pos]);
+    fS[pos] = s;
+    bad |= !(s >= 0.f) || isinf(s);
+    if (told[pos] == T3) ++c_t3;
+    else if (pos >= prot_lo && pos < prot_hi) ++c_live;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    c_live += __shfl_xor_sync(0xffffffffu, c_live, off);
+    c_t3 += __shfl_xor_sync(0xffffffffu, c_t3, off);
+  }
+  if (lane == 0) {
+    atomicAdd(&s_cnt[0], c_live);
+    atomicAdd(&s_cnt[1], c_t3);
+  }
+  if (bad) atomicOr(&v.st->err, 1);
+  __syncthreads();
+  if (tid == 0) {
+    // Alg. 1 floor arithmetic in integer basis points (AMB-8/9/11)
+    const long long nl = s_cnt[0], n3 = s_cnt[1];
+    long long n_new;
+    if (v.evict_mode == 0) {
+      n_new = ((long long)v.evict_bp * (nl + n3)) / 10000 - n3;
+      if (n_new < 0) n_new = 0;
+    } else {
+      n_new = ((long long)v.evict_bp * nl) / 10000;
+    }
+    const long long surv = nl - n_new;
+    const long long n_hbm = ((long long)v.hbm_bp * surv) / 10000;
+    const long long n_t2 = ((long long)v.t2_bp * (surv - n_hbm)) / 10000;
+    const long long rk[3] = {n_new, n_new + n_t2, nl - n_hbm};
+    for (int k = 0; k < 3; ++k) {
+      s_active[k] = rk[k] < nl;
+      s_rank[k] = rk[k];
+      s_prefix[k] = 0ull;
+    }
+  }
+  __syncthreads();
+
+  // radix select: key at rank s_rank[k] among the live keys
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 3 * 256; i += CLS_THREADS) (&hist[0][0])[i] = 0u;
+    __syncthreads();
+    for (int pos = tid; pos < n; pos += CLS_THREADS) {
+      if (told[pos] == T3 || pos < prot_lo || pos >= prot_hi) continue;
+      const unsigned long long key = ((unsigned long long)__float_as_uint(fS[pos]) << 32) | (unsigned)pos;
+      const unsigned dig = (unsigned)(key >> shift) & 255u;
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        if (s_active[k] && (shift == 56 || (key >> (shift + 8)) == (s_prefix[k] >> (shift + 8))))
+          atomicAdd(&hist[k][dig], 1u);
+    }
+    __syncthreads();
+    if (w < 3 && s_active[w]) {
+      const long long rank = s_rank[w];
+      unsigned loc[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        loc[j] = hist[w][lane * 8 + j];
+        sum += loc[j];
+      }
+      unsigned inc = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += y;
+      }
+      const unsigned excl = inc - sum;
+      __syncwarp();
+      if ((long long)excl <= rank && rank < (long long)inc) {
+        unsigned c = excl;
+        int j = 0;
+        while (c + loc[j] <= rank) c += loc[j++];
+        s_rank[w] = rank - c;
+        s_prefix[w] |= ((unsigned long long)(lane * 8 + j)) << shift;
+      }
+    }
+    __syncthreads();
+  }
+  const unsigned long long thr_e = s_active[0] ? s_prefix[0] : ~0ull;   // keys below -> T3
+  const unsigned long long thr_2 = s_active[1] ? s_prefix[1] : ~0ull;   // keys below -> T2
+  const unsigned long long thr_1 = s_active[2] ? s_prefix[2] : ~0ull;   // keys below -> T1, else T0
+
+  // assign + ascending compaction of T0 / T1 / T2 / visible lists
+  if (tid < 4) s_base[tid] = 0;
+  __syncthreads();
+  uint8_t* tnew = v.tier[nxt] + (size_t)b * v.Nmax;
+  int* rnew = v.rowof[nxt] + (size_t)b * v.Nmax;
+  const int caps[3] = {v.cap0, v.cap1, v.cap2};
+  for (int base = 0; base < n; base += CLS_THREADS) {
+    const int pos = base + tid;
+    int t = -1;
+    if (pos < n) {
+      const int to = told[pos];
+      if (to == T3) t = T3;
+      else if (pos < prot_lo || pos >= prot_hi) t = T0;
+      else {
+        const unsigned long long key = ((unsigned long long)__float_as_uint(fS[pos]) << 32) | (unsigned)pos;
+        t = key < thr_e ? T3 : key < thr_2 ? T2 : key < thr_1 ? T1 : T0;
+      }
+      tnew[pos] = (uint8_t)t;
+      if (t == T3) rnew[pos] = -1;
+    }
+    unsigned m[4];
+#pragma unroll
+    for (int L4 = 0; L4 < 4; ++L4) {
+      const bool f = L4 < 3 ? (t == L4) : (t >= 0 && t != T3);
+      m[L4] = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) s_wsum[L4][w] = __popc(m[L4]);
+    }
+    __syncthreads();
+    if (w < 4) {
+      const int x = s_wsum[w][lane];
+      int inc = x;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += y;
+      }
+      s_wsum[w][lane] = inc - x;
+      if (lane == 31) s_tot[w] = inc;
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int L4 = 0; L4 < 4; ++L4) {
+      if (m[L4] & (1u << lane)) {
+        const int off = s_base[L4] + s_wsum[L4][w] + __popc(m[L4] & lt);
+        if (L4 < 3) {
+          v.idx[nxt][L4][(size_t)b * caps[L4] + off] = pos;
+          rnew[pos] = off;
+        } else {
+          v.idxvis[nxt][(size_t)b * v.Nmax + off] = pos;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < 4) s_base[tid] += s_tot[tid];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    int* cn = v.cnt[nxt] + b * CNT_STRIDE;
+    cn[0] = s_base[0];
+    cn[1] = s_base[1];
+    cn[2] = s_base[2];
+    cn[3] = n - s_base[3];
+    cn[4] = s_base[3];
+  }
+}
+
+// ------------------------------------------------------------------ a6 migrate
+// Rows of one lane: D/32 bf16 (D = 64 or 128).
+template <int D>
+struct RowIO {
+  static constexpr int E = D / 32;
+};
+
+__device__ __forceinline__ void load_bits(uint16_t* x, const uint16_t* src, int e) {
+  if (e == 4) {
+    const uint2 u = *reinterpret_cast<const uint2*>(src);
+    x[0] = u.x & 0xFFFF; x[1] = u.x >> 16; x[2] = u.y & 0xFFFF; x[3] = u.y >> 16;
+  } else {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(src);
+    x[0] = u & 0xFFFF; x[1] = u >> 16;
+  }
+}
+__device__ __forceinline__ void store_bits(uint16_t* dst, const uint16_t* x, int e) {
+  if (e == 4) {
+    *reinterpret_cast<uint2*>(dst) = make_uint2((uint32_t)x[0] | ((uint32_t)x[1] << 16),
+                                                (uint32_t)x[2] | ((uint32_t)x[3] << 16));
+  } else {
+    *reinterpret_cast<uint32_t*>(dst) = (uint32_t)x[0] | ((uint32_t)x[1] << 16);
+  }
+}
+
+// Source row (bf16 bit pattern) of position `pos` of layer/group `grp` in tier `ot`
+// with row `orow` of the buffer `cur`.  T2 sources return bf16(dequant) (AMB-12).
+template <int D>
+__device__ __forceinline__ void source_row(const DevView& v, int cur, int kv, size_t grp, int ot, int orow,
+                                           int pos, int lane, uint16_t* x) {
+  constexpr int E = D / 32;
+  if (ot == T0) {
+    const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v0[cur] : v.k0[cur]) + (grp * v.cap0 + orow) * D;
+    load_bits(x, s + lane * E, E);
+  } else if (ot == T1) {
+    const uint16_t* s;
+    if (v.stream_mode) s = reinterpret_cast<const uint16_t*>(kv ? v.hv1 : v.hk1) + (grp * v.Nmax + pos) * D;
+    else s = reinterpret_cast<const uint16_t*>(kv ? v.v1[cur] : v.k1[cur]) + (grp * v.cap1 + orow) * D;
+    load_bits(x, s + lane * E, E);
+  } else {
+    const int8_t* c = (kv ? v.c2v[cur] : v.c2k[cur]) + (grp * v.cap2 + orow) * D + lane * E;
+    const float sc = (kv ? v.s2v[cur] : v.s2k[cur])[grp * v.cap2 + orow];
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = f_to_bf16_bits(__fmul_rn((float)c[k], sc));
+  }
+}
+
+// per-row symmetric int8: scale = fp32(absmax/127), code = clamp(rint(x/scale)) (AMB-12)
+template <int D>
+__device__ __forceinline__ void quantize_row(const uint16_t* x, int8_t* codes, float* scale, int lane) {
+  constexpr int E = D / 32;
+  float f[E];
+  float amax = 0.f;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    f[k] = bf16_bits_to_f(x[k]);
+    amax = fmaxf(amax, fabsf(f[k]));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  const float sc = amax == 0.f ? 1.0f : __fdiv_rn(amax, 127.0f);
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    float qv = amax == 0.f ? 0.f : rintf(__fdiv_rn(f[k], sc));
+    qv = fminf(127.f, fmaxf(-127.f, qv));
+    codes[k] = (int8_t)qv;
+  }
+  *scale = sc;
+}
+
+// Rebuild the nxt stores from the cur ones (ping-pong): dst list z = 0 (T0 store),
+// 1 (T1 staging, differential mode), 2 (T2 store).  One warp per (row, K|V).
+template <int D>
+__global__ void __launch_bounds__(256) k_migrate(const DevView v, const int cur) {
+  constexpr int E = D / 32;
+  const int T = blockIdx.z;
+  if (T == 1 && v.stream_mode) return;
+  if (T == 2 && v.cap2 == 0) return;
+  const int nxt = cur ^ 1;
+  const int grpi = blockIdx.y;
+  const int g = grpi % v.Hkv, b = (grpi / v.Hkv) % v.B;
+  const size_t grp = (size_t)grpi;
+  const int capT = T == 0 ? v.cap0 : (T == 1 ? v.cap1 : v.cap2);
+  const int cntT = v.cnt[nxt][b * CNT_STRIDE + T];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = blockIdx.x * 32;
+  const int j1 = min(j0 + 32, cntT);
+  for (int j = j0 + w; j < j1; j += 8) {
+    const int pos = v.idx[nxt][T][(size_t)b * capT + j];
+    const int ot = v.tier[cur][(size_t)b * v.Nmax + pos];
+    const int orow = v.rowof[cur][(size_t)b * v.Nmax + pos];
+    for (int kv = 0; kv < 2; ++kv) {
+      if (T == 2) {
+        int8_t* dc = (kv ? v.c2v[nxt] : v.c2k[nxt]) + (grp * v.cap2 + j) * D + lane * E;
+        float* ds = (kv ? v.s2v[nxt] : v.s2k[nxt]) + grp * v.cap2 + j;
+        if (ot == T2) {
+          const int8_t* sc = (kv ? v.c2v[cur] : v.c2k[cur]) + (grp * v.cap2 + orow) * D + lane * E;
+#pragma unroll
+          for (int k = 0; k < E; ++k) dc[k] = sc[k];
+          if (lane == 0) *ds = (kv ? v.s2v[cur] : v.s2k[cur])[grp * v.cap2 + orow];
+        } else {
+          uint16_t x[E];
+          source_row<D>(v, cur, kv, grp, ot, orow, pos, lane, x);
+          int8_t codes[E];
+          float sc;
+          quantize_row<D>(x, codes, &sc, lane);
+#pragma unroll
+          for (int k = 0; k < E; ++k) dc[k] = codes[k];
+          if (lane == 0) *ds = sc;
+        }
+      } else {
+        uint16_t x[E];
+        source_row<D>(v, cur, kv, grp, ot, orow, pos, lane, x);
+        uint16_t* dst = T == 0
+            ? reinterpret_cast<uint16_t*>(kv ? v.v0[nxt] : v.k0[nxt]) + (grp * v.cap0 + j) * D
+            : reinterpret_cast<uint16_t*>(kv ? v.v1[nxt] : v.k1[nxt]) + (grp * v.cap1 + j) * D;
+        store_bits(dst + lane * E, x, E);
+      }
+    }
+  }
+}
+
+// Offload to the pinned host stores (zero-copy stores over the host link), on the
+// side stream: rows newly in T1 (paper: "Offload T1 entries") and new T2 codes.
+template <int D>
+__global__ void __launch_bounds__(256) k_offload_host(const DevView v, const int cur) {
+  constexpr int E = D / 32;
+  const int T = blockIdx.z + 1;            // 1: T1 rows, 2: T2 codes
+  if (T == 2 && (v.cap2 == 0 || v.hc2k == nullptr)) return;
+  const int nxt = cur ^ 1;
+  const int grpi = blockIdx.y;
+  const int g = grpi % v.Hkv, b = (grpi / v.Hkv) % v.B;
+  const size_t grp = (size_t)grpi;
+  const int capT = T == 1 ? v.cap1 : v.cap2;
+  const int cntT = v.cnt[nxt][b * CNT_STRIDE + T];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = blockIdx.x * 32;
+  const int j1 = min(j0 + 32, cntT);
+  unsigned long long rows = 0;
+  for (int j = j0 + w; j < j1; j += 8) {
+    const int pos = v.idx[nxt][T][(size_t)b * capT + j];
+    const int ot = v.tier[cur][(size_t)b * v.Nmax + pos];
+    if (ot == T) continue;          // already in this host store
+    const int orow = v.rowof[cur][(size_t)b * v.Nmax + pos];
+    for (int kv = 0; kv < 2; ++kv) {
+      if (T == 1) {
+        uint16_t x[E];
+        if (!v.stream_mode) {
+          const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v1[nxt] : v.k1[nxt]) + (grp * v.cap1 + j) * D;
+          load_bits(x, s + lane * E, E);
+        } else {
+          source_row<D>(v, cur, kv, grp, ot, orow, pos, lane, x);
+        }
+        uint16_t* dst = reinterpret_cast<uint16_t*>(kv ? v.hv1 : v.hk1) + (grp * v.Nmax + pos) * D;
+        store_bits(dst + lane * E, x, E);
+      } else {
+        const int8_t* sc = (kv ? v.c2v[nxt] : v.c2k[nxt]) + (grp * v.cap2 + j) * D + lane * E;
+        int8_t* dc = (kv ? v.hc2v : v.hc2k) + (grp * v.Nmax + pos) * D + lane * E;
+#pragma unroll
+        for (int k = 0; k < E; ++k) dc[k] = sc[k];
+        if (lane == 0) (kv ? v.hs2v : v.hs2k)[grp * v.Nmax + pos] = (kv ? v.s2v[nxt] : v.s2k[nxt])[grp * v.cap2 + j];
+      }
+    }
+    rows += 2;
+  }
+  if (lane == 0 && rows) atomicAdd(&v.st->d2h_rows, rows);
+}
+
+__global__ void k_commit(const DevView v) {
+  if (threadIdx.x == 0) {
+    v.st->cur ^= 1;
+    v.st->n_event = v.st->n;
+  }
+}
+
+// a2 stream mode: T1 rows of `layer` from pinned host memory -> HBM ring slot layer&1.
+template <int D>
+__global__ void __launch_bounds__(256) k_prefetch(const DevView v, const int layer) {
+  constexpr int E = D / 32;
+  const int unit = blockIdx.y;
+  const int b = unit / v.Hkv, g = unit % v.Hkv;
+  const int cur = v.st->cur;
+  const int n1 = v.cnt[cur][b * CNT_STRIDE + 1];
+  const size_t grp = grp_of(v, layer, b, g);
+  const size_t sg = ((size_t)(layer & 1) * v.B + b) * v.Hkv + g;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = blockIdx.x * 32;
+  const int j1 = min(j0 + 32, n1);
+  for (int j = j0 + w; j < j1; j += 8) {
+    const int pos = v.idx[cur][1][(size_t)b * v.cap1 + j];
+    for (int kv = 0; kv < 2; ++kv) {
+      const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.hv1 : v.hk1) + (grp * v.Nmax + pos) * D;
+      uint16_t* d = reinterpret_cast<uint16_t*>(kv ? v.v1[0] : v.k1[0]) + (sg * v.cap1 + j) * D;
+      uint16_t x[E];
+      load_bits(x, s + lane * E, E);
+      store_bits(d + lane * E, x, E);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+cudaError_t launch_begin_step(const DevView& v, cudaStream_t s) {
+  k_begin_step<<<1, ((v.B + 31) / 32) * 32, 0, s>>>(v);
+  return cudaGetLastError();
+}
+cudaError_t launch_end_step(const DevView& v, cudaStream_t s) {
+  k_end_step<<<1, 32, 0, s>>>(v);
+  return cudaGetLastError();
+}
+cudaError_t launch_append(const DevView& v, int layer, const void* k, const void* vv, cudaStream_t s) {
+  k_append<<<v.B * v.Hkv, 64, 0, s>>>(v, layer, reinterpret_cast<const uint16_t*>(k),
+                                      reinterpret_cast<const uint16_t*>(vv));
+  return cudaGetLastError();
+}
+cudaError_t launch_load_prefix(const DevView& v, int layer, const void* k, const void* vv, int n0, cudaStream_t s) {
+  dim3 grid(64, v.B * v.Hkv);
+  k_load_prefix<<<grid, 256, 0, s>>>(v, layer, reinterpret_cast<const uint16_t*>(k),
+                                    reinterpret_cast<const uint16_t*>(vv), n0);
+  return cudaGetLastError();
+}
+cudaError_t launch_init_meta(const DevView& v, int n0, cudaStream_t s) {
+  dim3 grid((v.Nmax + 255) / 256, v.B);
+  k_init_meta<<<grid, 256, 0, s>>>(v, n0);
+  return cudaGetLastError();
+}
+cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s) {
+  (void)layer;
+  dim3 grid((v.Nmax + 255) / 256, v.B * v.Hkv);
+  k_score_update<<<grid, 256, 0, s>>>(v, probs);
+  return cudaGetLastError();
+}
+cudaError_t launch_classify(const DevView& v, cudaStream_t s) {
+  k_classify<<<v.B, CLS_THREADS, 0, s>>>(v);
+  return cudaGetLastError();
+}
+cudaError_t launch_migrate(const DevView& v, int cur, cudaStream_t s) {
+  const int capmax = max(v.cap0, max(v.cap1, v.cap2));
+  dim3 grid((capmax + 31) / 32, v.L * v.B * v.Hkv, 3);
+  if (v.D == 128) k_migrate<128><<<grid, 256, 0, s>>>(v, cur);
+  else k_migrate<64><<<grid, 256, 0, s>>>(v, cur);
+  return cudaGetLastError();
+}
+cudaError_t launch_offload_host(const DevView& v, int cur, cudaStream_t s) {
+  const int capmax = max(v.cap1, v.cap2);
+  if (capmax == 0) return cudaSuccess;
+  dim3 grid((capmax + 31) / 32, v.L * v.B * v.Hkv, 2);
+  if (v.D == 128) k_offload_host<128><<<grid, 256, 0, s>>>(v, cur);
+  else k_offload_host<64><<<grid, 256, 0, s>>>(v, cur);
+  return cudaGetLastError();
+}
+cudaError_t launch_commit(const DevView& v, cudaStream_t s) {
+  k_commit<<<1, 32, 0, s>>>(v);
+  return cudaGetLastError();
+}
+cudaError_t launch_prefetch(const DevView& v, int layer, cudaStream_t s) {
+  if (v.cap1 == 0) return cudaSuccess;
+  dim3 grid((v.cap1 + 31) / 32, v.B * v.Hkv);
+  if (v.D == 128) k_prefetch<128><<<grid, 256, 0, s>>>(v, layer);
+  else k_prefetch<64><<<grid, 256, 0, s>>>(v, layer);
+  return cudaGetLastError();
+}
+
+}  // namespace kvt

@@ -1,0 +1,243 @@
+"""Thin ctypes binding of libkvtier.so (include/kv_tier.h) -- argument marshalling only.
+
+Every step of the path runs in the library's CUDA kernels; PyTorch only provides
+device memory (one arena tensor) and streams.  Functions keep the C names.
+There is no fallback: if the library or a GPU is missing, loading fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(_HERE, "lib")
+
+KV_TIER_OK = 0
+STATUS = {0: "OK", -1: "E_INVAL", -2: "E_CUDA", -3: "E_NCCL", -4: "E_STATE", -5: "E_CAPACITY",
+          -6: "E_OOM", -7: "E_NUMERIC"}
+EVICT_TOTAL, EVICT_PER_EVENT = 0, 1
+STAGING_ALL = 0xFFFFFFFF
+X_SCORES, X_TIERS, X_IDX_T0, X_IDX_T1, X_IDX_T2, X_T0_ROWS, X_T1_ROWS, X_STAGING, X_T2_CODES, X_T2_SCALES = range(10)
+
+
+class KvTierError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "num_requests", "num_layers", "num_q_heads", "num_kv_heads", "head_dim", "max_tokens",
+        "prompt_len", "sink_size", "window_size", "manage_interval")] + [
+        ("hbm_ratio_bp", C.c_uint32), ("evict_ratio_bp", C.c_uint32), ("t2_fraction_bp", C.c_uint32),
+        ("evict_mode", C.c_int32), ("staging_tokens", C.c_uint32),
+        ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("shard", C.c_int32),
+        ("out_fp32", C.c_int32), ("split", C.c_int32)]
+
+
+class Sizes(C.Structure):
+    _fields_ = [(n, C.c_size_t) for n in (
+        "device_arena", "t0_store", "t1_staging", "t2_store", "scores", "meta", "host_t1", "host_t2")] + [
+        ("cap_t0", C.c_int32), ("cap_t1", C.c_int32), ("cap_t2", C.c_int32)]
+
+
+class Buffers(C.Structure):
+    _fields_ = [("device_arena", C.c_void_p)]
+
+
+_lib = None
+_SIGS = {
+    "kv_tier_query_sizes": [C.POINTER(Config), C.POINTER(Sizes)],
+    "kv_tier_init": [C.POINTER(Config), C.POINTER(Buffers), C.c_void_p, C.POINTER(C.c_void_p)],
+    "kv_tier_destroy": [C.c_void_p],
+    "kv_tier_load_prefix": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p],
+    "kv_tier_begin_step": [C.c_void_p, C.c_void_p],
+    "kv_tier_append": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p],
+    "kv_tier_prefetch": [C.c_void_p, C.c_int32, C.c_void_p],
+    "kv_tier_decode_attention": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p],
+    "kv_tier_score_update": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p],
+    "kv_tier_visible_count": [C.c_void_p, C.POINTER(C.c_int32)],
+    "kv_tier_end_step": [C.c_void_p, C.c_void_p],
+    "kv_tier_step": [C.c_void_p] + [C.c_void_p] * 4 + [C.c_int32, C.c_void_p, C.c_void_p],
+    "kv_tier_step_graph_capture": [C.c_void_p] + [C.c_void_p] * 4 + [C.c_int32, C.c_void_p, C.c_void_p],
+    "kv_tier_step_graph_launch": [C.c_void_p, C.c_void_p],
+    "kv_tier_classify": [C.c_void_p, C.c_void_p],
+    "kv_tier_migrate": [C.c_void_p, C.c_void_p, C.c_void_p],
+    "kv_tier_sync": [C.c_void_p],
+    "kv_tier_census": [C.c_void_p, C.c_void_p, C.c_void_p],
+    "kv_tier_position": [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
+    "kv_tier_export_size": [C.c_void_p, C.c_int32, C.POINTER(C.c_size_t)],
+    "kv_tier_export": [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t],
+    "kv_tier_import_scores": [C.c_void_p, C.c_void_p, C.c_size_t],
+    "kv_tier_last_error": [C.c_void_p],
+    "kv_tier_version": [],
+}
+EXPORTED = sorted(_SIGS)
+
+
+def lib_path(name="libkvtier.so"):
+    return os.path.join(LIB_DIR, name)
+
+
+def load():
+    """dlopen libkvtier.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        p = lib_path()
+        if not os.path.exists(p):
+            raise FileNotFoundError(f"{p} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = C.CDLL(p)
+        for name, args in _SIGS.items():
+            f = getattr(lib, name)
+            f.argtypes = args
+            f.restype = C.c_char_p if name in ("kv_tier_last_error", "kv_tier_version") else C.c_int
+        _lib = lib
+    return _lib
+
+
+def _check(st, ctx=None):
+    if st != KV_TIER_OK:
+        msg = load().kv_tier_last_error(ctx)
+        raise KvTierError(st, msg.decode() if msg else "")
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+def make_config(B, L, Hq, Hkv, d, max_tokens, prompt_len, hbm_bp=5000, evict_bp=500, t2_bp=0,
+                sink_size=4, window_size=128, manage_interval=64, evict_mode=EVICT_TOTAL,
+                staging=STAGING_ALL, device=0, out_fp32=1, split=0, rank=0, world=1):
+    return Config(num_requests=B, num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=d,
+                  max_tokens=max_tokens, prompt_len=prompt_len, sink_size=sink_size,
+                  window_size=window_size, manage_interval=manage_interval, hbm_ratio_bp=hbm_bp,
+                  evict_ratio_bp=evict_bp, t2_fraction_bp=t2_bp, evict_mode=evict_mode,
+                  staging_tokens=staging, device=device, rank=rank, world=world, shard=0,
+                  out_fp32=out_fp32, split=split)
+
+
+def query_sizes(cfg):
+    s = Sizes()
+    _check(load().kv_tier_query_sizes(C.byref(cfg), C.byref(s)))
+    return s
+
+
+class KvTier:
+    """One ctx.  The device arena is a torch uint8 tensor owned by this object."""
+
+    def __init__(self, cfg: Config):
+        import torch
+        self.cfg = cfg
+        self.sizes = query_sizes(cfg)
+        self.arena = torch.empty(self.sizes.device_arena, dtype=torch.uint8, device=f"cuda:{cfg.device}")
+        buf = Buffers(device_arena=C.c_void_p(self.arena.data_ptr()))
+        h = C.c_void_p()
+        _check(load().kv_tier_init(C.byref(cfg), C.byref(buf), None, C.byref(h)))
+        self.ctx = h
+
+    def close(self):
+        if self.ctx:
+            load().kv_tier_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # --- the path (names as in kv_tier.h)
+    def load_prefix(self, layer, k, v, n0, stream=None):
+        _check(load().kv_tier_load_prefix(self.ctx, layer, C.c_void_p(k.data_ptr()), C.c_void_p(v.data_ptr()),
+                                          n0, _stream_ptr(stream)), self.ctx)
+
+    def begin_step(self, stream=None):
+        _check(load().kv_tier_begin_step(self.ctx, _stream_ptr(stream)), self.ctx)
+
+    def append(self, layer, k_new, v_new, stream=None):
+        _check(load().kv_tier_append(self.ctx, layer, C.c_void_p(k_new.data_ptr()), C.c_void_p(v_new.data_ptr()),
+                                     _stream_ptr(stream)), self.ctx)
+
+    def prefetch(self, layer, side=None):
+        _check(load().kv_tier_prefetch(self.ctx, layer, _stream_ptr(side)), self.ctx)
+
+    def decode_attention(self, layer, q, o, fuse_score_update=1, stream=None):
+        _check(load().kv_tier_decode_attention(self.ctx, layer, C.c_void_p(q.data_ptr()), C.c_void_p(o.data_ptr()),
+                                               fuse_score_update, _stream_ptr(stream)), self.ctx)
+
+    def score_update(self, layer, probs, stream=None):
+        _check(load().kv_tier_score_update(self.ctx, layer, C.c_void_p(probs.data_ptr()), _stream_ptr(stream)),
+               self.ctx)
+
+    def visible_count(self):
+        n = C.c_int32()
+        _check(load().kv_tier_visible_count(self.ctx, C.byref(n)), self.ctx)
+        return n.value
+
+    def end_step(self, stream=None):
+        _check(load().kv_tier_end_step(self.ctx, _stream_ptr(stream)), self.ctx)
+
+    def step(self, q, k_new, v_new, o, fuse_score_update=1, stream=None, side=None):
+        _check(load().kv_tier_step(self.ctx, *(C.c_void_p(x.data_ptr()) for x in (q, k_new, v_new, o)),
+                                   fuse_score_update, _stream_ptr(stream), _stream_ptr(side)), self.ctx)
+
+    def step_graph_capture(self, q, k_new, v_new, o, fuse_score_update=1, stream=None, side=None):
+        _check(load().kv_tier_step_graph_capture(self.ctx, *(C.c_void_p(x.data_ptr()) for x in (q, k_new, v_new, o)),
+                                                 fuse_score_update, _stream_ptr(stream), _stream_ptr(side)), self.ctx)
+
+    def step_graph_launch(self, stream=None):
+        _check(load().kv_tier_step_graph_launch(self.ctx, _stream_ptr(stream)), self.ctx)
+
+    def classify(self, stream=None):
+        _check(load().kv_tier_classify(self.ctx, _stream_ptr(stream)), self.ctx)
+
+    def migrate(self, stream=None, side=None):
+        _check(load().kv_tier_migrate(self.ctx, _stream_ptr(stream), _stream_ptr(side)), self.ctx)
+
+    def sync(self):
+        _check(load().kv_tier_sync(self.ctx), self.ctx)
+
+    def census(self):
+        counts = np.zeros((self.cfg.num_requests, 4), dtype=np.int32)
+        rows = C.c_int64()
+        _check(load().kv_tier_census(self.ctx, counts.ctypes.data_as(C.c_void_p), C.byref(rows)), self.ctx)
+        return counts, rows.value
+
+    def position(self):
+        n, t = C.c_int32(), C.c_int32()
+        _check(load().kv_tier_position(self.ctx, C.byref(n), C.byref(t)), self.ctx)
+        return n.value, t.value
+
+    def export(self, what, layer=0):
+        nbytes = C.c_size_t()
+        _check(load().kv_tier_export_size(self.ctx, what, C.byref(nbytes)), self.ctx)
+        buf = np.zeros(nbytes.value, dtype=np.uint8)
+        _check(load().kv_tier_export(self.ctx, what, layer, buf.ctypes.data_as(C.c_void_p), nbytes.value), self.ctx)
+        B, H, D = self.cfg.num_requests, self.cfg.num_kv_heads, self.cfg.head_dim
+        if what == X_SCORES:
+            return buf.view(np.float32).reshape(B, H, -1)
+        if what == X_TIERS:
+            return buf.reshape(B, -1)
+        if what in (X_IDX_T0, X_IDX_T1, X_IDX_T2):
+            return buf.view(np.int32).reshape(B, -1)
+        if what in (X_T0_ROWS, X_T1_ROWS, X_STAGING):
+            return buf.view(np.uint16).reshape(B, H, -1, 2, D)
+        if what == X_T2_CODES:
+            return buf.view(np.int8).reshape(B, H, -1, 2, D)
+        return buf.view(np.float32).reshape(B, H, -1, 2)
+
+    def import_scores(self, S):
+        S = np.ascontiguousarray(S, dtype=np.float32)
+        _check(load().kv_tier_import_scores(self.ctx, S.ctypes.data_as(C.c_void_p), S.nbytes), self.ctx)
+
+
+def version():
+    return load().kv_tier_version().decode()

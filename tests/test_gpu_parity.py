@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on identical seeded inputs.
+
+Bars (BASELINE.json north star, DESIGN.md AMB-17/18): tiers, index lists and migrated
+T0/T1 bytes and T2 codes bit-exact; attention o within |g-o| <= 2e-3 + 1e-2|o|;
+scores within 1e-5 relative.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import kvtier_oracle as O
+from paper_2605_09490_b200 import harness as H
+from paper_2605_09490_b200 import kvtier as kt
+from paper_2605_09490_b200.synth import synth as S
+from tests.oracle_runner import OracleRun, o_close, s_close
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests (no CPU fallback exists)")
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def _bf16_bits(a):
+    return np.asarray(a, dtype=np.float32).view(np.uint32) >> 16
+
+
+def _check_event_state(run, orc, reqs_gpu, layers=(0,)):
+    """Tiers, index lists, census and store bytes after a manage event."""
+    kv = run.kv
+    st = orc.st
+    n = st.n
+    tiers = kv.export(kt.X_TIERS)
+    idx = [kv.export(w) for w in (kt.X_IDX_T0, kt.X_IDX_T1, kt.X_IDX_T2)]
+    counts, _ = kv.census()
+    for bo, bg in enumerate(reqs_gpu):
+        want = st.tier[bo, :n]
+        assert np.array_equal(tiers[bg], want), f"tiers differ for request {bg}"
+        for T in range(3):
+            assert np.array_equal(idx[T][bg], O.export_index(st, bo, T)), f"idx T{T} request {bg}"
+        assert counts[bg].tolist() == O.census(st, bo).tolist()
+    for l in layers:
+        t0 = kv.export(kt.X_T0_ROWS, l)
+        t1 = kv.export(kt.X_T1_ROWS, l)
+        stg = kv.export(kt.X_STAGING, l) if run.w["staging"] != 0 else None
+        for bo, bg in enumerate(reqs_gpu):
+            for T, rows in ((0, t0), (1, t1)):
+                pos = O.export_index(st, bo, T)
+                wk = _bf16_bits(st.rowK[l, bo, :, pos].transpose(1, 0, 2))
+                wv = _bf16_bits(st.rowV[l, bo, :, pos].transpose(1, 0, 2))
+                assert np.array_equal(rows[bg][:, :, 0, :], wk), f"T{T} K rows layer {l} req {bg}"
+                assert np.array_equal(rows[bg][:, :, 1, :], wv), f"T{T} V rows layer {l} req {bg}"
+            if stg is not None:
+                assert np.array_equal(stg[bg], t1[bg]), "HBM staging != pinned host T1 store"
+        if run.w["t2_bp"]:
+            codes = kv.export(kt.X_T2_CODES, l)
+            scales = kv.export(kt.X_T2_SCALES, l)
+            for bo, bg in enumerate(reqs_gpu):
+                pos = O.export_index(st, bo, 2)
+                assert np.array_equal(codes[bg][:, :, 0, :], st.codeK[l, bo, :, pos].transpose(1, 0, 2))
+                assert np.array_equal(codes[bg][:, :, 1, :], st.codeV[l, bo, :, pos].transpose(1, 0, 2))
+                assert np.array_equal(scales[bg][:, :, 0], st.scaleK[l, bo, :, pos].T)
+                assert np.array_equal(scales[bg][:, :, 1], st.scaleV[l, bo, :, pos].T)
+
+
+def _run_pair(w, reqs=None, graph=False, check_every=1, layers_api=False, split=0):
+    run = H.TieredDecode(w, split=split)
+    orc = OracleRun(w, reqs=reqs)
+    reqs_gpu = orc.reqs
+    if graph:
+        run.capture()
+    worst = 0.0
+    for t in range(w["steps"]):
+        o_gpu = (run.step_layers() if layers_api else run.step()).cpu().numpy()
+        o_ref = orc.step()
+        if t % check_every == 0 or run.is_event(t) or t == w["steps"] - 1:
+            run.sync()
+            ok, mabs, _ = o_close(o_gpu[:, reqs_gpu], o_ref)
+            worst = max(worst, mabs)
+            assert ok, f"attention o mismatch at step {t}: max abs {mabs}"
+            S_gpu = run.kv.export(kt.X_SCORES)
+            ok, mrel = s_close(S_gpu[reqs_gpu], orc.st.S_part[:, :, :orc.st.n])
+            assert ok, f"scores mismatch at step {t}: max rel {mrel}"
+            if run.is_event(t):
+                _check_event_state(run, orc, reqs_gpu)
+    run.close()
+    return worst
+
+
+# --------------------------------------------------------------------- generator
+def test_synth_gpu_matches_cpu():
+    from paper_2605_09490_b200.synth import synth_gpu as SG
+    import __graft_entry__
+    __graft_entry__.build()
+    dev = torch.device("cuda:0")
+    for which in ("k", "v"):
+        g = SG.gen_kv(7, which, 3, 2, 2, 64, 100, 40, 16, 4, dev).view(torch.int16).cpu().numpy().view(np.uint16)
+        c = S.gen_kv(7, which, 3, 2, 2, 64, 100, 40, 16, 4)
+        assert np.array_equal(g, c)
+    g = SG.gen_q(9, 5, 3, 2, 2, 8, 2, 128, dev).view(torch.int16).cpu().numpy().view(np.uint16)
+    assert np.array_equal(g, S.gen_q(9, 5, 3, 2, 2, 8, 2, 128))
+
+
+# --------------------------------------------------------------------- tiny end to end
+def test_tiny_32_steps():                     # BASELINE.json configs[0]
+    _run_pair(H.workload("tiny"))
+
+
+def test_tiny_delta8_events():                # events at t = 0, 8, 16, 24
+    _run_pair(H.workload("tiny", interval=8))
+
+
+def test_tiny_t2_half():                      # f2 = 50 %: int8 T2 rows in attention + codec bytes
+    _run_pair(H.workload("tiny", interval=8, t2_bp=5000))
+
+
+def test_tiny_per_event_mode():               # AMB-9 literal Alg. 1
+    _run_pair(H.workload("tiny", interval=8, evict_mode=kt.EVICT_PER_EVENT, evict_bp=1000))
+
+
+def test_tiny_stream_mode_layers_api():       # S = 0: T1 re-fetched from pinned host every step
+    _run_pair(H.workload("tiny", interval=8, staging=0, L=3), layers_api=True)
+
+
+def test_tiny_graph_stream_mode():
+    _run_pair(H.workload("tiny", interval=8, staging=0, L=3, t2_bp=3000), graph=True)
+
+
+@pytest.mark.parametrize("split", [1, 3, 8])
+def test_tiny_cluster_splits(split):          # DSMEM merge at several cluster sizes
+    _run_pair(H.workload("tiny", interval=8, B=3, L=2, steps=17), split=split)
+
+
+def test_multi_request_multi_layer_graph():   # several tiles, ragged tails, B > 1, d = 128
+    w = H.workload("tiny", B=3, L=2, Hq=12, Hkv=2, d=128, N=700, P=40, interval=16, steps=40,
+                   hbm_bp=3000, evict_bp=1000, t2_bp=2500)
+    _run_pair(w, graph=True, check_every=7)
+
+
+# --------------------------------------------------------------------- 7B-shaped, sampled
+def test_7b_sampled_requests():               # BASELINE.json configs[1], bench launch configuration
+    w = H.workload("7b", steps=66)
+    _run_pair(w, reqs=[0, 5], graph=True, check_every=16)
+
+
+# --------------------------------------------------------------------- classify cross-fed
+@pytest.mark.parametrize("kind", ["ties", "cont"])
+def test_classify_crossfed_bit_exact(kind):   # AMB-18 (i): identical S -> identical tiers
+    w = H.workload("tiny", B=4, L=1, N=3000, P=64, steps=3, interval=1, hbm_bp=3000, evict_bp=700,
+                   t2_bp=4000)
+    run = H.TieredDecode(w)
+    cfg = O.OracleConfig(B=4, L=1, Hq=4, Hkv=2, d=64, prompt_len=64, hbm_bp=3000, evict_bp=700, t2_bp=4000)
+    tier = np.zeros((4, 3002), np.uint8)
+    for t in range(3):
+        with torch.cuda.stream(run.main):
+            run.kv.step(run.Q[t], run.Kn[t], run.Vn[t], run.O, 1, stream=run.main, side=run.side)
+        run.sync()
+        n = run.kv.position()[0]
+        Sp = S.gen_scores(100 + t, 4, 2, n, kind)
+        run.kv.import_scores(Sp)
+        run.kv.classify(stream=run.main)
+        run.kv.migrate(stream=run.main, side=run.side)
+        run.sync()
+        got = run.kv.export(kt.X_TIERS)
+        tier[:, n - 1] = 0
+        for b in range(4):
+            want = O.classify_request(Sp[b], tier[b], n, cfg)
+            assert np.array_equal(got[b], want), (t, b)
+            tier[b, :n] = want
+    run.close()
+
+
+# --------------------------------------------------------------------- Prop. 1 on the GPU
+def test_prop1_gpu_outputs_independent_of_beta():
+    outs, t3 = [], []
+    for beta in (3000, 5000, 7000):
+        w = H.workload("tiny", interval=8, hbm_bp=beta, B=2, L=2)
+        run = H.TieredDecode(w)
+        run.capture()
+        seq = []
+        for t in range(w["steps"]):
+            seq.append(run.step().cpu().numpy().copy())
+        run.sync()
+        outs.append(np.stack(seq))
+        t3.append(run.kv.export(kt.X_TIERS) == 3)
+        run.close()
+    for k in (1, 2):
+        assert np.array_equal(t3[k], t3[0])
+        ok, mabs, _ = o_close(outs[k], outs[0].astype(np.float64))
+        assert ok and mabs < 1e-4, mabs
+
+
+def test_graph_equals_layer_calls_bitwise():
+    w = H.workload("tiny", interval=8, B=2, L=2, t2_bp=3000)
+    a = H.TieredDecode(w)
+    b = H.TieredDecode(w)
+    b.capture()
+    for t in range(w["steps"]):
+        oa = a.step_layers().cpu().numpy()
+        ob = b.step().cpu().numpy()
+        assert np.array_equal(oa, ob), t
+    a.sync(); b.sync()
+    assert np.array_equal(a.kv.export(kt.X_SCORES), b.kv.export(kt.X_SCORES))
+    a.close(); b.close()
+
+
+def test_stream_mode_equals_differential_bitwise():   # same rows, same order -> same bits
+    outs = []
+    for staging in (kt.STAGING_ALL, 0):
+        w = H.workload("tiny", interval=8, B=2, L=3, staging=staging)
+        run = H.TieredDecode(w)
+        run.capture()
+        outs.append(np.stack([run.step().cpu().numpy().copy() for _ in range(w["steps"])]))
+        run.close()
+    assert np.array_equal(outs[0], outs[1])
+
+
+# --------------------------------------------------------------------- standalone score update
+def test_score_update_external_matches_oracle():
+    w = H.workload("tiny", interval=8, B=2, L=1, steps=12)
+    run = H.TieredDecode(w)
+    cfg_G = w["Hq"] // w["Hkv"]
+    for t in range(12):
+        run.step()
+    run.sync()
+    S_before = run.kv.export(kt.X_SCORES).copy()
+    tiers = run.kv.export(kt.X_TIERS)
+    nvis = run.kv.visible_count()
+    rng = np.random.default_rng(0)
+    probs = rng.random((2, w["Hq"], nvis)).astype(np.float32)
+    run.kv.score_update(0, torch.from_numpy(probs).cuda(), stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    got = run.kv.export(kt.X_SCORES)
+    for b in range(2):
+        vis = np.nonzero(tiers[b] != 3)[0]
+        assert len(vis) == nvis
+        want = O.score_update_external(S_before[b].copy(), vis, probs[b], cfg_G)
+        assert np.array_equal(got[b], want) or s_close(got[b], want)[0]
+    run.close()
+
+
+# --------------------------------------------------------------------- error behaviour
+def test_abi_errors():
+    w = H.workload("tiny", steps=2)
+    run = H.TieredDecode(w)
+    with pytest.raises(kt.KvTierError) as e:
+        run.kv.migrate(stream=run.main, side=run.side)
+    assert e.value.status == -4                       # E_STATE: migrate without classify
+    with pytest.raises(kt.KvTierError) as e:
+        run.kv.decode_attention(5, run.Q[0, 0], run.O[0], 1, stream=run.main)
+    assert e.value.status == -1                       # E_INVAL: layer out of range
+    run.step()
+    run.step()
+    with pytest.raises(kt.KvTierError) as e:          # E_CAPACITY: N_max reached
+        run.step()
+    assert e.value.status == -5
+    run.close()
