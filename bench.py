@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the tiered-KV decode hot path (BASELINE.json metric):
+tiered decode steps/s, HBM GB/s vs roofline, T1 prefetch overhead % of step time.
+
+A step = one decode step of the whole path over one batch: new-token append, prefetch,
+GQA decode attention + fused score update for every layer, and (every Delta = 64 steps)
+classify + migrate.  Default workload: BASELINE.json configs[1], 7B-shaped, beta 50% /
+r 5%, differential staging (paper §3.4).  Inputs are synthetic (synth.py recipe) and
+the per-step K/V traffic (876 MB) exceeds the 126 MB L2, so no L2 flush is needed.
+
+    python bench.py [--gpus N --steps K --warmup W]          # our CUDA path
+    python bench.py --impl reference ...                      # the CPU oracle (reference arm)
+Multi-GPU: one process per GPU (torchrun), requests sharded across ranks (weak scaling,
+no collective in the step), time = max over ranks.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured (MEASURED_PEAKS.json)"}
+    return PEAKS_FALLBACK
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=192)
+    ap.add_argument("--warmup", type=int, default=64)
+    ap.add_argument("--impl", default="kvtier", choices=["kvtier", "reference"])
+    ap.add_argument("--config", default="7b")
+    ap.add_argument("--hbm", type=int, default=5000, help="beta in basis points")
+    ap.add_argument("--evict", type=int, default=500, help="r in basis points")
+    ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--no-extras", action="store_true", help="skip control/e2e/stream/cpu legs")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """NVML clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index, self.samples, self.reasons, self._stop = index, [], set(), threading.Event()
+        self.max_mhz = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.nv = pynvml
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        except Exception as e:           # no NVML: report it
+            self.nv = None
+            self.err = str(e)
+        return self
+
+    def _run(self):
+        nv = self.nv
+        names = {getattr(nv, k): k.replace("nvmlClocksThrottleReason", "").replace("nvmlClocksEventReason", "")
+                 for k in dir(nv) if k.startswith(("nvmlClocksThrottleReason", "nvmlClocksEventReason"))
+                 and isinstance(getattr(nv, k), int)}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in names.items():
+                    if bit and bit not in (0,) and (mask & bit) == bit and name not in ("None", "All", "GpuIdle"):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join(timeout=1)
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ byte accounting
+def attn_bytes_per_layer(w, counts, n_vis, out_bytes=2):
+    """Algorithmic HBM bytes of one decode_attention launch: every visible
+    K/V row once (4*d B per bf16 token per kv head; 2*(d+4) B per int8 T2 token), q and o,
+    and the 8 B fp32 read+write of the score per visible token per kv head."""
+    B, Hq, Hkv, d = w["B"], w["Hq"], w["Hkv"], w["d"]
+    n01, n2 = counts[0] + counts[1], counts[2]
+    kv = B * Hkv * (n01 * 4 * d + n2 * 2 * (d + 4))
+    return kv + B * Hq * d * (2 + out_bytes) + 8 * B * Hkv * n_vis
+
+
+def timed(fn, stream, n):
+    import torch
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(n):
+        fn()
+    b.record(stream)
+    b.synchronize()
+    return a.elapsed_time(b) / 1e3
+
+
+def _max_over_ranks(x):
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier_sync():
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def cpu_oracle_sample(w, budget_s):
+    """Time the CPU oracle (as it stands) on 1 request of the workload, all layers, a few
+    decode steps (first includes the t=0 manage event); return per-full-batch steps/s."""
+    import numpy as np
+    from tests.oracle_runner import OracleRun
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
+    except Exception:
+        threads = 1
+    probe = dict(w, steps=64)
+    orc = OracleRun(probe, reqs=[0])
+    t0 = time.perf_counter()
+    orc.step()
+    first = time.perf_counter() - t0
+    k = 1
+    t0 = time.perf_counter()
+    while k < 64 and (time.perf_counter() - t0) + first < budget_s:
+        orc.step()
+        k += 1
+    el = first + (time.perf_counter() - t0)
+    per_req_step = el / k
+    sps = 1.0 / (per_req_step * w["B"])
+    return {"value": sps, "unit": "steps/s", "cores": int(threads), "kind": "oracle",
+            "sample": f"1 of {w['B']} requests x {w['L']} layers x {k} decode steps (t=0 event incl.), "
+                      f"{el:.1f} s; scaled x{w['B']} requests to the full batch"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2605_09490_b200.synth import synth as S
+    w = dict(S.WORKLOADS[args.config], hbm_bp=args.hbm, evict_bp=args.evict, interval=64, t2_bp=0, evict_mode=0)
+    budget = max(5.0, min(60.0, args.cpu_seconds * (args.steps + args.warmup) / 256))
+    cb = cpu_oracle_sample(w, budget)
+    val = cb["value"]
+    print(json.dumps({
+        "impl": "reference", "metric": f"tiered decode steps/sec ({args.config}-shaped)", "value": val,
+        "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / val, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}-shaped B={w['B']} L={w['L']} Hq/Hkv={w['Hq']}/{w['Hkv']} d={w['d']} "
+                               f"N={w['N']} beta={args.hbm}bp r={args.evict}bp"},
+        "cpu_baseline": cb,
+        "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ------------------------------------------------------------------ GPU legs
+def main():
+    args = _args()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_2605_09490_b200 import harness as H
+    from paper_2605_09490_b200 import kvtier as kt
+
+    W, K = args.warmup, args.steps
+    E = 0 if args.no_extras else min(K, 64)
+    w = H.workload(args.config, hbm_bp=args.hbm, evict_bp=args.evict, steps=W + K + E + 1)
+    dev = f"cuda:{local}"
+    peaks = _peaks()
+    seed_off = 1000 * rank
+
+    # ---- leg 1: tiered, differential staging, device-resident inputs -> value
+    run = H.TieredDecode(w, device=dev, out_fp32=False, split=args.split, seed_offset=seed_off)
+    run.capture()
+    for _ in range(W):
+        run.step()
+    n_events = sum(1 for t in range(W, W + K) if run.is_event(t))
+    _barrier_sync()
+    with ClockSampler(local) as clk:
+        el = timed(run.step, run.main, K)
+    _barrier_sync()
+    el_max = _max_over_ranks(el)
+    run.sync()
+    counts, _ = run.kv.census()
+    c = counts[0].tolist()
+    n_vis = run.kv.visible_count()
+    per_layer = attn_bytes_per_layer(w, c, n_vis)
+    L = w["L"]
+    step_bytes = L * per_layer   # + append + amortised classify/migrate (below)
+    B, Hkv, d = w["B"], w["Hkv"], w["d"]
+    n_now = run.kv.position()[0]
+    step_bytes += L * B * Hkv * 4 * d * 2                                  # append: row write + staging read
+    event_bytes = B * n_now * (4 * Hkv + 1 + 4) + 2 * L * B * Hkv * (c[0] + c[1]) * 4 * d   # classify + rebuild
+    step_bytes += event_bytes / w["interval"]
+    sps = world * K / el_max
+    ms = 1e3 * el_max / K
+    launches = K * (L + 2) + n_events * 4       # begin_step + L fused append/attention + end_step; 4 per event
+
+    # ---- e2e: same step through the public API with pinned host inputs/outputs
+    e2e = None
+    if E:
+        qh = run.Q[W + K:].cpu().pin_memory()
+        kh = run.Kn[W + K:].cpu().pin_memory()
+        vh = run.Vn[W + K:].cpu().pin_memory()
+        oh = torch.empty(run.O.shape, dtype=run.O.dtype).pin_memory()
+        j = [0]
+
+        def e2e_step():
+            i = j[0]
+            with torch.cuda.stream(run.main):
+                run.qbuf.copy_(qh[i], non_blocking=True)
+                run.kbuf.copy_(kh[i], non_blocking=True)
+                run.vbuf.copy_(vh[i], non_blocking=True)
+                run.kv.step_graph_launch(stream=run.main)
+                if run.is_event(run.t):
+                    run.kv.classify(stream=run.main)
+                    run.kv.migrate(stream=run.main, side=run.side)
+                oh.copy_(run.O, non_blocking=True)
+            run.t += 1
+            j[0] += 1
+
+        _barrier_sync()
+        el_e = _max_over_ranks(timed(e2e_step, run.main, E))
+        run.sync()
+        h2d = qh[0].numel() * 2 + kh[0].numel() * 2 + vh[0].numel() * 2
+        e2e = {"value": world * E / el_e, "unit": "steps/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(oh.numel() * oh.element_size()), "steps": E}
+    # ---- the attention kernel alone: one more decode step through the per-layer ABI,
+    #      CUDA events around every launch on its stream (no PDL overlap, cold start)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
+    t_last = W + K + E
+    with torch.cuda.stream(run.main):
+        run.qbuf.copy_(run.Q[t_last])
+        run.kbuf.copy_(run.Kn[t_last])
+        run.vbuf.copy_(run.Vn[t_last])
+        run.kv.begin_step(stream=run.main)
+        for l in range(L):
+            ev[l][0].record(run.main)
+            run.kv.decode_attention(l, run.qbuf[l], run.O[l], 1, stream=run.main, k_new=run.kbuf[l], v_new=run.vbuf[l])
+            ev[l][1].record(run.main)
+        run.kv.end_step(stream=run.main)
+    run.t += 1
+    run.main.synchronize()
+    durs = [a.elapsed_time(b) * 1e3 for a, b in ev]           # us
+    attn_us = statistics.mean(durs[1:]) if L > 1 else durs[0]
+    achieved = per_layer / (attn_us * 1e-6) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        if tj.get("config") == args.config and tj.get("hbm") == args.hbm and tj.get("evict") == args.evict:
+            traffic = tj.get("dram_bytes_per_launch")
+
+    run.close()
+    del run
+    torch.cuda.empty_cache()
+
+    # ---- control: same visible set, everything HBM-resident, no classify/migrate in window
+    overhead = None
+    control_ms = None
+    stream_leg = None
+    if not args.no_extras:
+        ctl = H.TieredDecode(dict(w, steps=W + K), device=dev, out_fp32=False, split=args.split, seed_offset=seed_off)
+        ctl.capture()
+        for _ in range(W):
+            ctl.step()
+        _barrier_sync()
+
+        def ctl_step():
+            with torch.cuda.stream(ctl.main):
+                ctl.qbuf.copy_(ctl.Q[ctl.t], non_blocking=True)
+                ctl.kbuf.copy_(ctl.Kn[ctl.t], non_blocking=True)
+                ctl.vbuf.copy_(ctl.Vn[ctl.t], non_blocking=True)
+                ctl.kv.step_graph_launch(stream=ctl.main)
+            ctl.t += 1
+        el_c = _max_over_ranks(timed(ctl_step, ctl.main, K))
+        control_ms = 1e3 * el_c / K
+        overhead = 100.0 * (1.0 - el_c / el_max)
+        ctl.close()
+        del ctl
+        torch.cuda.empty_cache()
+
+        # ---- stream mode (S = 0): T1 rows cross the host link every step (AMB-13)
+        Ks, Ws = 8, 2
+        ws = dict(w, staging=0, steps=Ws + Ks)
+        sr = H.TieredDecode(ws, device=dev, out_fp32=False, split=args.split, seed_offset=seed_off)
+        sr.capture()
+        for _ in range(Ws):
+            sr.step()
+        sr.sync()
+        cs = sr.kv.census()[0][0].tolist()
+        _barrier_sync()
+        el_s = _max_over_ranks(timed(sr.step, sr.main, Ks))
+        t1_bytes = L * B * Hkv * cs[1] * 4 * d
+        stream_leg = {"steps_per_s": world * Ks / el_s, "ms_per_step": 1e3 * el_s / Ks,
+                      "host_link_gbs": t1_bytes / (el_s / Ks) / 1e9, "t1_bytes_per_step": int(t1_bytes),
+                      "overhead_pct_vs_control": (100.0 * (1 - control_ms / (1e3 * el_s / Ks))) if control_ms else None,
+                      "note": "strict DDR residency: every T1 row re-read from pinned host memory per step "
+                              "(zero-copy gather, layer-ahead on a side stream); host-link bound by design"}
+        sr.close()
+        del sr
+        torch.cuda.empty_cache()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        cpu = cpu_oracle_sample(w, args.cpu_seconds)
+
+    if rank == 0:
+        hbm_gbs = step_bytes * (K / el_max) / 1e9
+        out = {
+            "metric": "tiered decode steps/sec (+ HBM GB/s vs roofline, T1 prefetch overhead %)",
+            "value": sps, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.config}-shaped (BASELINE.json configs[1]): B={B}/GPU L={L} "
+                                   f"Hq/Hkv={w['Hq']}/{Hkv} d={d} N={w['N']} beta={args.hbm}bp r={args.evict}bp "
+                                   f"Delta={w['interval']} differential staging",
+                       "global_batch": B * world, "parallelism": f"request-sharded x{world}",
+                       "l2": "no flush: per-step K/V traffic > 126 MB L2", "split": run_split(w, args)},
+            "hbm_gbs": hbm_gbs, "hbm_frac_of_measured_peak": hbm_gbs / peaks["hbm_gbs"],
+            "step_bytes": int(step_bytes), "census_b0": c, "n_visible": n_vis,
+            "prefetch_overhead_pct": overhead, "control_ms_per_step": control_ms,
+            "roofline": {"bound": "hbm", "kernel": "k_decode_attn", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                         "launch_us": attn_us, "algorithmic_bytes_per_launch": int(per_layer),
+                         "peak_src": peaks["src"]},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+            "stream_mode": stream_leg,
+            "context": "paper: 5-7% transfer overhead on RTX 5080 PCIe Gen5, unpinned, 7B int8, batch 1 (P:642)",
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_split(w, args):
+    if args.split:
+        return args.split
+    units = w["B"] * w["Hkv"]
+    return max(1, min(8, (2 * 148 + units - 1) // units))
+
+
+if __name__ == "__main__":
+    main()

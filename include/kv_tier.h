@@ -135,13 +135,17 @@ KV_TIER_API kv_tier_status kv_tier_append(kv_tier_ctx* ctx, int32_t layer, const
  * reads over the host link), layer-ahead.  decode_attention(layer) waits on it. */
 KV_TIER_API kv_tier_status kv_tier_prefetch(kv_tier_ctx* ctx, int32_t layer, void* side);
 
-/* a3 + a4: o[b][h] = sum_{i visible} softmax_i(q[b][h].k_i / sqrt d) v_i with
- * visible = T0 u T1 u T2 (T3 masked, Eq. 3; T2 rows dequantised,
- * AMB-12), and, if fuse_score_update, S_part[b][g][i] += sum_{h in g} p_{b,h,i}
- * from the exact, globally normalised probabilities (Eq. 1, AMB-1/14/15).
- * q: device bf16 [B][H_q][d]; o: device [B][H_q][d] fp32 (out_fp32) or bf16. */
-KV_TIER_API kv_tier_status kv_tier_decode_attention(kv_tier_ctx* ctx, int32_t layer, const void* q, void* o,
-                                        int32_t fuse_score_update, void* stream);
+/* a1 + a3 + a4: o[b][h] = sum_{i visible} softmax_i(q[b][h].k_i / sqrt d) v_i with
+ * visible = T0 u T1 u T2 (T3 masked, Eq. 3; T2 rows dequantised, AMB-12), and,
+ * if fuse_score_update, S_part[b][g][i] += sum_{h in g} p_{b,h,i} from the exact, globally
+ * normalised probabilities (Eq. 1, AMB-1/14/15).
+ * q: device bf16 [B][H_q][d]; o: device [B][H_q][d] fp32 (out_fp32) or bf16.
+ * k_new, v_new: device bf16 [B][H_kv][d] rows of the new token for this layer, appended
+ * to T0 inside the kernel (a1 fused); pass NULL for both if kv_tier_append already wrote
+ * them this step.  E_STATE if neither happened. */
+KV_TIER_API kv_tier_status kv_tier_decode_attention(kv_tier_ctx* ctx, int32_t layer, const void* q,
+                                                    const void* k_new, const void* v_new, void* o,
+                                                    int32_t fuse_score_update, void* stream);
 
 /* a4 standalone (external probabilities, e.g. from another attention kernel):
  * probs: device fp32 [B][H_q][n_vis] over the visible tokens in ascending position

@@ -1,22 +1,24 @@
-// a3 + a4: GQA decode attention over the visible tiers with the fused cumulative
-// score update (Eq. 1, Eq. 3, Prop. 1).
+// a1 + a3 + a4: fused new-token append, GQA decode attention over the visible tiers, and the
+// cumulative score update (Eq. 1, Eq. 3, Prop. 1).
 //
-// One thread-block cluster of C CTAs per (request b, kv head g); CTA r of the cluster
-// owns a contiguous chunk of the visible tokens [T0 rows | T1 staging rows | T2 rows].
+// One thread-block cluster of C CTAs per (request b, kv head g).  The visible rows of the
+// unit are ordered [T0 rows except the new token | T1 staging | T2 int8 | new token]; CTA r
+// of the cluster owns a contiguous 1/C chunk.
 //
-//   phase A  K tiles (cp.async 4-stage ring, XOR-swizzled SMEM) -> S^T = K q^T on the
-//            tensor cores (mma.sync m16n8k16 bf16, swap-AB: tokens = M, heads = N = 8);
-//            logits (log2 domain) kept in SMEM for the whole chunk, running max.
-//   phase B  V tiles -> p = exp2(z - m_local) -> o^T += V^T p^T on the tensor cores
-//            (P moved C-fragment -> B-fragment with movmatrix.trans).
-//   merge    (m, l, o) of the C CTAs exchanged through distributed shared memory
-//            (no HBM round trip); each CTA writes a 1/C slice of o.
-//   score    exact globally-normalised p_i = exp2(z_i - M)/L re-derived from the SMEM
-//            logits; S_part[b][g][pos_i] += sum_{h in g} p_{h,i}  (one fp32 add per
-//            layer, AMB-14).  Every (b, g, pos) is owned by exactly one CTA: no atomics.
+//   prologue  (before griddepcontrol.wait, overlaps the previous layer's kernel under PDL)
+//            counters, positions of the chunk -> SMEM, first K tiles in flight
+//   phase A  K tiles (cp.async ring, XOR-swizzled SMEM) -> S^T = K q^T on the tensor cores
+//            (mma.sync m16n8k16 bf16, swap-AB: tokens = M, heads = N = 8); logits (log2
+//            domain) stay in SMEM for the whole chunk; running max per head
+//   phase B  V tiles -> p = exp2(z - m_local) -> o^T += V^T p^T (movmatrix.trans turns the
+//            C fragment into the B fragment; ldmatrix.trans reads V^T)
+//   merge    (m, l, o) of the C CTAs through distributed shared memory; CTA r writes 1/C of o
+//   score    exact p_i = exp2(z_i - M)/L from the SMEM logits; S_part[b][g][pos_i] += sum over
+//            the group's heads (one fp32 add per layer, AMB-14); each (b,g,pos) belongs to one
+//            CTA -> no atomics, bit-reproducible
 //
-// HBM traffic per launch = the algorithmic bytes: every visible K/V row once,
-// q, o, and 8 B of score RMW per visible token per kv head.
+// HBM traffic per launch = algorithmic bytes: every visible K/V row once, q, o, the new row
+// (read + written), and 8 B of score read+write per visible token per kv head.
 #include "kv_internal.cuh"
 #include <cooperative_groups.h>
 
@@ -26,7 +28,7 @@ namespace kvt {
 
 constexpr int ATT_THREADS = 128;   // 4 warps, 16 tokens each per tile
 constexpr int TILE = 64;           // tokens per pipeline stage
-constexpr int NST = 4;             // pipeline depth
+constexpr int NST = 3;             // pipeline depth (3 x 16 KB at d = 128 -> 3 CTAs / SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -37,6 +39,8 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int nb
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3, uint32_t addr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -66,24 +70,20 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 __device__ __forceinline__ uint32_t i8pair_to_bf16x2(uint32_t word, int k) {
-  // bytes 2k, 2k+1 of `word` (signed) -> bf16x2 (exact: |code| <= 127)
-  const float lo = (float)(int8_t)((word >> (16 * k)) & 0xFF);
+  const float lo = (float)(int8_t)((word >> (16 * k)) & 0xFF);   // exact: |code| <= 127
   const float hi = (float)(int8_t)((word >> (16 * k + 8)) & 0xFF);
   return pack_bf16(lo, hi);
 }
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
 template <int D>
-struct AttnSmem {
-  static constexpr int ROWB = D * 2;
-  static constexpr int TILEB = TILE * ROWB;
-};
-
-template <int D>
-__global__ void __launch_bounds__(ATT_THREADS, 2)
+__global__ void __launch_bounds__(ATT_THREADS, 3)
     k_decode_attn(const DevView v, const int layer, const __nv_bfloat16* __restrict__ q,
+                  const __nv_bfloat16* __restrict__ knew, const __nv_bfloat16* __restrict__ vnew,
                   void* __restrict__ o, const int fuse) {
-  constexpr int ROWB = AttnSmem<D>::ROWB;
-  constexpr int TILEB = AttnSmem<D>::TILEB;
+  constexpr int ROWB = D * 2;
+  constexpr int TILEB = TILE * ROWB;
   constexpr int KS = D / 16;
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();
@@ -96,23 +96,28 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
 
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;
-  float* zs = reinterpret_cast<float*>(smem + NST * TILEB);   // [chunk_max][8]
-  float* xo = zs + (size_t)v.chunk_max * 8;                   // [8][D]   exchange: o partial
-  float* xm = xo + 8 * D;                                      // [8]      exchange: max (log2)
-  float* xl = xm + 8;                                          // [8]      exchange: sum
+  float* zs = reinterpret_cast<float*>(smem + NST * TILEB);   // [chunk_max][8] logits (log2)
+  int* spos = reinterpret_cast<int*>(zs + (size_t)v.chunk_max * 8);   // [chunk_max] positions
+  float* xo = reinterpret_cast<float*>(spos + v.chunk_max);    // [8][D]  exchange: o partial
+  float* xm = xo + 8 * D;                                      // [8]     exchange: max (log2)
+  float* xl = xm + 8;                                          // [8]     exchange: sum
   float* red = xl + 8;                                         // [2][4][8] warp max / warp l
   float* sML = red + 64;                                       // [16] merged M, 1/L
-  float* t2sc = sML + 16;                                      // [TILE] T2 row scales
-  unsigned char* t2buf = reinterpret_cast<unsigned char*>(t2sc + TILE);   // [TILE][D] bf16 (T2 only)
+  float* nrow = sML + 16;                                      // [2][D] new token K, V (fp32)
+  float* t2sc = nrow + 2 * D;                                  // [TILE] T2 row scales
+  unsigned char* t2buf = reinterpret_cast<unsigned char*>(t2sc + TILE);   // [TILE][D] bf16
 
+  // ---------------------------------------------------------------- prologue (pre-PDL-wait)
   const int cur = v.st->cur;
   const int* cn = v.cnt[cur] + b * CNT_STRIDE;
   const int n0 = cn[0], n1 = cn[1], n2 = cn[2];
-  const int n01 = n0 + n1, nvis = n01 + n2;
+  const int n0o = n0 - 1;                           // T0 rows before the new token
+  const int n01 = n0o + n1, n012 = n01 + n2, nvis = n012 + 1;
   const int chunk = (nvis + C - 1) / C;
   const int vbeg = min(r * chunk, nvis), vend = min(vbeg + chunk, nvis);
   const int aend = min(vend, n01);                  // bf16 segment [vbeg, aend)
-  const int t2beg = max(vbeg, n01);                 // int8 segment [t2beg, vend)
+  const int t2beg = max(vbeg, n01), t2end = min(vend, n012);   // int8 segment
+  const bool has_new = vend == nvis && nvis > vbeg; // this CTA owns the new token
   const int nb = max(0, aend - vbeg);
   const int nt = (nb + TILE - 1) / TILE;
 
@@ -130,7 +135,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
     V1 = v.v1[cur] + grp * v.cap1 * D;
   }
 
-  // ---- stage the first tiles while q is loaded
   auto load_tile = [&](int i) {
     const bool isV = i >= nt;
     const int tv0 = vbeg + (isV ? i - nt : i) * TILE;
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
       int nbytes = 0;
       if (tok < aend) {
         nbytes = 16;
-        src = tok < n0 ? S0 + (size_t)tok * D : S1 + (size_t)(tok - n0) * D;
+        src = tok < n0o ? S0 + (size_t)tok * D : S1 + (size_t)(tok - n0o) * D;
       }
       cp_async16(sbase + row * ROWB + ((c ^ (row & 7)) << 4), src + c * 8, nbytes);
     }
@@ -159,6 +163,19 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
     if (s < total) load_tile(s);
     cp_commit();
   }
+  // positions of the chunk's tokens (for the score update)
+  if (fuse) {
+    const int* I0 = v.idx[cur][0] + (size_t)b * v.cap0;
+    const int* I1 = v.idx[cur][1] + (size_t)b * v.cap1;
+    const int* I2 = v.idx[cur][2] + (size_t)b * v.cap2;
+    for (int j = tid; j < vend - vbeg; j += ATT_THREADS) {
+      const int tok = vbeg + j;
+      spos[j] = tok < n0o ? I0[tok] : tok < n01 ? I1[tok - n0o] : tok < n012 ? I2[tok - n01] : I0[n0o];
+    }
+  }
+  pdl_trigger();
+  // ---------------------------------------------------------------- dependent inputs
+  pdl_wait();
 
   uint32_t qf[KS][2];
   {
@@ -176,13 +193,27 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
   }
   const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));   // log2(e)/sqrt(d)
 
+  // new token (a1): append its K/V row to T0 row n0-1 and keep it in SMEM (fp32)
+  if (has_new) {
+    uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[cur]) + (grp * v.cap0 + n0o) * D;
+    uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[cur]) + (grp * v.cap0 + n0o) * D;
+    const uint16_t* ks_ = knew ? reinterpret_cast<const uint16_t*>(knew) + ((size_t)b * v.Hkv + g) * D : K0w;
+    const uint16_t* vs_ = vnew ? reinterpret_cast<const uint16_t*>(vnew) + ((size_t)b * v.Hkv + g) * D : V0w;
+    for (int e = tid; e < D; e += ATT_THREADS) {
+      const uint16_t kb = ks_[e], vb = vs_[e];
+      nrow[e] = bf16_bits_to_f(kb);
+      nrow[D + e] = bf16_bits_to_f(vb);
+      if (knew) K0w[e] = kb;
+      if (vnew) V0w[e] = vb;
+    }
+  }
+
   float mx0 = -INFINITY, mx1 = -INFINITY;    // running max, heads 2tq, 2tq+1
   float l0 = 0.f, l1 = 0.f;
   float oacc[KS][4];
 #pragma unroll
   for (int mt = 0; mt < KS; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
 
-  // QK^T for one warp's 16 tokens of a tile staged at sbase; row scale `rs` (T2) or 1
   auto qk_warp = [&](uint32_t sbase, int tv0, int tend, const float* rsc) {
     if (tv0 + w * 16 >= tend) return;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -246,7 +277,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
       mma16816(oacc[mt], a0, a1, a2, a3, b0, b1);
     }
   };
-  // int8 T2 rows: codes -> bf16 (exact) into the swizzled t2buf, scales -> t2sc
   auto stage_t2 = [&](int tv0, bool isV) {
     const int8_t* C2 = (isV ? v.c2v[cur] : v.c2k[cur]) + grp * v.cap2 * D;
     const float* S2 = (isV ? v.s2v[cur] : v.s2k[cur]) + grp * v.cap2;
@@ -254,7 +284,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
       const int row = e / (D / 16), j = e % (D / 16);
       const int tok = tv0 + row;
       uint4 cw = make_uint4(0u, 0u, 0u, 0u);
-      if (tok < vend) cw = *reinterpret_cast<const uint4*>(C2 + (size_t)(tok - n01) * D + 16 * j);
+      if (tok < t2end) cw = *reinterpret_cast<const uint4*>(C2 + (size_t)(tok - n01) * D + 16 * j);
       uint4 lo, hi;
       lo.x = i8pair_to_bf16x2(cw.x, 0); lo.y = i8pair_to_bf16x2(cw.x, 1);
       lo.z = i8pair_to_bf16x2(cw.y, 0); lo.w = i8pair_to_bf16x2(cw.y, 1);
@@ -265,26 +295,32 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
     }
     for (int row = tid; row < TILE; row += ATT_THREADS) {
       const int tok = tv0 + row;
-      t2sc[row] = tok < vend ? S2[tok - n01] : 0.f;
+      t2sc[row] = tok < t2end ? S2[tok - n01] : 0.f;
     }
   };
 
   // ---- phase A on T2 rows (rare; synchronous)
-  for (int tv0 = t2beg; tv0 < vend; tv0 += TILE) {
+  for (int tv0 = t2beg; tv0 < t2end; tv0 += TILE) {
+    __syncthreads();
     stage_t2(tv0, false);
     __syncthreads();
-    qk_warp(smem_u32(t2buf), tv0, vend, t2sc);
-    __syncthreads();
+    qk_warp(smem_u32(t2buf), tv0, t2end, t2sc);
+  }
+  // ---- phase A on the new token (CUDA cores, fp32): warp 0 computes all G logits
+  __syncthreads();   // nrow visible
+  if (has_new && w == 0) {
+    float part = 0.f;   // head gq, dims of this lane's q fragments
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int d0 = ks * 16 + 2 * tq;
+      part += bf16lo(qf[ks][0]) * nrow[d0] + bf16hi(qf[ks][0]) * nrow[d0 + 1];
+      part += bf16lo(qf[ks][1]) * nrow[d0 + 8] + bf16hi(qf[ks][1]) * nrow[d0 + 9];
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    if (tq == 0) zs[(nvis - 1 - vbeg) * 8 + gq] = part * sl2;
   }
 
-  auto reduce_max = [&]() {   // all threads: CTA max of the two heads this lane owns
-    m2a = fmaxf(fmaxf(red[0 * 8 + 2 * tq], red[1 * 8 + 2 * tq]), fmaxf(red[2 * 8 + 2 * tq], red[3 * 8 + 2 * tq]));
-    m2b = fmaxf(fmaxf(red[0 * 8 + 2 * tq + 1], red[1 * 8 + 2 * tq + 1]),
-                fmaxf(red[2 * 8 + 2 * tq + 1], red[3 * 8 + 2 * tq + 1]));
-    if (tid < 8) xm[tid] = fmaxf(fmaxf(red[tid], red[8 + tid]), fmaxf(red[16 + tid], red[24 + tid]));
-    if (m2a == -INFINITY) m2a = 0.f;
-    if (m2b == -INFINITY) m2b = 0.f;
-  };
   auto write_warp_max = [&]() {
     float a = mx0, c = mx1;
 #pragma unroll
@@ -296,6 +332,22 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
       red[w * 8 + 2 * lane] = a;
       red[w * 8 + 2 * lane + 1] = c;
     }
+  };
+  auto reduce_max = [&]() {   // after a barrier: CTA max incl. the new token
+    float nz0 = -INFINITY, nz1 = -INFINITY;
+    if (has_new) {
+      nz0 = zs[(nvis - 1 - vbeg) * 8 + 2 * tq];
+      nz1 = zs[(nvis - 1 - vbeg) * 8 + 2 * tq + 1];
+    }
+    m2a = fmaxf(fmaxf(fmaxf(red[2 * tq], red[8 + 2 * tq]), fmaxf(red[16 + 2 * tq], red[24 + 2 * tq])), nz0);
+    m2b = fmaxf(fmaxf(fmaxf(red[2 * tq + 1], red[9 + 2 * tq]), fmaxf(red[17 + 2 * tq], red[25 + 2 * tq])), nz1);
+    if (tid < 8) {
+      float m = fmaxf(fmaxf(red[tid], red[8 + tid]), fmaxf(red[16 + tid], red[24 + tid]));
+      if (has_new) m = fmaxf(m, zs[(nvis - 1 - vbeg) * 8 + tid]);
+      xm[tid] = m;
+    }
+    if (m2a == -INFINITY) m2a = 0.f;
+    if (m2b == -INFINITY) m2b = 0.f;
   };
 
   // ---- phases A (K tiles) and B (V tiles) through the cp.async ring
@@ -319,13 +371,26 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
     __syncthreads();
     reduce_max();
   }
-
   // ---- phase B on T2 rows
-  for (int tv0 = t2beg; tv0 < vend; tv0 += TILE) {
+  for (int tv0 = t2beg; tv0 < t2end; tv0 += TILE) {
     __syncthreads();
     stage_t2(tv0, true);
     __syncthreads();
-    pv_warp(smem_u32(t2buf), tv0, vend, t2sc);
+    pv_warp(smem_u32(t2buf), tv0, t2end, t2sc);
+  }
+  // ---- phase B on the new token: rank-1 update of this thread's o^T fragments
+  if (has_new && w == 0) {
+    const float* zr = zs + (nvis - 1 - vbeg) * 8;
+    const float pa = exp2f(zr[2 * tq] - m2a), pb = exp2f(zr[2 * tq + 1] - m2b);
+    if (gq == 0) { l0 += pa; l1 += pb; }          // counted once per head (lanes 0..3)
+#pragma unroll
+    for (int mt = 0; mt < KS; ++mt) {
+      const float va = nrow[D + mt * 16 + gq], vb = nrow[D + mt * 16 + gq + 8];
+      oacc[mt][0] += pa * va;
+      oacc[mt][1] += pb * va;
+      oacc[mt][2] += pa * vb;
+      oacc[mt][3] += pb * vb;
+    }
   }
 
   // ---- CTA reduction of l and o (ring reused as [4 warps][8 heads][D] fp32)
@@ -385,31 +450,29 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
       else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(val);
     }
   }
+  // done reading peers' shared memory: arrive now, wait before exit (score work overlaps)
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   if (fuse) {
-    const int* I0 = v.idx[cur][0] + (size_t)b * v.cap0;
-    const int* I1 = v.idx[cur][1] + (size_t)b * v.cap1;
-    const int* I2 = v.idx[cur][2] + (size_t)b * v.cap2;
     float* Sg = v.S + ((size_t)b * v.Hkv + g) * v.Nmax;
     bool bad = false;
     for (int j = tid; j < vend - vbeg; j += ATT_THREADS) {
-      const int tok = vbeg + j;
       const float* zr = zs + j * 8;
       float inc = 0.f;
       for (int h = 0; h < G; ++h) inc += exp2f(zr[h] - sML[h]) * sML[8 + h];
-      const int pos = tok < n0 ? I0[tok] : (tok < n01 ? I1[tok - n0] : I2[tok - n01]);
+      const int pos = spos[j];
       Sg[pos] = Sg[pos] + inc;
       bad |= !isfinite(inc);
     }
     if (bad) atomicOr(&v.st->err, 1);
   }
-  cluster.sync();   // keep this CTA's shared memory alive until every peer has read it
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
 size_t attn_smem_bytes(const DevView& v) {
   const size_t ringb = (size_t)NST * TILE * v.D * 2;
-  const size_t zsb = (size_t)v.chunk_max * 8 * 4;
+  const size_t zsb = (size_t)v.chunk_max * 8 * 4 + (size_t)v.chunk_max * 4;
   const size_t xob = (size_t)8 * v.D * 4;
-  const size_t misc = (size_t)(8 + 8 + 64 + 16 + TILE) * 4;
+  const size_t misc = (size_t)(8 + 8 + 64 + 16 + 2 * v.D + TILE) * 4;
   const size_t t2 = (v.cap2 > 0) ? (size_t)TILE * v.D * 2 : 0;
   return ringb + zsb + xob + misc + t2;
 }
@@ -427,22 +490,27 @@ cudaError_t attn_configure(const DevView& v) {
   return v.D == 128 ? configure_d<128>(v) : configure_d<64>(v);
 }
 
-cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, void* o, int fuse, cudaStream_t s) {
+cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
+                               void* o, int fuse, int pdl, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(v.split, v.B * v.Hkv, 1);
   cfg.blockDim = dim3(ATT_THREADS, 1, 1);
   cfg.dynamicSmemBytes = attn_smem_bytes(v);
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = v.split;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   const __nv_bfloat16* qq = reinterpret_cast<const __nv_bfloat16*>(q);
-  if (v.D == 128) return cudaLaunchKernelEx(&cfg, k_decode_attn<128>, v, layer, qq, o, fuse);
-  return cudaLaunchKernelEx(&cfg, k_decode_attn<64>, v, layer, qq, o, fuse);
+  const __nv_bfloat16* kk = reinterpret_cast<const __nv_bfloat16*>(knew);
+  const __nv_bfloat16* vv = reinterpret_cast<const __nv_bfloat16*>(vnew);
+  if (v.D == 128) return cudaLaunchKernelEx(&cfg, k_decode_attn<128>, v, layer, qq, kk, vv, o, fuse);
+  return cudaLaunchKernelEx(&cfg, k_decode_attn<64>, v, layer, qq, kk, vv, o, fuse);
 }
 
 }  // namespace kvt

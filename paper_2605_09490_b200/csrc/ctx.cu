@@ -29,6 +29,7 @@ struct kv_tier_ctx {
   cudaEvent_t ev_slot_free[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_prefetched;
   std::vector<int> prefetched_step;
+  std::vector<int> appended_step;          // step in which layer l's new row was written
   bool offload_pending = false;
   bool capturing = false;
   bool slot_recorded[2] = {false, false};   // ev_slot_free[x] recorded within the open step
@@ -272,6 +273,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   }
   ctx->loaded_layers.assign(v.L, 0);
   ctx->prefetched_step.assign(v.L, -1);
+  ctx->appended_step.assign(v.L, -1);
   *out = ctx;
   return KV_TIER_OK;
 }
@@ -345,7 +347,9 @@ kv_tier_status kv_tier_append(kv_tier_ctx* ctx, int32_t layer, const void* k_new
   if (!ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "append outside begin_step/end_step");
   if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
   if (!k_new || !v_new) return fail(ctx, KV_TIER_E_INVAL, "null k/v");
-  return cuda_check(ctx, launch_append(ctx->v, layer, k_new, v_new, reinterpret_cast<cudaStream_t>(stream)), "append");
+  kv_tier_status st = cuda_check(ctx, launch_append(ctx->v, layer, k_new, v_new, reinterpret_cast<cudaStream_t>(stream)), "append");
+  if (!st) ctx->appended_step[layer] = ctx->t;
+  return st;
 }
 
 kv_tier_status kv_tier_prefetch(kv_tier_ctx* ctx, int32_t layer, void* side) {
@@ -366,24 +370,34 @@ kv_tier_status kv_tier_prefetch(kv_tier_ctx* ctx, int32_t layer, void* side) {
   return cuda_check(ctx, e, "prefetch");
 }
 
-kv_tier_status kv_tier_decode_attention(kv_tier_ctx* ctx, int32_t layer, const void* q, void* o,
-                                        int32_t fuse_score_update, void* stream) {
+static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, const void* q, const void* k_new,
+                                            const void* v_new, void* o, int32_t fuse_score_update, void* stream,
+                                            int pdl) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
   if (!q || !o) return fail(ctx, KV_TIER_E_INVAL, "null q/o");
+  if ((k_new == nullptr) != (v_new == nullptr)) return fail(ctx, KV_TIER_E_INVAL, "k_new and v_new go together");
   if (((uintptr_t)q & 15) || ((uintptr_t)o & 15)) return fail(ctx, KV_TIER_E_INVAL, "q/o must be 16-B aligned");
-  if (!ctx->loaded) return fail(ctx, KV_TIER_E_STATE, "no prefix loaded");
-  if (ctx->v.stream_mode && (!ctx->step_open || ctx->prefetched_step[layer] != ctx->t))
+  if (!ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "decode_attention outside begin_step/end_step");
+  if (!k_new && ctx->appended_step[layer] != ctx->t)
+    return fail(ctx, KV_TIER_E_STATE, "layer %d: no new-token row (pass k_new/v_new or call kv_tier_append)", layer);
+  if (ctx->v.stream_mode && ctx->prefetched_step[layer] != ctx->t)
     return fail(ctx, KV_TIER_E_STATE, "stream mode: kv_tier_prefetch(layer %d) must precede decode_attention in every step", layer);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
   if (ctx->v.stream_mode) e = cudaStreamWaitEvent(s, ctx->ev_prefetched[layer], 0);
-  if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, o, fuse_score_update, s);
+  if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, fuse_score_update, pdl, s);
   if (e == cudaSuccess && ctx->v.stream_mode) {
     e = cudaEventRecord(ctx->ev_slot_free[layer & 1], s);
     ctx->slot_recorded[layer & 1] = true;
   }
+  if (e == cudaSuccess && k_new) ctx->appended_step[layer] = ctx->t;
   return cuda_check(ctx, e, "decode_attention");
+}
+
+kv_tier_status kv_tier_decode_attention(kv_tier_ctx* ctx, int32_t layer, const void* q, const void* k_new,
+                                        const void* v_new, void* o, int32_t fuse_score_update, void* stream) {
+  return decode_attention_impl(ctx, layer, q, k_new, v_new, o, fuse_score_update, stream, 0);
 }
 
 kv_tier_status kv_tier_visible_count(const kv_tier_ctx* ctx, int32_t* n_vis) {
@@ -473,9 +487,11 @@ kv_tier_status kv_tier_step(kv_tier_ctx* ctx, const void* q, const void* k_new, 
   if (st) return st;
   if (v.stream_mode)
     for (int l = 0; l < std::min(2, v.L) && !st; ++l) st = kv_tier_prefetch(ctx, l, side);
+  // a1 fused into the attention kernel; consecutive layers chained with programmatic
+  // dependent launch (each kernel's prologue overlaps the previous layer's tail)
   for (int l = 0; l < v.L && !st; ++l) {
-    st = kv_tier_append(ctx, l, kb + l * ks * 2, vb + l * ks * 2, stream);
-    if (!st) st = kv_tier_decode_attention(ctx, l, qb + l * qs * 2, ob + l * os, fuse_score_update, stream);
+    st = decode_attention_impl(ctx, l, qb + l * qs * 2, kb + l * ks * 2, vb + l * ks * 2, ob + l * os,
+                               fuse_score_update, stream, l > 0 && !v.stream_mode);
     if (!st && v.stream_mode && l + 2 < v.L) st = kv_tier_prefetch(ctx, l + 2, side);
   }
   if (st) return st;
@@ -495,6 +511,7 @@ kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const
   const int n = ctx->n, t = ctx->t, c0 = ctx->c[0];
   const bool classified = ctx->classified;
   const std::vector<int> pstep = ctx->prefetched_step;
+  const std::vector<int> astep = ctx->appended_step;
   cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return cuda_check(ctx, e, "begin capture");
   ctx->capturing = true;
@@ -504,6 +521,7 @@ kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const
   e = cudaStreamEndCapture(s, &g);
   ctx->n = n; ctx->t = t; ctx->c[0] = c0; ctx->classified = classified; ctx->step_open = false;
   ctx->prefetched_step = pstep;
+  ctx->appended_step = astep;
   if (st) { if (g) cudaGraphDestroy(g); return st; }
   if (e != cudaSuccess) return cuda_check(ctx, e, "end capture");
   e = cudaGraphInstantiate(&ctx->graph_exec, g, 0);

@@ -66,7 +66,8 @@ cudaError_t launch_begin_step(const DevView& v, cudaStream_t s);
 cudaError_t launch_append(const DevView& v, int layer, const void* k, const void* vv, cudaStream_t s);
 cudaError_t launch_load_prefix(const DevView& v, int layer, const void* k, const void* vv, int n0, cudaStream_t s);
 cudaError_t launch_init_meta(const DevView& v, int n0, cudaStream_t s);
-cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, void* o, int fuse, cudaStream_t s);
+cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
+                               void* o, int fuse, int pdl, cudaStream_t s);
 cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s);
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);
 cudaError_t launch_classify(const DevView& v, cudaStream_t s);

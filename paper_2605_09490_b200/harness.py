@@ -79,8 +79,14 @@ class TieredDecode:
     def is_event(self, t):
         return t % self.w["interval"] == 0
 
+    def output(self):
+        """Host copy of the last step's o [L][B][Hq][d] (waits for the main stream)."""
+        self.main.synchronize()
+        return self.O.cpu().numpy()
+
     def step(self):
-        """One decode step t (+ manage event when t mod Delta == 0)."""
+        """One decode step t (+ manage event when t mod Delta == 0).  Asynchronous on
+        self.main: read results through output()."""
         t = self.t
         with torch.cuda.stream(self.main):
             if self.graph:

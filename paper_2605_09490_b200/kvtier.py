@@ -57,7 +57,8 @@ _SIGS = {
     "kv_tier_begin_step": [C.c_void_p, C.c_void_p],
     "kv_tier_append": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p],
     "kv_tier_prefetch": [C.c_void_p, C.c_int32, C.c_void_p],
-    "kv_tier_decode_attention": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p],
+    "kv_tier_decode_attention": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_int32, C.c_void_p],
     "kv_tier_score_update": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p],
     "kv_tier_visible_count": [C.c_void_p, C.POINTER(C.c_int32)],
     "kv_tier_end_step": [C.c_void_p, C.c_void_p],
@@ -169,9 +170,13 @@ class KvTier:
     def prefetch(self, layer, side=None):
         _check(load().kv_tier_prefetch(self.ctx, layer, _stream_ptr(side)), self.ctx)
 
-    def decode_attention(self, layer, q, o, fuse_score_update=1, stream=None):
-        _check(load().kv_tier_decode_attention(self.ctx, layer, C.c_void_p(q.data_ptr()), C.c_void_p(o.data_ptr()),
-                                               fuse_score_update, _stream_ptr(stream)), self.ctx)
+    def decode_attention(self, layer, q, o, fuse_score_update=1, stream=None, k_new=None, v_new=None):
+        """k_new/v_new: fused append of the new token's row (None: kv_tier_append was called)."""
+        kp = C.c_void_p(k_new.data_ptr()) if k_new is not None else None
+        vp = C.c_void_p(v_new.data_ptr()) if v_new is not None else None
+        _check(load().kv_tier_decode_attention(self.ctx, layer, C.c_void_p(q.data_ptr()), kp, vp,
+                                               C.c_void_p(o.data_ptr()), fuse_score_update, _stream_ptr(stream)),
+               self.ctx)
 
     def score_update(self, layer, probs, stream=None):
         _check(load().kv_tier_score_update(self.ctx, layer, C.c_void_p(probs.data_ptr()), _stream_ptr(stream)),
