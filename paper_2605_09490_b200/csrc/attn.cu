@@ -26,9 +26,7 @@ namespace cg = cooperative_groups;
 
 namespace kvt {
 
-constexpr int ATT_THREADS = 128;   // 4 warps, 16 tokens each per tile
-constexpr int TILE = 64;           // tokens per pipeline stage
-constexpr int NST = 3;             // pipeline depth (3 x 16 KB at d = 128 -> 3 CTAs / SM)
+// Variants (warps per CTA NW, pipeline stages NST): a tile is 16 tokens per warp.
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -77,11 +75,13 @@ __device__ __forceinline__ uint32_t i8pair_to_bf16x2(uint32_t word, int k) {
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
-template <int D>
-__global__ void __launch_bounds__(ATT_THREADS, 3)
+template <int D, int NW, int NST>
+__global__ void __launch_bounds__(NW * 32, (NW == 4 ? 3 : 2))
     k_decode_attn(const DevView v, const int layer, const __nv_bfloat16* __restrict__ q,
                   const __nv_bfloat16* __restrict__ knew, const __nv_bfloat16* __restrict__ vnew,
                   void* __restrict__ o, const int fuse) {
+  constexpr int ATT_THREADS = NW * 32;
+  constexpr int TILE = NW * 16;
   constexpr int ROWB = D * 2;
   constexpr int TILEB = TILE * ROWB;
   constexpr int KS = D / 16;
@@ -101,8 +101,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 3)
   float* xo = reinterpret_cast<float*>(spos + v.chunk_max);    // [8][D]  exchange: o partial
   float* xm = xo + 8 * D;                                      // [8]     exchange: max (log2)
   float* xl = xm + 8;                                          // [8]     exchange: sum
-  float* red = xl + 8;                                         // [2][4][8] warp max / warp l
-  float* sML = red + 64;                                       // [16] merged M, 1/L
+  float* red = xl + 8;                                         // [2][NW][8] warp max / warp l
+  float* sML = red + 16 * NW;                                  // [16] merged M, 1/L
   float* nrow = sML + 16;                                      // [2][D] new token K, V (fp32)
   float* t2sc = nrow + 2 * D;                                  // [TILE] T2 row scales
   unsigned char* t2buf = reinterpret_cast<unsigned char*>(t2sc + TILE);   // [TILE][D] bf16
@@ -339,11 +339,17 @@ __global__ void __launch_bounds__(ATT_THREADS, 3)
       nz0 = zs[(nvis - 1 - vbeg) * 8 + 2 * tq];
       nz1 = zs[(nvis - 1 - vbeg) * 8 + 2 * tq + 1];
     }
-    m2a = fmaxf(fmaxf(fmaxf(red[2 * tq], red[8 + 2 * tq]), fmaxf(red[16 + 2 * tq], red[24 + 2 * tq])), nz0);
-    m2b = fmaxf(fmaxf(fmaxf(red[2 * tq + 1], red[9 + 2 * tq]), fmaxf(red[17 + 2 * tq], red[25 + 2 * tq])), nz1);
+    m2a = nz0;
+    m2b = nz1;
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) {
+      m2a = fmaxf(m2a, red[ww * 8 + 2 * tq]);
+      m2b = fmaxf(m2b, red[ww * 8 + 2 * tq + 1]);
+    }
     if (tid < 8) {
-      float m = fmaxf(fmaxf(red[tid], red[8 + tid]), fmaxf(red[16 + tid], red[24 + tid]));
-      if (has_new) m = fmaxf(m, zs[(nvis - 1 - vbeg) * 8 + tid]);
+      float m = has_new ? zs[(nvis - 1 - vbeg) * 8 + tid] : -INFINITY;
+#pragma unroll
+      for (int ww = 0; ww < NW; ++ww) m = fmaxf(m, red[ww * 8 + tid]);
       xm[tid] = m;
     }
     if (m2a == -INFINITY) m2a = 0.f;
@@ -393,7 +399,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 3)
     }
   }
 
-  // ---- CTA reduction of l and o (ring reused as [4 warps][8 heads][D] fp32)
+  // ---- CTA reduction of l and o (ring reused as [NW warps][8 heads][D] fp32)
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
     l0 += __shfl_xor_sync(0xffffffffu, l0, off);
@@ -402,8 +408,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 3)
   __syncthreads();
   float* ow = reinterpret_cast<float*>(ring);
   if (lane < 4) {
-    red[32 + w * 8 + 2 * lane] = l0;
-    red[32 + w * 8 + 2 * lane + 1] = l1;
+    red[8 * NW + w * 8 + 2 * lane] = l0;
+    red[8 * NW + w * 8 + 2 * lane + 1] = l1;
   }
 #pragma unroll
   for (int mt = 0; mt < KS; ++mt) {
@@ -415,9 +421,18 @@ __global__ void __launch_bounds__(ATT_THREADS, 3)
     o1[8] = oacc[mt][3];
   }
   __syncthreads();
-  for (int e = tid; e < 8 * D; e += ATT_THREADS)
-    xo[e] = (ow[e] + ow[8 * D + e]) + (ow[16 * D + e] + ow[24 * D + e]);
-  if (tid < 8) xl[tid] = (red[32 + tid] + red[40 + tid]) + (red[48 + tid] + red[56 + tid]);
+  for (int e = tid; e < 8 * D; e += ATT_THREADS) {
+    float a = ow[e];
+#pragma unroll
+    for (int ww = 1; ww < NW; ++ww) a += ow[ww * 8 * D + e];
+    xo[e] = a;
+  }
+  if (tid < 8) {
+    float a = red[8 * NW + tid];
+#pragma unroll
+    for (int ww = 1; ww < NW; ++ww) a += red[8 * NW + ww * 8 + tid];
+    xl[tid] = a;
+  }
 
   // ---- cluster merge through distributed shared memory
   cluster.sync();
@@ -468,33 +483,58 @@ __global__ void __launch_bounds__(ATT_THREADS, 3)
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+// (warps, stages) variants; DevView::variant selects one (0 = default)
+struct Variant { int nw, nst; };
+static constexpr Variant kVariants[] = {{4, 3}, {4, 4}, {8, 3}, {8, 4}, {4, 6}, {8, 6}};
+constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+
 size_t attn_smem_bytes(const DevView& v) {
-  const size_t ringb = (size_t)NST * TILE * v.D * 2;
+  const Variant vr = kVariants[v.variant];
+  const int tile = 16 * vr.nw;
+  const size_t ringb = (size_t)vr.nst * tile * v.D * 2;
   const size_t zsb = (size_t)v.chunk_max * 8 * 4 + (size_t)v.chunk_max * 4;
   const size_t xob = (size_t)8 * v.D * 4;
-  const size_t misc = (size_t)(8 + 8 + 64 + 16 + 2 * v.D + TILE) * 4;
-  const size_t t2 = (v.cap2 > 0) ? (size_t)TILE * v.D * 2 : 0;
+  const size_t misc = (size_t)(8 + 8 + 16 * vr.nw + 16 + 2 * v.D + tile) * 4;
+  const size_t t2 = (v.cap2 > 0) ? (size_t)tile * v.D * 2 : 0;
   return ringb + zsb + xob + misc + t2;
 }
 
-template <int D>
-static cudaError_t configure_d(const DevView& v) {
-  cudaError_t e = cudaFuncSetAttribute(k_decode_attn<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int D, int NW, int NST>
+static cudaError_t configure_k(const DevView& v) {
+  cudaError_t e = cudaFuncSetAttribute(k_decode_attn<D, NW, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)attn_smem_bytes(v));
   if (e != cudaSuccess) return e;
-  if (v.split > 8) e = cudaFuncSetAttribute(k_decode_attn<D>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (v.split > 8)
+    e = cudaFuncSetAttribute(k_decode_attn<D, NW, NST>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 
+template <int D, int NW, int NST>
+static cudaError_t launch_k(const DevView& v, cudaLaunchConfig_t& cfg, int layer, const void* q, const void* knew,
+                            const void* vnew, void* o, int fuse) {
+  cfg.blockDim = dim3(NW * 32, 1, 1);
+  return cudaLaunchKernelEx(&cfg, k_decode_attn<D, NW, NST>, v, layer, reinterpret_cast<const __nv_bfloat16*>(q),
+                            reinterpret_cast<const __nv_bfloat16*>(knew), reinterpret_cast<const __nv_bfloat16*>(vnew),
+                            o, fuse);
+}
+
+#define KVT_VARIANTS(X, D) X(D, 4, 3) X(D, 4, 4) X(D, 8, 3) X(D, 8, 4) X(D, 4, 6) X(D, 8, 6)
+
 cudaError_t attn_configure(const DevView& v) {
-  return v.D == 128 ? configure_d<128>(v) : configure_d<64>(v);
+  if (v.variant < 0 || v.variant >= kNumVariants) return cudaErrorInvalidValue;
+  const Variant vr = kVariants[v.variant];
+#define KVT_CONF(DD, NWW, NSS) \
+  if (v.D == DD && vr.nw == NWW && vr.nst == NSS) return configure_k<DD, NWW, NSS>(v);
+  KVT_VARIANTS(KVT_CONF, 128)
+  KVT_VARIANTS(KVT_CONF, 64)
+#undef KVT_CONF
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
                                void* o, int fuse, int pdl, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(v.split, v.B * v.Hkv, 1);
-  cfg.blockDim = dim3(ATT_THREADS, 1, 1);
   cfg.dynamicSmemBytes = attn_smem_bytes(v);
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -506,11 +546,13 @@ cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 2 : 1;
-  const __nv_bfloat16* qq = reinterpret_cast<const __nv_bfloat16*>(q);
-  const __nv_bfloat16* kk = reinterpret_cast<const __nv_bfloat16*>(knew);
-  const __nv_bfloat16* vv = reinterpret_cast<const __nv_bfloat16*>(vnew);
-  if (v.D == 128) return cudaLaunchKernelEx(&cfg, k_decode_attn<128>, v, layer, qq, kk, vv, o, fuse);
-  return cudaLaunchKernelEx(&cfg, k_decode_attn<64>, v, layer, qq, kk, vv, o, fuse);
+  const Variant vr = kVariants[v.variant];
+#define KVT_LAUNCH(DD, NWW, NSS) \
+  if (v.D == DD && vr.nw == NWW && vr.nst == NSS) return launch_k<DD, NWW, NSS>(v, cfg, layer, q, knew, vnew, o, fuse);
+  KVT_VARIANTS(KVT_LAUNCH, 128)
+  KVT_VARIANTS(KVT_LAUNCH, 64)
+#undef KVT_LAUNCH
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace kvt

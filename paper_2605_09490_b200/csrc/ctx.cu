@@ -88,6 +88,7 @@ kv_tier_status validate(const kv_tier_config* c) {
     return fail(nullptr, KV_TIER_E_INVAL, "staging_tokens must be 0 (stream) or KV_TIER_STAGING_ALL (differential)");
   if (c->shard != KV_TIER_SHARD_REQUEST) return fail(nullptr, KV_TIER_E_INVAL, "only request sharding is implemented");
   if (c->split < 0 || c->split > 16) return fail(nullptr, KV_TIER_E_INVAL, "split must be in [0, 16]");
+  if (c->variant < 0 || c->variant > 5) return fail(nullptr, KV_TIER_E_INVAL, "variant must be in [0, 5]");
   return KV_TIER_OK;
 }
 
@@ -219,6 +220,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.stream_mode = cfg->staging_tokens == 0;
   v.out_fp32 = cfg->out_fp32;
   v.split = auto_split(*cfg);
+  v.variant = cfg->variant;
   v.chunk_max = round16((cfg->max_tokens + v.split - 1) / v.split);
   for (int i = 0; i < 2; ++i) {
     v.k0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_k0[i]);

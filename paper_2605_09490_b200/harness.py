@@ -29,7 +29,7 @@ class TieredDecode:
     The chain holds n0 = N - 1 prefix tokens; step 0 appends position N - 1, so the
     first manage event (t = 0) sees exactly N tokens (reading AMB-22)."""
 
-    def __init__(self, w, device="cuda:0", out_fp32=True, split=0, seed_offset=0, keep_inputs=False):
+    def __init__(self, w, device="cuda:0", out_fp32=True, split=0, seed_offset=0, keep_inputs=False, variant=0):
         self.w = w
         self.dev = torch.device(device)
         torch.cuda.set_device(self.dev)
@@ -40,7 +40,7 @@ class TieredDecode:
         self.cfg = kt.make_config(B, L, Hq, Hkv, d, self.n0 + T, P, hbm_bp=w["hbm_bp"], evict_bp=w["evict_bp"],
                                   t2_bp=w["t2_bp"], manage_interval=w["interval"], evict_mode=w["evict_mode"],
                                   staging=w["staging"], device=self.dev.index or 0, out_fp32=int(out_fp32),
-                                  split=split)
+                                  split=split, variant=variant)
         self.kv = kt.KvTier(self.cfg)
         self.main = torch.cuda.Stream(self.dev)
         self.side = torch.cuda.Stream(self.dev)

@@ -35,7 +35,7 @@ class Config(C.Structure):
         ("hbm_ratio_bp", C.c_uint32), ("evict_ratio_bp", C.c_uint32), ("t2_fraction_bp", C.c_uint32),
         ("evict_mode", C.c_int32), ("staging_tokens", C.c_uint32),
         ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("shard", C.c_int32),
-        ("out_fp32", C.c_int32), ("split", C.c_int32)]
+        ("out_fp32", C.c_int32), ("split", C.c_int32), ("variant", C.c_int32)]
 
 
 class Sizes(C.Structure):
@@ -116,13 +116,13 @@ def _stream_ptr(stream):
 
 def make_config(B, L, Hq, Hkv, d, max_tokens, prompt_len, hbm_bp=5000, evict_bp=500, t2_bp=0,
                 sink_size=4, window_size=128, manage_interval=64, evict_mode=EVICT_TOTAL,
-                staging=STAGING_ALL, device=0, out_fp32=1, split=0, rank=0, world=1):
+                staging=STAGING_ALL, device=0, out_fp32=1, split=0, rank=0, world=1, variant=0):
     return Config(num_requests=B, num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=d,
                   max_tokens=max_tokens, prompt_len=prompt_len, sink_size=sink_size,
                   window_size=window_size, manage_interval=manage_interval, hbm_ratio_bp=hbm_bp,
                   evict_ratio_bp=evict_bp, t2_fraction_bp=t2_bp, evict_mode=evict_mode,
                   staging_tokens=staging, device=device, rank=rank, world=world, shard=0,
-                  out_fp32=out_fp32, split=split)
+                  out_fp32=out_fp32, split=split, variant=variant)
 
 
 def query_sizes(cfg):

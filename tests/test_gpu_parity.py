@@ -67,8 +67,8 @@ def _check_event_state(run, orc, reqs_gpu, layers=(0,)):
                 assert np.array_equal(scales[bg][:, :, 1], st.scaleV[l, bo, :, pos].T)
 
 
-def _run_pair(w, reqs=None, graph=False, check_every=1, layers_api=False, split=0):
-    run = H.TieredDecode(w, split=split)
+def _run_pair(w, reqs=None, graph=False, check_every=1, layers_api=False, split=0, variant=0):
+    run = H.TieredDecode(w, split=split, variant=variant)
     orc = OracleRun(w, reqs=reqs)
     reqs_gpu = orc.reqs
     if graph:
@@ -136,10 +136,16 @@ def test_tiny_cluster_splits(split):          # DSMEM merge at several cluster s
     _run_pair(H.workload("tiny", interval=8, B=3, L=2, steps=17), split=split)
 
 
-def test_multi_request_multi_layer_graph():   # several tiles, ragged tails, B > 1, d = 128
+@pytest.mark.parametrize("variant", range(6))
+def test_multi_request_multi_layer_graph(variant):   # several tiles, ragged tails, B > 1, d = 128
     w = H.workload("tiny", B=3, L=2, Hq=12, Hkv=2, d=128, N=700, P=40, interval=16, steps=40,
                    hbm_bp=3000, evict_bp=1000, t2_bp=2500)
-    _run_pair(w, graph=True, check_every=7)
+    _run_pair(w, graph=True, check_every=7, variant=variant, split=(0, 4, 2, 3, 1, 8)[variant])
+
+
+@pytest.mark.parametrize("variant", [0, 2, 5])
+def test_tiny_variants(variant):                      # d = 64 kernels
+    _run_pair(H.workload("tiny", interval=8, t2_bp=3000, B=2, L=2, steps=20), graph=True, variant=variant)
 
 
 # --------------------------------------------------------------------- 7B-shaped, sampled
