@@ -2,12 +2,16 @@
 // cumulative score update (Eq. 1, Eq. 3, Prop. 1).
 //
 // One thread-block cluster of C CTAs per (request b, kv head g).  The visible rows of the
-// unit are ordered [T0 rows except the new token | T1 staging | T2 int8 | new token]; CTA r
-// of the cluster owns a contiguous 1/C chunk.
+// unit are laid out virtually as [T0 rows except the new token | pad | T1 staging | pad |
+// T2 int8 | pad | new token] (segments start at multiples of 16); CTA r of the cluster owns
+// a contiguous 1/C chunk.  Warp NW is the producer: it streams the chunk's K tiles, then its
+// V tiles, with 1-D bulk async copies (cp.async.bulk, one or two per tile) into an NST-deep
+// shared-memory ring guarded by full/empty mbarriers.  Rows are stored pre-swizzled in HBM
+// (16-B chunk c of store row j at c ^ (j & 7)), so a linear copy is the conflict-free layout.
 //
 //   prologue  (before griddepcontrol.wait, overlaps the previous layer's kernel under PDL)
-//            counters, positions of the chunk -> SMEM, first K tiles in flight
-//   phase A  K tiles (cp.async ring, XOR-swizzled SMEM) -> S^T = K q^T on the tensor cores
+//            counters, the first tiles in flight, positions of the chunk -> SMEM
+//   phase A  K tiles -> S^T = K q^T on the tensor cores
 //            (mma.sync m16n8k16 bf16, swap-AB: tokens = M, heads = N = 8); logits (log2
 //            domain) stay in SMEM for the whole chunk; running max per head
 //   phase B  V tiles -> p = exp2(z - m_local) -> o^T += V^T p^T (movmatrix.trans turns the
@@ -26,7 +30,37 @@ namespace cg = cooperative_groups;
 
 namespace kvt {
 
-// Variants (warps per CTA NW, pipeline stages NST): a tile is 16 tokens per warp.
+// Variants (consumer warps NW, pipeline stages NST): a tile is 16 tokens per consumer warp.
+
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok)
+                 : "r"(a), "r"(parity)
+                 : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ int ru16(int x) { return (x + 15) & ~15; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -76,11 +110,12 @@ __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w <
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
 template <int D, int NW, int NST>
-__global__ void __launch_bounds__(NW * 32, (NW == 4 ? 3 : 2))
+__global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
     k_decode_attn(const DevView v, const int layer, const __nv_bfloat16* __restrict__ q,
                   const __nv_bfloat16* __restrict__ knew, const __nv_bfloat16* __restrict__ vnew,
                   void* __restrict__ o, const int fuse) {
-  constexpr int ATT_THREADS = NW * 32;
+  constexpr int NCONS = NW * 32;              // consumer threads
+  constexpr int NTHR = NCONS + 32;            // + producer warp
   constexpr int TILE = NW * 16;
   constexpr int ROWB = D * 2;
   constexpr int TILEB = TILE * ROWB;
@@ -96,30 +131,35 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 3 : 2))
 
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;
-  float* zs = reinterpret_cast<float*>(smem + NST * TILEB);   // [chunk_max][8] logits (log2)
-  int* spos = reinterpret_cast<int*>(zs + (size_t)v.chunk_max * 8);   // [chunk_max] positions
-  float* xo = reinterpret_cast<float*>(spos + v.chunk_max);    // [8][D]  exchange: o partial
-  float* xm = xo + 8 * D;                                      // [8]     exchange: max (log2)
-  float* xl = xm + 8;                                          // [8]     exchange: sum
-  float* red = xl + 8;                                         // [2][NW][8] warp max / warp l
-  float* sML = red + 16 * NW;                                  // [16] merged M, 1/L
-  float* nrow = sML + 16;                                      // [2][D] new token K, V (fp32)
-  float* t2sc = nrow + 2 * D;                                  // [TILE] T2 row scales
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + NST * TILEB);   // full[NST], empty[NST]
+  float* zs = reinterpret_cast<float*>(bars + 2 * NST + 2);     // [chunk_max][8] logits (log2)
+  int* spos = reinterpret_cast<int*>(zs + (size_t)v.chunk_max * 8);   // [chunk_max] positions (-1: pad)
+  float* sS = reinterpret_cast<float*>(spos + v.chunk_max);     // [chunk_max] S_part values
+  float* xo = sS + v.chunk_max;                                 // [8][D]  exchange: o partial
+  float* xm = xo + 8 * D;                                       // [8]     exchange: max (log2)
+  float* xl = xm + 8;                                           // [8]     exchange: sum
+  float* red = xl + 8;                                          // [2][NW][8] warp max / warp l
+  float* sML = red + 16 * NW;                                   // [16] merged M, 1/L
+  float* nrow = sML + 16;                                       // [2][D] new token K, V (fp32)
+  float* t2sc = nrow + 2 * D;                                   // [TILE] T2 row scales
   unsigned char* t2buf = reinterpret_cast<unsigned char*>(t2sc + TILE);   // [TILE][D] bf16
 
   // ---------------------------------------------------------------- prologue (pre-PDL-wait)
   const int cur = v.st->cur;
   const int* cn = v.cnt[cur] + b * CNT_STRIDE;
   const int n0 = cn[0], n1 = cn[1], n2 = cn[2];
-  const int n0o = n0 - 1;                           // T0 rows before the new token
-  const int n01 = n0o + n1, n012 = n01 + n2, nvis = n012 + 1;
-  const int chunk = (nvis + C - 1) / C;
-  const int vbeg = min(r * chunk, nvis), vend = min(vbeg + chunk, nvis);
-  const int aend = min(vend, n01);                  // bf16 segment [vbeg, aend)
-  const int t2beg = max(vbeg, n01), t2end = min(vend, n012);   // int8 segment
-  const bool has_new = vend == nvis && nvis > vbeg; // this CTA owns the new token
+  const int n0o = n0 - 1;                                  // T0 rows before the new token
+  const int a1 = ru16(n0o), a2 = ru16(a1 + n1), a3 = ru16(a2 + n2);   // segment starts
+  const int nvirt = a3 + 1;
+  const int chunk = ru16((nvirt + C - 1) / C);
+  const int vbeg = min(r * chunk, nvirt), vend = min(vbeg + chunk, nvirt);
+  const int aend = min(vend, a2);                          // bf16 tiles cover [vbeg, aend)
+  const int t2beg = max(vbeg, a2), t2end = min(vend, a2 + n2);
+  const bool has_new = vbeg <= a3 && a3 < vend;
   const int nb = max(0, aend - vbeg);
   const int nt = (nb + TILE - 1) / TILE;
+  const int total = 2 * nt;
+  auto bf16_valid = [&](int t) { return t < n0o || (t >= a1 && t < a1 + n1); };
 
   const size_t grp = grp_of(v, layer, b, g);
   const __nv_bfloat16* K0 = v.k0[cur] + grp * v.cap0 * D;
@@ -134,294 +174,329 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 3 : 2))
     K1 = v.k1[cur] + grp * v.cap1 * D;
     V1 = v.v1[cur] + grp * v.cap1 * D;
   }
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + NST);
 
-  auto load_tile = [&](int i) {
-    const bool isV = i >= nt;
-    const int tv0 = vbeg + (isV ? i - nt : i) * TILE;
-    const __nv_bfloat16* S0 = isV ? V0 : K0;
-    const __nv_bfloat16* S1 = isV ? V1 : K1;
-    const uint32_t sbase = smem_u32(ring + (i % NST) * TILEB);
-    constexpr int CPR = D / 8;                // 16-B chunks per row
-    constexpr int RPP = ATT_THREADS / CPR;    // rows per pass
-    const int c = tid % CPR, r0 = tid / CPR;
-#pragma unroll
-    for (int p = 0; p < TILE / RPP; ++p) {
-      const int row = r0 + p * RPP;
-      const int tok = tv0 + row;
-      const __nv_bfloat16* src = S0;
-      int nbytes = 0;
-      if (tok < aend) {
-        nbytes = 16;
-        src = tok < n0o ? S0 + (size_t)tok * D : S1 + (size_t)(tok - n0o) * D;
+  if (tid == 0) {
+    for (int s2 = 0; s2 < NST; ++s2) {
+      mbar_init(full0 + 8 * s2, 1);
+      mbar_init(empty0 + 8 * s2, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (w == NW) {
+    // ============================ producer warp ============================
+    if (lane == 0) {
+      for (int i = 0; i < total; ++i) {
+        const int s2 = i % NST;
+        if (i >= NST) mbar_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
+        const bool isV = i >= nt;
+        const int ts = vbeg + (isV ? i - nt : i) * TILE;
+        const uint32_t full = full0 + 8 * s2, dst = ring_s + s2 * TILEB;
+        mbar_expect_tx(full, TILEB);
+        if (ts < a1) {   // T0 rows [ts, min(ts+TILE, a1)) (pad rows beyond n0o are stale but finite)
+          const int nrows = min(TILE, a1 - ts);
+          bulk_g2s(dst, (isV ? V0 : K0) + (size_t)ts * D, nrows * ROWB, full);
+          if (nrows < TILE)
+            bulk_g2s(dst + nrows * ROWB, isV ? V1 : K1, (TILE - nrows) * ROWB, full);
+        } else {
+          bulk_g2s(dst, (isV ? V1 : K1) + (size_t)(ts - a1) * D, TILEB, full);
+        }
       }
-      cp_async16(sbase + row * ROWB + ((c ^ (row & 7)) << 4), src + c * 8, nbytes);
     }
-  };
-  const int total = 2 * nt;
-#pragma unroll
-  for (int s = 0; s < NST - 1; ++s) {
-    if (s < total) load_tile(s);
-    cp_commit();
-  }
-  // positions of the chunk's tokens (for the score update)
-  if (fuse) {
-    const int* I0 = v.idx[cur][0] + (size_t)b * v.cap0;
-    const int* I1 = v.idx[cur][1] + (size_t)b * v.cap1;
-    const int* I2 = v.idx[cur][2] + (size_t)b * v.cap2;
-    for (int j = tid; j < vend - vbeg; j += ATT_THREADS) {
-      const int tok = vbeg + j;
-      spos[j] = tok < n0o ? I0[tok] : tok < n01 ? I1[tok - n0o] : tok < n012 ? I2[tok - n01] : I0[n0o];
+    __syncwarp();
+    pdl_trigger();
+  } else {
+    // ============================ consumer warps ============================
+    // positions of the chunk (for the score update), cp.async: no stall
+    if (fuse) {
+      const int* I0 = v.idx[cur][0] + (size_t)b * v.cap0;
+      const int* I1 = v.idx[cur][1] + (size_t)b * v.cap1;
+      const int* I2 = v.idx[cur][2] + (size_t)b * v.cap2;
+      for (int j = tid; j < vend - vbeg; j += NCONS) {
+        const int t = vbeg + j;
+        const int* src = t < n0o ? I0 + t
+                       : (t >= a1 && t < a1 + n1) ? I1 + (t - a1)
+                       : (t >= a2 && t < a2 + n2) ? I2 + (t - a2)
+                       : t == a3 ? I0 + n0o : nullptr;
+        if (src) cp_async4(smem_u32(spos + j), src);
+        else spos[j] = -1;
+      }
+      cp_commit();
     }
+    pdl_trigger();
   }
-  pdl_trigger();
   // ---------------------------------------------------------------- dependent inputs
   pdl_wait();
+  if (w == NW) {
+    // the producer warp only joins the CTA-wide barriers below
+  } else {
+    if (fuse) {   // S_part values of the chunk's tokens (written by the previous layer)
+      cp_wait<0>();
+      float* Sg = v.S + ((size_t)b * v.Hkv + g) * v.Nmax;
+      for (int j = tid; j < vend - vbeg; j += NCONS) {
+        const int pos = spos[j];
+        if (pos >= 0) cp_async4(smem_u32(sS + j), Sg + pos);
+      }
+      cp_commit();
+    }
+  }
 
   uint32_t qf[KS][2];
-  {
-    const __nv_bfloat16* qh = q + ((size_t)b * v.Hq + g * G + gq) * D;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      if (gq < G) {
-        qf[ks][0] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 2 * tq);
-        qf[ks][1] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 8 + 2 * tq);
-      } else {
-        qf[ks][0] = 0u;
-        qf[ks][1] = 0u;
-      }
-    }
-  }
   const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));   // log2(e)/sqrt(d)
-
-  // new token (a1): append its K/V row to T0 row n0-1 and keep it in SMEM (fp32)
-  if (has_new) {
-    uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[cur]) + (grp * v.cap0 + n0o) * D;
-    uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[cur]) + (grp * v.cap0 + n0o) * D;
-    const uint16_t* ks_ = knew ? reinterpret_cast<const uint16_t*>(knew) + ((size_t)b * v.Hkv + g) * D : K0w;
-    const uint16_t* vs_ = vnew ? reinterpret_cast<const uint16_t*>(vnew) + ((size_t)b * v.Hkv + g) * D : V0w;
-    for (int e = tid; e < D; e += ATT_THREADS) {
-      const uint16_t kb = ks_[e], vb = vs_[e];
-      nrow[e] = bf16_bits_to_f(kb);
-      nrow[D + e] = bf16_bits_to_f(vb);
-      if (knew) K0w[e] = kb;
-      if (vnew) V0w[e] = vb;
-    }
-  }
-
   float mx0 = -INFINITY, mx1 = -INFINITY;    // running max, heads 2tq, 2tq+1
   float l0 = 0.f, l1 = 0.f;
   float oacc[KS][4];
 #pragma unroll
   for (int mt = 0; mt < KS; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
-
-  auto qk_warp = [&](uint32_t sbase, int tv0, int tend, const float* rsc) {
-    if (tv0 + w * 16 >= tend) return;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    const int mi = lane >> 3, ii = lane & 7;
-    const int row = w * 16 + ii + ((mi & 1) << 3);
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int ch = 2 * ks + (mi >> 1);
-      uint32_t a0, a1, a2, a3;
-      ldsm_x4(a0, a1, a2, a3, sbase + row * ROWB + ((ch ^ (row & 7)) << 4));
-      mma16816(acc, a0, a1, a2, a3, qf[ks][0], qf[ks][1]);
-    }
-    const int r0 = w * 16 + gq, r1 = r0 + 8;
-    const int t0 = tv0 + r0, t1 = tv0 + r1;
-    if (t0 < tend) {
-      const float f = rsc ? rsc[r0] * sl2 : sl2;
-      const float z0 = acc[0] * f, z1 = acc[1] * f;
-      *reinterpret_cast<float2*>(&zs[(t0 - vbeg) * 8 + 2 * tq]) = make_float2(z0, z1);
-      mx0 = fmaxf(mx0, z0);
-      mx1 = fmaxf(mx1, z1);
-    }
-    if (t1 < tend) {
-      const float f = rsc ? rsc[r1] * sl2 : sl2;
-      const float z0 = acc[2] * f, z1 = acc[3] * f;
-      *reinterpret_cast<float2*>(&zs[(t1 - vbeg) * 8 + 2 * tq]) = make_float2(z0, z1);
-      mx0 = fmaxf(mx0, z0);
-      mx1 = fmaxf(mx1, z1);
-    }
-  };
   float m2a = 0.f, m2b = 0.f;   // CTA max for heads 2tq, 2tq+1
-  auto pv_warp = [&](uint32_t sbase, int tv0, int tend, const float* rsc) {
-    if (tv0 + w * 16 >= tend) return;
-    const int r0 = w * 16 + gq, r1 = r0 + 8;
-    const int t0 = tv0 + r0, t1 = tv0 + r1;
-    float p00 = 0.f, p01 = 0.f, p10 = 0.f, p11 = 0.f;
-    if (t0 < tend) {
-      const float2 z = *reinterpret_cast<const float2*>(&zs[(t0 - vbeg) * 8 + 2 * tq]);
-      p00 = exp2f(z.x - m2a);
-      p01 = exp2f(z.y - m2b);
-    }
-    if (t1 < tend) {
-      const float2 z = *reinterpret_cast<const float2*>(&zs[(t1 - vbeg) * 8 + 2 * tq]);
-      p10 = exp2f(z.x - m2a);
-      p11 = exp2f(z.y - m2b);
-    }
-    l0 += p00 + p10;
-    l1 += p01 + p11;
-    if (rsc) {   // T2: o += p * scale_v * code  (codes are exact in bf16)
-      p00 *= rsc[r0]; p01 *= rsc[r0];
-      p10 *= rsc[r1]; p11 *= rsc[r1];
-    }
-    const uint32_t b0 = movm_t(pack_bf16(p00, p01));
-    const uint32_t b1 = movm_t(pack_bf16(p10, p11));
-    const int mi = lane >> 3, ii = lane & 7;
-    const int row = w * 16 + ii + ((mi >> 1) << 3);
-#pragma unroll
-    for (int mt = 0; mt < KS; ++mt) {
-      const int ch = 2 * mt + (mi & 1);
-      uint32_t a0, a1, a2, a3;
-      ldsm_x4_t(a0, a1, a2, a3, sbase + row * ROWB + ((ch ^ (row & 7)) << 4));
-      mma16816(oacc[mt], a0, a1, a2, a3, b0, b1);
-    }
-  };
-  auto stage_t2 = [&](int tv0, bool isV) {
-    const int8_t* C2 = (isV ? v.c2v[cur] : v.c2k[cur]) + grp * v.cap2 * D;
-    const float* S2 = (isV ? v.s2v[cur] : v.s2k[cur]) + grp * v.cap2;
-    for (int e = tid; e < TILE * (D / 16); e += ATT_THREADS) {
-      const int row = e / (D / 16), j = e % (D / 16);
-      const int tok = tv0 + row;
-      uint4 cw = make_uint4(0u, 0u, 0u, 0u);
-      if (tok < t2end) cw = *reinterpret_cast<const uint4*>(C2 + (size_t)(tok - n01) * D + 16 * j);
-      uint4 lo, hi;
-      lo.x = i8pair_to_bf16x2(cw.x, 0); lo.y = i8pair_to_bf16x2(cw.x, 1);
-      lo.z = i8pair_to_bf16x2(cw.y, 0); lo.w = i8pair_to_bf16x2(cw.y, 1);
-      hi.x = i8pair_to_bf16x2(cw.z, 0); hi.y = i8pair_to_bf16x2(cw.z, 1);
-      hi.z = i8pair_to_bf16x2(cw.w, 0); hi.w = i8pair_to_bf16x2(cw.w, 1);
-      *reinterpret_cast<uint4*>(t2buf + row * ROWB + (((2 * j) ^ (row & 7)) << 4)) = lo;
-      *reinterpret_cast<uint4*>(t2buf + row * ROWB + (((2 * j + 1) ^ (row & 7)) << 4)) = hi;
-    }
-    for (int row = tid; row < TILE; row += ATT_THREADS) {
-      const int tok = tv0 + row;
-      t2sc[row] = tok < t2end ? S2[tok - n01] : 0.f;
-    }
-  };
 
-  // ---- phase A on T2 rows (rare; synchronous)
-  for (int tv0 = t2beg; tv0 < t2end; tv0 += TILE) {
-    __syncthreads();
-    stage_t2(tv0, false);
-    __syncthreads();
-    qk_warp(smem_u32(t2buf), tv0, t2end, t2sc);
-  }
-  // ---- phase A on the new token (CUDA cores, fp32): warp 0 computes all G logits
-  __syncthreads();   // nrow visible
-  if (has_new && w == 0) {
-    float part = 0.f;   // head gq, dims of this lane's q fragments
+  if (w < NW) {
+    {
+      const __nv_bfloat16* qh = q + ((size_t)b * v.Hq + g * G + gq) * D;
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int d0 = ks * 16 + 2 * tq;
-      part += bf16lo(qf[ks][0]) * nrow[d0] + bf16hi(qf[ks][0]) * nrow[d0 + 1];
-      part += bf16lo(qf[ks][1]) * nrow[d0 + 8] + bf16hi(qf[ks][1]) * nrow[d0 + 9];
+      for (int ks = 0; ks < KS; ++ks) {
+        if (gq < G) {
+          qf[ks][0] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 2 * tq);
+          qf[ks][1] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 8 + 2 * tq);
+        } else {
+          qf[ks][0] = 0u;
+          qf[ks][1] = 0u;
+        }
+      }
     }
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    if (tq == 0) zs[(nvis - 1 - vbeg) * 8 + gq] = part * sl2;
-  }
+    // new token (a1): append its K/V row to T0 row n0-1 (swizzled) and keep it in SMEM (fp32)
+    if (has_new) {
+      uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[cur]) + (grp * v.cap0 + n0o) * D;
+      uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[cur]) + (grp * v.cap0 + n0o) * D;
+      const uint16_t* kin = knew ? reinterpret_cast<const uint16_t*>(knew) + ((size_t)b * v.Hkv + g) * D : nullptr;
+      const uint16_t* vin = vnew ? reinterpret_cast<const uint16_t*>(vnew) + ((size_t)b * v.Hkv + g) * D : nullptr;
+      for (int e = tid; e < D; e += NCONS) {
+        const int se = swz_off(n0o, e);
+        const uint16_t kb = kin ? kin[e] : K0w[se];
+        const uint16_t vb = vin ? vin[e] : V0w[se];
+        nrow[e] = bf16_bits_to_f(kb);
+        nrow[D + e] = bf16_bits_to_f(vb);
+        if (kin) K0w[se] = kb;
+        if (vin) V0w[se] = vb;
+      }
+    }
 
-  auto write_warp_max = [&]() {
-    float a = mx0, c = mx1;
+    auto qk_warp = [&](uint32_t sbase, int tv0, int tend, const float* rsc, bool t2seg) {
+      if (tv0 + w * 16 >= tend) return;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
+      const int mi = lane >> 3, ii = lane & 7;
+      const int row = w * 16 + ii + ((mi & 1) << 3);
+#pragma unroll
+      for (int ks = 0; ks < KS; ks += 2) {
+        uint32_t a0, a1_, a2_, a3_;
+        ldsm_x4(a0, a1_, a2_, a3_, sbase + row * ROWB + (((2 * ks + (mi >> 1)) ^ (row & 7)) << 4));
+        mma16816(acc, a0, a1_, a2_, a3_, qf[ks][0], qf[ks][1]);
+        ldsm_x4(a0, a1_, a2_, a3_, sbase + row * ROWB + (((2 * ks + 2 + (mi >> 1)) ^ (row & 7)) << 4));
+        mma16816(acc2, a0, a1_, a2_, a3_, qf[ks + 1][0], qf[ks + 1][1]);
+      }
+      const int r0 = w * 16 + gq, r1 = r0 + 8;
+      const int t0 = tv0 + r0, t1 = tv0 + r1;
+      if (t0 < tend && (t2seg || bf16_valid(t0))) {
+        const float f = rsc ? rsc[r0] * sl2 : sl2;
+        const float z0 = (acc[0] + acc2[0]) * f, z1 = (acc[1] + acc2[1]) * f;
+        *reinterpret_cast<float2*>(&zs[(t0 - vbeg) * 8 + 2 * tq]) = make_float2(z0, z1);
+        mx0 = fmaxf(mx0, z0);
+        mx1 = fmaxf(mx1, z1);
+      }
+      if (t1 < tend && (t2seg || bf16_valid(t1))) {
+        const float f = rsc ? rsc[r1] * sl2 : sl2;
+        const float z0 = (acc[2] + acc2[2]) * f, z1 = (acc[3] + acc2[3]) * f;
+        *reinterpret_cast<float2*>(&zs[(t1 - vbeg) * 8 + 2 * tq]) = make_float2(z0, z1);
+        mx0 = fmaxf(mx0, z0);
+        mx1 = fmaxf(mx1, z1);
+      }
+    };
+    auto pv_warp = [&](uint32_t sbase, int tv0, int tend, const float* rsc, bool t2seg) {
+      if (tv0 + w * 16 >= tend) return;
+      const int r0 = w * 16 + gq, r1 = r0 + 8;
+      const int t0 = tv0 + r0, t1 = tv0 + r1;
+      float p00 = 0.f, p01 = 0.f, p10 = 0.f, p11 = 0.f;
+      if (t0 < tend && (t2seg || bf16_valid(t0))) {
+        const float2 z = *reinterpret_cast<const float2*>(&zs[(t0 - vbeg) * 8 + 2 * tq]);
+        p00 = exp2f(z.x - m2a);
+        p01 = exp2f(z.y - m2b);
+      }
+      if (t1 < tend && (t2seg || bf16_valid(t1))) {
+        const float2 z = *reinterpret_cast<const float2*>(&zs[(t1 - vbeg) * 8 + 2 * tq]);
+        p10 = exp2f(z.x - m2a);
+        p11 = exp2f(z.y - m2b);
+      }
+      l0 += p00 + p10;
+      l1 += p01 + p11;
+      if (rsc) {   // T2: o += p * scale_v * code  (codes are exact in bf16)
+        p00 *= rsc[r0]; p01 *= rsc[r0];
+        p10 *= rsc[r1]; p11 *= rsc[r1];
+      }
+      const uint32_t b0 = movm_t(pack_bf16(p00, p01));
+      const uint32_t b1 = movm_t(pack_bf16(p10, p11));
+      const int mi = lane >> 3, ii = lane & 7;
+      const int row = w * 16 + ii + ((mi >> 1) << 3);
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) {
+        const int ch = 2 * mt + (mi & 1);
+        uint32_t a0, a1_, a2_, a3_;
+        ldsm_x4_t(a0, a1_, a2_, a3_, sbase + row * ROWB + ((ch ^ (row & 7)) << 4));
+        mma16816(oacc[mt], a0, a1_, a2_, a3_, b0, b1);
+      }
+    };
+    auto stage_t2 = [&](int tv0, bool isV) {   // int8 codes -> exact bf16 (canonical codes, swizzled in SMEM)
+      const int8_t* C2 = (isV ? v.c2v[cur] : v.c2k[cur]) + grp * v.cap2 * D;
+      const float* S2 = (isV ? v.s2v[cur] : v.s2k[cur]) + grp * v.cap2;
+      for (int e = tid; e < TILE * (D / 16); e += NCONS) {
+        const int row = e / (D / 16), j = e % (D / 16);
+        const int tok = tv0 + row;
+        uint4 cw = make_uint4(0u, 0u, 0u, 0u);
+        if (tok < t2end) cw = *reinterpret_cast<const uint4*>(C2 + (size_t)(tok - a2) * D + 16 * j);
+        uint4 lo, hi;
+        lo.x = i8pair_to_bf16x2(cw.x, 0); lo.y = i8pair_to_bf16x2(cw.x, 1);
+        lo.z = i8pair_to_bf16x2(cw.y, 0); lo.w = i8pair_to_bf16x2(cw.y, 1);
+        hi.x = i8pair_to_bf16x2(cw.z, 0); hi.y = i8pair_to_bf16x2(cw.z, 1);
+        hi.z = i8pair_to_bf16x2(cw.w, 0); hi.w = i8pair_to_bf16x2(cw.w, 1);
+        *reinterpret_cast<uint4*>(t2buf + row * ROWB + (((2 * j) ^ (row & 7)) << 4)) = lo;
+        *reinterpret_cast<uint4*>(t2buf + row * ROWB + (((2 * j + 1) ^ (row & 7)) << 4)) = hi;
+      }
+      for (int row = tid; row < TILE; row += NCONS) {
+        const int tok = tv0 + row;
+        t2sc[row] = tok < t2end ? S2[tok - a2] : 0.f;
+      }
+    };
+
+    // ---- phase A on T2 rows (rare; synchronous, consumer barrier 1)
+    for (int tv0 = t2beg; tv0 < t2end; tv0 += TILE) {
+      named_sync(1, NCONS);
+      stage_t2(tv0, false);
+      named_sync(1, NCONS);
+      qk_warp(smem_u32(t2buf), tv0, t2end, t2sc, true);
+    }
+    // ---- phase A on the new token (CUDA cores, fp32): warp 0 computes all heads' logits
+    if (has_new) named_sync(1, NCONS);   // nrow visible
+    if (has_new && w == 0) {
+      float part = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int d0 = ks * 16 + 2 * tq;
+        part += bf16lo(qf[ks][0]) * nrow[d0] + bf16hi(qf[ks][0]) * nrow[d0 + 1];
+        part += bf16lo(qf[ks][1]) * nrow[d0 + 8] + bf16hi(qf[ks][1]) * nrow[d0 + 9];
+      }
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      if (tq == 0) zs[(a3 - vbeg) * 8 + gq] = part * sl2;
+    }
+
+    auto write_warp_max = [&]() {
+      float a = mx0, c = mx1;
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, off));
+        c = fmaxf(c, __shfl_xor_sync(0xffffffffu, c, off));
+      }
+      if (lane < 4) {
+        red[w * 8 + 2 * lane] = a;
+        red[w * 8 + 2 * lane + 1] = c;
+      }
+    };
+    auto reduce_max = [&]() {   // after a consumer barrier: CTA max incl. the new token
+      float nz0 = -INFINITY, nz1 = -INFINITY;
+      if (has_new) {
+        nz0 = zs[(a3 - vbeg) * 8 + 2 * tq];
+        nz1 = zs[(a3 - vbeg) * 8 + 2 * tq + 1];
+      }
+      m2a = nz0;
+      m2b = nz1;
+#pragma unroll
+      for (int ww = 0; ww < NW; ++ww) {
+        m2a = fmaxf(m2a, red[ww * 8 + 2 * tq]);
+        m2b = fmaxf(m2b, red[ww * 8 + 2 * tq + 1]);
+      }
+      if (tid < 8) {
+        float m = has_new ? zs[(a3 - vbeg) * 8 + tid] : -INFINITY;
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) m = fmaxf(m, red[ww * 8 + tid]);
+        xm[tid] = m;
+      }
+      if (m2a == -INFINITY) m2a = 0.f;
+      if (m2b == -INFINITY) m2b = 0.f;
+    };
+
+    // ---- phases A (K tiles) and B (V tiles) from the bulk-copy ring
+    for (int i = 0; i < total; ++i) {
+      const int s2 = i % NST;
+      if (i == nt) {                 // every warp's max of phase A is in `red`
+        named_sync(1, NCONS);
+        reduce_max();
+      }
+      mbar_wait(full0 + 8 * s2, (i / NST) & 1);
+      const uint32_t sbase = ring_s + s2 * TILEB;
+      if (i < nt) {
+        qk_warp(sbase, vbeg + i * TILE, aend, nullptr, false);
+        if (i == nt - 1) write_warp_max();
+      } else {
+        pv_warp(sbase, vbeg + (i - nt) * TILE, aend, nullptr, false);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * s2);
+    }
+    if (nt == 0) {
+      write_warp_max();
+      named_sync(1, NCONS);
+      reduce_max();
+    }
+    // ---- phase B on T2 rows
+    for (int tv0 = t2beg; tv0 < t2end; tv0 += TILE) {
+      named_sync(1, NCONS);
+      stage_t2(tv0, true);
+      named_sync(1, NCONS);
+      pv_warp(smem_u32(t2buf), tv0, t2end, t2sc, true);
+    }
+    // ---- phase B on the new token: rank-1 update of warp 0's o^T fragments
+    if (has_new && w == 0) {
+      const float* zr = zs + (a3 - vbeg) * 8;
+      const float pa = exp2f(zr[2 * tq] - m2a), pb = exp2f(zr[2 * tq + 1] - m2b);
+      if (gq == 0) { l0 += pa; l1 += pb; }          // counted once per head (lanes 0..3)
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) {
+        const float va = nrow[D + mt * 16 + gq], vb = nrow[D + mt * 16 + gq + 8];
+        oacc[mt][0] += pa * va;
+        oacc[mt][1] += pb * va;
+        oacc[mt][2] += pa * vb;
+        oacc[mt][3] += pb * vb;
+      }
+    }
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
-      a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, off));
-      c = fmaxf(c, __shfl_xor_sync(0xffffffffu, c, off));
-    }
-    if (lane < 4) {
-      red[w * 8 + 2 * lane] = a;
-      red[w * 8 + 2 * lane + 1] = c;
-    }
-  };
-  auto reduce_max = [&]() {   // after a barrier: CTA max incl. the new token
-    float nz0 = -INFINITY, nz1 = -INFINITY;
-    if (has_new) {
-      nz0 = zs[(nvis - 1 - vbeg) * 8 + 2 * tq];
-      nz1 = zs[(nvis - 1 - vbeg) * 8 + 2 * tq + 1];
-    }
-    m2a = nz0;
-    m2b = nz1;
-#pragma unroll
-    for (int ww = 0; ww < NW; ++ww) {
-      m2a = fmaxf(m2a, red[ww * 8 + 2 * tq]);
-      m2b = fmaxf(m2b, red[ww * 8 + 2 * tq + 1]);
-    }
-    if (tid < 8) {
-      float m = has_new ? zs[(nvis - 1 - vbeg) * 8 + tid] : -INFINITY;
-#pragma unroll
-      for (int ww = 0; ww < NW; ++ww) m = fmaxf(m, red[ww * 8 + tid]);
-      xm[tid] = m;
-    }
-    if (m2a == -INFINITY) m2a = 0.f;
-    if (m2b == -INFINITY) m2b = 0.f;
-  };
-
-  // ---- phases A (K tiles) and B (V tiles) through the cp.async ring
-  for (int i = 0; i < total; ++i) {
-    cp_wait<NST - 2>();
-    __syncthreads();
-    if (i + NST - 1 < total) load_tile(i + NST - 1);
-    cp_commit();
-    if (i == nt) reduce_max();
-    const uint32_t sbase = smem_u32(ring + (i % NST) * TILEB);
-    if (i < nt) {
-      qk_warp(sbase, vbeg + i * TILE, aend, nullptr);
-      if (i == nt - 1) write_warp_max();
-    } else {
-      pv_warp(sbase, vbeg + (i - nt) * TILE, aend, nullptr);
-    }
-  }
-  cp_wait<0>();
-  if (nt == 0) {
-    write_warp_max();
-    __syncthreads();
-    reduce_max();
-  }
-  // ---- phase B on T2 rows
-  for (int tv0 = t2beg; tv0 < t2end; tv0 += TILE) {
-    __syncthreads();
-    stage_t2(tv0, true);
-    __syncthreads();
-    pv_warp(smem_u32(t2buf), tv0, t2end, t2sc);
-  }
-  // ---- phase B on the new token: rank-1 update of this thread's o^T fragments
-  if (has_new && w == 0) {
-    const float* zr = zs + (nvis - 1 - vbeg) * 8;
-    const float pa = exp2f(zr[2 * tq] - m2a), pb = exp2f(zr[2 * tq + 1] - m2b);
-    if (gq == 0) { l0 += pa; l1 += pb; }          // counted once per head (lanes 0..3)
-#pragma unroll
-    for (int mt = 0; mt < KS; ++mt) {
-      const float va = nrow[D + mt * 16 + gq], vb = nrow[D + mt * 16 + gq + 8];
-      oacc[mt][0] += pa * va;
-      oacc[mt][1] += pb * va;
-      oacc[mt][2] += pa * vb;
-      oacc[mt][3] += pb * vb;
+      l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, off);
     }
   }
 
   // ---- CTA reduction of l and o (ring reused as [NW warps][8 heads][D] fp32)
-#pragma unroll
-  for (int off = 4; off < 32; off <<= 1) {
-    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
-  }
   __syncthreads();
   float* ow = reinterpret_cast<float*>(ring);
-  if (lane < 4) {
-    red[8 * NW + w * 8 + 2 * lane] = l0;
-    red[8 * NW + w * 8 + 2 * lane + 1] = l1;
-  }
+  if (w < NW) {
+    if (lane < 4) {
+      red[8 * NW + w * 8 + 2 * lane] = l0;
+      red[8 * NW + w * 8 + 2 * lane + 1] = l1;
+    }
 #pragma unroll
-  for (int mt = 0; mt < KS; ++mt) {
-    float* o0 = ow + (w * 8 + 2 * tq) * D + mt * 16 + gq;
-    float* o1 = ow + (w * 8 + 2 * tq + 1) * D + mt * 16 + gq;
-    o0[0] = oacc[mt][0];
-    o1[0] = oacc[mt][1];
-    o0[8] = oacc[mt][2];
-    o1[8] = oacc[mt][3];
+    for (int mt = 0; mt < KS; ++mt) {
+      float* o0 = ow + (w * 8 + 2 * tq) * D + mt * 16 + gq;
+      float* o1 = ow + (w * 8 + 2 * tq + 1) * D + mt * 16 + gq;
+      o0[0] = oacc[mt][0];
+      o1[0] = oacc[mt][1];
+      o0[8] = oacc[mt][2];
+      o1[8] = oacc[mt][3];
+    }
   }
   __syncthreads();
-  for (int e = tid; e < 8 * D; e += ATT_THREADS) {
+  for (int e = tid; e < 8 * D; e += NTHR) {
     float a = ow[e];
 #pragma unroll
     for (int ww = 1; ww < NW; ++ww) a += ow[ww * 8 * D + e];
@@ -452,7 +527,7 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 3 : 2))
     const int tot = G * D;
     const int per = (tot + C - 1) / C;
     const int e1 = min(tot, (r + 1) * per);
-    for (int e = r * per + tid; e < e1; e += ATT_THREADS) {
+    for (int e = r * per + tid; e < e1; e += NTHR) {
       const int h = e / D, dd = e - h * D;
       float acc = 0.f;
       for (int c = 0; c < C; ++c) {
@@ -467,15 +542,17 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 3 : 2))
   }
   // done reading peers' shared memory: arrive now, wait before exit (score work overlaps)
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  if (fuse) {
+  if (fuse && w < NW) {
+    cp_wait<0>();                    // this thread's S_part values are in sS
     float* Sg = v.S + ((size_t)b * v.Hkv + g) * v.Nmax;
     bool bad = false;
-    for (int j = tid; j < vend - vbeg; j += ATT_THREADS) {
+    for (int j = tid; j < vend - vbeg; j += NCONS) {
+      const int pos = spos[j];
+      if (pos < 0) continue;
       const float* zr = zs + j * 8;
       float inc = 0.f;
       for (int h = 0; h < G; ++h) inc += exp2f(zr[h] - sML[h]) * sML[8 + h];
-      const int pos = spos[j];
-      Sg[pos] = Sg[pos] + inc;
+      Sg[pos] = sS[j] + inc;
       bad |= !isfinite(inc);
     }
     if (bad) atomicOr(&v.st->err, 1);
@@ -485,14 +562,14 @@ __global__ void __launch_bounds__(NW * 32, (NW == 4 ? 3 : 2))
 
 // (warps, stages) variants; DevView::variant selects one (0 = default)
 struct Variant { int nw, nst; };
-static constexpr Variant kVariants[] = {{4, 3}, {4, 4}, {8, 3}, {8, 4}, {4, 6}, {8, 6}};
+static constexpr Variant kVariants[] = {{4, 4}, {4, 6}, {8, 3}, {8, 4}, {4, 8}, {8, 6}};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 size_t attn_smem_bytes(const DevView& v) {
   const Variant vr = kVariants[v.variant];
   const int tile = 16 * vr.nw;
-  const size_t ringb = (size_t)vr.nst * tile * v.D * 2;
-  const size_t zsb = (size_t)v.chunk_max * 8 * 4 + (size_t)v.chunk_max * 4;
+  const size_t ringb = (size_t)vr.nst * tile * v.D * 2 + (2 * vr.nst + 2) * 8;
+  const size_t zsb = (size_t)v.chunk_max * 8 * 4 + (size_t)v.chunk_max * 8;
   const size_t xob = (size_t)8 * v.D * 4;
   const size_t misc = (size_t)(8 + 8 + 16 * vr.nw + 16 + 2 * v.D + tile) * 4;
   const size_t t2 = (v.cap2 > 0) ? (size_t)tile * v.D * 2 : 0;
@@ -512,13 +589,13 @@ static cudaError_t configure_k(const DevView& v) {
 template <int D, int NW, int NST>
 static cudaError_t launch_k(const DevView& v, cudaLaunchConfig_t& cfg, int layer, const void* q, const void* knew,
                             const void* vnew, void* o, int fuse) {
-  cfg.blockDim = dim3(NW * 32, 1, 1);
+  cfg.blockDim = dim3((NW + 1) * 32, 1, 1);
   return cudaLaunchKernelEx(&cfg, k_decode_attn<D, NW, NST>, v, layer, reinterpret_cast<const __nv_bfloat16*>(q),
                             reinterpret_cast<const __nv_bfloat16*>(knew), reinterpret_cast<const __nv_bfloat16*>(vnew),
                             o, fuse);
 }
 
-#define KVT_VARIANTS(X, D) X(D, 4, 3) X(D, 4, 4) X(D, 8, 3) X(D, 8, 4) X(D, 4, 6) X(D, 8, 6)
+#define KVT_VARIANTS(X, D) X(D, 4, 4) X(D, 4, 6) X(D, 8, 3) X(D, 8, 4) X(D, 4, 8) X(D, 8, 6)
 
 cudaError_t attn_configure(const DevView& v) {
   if (v.variant < 0 || v.variant >= kNumVariants) return cudaErrorInvalidValue;

@@ -123,13 +123,14 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   const size_t D = c.head_dim, B = c.num_requests, N = c.max_tokens;
   const bool stream = c.staging_tokens == 0;
   size_t s0 = o;
-  for (int i = 0; i < 2; ++i) { L.off_k0[i] = take(LBH * cap0 * D * 2); L.off_v0[i] = take(LBH * cap0 * D * 2); }
+  const size_t SL = STORE_SLACK_ROWS;
+  for (int i = 0; i < 2; ++i) { L.off_k0[i] = take((LBH * cap0 + SL) * D * 2); L.off_v0[i] = take((LBH * cap0 + SL) * D * 2); }
   L.b_t0 = o - s0; s0 = o;
   if (stream) {
-    L.off_k1[0] = L.off_k1[1] = take(2 * BH * cap1 * D * 2);
-    L.off_v1[0] = L.off_v1[1] = take(2 * BH * cap1 * D * 2);
+    L.off_k1[0] = L.off_k1[1] = take((2 * BH * cap1 + SL) * D * 2);
+    L.off_v1[0] = L.off_v1[1] = take((2 * BH * cap1 + SL) * D * 2);
   } else {
-    for (int i = 0; i < 2; ++i) { L.off_k1[i] = take(LBH * cap1 * D * 2); L.off_v1[i] = take(LBH * cap1 * D * 2); }
+    for (int i = 0; i < 2; ++i) { L.off_k1[i] = take((LBH * cap1 + SL) * D * 2); L.off_v1[i] = take((LBH * cap1 + SL) * D * 2); }
   }
   L.b_t1 = o - s0; s0 = o;
   for (int i = 0; i < 2; ++i) {
@@ -221,7 +222,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.out_fp32 = cfg->out_fp32;
   v.split = auto_split(*cfg);
   v.variant = cfg->variant;
-  v.chunk_max = round16((cfg->max_tokens + v.split - 1) / v.split);
+  v.chunk_max = round16((cfg->max_tokens + 64 + v.split - 1) / v.split) + 16;   // virtual layout pads 3 segments to 16
   for (int i = 0; i < 2; ++i) {
     v.k0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_k0[i]);
     v.v0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_v0[i]);
@@ -261,7 +262,15 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     v.hs2k = reinterpret_cast<float*>(h + 2 * rows * v.D);
     v.hs2v = reinterpret_cast<float*>(h + 2 * rows * v.D + rows * 4);
   }
-  e = attn_configure(v);
+  if (attn_smem_bytes(v) > 227 * 1024) {
+    const size_t need = attn_smem_bytes(v);
+    if (ctx->host_t1) cudaFreeHost(ctx->host_t1);
+    if (ctx->host_t2) cudaFreeHost(ctx->host_t2);
+    delete ctx;
+    return fail(nullptr, KV_TIER_E_INVAL, "decode kernel needs %zu B shared memory (> 227 KB): raise split or pick a smaller variant", need);
+  }
+  e = cudaMemset(buf->device_arena, 0, ctx->sz.device_arena);   // stale rows read as masked padding stay finite
+  if (e == cudaSuccess) e = attn_configure(v);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_step_begin, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_migrated, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_offload_done, cudaEventDisableTiming);
@@ -652,10 +661,11 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
         e = d2h(tk.data(), Ks + grp * cap * D, tk.size() * 2);
         if (e == cudaSuccess) e = d2h(tv.data(), Vs + grp * cap * D, tv.size() * 2);
         uint16_t* o16 = reinterpret_cast<uint16_t*>(out) + ((b * H + g) * cnt) * 2 * D;
-        for (int j = 0; j < cnt; ++j) {
-          memcpy(o16 + (size_t)j * 2 * D, tk.data() + (size_t)j * D, D * 2);
-          memcpy(o16 + (size_t)j * 2 * D + D, tv.data() + (size_t)j * D, D * 2);
-        }
+        for (int j = 0; j < cnt; ++j)
+          for (size_t el = 0; el < D; ++el) {     // undo the store swizzle
+            o16[(size_t)j * 2 * D + el] = tk[(size_t)j * D + swz_off(j, (int)el)];
+            o16[(size_t)j * 2 * D + D + el] = tv[(size_t)j * D + swz_off(j, (int)el)];
+          }
       }
   } else if (what == KV_TIER_X_T1_ROWS) {
     const int cnt = cnts[1];

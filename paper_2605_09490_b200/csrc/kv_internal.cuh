@@ -50,6 +50,14 @@ __device__ __forceinline__ size_t grp_of(const DevView& v, int l, int b, int g) 
   return ((size_t)l * v.B + b) * v.Hkv + g;
 }
 
+// bf16 K/V rows in the T0 store and the T1 staging are stored pre-swizzled: the 16-byte
+// chunk c of store row j sits at chunk position c ^ (j & 7).  A linear bulk copy of rows
+// into shared memory then lands in the bank-conflict-free layout ldmatrix reads.
+__host__ __device__ __forceinline__ int swz_off(int j, int e) {
+  return ((((e >> 3) ^ (j & 7)) << 3) | (e & 7));
+}
+constexpr int STORE_SLACK_ROWS = 128;   // rows of slack after each bf16 store buffer
+
 __device__ __forceinline__ float bf16_bits_to_f(uint16_t h) { return __uint_as_float(((uint32_t)h) << 16); }
 
 // fp32 -> bf16 round-to-nearest-even on the bit pattern (finite inputs)

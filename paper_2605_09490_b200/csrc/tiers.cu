@@ -40,8 +40,8 @@ __global__ void k_append(const DevView v, const int layer, const uint16_t* __res
   uint16_t* K = reinterpret_cast<uint16_t*>(v.k0[cur]);
   uint16_t* V = reinterpret_cast<uint16_t*>(v.v0[cur]);
   for (int e = threadIdx.x; e < v.D; e += blockDim.x) {
-    K[dst + e] = k[(size_t)unit * v.D + e];
-    V[dst + e] = vv[(size_t)unit * v.D + e];
+    K[dst + swz_off(row, e)] = k[(size_t)unit * v.D + e];
+    V[dst + swz_off(row, e)] = vv[(size_t)unit * v.D + e];
   }
 }
 
@@ -55,8 +55,10 @@ __global__ void k_load_prefix(const DevView v, const int layer, const uint16_t* 
   uint16_t* V = reinterpret_cast<uint16_t*>(v.v0[0]);
   const size_t tot = (size_t)n0 * v.D;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
-    K[base + e] = k[(size_t)unit * tot + e];
-    V[base + e] = vv[(size_t)unit * tot + e];
+    const int j = (int)(e / v.D), el = (int)(e % v.D);
+    const size_t dst = base + (size_t)j * v.D + swz_off(j, el);
+    K[dst] = k[(size_t)unit * tot + e];
+    V[dst] = vv[(size_t)unit * tot + e];
   }
 }
 
@@ -324,12 +326,15 @@ __device__ __forceinline__ void source_row(const DevView& v, int cur, int kv, si
   constexpr int E = D / 32;
   if (ot == T0) {
     const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v0[cur] : v.k0[cur]) + (grp * v.cap0 + orow) * D;
-    load_bits(x, s + lane * E, E);
+    load_bits(x, s + swz_off(orow, lane * E), E);
   } else if (ot == T1) {
-    const uint16_t* s;
-    if (v.stream_mode) s = reinterpret_cast<const uint16_t*>(kv ? v.hv1 : v.hk1) + (grp * v.Nmax + pos) * D;
-    else s = reinterpret_cast<const uint16_t*>(kv ? v.v1[cur] : v.k1[cur]) + (grp * v.cap1 + orow) * D;
-    load_bits(x, s + lane * E, E);
+    if (v.stream_mode) {
+      const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.hv1 : v.hk1) + (grp * v.Nmax + pos) * D;
+      load_bits(x, s + lane * E, E);   // pinned host store: canonical layout
+    } else {
+      const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v1[cur] : v.k1[cur]) + (grp * v.cap1 + orow) * D;
+      load_bits(x, s + swz_off(orow, lane * E), E);
+    }
   } else {
     const int8_t* c = (kv ? v.c2v[cur] : v.c2k[cur]) + (grp * v.cap2 + orow) * D + lane * E;
     const float sc = (kv ? v.s2v[cur] : v.s2k[cur])[grp * v.cap2 + orow];
@@ -407,7 +412,7 @@ __global__ void __launch_bounds__(256) k_migrate(const DevView v, const int cur)
         uint16_t* dst = T == 0
             ? reinterpret_cast<uint16_t*>(kv ? v.v0[nxt] : v.k0[nxt]) + (grp * v.cap0 + j) * D
             : reinterpret_cast<uint16_t*>(kv ? v.v1[nxt] : v.k1[nxt]) + (grp * v.cap1 + j) * D;
-        store_bits(dst + lane * E, x, E);
+        store_bits(dst + swz_off(j, lane * E), x, E);
       }
     }
   }
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(256) k_offload_host(const DevView v, const int
         uint16_t x[E];
         if (!v.stream_mode) {
           const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v1[nxt] : v.k1[nxt]) + (grp * v.cap1 + j) * D;
-          load_bits(x, s + lane * E, E);
+          load_bits(x, s + swz_off(j, lane * E), E);
         } else {
           source_row<D>(v, cur, kv, grp, ot, orow, pos, lane, x);
         }
@@ -486,7 +491,7 @@ __global__ void __launch_bounds__(256) k_prefetch(const DevView v, const int lay
       uint16_t* d = reinterpret_cast<uint16_t*>(kv ? v.v1[0] : v.k1[0]) + (sg * v.cap1 + j) * D;
       uint16_t x[E];
       load_bits(x, s + lane * E, E);
-      store_bits(d + lane * E, x, E);
+      store_bits(d + swz_off(j, lane * E), x, E);
     }
   }
 }
