@@ -123,22 +123,13 @@ def timed(fn, stream, n):
 
 
 def _max_over_ranks(x):
-    import torch
-    import torch.distributed as dist
-    if not (dist.is_available() and dist.is_initialized()):
-        return x
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2605_09490_b200.dist import max_over_ranks
+    return max_over_ranks(x)
 
 
 def _barrier_sync():
-    import torch
-    import torch.distributed as dist
-    torch.cuda.synchronize()
-    if dist.is_available() and dist.is_initialized():
-        dist.barrier()
-    torch.cuda.synchronize()
+    from paper_2605_09490_b200.dist import barrier_sync
+    barrier_sync()
 
 
 # ------------------------------------------------------------------ CPU oracle leg
@@ -213,7 +204,8 @@ def main():
     w = H.workload(args.config, hbm_bp=args.hbm, evict_bp=args.evict, steps=W + K + E + 1)
     dev = f"cuda:{local}"
     peaks = _peaks()
-    seed_off = 1000 * rank
+    from paper_2605_09490_b200.dist import shard_plan
+    seed_off, _ = shard_plan(world, rank, 1)
 
     # ---- leg 1: tiered, differential staging, device-resident inputs -> value
     run = H.TieredDecode(w, device=dev, out_fp32=False, split=args.split, seed_offset=seed_off)

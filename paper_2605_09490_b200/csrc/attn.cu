@@ -61,6 +61,12 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ int ru16(int x) { return (x + 15) & ~15; }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr int NTRACE = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -129,6 +135,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
   const int gq = lane >> 2, tq = lane & 3;
   const int G = v.G;
 
+  unsigned long long* tr = v.trace ? v.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * NTRACE : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = gtimer();
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + NST * TILEB);   // full[NST], empty[NST]
@@ -230,6 +238,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
   }
   // ---------------------------------------------------------------- dependent inputs
   pdl_wait();
+  if (tr && tid == 0) tr[1] = gtimer();
   if (w == NW) {
     // the producer warp only joins the CTA-wide barriers below
   } else {
@@ -434,6 +443,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
         reduce_max();
       }
       mbar_wait(full0 + 8 * s2, (i / NST) & 1);
+      if (tr && tid == 0 && i == 0) tr[2] = gtimer();
+      if (tr && tid == 0 && i == nt) tr[3] = gtimer();
       const uint32_t sbase = ring_s + s2 * TILEB;
       if (i < nt) {
         qk_warp(sbase, vbeg + i * TILE, aend, nullptr, false);
@@ -478,6 +489,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
   }
 
   // ---- CTA reduction of l and o (ring reused as [NW warps][8 heads][D] fp32)
+  if (tr && tid == 0) tr[4] = gtimer();
   __syncthreads();
   float* ow = reinterpret_cast<float*>(ring);
   if (w < NW) {
@@ -511,6 +523,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
 
   // ---- cluster merge through distributed shared memory
   cluster.sync();
+  if (tr && tid == 0) tr[5] = gtimer();
   if (tid < 8) {
     float M = -INFINITY;
     for (int c = 0; c < C; ++c) M = fmaxf(M, cluster.map_shared_rank(xm, c)[tid]);
@@ -541,6 +554,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
     }
   }
   // done reading peers' shared memory: arrive now, wait before exit (score work overlaps)
+  if (tr && tid == 0) tr[6] = gtimer();
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   if (fuse && w < NW) {
     cp_wait<0>();                    // this thread's S_part values are in sS
@@ -558,6 +572,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
     if (bad) atomicOr(&v.st->err, 1);
   }
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (tr && tid == 0) tr[7] = gtimer();
 }
 
 // (warps, stages) variants; DevView::variant selects one (0 = default)

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -35,6 +36,7 @@ struct kv_tier_ctx {
   bool slot_recorded[2] = {false, false};   // ev_slot_free[x] recorded within the open step
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
+  unsigned long long* trace = nullptr;     // debug timeline buffer (KVTIER_TRACE=1)
   std::string err;
 };
 
@@ -262,6 +264,10 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     v.hs2k = reinterpret_cast<float*>(h + 2 * rows * v.D);
     v.hs2v = reinterpret_cast<float*>(h + 2 * rows * v.D + rows * 4);
   }
+  if (getenv("KVTIER_TRACE") && atoi(getenv("KVTIER_TRACE")) > 0) {
+    const size_t tb = (size_t)v.split * v.B * v.Hkv * 8 * sizeof(unsigned long long);
+    if (cudaMalloc(&ctx->trace, tb) == cudaSuccess) { cudaMemset(ctx->trace, 0, tb); v.trace = ctx->trace; }
+  }
   if (attn_smem_bytes(v) > 227 * 1024) {
     const size_t need = attn_smem_bytes(v);
     if (ctx->host_t1) cudaFreeHost(ctx->host_t1);
@@ -301,6 +307,7 @@ kv_tier_status kv_tier_destroy(kv_tier_ctx* ctx) {
   for (auto& ev : ctx->ev_prefetched) if (ev) cudaEventDestroy(ev);
   if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
   if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  if (ctx->trace) cudaFree(ctx->trace);
   delete ctx;
   return KV_TIER_OK;
 }
@@ -710,6 +717,16 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
       }
   }
   return cuda_check(ctx, e, "export");
+}
+
+kv_tier_status kv_tier_debug_trace(kv_tier_ctx* ctx, uint64_t* host_dst, size_t n) {
+  if (!ctx || !host_dst) return fail(ctx, KV_TIER_E_INVAL, "null arg");
+  const size_t need = (size_t)ctx->v.split * ctx->v.B * ctx->v.Hkv * 8;
+  if (!ctx->trace) return fail(ctx, KV_TIER_E_STATE, "tracing off (set KVTIER_TRACE=1 before kv_tier_init)");
+  if (n != need) return fail(ctx, KV_TIER_E_INVAL, "trace needs %zu entries", need);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(host_dst, ctx->trace, need * 8, cudaMemcpyDeviceToHost);
+  return cuda_check(ctx, e, "trace");
 }
 
 kv_tier_status kv_tier_import_scores(kv_tier_ctx* ctx, const float* host_S, size_t bytes) {

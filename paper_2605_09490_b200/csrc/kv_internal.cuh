@@ -30,6 +30,7 @@ struct DevView {
   int split;            // CTAs per (b, g) cluster
   int chunk_max;        // max tokens per CTA (logit buffer rows)
   int variant;          // decode-attention kernel variant (warps x pipeline stages)
+  unsigned long long* trace;   // debug: per-CTA %globaltimer checkpoints (null = off)
   __nv_bfloat16* k0[2]; __nv_bfloat16* v0[2];        // T0 store  [L][B][Hkv][cap0][D]
   __nv_bfloat16* k1[2]; __nv_bfloat16* v1[2];        // T1 staging [L][B][Hkv][cap1][D] (stream: [2][B][Hkv][cap1][D] in k1[0]/v1[0])
   int8_t* c2k[2]; int8_t* c2v[2];                      // T2 codes  [L][B][Hkv][cap2][D]

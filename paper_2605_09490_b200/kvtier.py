@@ -73,6 +73,7 @@ _SIGS = {
     "kv_tier_export_size": [C.c_void_p, C.c_int32, C.POINTER(C.c_size_t)],
     "kv_tier_export": [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t],
     "kv_tier_import_scores": [C.c_void_p, C.c_void_p, C.c_size_t],
+    "kv_tier_debug_trace": [C.c_void_p, C.c_void_p, C.c_size_t],
     "kv_tier_last_error": [C.c_void_p],
     "kv_tier_version": [],
 }
@@ -238,6 +239,22 @@ class KvTier:
         if what == X_T2_CODES:
             return buf.view(np.int8).reshape(B, H, -1, 2, D)
         return buf.view(np.float32).reshape(B, H, -1, 2)
+
+    def debug_trace(self):
+        """[split*B*H_kv][8] %globaltimer ns checkpoints of the last decode_attention (KVTIER_TRACE=1)."""
+        n = self.cfg.num_requests * self.cfg.num_kv_heads * 8 * max(1, self._split())
+        buf = np.zeros(n, dtype=np.uint64)
+        _check(load().kv_tier_debug_trace(self.ctx, buf.ctypes.data_as(C.c_void_p), n), self.ctx)
+        return buf.reshape(-1, 8)
+
+    def _split(self):
+        if self.cfg.split:
+            return self.cfg.split
+        units = self.cfg.num_requests * self.cfg.num_kv_heads
+        s = max(1, min(8, (2 * 148 + units - 1) // units))
+        while s < 16 and (self.cfg.max_tokens + s - 1) // s > 2048:
+            s += 1
+        return s
 
     def import_scores(self, S):
         S = np.ascontiguousarray(S, dtype=np.float32)

@@ -1,0 +1,39 @@
+"""Timeline of one decode_attention launch per layer (KVTIER_TRACE=1): per-CTA phase durations.
+
+    KVTIER_TRACE=1 python scripts/trace_attn.py --split 4 --variant 3
+"""
+import argparse
+import json
+import os
+import sys
+
+os.environ.setdefault("KVTIER_TRACE", "1")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2605_09490_b200 import harness as H  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="7b")
+ap.add_argument("--split", type=int, default=0)
+ap.add_argument("--variant", type=int, default=0)
+ap.add_argument("--graph", type=int, default=1)
+a = ap.parse_args()
+w = H.workload(a.config, steps=4)
+run = H.TieredDecode(w, out_fp32=False, split=a.split, variant=a.variant)
+if a.graph:
+    run.capture()
+for _ in range(3):
+    run.step()
+run.sync()
+tr = run.kv.debug_trace().astype(np.int64)        # last layer of the last step
+names = ["start", "pdl_wait", "first_tile", "K_done", "V_done", "merge_sync", "o_written", "end"]
+t0 = tr[:, 0].min()
+rel = (tr - t0) / 1e3
+out = {"config": a.config, "split": a.split, "variant": a.variant, "ctas": int(tr.shape[0])}
+for i, n in enumerate(names):
+    col = rel[:, i]
+    out[n] = [round(float(col.min()), 2), round(float(np.median(col)), 2), round(float(col.max()), 2)]
+print(json.dumps(out))
+run.close()
