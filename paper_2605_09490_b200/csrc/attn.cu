@@ -488,8 +488,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
     }
   }
 
-  // ---- CTA reduction of l and o (ring reused as [NW warps][8 heads][D] fp32)
+  // ---- CTA reduction of l and o (ring reused as [NW warps][8 heads][D+4] fp32, padded rows)
   if (tr && tid == 0) tr[4] = gtimer();
+  constexpr int OWS = D + 4;
   __syncthreads();
   float* ow = reinterpret_cast<float*>(ring);
   if (w < NW) {
@@ -499,8 +500,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
     }
 #pragma unroll
     for (int mt = 0; mt < KS; ++mt) {
-      float* o0 = ow + (w * 8 + 2 * tq) * D + mt * 16 + gq;
-      float* o1 = ow + (w * 8 + 2 * tq + 1) * D + mt * 16 + gq;
+      float* o0 = ow + (w * 8 + 2 * tq) * OWS + mt * 16 + gq;
+      float* o1 = o0 + OWS;
       o0[0] = oacc[mt][0];
       o1[0] = oacc[mt][1];
       o0[8] = oacc[mt][2];
@@ -508,10 +509,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
     }
   }
   __syncthreads();
-  for (int e = tid; e < 8 * D; e += NTHR) {
-    float a = ow[e];
+  for (int e = tid; e < G * D; e += NTHR) {
+    const int h = e / D, dd = e - h * D;
+    float a = ow[h * OWS + dd];
 #pragma unroll
-    for (int ww = 1; ww < NW; ++ww) a += ow[ww * 8 * D + e];
+    for (int ww = 1; ww < NW; ++ww) a += ow[(ww * 8 + h) * OWS + dd];
     xo[e] = a;
   }
   if (tid < 8) {
@@ -521,19 +523,34 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
     xl[tid] = a;
   }
 
-  // ---- cluster merge through distributed shared memory
+  // ---- cluster merge through distributed shared memory (all remote reads issued in parallel)
   cluster.sync();
   if (tr && tid == 0) tr[5] = gtimer();
+  float* gm = ow;                 // [16][8] peers' m    (ring is free now)
+  float* gl = ow + 128;           // [16][8] peers' l
+  float* gf = ow + 256;           // [16][8] merge factors exp2(m_c - M) / L
+  if (tid < 8 * C) {
+    const int c = tid >> 3, h = tid & 7;
+    gm[tid] = cluster.map_shared_rank(xm, c)[h];
+    gl[tid] = cluster.map_shared_rank(xl, c)[h];
+  }
+  __syncthreads();
   if (tid < 8) {
     float M = -INFINITY;
-    for (int c = 0; c < C; ++c) M = fmaxf(M, cluster.map_shared_rank(xm, c)[tid]);
+    for (int c = 0; c < C; ++c) M = fmaxf(M, gm[c * 8 + tid]);
     float Ls = 0.f;
     for (int c = 0; c < C; ++c) {
-      const float mc = cluster.map_shared_rank(xm, c)[tid];
-      if (mc != -INFINITY) Ls += cluster.map_shared_rank(xl, c)[tid] * exp2f(mc - M);
+      const float mc = gm[c * 8 + tid];
+      if (mc != -INFINITY) Ls += gl[c * 8 + tid] * exp2f(mc - M);
     }
     sML[tid] = M;
     sML[8 + tid] = 1.0f / Ls;
+  }
+  __syncthreads();
+  if (tid < 8 * C) {
+    const int h = tid & 7;
+    const float mc = gm[tid];
+    gf[tid] = mc == -INFINITY ? 0.f : exp2f(mc - sML[h]) * sML[8 + h];
   }
   __syncthreads();
   {
@@ -541,16 +558,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
     const int per = (tot + C - 1) / C;
     const int e1 = min(tot, (r + 1) * per);
     for (int e = r * per + tid; e < e1; e += NTHR) {
-      const int h = e / D, dd = e - h * D;
+      const int h = e / D;
+      float part[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < C) part[c] = cluster.map_shared_rank(xo, c)[e];
       float acc = 0.f;
-      for (int c = 0; c < C; ++c) {
-        const float mc = cluster.map_shared_rank(xm, c)[h];
-        if (mc != -INFINITY) acc += exp2f(mc - sML[h]) * cluster.map_shared_rank(xo, c)[h * D + dd];
-      }
-      const float val = acc * sML[8 + h];
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < C) acc += gf[c * 8 + h] * part[c];
+      const int dd = e - h * D;
       const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
-      if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = val;
-      else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(val);
+      if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = acc;
+      else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(acc);
     }
   }
   // done reading peers' shared memory: arrive now, wait before exit (score work overlaps)
@@ -577,7 +597,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
 
 // (warps, stages) variants; DevView::variant selects one (0 = default)
 struct Variant { int nw, nst; };
-static constexpr Variant kVariants[] = {{4, 4}, {4, 6}, {8, 3}, {8, 4}, {4, 8}, {8, 6}};
+static constexpr Variant kVariants[] = {{4, 4}, {4, 6}, {8, 3}, {8, 4}, {4, 5}, {8, 6}};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 size_t attn_smem_bytes(const DevView& v) {
@@ -610,7 +630,7 @@ static cudaError_t launch_k(const DevView& v, cudaLaunchConfig_t& cfg, int layer
                             o, fuse);
 }
 
-#define KVT_VARIANTS(X, D) X(D, 4, 4) X(D, 4, 6) X(D, 8, 3) X(D, 8, 4) X(D, 4, 8) X(D, 8, 6)
+#define KVT_VARIANTS(X, D) X(D, 4, 4) X(D, 4, 6) X(D, 8, 3) X(D, 8, 4) X(D, 4, 5) X(D, 8, 6)
 
 cudaError_t attn_configure(const DevView& v) {
   if (v.variant < 0 || v.variant >= kNumVariants) return cudaErrorInvalidValue;
