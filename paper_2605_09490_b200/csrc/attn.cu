@@ -1,28 +1,31 @@
 // a1 + a3 + a4: fused new-token append, GQA decode attention over the visible tiers, and the
 // cumulative score update (Eq. 1, Eq. 3, Prop. 1).
 //
-// One thread-block cluster of C CTAs per (request b, kv head g).  The visible rows of the
-// unit are laid out virtually as [T0 rows except the new token | pad | T1 staging | pad |
-// T2 int8 | pad | new token] (segments start at multiples of 16); CTA r of the cluster owns
-// a contiguous 1/C chunk.  Warp NW is the producer: it streams the chunk's K tiles, then its
-// V tiles, with 1-D bulk async copies (cp.async.bulk, one or two per tile) into an NST-deep
-// shared-memory ring guarded by full/empty mbarriers.  Rows are stored pre-swizzled in HBM
-// (16-B chunk c of store row j at c ^ (j & 7)), so a linear copy is the conflict-free layout.
+// One thread-block cluster of C CTAs per unit (request b, kv head g).  The unit's visible rows
+// are laid out virtually as [T0 rows except the new token | pad | T1 staging | pad | T2 int8 |
+// pad | new token], segments starting at multiples of 16, cut into tiles of TILE tokens.
 //
-//   prologue  (before griddepcontrol.wait, overlaps the previous layer's kernel under PDL)
-//            counters, the first tiles in flight, positions of the chunk -> SMEM
-//   phase A  K tiles -> S^T = K q^T on the tensor cores
-//            (mma.sync m16n8k16 bf16, swap-AB: tokens = M, heads = N = 8); logits (log2
-//            domain) stay in SMEM for the whole chunk; running max per head
-//   phase B  V tiles -> p = exp2(z - m_local) -> o^T += V^T p^T (movmatrix.trans turns the
-//            C fragment into the B fragment; ldmatrix.trans reads V^T)
-//   merge    (m, l, o) of the C CTAs through distributed shared memory; CTA r writes 1/C of o
-//   score    exact p_i = exp2(z_i - M)/L from the SMEM logits; S_part[b][g][pos_i] += sum over
-//            the group's heads (one fp32 add per layer, AMB-14); each (b,g,pos) belongs to one
-//            CTA -> no atomics, bit-reproducible
+//   producer warp   claims the next tile of its unit from a cluster-shared counter (DSMEM
+//                   atomic: CTAs that stream faster take more tiles, so the cluster finishes
+//                   together) and streams the tile's K rows and V rows with 1-D bulk async
+//                   copies (cp.async.bulk) into an NST-deep shared-memory ring guarded by
+//                   full/empty mbarriers.  Rows are stored pre-swizzled in HBM (16-B chunk c
+//                   of store row j at c ^ (j & 7)), so a linear copy is the conflict-free layout.
+//   consumer warps  each owns 16 rows of a tile: S^T = K q^T on the tensor cores (mma.sync
+//                   m16n8k16 bf16, swap-AB: tokens = M, the G <= 8 heads of the group = N),
+//                   per-warp online softmax in fp32, o^T += V^T p^T (movmatrix.trans turns the
+//                   C fragment into the B fragment).  Logits (log2 domain) go to an
+//                   L2-resident buffer for the score update.
+//   merge           warps -> CTA (shared memory) -> cluster (distributed shared memory, all
+//                   remote reads issued in parallel); CTA r writes 1/C of o; rank 0 publishes
+//                   the global (max, 1/sum) per head.
+//   score warp      meanwhile applies the PREVIOUS layer's cumulative score update:
+//                   S_part[b][g][pos] += sum_{h in g} exp2(z - M_h) / L_h (one fp32 add per
+//                   layer in layer order, AMB-14; every (b, g, pos) written by one thread ->
+//                   no atomics, bit-reproducible).  The last layer's update runs in end_step.
 //
-// HBM traffic per launch = algorithmic bytes: every visible K/V row once, q, o, the new row
-// (read + written), and 8 B of score read+write per visible token per kv head.
+// HBM traffic per launch = algorithmic bytes: every visible K/V row once, q, o, the new row,
+// and the 8 B score read+write per visible token per kv head (of the previous layer).
 #include "kv_internal.cuh"
 #include <cooperative_groups.h>
 
@@ -115,17 +118,77 @@ __device__ __forceinline__ uint32_t i8pair_to_bf16x2(uint32_t word, int k) {
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
+__device__ __forceinline__ int atomic_add_cluster(int* local_ptr_in_rank0, int val) {
+  // DSMEM atomic on the rank-0 CTA's shared counter
+  cg::cluster_group cluster = cg::this_cluster();
+  int* p = cluster.map_shared_rank(local_ptr_in_rank0, 0);
+  return atomicAdd(p, val);
+}
+
+// Virtual-token bookkeeping shared by the decode kernel and the score pass.
+struct Seg {
+  int n0o, n1, n2, a1, a2, a3, nvirt;
+  __device__ __forceinline__ void init(const int* cn) {
+    n0o = cn[0] - 1;
+    n1 = cn[1];
+    n2 = cn[2];
+    a1 = ru16(n0o);
+    a2 = ru16(a1 + n1);
+    a3 = ru16(a2 + n2);
+    nvirt = a3 + 1;
+  }
+  __device__ __forceinline__ bool bf16_valid(int t) const { return t < n0o || (t >= a1 && t < a1 + n1); }
+  __device__ __forceinline__ bool valid(int t) const {
+    return t < n0o || (t >= a1 && t < a1 + n1) || (t >= a2 && t < a2 + n2) || t == a3;
+  }
+  // position of virtual token t (valid t only)
+  __device__ __forceinline__ int pos(const DevView& v, int cur, int b, int t) const {
+    if (t < n0o) return v.idx[cur][0][(size_t)b * v.cap0 + t];
+    if (t < a2) return v.idx[cur][1][(size_t)b * v.cap1 + (t - a1)];
+    if (t < a3) return v.idx[cur][2][(size_t)b * v.cap2 + (t - a2)];
+    return v.idx[cur][0][(size_t)b * v.cap0 + n0o];
+  }
+};
+
+// Score pass of one layer over virtual tokens [i0, i1) of the flattened (unit, token) space
+// (called by the score warp of the next layer's kernel and by the end-of-step flush).
+__device__ __forceinline__ void score_range(const DevView& v, const Seg& sg, int cur, int zpar, long long i0,
+                                            long long i1, int lane0, int stride, bool& bad) {
+  const float* zb = v.zbuf + (size_t)zpar * v.B * v.Hkv * v.zrows * 8;
+  const float* ML = v.ml + (size_t)zpar * v.B * v.Hkv * 16;
+  for (long long i = i0 + lane0; i < i1; i += stride) {
+    const int u = (int)(i / sg.nvirt), t = (int)(i - (long long)u * sg.nvirt);
+    if (!sg.valid(t)) continue;
+    const int b = u / v.Hkv, g = u - b * v.Hkv;
+    const float* z = zb + ((size_t)u * v.zrows + t) * 8;
+    const float4 z0 = *reinterpret_cast<const float4*>(z);
+    const float4 z1 = *reinterpret_cast<const float4*>(z + 4);
+    const float* ml = ML + (size_t)u * 16;
+    const float zz[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
+    float inc = 0.f;
+    for (int h = 0; h < v.G; ++h) inc += exp2f(zz[h] - ml[h]) * ml[8 + h];
+    float* S = v.S + ((size_t)b * v.Hkv + g) * v.Nmax + sg.pos(v, cur, b, t);
+    *S = *S + inc;
+    bad |= !isfinite(inc);
+  }
+}
+
 template <int D, int NW, int NST>
-__global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
+__global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     k_decode_attn(const DevView v, const int layer, const __nv_bfloat16* __restrict__ q,
                   const __nv_bfloat16* __restrict__ knew, const __nv_bfloat16* __restrict__ vnew,
-                  void* __restrict__ o, const int fuse) {
+                  void* __restrict__ o, const int zpar, const int prev_zpar) {
+  // zpar: logits buffer of this launch (-1: no score update); prev_zpar: pending score pass
+  // of the previous launch to apply in the background (-1: none)
   constexpr int NCONS = NW * 32;              // consumer threads
-  constexpr int NTHR = NCONS + 32;            // + producer warp
+  constexpr int NTHR = NCONS + 64;            // + producer warp + score warp
+  constexpr int WPROD = NW, WSCORE = NW + 1;
   constexpr int TILE = NW * 16;
   constexpr int ROWB = D * 2;
   constexpr int TILEB = TILE * ROWB;
+  constexpr int STAGEB = 2 * TILEB;           // K tile + V tile
   constexpr int KS = D / 16;
+  constexpr int OWS = D + 4;
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();
   const int r = (int)cluster.block_rank();
@@ -134,40 +197,33 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int G = v.G;
-
   unsigned long long* tr = v.trace ? v.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * NTRACE : nullptr;
-  if (tr && threadIdx.x == 0) tr[0] = gtimer();
+  if (tr && tid == 0) tr[0] = gtimer();
+
   extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* ring = smem;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + NST * TILEB);   // full[NST], empty[NST]
-  float* zs = reinterpret_cast<float*>(bars + 2 * NST + 2);     // [chunk_max][8] logits (log2)
-  int* spos = reinterpret_cast<int*>(zs + (size_t)v.chunk_max * 8);   // [chunk_max] positions (-1: pad)
-  float* sS = reinterpret_cast<float*>(spos + v.chunk_max);     // [chunk_max] S_part values
-  float* xo = sS + v.chunk_max;                                 // [8][D]  exchange: o partial
-  float* xm = xo + 8 * D;                                       // [8]     exchange: max (log2)
-  float* xl = xm + 8;                                           // [8]     exchange: sum
-  float* red = xl + 8;                                          // [2][NW][8] warp max / warp l
-  float* sML = red + 16 * NW;                                   // [16] merged M, 1/L
-  float* nrow = sML + 16;                                       // [2][D] new token K, V (fp32)
-  float* t2sc = nrow + 2 * D;                                   // [TILE] T2 row scales
-  unsigned char* t2buf = reinterpret_cast<unsigned char*>(t2sc + TILE);   // [TILE][D] bf16
+  unsigned char* ring = smem;                                             // [NST][K tile | V tile]
+  unsigned char* t2w = ring + NST * STAGEB;                               // [NW][16][D] bf16 (T2 only)
+  unsigned long long* bars =
+      reinterpret_cast<unsigned long long*>(t2w + (v.cap2 > 0 ? NW * 16 * ROWB : 0));   // full, empty
+  int* stile = reinterpret_cast<int*>(bars + 2 * NST);                    // [NST] tile of each stage
+  int* sctr = stile + NST;                                                // cluster tile counter (rank 0)
+  float* xo = reinterpret_cast<float*>(sctr + 4);                         // [8][D] exchange: o partial
+  float* xm = xo + 8 * D;                                                 // [8]  exchange: max (log2)
+  float* xl = xm + 8;                                                     // [8]  exchange: sum
+  float* redm = xl + 8;                                                   // [NW][8] warp max
+  float* redl = redm + 8 * NW;                                            // [NW][8] warp sum
+  float* sML = redl + 8 * NW;                                             // [16] merged M, 1/L
+  float* nrow = sML + 16;                                                 // [2][D] new token K, V
+  float* zn = nrow + 2 * D;                                               // [8] new token logits
 
   // ---------------------------------------------------------------- prologue (pre-PDL-wait)
   const int cur = v.st->cur;
-  const int* cn = v.cnt[cur] + b * CNT_STRIDE;
-  const int n0 = cn[0], n1 = cn[1], n2 = cn[2];
-  const int n0o = n0 - 1;                                  // T0 rows before the new token
-  const int a1 = ru16(n0o), a2 = ru16(a1 + n1), a3 = ru16(a2 + n2);   // segment starts
-  const int nvirt = a3 + 1;
-  const int chunk = ru16((nvirt + C - 1) / C);
-  const int vbeg = min(r * chunk, nvirt), vend = min(vbeg + chunk, nvirt);
-  const int aend = min(vend, a2);                          // bf16 tiles cover [vbeg, aend)
-  const int t2beg = max(vbeg, a2), t2end = min(vend, a2 + n2);
-  const bool has_new = vbeg <= a3 && a3 < vend;
-  const int nb = max(0, aend - vbeg);
-  const int nt = (nb + TILE - 1) / TILE;
-  const int total = 2 * nt;
-  auto bf16_valid = [&](int t) { return t < n0o || (t >= a1 && t < a1 + n1); };
+  Seg sg;
+  sg.init(v.cnt[cur] + b * CNT_STRIDE);
+  const int ntb = (sg.a2 + TILE - 1) / TILE;                 // bf16 tiles [0, a2)
+  const int nt2 = (sg.n2 + TILE - 1) / TILE;                 // int8 tiles [a2, a2 + n2)
+  const int ntiles = ntb + nt2;
+  const bool has_new = r == 0;                               // rank 0 handles the new token
 
   const size_t grp = grp_of(v, layer, b, g);
   const __nv_bfloat16* K0 = v.k0[cur] + grp * v.cap0 * D;
@@ -175,9 +231,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
   const __nv_bfloat16* K1;
   const __nv_bfloat16* V1;
   if (v.stream_mode) {
-    const size_t sg = ((size_t)(layer & 1) * v.B + b) * v.Hkv + g;
-    K1 = v.k1[0] + sg * v.cap1 * D;
-    V1 = v.v1[0] + sg * v.cap1 * D;
+    const size_t sgi = ((size_t)(layer & 1) * v.B + b) * v.Hkv + g;
+    K1 = v.k1[0] + sgi * v.cap1 * D;
+    V1 = v.v1[0] + sgi * v.cap1 * D;
   } else {
     K1 = v.k1[cur] + grp * v.cap1 * D;
     V1 = v.v1[cur] + grp * v.cap1 * D;
@@ -190,79 +246,84 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
       mbar_init(full0 + 8 * s2, 1);
       mbar_init(empty0 + 8 * s2, NW);
     }
+    *sctr = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  __syncthreads();
+  // cluster barrier #1 (split): counter initialised before any producer claims
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 
-  if (w == NW) {
-    // ============================ producer warp ============================
+  if (w == WPROD) {
+    // ============================ producer ============================
     if (lane == 0) {
-      for (int i = 0; i < total; ++i) {
+      for (int i = 0;; ++i) {
         const int s2 = i % NST;
         if (i >= NST) mbar_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
-        const bool isV = i >= nt;
-        const int ts = vbeg + (isV ? i - nt : i) * TILE;
-        const uint32_t full = full0 + 8 * s2, dst = ring_s + s2 * TILEB;
-        mbar_expect_tx(full, TILEB);
-        if (ts < a1) {   // T0 rows [ts, min(ts+TILE, a1)) (pad rows beyond n0o are stale but finite)
-          const int nrows = min(TILE, a1 - ts);
-          bulk_g2s(dst, (isV ? V0 : K0) + (size_t)ts * D, nrows * ROWB, full);
-          if (nrows < TILE)
-            bulk_g2s(dst + nrows * ROWB, isV ? V1 : K1, (TILE - nrows) * ROWB, full);
-        } else {
-          bulk_g2s(dst, (isV ? V1 : K1) + (size_t)(ts - a1) * D, TILEB, full);
+        const int k = atomic_add_cluster(sctr, 1);
+        const uint32_t full = full0 + 8 * s2, dst = ring_s + s2 * STAGEB;
+        if (k >= ntiles) {
+          stile[s2] = -1;
+          mbar_arrive(full);          // sentinel stage (no data)
+          break;
+        }
+        stile[s2] = k;
+        if (k < ntb) {
+          const int ts = k * TILE;
+          mbar_expect_tx(full, STAGEB);
+          if (ts < sg.a1) {           // T0 rows (pad rows beyond n0o are stale but finite)
+            const int nrows = min(TILE, sg.a1 - ts);
+            bulk_g2s(dst, K0 + (size_t)ts * D, nrows * ROWB, full);
+            bulk_g2s(dst + TILEB, V0 + (size_t)ts * D, nrows * ROWB, full);
+            if (nrows < TILE) {
+              bulk_g2s(dst + nrows * ROWB, K1, (TILE - nrows) * ROWB, full);
+              bulk_g2s(dst + TILEB + nrows * ROWB, V1, (TILE - nrows) * ROWB, full);
+            }
+          } else {
+            bulk_g2s(dst, K1 + (size_t)(ts - sg.a1) * D, TILEB, full);
+            bulk_g2s(dst + TILEB, V1 + (size_t)(ts - sg.a1) * D, TILEB, full);
+          }
+        } else {                      // T2: int8 codes + fp32 scales (canonical layout)
+          const int j0 = (k - ntb) * TILE;
+          const int8_t* CK = v.c2k[cur] + (grp * v.cap2 + j0) * D;
+          const int8_t* CV = v.c2v[cur] + (grp * v.cap2 + j0) * D;
+          const float* SK = v.s2k[cur] + grp * v.cap2 + j0;
+          const float* SV = v.s2v[cur] + grp * v.cap2 + j0;
+          mbar_expect_tx(full, 2 * (TILE * D + TILE * 4));
+          bulk_g2s(dst, CK, TILE * D, full);
+          bulk_g2s(dst + TILE * D, SK, TILE * 4, full);
+          bulk_g2s(dst + TILEB, CV, TILE * D, full);
+          bulk_g2s(dst + TILEB + TILE * D, SV, TILE * 4, full);
         }
       }
     }
     __syncwarp();
-    pdl_trigger();
-  } else {
-    // ============================ consumer warps ============================
-    // positions of the chunk (for the score update), cp.async: no stall
-    if (fuse) {
-      const int* I0 = v.idx[cur][0] + (size_t)b * v.cap0;
-      const int* I1 = v.idx[cur][1] + (size_t)b * v.cap1;
-      const int* I2 = v.idx[cur][2] + (size_t)b * v.cap2;
-      for (int j = tid; j < vend - vbeg; j += NCONS) {
-        const int t = vbeg + j;
-        const int* src = t < n0o ? I0 + t
-                       : (t >= a1 && t < a1 + n1) ? I1 + (t - a1)
-                       : (t >= a2 && t < a2 + n2) ? I2 + (t - a2)
-                       : t == a3 ? I0 + n0o : nullptr;
-        if (src) cp_async4(smem_u32(spos + j), src);
-        else spos[j] = -1;
-      }
-      cp_commit();
-    }
-    pdl_trigger();
   }
+  pdl_trigger();
   // ---------------------------------------------------------------- dependent inputs
   pdl_wait();
   if (tr && tid == 0) tr[1] = gtimer();
-  if (w == NW) {
-    // the producer warp only joins the CTA-wide barriers below
-  } else {
-    if (fuse) {   // S_part values of the chunk's tokens (written by the previous layer)
-      cp_wait<0>();
-      float* Sg = v.S + ((size_t)b * v.Hkv + g) * v.Nmax;
-      for (int j = tid; j < vend - vbeg; j += NCONS) {
-        const int pos = spos[j];
-        if (pos >= 0) cp_async4(smem_u32(sS + j), Sg + pos);
-      }
-      cp_commit();
+
+  bool bad = false;
+  if (w == WSCORE) {
+    // ============================ score warp: previous layer's S_part update ============================
+    if (prev_zpar >= 0) {
+      const long long tot = (long long)v.B * v.Hkv * sg.nvirt;
+      const long long ncta = (long long)gridDim.x * gridDim.y;
+      const long long cid = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+      const long long per = (tot + ncta - 1) / ncta;
+      score_range(v, sg, cur, prev_zpar, cid * per, min(tot, (cid + 1) * per), lane, 32, bad);
     }
   }
 
-  uint32_t qf[KS][2];
-  const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));   // log2(e)/sqrt(d)
-  float mx0 = -INFINITY, mx1 = -INFINITY;    // running max, heads 2tq, 2tq+1
-  float l0 = 0.f, l1 = 0.f;
+  float mxa = -INFINITY, mxb = -INFINITY;   // per-warp running max, heads 2tq, 2tq+1 (log2)
+  float la = 0.f, lb = 0.f;                 // per-thread partial sums
   float oacc[KS][4];
 #pragma unroll
   for (int mt = 0; mt < KS; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
-  float m2a = 0.f, m2b = 0.f;   // CTA max for heads 2tq, 2tq+1
 
   if (w < NW) {
+    // ============================ consumers ============================
+    uint32_t qf[KS][2];
     {
       const __nv_bfloat16* qh = q + ((size_t)b * v.Hq + g * G + gq) * D;
 #pragma unroll
@@ -276,14 +337,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
         }
       }
     }
-    // new token (a1): append its K/V row to T0 row n0-1 (swizzled) and keep it in SMEM (fp32)
-    if (has_new) {
-      uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[cur]) + (grp * v.cap0 + n0o) * D;
-      uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[cur]) + (grp * v.cap0 + n0o) * D;
+    const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));   // log2(e)/sqrt(d)
+    float* zrow = zpar >= 0 ? v.zbuf + ((size_t)zpar * v.B * v.Hkv + unit) * v.zrows * 8 : nullptr;
+
+    if (has_new) {   // new token (a1): append its row to T0 row n0-1 (swizzled), keep it in SMEM
+      uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[cur]) + (grp * v.cap0 + sg.n0o) * D;
+      uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[cur]) + (grp * v.cap0 + sg.n0o) * D;
       const uint16_t* kin = knew ? reinterpret_cast<const uint16_t*>(knew) + ((size_t)b * v.Hkv + g) * D : nullptr;
       const uint16_t* vin = vnew ? reinterpret_cast<const uint16_t*>(vnew) + ((size_t)b * v.Hkv + g) * D : nullptr;
       for (int e = tid; e < D; e += NCONS) {
-        const int se = swz_off(n0o, e);
+        const int se = swz_off(sg.n0o, e);
         const uint16_t kb = kin ? kin[e] : K0w[se];
         const uint16_t vb = vin ? vin[e] : V0w[se];
         nrow[e] = bf16_bits_to_f(kb);
@@ -293,99 +356,166 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
       }
     }
 
-    auto qk_warp = [&](uint32_t sbase, int tv0, int tend, const float* rsc, bool t2seg) {
-      if (tv0 + w * 16 >= tend) return;
+    // one warp-slice (16 rows) of a tile: logits, online softmax, P.V
+    auto do_rows = [&](uint32_t sK, uint32_t sV, int tv0, const float* scK, const float* scV, bool t2) {
+      const int r0 = w * 16 + gq, r1 = r0 + 8;
+      const int t0 = tv0 + r0, t1 = tv0 + r1;
+      const bool v0 = t2 ? (t0 - sg.a2 < sg.n2) : sg.bf16_valid(t0);
+      const bool v1 = t2 ? (t1 - sg.a2 < sg.n2) : sg.bf16_valid(t1);
+      if (!__any_sync(0xffffffffu, v0 || v1)) return;
       float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
       const int mi = lane >> 3, ii = lane & 7;
-      const int row = w * 16 + ii + ((mi & 1) << 3);
+      {
+        const int row = (t2 ? 0 : w * 16) + ii + ((mi & 1) << 3);
 #pragma unroll
-      for (int ks = 0; ks < KS; ks += 2) {
-        uint32_t a0, a1_, a2_, a3_;
-        ldsm_x4(a0, a1_, a2_, a3_, sbase + row * ROWB + (((2 * ks + (mi >> 1)) ^ (row & 7)) << 4));
-        mma16816(acc, a0, a1_, a2_, a3_, qf[ks][0], qf[ks][1]);
-        ldsm_x4(a0, a1_, a2_, a3_, sbase + row * ROWB + (((2 * ks + 2 + (mi >> 1)) ^ (row & 7)) << 4));
-        mma16816(acc2, a0, a1_, a2_, a3_, qf[ks + 1][0], qf[ks + 1][1]);
+        for (int ks = 0; ks < KS; ks += 2) {
+          uint32_t a0, a1_, a2_, a3_;
+          ldsm_x4(a0, a1_, a2_, a3_, sK + row * ROWB + (((2 * ks + (mi >> 1)) ^ (row & 7)) << 4));
+          mma16816(acc, a0, a1_, a2_, a3_, qf[ks][0], qf[ks][1]);
+          ldsm_x4(a0, a1_, a2_, a3_, sK + row * ROWB + (((2 * ks + 2 + (mi >> 1)) ^ (row & 7)) << 4));
+          mma16816(acc2, a0, a1_, a2_, a3_, qf[ks + 1][0], qf[ks + 1][1]);
+        }
       }
-      const int r0 = w * 16 + gq, r1 = r0 + 8;
-      const int t0 = tv0 + r0, t1 = tv0 + r1;
-      if (t0 < tend && (t2seg || bf16_valid(t0))) {
-        const float f = rsc ? rsc[r0] * sl2 : sl2;
-        const float z0 = (acc[0] + acc2[0]) * f, z1 = (acc[1] + acc2[1]) * f;
-        *reinterpret_cast<float2*>(&zs[(t0 - vbeg) * 8 + 2 * tq]) = make_float2(z0, z1);
-        mx0 = fmaxf(mx0, z0);
-        mx1 = fmaxf(mx1, z1);
+      const float f0 = scK ? scK[r0] * sl2 : sl2, f1 = scK ? scK[r1] * sl2 : sl2;
+      const float z00 = v0 ? (acc[0] + acc2[0]) * f0 : -INFINITY, z01 = v0 ? (acc[1] + acc2[1]) * f0 : -INFINITY;
+      const float z10 = v1 ? (acc[2] + acc2[2]) * f1 : -INFINITY, z11 = v1 ? (acc[3] + acc2[3]) * f1 : -INFINITY;
+      if (zrow) {
+        if (v0) *reinterpret_cast<float2*>(zrow + (size_t)t0 * 8 + 2 * tq) = make_float2(z00, z01);
+        if (v1) *reinterpret_cast<float2*>(zrow + (size_t)t1 * 8 + 2 * tq) = make_float2(z10, z11);
       }
-      if (t1 < tend && (t2seg || bf16_valid(t1))) {
-        const float f = rsc ? rsc[r1] * sl2 : sl2;
-        const float z0 = (acc[2] + acc2[2]) * f, z1 = (acc[3] + acc2[3]) * f;
-        *reinterpret_cast<float2*>(&zs[(t1 - vbeg) * 8 + 2 * tq]) = make_float2(z0, z1);
-        mx0 = fmaxf(mx0, z0);
-        mx1 = fmaxf(mx1, z1);
+      float ta = fmaxf(z00, z10), tb = fmaxf(z01, z11);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        ta = fmaxf(ta, __shfl_xor_sync(0xffffffffu, ta, off));
+        tb = fmaxf(tb, __shfl_xor_sync(0xffffffffu, tb, off));
       }
-    };
-    auto pv_warp = [&](uint32_t sbase, int tv0, int tend, const float* rsc, bool t2seg) {
-      if (tv0 + w * 16 >= tend) return;
-      const int r0 = w * 16 + gq, r1 = r0 + 8;
-      const int t0 = tv0 + r0, t1 = tv0 + r1;
-      float p00 = 0.f, p01 = 0.f, p10 = 0.f, p11 = 0.f;
-      if (t0 < tend && (t2seg || bf16_valid(t0))) {
-        const float2 z = *reinterpret_cast<const float2*>(&zs[(t0 - vbeg) * 8 + 2 * tq]);
-        p00 = exp2f(z.x - m2a);
-        p01 = exp2f(z.y - m2b);
+      const float na = fmaxf(mxa, ta), nb = fmaxf(mxb, tb);     // finite: some row is valid
+      const float ca = exp2f(mxa - na), cb = exp2f(mxb - nb);   // 0 when the old max is -inf
+      mxa = na;
+      mxb = nb;
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) {
+        oacc[mt][0] *= ca;
+        oacc[mt][2] *= ca;
+        oacc[mt][1] *= cb;
+        oacc[mt][3] *= cb;
       }
-      if (t1 < tend && (t2seg || bf16_valid(t1))) {
-        const float2 z = *reinterpret_cast<const float2*>(&zs[(t1 - vbeg) * 8 + 2 * tq]);
-        p10 = exp2f(z.x - m2a);
-        p11 = exp2f(z.y - m2b);
-      }
-      l0 += p00 + p10;
-      l1 += p01 + p11;
-      if (rsc) {   // T2: o += p * scale_v * code  (codes are exact in bf16)
-        p00 *= rsc[r0]; p01 *= rsc[r0];
-        p10 *= rsc[r1]; p11 *= rsc[r1];
+      float p00 = exp2f(z00 - na), p01 = exp2f(z01 - nb), p10 = exp2f(z10 - na), p11 = exp2f(z11 - nb);
+      la = la * ca + p00 + p10;
+      lb = lb * cb + p01 + p11;
+      if (scV) {   // T2: o += p * scale_v * code  (codes are exact in bf16)
+        p00 *= scV[r0]; p01 *= scV[r0];
+        p10 *= scV[r1]; p11 *= scV[r1];
       }
       const uint32_t b0 = movm_t(pack_bf16(p00, p01));
       const uint32_t b1 = movm_t(pack_bf16(p10, p11));
-      const int mi = lane >> 3, ii = lane & 7;
-      const int row = w * 16 + ii + ((mi >> 1) << 3);
+      const int row = (t2 ? 0 : w * 16) + ii + ((mi >> 1) << 3);
 #pragma unroll
       for (int mt = 0; mt < KS; ++mt) {
-        const int ch = 2 * mt + (mi & 1);
         uint32_t a0, a1_, a2_, a3_;
-        ldsm_x4_t(a0, a1_, a2_, a3_, sbase + row * ROWB + ((ch ^ (row & 7)) << 4));
+        ldsm_x4_t(a0, a1_, a2_, a3_, sV + row * ROWB + (((2 * mt + (mi & 1)) ^ (row & 7)) << 4));
         mma16816(oacc[mt], a0, a1_, a2_, a3_, b0, b1);
       }
     };
-    auto stage_t2 = [&](int tv0, bool isV) {   // int8 codes -> exact bf16 (canonical codes, swizzled in SMEM)
-      const int8_t* C2 = (isV ? v.c2v[cur] : v.c2k[cur]) + grp * v.cap2 * D;
-      const float* S2 = (isV ? v.s2v[cur] : v.s2k[cur]) + grp * v.cap2;
-      for (int e = tid; e < TILE * (D / 16); e += NCONS) {
+    // this warp's 16 rows of int8 codes -> exact bf16 into its scratch (swizzled by row)
+    auto stage_t2_rows = [&](const int8_t* codes, unsigned char* scr) {
+      for (int e = lane; e < 16 * (D / 16); e += 32) {
         const int row = e / (D / 16), j = e % (D / 16);
-        const int tok = tv0 + row;
-        uint4 cw = make_uint4(0u, 0u, 0u, 0u);
-        if (tok < t2end) cw = *reinterpret_cast<const uint4*>(C2 + (size_t)(tok - a2) * D + 16 * j);
+        const uint4 cw = *reinterpret_cast<const uint4*>(codes + (size_t)(w * 16 + row) * D + 16 * j);
         uint4 lo, hi;
         lo.x = i8pair_to_bf16x2(cw.x, 0); lo.y = i8pair_to_bf16x2(cw.x, 1);
         lo.z = i8pair_to_bf16x2(cw.y, 0); lo.w = i8pair_to_bf16x2(cw.y, 1);
         hi.x = i8pair_to_bf16x2(cw.z, 0); hi.y = i8pair_to_bf16x2(cw.z, 1);
         hi.z = i8pair_to_bf16x2(cw.w, 0); hi.w = i8pair_to_bf16x2(cw.w, 1);
-        *reinterpret_cast<uint4*>(t2buf + row * ROWB + (((2 * j) ^ (row & 7)) << 4)) = lo;
-        *reinterpret_cast<uint4*>(t2buf + row * ROWB + (((2 * j + 1) ^ (row & 7)) << 4)) = hi;
+        *reinterpret_cast<uint4*>(scr + row * ROWB + (((2 * j) ^ (row & 7)) << 4)) = lo;
+        *reinterpret_cast<uint4*>(scr + row * ROWB + (((2 * j + 1) ^ (row & 7)) << 4)) = hi;
       }
-      for (int row = tid; row < TILE; row += NCONS) {
-        const int tok = tv0 + row;
-        t2sc[row] = tok < t2end ? S2[tok - a2] : 0.f;
-      }
+      __syncwarp();
     };
 
-    // ---- phase A on T2 rows (rare; synchronous, consumer barrier 1)
-    for (int tv0 = t2beg; tv0 < t2end; tv0 += TILE) {
-      named_sync(1, NCONS);
-      stage_t2(tv0, false);
-      named_sync(1, NCONS);
-      qk_warp(smem_u32(t2buf), tv0, t2end, t2sc, true);
+    for (int i = 0;; ++i) {
+      const int s2 = i % NST;
+      mbar_wait(full0 + 8 * s2, (i / NST) & 1);
+      const int k = stile[s2];
+      if (k < 0) break;
+      if (tr && tid == 0 && i == 0) tr[2] = gtimer();
+      const uint32_t sK = ring_s + s2 * STAGEB, sV = sK + TILEB;
+      if (k < ntb) {
+        do_rows(sK, sV, k * TILE, nullptr, nullptr, false);
+      } else {
+        unsigned char* st = ring + s2 * STAGEB;
+        unsigned char* scr = t2w + (size_t)w * 16 * ROWB;
+        const float* scK = reinterpret_cast<const float*>(st + TILE * D);
+        const float* scV = reinterpret_cast<const float*>(st + TILEB + TILE * D);
+        // K codes -> scratch; logits; then V codes -> scratch; P.V (do_rows reads both via scratch)
+        stage_t2_rows(reinterpret_cast<const int8_t*>(st), scr);
+        // split do_rows: QK on K scratch, then restage V into the same scratch before P.V
+        {
+          const int tv0 = sg.a2 + (k - ntb) * TILE;
+          const int r0 = w * 16 + gq, r1 = r0 + 8;
+          const int t0 = tv0 + r0, t1 = tv0 + r1;
+          const bool v0 = t0 - sg.a2 < sg.n2, v1 = t1 - sg.a2 < sg.n2;
+          if (__any_sync(0xffffffffu, v0 || v1)) {
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            const int mi = lane >> 3, ii = lane & 7;
+            const uint32_t sscr = smem_u32(scr);
+            {
+              const int row = ii + ((mi & 1) << 3);
+#pragma unroll
+              for (int ks = 0; ks < KS; ++ks) {
+                uint32_t a0, a1_, a2_, a3_;
+                ldsm_x4(a0, a1_, a2_, a3_, sscr + row * ROWB + (((2 * ks + (mi >> 1)) ^ (row & 7)) << 4));
+                mma16816(acc, a0, a1_, a2_, a3_, qf[ks][0], qf[ks][1]);
+              }
+            }
+            const float z00 = v0 ? acc[0] * scK[r0] * sl2 : -INFINITY, z01 = v0 ? acc[1] * scK[r0] * sl2 : -INFINITY;
+            const float z10 = v1 ? acc[2] * scK[r1] * sl2 : -INFINITY, z11 = v1 ? acc[3] * scK[r1] * sl2 : -INFINITY;
+            if (zrow) {
+              if (v0) *reinterpret_cast<float2*>(zrow + (size_t)t0 * 8 + 2 * tq) = make_float2(z00, z01);
+              if (v1) *reinterpret_cast<float2*>(zrow + (size_t)t1 * 8 + 2 * tq) = make_float2(z10, z11);
+            }
+            float ta = fmaxf(z00, z10), tb = fmaxf(z01, z11);
+#pragma unroll
+            for (int off = 4; off < 32; off <<= 1) {
+              ta = fmaxf(ta, __shfl_xor_sync(0xffffffffu, ta, off));
+              tb = fmaxf(tb, __shfl_xor_sync(0xffffffffu, tb, off));
+            }
+            const float na = fmaxf(mxa, ta), nb = fmaxf(mxb, tb);
+            const float ca = exp2f(mxa - na), cb = exp2f(mxb - nb);
+            mxa = na;
+            mxb = nb;
+#pragma unroll
+            for (int mt = 0; mt < KS; ++mt) {
+              oacc[mt][0] *= ca;
+              oacc[mt][2] *= ca;
+              oacc[mt][1] *= cb;
+              oacc[mt][3] *= cb;
+            }
+            float p00 = exp2f(z00 - na), p01 = exp2f(z01 - nb), p10 = exp2f(z10 - na), p11 = exp2f(z11 - nb);
+            la = la * ca + p00 + p10;
+            lb = lb * cb + p01 + p11;
+            p00 *= scV[r0]; p01 *= scV[r0];
+            p10 *= scV[r1]; p11 *= scV[r1];
+            const uint32_t b0 = movm_t(pack_bf16(p00, p01));
+            const uint32_t b1 = movm_t(pack_bf16(p10, p11));
+            __syncwarp();
+            stage_t2_rows(reinterpret_cast<const int8_t*>(st + TILEB), scr);
+            const int row = ii + ((mi >> 1) << 3);
+#pragma unroll
+            for (int mt = 0; mt < KS; ++mt) {
+              uint32_t a0, a1_, a2_, a3_;
+              ldsm_x4_t(a0, a1_, a2_, a3_, sscr + row * ROWB + (((2 * mt + (mi & 1)) ^ (row & 7)) << 4));
+              mma16816(oacc[mt], a0, a1_, a2_, a3_, b0, b1);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * s2);
     }
-    // ---- phase A on the new token (CUDA cores, fp32): warp 0 computes all heads' logits
+    if (tr && tid == 0) tr[3] = gtimer();
+
+    // new token: warp 0 of rank 0, CUDA cores, fp32 (rank-1 online update)
     if (has_new) named_sync(1, NCONS);   // nrow visible
     if (has_new && w == 0) {
       float part = 0.f;
@@ -397,106 +527,41 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
       }
       part += __shfl_xor_sync(0xffffffffu, part, 1);
       part += __shfl_xor_sync(0xffffffffu, part, 2);
-      if (tq == 0) zs[(a3 - vbeg) * 8 + gq] = part * sl2;
-    }
-
-    auto write_warp_max = [&]() {
-      float a = mx0, c = mx1;
-#pragma unroll
-      for (int off = 4; off < 32; off <<= 1) {
-        a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, off));
-        c = fmaxf(c, __shfl_xor_sync(0xffffffffu, c, off));
-      }
-      if (lane < 4) {
-        red[w * 8 + 2 * lane] = a;
-        red[w * 8 + 2 * lane + 1] = c;
-      }
-    };
-    auto reduce_max = [&]() {   // after a consumer barrier: CTA max incl. the new token
-      float nz0 = -INFINITY, nz1 = -INFINITY;
-      if (has_new) {
-        nz0 = zs[(a3 - vbeg) * 8 + 2 * tq];
-        nz1 = zs[(a3 - vbeg) * 8 + 2 * tq + 1];
-      }
-      m2a = nz0;
-      m2b = nz1;
-#pragma unroll
-      for (int ww = 0; ww < NW; ++ww) {
-        m2a = fmaxf(m2a, red[ww * 8 + 2 * tq]);
-        m2b = fmaxf(m2b, red[ww * 8 + 2 * tq + 1]);
-      }
-      if (tid < 8) {
-        float m = has_new ? zs[(a3 - vbeg) * 8 + tid] : -INFINITY;
-#pragma unroll
-        for (int ww = 0; ww < NW; ++ww) m = fmaxf(m, red[ww * 8 + tid]);
-        xm[tid] = m;
-      }
-      if (m2a == -INFINITY) m2a = 0.f;
-      if (m2b == -INFINITY) m2b = 0.f;
-    };
-
-    // ---- phases A (K tiles) and B (V tiles) from the bulk-copy ring
-    for (int i = 0; i < total; ++i) {
-      const int s2 = i % NST;
-      if (i == nt) {                 // every warp's max of phase A is in `red`
-        named_sync(1, NCONS);
-        reduce_max();
-      }
-      mbar_wait(full0 + 8 * s2, (i / NST) & 1);
-      if (tr && tid == 0 && i == 0) tr[2] = gtimer();
-      if (tr && tid == 0 && i == nt) tr[3] = gtimer();
-      const uint32_t sbase = ring_s + s2 * TILEB;
-      if (i < nt) {
-        qk_warp(sbase, vbeg + i * TILE, aend, nullptr, false);
-        if (i == nt - 1) write_warp_max();
-      } else {
-        pv_warp(sbase, vbeg + (i - nt) * TILE, aend, nullptr, false);
+      if (tq == 0) {
+        zn[gq] = part * sl2;
+        if (zrow) zrow[(size_t)sg.a3 * 8 + gq] = part * sl2;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8 * s2);
-    }
-    if (nt == 0) {
-      write_warp_max();
-      named_sync(1, NCONS);
-      reduce_max();
-    }
-    // ---- phase B on T2 rows
-    for (int tv0 = t2beg; tv0 < t2end; tv0 += TILE) {
-      named_sync(1, NCONS);
-      stage_t2(tv0, true);
-      named_sync(1, NCONS);
-      pv_warp(smem_u32(t2buf), tv0, t2end, t2sc, true);
-    }
-    // ---- phase B on the new token: rank-1 update of warp 0's o^T fragments
-    if (has_new && w == 0) {
-      const float* zr = zs + (a3 - vbeg) * 8;
-      const float pa = exp2f(zr[2 * tq] - m2a), pb = exp2f(zr[2 * tq + 1] - m2b);
-      if (gq == 0) { l0 += pa; l1 += pb; }          // counted once per head (lanes 0..3)
+      const float za = zn[2 * tq], zb = zn[2 * tq + 1];
+      const float na = fmaxf(mxa, za), nb = fmaxf(mxb, zb);
+      const float ca = exp2f(mxa - na), cb = exp2f(mxb - nb);
+      mxa = na;
+      mxb = nb;
+      const float pa = exp2f(za - na), pb = exp2f(zb - nb);
+      la = la * ca + (gq == 0 ? pa : 0.f);       // counted once per head (lanes 0..3)
+      lb = lb * cb + (gq == 0 ? pb : 0.f);
 #pragma unroll
       for (int mt = 0; mt < KS; ++mt) {
         const float va = nrow[D + mt * 16 + gq], vb = nrow[D + mt * 16 + gq + 8];
-        oacc[mt][0] += pa * va;
-        oacc[mt][1] += pb * va;
-        oacc[mt][2] += pa * vb;
-        oacc[mt][3] += pb * vb;
+        oacc[mt][0] = oacc[mt][0] * ca + pa * va;
+        oacc[mt][1] = oacc[mt][1] * cb + pb * va;
+        oacc[mt][2] = oacc[mt][2] * ca + pa * vb;
+        oacc[mt][3] = oacc[mt][3] * cb + pb * vb;
       }
     }
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
-      l0 += __shfl_xor_sync(0xffffffffu, l0, off);
-      l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+      la += __shfl_xor_sync(0xffffffffu, la, off);
+      lb += __shfl_xor_sync(0xffffffffu, lb, off);
     }
-  }
-
-  // ---- CTA reduction of l and o (ring reused as [NW warps][8 heads][D+4] fp32, padded rows)
-  if (tr && tid == 0) tr[4] = gtimer();
-  constexpr int OWS = D + 4;
-  __syncthreads();
-  float* ow = reinterpret_cast<float*>(ring);
-  if (w < NW) {
+    // ---- warps -> CTA partial (ring reused as [NW][8][D+4] fp32)
+    named_sync(1, NCONS);                // every consumer is done with the ring
+    float* ow = reinterpret_cast<float*>(ring);
     if (lane < 4) {
-      red[8 * NW + w * 8 + 2 * lane] = l0;
-      red[8 * NW + w * 8 + 2 * lane + 1] = l1;
+      redm[w * 8 + 2 * lane] = mxa;
+      redm[w * 8 + 2 * lane + 1] = mxb;
+      redl[w * 8 + 2 * lane] = la;
+      redl[w * 8 + 2 * lane + 1] = lb;
     }
 #pragma unroll
     for (int mt = 0; mt < KS; ++mt) {
@@ -507,28 +572,41 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
       o0[8] = oacc[mt][2];
       o1[8] = oacc[mt][3];
     }
-  }
-  __syncthreads();
-  for (int e = tid; e < G * D; e += NTHR) {
-    const int h = e / D, dd = e - h * D;
-    float a = ow[h * OWS + dd];
+    named_sync(1, NCONS);
+    if (tid < 8) {
+      float M = -INFINITY;
 #pragma unroll
-    for (int ww = 1; ww < NW; ++ww) a += ow[(ww * 8 + h) * OWS + dd];
-    xo[e] = a;
-  }
-  if (tid < 8) {
-    float a = red[8 * NW + tid];
+      for (int ww = 0; ww < NW; ++ww) M = fmaxf(M, redm[ww * 8 + tid]);
+      float Ls = 0.f;
 #pragma unroll
-    for (int ww = 1; ww < NW; ++ww) a += red[8 * NW + ww * 8 + tid];
-    xl[tid] = a;
+      for (int ww = 0; ww < NW; ++ww) {
+        const float m = redm[ww * 8 + tid];
+        if (m != -INFINITY) Ls += redl[ww * 8 + tid] * exp2f(m - M);
+      }
+      xm[tid] = M;
+      xl[tid] = Ls;
+    }
+    named_sync(1, NCONS);
+    for (int e = tid; e < G * D; e += NCONS) {
+      const int h = e / D, dd = e - h * D;
+      const float M = xm[h];
+      float a = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < NW; ++ww) {
+        const float m = redm[ww * 8 + h];
+        if (m != -INFINITY) a += exp2f(m - M) * ow[(ww * 8 + h) * OWS + dd];
+      }
+      xo[e] = a;
+    }
   }
+  if (tr && tid == 0) tr[4] = gtimer();
 
   // ---- cluster merge through distributed shared memory (all remote reads issued in parallel)
   cluster.sync();
   if (tr && tid == 0) tr[5] = gtimer();
-  float* gm = ow;                 // [16][8] peers' m    (ring is free now)
-  float* gl = ow + 128;           // [16][8] peers' l
-  float* gf = ow + 256;           // [16][8] merge factors exp2(m_c - M) / L
+  float* gm = reinterpret_cast<float*>(ring);   // [16][8] peers' m
+  float* gl = gm + 128;                          // [16][8] peers' l
+  float* gf = gm + 256;                          // [16][8] exp2(m_c - M) / L
   if (tid < 8 * C) {
     const int c = tid >> 3, h = tid & 7;
     gm[tid] = cluster.map_shared_rank(xm, c)[h];
@@ -545,6 +623,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
     }
     sML[tid] = M;
     sML[8 + tid] = 1.0f / Ls;
+    if (r == 0 && zpar >= 0) {     // publish (M, 1/L) for the deferred score pass
+      float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
+      ml[tid] = M;
+      ml[8 + tid] = 1.0f / Ls;
+    }
   }
   __syncthreads();
   if (tid < 8 * C) {
@@ -573,42 +656,43 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW == 4 ? 2 : 1))
       else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(acc);
     }
   }
-  // done reading peers' shared memory: arrive now, wait before exit (score work overlaps)
   if (tr && tid == 0) tr[6] = gtimer();
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  if (fuse && w < NW) {
-    cp_wait<0>();                    // this thread's S_part values are in sS
-    float* Sg = v.S + ((size_t)b * v.Hkv + g) * v.Nmax;
-    bool bad = false;
-    for (int j = tid; j < vend - vbeg; j += NCONS) {
-      const int pos = spos[j];
-      if (pos < 0) continue;
-      const float* zr = zs + j * 8;
-      float inc = 0.f;
-      for (int h = 0; h < G; ++h) inc += exp2f(zr[h] - sML[h]) * sML[8 + h];
-      Sg[pos] = sS[j] + inc;
-      bad |= !isfinite(inc);
-    }
-    if (bad) atomicOr(&v.st->err, 1);
-  }
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (bad) atomicOr(&v.st->err, 1);
+  cluster.sync();                 // peers' shared memory stays alive until every read is done
   if (tr && tid == 0) tr[7] = gtimer();
 }
 
-// (warps, stages) variants; DevView::variant selects one (0 = default)
+// End-of-step flush of the last layer's deferred score update.
+__global__ void __launch_bounds__(256) k_score_flush(const DevView v, const int zpar) {
+  const int cur = v.st->cur;
+  Seg sg;
+  sg.init(v.cnt[cur]);          // counts are uniform across requests
+  const long long tot = (long long)v.B * v.Hkv * sg.nvirt;
+  bool bad = false;
+  score_range(v, sg, cur, zpar, 0, tot, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, bad);
+  if (bad) atomicOr(&v.st->err, 1);
+}
+
+cudaError_t launch_score_flush(const DevView& v, int zpar, cudaStream_t s) {
+  k_score_flush<<<2 * 148, 256, 0, s>>>(v, zpar);
+  return cudaGetLastError();
+}
+
+// (consumer warps, stages) variants; DevView::variant selects one (0 = default)
 struct Variant { int nw, nst; };
-static constexpr Variant kVariants[] = {{4, 4}, {4, 6}, {8, 3}, {8, 4}, {4, 5}, {8, 6}};
+static constexpr Variant kVariants[] = {{4, 3}, {4, 4}, {8, 2}, {8, 3}, {4, 2}, {8, 4}};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 size_t attn_smem_bytes(const DevView& v) {
   const Variant vr = kVariants[v.variant];
   const int tile = 16 * vr.nw;
-  const size_t ringb = (size_t)vr.nst * tile * v.D * 2 + (2 * vr.nst + 2) * 8;
-  const size_t zsb = (size_t)v.chunk_max * 8 * 4 + (size_t)v.chunk_max * 8;
-  const size_t xob = (size_t)8 * v.D * 4;
-  const size_t misc = (size_t)(8 + 8 + 16 * vr.nw + 16 + 2 * v.D + tile) * 4;
-  const size_t t2 = (v.cap2 > 0) ? (size_t)tile * v.D * 2 : 0;
-  return ringb + zsb + xob + misc + t2;
+  const size_t ringb = (size_t)vr.nst * 2 * tile * v.D * 2 + (2 * vr.nst) * 8 + (vr.nst + 4) * 4 + 16;
+  const size_t xob = (size_t)8 * v.D * 4 + (8 + 8 + 16 * vr.nw + 16 + 2 * v.D + 8) * 4;
+  const size_t t2 = (v.cap2 > 0) ? (size_t)vr.nw * 16 * v.D * 2 : 0;
+  size_t total = ringb + xob + t2;
+  const size_t ow = (size_t)vr.nw * 8 * (v.D + 4) * 4;   // end-of-kernel reuse of the ring
+  if (ow + 3 * 128 * 4 > (size_t)vr.nst * 2 * tile * v.D * 2) total += ow;   // (never for the shipped variants)
+  return total;
 }
 
 template <int D, int NW, int NST>
@@ -623,14 +707,14 @@ static cudaError_t configure_k(const DevView& v) {
 
 template <int D, int NW, int NST>
 static cudaError_t launch_k(const DevView& v, cudaLaunchConfig_t& cfg, int layer, const void* q, const void* knew,
-                            const void* vnew, void* o, int fuse) {
-  cfg.blockDim = dim3((NW + 1) * 32, 1, 1);
+                            const void* vnew, void* o, int zpar, int prev_zpar) {
+  cfg.blockDim = dim3((NW + 2) * 32, 1, 1);
   return cudaLaunchKernelEx(&cfg, k_decode_attn<D, NW, NST>, v, layer, reinterpret_cast<const __nv_bfloat16*>(q),
                             reinterpret_cast<const __nv_bfloat16*>(knew), reinterpret_cast<const __nv_bfloat16*>(vnew),
-                            o, fuse);
+                            o, zpar, prev_zpar);
 }
 
-#define KVT_VARIANTS(X, D) X(D, 4, 4) X(D, 4, 6) X(D, 8, 3) X(D, 8, 4) X(D, 4, 5) X(D, 8, 6)
+#define KVT_VARIANTS(X, D) X(D, 4, 3) X(D, 4, 4) X(D, 8, 2) X(D, 8, 3) X(D, 4, 2) X(D, 8, 4)
 
 cudaError_t attn_configure(const DevView& v) {
   if (v.variant < 0 || v.variant >= kNumVariants) return cudaErrorInvalidValue;
@@ -644,7 +728,7 @@ cudaError_t attn_configure(const DevView& v) {
 }
 
 cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
-                               void* o, int fuse, int pdl, cudaStream_t s) {
+                               void* o, int zpar, int prev_zpar, int pdl, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(v.split, v.B * v.Hkv, 1);
   cfg.dynamicSmemBytes = attn_smem_bytes(v);
@@ -659,8 +743,9 @@ cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 2 : 1;
   const Variant vr = kVariants[v.variant];
-#define KVT_LAUNCH(DD, NWW, NSS) \
-  if (v.D == DD && vr.nw == NWW && vr.nst == NSS) return launch_k<DD, NWW, NSS>(v, cfg, layer, q, knew, vnew, o, fuse);
+#define KVT_LAUNCH(DD, NWW, NSS)                          \
+  if (v.D == DD && vr.nw == NWW && vr.nst == NSS)         \
+    return launch_k<DD, NWW, NSS>(v, cfg, layer, q, knew, vnew, o, zpar, prev_zpar);
   KVT_VARIANTS(KVT_LAUNCH, 128)
   KVT_VARIANTS(KVT_LAUNCH, 64)
 #undef KVT_LAUNCH

@@ -33,6 +33,8 @@ struct kv_tier_ctx {
   std::vector<int> appended_step;          // step in which layer l's new row was written
   bool offload_pending = false;
   bool capturing = false;
+  int zpar_next = 0;                       // logits buffer of the next fused decode_attention
+  int pending_zpar = -1;                   // deferred score pass not yet applied
   bool slot_recorded[2] = {false, false};   // ev_slot_free[x] recorded within the open step
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -67,9 +69,7 @@ int auto_split(const kv_tier_config& c) {
   if (c.split > 0) return c.split;
   const int units = c.num_requests * c.num_kv_heads;
   int s = (2 * 148 + units - 1) / units;
-  s = std::max(1, std::min(8, s));
-  while (s < 16 && (c.max_tokens + s - 1) / s > 2048) ++s;   // logits of a chunk stay in SMEM
-  return s;
+  return std::max(1, std::min(8, s));
 }
 
 kv_tier_status validate(const kv_tier_config* c) {
@@ -112,7 +112,7 @@ void capacities(const kv_tier_config& c, int* cap0, int* cap1, int* cap2) {
 
 struct Layout {
   size_t off_k0[2], off_v0[2], off_k1[2], off_v1[2], off_c2k[2], off_c2v[2], off_s2k[2], off_s2v[2];
-  size_t off_idx[2][3], off_vis[2], off_tier[2], off_row[2], off_cnt[2], off_S, off_fS, off_st, total;
+  size_t off_idx[2][3], off_vis[2], off_tier[2], off_row[2], off_cnt[2], off_S, off_fS, off_st, off_z, off_ml, total;
   size_t b_t0, b_t1, b_t2, b_scores, b_meta;
 };
 
@@ -141,6 +141,8 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   }
   L.b_t2 = o - s0; s0 = o;
   L.off_S = take(BH * N * 4);
+  L.off_z = take(2 * BH * (N + 64) * 8 * 4);     // deferred-score logits (two launches)
+  L.off_ml = take(2 * BH * 16 * 4);
   L.b_scores = o - s0; s0 = o;
   for (int i = 0; i < 2; ++i) {
     L.off_idx[i][0] = take(B * cap0 * 4);
@@ -224,7 +226,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.out_fp32 = cfg->out_fp32;
   v.split = auto_split(*cfg);
   v.variant = cfg->variant;
-  v.chunk_max = round16((cfg->max_tokens + 64 + v.split - 1) / v.split) + 16;   // virtual layout pads 3 segments to 16
+  v.chunk_max = 0;
   for (int i = 0; i < 2; ++i) {
     v.k0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_k0[i]);
     v.v0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_v0[i]);
@@ -241,6 +243,9 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     v.cnt[i] = reinterpret_cast<int*>(A + L.off_cnt[i]);
   }
   v.S = reinterpret_cast<float*>(A + L.off_S);
+  v.zbuf = reinterpret_cast<float*>(A + L.off_z);
+  v.ml = reinterpret_cast<float*>(A + L.off_ml);
+  v.zrows = cfg->max_tokens + 64;
   v.fS = reinterpret_cast<float*>(A + L.off_fS);
   v.st = reinterpret_cast<DevState*>(A + L.off_st);
   // pinned, mapped host stores (NUMA placement follows the calling thread's node)
@@ -404,7 +409,12 @@ static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, con
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
   if (ctx->v.stream_mode) e = cudaStreamWaitEvent(s, ctx->ev_prefetched[layer], 0);
-  if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, fuse_score_update, pdl, s);
+  const int zpar = fuse_score_update ? ctx->zpar_next : -1;
+  if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, zpar, ctx->pending_zpar, pdl, s);
+  if (e == cudaSuccess) {
+    ctx->pending_zpar = zpar;
+    if (zpar >= 0) ctx->zpar_next ^= 1;
+  }
   if (e == cudaSuccess && ctx->v.stream_mode) {
     e = cudaEventRecord(ctx->ev_slot_free[layer & 1], s);
     ctx->slot_recorded[layer & 1] = true;
@@ -434,8 +444,12 @@ kv_tier_status kv_tier_score_update(kv_tier_ctx* ctx, int32_t layer, const float
 kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (!ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "end_step without begin_step");
-  kv_tier_status st = cuda_check(ctx, launch_end_step(ctx->v, reinterpret_cast<cudaStream_t>(stream)), "end_step");
+  cudaError_t e = cudaSuccess;
+  if (ctx->pending_zpar >= 0) e = launch_score_flush(ctx->v, ctx->pending_zpar, reinterpret_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) e = launch_end_step(ctx->v, reinterpret_cast<cudaStream_t>(stream));
+  kv_tier_status st = cuda_check(ctx, e, "end_step");
   if (st) return st;
+  ctx->pending_zpar = -1;
   ctx->step_open = false;
   ctx->t += 1;
   return KV_TIER_OK;
@@ -530,6 +544,7 @@ kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const
   const bool classified = ctx->classified;
   const std::vector<int> pstep = ctx->prefetched_step;
   const std::vector<int> astep = ctx->appended_step;
+  const int zpn = ctx->zpar_next, pzp = ctx->pending_zpar;
   cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return cuda_check(ctx, e, "begin capture");
   ctx->capturing = true;
@@ -540,6 +555,8 @@ kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const
   ctx->n = n; ctx->t = t; ctx->c[0] = c0; ctx->classified = classified; ctx->step_open = false;
   ctx->prefetched_step = pstep;
   ctx->appended_step = astep;
+  ctx->zpar_next = zpn;
+  ctx->pending_zpar = pzp;
   if (st) { if (g) cudaGraphDestroy(g); return st; }
   if (e != cudaSuccess) return cuda_check(ctx, e, "end capture");
   e = cudaGraphInstantiate(&ctx->graph_exec, g, 0);
@@ -564,6 +581,8 @@ kv_tier_status kv_tier_step_graph_launch(kv_tier_ctx* ctx, void* stream) {
   ctx->c[0] += 1;
   ctx->t += 1;
   ctx->classified = false;
+  ctx->zpar_next ^= (ctx->v.L & 1);        // same transitions as kv_tier_step
+  ctx->pending_zpar = -1;
   return KV_TIER_OK;
 }
 

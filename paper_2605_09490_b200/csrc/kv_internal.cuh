@@ -31,6 +31,9 @@ struct DevView {
   int chunk_max;        // max tokens per CTA (logit buffer rows)
   int variant;          // decode-attention kernel variant (warps x pipeline stages)
   unsigned long long* trace;   // debug: per-CTA %globaltimer checkpoints (null = off)
+  float* zbuf;          // [2][B*Hkv][zrows][8] logits (log2 domain) of the last two launches
+  float* ml;            // [2][B*Hkv][16] per-head (max, 1/sum) of the last two launches
+  int zrows;            // virtual rows per unit (N_max + padding)
   __nv_bfloat16* k0[2]; __nv_bfloat16* v0[2];        // T0 store  [L][B][Hkv][cap0][D]
   __nv_bfloat16* k1[2]; __nv_bfloat16* v1[2];        // T1 staging [L][B][Hkv][cap1][D] (stream: [2][B][Hkv][cap1][D] in k1[0]/v1[0])
   int8_t* c2k[2]; int8_t* c2v[2];                      // T2 codes  [L][B][Hkv][cap2][D]
@@ -77,7 +80,8 @@ cudaError_t launch_append(const DevView& v, int layer, const void* k, const void
 cudaError_t launch_load_prefix(const DevView& v, int layer, const void* k, const void* vv, int n0, cudaStream_t s);
 cudaError_t launch_init_meta(const DevView& v, int n0, cudaStream_t s);
 cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
-                               void* o, int fuse, int pdl, cudaStream_t s);
+                               void* o, int zpar, int prev_zpar, int pdl, cudaStream_t s);
+cudaError_t launch_score_flush(const DevView& v, int zpar, cudaStream_t s);
 cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s);
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);
 cudaError_t launch_classify(const DevView& v, cudaStream_t s);

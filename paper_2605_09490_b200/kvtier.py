@@ -251,10 +251,7 @@ class KvTier:
         if self.cfg.split:
             return self.cfg.split
         units = self.cfg.num_requests * self.cfg.num_kv_heads
-        s = max(1, min(8, (2 * 148 + units - 1) // units))
-        while s < 16 and (self.cfg.max_tokens + s - 1) // s > 2048:
-            s += 1
-        return s
+        return max(1, min(8, (2 * 148 + units - 1) // units))
 
     def import_scores(self, S):
         S = np.ascontiguousarray(S, dtype=np.float32)
