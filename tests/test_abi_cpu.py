@@ -44,7 +44,8 @@ def test_sass_is_sm100a_and_uses_tensor_cores():
                          text=True, check=True).stdout
     assert "sm_100a" in out
     assert "HMMA" in out                 # mma.sync bf16 tiles in the decode kernel
-    assert "LDGSTS" in out               # cp.async ring
+    assert "UBLKCP" in out               # cp.async.bulk ring (TMA bulk copy engine)
+    assert "SYNCS" in out                # mbarrier full/empty pipeline
 
 
 def test_library_loads_and_versions():
