@@ -152,24 +152,51 @@ struct Seg {
 
 // Score pass of one layer over virtual tokens [i0, i1) of the flattened (unit, token) space
 // (called by the score warp of the next layer's kernel and by the end-of-step flush).
+// Batches of SB tokens per thread with every load hoisted (three dependent round trips per
+// batch: position, then S_part + logits, then the store).
 __device__ __forceinline__ void score_range(const DevView& v, const Seg& sg, int cur, int zpar, long long i0,
                                             long long i1, int lane0, int stride, bool& bad) {
+  constexpr int SB = 8;
   const float* zb = v.zbuf + (size_t)zpar * v.B * v.Hkv * v.zrows * 8;
   const float* ML = v.ml + (size_t)zpar * v.B * v.Hkv * 16;
-  for (long long i = i0 + lane0; i < i1; i += stride) {
-    const int u = (int)(i / sg.nvirt), t = (int)(i - (long long)u * sg.nvirt);
-    if (!sg.valid(t)) continue;
-    const int b = u / v.Hkv, g = u - b * v.Hkv;
-    const float* z = zb + ((size_t)u * v.zrows + t) * 8;
-    const float4 z0 = *reinterpret_cast<const float4*>(z);
-    const float4 z1 = *reinterpret_cast<const float4*>(z + 4);
-    const float* ml = ML + (size_t)u * 16;
-    const float zz[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
-    float inc = 0.f;
-    for (int h = 0; h < v.G; ++h) inc += exp2f(zz[h] - ml[h]) * ml[8 + h];
-    float* S = v.S + ((size_t)b * v.Hkv + g) * v.Nmax + sg.pos(v, cur, b, t);
-    *S = *S + inc;
-    bad |= !isfinite(inc);
+  for (long long base = i0 + lane0; base < i1; base += (long long)stride * SB) {
+    int pos[SB], uu[SB], tt[SB];
+#pragma unroll
+    for (int k = 0; k < SB; ++k) {
+      const long long i = base + (long long)k * stride;
+      pos[k] = -1;
+      uu[k] = 0;
+      tt[k] = 0;
+      if (i < i1) {
+        const int u = (int)(i / sg.nvirt), t = (int)(i - (long long)u * sg.nvirt);
+        uu[k] = u;
+        tt[k] = t;
+        if (sg.valid(t)) pos[k] = sg.pos(v, cur, u / v.Hkv, t);
+      }
+    }
+    float sv[SB];
+    float4 z0[SB], z1[SB];
+#pragma unroll
+    for (int k = 0; k < SB; ++k) {
+      if (pos[k] >= 0) {
+        sv[k] = v.S[(size_t)uu[k] * v.Nmax + pos[k]];     // S_part[b][g] rows are unit-major
+        const float* z = zb + ((size_t)uu[k] * v.zrows + tt[k]) * 8;
+        z0[k] = *reinterpret_cast<const float4*>(z);
+        z1[k] = *reinterpret_cast<const float4*>(z + 4);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < SB; ++k) {
+      if (pos[k] < 0) continue;
+      const float* ml = ML + (size_t)uu[k] * 16;
+      const float zz[8] = {z0[k].x, z0[k].y, z0[k].z, z0[k].w, z1[k].x, z1[k].y, z1[k].z, z1[k].w};
+      float inc = 0.f;
+#pragma unroll
+      for (int h = 0; h < 8; ++h)
+        if (h < v.G) inc += exp2f(zz[h] - ml[h]) * ml[8 + h];
+      v.S[(size_t)uu[k] * v.Nmax + pos[k]] = sv[k] + inc;
+      bad |= !isfinite(inc);
+    }
   }
 }
 
@@ -680,7 +707,7 @@ cudaError_t launch_score_flush(const DevView& v, int zpar, cudaStream_t s) {
 
 // (consumer warps, stages) variants; DevView::variant selects one (0 = default)
 struct Variant { int nw, nst; };
-static constexpr Variant kVariants[] = {{4, 3}, {4, 4}, {8, 2}, {8, 3}, {4, 2}, {8, 4}};
+static constexpr Variant kVariants[] = {{4, 3}, {4, 4}, {8, 2}, {8, 3}, {4, 2}, {4, 6}};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 size_t attn_smem_bytes(const DevView& v) {
@@ -714,7 +741,7 @@ static cudaError_t launch_k(const DevView& v, cudaLaunchConfig_t& cfg, int layer
                             o, zpar, prev_zpar);
 }
 
-#define KVT_VARIANTS(X, D) X(D, 4, 3) X(D, 4, 4) X(D, 8, 2) X(D, 8, 3) X(D, 4, 2) X(D, 8, 4)
+#define KVT_VARIANTS(X, D) X(D, 4, 3) X(D, 4, 4) X(D, 8, 2) X(D, 8, 3) X(D, 4, 2) X(D, 4, 6)
 
 cudaError_t attn_configure(const DevView& v) {
   if (v.variant < 0 || v.variant >= kNumVariants) return cudaErrorInvalidValue;

@@ -139,7 +139,7 @@ def test_tiny_cluster_splits(split):          # DSMEM merge at several cluster s
 @pytest.mark.parametrize("variant", range(6))
 def test_multi_request_multi_layer_graph(variant):   # several tiles, ragged tails, B > 1, d = 128
     w = H.workload("tiny", B=3, L=2, Hq=12, Hkv=2, d=128, N=700, P=40, interval=16, steps=40,
-                   hbm_bp=3000, evict_bp=1000, t2_bp=0 if variant == 5 else 2500)
+                   hbm_bp=3000, evict_bp=1000, t2_bp=0 if variant == 3 else 2500)
     _run_pair(w, graph=True, check_every=7, variant=variant, split=(0, 4, 2, 3, 1, 16)[variant])
 
 
