@@ -118,13 +118,6 @@ __device__ __forceinline__ uint32_t i8pair_to_bf16x2(uint32_t word, int k) {
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
-__device__ __forceinline__ int atomic_add_cluster(int* local_ptr_in_rank0, int val) {
-  // DSMEM atomic on the rank-0 CTA's shared counter
-  cg::cluster_group cluster = cg::this_cluster();
-  int* p = cluster.map_shared_rank(local_ptr_in_rank0, 0);
-  return atomicAdd(p, val);
-}
-
 // Virtual-token bookkeeping shared by the decode kernel and the score pass.
 struct Seg {
   int n0o, n1, n2, a1, a2, a3, nvirt;
@@ -208,7 +201,6 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   // zpar: logits buffer of this launch (-1: no score update); prev_zpar: pending score pass
   // of the previous launch to apply in the background (-1: none)
   constexpr int NCONS = NW * 32;              // consumer threads
-  constexpr int NTHR = NCONS + 64;            // + producer warp + score warp
   constexpr int WPROD = NW, WSCORE = NW + 1;
   constexpr int TILE = NW * 16;
   constexpr int ROWB = D * 2;
@@ -233,8 +225,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   unsigned long long* bars =
       reinterpret_cast<unsigned long long*>(t2w + (v.cap2 > 0 ? NW * 16 * ROWB : 0));   // full, empty
   int* stile = reinterpret_cast<int*>(bars + 2 * NST);                    // [NST] tile of each stage
-  int* sctr = stile + NST;                                                // cluster tile counter (rank 0)
-  float* xo = reinterpret_cast<float*>(sctr + 4);                         // [8][D] exchange: o partial
+  float* xo = reinterpret_cast<float*>(stile + NST + 4);                 // [8][D] CTA partial o
   float* xm = xo + 8 * D;                                                 // [8]  exchange: max (log2)
   float* xl = xm + 8;                                                     // [8]  exchange: sum
   float* redm = xl + 8;                                                   // [NW][8] warp max
@@ -242,6 +233,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   float* sML = redl + 8 * NW;                                             // [16] merged M, 1/L
   float* nrow = sML + 16;                                                 // [2][D] new token K, V
   float* zn = nrow + 2 * D;                                               // [8] new token logits
+  float* rbuf = zn + 8;                                                   // [C][RB] pushed partials
 
   // ---------------------------------------------------------------- prologue (pre-PDL-wait)
   const int cur = v.st->cur;
@@ -273,20 +265,19 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       mbar_init(full0 + 8 * s2, 1);
       mbar_init(empty0 + 8 * s2, NW);
     }
-    *sctr = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  // cluster barrier #1 (split): counter initialised before any producer claims
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  __syncthreads();
 
   if (w == WPROD) {
     // ============================ producer ============================
+    // tiles are dealt round-robin to the cluster's CTAs (tile k -> rank k mod C): balanced,
+    // and deterministic (the fp32 summation order never depends on timing)
     if (lane == 0) {
       for (int i = 0;; ++i) {
         const int s2 = i % NST;
         if (i >= NST) mbar_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
-        const int k = atomic_add_cluster(sctr, 1);
+        const int k = r + i * C;
         const uint32_t full = full0 + 8 * s2, dst = ring_s + s2 * STAGEB;
         if (k >= ntiles) {
           stile[s2] = -1;
@@ -324,15 +315,18 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       }
     }
     __syncwarp();
+    // the producer never reads remote shared memory: arrive on the merge barrier and leave
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    return;
   }
   pdl_trigger();
   // ---------------------------------------------------------------- dependent inputs
   pdl_wait();
   if (tr && tid == 0) tr[1] = gtimer();
 
-  bool bad = false;
   if (w == WSCORE) {
     // ============================ score warp: previous layer's S_part update ============================
+    bool bad = false;
     if (prev_zpar >= 0) {
       const long long tot = (long long)v.B * v.Hkv * sg.nvirt;
       const long long ncta = (long long)gridDim.x * gridDim.y;
@@ -340,353 +334,294 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       const long long per = (tot + ncta - 1) / ncta;
       score_range(v, sg, cur, prev_zpar, cid * per, min(tot, (cid + 1) * per), lane, 32, bad);
     }
+    if (bad) atomicOr(&v.st->err, 1);
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    return;
   }
 
+  // ============================ consumers ============================
   float mxa = -INFINITY, mxb = -INFINITY;   // per-warp running max, heads 2tq, 2tq+1 (log2)
   float la = 0.f, lb = 0.f;                 // per-thread partial sums
   float oacc[KS][4];
 #pragma unroll
   for (int mt = 0; mt < KS; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
-
-  if (w < NW) {
-    // ============================ consumers ============================
-    uint32_t qf[KS][2];
-    {
-      const __nv_bfloat16* qh = q + ((size_t)b * v.Hq + g * G + gq) * D;
+  uint32_t qf[KS][2];
+  {
+    const __nv_bfloat16* qh = q + ((size_t)b * v.Hq + g * G + gq) * D;
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        if (gq < G) {
-          qf[ks][0] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 2 * tq);
-          qf[ks][1] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 8 + 2 * tq);
-        } else {
-          qf[ks][0] = 0u;
-          qf[ks][1] = 0u;
-        }
+    for (int ks = 0; ks < KS; ++ks) {
+      if (gq < G) {
+        qf[ks][0] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 2 * tq);
+        qf[ks][1] = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 8 + 2 * tq);
+      } else {
+        qf[ks][0] = 0u;
+        qf[ks][1] = 0u;
       }
     }
-    const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));   // log2(e)/sqrt(d)
-    float* zrow = zpar >= 0 ? v.zbuf + ((size_t)zpar * v.B * v.Hkv + unit) * v.zrows * 8 : nullptr;
+  }
+  const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));   // log2(e)/sqrt(d)
+  float* zrow = zpar >= 0 ? v.zbuf + ((size_t)zpar * v.B * v.Hkv + unit) * v.zrows * 8 : nullptr;
 
-    if (has_new) {   // new token (a1): append its row to T0 row n0-1 (swizzled), keep it in SMEM
-      uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[cur]) + (grp * v.cap0 + sg.n0o) * D;
-      uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[cur]) + (grp * v.cap0 + sg.n0o) * D;
-      const uint16_t* kin = knew ? reinterpret_cast<const uint16_t*>(knew) + ((size_t)b * v.Hkv + g) * D : nullptr;
-      const uint16_t* vin = vnew ? reinterpret_cast<const uint16_t*>(vnew) + ((size_t)b * v.Hkv + g) * D : nullptr;
-      for (int e = tid; e < D; e += NCONS) {
-        const int se = swz_off(sg.n0o, e);
-        const uint16_t kb = kin ? kin[e] : K0w[se];
-        const uint16_t vb = vin ? vin[e] : V0w[se];
-        nrow[e] = bf16_bits_to_f(kb);
-        nrow[D + e] = bf16_bits_to_f(vb);
-        if (kin) K0w[se] = kb;
-        if (vin) V0w[se] = vb;
-      }
+  // ---- new token (a1 + its own attention term), warp 0 of rank 0, before the tiles:
+  //      append the row to T0 row n0-1 (swizzled); logits on CUDA cores in fp32
+  if (has_new && w == 0) {
+    uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[cur]) + (grp * v.cap0 + sg.n0o) * D;
+    uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[cur]) + (grp * v.cap0 + sg.n0o) * D;
+    const uint16_t* kin = knew ? reinterpret_cast<const uint16_t*>(knew) + ((size_t)b * v.Hkv + g) * D : nullptr;
+    const uint16_t* vin = vnew ? reinterpret_cast<const uint16_t*>(vnew) + ((size_t)b * v.Hkv + g) * D : nullptr;
+    for (int e = lane; e < D; e += 32) {
+      const int se = swz_off(sg.n0o, e);
+      const uint16_t kb = kin ? kin[e] : K0w[se];
+      const uint16_t vb = vin ? vin[e] : V0w[se];
+      nrow[e] = bf16_bits_to_f(kb);
+      nrow[D + e] = bf16_bits_to_f(vb);
+      if (kin) K0w[se] = kb;
+      if (vin) V0w[se] = vb;
     }
-
-    // one warp-slice (16 rows) of a tile: logits, online softmax, P.V
-    auto do_rows = [&](uint32_t sK, uint32_t sV, int tv0, const float* scK, const float* scV, bool t2) {
-      const int r0 = w * 16 + gq, r1 = r0 + 8;
-      const int t0 = tv0 + r0, t1 = tv0 + r1;
-      const bool v0 = t2 ? (t0 - sg.a2 < sg.n2) : sg.bf16_valid(t0);
-      const bool v1 = t2 ? (t1 - sg.a2 < sg.n2) : sg.bf16_valid(t1);
-      if (!__any_sync(0xffffffffu, v0 || v1)) return;
-      float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
-      const int mi = lane >> 3, ii = lane & 7;
-      {
-        const int row = (t2 ? 0 : w * 16) + ii + ((mi & 1) << 3);
+    __syncwarp();
+    float part = 0.f;
 #pragma unroll
-        for (int ks = 0; ks < KS; ks += 2) {
-          uint32_t a0, a1_, a2_, a3_;
-          ldsm_x4(a0, a1_, a2_, a3_, sK + row * ROWB + (((2 * ks + (mi >> 1)) ^ (row & 7)) << 4));
-          mma16816(acc, a0, a1_, a2_, a3_, qf[ks][0], qf[ks][1]);
-          ldsm_x4(a0, a1_, a2_, a3_, sK + row * ROWB + (((2 * ks + 2 + (mi >> 1)) ^ (row & 7)) << 4));
-          mma16816(acc2, a0, a1_, a2_, a3_, qf[ks + 1][0], qf[ks + 1][1]);
-        }
+    for (int ks = 0; ks < KS; ++ks) {
+      const int d0 = ks * 16 + 2 * tq;
+      part += bf16lo(qf[ks][0]) * nrow[d0] + bf16hi(qf[ks][0]) * nrow[d0 + 1];
+      part += bf16lo(qf[ks][1]) * nrow[d0 + 8] + bf16hi(qf[ks][1]) * nrow[d0 + 9];
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    if (tq == 0) {
+      zn[gq] = part * sl2;
+      if (zrow) zrow[(size_t)sg.a3 * 8 + gq] = part * sl2;
+    }
+    __syncwarp();
+    mxa = zn[2 * tq];
+    mxb = zn[2 * tq + 1];
+    la = gq == 0 ? 1.f : 0.f;                // p = exp2(z - max) = 1, counted once per head
+    lb = la;
+#pragma unroll
+    for (int mt = 0; mt < KS; ++mt) {
+      const float va = nrow[D + mt * 16 + gq], vb = nrow[D + mt * 16 + gq + 8];
+      oacc[mt][0] = va;
+      oacc[mt][1] = va;
+      oacc[mt][2] = vb;
+      oacc[mt][3] = vb;
+    }
+  }
+
+  // one warp-slice (16 rows) of a tile: logits, online softmax, P.V
+  auto online = [&](float z00, float z01, float z10, float z11, float& p00, float& p01, float& p10, float& p11) {
+    float ta = fmaxf(z00, z10), tb = fmaxf(z01, z11);
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      ta = fmaxf(ta, __shfl_xor_sync(0xffffffffu, ta, off));
+      tb = fmaxf(tb, __shfl_xor_sync(0xffffffffu, tb, off));
+    }
+    const float na = fmaxf(mxa, ta), nb = fmaxf(mxb, tb);     // finite: some row is valid
+    const float ca = exp2f(mxa - na), cb = exp2f(mxb - nb);   // 0 when the old max is -inf
+    mxa = na;
+    mxb = nb;
+#pragma unroll
+    for (int mt = 0; mt < KS; ++mt) {
+      oacc[mt][0] *= ca;
+      oacc[mt][2] *= ca;
+      oacc[mt][1] *= cb;
+      oacc[mt][3] *= cb;
+    }
+    p00 = exp2f(z00 - na);
+    p01 = exp2f(z01 - nb);
+    p10 = exp2f(z10 - na);
+    p11 = exp2f(z11 - nb);
+    la = la * ca + p00 + p10;
+    lb = lb * cb + p01 + p11;
+  };
+  const int mi = lane >> 3, ii = lane & 7;
+  auto qk = [&](uint32_t sK, int rowbase, float* acc) {
+    float acc2[4] = {0.f, 0.f, 0.f, 0.f};
+    const int row = rowbase + ii + ((mi & 1) << 3);
+#pragma unroll
+    for (int ks = 0; ks < KS; ks += 2) {
+      uint32_t a0, a1_, a2_, a3_;
+      ldsm_x4(a0, a1_, a2_, a3_, sK + row * ROWB + (((2 * ks + (mi >> 1)) ^ (row & 7)) << 4));
+      mma16816(acc, a0, a1_, a2_, a3_, qf[ks][0], qf[ks][1]);
+      ldsm_x4(a0, a1_, a2_, a3_, sK + row * ROWB + (((2 * ks + 2 + (mi >> 1)) ^ (row & 7)) << 4));
+      mma16816(acc2, a0, a1_, a2_, a3_, qf[ks + 1][0], qf[ks + 1][1]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] += acc2[j];
+  };
+  auto pv = [&](uint32_t sV, int rowbase, float p00, float p01, float p10, float p11) {
+    const uint32_t b0 = movm_t(pack_bf16(p00, p01));
+    const uint32_t b1 = movm_t(pack_bf16(p10, p11));
+    const int row = rowbase + ii + ((mi >> 1) << 3);
+#pragma unroll
+    for (int mt = 0; mt < KS; ++mt) {
+      uint32_t a0, a1_, a2_, a3_;
+      ldsm_x4_t(a0, a1_, a2_, a3_, sV + row * ROWB + (((2 * mt + (mi & 1)) ^ (row & 7)) << 4));
+      mma16816(oacc[mt], a0, a1_, a2_, a3_, b0, b1);
+    }
+  };
+  // this warp's 16 rows of int8 codes -> exact bf16 into its scratch (swizzled by row)
+  auto stage_t2_rows = [&](const int8_t* codes, unsigned char* scr) {
+    for (int e = lane; e < 16 * (D / 16); e += 32) {
+      const int row = e / (D / 16), j = e % (D / 16);
+      const uint4 cw = *reinterpret_cast<const uint4*>(codes + (size_t)(w * 16 + row) * D + 16 * j);
+      uint4 lo, hi;
+      lo.x = i8pair_to_bf16x2(cw.x, 0); lo.y = i8pair_to_bf16x2(cw.x, 1);
+      lo.z = i8pair_to_bf16x2(cw.y, 0); lo.w = i8pair_to_bf16x2(cw.y, 1);
+      hi.x = i8pair_to_bf16x2(cw.z, 0); hi.y = i8pair_to_bf16x2(cw.z, 1);
+      hi.z = i8pair_to_bf16x2(cw.w, 0); hi.w = i8pair_to_bf16x2(cw.w, 1);
+      *reinterpret_cast<uint4*>(scr + row * ROWB + (((2 * j) ^ (row & 7)) << 4)) = lo;
+      *reinterpret_cast<uint4*>(scr + row * ROWB + (((2 * j + 1) ^ (row & 7)) << 4)) = hi;
+    }
+    __syncwarp();
+  };
+
+  for (int i = 0;; ++i) {
+    const int s2 = i % NST;
+    mbar_wait(full0 + 8 * s2, (i / NST) & 1);
+    const int k = stile[s2];
+    if (k < 0) break;
+    if (tr && tid == 0 && i == 0) tr[2] = gtimer();
+    const uint32_t sK = ring_s + s2 * STAGEB, sV = sK + TILEB;
+    const bool t2 = k >= ntb;
+    const int tv0 = t2 ? sg.a2 + (k - ntb) * TILE : k * TILE;
+    const int r0 = w * 16 + gq, r1 = r0 + 8;
+    const int t0 = tv0 + r0, t1 = tv0 + r1;
+    const bool v0 = t2 ? (t0 - sg.a2 < sg.n2) : sg.bf16_valid(t0);
+    const bool v1 = t2 ? (t1 - sg.a2 < sg.n2) : sg.bf16_valid(t1);
+    if (__any_sync(0xffffffffu, v0 || v1)) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      float fk0 = sl2, fk1 = sl2, fv0 = 1.f, fv1 = 1.f;
+      unsigned char* scr = t2w + (size_t)w * 16 * ROWB;
+      if (!t2) {
+        qk(sK, w * 16, acc);
+      } else {
+        unsigned char* st = ring + s2 * STAGEB;
+        const float* scK = reinterpret_cast<const float*>(st + TILE * D);
+        const float* scV = reinterpret_cast<const float*>(st + TILEB + TILE * D);
+        fk0 = scK[r0] * sl2; fk1 = scK[r1] * sl2;
+        fv0 = scV[r0]; fv1 = scV[r1];
+        stage_t2_rows(reinterpret_cast<const int8_t*>(st), scr);
+        qk(smem_u32(scr), 0, acc);
       }
-      const float f0 = scK ? scK[r0] * sl2 : sl2, f1 = scK ? scK[r1] * sl2 : sl2;
-      const float z00 = v0 ? (acc[0] + acc2[0]) * f0 : -INFINITY, z01 = v0 ? (acc[1] + acc2[1]) * f0 : -INFINITY;
-      const float z10 = v1 ? (acc[2] + acc2[2]) * f1 : -INFINITY, z11 = v1 ? (acc[3] + acc2[3]) * f1 : -INFINITY;
+      const float z00 = v0 ? acc[0] * fk0 : -INFINITY, z01 = v0 ? acc[1] * fk0 : -INFINITY;
+      const float z10 = v1 ? acc[2] * fk1 : -INFINITY, z11 = v1 ? acc[3] * fk1 : -INFINITY;
       if (zrow) {
         if (v0) *reinterpret_cast<float2*>(zrow + (size_t)t0 * 8 + 2 * tq) = make_float2(z00, z01);
         if (v1) *reinterpret_cast<float2*>(zrow + (size_t)t1 * 8 + 2 * tq) = make_float2(z10, z11);
       }
-      float ta = fmaxf(z00, z10), tb = fmaxf(z01, z11);
-#pragma unroll
-      for (int off = 4; off < 32; off <<= 1) {
-        ta = fmaxf(ta, __shfl_xor_sync(0xffffffffu, ta, off));
-        tb = fmaxf(tb, __shfl_xor_sync(0xffffffffu, tb, off));
+      float p00, p01, p10, p11;
+      online(z00, z01, z10, z11, p00, p01, p10, p11);
+      if (!t2) {
+        pv(sV, w * 16, p00, p01, p10, p11);
+      } else {                    // o += p * scale_v * code (codes exact in bf16)
+        __syncwarp();
+        stage_t2_rows(reinterpret_cast<const int8_t*>(ring + s2 * STAGEB + TILEB), scr);
+        pv(smem_u32(scr), 0, p00 * fv0, p01 * fv0, p10 * fv1, p11 * fv1);
       }
-      const float na = fmaxf(mxa, ta), nb = fmaxf(mxb, tb);     // finite: some row is valid
-      const float ca = exp2f(mxa - na), cb = exp2f(mxb - nb);   // 0 when the old max is -inf
-      mxa = na;
-      mxb = nb;
-#pragma unroll
-      for (int mt = 0; mt < KS; ++mt) {
-        oacc[mt][0] *= ca;
-        oacc[mt][2] *= ca;
-        oacc[mt][1] *= cb;
-        oacc[mt][3] *= cb;
-      }
-      float p00 = exp2f(z00 - na), p01 = exp2f(z01 - nb), p10 = exp2f(z10 - na), p11 = exp2f(z11 - nb);
-      la = la * ca + p00 + p10;
-      lb = lb * cb + p01 + p11;
-      if (scV) {   // T2: o += p * scale_v * code  (codes are exact in bf16)
-        p00 *= scV[r0]; p01 *= scV[r0];
-        p10 *= scV[r1]; p11 *= scV[r1];
-      }
-      const uint32_t b0 = movm_t(pack_bf16(p00, p01));
-      const uint32_t b1 = movm_t(pack_bf16(p10, p11));
-      const int row = (t2 ? 0 : w * 16) + ii + ((mi >> 1) << 3);
-#pragma unroll
-      for (int mt = 0; mt < KS; ++mt) {
-        uint32_t a0, a1_, a2_, a3_;
-        ldsm_x4_t(a0, a1_, a2_, a3_, sV + row * ROWB + (((2 * mt + (mi & 1)) ^ (row & 7)) << 4));
-        mma16816(oacc[mt], a0, a1_, a2_, a3_, b0, b1);
-      }
-    };
-    // this warp's 16 rows of int8 codes -> exact bf16 into its scratch (swizzled by row)
-    auto stage_t2_rows = [&](const int8_t* codes, unsigned char* scr) {
-      for (int e = lane; e < 16 * (D / 16); e += 32) {
-        const int row = e / (D / 16), j = e % (D / 16);
-        const uint4 cw = *reinterpret_cast<const uint4*>(codes + (size_t)(w * 16 + row) * D + 16 * j);
-        uint4 lo, hi;
-        lo.x = i8pair_to_bf16x2(cw.x, 0); lo.y = i8pair_to_bf16x2(cw.x, 1);
-        lo.z = i8pair_to_bf16x2(cw.y, 0); lo.w = i8pair_to_bf16x2(cw.y, 1);
-        hi.x = i8pair_to_bf16x2(cw.z, 0); hi.y = i8pair_to_bf16x2(cw.z, 1);
-        hi.z = i8pair_to_bf16x2(cw.w, 0); hi.w = i8pair_to_bf16x2(cw.w, 1);
-        *reinterpret_cast<uint4*>(scr + row * ROWB + (((2 * j) ^ (row & 7)) << 4)) = lo;
-        *reinterpret_cast<uint4*>(scr + row * ROWB + (((2 * j + 1) ^ (row & 7)) << 4)) = hi;
-      }
-      __syncwarp();
-    };
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * s2);
+  }
+  if (tr && tid == 0) tr[3] = gtimer();
 
-    for (int i = 0;; ++i) {
-      const int s2 = i % NST;
-      mbar_wait(full0 + 8 * s2, (i / NST) & 1);
-      const int k = stile[s2];
-      if (k < 0) break;
-      if (tr && tid == 0 && i == 0) tr[2] = gtimer();
-      const uint32_t sK = ring_s + s2 * STAGEB, sV = sK + TILEB;
-      if (k < ntb) {
-        do_rows(sK, sV, k * TILE, nullptr, nullptr, false);
-      } else {
-        unsigned char* st = ring + s2 * STAGEB;
-        unsigned char* scr = t2w + (size_t)w * 16 * ROWB;
-        const float* scK = reinterpret_cast<const float*>(st + TILE * D);
-        const float* scV = reinterpret_cast<const float*>(st + TILEB + TILE * D);
-        // K codes -> scratch; logits; then V codes -> scratch; P.V (do_rows reads both via scratch)
-        stage_t2_rows(reinterpret_cast<const int8_t*>(st), scr);
-        // split do_rows: QK on K scratch, then restage V into the same scratch before P.V
-        {
-          const int tv0 = sg.a2 + (k - ntb) * TILE;
-          const int r0 = w * 16 + gq, r1 = r0 + 8;
-          const int t0 = tv0 + r0, t1 = tv0 + r1;
-          const bool v0 = t0 - sg.a2 < sg.n2, v1 = t1 - sg.a2 < sg.n2;
-          if (__any_sync(0xffffffffu, v0 || v1)) {
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            const int mi = lane >> 3, ii = lane & 7;
-            const uint32_t sscr = smem_u32(scr);
-            {
-              const int row = ii + ((mi & 1) << 3);
+  // ---- warps -> CTA partial (ring reused as [NW][8][D+4] fp32)
 #pragma unroll
-              for (int ks = 0; ks < KS; ++ks) {
-                uint32_t a0, a1_, a2_, a3_;
-                ldsm_x4(a0, a1_, a2_, a3_, sscr + row * ROWB + (((2 * ks + (mi >> 1)) ^ (row & 7)) << 4));
-                mma16816(acc, a0, a1_, a2_, a3_, qf[ks][0], qf[ks][1]);
-              }
-            }
-            const float z00 = v0 ? acc[0] * scK[r0] * sl2 : -INFINITY, z01 = v0 ? acc[1] * scK[r0] * sl2 : -INFINITY;
-            const float z10 = v1 ? acc[2] * scK[r1] * sl2 : -INFINITY, z11 = v1 ? acc[3] * scK[r1] * sl2 : -INFINITY;
-            if (zrow) {
-              if (v0) *reinterpret_cast<float2*>(zrow + (size_t)t0 * 8 + 2 * tq) = make_float2(z00, z01);
-              if (v1) *reinterpret_cast<float2*>(zrow + (size_t)t1 * 8 + 2 * tq) = make_float2(z10, z11);
-            }
-            float ta = fmaxf(z00, z10), tb = fmaxf(z01, z11);
+  for (int off = 4; off < 32; off <<= 1) {
+    la += __shfl_xor_sync(0xffffffffu, la, off);
+    lb += __shfl_xor_sync(0xffffffffu, lb, off);
+  }
+  named_sync(1, NCONS);                // every consumer is done with the ring
+  float* ow = reinterpret_cast<float*>(ring);
+  float* fw = ow + NW * 8 * OWS;       // [NW][8] warp factors exp2(m_w - M)
+  if (lane < 4) {
+    redm[w * 8 + 2 * lane] = mxa;
+    redm[w * 8 + 2 * lane + 1] = mxb;
+    redl[w * 8 + 2 * lane] = la;
+    redl[w * 8 + 2 * lane + 1] = lb;
+  }
 #pragma unroll
-            for (int off = 4; off < 32; off <<= 1) {
-              ta = fmaxf(ta, __shfl_xor_sync(0xffffffffu, ta, off));
-              tb = fmaxf(tb, __shfl_xor_sync(0xffffffffu, tb, off));
-            }
-            const float na = fmaxf(mxa, ta), nb = fmaxf(mxb, tb);
-            const float ca = exp2f(mxa - na), cb = exp2f(mxb - nb);
-            mxa = na;
-            mxb = nb;
+  for (int mt = 0; mt < KS; ++mt) {
+    float* o0 = ow + (w * 8 + 2 * tq) * OWS + mt * 16 + gq;
+    float* o1 = o0 + OWS;
+    o0[0] = oacc[mt][0];
+    o1[0] = oacc[mt][1];
+    o0[8] = oacc[mt][2];
+    o1[8] = oacc[mt][3];
+  }
+  named_sync(1, NCONS);
+  if (tid < 8 * NW) {                  // factors of every (warp, head)
+    const int ww = tid >> 3, h = tid & 7;
+    float M = -INFINITY;
 #pragma unroll
-            for (int mt = 0; mt < KS; ++mt) {
-              oacc[mt][0] *= ca;
-              oacc[mt][2] *= ca;
-              oacc[mt][1] *= cb;
-              oacc[mt][3] *= cb;
-            }
-            float p00 = exp2f(z00 - na), p01 = exp2f(z01 - nb), p10 = exp2f(z10 - na), p11 = exp2f(z11 - nb);
-            la = la * ca + p00 + p10;
-            lb = lb * cb + p01 + p11;
-            p00 *= scV[r0]; p01 *= scV[r0];
-            p10 *= scV[r1]; p11 *= scV[r1];
-            const uint32_t b0 = movm_t(pack_bf16(p00, p01));
-            const uint32_t b1 = movm_t(pack_bf16(p10, p11));
-            __syncwarp();
-            stage_t2_rows(reinterpret_cast<const int8_t*>(st + TILEB), scr);
-            const int row = ii + ((mi >> 1) << 3);
+    for (int x = 0; x < NW; ++x) M = fmaxf(M, redm[x * 8 + h]);
+    const float m = redm[ww * 8 + h];
+    fw[tid] = m == -INFINITY ? 0.f : exp2f(m - M);
+    if (ww == 0) xm[h] = M;
+  }
+  named_sync(1, NCONS);
+  if (tid < 8) {
+    float Ls = 0.f;
 #pragma unroll
-            for (int mt = 0; mt < KS; ++mt) {
-              uint32_t a0, a1_, a2_, a3_;
-              ldsm_x4_t(a0, a1_, a2_, a3_, sscr + row * ROWB + (((2 * mt + (mi & 1)) ^ (row & 7)) << 4));
-              mma16816(oacc[mt], a0, a1_, a2_, a3_, b0, b1);
-            }
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8 * s2);
+    for (int x = 0; x < NW; ++x) Ls += redl[x * 8 + tid] * fw[x * 8 + tid];
+    xl[tid] = Ls;
+  }
+  // ---- push this CTA's partial to every rank of the cluster (rank c receives slice c)
+  const int tot = G * D;
+  const int per = (((tot + C - 1) / C) + 3) & ~3;          // float4-aligned slice
+  const int RB = per + 16;                                  // + m[8], l[8]
+  for (int e = tid; e < C * per; e += NCONS) {
+    const int c = e / per, j = e - c * per, idx = c * per + j;
+    float a = 0.f;
+    if (idx < tot) {
+      const int h = idx / D, dd = idx - h * D;
+#pragma unroll
+      for (int x = 0; x < NW; ++x) a += fw[x * 8 + h] * ow[(x * 8 + h) * OWS + dd];
     }
-    if (tr && tid == 0) tr[3] = gtimer();
-
-    // new token: warp 0 of rank 0, CUDA cores, fp32 (rank-1 online update)
-    if (has_new) named_sync(1, NCONS);   // nrow visible
-    if (has_new && w == 0) {
-      float part = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const int d0 = ks * 16 + 2 * tq;
-        part += bf16lo(qf[ks][0]) * nrow[d0] + bf16hi(qf[ks][0]) * nrow[d0 + 1];
-        part += bf16lo(qf[ks][1]) * nrow[d0 + 8] + bf16hi(qf[ks][1]) * nrow[d0 + 9];
-      }
-      part += __shfl_xor_sync(0xffffffffu, part, 1);
-      part += __shfl_xor_sync(0xffffffffu, part, 2);
-      if (tq == 0) {
-        zn[gq] = part * sl2;
-        if (zrow) zrow[(size_t)sg.a3 * 8 + gq] = part * sl2;
-      }
-      __syncwarp();
-      const float za = zn[2 * tq], zb = zn[2 * tq + 1];
-      const float na = fmaxf(mxa, za), nb = fmaxf(mxb, zb);
-      const float ca = exp2f(mxa - na), cb = exp2f(mxb - nb);
-      mxa = na;
-      mxb = nb;
-      const float pa = exp2f(za - na), pb = exp2f(zb - nb);
-      la = la * ca + (gq == 0 ? pa : 0.f);       // counted once per head (lanes 0..3)
-      lb = lb * cb + (gq == 0 ? pb : 0.f);
-#pragma unroll
-      for (int mt = 0; mt < KS; ++mt) {
-        const float va = nrow[D + mt * 16 + gq], vb = nrow[D + mt * 16 + gq + 8];
-        oacc[mt][0] = oacc[mt][0] * ca + pa * va;
-        oacc[mt][1] = oacc[mt][1] * cb + pb * va;
-        oacc[mt][2] = oacc[mt][2] * ca + pa * vb;
-        oacc[mt][3] = oacc[mt][3] * cb + pb * vb;
-      }
-    }
-#pragma unroll
-    for (int off = 4; off < 32; off <<= 1) {
-      la += __shfl_xor_sync(0xffffffffu, la, off);
-      lb += __shfl_xor_sync(0xffffffffu, lb, off);
-    }
-    // ---- warps -> CTA partial (ring reused as [NW][8][D+4] fp32)
-    named_sync(1, NCONS);                // every consumer is done with the ring
-    float* ow = reinterpret_cast<float*>(ring);
-    if (lane < 4) {
-      redm[w * 8 + 2 * lane] = mxa;
-      redm[w * 8 + 2 * lane + 1] = mxb;
-      redl[w * 8 + 2 * lane] = la;
-      redl[w * 8 + 2 * lane + 1] = lb;
-    }
-#pragma unroll
-    for (int mt = 0; mt < KS; ++mt) {
-      float* o0 = ow + (w * 8 + 2 * tq) * OWS + mt * 16 + gq;
-      float* o1 = o0 + OWS;
-      o0[0] = oacc[mt][0];
-      o1[0] = oacc[mt][1];
-      o0[8] = oacc[mt][2];
-      o1[8] = oacc[mt][3];
-    }
-    named_sync(1, NCONS);
-    if (tid < 8) {
-      float M = -INFINITY;
-#pragma unroll
-      for (int ww = 0; ww < NW; ++ww) M = fmaxf(M, redm[ww * 8 + tid]);
-      float Ls = 0.f;
-#pragma unroll
-      for (int ww = 0; ww < NW; ++ww) {
-        const float m = redm[ww * 8 + tid];
-        if (m != -INFINITY) Ls += redl[ww * 8 + tid] * exp2f(m - M);
-      }
-      xm[tid] = M;
-      xl[tid] = Ls;
-    }
-    named_sync(1, NCONS);
-    for (int e = tid; e < G * D; e += NCONS) {
-      const int h = e / D, dd = e - h * D;
-      const float M = xm[h];
-      float a = 0.f;
-#pragma unroll
-      for (int ww = 0; ww < NW; ++ww) {
-        const float m = redm[ww * 8 + h];
-        if (m != -INFINITY) a += exp2f(m - M) * ow[(ww * 8 + h) * OWS + dd];
-      }
-      xo[e] = a;
-    }
+    cluster.map_shared_rank(rbuf, c)[r * RB + j] = a;
+  }
+  named_sync(1, NCONS);                // xl ready
+  for (int e = tid; e < 16 * C; e += NCONS) {
+    const int c = e >> 4, h = e & 15;
+    cluster.map_shared_rank(rbuf, c)[r * RB + per + h] = h < 8 ? xm[h] : xl[h - 8];
   }
   if (tr && tid == 0) tr[4] = gtimer();
-
-  // ---- cluster merge through distributed shared memory (all remote reads issued in parallel)
-  cluster.sync();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   if (tr && tid == 0) tr[5] = gtimer();
-  float* gm = reinterpret_cast<float*>(ring);   // [16][8] peers' m
-  float* gl = gm + 128;                          // [16][8] peers' l
-  float* gf = gm + 256;                          // [16][8] exp2(m_c - M) / L
-  if (tid < 8 * C) {
-    const int c = tid >> 3, h = tid & 7;
-    gm[tid] = cluster.map_shared_rank(xm, c)[h];
-    gl[tid] = cluster.map_shared_rank(xl, c)[h];
-  }
-  __syncthreads();
-  if (tid < 8) {
-    float M = -INFINITY;
-    for (int c = 0; c < C; ++c) M = fmaxf(M, gm[c * 8 + tid]);
-    float Ls = 0.f;
-    for (int c = 0; c < C; ++c) {
-      const float mc = gm[c * 8 + tid];
-      if (mc != -INFINITY) Ls += gl[c * 8 + tid] * exp2f(mc - M);
+
+  // ---- merge the C partials of this rank's slice (local shared memory only)
+  {
+    const int e0 = r * per;
+    for (int j = tid; j < per && e0 + j < tot; j += NCONS) {
+      const int e = e0 + j, h = e / D, dd = e - h * D;
+      float M = -INFINITY;
+      for (int c = 0; c < C; ++c) M = fmaxf(M, rbuf[c * RB + per + h]);
+      float Ls = 0.f, acc = 0.f;
+      for (int c = 0; c < C; ++c) {
+        const float mc = rbuf[c * RB + per + h];
+        const float f = mc == -INFINITY ? 0.f : exp2f(mc - M);
+        Ls += f * rbuf[c * RB + per + 8 + h];
+        acc += f * rbuf[c * RB + j];
+      }
+      const float val = acc / Ls;
+      const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
+      if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = val;
+      else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(val);
     }
-    sML[tid] = M;
-    sML[8 + tid] = 1.0f / Ls;
-    if (r == 0 && zpar >= 0) {     // publish (M, 1/L) for the deferred score pass
+    if (r == 0 && zpar >= 0 && tid < 8) {     // publish (M, 1/L) for the deferred score pass
+      float M = -INFINITY;
+      for (int c = 0; c < C; ++c) M = fmaxf(M, rbuf[c * RB + per + tid]);
+      float Ls = 0.f;
+      for (int c = 0; c < C; ++c) {
+        const float mc = rbuf[c * RB + per + tid];
+        if (mc != -INFINITY) Ls += exp2f(mc - M) * rbuf[c * RB + per + 8 + tid];
+      }
       float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
       ml[tid] = M;
       ml[8 + tid] = 1.0f / Ls;
     }
   }
-  __syncthreads();
-  if (tid < 8 * C) {
-    const int h = tid & 7;
-    const float mc = gm[tid];
-    gf[tid] = mc == -INFINITY ? 0.f : exp2f(mc - sML[h]) * sML[8 + h];
-  }
-  __syncthreads();
-  {
-    const int tot = G * D;
-    const int per = (tot + C - 1) / C;
-    const int e1 = min(tot, (r + 1) * per);
-    for (int e = r * per + tid; e < e1; e += NTHR) {
-      const int h = e / D;
-      float part[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c)
-        if (c < C) part[c] = cluster.map_shared_rank(xo, c)[e];
-      float acc = 0.f;
-#pragma unroll
-      for (int c = 0; c < 16; ++c)
-        if (c < C) acc += gf[c * 8 + h] * part[c];
-      const int dd = e - h * D;
-      const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
-      if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = acc;
-      else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(acc);
-    }
-  }
-  if (tr && tid == 0) tr[6] = gtimer();
-  if (bad) atomicOr(&v.st->err, 1);
-  cluster.sync();                 // peers' shared memory stays alive until every read is done
-  if (tr && tid == 0) tr[7] = gtimer();
+  if (tr && tid == 0) { tr[6] = gtimer(); tr[7] = tr[6]; }
 }
 
 // End-of-step flush of the last layer's deferred score update.
@@ -714,11 +649,13 @@ size_t attn_smem_bytes(const DevView& v) {
   const Variant vr = kVariants[v.variant];
   const int tile = 16 * vr.nw;
   const size_t ringb = (size_t)vr.nst * 2 * tile * v.D * 2 + (2 * vr.nst) * 8 + (vr.nst + 4) * 4 + 16;
-  const size_t xob = (size_t)8 * v.D * 4 + (8 + 8 + 16 * vr.nw + 16 + 2 * v.D + 8) * 4;
+  const int tot = v.G * v.D, per = (((tot + v.split - 1) / v.split) + 3) & ~3;
+  const size_t xob = (size_t)8 * v.D * 4 + (8 + 8 + 16 * vr.nw + 16 + 2 * v.D + 8) * 4 +
+                     (size_t)v.split * (per + 16) * 4;
   const size_t t2 = (v.cap2 > 0) ? (size_t)vr.nw * 16 * v.D * 2 : 0;
   size_t total = ringb + xob + t2;
-  const size_t ow = (size_t)vr.nw * 8 * (v.D + 4) * 4;   // end-of-kernel reuse of the ring
-  if (ow + 3 * 128 * 4 > (size_t)vr.nst * 2 * tile * v.D * 2) total += ow;   // (never for the shipped variants)
+  const size_t ow = (size_t)vr.nw * 8 * (v.D + 4) * 4 + vr.nw * 8 * 4;   // end-of-kernel reuse of the ring
+  if (ow > (size_t)vr.nst * 2 * tile * v.D * 2) total += ow;   // (never for the shipped variants)
   return total;
 }
 
