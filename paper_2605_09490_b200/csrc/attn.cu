@@ -216,7 +216,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int G = v.G;
-  unsigned long long* tr = v.trace ? v.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * NTRACE : nullptr;
+  unsigned long long* tr = v.trace ? v.trace + (((size_t)layer * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * NTRACE : nullptr;
   if (tr && tid == 0) tr[0] = gtimer();
 
   extern __shared__ __align__(128) unsigned char smem[];

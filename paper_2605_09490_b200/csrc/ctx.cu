@@ -270,7 +270,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     v.hs2v = reinterpret_cast<float*>(h + 2 * rows * v.D + rows * 4);
   }
   if (getenv("KVTIER_TRACE") && atoi(getenv("KVTIER_TRACE")) > 0) {
-    const size_t tb = (size_t)v.split * v.B * v.Hkv * 8 * sizeof(unsigned long long);
+    const size_t tb = (size_t)v.L * v.split * v.B * v.Hkv * 8 * sizeof(unsigned long long);
     if (cudaMalloc(&ctx->trace, tb) == cudaSuccess) { cudaMemset(ctx->trace, 0, tb); v.trace = ctx->trace; }
   }
   if (attn_smem_bytes(v) > 227 * 1024) {
@@ -740,7 +740,7 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
 
 kv_tier_status kv_tier_debug_trace(kv_tier_ctx* ctx, uint64_t* host_dst, size_t n) {
   if (!ctx || !host_dst) return fail(ctx, KV_TIER_E_INVAL, "null arg");
-  const size_t need = (size_t)ctx->v.split * ctx->v.B * ctx->v.Hkv * 8;
+  const size_t need = (size_t)ctx->v.L * ctx->v.split * ctx->v.B * ctx->v.Hkv * 8;
   if (!ctx->trace) return fail(ctx, KV_TIER_E_STATE, "tracing off (set KVTIER_TRACE=1 before kv_tier_init)");
   if (n != need) return fail(ctx, KV_TIER_E_INVAL, "trace needs %zu entries", need);
   cudaError_t e = cudaDeviceSynchronize();

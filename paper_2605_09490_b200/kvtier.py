@@ -242,10 +242,10 @@ class KvTier:
 
     def debug_trace(self):
         """[split*B*H_kv][8] %globaltimer ns checkpoints of the last decode_attention (KVTIER_TRACE=1)."""
-        n = self.cfg.num_requests * self.cfg.num_kv_heads * 8 * max(1, self._split())
+        n = self.cfg.num_layers * self.cfg.num_requests * self.cfg.num_kv_heads * 8 * max(1, self._split())
         buf = np.zeros(n, dtype=np.uint64)
         _check(load().kv_tier_debug_trace(self.ctx, buf.ctypes.data_as(C.c_void_p), n), self.ctx)
-        return buf.reshape(-1, 8)
+        return buf.reshape(self.cfg.num_layers, -1, 8)
 
     def _split(self):
         if self.cfg.split:
