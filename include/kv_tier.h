@@ -87,7 +87,7 @@ typedef struct {
   int32_t  device;           /* CUDA device ordinal                                   */
   int32_t  rank, world, shard;
   int32_t  out_fp32;         /* 1: o is fp32 [B][H_q][d]; 0: bf16                      */
-  int32_t  split;            /* CTAs per (request, kv head) cluster; 0 = auto          */
+  int32_t  split;            /* CTAs per (request, kv head), <= 64; 0 = auto            */
   int32_t  variant;          /* decode kernel (consumer warps, stages): 0 (4,3) 1 (4,4)
                                 2 (8,2) 3 (8,3) 4 (4,2) 5 (4,6)                        */
 } kv_tier_config;

@@ -1,24 +1,24 @@
 // a1 + a3 + a4: fused new-token append, GQA decode attention over the visible tiers, and the
 // cumulative score update (Eq. 1, Eq. 3, Prop. 1).
 //
-// One thread-block cluster of C CTAs per unit (request b, kv head g).  The unit's visible rows
-// are laid out virtually as [T0 rows except the new token | pad | T1 staging | pad | T2 int8 |
-// pad | new token], segments starting at multiples of 16, cut into tiles of TILE tokens.
+// C CTAs per unit (request b, kv head g).  The unit's visible rows are laid out virtually as
+// [T0 rows except the new token | pad | T1 staging | pad | T2 int8 | pad | new token],
+// segments starting at multiples of 16, cut into tiles of TILE tokens dealt round-robin to
+// the unit's CTAs (tile k -> CTA k mod C: balanced and deterministic).
 //
-//   producer warp   claims the next tile of its unit from a cluster-shared counter (DSMEM
-//                   atomic: CTAs that stream faster take more tiles, so the cluster finishes
-//                   together) and streams the tile's K rows and V rows with 1-D bulk async
-//                   copies (cp.async.bulk) into an NST-deep shared-memory ring guarded by
-//                   full/empty mbarriers.  Rows are stored pre-swizzled in HBM (16-B chunk c
-//                   of store row j at c ^ (j & 7)), so a linear copy is the conflict-free layout.
+//   producer warp   streams its tiles' K rows and V rows with 1-D bulk async copies
+//                   (cp.async.bulk) into an NST-deep shared-memory ring guarded by full/empty
+//                   mbarriers.  Rows are stored pre-swizzled in HBM (16-B chunk c of store
+//                   row j at c ^ (j & 7)), so a linear copy is the conflict-free layout.
 //   consumer warps  each owns 16 rows of a tile: S^T = K q^T on the tensor cores (mma.sync
 //                   m16n8k16 bf16, swap-AB: tokens = M, the G <= 8 heads of the group = N),
 //                   per-warp online softmax in fp32, o^T += V^T p^T (movmatrix.trans turns the
 //                   C fragment into the B fragment).  Logits (log2 domain) go to an
 //                   L2-resident buffer for the score update.
-//   merge           warps -> CTA (shared memory) -> cluster (distributed shared memory, all
-//                   remote reads issued in parallel); CTA r writes 1/C of o; rank 0 publishes
-//                   the global (max, 1/sum) per head.
+//   merge           warps -> CTA partial (shared memory) -> global partial slot; the LAST CTA
+//                   of the unit to finish (atomic counter) merges the C partials in rank order
+//                   (deterministic), writes o and the per-head (max, 1/sum).  Nobody waits for
+//                   a straggler: finished CTAs exit and free their SM for the next layer.
 //   score warp      meanwhile applies the PREVIOUS layer's cumulative score update:
 //                   S_part[b][g][pos] += sum_{h in g} exp2(z - M_h) / L_h (one fp32 add per
 //                   layer in layer order, AMB-14; every (b, g, pos) written by one thread ->
@@ -27,9 +27,6 @@
 // HBM traffic per launch = algorithmic bytes: every visible K/V row once, q, o, the new row,
 // and the 8 B score read+write per visible token per kv head (of the previous layer).
 #include "kv_internal.cuh"
-#include <cooperative_groups.h>
-
-namespace cg = cooperative_groups;
 
 namespace kvt {
 
@@ -208,9 +205,8 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   constexpr int STAGEB = 2 * TILEB;           // K tile + V tile
   constexpr int KS = D / 16;
   constexpr int OWS = D + 4;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int C = (int)cluster.num_blocks();
-  const int r = (int)cluster.block_rank();
+  const int C = (int)gridDim.x;
+  const int r = (int)blockIdx.x;
   const int unit = blockIdx.y;
   const int b = unit / v.Hkv, g = unit - b * v.Hkv;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -233,7 +229,6 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   float* sML = redl + 8 * NW;                                             // [16] merged M, 1/L
   float* nrow = sML + 16;                                                 // [2][D] new token K, V
   float* zn = nrow + 2 * D;                                               // [8] new token logits
-  float* rbuf = zn + 8;                                                   // [C][RB] pushed partials
 
   // ---------------------------------------------------------------- prologue (pre-PDL-wait)
   const int cur = v.st->cur;
@@ -271,7 +266,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
 
   if (w == WPROD) {
     // ============================ producer ============================
-    // tiles are dealt round-robin to the cluster's CTAs (tile k -> rank k mod C): balanced,
+    // tiles are dealt round-robin to the unit's CTAs (tile k -> rank k mod C): balanced,
     // and deterministic (the fp32 summation order never depends on timing)
     if (lane == 0) {
       for (int i = 0;; ++i) {
@@ -315,8 +310,6 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       }
     }
     __syncwarp();
-    // the producer never reads remote shared memory: arrive on the merge barrier and leave
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
     return;
   }
   pdl_trigger();
@@ -335,7 +328,6 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       score_range(v, sg, cur, prev_zpar, cid * per, min(tot, (cid + 1) * per), lane, 32, bad);
     }
     if (bad) atomicOr(&v.st->err, 1);
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
     return;
   }
 
@@ -565,61 +557,63 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     for (int x = 0; x < NW; ++x) Ls += redl[x * 8 + tid] * fw[x * 8 + tid];
     xl[tid] = Ls;
   }
-  // ---- push this CTA's partial to every rank of the cluster (rank c receives slice c)
+  // ---- CTA partial -> global slot [unit][rank]: (m[8], l[8], o[G][D])
   const int tot = G * D;
-  const int per = (((tot + C - 1) / C) + 3) & ~3;          // float4-aligned slice
-  const int RB = per + 16;                                  // + m[8], l[8]
-  for (int e = tid; e < C * per; e += NCONS) {
-    const int c = e / per, j = e - c * per, idx = c * per + j;
+  float* part = v.part + ((size_t)unit * C + r) * v.part_stride;
+  named_sync(1, NCONS);                // xm, xl ready
+  if (tid < 16) part[tid] = tid < 8 ? xm[tid] : xl[tid - 8];
+  for (int e = tid; e < tot; e += NCONS) {
+    const int h = e / D, dd = e - h * D;
     float a = 0.f;
-    if (idx < tot) {
-      const int h = idx / D, dd = idx - h * D;
 #pragma unroll
-      for (int x = 0; x < NW; ++x) a += fw[x * 8 + h] * ow[(x * 8 + h) * OWS + dd];
-    }
-    cluster.map_shared_rank(rbuf, c)[r * RB + j] = a;
+    for (int x = 0; x < NW; ++x) a += fw[x * 8 + h] * ow[(x * 8 + h) * OWS + dd];
+    part[16 + e] = a;
   }
-  named_sync(1, NCONS);                // xl ready
-  for (int e = tid; e < 16 * C; e += NCONS) {
-    const int c = e >> 4, h = e & 15;
-    cluster.map_shared_rank(rbuf, c)[r * RB + per + h] = h < 8 ? xm[h] : xl[h - 8];
+  __threadfence();
+  named_sync(1, NCONS);
+  int* sflag = reinterpret_cast<int*>(zn);
+  if (tid == 0) {
+    const int old = atomicAdd(v.unit_ctr + unit, 1);
+    const int last = old == C - 1;
+    if (last) v.unit_ctr[unit] = 0;     // reset for the next launch (nobody else touches it now)
+    *sflag = last;
   }
   if (tr && tid == 0) tr[4] = gtimer();
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  named_sync(1, NCONS);
+  if (!*sflag) return;                 // another CTA of the unit finishes the merge
+  __threadfence();
   if (tr && tid == 0) tr[5] = gtimer();
 
-  // ---- merge the C partials of this rank's slice (local shared memory only)
-  {
-    const int e0 = r * per;
-    for (int j = tid; j < per && e0 + j < tot; j += NCONS) {
-      const int e = e0 + j, h = e / D, dd = e - h * D;
-      float M = -INFINITY;
-      for (int c = 0; c < C; ++c) M = fmaxf(M, rbuf[c * RB + per + h]);
-      float Ls = 0.f, acc = 0.f;
-      for (int c = 0; c < C; ++c) {
-        const float mc = rbuf[c * RB + per + h];
-        const float f = mc == -INFINITY ? 0.f : exp2f(mc - M);
-        Ls += f * rbuf[c * RB + per + 8 + h];
-        acc += f * rbuf[c * RB + j];
-      }
-      const float val = acc / Ls;
-      const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
-      if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = val;
-      else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(val);
+  // ---- last CTA: merge the C partials in rank order (deterministic), write o and (M, 1/L)
+  const float* P = v.part + (size_t)unit * C * v.part_stride;
+  float* gmf = reinterpret_cast<float*>(ring);     // [C][8] factors exp2(m_c - M) / L
+  if (tid < 8) {
+    float M = -INFINITY;
+    for (int c = 0; c < C; ++c) M = fmaxf(M, __ldcg(P + (size_t)c * v.part_stride + tid));
+    float Ls = 0.f;
+    for (int c = 0; c < C; ++c) {
+      const float mc = __ldcg(P + (size_t)c * v.part_stride + tid);
+      if (mc != -INFINITY) Ls += exp2f(mc - M) * __ldcg(P + (size_t)c * v.part_stride + 8 + tid);
     }
-    if (r == 0 && zpar >= 0 && tid < 8) {     // publish (M, 1/L) for the deferred score pass
-      float M = -INFINITY;
-      for (int c = 0; c < C; ++c) M = fmaxf(M, rbuf[c * RB + per + tid]);
-      float Ls = 0.f;
-      for (int c = 0; c < C; ++c) {
-        const float mc = rbuf[c * RB + per + tid];
-        if (mc != -INFINITY) Ls += exp2f(mc - M) * rbuf[c * RB + per + 8 + tid];
-      }
+    const float invL = 1.0f / Ls;
+    for (int c = 0; c < C; ++c) {
+      const float mc = __ldcg(P + (size_t)c * v.part_stride + tid);
+      gmf[c * 8 + tid] = mc == -INFINITY ? 0.f : exp2f(mc - M) * invL;
+    }
+    if (zpar >= 0) {                   // publish (M, 1/L) for the deferred score pass
       float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
       ml[tid] = M;
-      ml[8 + tid] = 1.0f / Ls;
+      ml[8 + tid] = invL;
     }
+  }
+  named_sync(1, NCONS);
+  for (int e = tid; e < tot; e += NCONS) {
+    const int h = e / D, dd = e - h * D;
+    float acc = 0.f;
+    for (int c = 0; c < C; ++c) acc += gmf[c * 8 + h] * __ldcg(P + (size_t)c * v.part_stride + 16 + e);
+    const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
+    if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = acc;
+    else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(acc);
   }
   if (tr && tid == 0) { tr[6] = gtimer(); tr[7] = tr[6]; }
 }
@@ -649,9 +643,7 @@ size_t attn_smem_bytes(const DevView& v) {
   const Variant vr = kVariants[v.variant];
   const int tile = 16 * vr.nw;
   const size_t ringb = (size_t)vr.nst * 2 * tile * v.D * 2 + (2 * vr.nst) * 8 + (vr.nst + 4) * 4 + 16;
-  const int tot = v.G * v.D, per = (((tot + v.split - 1) / v.split) + 3) & ~3;
-  const size_t xob = (size_t)8 * v.D * 4 + (8 + 8 + 16 * vr.nw + 16 + 2 * v.D + 8) * 4 +
-                     (size_t)v.split * (per + 16) * 4;
+  const size_t xob = (size_t)8 * v.D * 4 + (8 + 8 + 16 * vr.nw + 16 + 2 * v.D + 8) * 4;
   const size_t t2 = (v.cap2 > 0) ? (size_t)vr.nw * 16 * v.D * 2 : 0;
   size_t total = ringb + xob + t2;
   const size_t ow = (size_t)vr.nw * 8 * (v.D + 4) * 4 + vr.nw * 8 * 4;   // end-of-kernel reuse of the ring
@@ -663,9 +655,6 @@ template <int D, int NW, int NST>
 static cudaError_t configure_k(const DevView& v) {
   cudaError_t e = cudaFuncSetAttribute(k_decode_attn<D, NW, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)attn_smem_bytes(v));
-  if (e != cudaSuccess) return e;
-  if (v.split > 8)
-    e = cudaFuncSetAttribute(k_decode_attn<D, NW, NST>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 
@@ -697,15 +686,11 @@ cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const
   cfg.gridDim = dim3(v.split, v.B * v.Hkv, 1);
   cfg.dynamicSmemBytes = attn_smem_bytes(v);
   cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = v.split;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl ? 2 : 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   const Variant vr = kVariants[v.variant];
 #define KVT_LAUNCH(DD, NWW, NSS)                          \
   if (v.D == DD && vr.nw == NWW && vr.nst == NSS)         \

@@ -89,7 +89,7 @@ kv_tier_status validate(const kv_tier_config* c) {
   if (c->staging_tokens != 0 && c->staging_tokens != KV_TIER_STAGING_ALL)
     return fail(nullptr, KV_TIER_E_INVAL, "staging_tokens must be 0 (stream) or KV_TIER_STAGING_ALL (differential)");
   if (c->shard != KV_TIER_SHARD_REQUEST) return fail(nullptr, KV_TIER_E_INVAL, "only request sharding is implemented");
-  if (c->split < 0 || c->split > 16) return fail(nullptr, KV_TIER_E_INVAL, "split must be in [0, 16]");
+  if (c->split < 0 || c->split > 64) return fail(nullptr, KV_TIER_E_INVAL, "split must be in [0, 64]");
   if (c->variant < 0 || c->variant > 5) return fail(nullptr, KV_TIER_E_INVAL, "variant must be in [0, 5]");
   return KV_TIER_OK;
 }
@@ -112,7 +112,8 @@ void capacities(const kv_tier_config& c, int* cap0, int* cap1, int* cap2) {
 
 struct Layout {
   size_t off_k0[2], off_v0[2], off_k1[2], off_v1[2], off_c2k[2], off_c2v[2], off_s2k[2], off_s2v[2];
-  size_t off_idx[2][3], off_vis[2], off_tier[2], off_row[2], off_cnt[2], off_S, off_fS, off_st, off_z, off_ml, total;
+  size_t off_idx[2][3], off_vis[2], off_tier[2], off_row[2], off_cnt[2], off_S, off_fS, off_st, off_z, off_ml;
+  size_t off_part, off_uctr, total;
   size_t b_t0, b_t1, b_t2, b_scores, b_meta;
 };
 
@@ -143,6 +144,8 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   L.off_S = take(BH * N * 4);
   L.off_z = take(2 * BH * (N + 64) * 8 * 4);     // deferred-score logits (two launches)
   L.off_ml = take(2 * BH * 16 * 4);
+  L.off_part = take(BH * 64 * (16 + 8 * D) * 4);   // per-CTA partials (split <= 64)
+  L.off_uctr = take(BH * 4);
   L.b_scores = o - s0; s0 = o;
   for (int i = 0; i < 2; ++i) {
     L.off_idx[i][0] = take(B * cap0 * 4);
@@ -246,6 +249,9 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.zbuf = reinterpret_cast<float*>(A + L.off_z);
   v.ml = reinterpret_cast<float*>(A + L.off_ml);
   v.zrows = cfg->max_tokens + 64;
+  v.part = reinterpret_cast<float*>(A + L.off_part);
+  v.part_stride = 16 + 8 * v.D;
+  v.unit_ctr = reinterpret_cast<int*>(A + L.off_uctr);
   v.fS = reinterpret_cast<float*>(A + L.off_fS);
   v.st = reinterpret_cast<DevState*>(A + L.off_st);
   // pinned, mapped host stores (NUMA placement follows the calling thread's node)

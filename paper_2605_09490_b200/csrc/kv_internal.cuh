@@ -34,6 +34,9 @@ struct DevView {
   float* zbuf;          // [2][B*Hkv][zrows][8] logits (log2 domain) of the last two launches
   float* ml;            // [2][B*Hkv][16] per-head (max, 1/sum) of the last two launches
   int zrows;            // virtual rows per unit (N_max + padding)
+  float* part;          // [B*Hkv][split][part_stride] per-CTA partials (m[8], l[8], o[G][D])
+  int part_stride;
+  int* unit_ctr;        // [B*Hkv] CTAs of the current launch that finished (reset by the last)
   __nv_bfloat16* k0[2]; __nv_bfloat16* v0[2];        // T0 store  [L][B][Hkv][cap0][D]
   __nv_bfloat16* k1[2]; __nv_bfloat16* v1[2];        // T1 staging [L][B][Hkv][cap1][D] (stream: [2][B][Hkv][cap1][D] in k1[0]/v1[0])
   int8_t* c2k[2]; int8_t* c2v[2];                      // T2 codes  [L][B][Hkv][cap2][D]
