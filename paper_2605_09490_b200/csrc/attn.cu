@@ -584,36 +584,70 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   __threadfence();
   if (tr && tid == 0) tr[5] = gtimer();
 
-  // ---- last CTA: merge the C partials in rank order (deterministic), write o and (M, 1/L)
+  // ---- last CTA: merge the C partials in rank order (deterministic), write o and (M, 1/L).
+  //      Partials are staged into shared memory (the free ring) with parallel 16-B loads, in
+  //      batches of CB ranks, so the merge costs ~one L2 round trip per batch.
   const float* P = v.part + (size_t)unit * C * v.part_stride;
-  float* gmf = reinterpret_cast<float*>(ring);     // [C][8] factors exp2(m_c - M) / L
-  if (tid < 8) {
+  const int ps4 = (16 + tot + 3) / 4;                 // float4s per partial actually used
+  const int ringf = NST * STAGEB / 4;                 // ring capacity in floats
+  const int CB = max(1, min(C, (ringf - 64 * 8 - 16) / (ps4 * 4)));
+  float* stg = reinterpret_cast<float*>(ring);        // [CB][ps4*4]
+  float* gmf = stg + CB * ps4 * 4;                    // [C <= 64][8] merge factors (fits: checked on host)
+  float* Mh = gmf + 64 * 8;                           // [16] M, 1/L
+  if (tid < 8) {                                      // M and L from the (m, l) heads of every partial
     float M = -INFINITY;
     for (int c = 0; c < C; ++c) M = fmaxf(M, __ldcg(P + (size_t)c * v.part_stride + tid));
-    float Ls = 0.f;
-    for (int c = 0; c < C; ++c) {
-      const float mc = __ldcg(P + (size_t)c * v.part_stride + tid);
-      if (mc != -INFINITY) Ls += exp2f(mc - M) * __ldcg(P + (size_t)c * v.part_stride + 8 + tid);
-    }
-    const float invL = 1.0f / Ls;
-    for (int c = 0; c < C; ++c) {
-      const float mc = __ldcg(P + (size_t)c * v.part_stride + tid);
-      gmf[c * 8 + tid] = mc == -INFINITY ? 0.f : exp2f(mc - M) * invL;
-    }
-    if (zpar >= 0) {                   // publish (M, 1/L) for the deferred score pass
-      float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
-      ml[tid] = M;
-      ml[8 + tid] = invL;
-    }
+    Mh[tid] = M;
   }
   named_sync(1, NCONS);
-  for (int e = tid; e < tot; e += NCONS) {
-    const int h = e / D, dd = e - h * D;
-    float acc = 0.f;
-    for (int c = 0; c < C; ++c) acc += gmf[c * 8 + h] * __ldcg(P + (size_t)c * v.part_stride + 16 + e);
-    const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
-    if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = acc;
-    else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(acc);
+  for (int i = tid; i < 8 * C; i += NCONS) {
+    const int c = i >> 3, h = i & 7;
+    const float mc = __ldcg(P + (size_t)c * v.part_stride + h);
+    gmf[i] = mc == -INFINITY ? 0.f : exp2f(mc - Mh[h]);   // exp2(m_c - M), before 1/L
+  }
+  named_sync(1, NCONS);
+  if (tid < 8) {
+    float Ls = 0.f;
+    for (int c = 0; c < C; ++c) Ls += gmf[c * 8 + tid] * __ldcg(P + (size_t)c * v.part_stride + 8 + tid);
+    Mh[8 + tid] = 1.0f / Ls;
+    if (zpar >= 0) {                   // publish (M, 1/L) for the deferred score pass
+      float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
+      ml[tid] = Mh[tid];
+      ml[8 + tid] = 1.0f / Ls;
+    }
+  }
+  float acc[8];
+  const int nel = (tot + NCONS - 1) / NCONS;          // <= 8 outputs per thread (G*D <= 1024)
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+  for (int c0 = 0; c0 < C; c0 += CB) {
+    const int cb = min(CB, C - c0);
+    named_sync(1, NCONS);                             // previous batch consumed
+    const float4* src = reinterpret_cast<const float4*>(P + (size_t)c0 * v.part_stride);
+    for (int i = tid; i < cb * ps4; i += NCONS) {
+      const int c = i / ps4, j = i - c * ps4;
+      reinterpret_cast<float4*>(stg)[i] = __ldcg(src + (size_t)c * (v.part_stride / 4) + j);
+    }
+    named_sync(1, NCONS);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = tid + k * NCONS;
+      if (k < nel && e < tot) {
+        const int h = e / D;
+        for (int c = 0; c < cb; ++c) acc[k] += gmf[(c0 + c) * 8 + h] * stg[c * ps4 * 4 + 16 + e];
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int e = tid + k * NCONS;
+    if (k < nel && e < tot) {
+      const int h = e / D, dd = e - h * D;
+      const float val = acc[k] * Mh[8 + h];
+      const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
+      if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = val;
+      else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(val);
+    }
   }
   if (tr && tid == 0) { tr[6] = gtimer(); tr[7] = tr[6]; }
 }
