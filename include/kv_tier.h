@@ -198,10 +198,10 @@ KV_TIER_API kv_tier_status kv_tier_position(const kv_tier_ctx* ctx, int32_t* n, 
 enum {
   KV_TIER_X_SCORES = 0,     /* fp32 [B][H_kv][n]   S_part (AMB-1)                        */
   KV_TIER_X_TIERS = 1,      /* u8   [B][n]                                                */
-  KV_TIER_X_IDX_T0 = 2,     /* i32  [B][|T0|] positions in store order (ascending)         */
+  KV_TIER_X_IDX_T0 = 2,     /* i32  [B][|T0|] positions, ascending (stores keep any order) */
   KV_TIER_X_IDX_T1 = 3,     /* i32  [B][|T1|]                                              */
   KV_TIER_X_IDX_T2 = 4,     /* i32  [B][|T2|]                                              */
-  KV_TIER_X_T0_ROWS = 5,    /* bf16 [B][H_kv][|T0|][2][d]  (K,V) in idx order, layer       */
+  KV_TIER_X_T0_ROWS = 5,    /* bf16 [B][H_kv][|T0|][2][d]  (K,V) in ascending position     */
   KV_TIER_X_T1_ROWS = 6,    /* bf16 [B][H_kv][|T1|][2][d]  from the pinned host store      */
   KV_TIER_X_STAGING = 7,    /* bf16 [B][H_kv][|T1|][2][d]  HBM staging (differential mode) */
   KV_TIER_X_T2_CODES = 8,   /* i8   [B][H_kv][|T2|][2][d]                                  */

@@ -239,9 +239,10 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   const int ntiles = ntb + nt2;
   const bool has_new = r == 0;                               // rank 0 handles the new token
 
+  const int sb = v.st->scur;                                 // row-store buffer
   const size_t grp = grp_of(v, layer, b, g);
-  const __nv_bfloat16* K0 = v.k0[cur] + grp * v.cap0 * D;
-  const __nv_bfloat16* V0 = v.v0[cur] + grp * v.cap0 * D;
+  const __nv_bfloat16* K0 = v.k0[sb] + grp * v.cap0 * D;
+  const __nv_bfloat16* V0 = v.v0[sb] + grp * v.cap0 * D;
   const __nv_bfloat16* K1;
   const __nv_bfloat16* V1;
   if (v.stream_mode) {
@@ -249,8 +250,8 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     K1 = v.k1[0] + sgi * v.cap1 * D;
     V1 = v.v1[0] + sgi * v.cap1 * D;
   } else {
-    K1 = v.k1[cur] + grp * v.cap1 * D;
-    V1 = v.v1[cur] + grp * v.cap1 * D;
+    K1 = v.k1[sb] + grp * v.cap1 * D;
+    V1 = v.v1[sb] + grp * v.cap1 * D;
   }
   const uint32_t ring_s = smem_u32(ring);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + NST);
@@ -297,10 +298,10 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
           }
         } else {                      // T2: int8 codes + fp32 scales (canonical layout)
           const int j0 = (k - ntb) * TILE;
-          const int8_t* CK = v.c2k[cur] + (grp * v.cap2 + j0) * D;
-          const int8_t* CV = v.c2v[cur] + (grp * v.cap2 + j0) * D;
-          const float* SK = v.s2k[cur] + grp * v.cap2 + j0;
-          const float* SV = v.s2v[cur] + grp * v.cap2 + j0;
+          const int8_t* CK = v.c2k[sb] + (grp * v.cap2 + j0) * D;
+          const int8_t* CV = v.c2v[sb] + (grp * v.cap2 + j0) * D;
+          const float* SK = v.s2k[sb] + grp * v.cap2 + j0;
+          const float* SV = v.s2v[sb] + grp * v.cap2 + j0;
           mbar_expect_tx(full, 2 * (TILE * D + TILE * 4));
           bulk_g2s(dst, CK, TILE * D, full);
           bulk_g2s(dst + TILE * D, SK, TILE * 4, full);
@@ -357,8 +358,8 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   // ---- new token (a1 + its own attention term), warp 0 of rank 0, before the tiles:
   //      append the row to T0 row n0-1 (swizzled); logits on CUDA cores in fp32
   if (has_new && w == 0) {
-    uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[cur]) + (grp * v.cap0 + sg.n0o) * D;
-    uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[cur]) + (grp * v.cap0 + sg.n0o) * D;
+    uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[sb]) + (grp * v.cap0 + sg.n0o) * D;
+    uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[sb]) + (grp * v.cap0 + sg.n0o) * D;
     const uint16_t* kin = knew ? reinterpret_cast<const uint16_t*>(knew) + ((size_t)b * v.Hkv + g) * D : nullptr;
     const uint16_t* vin = vnew ? reinterpret_cast<const uint16_t*>(vnew) + ((size_t)b * v.Hkv + g) * D : nullptr;
     for (int e = lane; e < D; e += 32) {
@@ -590,29 +591,28 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   const float* P = v.part + (size_t)unit * C * v.part_stride;
   const int ps4 = (16 + tot + 3) / 4;                 // float4s per partial actually used
   const int ringf = NST * STAGEB / 4;                 // ring capacity in floats
-  const int CB = max(1, min(C, (ringf - 64 * 8 - 16) / (ps4 * 4)));
+  const int CB = max(1, min(C, (ringf - 64 * 8 - 16 - 64 * 16) / (ps4 * 4)));
   float* stg = reinterpret_cast<float*>(ring);        // [CB][ps4*4]
   float* gmf = stg + CB * ps4 * 4;                    // [C <= 64][8] merge factors (fits: checked on host)
   float* Mh = gmf + 64 * 8;                           // [16] M, 1/L
-  if (tid < 8) {                                      // M and L from the (m, l) heads of every partial
+  float* hd = Mh + 16;                                // [C][16] (m, l) of every partial
+  for (int i = tid; i < 16 * C; i += NCONS) hd[i] = __ldcg(P + (size_t)(i >> 4) * v.part_stride + (i & 15));
+  named_sync(1, NCONS);
+  if (tid < 8) {                                      // M and 1/L per head, merge factors
     float M = -INFINITY;
-    for (int c = 0; c < C; ++c) M = fmaxf(M, __ldcg(P + (size_t)c * v.part_stride + tid));
-    Mh[tid] = M;
-  }
-  named_sync(1, NCONS);
-  for (int i = tid; i < 8 * C; i += NCONS) {
-    const int c = i >> 3, h = i & 7;
-    const float mc = __ldcg(P + (size_t)c * v.part_stride + h);
-    gmf[i] = mc == -INFINITY ? 0.f : exp2f(mc - Mh[h]);   // exp2(m_c - M), before 1/L
-  }
-  named_sync(1, NCONS);
-  if (tid < 8) {
+    for (int c = 0; c < C; ++c) M = fmaxf(M, hd[c * 16 + tid]);
     float Ls = 0.f;
-    for (int c = 0; c < C; ++c) Ls += gmf[c * 8 + tid] * __ldcg(P + (size_t)c * v.part_stride + 8 + tid);
+    for (int c = 0; c < C; ++c) {
+      const float mc = hd[c * 16 + tid];
+      const float f = mc == -INFINITY ? 0.f : exp2f(mc - M);
+      gmf[c * 8 + tid] = f;                           // exp2(m_c - M), before 1/L
+      Ls += f * hd[c * 16 + 8 + tid];
+    }
+    Mh[tid] = M;
     Mh[8 + tid] = 1.0f / Ls;
     if (zpar >= 0) {                   // publish (M, 1/L) for the deferred score pass
       float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
-      ml[tid] = Mh[tid];
+      ml[tid] = M;
       ml[8 + tid] = 1.0f / Ls;
     }
   }

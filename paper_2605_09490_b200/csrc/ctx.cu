@@ -113,9 +113,16 @@ void capacities(const kv_tier_config& c, int* cap0, int* cap1, int* cap2) {
 struct Layout {
   size_t off_k0[2], off_v0[2], off_k1[2], off_v1[2], off_c2k[2], off_c2v[2], off_s2k[2], off_s2v[2];
   size_t off_idx[2][3], off_vis[2], off_tier[2], off_row[2], off_cnt[2], off_S, off_fS, off_st, off_z, off_ml;
-  size_t off_part, off_uctr, total;
+  size_t off_part, off_uctr, off_moves, off_mcount, off_scratch, off_mtemp, total;
   size_t b_t0, b_t1, b_t2, b_scores, b_meta;
 };
+
+// Rows an incremental migrate may move per request; more -> full rebuild (first event).
+size_t mcap_of(const kv_tier_config& c) {
+  const char* ov = getenv("KVTIER_MCAP");                    // test hook: force the full-rebuild path
+  if (ov && atoi(ov) > 0) return (size_t)atoi(ov);
+  return std::max<size_t>(256, ((size_t)c.max_tokens / 8 + 15) / 16 * 16);
+}
 
 Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   Layout L{};
@@ -146,6 +153,11 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   L.off_ml = take(2 * BH * 16 * 4);
   L.off_part = take(BH * 64 * (16 + 8 * D) * 4);   // per-CTA partials (split <= 64)
   L.off_uctr = take(BH * 4);
+  const size_t mcap = mcap_of(c);
+  L.off_moves = take(B * mcap * 16);
+  L.off_mcount = take(B * 4);
+  L.off_scratch = take(B * N * 4);
+  L.off_mtemp = take(B * mcap * LBH / B * 2 * D * 2);
   L.b_scores = o - s0; s0 = o;
   for (int i = 0; i < 2; ++i) {
     L.off_idx[i][0] = take(B * cap0 * 4);
@@ -252,6 +264,11 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.part = reinterpret_cast<float*>(A + L.off_part);
   v.part_stride = 16 + 8 * v.D;
   v.unit_ctr = reinterpret_cast<int*>(A + L.off_uctr);
+  v.moves = reinterpret_cast<int4*>(A + L.off_moves);
+  v.mcount = reinterpret_cast<int*>(A + L.off_mcount);
+  v.mcap = (int)mcap_of(*cfg);
+  v.scratch = reinterpret_cast<int*>(A + L.off_scratch);
+  v.mtemp = reinterpret_cast<__nv_bfloat16*>(A + L.off_mtemp);
   v.fS = reinterpret_cast<float*>(A + L.off_fS);
   v.st = reinterpret_cast<DevState*>(A + L.off_st);
   // pinned, mapped host stores (NUMA placement follows the calling thread's node)
@@ -493,12 +510,16 @@ kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side) 
   if (!ctx->classified) return fail(ctx, KV_TIER_E_STATE, "migrate without a preceding classify");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(main_stream);
   cudaStream_t sd = reinterpret_cast<cudaStream_t>(side);
-  cudaError_t e = launch_migrate(ctx->v, ctx->cur, s);
+  // plan the new row layout; move only the rows that change (or rebuild when too many move)
+  cudaError_t e = launch_plan(ctx->v, s);
+  if (e == cudaSuccess) e = launch_moves(ctx->v, ctx->cur, s);
+  if (e == cudaSuccess) e = launch_migrate(ctx->v, ctx->cur, s);
+  if (e == cudaSuccess) e = launch_commit(ctx->v, s);
   if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_migrated, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, ctx->ev_migrated, 0);
+  if (e == cudaSuccess) e = launch_offload_moves(ctx->v, ctx->cur, sd);
   if (e == cudaSuccess) e = launch_offload_host(ctx->v, ctx->cur, sd);
   if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_offload_done, sd);
-  if (e == cudaSuccess) e = launch_commit(ctx->v, s);
   kv_tier_status st = cuda_check(ctx, e, "migrate");
   if (st) return st;
   ctx->offload_pending = true;
@@ -663,57 +684,78 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
   if (st) return st;
   const DevView& v = ctx->v;
   const int cur = ctx->cur;
+  DevState hs;
+  cudaError_t e = cudaMemcpy(&hs, v.st, sizeof(hs), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_check(ctx, e, "export state");
+  const int sb = hs.scur;              // row-store buffer
   const size_t B = v.B, H = v.Hkv, D = v.D, N = v.Nmax, n = ctx->n;
   char* out = reinterpret_cast<char*>(host_dst);
   auto d2h = [&](void* dst, const void* src, size_t nbytes) {
     return cudaMemcpy(dst, src, nbytes, cudaMemcpyDeviceToHost);
   };
-  cudaError_t e = cudaSuccess;
   const int cnts[3] = {ctx->c[0], ctx->c[1], ctx->c[2]};
   const int caps[3] = {v.cap0, v.cap1, v.cap2};
+  // store-order index list of tier T for request b and the permutation to ascending positions
+  auto order = [&](int T, size_t b, std::vector<int>& pos, std::vector<int>& perm) {
+    pos.assign((size_t)std::max(cnts[T], 1), 0);
+    cudaError_t ee = d2h(pos.data(), v.idx[cur][T] + b * caps[T], (size_t)cnts[T] * 4);
+    perm.resize(cnts[T]);
+    for (int j = 0; j < cnts[T]; ++j) perm[j] = j;
+    std::sort(perm.begin(), perm.end(), [&](int x, int y) { return pos[x] < pos[y]; });
+    return ee;
+  };
+  std::vector<int> pos, perm;
   if (what == KV_TIER_X_SCORES) {
     for (size_t bg = 0; bg < B * H && e == cudaSuccess; ++bg) e = d2h(out + bg * n * 4, v.S + bg * N, n * 4);
   } else if (what == KV_TIER_X_TIERS) {
     for (size_t b = 0; b < B && e == cudaSuccess; ++b) e = d2h(out + b * n, v.tier[cur] + b * N, n);
   } else if (what >= KV_TIER_X_IDX_T0 && what <= KV_TIER_X_IDX_T2) {
     const int T = what - KV_TIER_X_IDX_T0;
-    for (size_t b = 0; b < B && e == cudaSuccess; ++b)
-      e = d2h(out + b * cnts[T] * 4, v.idx[cur][T] + b * caps[T], (size_t)cnts[T] * 4);
+    for (size_t b = 0; b < B && e == cudaSuccess; ++b) {
+      e = order(T, b, pos, perm);
+      int* o32 = reinterpret_cast<int*>(out) + b * cnts[T];
+      for (int j = 0; j < cnts[T]; ++j) o32[j] = pos[perm[j]];
+    }
   } else if (what == KV_TIER_X_T0_ROWS || what == KV_TIER_X_STAGING) {
     const bool t0 = what == KV_TIER_X_T0_ROWS;
     if (!t0 && v.stream_mode) return fail(ctx, KV_TIER_E_STATE, "no persistent staging in stream mode");
-    const int cnt = t0 ? cnts[0] : cnts[1];
-    const int cap = t0 ? v.cap0 : v.cap1;
-    const __nv_bfloat16* Ks = t0 ? v.k0[cur] : v.k1[cur];
-    const __nv_bfloat16* Vs = t0 ? v.v0[cur] : v.v1[cur];
+    const int T = t0 ? 0 : 1;
+    const int cnt = cnts[T];
+    const int cap = caps[T];
+    const __nv_bfloat16* Ks = t0 ? v.k0[sb] : v.k1[sb];
+    const __nv_bfloat16* Vs = t0 ? v.v0[sb] : v.v1[sb];
     std::vector<uint16_t> tk((size_t)cnt * D), tv((size_t)cnt * D);
-    for (size_t b = 0; b < B && e == cudaSuccess; ++b)
+    for (size_t b = 0; b < B && e == cudaSuccess; ++b) {
+      e = order(T, b, pos, perm);
       for (size_t g = 0; g < H && e == cudaSuccess; ++g) {
         const size_t grp = ((size_t)layer * B + b) * H + g;
         e = d2h(tk.data(), Ks + grp * cap * D, tk.size() * 2);
         if (e == cudaSuccess) e = d2h(tv.data(), Vs + grp * cap * D, tv.size() * 2);
         uint16_t* o16 = reinterpret_cast<uint16_t*>(out) + ((b * H + g) * cnt) * 2 * D;
-        for (int j = 0; j < cnt; ++j)
+        for (int jj = 0; jj < cnt; ++jj) {
+          const int j = perm[jj];
           for (size_t el = 0; el < D; ++el) {     // undo the store swizzle
-            o16[(size_t)j * 2 * D + el] = tk[(size_t)j * D + swz_off(j, (int)el)];
-            o16[(size_t)j * 2 * D + D + el] = tv[(size_t)j * D + swz_off(j, (int)el)];
+            o16[(size_t)jj * 2 * D + el] = tk[(size_t)j * D + swz_off(j, (int)el)];
+            o16[(size_t)jj * 2 * D + D + el] = tv[(size_t)j * D + swz_off(j, (int)el)];
           }
+        }
       }
+    }
   } else if (what == KV_TIER_X_T1_ROWS) {
     const int cnt = cnts[1];
-    std::vector<int> idx((size_t)std::max(cnt, 1));
     const size_t rows = (size_t)v.L * B * H * N;
     const uint16_t* hk = reinterpret_cast<const uint16_t*>(ctx->host_t1);
     const uint16_t* hv = hk ? hk + rows * D : nullptr;
     if (cnt > 0 && !hk) return fail(ctx, KV_TIER_E_STATE, "no host T1 store");
     for (size_t b = 0; b < B && e == cudaSuccess; ++b) {
-      e = d2h(idx.data(), v.idx[cur][1] + b * v.cap1, (size_t)cnt * 4);
+      e = order(1, b, pos, perm);
       for (size_t g = 0; g < H && e == cudaSuccess; ++g) {
         const size_t grp = ((size_t)layer * B + b) * H + g;
         uint16_t* o16 = reinterpret_cast<uint16_t*>(out) + ((b * H + g) * cnt) * 2 * D;
-        for (int j = 0; j < cnt; ++j) {
-          memcpy(o16 + (size_t)j * 2 * D, hk + (grp * N + idx[j]) * D, D * 2);
-          memcpy(o16 + (size_t)j * 2 * D + D, hv + (grp * N + idx[j]) * D, D * 2);
+        for (int jj = 0; jj < cnt; ++jj) {
+          const int p = pos[perm[jj]];
+          memcpy(o16 + (size_t)jj * 2 * D, hk + (grp * N + p) * D, D * 2);
+          memcpy(o16 + (size_t)jj * 2 * D + D, hv + (grp * N + p) * D, D * 2);
         }
       }
     }
@@ -722,24 +764,26 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
     const bool codes = what == KV_TIER_X_T2_CODES;
     std::vector<int8_t> ck((size_t)cnt * D + 1), cv((size_t)cnt * D + 1);
     std::vector<float> sk((size_t)cnt + 1), sv((size_t)cnt + 1);
-    for (size_t b = 0; b < B && e == cudaSuccess; ++b)
+    for (size_t b = 0; b < B && e == cudaSuccess; ++b) {
+      e = order(2, b, pos, perm);
       for (size_t g = 0; g < H && e == cudaSuccess; ++g) {
         const size_t grp = ((size_t)layer * B + b) * H + g;
         if (codes) {
-          e = d2h(ck.data(), v.c2k[cur] + grp * v.cap2 * D, (size_t)cnt * D);
-          if (e == cudaSuccess) e = d2h(cv.data(), v.c2v[cur] + grp * v.cap2 * D, (size_t)cnt * D);
+          e = d2h(ck.data(), v.c2k[sb] + grp * v.cap2 * D, (size_t)cnt * D);
+          if (e == cudaSuccess) e = d2h(cv.data(), v.c2v[sb] + grp * v.cap2 * D, (size_t)cnt * D);
           int8_t* o8 = reinterpret_cast<int8_t*>(out) + ((b * H + g) * cnt) * 2 * D;
-          for (int j = 0; j < cnt; ++j) {
-            memcpy(o8 + (size_t)j * 2 * D, ck.data() + (size_t)j * D, D);
-            memcpy(o8 + (size_t)j * 2 * D + D, cv.data() + (size_t)j * D, D);
+          for (int jj = 0; jj < cnt; ++jj) {
+            memcpy(o8 + (size_t)jj * 2 * D, ck.data() + (size_t)perm[jj] * D, D);
+            memcpy(o8 + (size_t)jj * 2 * D + D, cv.data() + (size_t)perm[jj] * D, D);
           }
         } else {
-          e = d2h(sk.data(), v.s2k[cur] + grp * v.cap2, (size_t)cnt * 4);
-          if (e == cudaSuccess) e = d2h(sv.data(), v.s2v[cur] + grp * v.cap2, (size_t)cnt * 4);
+          e = d2h(sk.data(), v.s2k[sb] + grp * v.cap2, (size_t)cnt * 4);
+          if (e == cudaSuccess) e = d2h(sv.data(), v.s2v[sb] + grp * v.cap2, (size_t)cnt * 4);
           float* of = reinterpret_cast<float*>(out) + ((b * H + g) * cnt) * 2;
-          for (int j = 0; j < cnt; ++j) { of[2 * j] = sk[j]; of[2 * j + 1] = sv[j]; }
+          for (int jj = 0; jj < cnt; ++jj) { of[2 * jj] = sk[perm[jj]]; of[2 * jj + 1] = sv[perm[jj]]; }
         }
       }
+    }
   }
   return cuda_check(ctx, e, "export");
 }

@@ -16,7 +16,9 @@ struct DevState {
   int cur;          // ping-pong buffer holding the live stores / lists
   int n_event;      // n at the last committed manage event
   int err;          // sticky error bits: 1 = non-finite probability/score
-  int pad[3];
+  int scur;         // buffer holding the bf16/int8 row stores (flips only on a full rebuild)
+  int use_full;     // set by the migrate plan when the move list overflows -> full rebuild
+  int last_full;    // use_full of the last committed migrate (read by the offload kernels)
   unsigned long long d2h_rows;   // rows written to the pinned host stores
 };
 
@@ -37,6 +39,11 @@ struct DevView {
   float* part;          // [B*Hkv][split][part_stride] per-CTA partials (m[8], l[8], o[G][D])
   int part_stride;
   int* unit_ctr;        // [B*Hkv] CTAs of the current launch that finished (reset by the last)
+  int4* moves;          // [B][mcap] {src tier, src row, dst tier | dst row << 2, position}
+  int* mcount;          // [B] moves of the last plan (<= mcap)
+  int mcap;
+  int* scratch;         // [B][Nmax] plan scratch (hole rows)
+  __nv_bfloat16* mtemp; // [B][mcap][L][Hkv][2][D] rows in flight during an incremental migrate
   __nv_bfloat16* k0[2]; __nv_bfloat16* v0[2];        // T0 store  [L][B][Hkv][cap0][D]
   __nv_bfloat16* k1[2]; __nv_bfloat16* v1[2];        // T1 staging [L][B][Hkv][cap1][D] (stream: [2][B][Hkv][cap1][D] in k1[0]/v1[0])
   int8_t* c2k[2]; int8_t* c2v[2];                      // T2 codes  [L][B][Hkv][cap2][D]
@@ -89,6 +96,9 @@ cudaError_t launch_score_update(const DevView& v, int layer, const float* probs,
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);
 cudaError_t launch_classify(const DevView& v, cudaStream_t s);
 cudaError_t launch_migrate(const DevView& v, int cur, cudaStream_t s);
+cudaError_t launch_plan(const DevView& v, cudaStream_t s);
+cudaError_t launch_moves(const DevView& v, int cur, cudaStream_t s);
+cudaError_t launch_offload_moves(const DevView& v, int cur, cudaStream_t s);
 cudaError_t launch_offload_host(const DevView& v, int cur, cudaStream_t s);
 cudaError_t launch_commit(const DevView& v, cudaStream_t s);
 cudaError_t launch_prefetch(const DevView& v, int layer, cudaStream_t s);

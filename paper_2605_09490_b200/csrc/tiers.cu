@@ -37,8 +37,9 @@ __global__ void k_append(const DevView v, const int layer, const uint16_t* __res
   const int cur = v.st->cur;
   const int row = v.cnt[cur][b * CNT_STRIDE + 0] - 1;
   const size_t dst = (grp_of(v, layer, b, g) * v.cap0 + row) * v.D;
-  uint16_t* K = reinterpret_cast<uint16_t*>(v.k0[cur]);
-  uint16_t* V = reinterpret_cast<uint16_t*>(v.v0[cur]);
+  const int sb = v.st->scur;
+  uint16_t* K = reinterpret_cast<uint16_t*>(v.k0[sb]);
+  uint16_t* V = reinterpret_cast<uint16_t*>(v.v0[sb]);
   for (int e = threadIdx.x; e < v.D; e += blockDim.x) {
     K[dst + swz_off(row, e)] = k[(size_t)unit * v.D + e];
     V[dst + swz_off(row, e)] = vv[(size_t)unit * v.D + e];
@@ -88,6 +89,9 @@ __global__ void k_init_meta(const DevView v, const int n0) {
       v.st->cur = 0;
       v.st->n_event = n0;
       v.st->err = 0;
+      v.st->scur = 0;
+      v.st->use_full = 0;
+      v.st->last_full = 0;
       v.st->d2h_rows = 0ull;
     }
   }
@@ -318,26 +322,27 @@ __device__ __forceinline__ void store_bits(uint16_t* dst, const uint16_t* x, int
   }
 }
 
-// Source row (bf16 bit pattern) of position `pos` of layer/group `grp` in tier `ot`
-// with row `orow` of the buffer `cur`.  T2 sources return bf16(dequant) (AMB-12).
+// Source row (bf16 bit pattern, canonical element order) of position `pos` of layer/group
+// `grp` in tier `ot`, store row `orow` of the row-store buffer `sb`.  T2 sources return
+// bf16(dequant) (AMB-12); stream-mode T1 rows come from the pinned host store.
 template <int D>
-__device__ __forceinline__ void source_row(const DevView& v, int cur, int kv, size_t grp, int ot, int orow,
+__device__ __forceinline__ void source_row(const DevView& v, int sb, int kv, size_t grp, int ot, int orow,
                                            int pos, int lane, uint16_t* x) {
   constexpr int E = D / 32;
   if (ot == T0) {
-    const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v0[cur] : v.k0[cur]) + (grp * v.cap0 + orow) * D;
+    const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v0[sb] : v.k0[sb]) + (grp * v.cap0 + orow) * D;
     load_bits(x, s + swz_off(orow, lane * E), E);
   } else if (ot == T1) {
     if (v.stream_mode) {
       const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.hv1 : v.hk1) + (grp * v.Nmax + pos) * D;
       load_bits(x, s + lane * E, E);   // pinned host store: canonical layout
     } else {
-      const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v1[cur] : v.k1[cur]) + (grp * v.cap1 + orow) * D;
+      const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v1[sb] : v.k1[sb]) + (grp * v.cap1 + orow) * D;
       load_bits(x, s + swz_off(orow, lane * E), E);
     }
   } else {
-    const int8_t* c = (kv ? v.c2v[cur] : v.c2k[cur]) + (grp * v.cap2 + orow) * D + lane * E;
-    const float sc = (kv ? v.s2v[cur] : v.s2k[cur])[grp * v.cap2 + orow];
+    const int8_t* c = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + orow) * D + lane * E;
+    const float sc = (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + orow];
 #pragma unroll
     for (int k = 0; k < E; ++k) x[k] = f_to_bf16_bits(__fmul_rn((float)c[k], sc));
   }
@@ -366,17 +371,191 @@ __device__ __forceinline__ void quantize_row(const uint16_t* x, int8_t* codes, f
   *scale = sc;
 }
 
-// Rebuild the nxt stores from the cur ones (ping-pong): dst list z = 0 (T0 store),
-// 1 (T1 staging, differential mode), 2 (T2 store).  One warp per (row, K|V).
+// ------------------------------------------------------------------ a6 plan
+// New row layout of every tier store after a classify (one CTA per request).  Tokens that
+// stay in a store keep their row when it is below the new count; the free rows below the
+// new count ("holes", ascending) are filled first with the store's own tail rows, then
+// with the tokens entering the store (ascending position).  Emits the store-order index
+// lists and rowof of the nxt metadata buffer and the list of row moves; a move list longer
+// than mcap switches this migrate to a full rebuild into the other row-store buffer.
+constexpr int PLAN_THREADS = 1024;
+
+template <typename Flag, typename Act>
+__device__ __forceinline__ int block_compact(int lo, int hi, int* s_wsum, int* s_tot, Flag flag, Act act) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  int base = 0;
+  for (int c0 = lo; c0 < hi; c0 += PLAN_THREADS) {
+    const int i = c0 + tid;
+    const bool f = i < hi && flag(i);
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) s_wsum[w] = __popc(m);
+    __syncthreads();
+    if (w == 0) {
+      const int x = s_wsum[lane];
+      int inc = x;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += y;
+      }
+      s_wsum[lane] = inc - x;
+      if (lane == 31) *s_tot = inc;
+    }
+    __syncthreads();
+    if (f) act(i, base + s_wsum[w] + __popc(m & ((1u << lane) - 1u)));
+    base += *s_tot;
+    __syncthreads();
+  }
+  return base;
+}
+
+__global__ void __launch_bounds__(PLAN_THREADS) k_plan(const DevView v) {
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int cur = v.st->cur, nxt = cur ^ 1, n = v.st->n;
+  const uint8_t* told = v.tier[cur] + (size_t)b * v.Nmax;
+  const uint8_t* tnew = v.tier[nxt] + (size_t)b * v.Nmax;
+  const int* rold = v.rowof[cur] + (size_t)b * v.Nmax;
+  int* rnew = v.rowof[nxt] + (size_t)b * v.Nmax;
+  int* hole = v.scratch + (size_t)b * v.Nmax;
+  int4* mv = v.moves + (size_t)b * v.mcap;
+  __shared__ int s_wsum[32], s_tot, s_nm;
+  if (tid == 0) s_nm = 0;
+  __syncthreads();
+  const int caps[3] = {v.cap0, v.cap1, v.cap2};
+  for (int X = 0; X < 3; ++X) {
+    const int cap = caps[X];
+    if (cap == 0) continue;
+    const int c_old = v.cnt[cur][b * CNT_STRIDE + X], c_new = v.cnt[nxt][b * CNT_STRIDE + X];
+    const int* iold = v.idx[cur][X] + (size_t)b * cap;
+    int* inew = v.idx[nxt][X] + (size_t)b * cap;
+    auto kept = [&](int r) { return r < c_old && tnew[iold[r]] == X; };
+    // holes below the new count, ascending
+    block_compact(0, c_new, s_wsum, &s_tot, [&](int r) { return !kept(r); }, [&](int r, int k) { hole[k] = r; });
+    // kept in place
+    for (int r = tid; r < min(c_old, c_new); r += PLAN_THREADS)
+      if (kept(r)) {
+        inew[r] = iold[r];
+        rnew[iold[r]] = r;
+      }
+    __syncthreads();
+    const int m0 = s_nm;
+    // tail rows of the store -> holes
+    const int ntk = block_compact(c_new, c_old, s_wsum, &s_tot, [&](int r) { return kept(r); },
+                                  [&](int r, int k) {
+                                    const int pos = iold[r], dst = hole[k];
+                                    inew[dst] = pos;
+                                    rnew[pos] = dst;
+                                    if (m0 + k < v.mcap) mv[m0 + k] = make_int4(X, r, X | (dst << 2), pos);
+                                  });
+    // tokens entering the store -> remaining holes
+    const int nin = block_compact(0, n, s_wsum, &s_tot, [&](int p) { return tnew[p] == X && told[p] != X; },
+                                  [&](int p, int k) {
+                                    const int dst = hole[ntk + k];
+                                    inew[dst] = p;
+                                    rnew[p] = dst;
+                                    if (m0 + ntk + k < v.mcap)
+                                      mv[m0 + ntk + k] = make_int4(told[p], rold[p], X | (dst << 2), p);
+                                  });
+    if (tid == 0) s_nm = m0 + ntk + nin;
+    __syncthreads();
+  }
+  for (int p = tid; p < n; p += PLAN_THREADS)
+    if (tnew[p] == T3) rnew[p] = -1;
+  if (tid == 0) {
+    v.mcount[b] = min(s_nm, v.mcap);
+    if (s_nm > v.mcap) atomicOr(&v.st->use_full, 1);
+  }
+}
+
+// Incremental migrate, phase 1: every moved row (all layers, K and V) -> staging buffer in
+// the destination's format (bf16 canonical, or int8 codes + scale for T2).
+template <int D>
+__global__ void __launch_bounds__(256) k_move_gather(const DevView v, const int cur) {
+  constexpr int E = D / 32;
+  if (v.st->use_full) return;
+  const int b = blockIdx.z, lg = blockIdx.y, l = lg / v.Hkv, g = lg % v.Hkv;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = blockIdx.x * 8 + w;
+  if (m >= v.mcount[b]) return;
+  const int4 mv = v.moves[(size_t)b * v.mcap + m];
+  const int st = mv.x, srow = mv.y, dt = mv.z & 3, pos = mv.w;
+  if (st == T1 && dt == T1 && v.stream_mode) return;       // list-only move (rows live on the host)
+  const int sb = v.st->scur;
+  const size_t grp = grp_of(v, l, b, g);
+  uint16_t* tmp = reinterpret_cast<uint16_t*>(v.mtemp) + ((((size_t)b * v.mcap + m) * v.L + l) * v.Hkv + g) * 2 * D;
+  for (int kv = 0; kv < 2; ++kv) {
+    uint16_t* tk = tmp + kv * D;
+    if (dt == T2 && st == T2) {       // T2 -> T2: codes and scale verbatim
+      const int8_t* c = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + srow) * D + lane * E;
+      int8_t* o = reinterpret_cast<int8_t*>(tk) + lane * E;
+#pragma unroll
+      for (int k = 0; k < E; ++k) o[k] = c[k];
+      if (lane == 0) *reinterpret_cast<float*>(reinterpret_cast<int8_t*>(tk) + D) = (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + srow];
+    } else {
+      uint16_t x[E];
+      source_row<D>(v, sb, kv, grp, st, srow, pos, lane, x);
+      if (dt == T2) {
+        int8_t codes[E];
+        float sc;
+        quantize_row<D>(x, codes, &sc, lane);
+        int8_t* o = reinterpret_cast<int8_t*>(tk) + lane * E;
+#pragma unroll
+        for (int k = 0; k < E; ++k) o[k] = codes[k];
+        if (lane == 0) *reinterpret_cast<float*>(reinterpret_cast<int8_t*>(tk) + D) = sc;
+      } else {
+        store_bits(tk + lane * E, x, E);
+      }
+    }
+  }
+}
+
+// Incremental migrate, phase 2: staging buffer -> destination rows (same row-store buffer).
+template <int D>
+__global__ void __launch_bounds__(256) k_move_scatter(const DevView v, const int cur) {
+  constexpr int E = D / 32;
+  if (v.st->use_full) return;
+  const int b = blockIdx.z, lg = blockIdx.y, l = lg / v.Hkv, g = lg % v.Hkv;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = blockIdx.x * 8 + w;
+  if (m >= v.mcount[b]) return;
+  const int4 mv = v.moves[(size_t)b * v.mcap + m];
+  const int dt = mv.z & 3, drow = mv.z >> 2;
+  if (dt == T1 && v.stream_mode) return;                     // T1 rows live on the host
+  const int sb = v.st->scur;
+  const size_t grp = grp_of(v, l, b, g);
+  const uint16_t* tmp = reinterpret_cast<const uint16_t*>(v.mtemp) + ((((size_t)b * v.mcap + m) * v.L + l) * v.Hkv + g) * 2 * D;
+  for (int kv = 0; kv < 2; ++kv) {
+    const uint16_t* tk = tmp + kv * D;
+    if (dt == T2) {
+      const int8_t* c = reinterpret_cast<const int8_t*>(tk) + lane * E;
+      int8_t* o = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + drow) * D + lane * E;
+#pragma unroll
+      for (int k = 0; k < E; ++k) o[k] = c[k];
+      if (lane == 0) (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + drow] = *reinterpret_cast<const float*>(reinterpret_cast<const int8_t*>(tk) + D);
+    } else {
+      uint16_t x[E];
+      load_bits(x, tk + lane * E, E);
+      uint16_t* dst = dt == T0
+          ? reinterpret_cast<uint16_t*>(kv ? v.v0[sb] : v.k0[sb]) + (grp * v.cap0 + drow) * D
+          : reinterpret_cast<uint16_t*>(kv ? v.v1[sb] : v.k1[sb]) + (grp * v.cap1 + drow) * D;
+      store_bits(dst + swz_off(drow, lane * E), x, E);
+    }
+  }
+}
+
+// Full rebuild (when the move list overflowed, e.g. the first event): every row of the
+// planned layout is written into the other row-store buffer.  One warp per (row, K|V).
 template <int D>
 __global__ void __launch_bounds__(256) k_migrate(const DevView v, const int cur) {
   constexpr int E = D / 32;
+  if (!v.st->use_full) return;
   const int T = blockIdx.z;
   if (T == 1 && v.stream_mode) return;
   if (T == 2 && v.cap2 == 0) return;
   const int nxt = cur ^ 1;
+  const int sb = v.st->scur, db = sb ^ 1;
   const int grpi = blockIdx.y;
-  const int g = grpi % v.Hkv, b = (grpi / v.Hkv) % v.B;
+  const int b = (grpi / v.Hkv) % v.B;
   const size_t grp = (size_t)grpi;
   const int capT = T == 0 ? v.cap0 : (T == 1 ? v.cap1 : v.cap2);
   const int cntT = v.cnt[nxt][b * CNT_STRIDE + T];
@@ -389,16 +568,16 @@ __global__ void __launch_bounds__(256) k_migrate(const DevView v, const int cur)
     const int orow = v.rowof[cur][(size_t)b * v.Nmax + pos];
     for (int kv = 0; kv < 2; ++kv) {
       if (T == 2) {
-        int8_t* dc = (kv ? v.c2v[nxt] : v.c2k[nxt]) + (grp * v.cap2 + j) * D + lane * E;
-        float* ds = (kv ? v.s2v[nxt] : v.s2k[nxt]) + grp * v.cap2 + j;
+        int8_t* dc = (kv ? v.c2v[db] : v.c2k[db]) + (grp * v.cap2 + j) * D + lane * E;
+        float* ds = (kv ? v.s2v[db] : v.s2k[db]) + grp * v.cap2 + j;
         if (ot == T2) {
-          const int8_t* sc = (kv ? v.c2v[cur] : v.c2k[cur]) + (grp * v.cap2 + orow) * D + lane * E;
+          const int8_t* sc = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + orow) * D + lane * E;
 #pragma unroll
           for (int k = 0; k < E; ++k) dc[k] = sc[k];
-          if (lane == 0) *ds = (kv ? v.s2v[cur] : v.s2k[cur])[grp * v.cap2 + orow];
+          if (lane == 0) *ds = (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + orow];
         } else {
           uint16_t x[E];
-          source_row<D>(v, cur, kv, grp, ot, orow, pos, lane, x);
+          source_row<D>(v, sb, kv, grp, ot, orow, pos, lane, x);
           int8_t codes[E];
           float sc;
           quantize_row<D>(x, codes, &sc, lane);
@@ -408,26 +587,29 @@ __global__ void __launch_bounds__(256) k_migrate(const DevView v, const int cur)
         }
       } else {
         uint16_t x[E];
-        source_row<D>(v, cur, kv, grp, ot, orow, pos, lane, x);
+        source_row<D>(v, sb, kv, grp, ot, orow, pos, lane, x);
         uint16_t* dst = T == 0
-            ? reinterpret_cast<uint16_t*>(kv ? v.v0[nxt] : v.k0[nxt]) + (grp * v.cap0 + j) * D
-            : reinterpret_cast<uint16_t*>(kv ? v.v1[nxt] : v.k1[nxt]) + (grp * v.cap1 + j) * D;
+            ? reinterpret_cast<uint16_t*>(kv ? v.v0[db] : v.k0[db]) + (grp * v.cap0 + j) * D
+            : reinterpret_cast<uint16_t*>(kv ? v.v1[db] : v.k1[db]) + (grp * v.cap1 + j) * D;
         store_bits(dst + swz_off(j, lane * E), x, E);
       }
     }
   }
 }
 
-// Offload to the pinned host stores (zero-copy stores over the host link), on the
-// side stream: rows newly in T1 (paper: "Offload T1 entries") and new T2 codes.
+// Offload to the pinned host stores (zero-copy stores over the host link), on the side
+// stream after the commit: rows newly in T1 (paper: "Offload T1 entries") and new T2
+// codes.  Full-rebuild variant: scans the new T1/T2 lists.
 template <int D>
 __global__ void __launch_bounds__(256) k_offload_host(const DevView v, const int cur) {
   constexpr int E = D / 32;
+  if (!v.st->last_full) return;
   const int T = blockIdx.z + 1;            // 1: T1 rows, 2: T2 codes
   if (T == 2 && (v.cap2 == 0 || v.hc2k == nullptr)) return;
   const int nxt = cur ^ 1;
+  const int sb = v.st->scur;               // the rebuilt buffer (committed)
   const int grpi = blockIdx.y;
-  const int g = grpi % v.Hkv, b = (grpi / v.Hkv) % v.B;
+  const int b = (grpi / v.Hkv) % v.B;
   const size_t grp = (size_t)grpi;
   const int capT = T == 1 ? v.cap1 : v.cap2;
   const int cntT = v.cnt[nxt][b * CNT_STRIDE + T];
@@ -444,19 +626,19 @@ __global__ void __launch_bounds__(256) k_offload_host(const DevView v, const int
       if (T == 1) {
         uint16_t x[E];
         if (!v.stream_mode) {
-          const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v1[nxt] : v.k1[nxt]) + (grp * v.cap1 + j) * D;
+          const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v1[sb] : v.k1[sb]) + (grp * v.cap1 + j) * D;
           load_bits(x, s + swz_off(j, lane * E), E);
         } else {
-          source_row<D>(v, cur, kv, grp, ot, orow, pos, lane, x);
+          source_row<D>(v, sb ^ 1, kv, grp, ot, orow, pos, lane, x);   // pre-rebuild buffer
         }
         uint16_t* dst = reinterpret_cast<uint16_t*>(kv ? v.hv1 : v.hk1) + (grp * v.Nmax + pos) * D;
         store_bits(dst + lane * E, x, E);
       } else {
-        const int8_t* sc = (kv ? v.c2v[nxt] : v.c2k[nxt]) + (grp * v.cap2 + j) * D + lane * E;
+        const int8_t* sc = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + j) * D + lane * E;
         int8_t* dc = (kv ? v.hc2v : v.hc2k) + (grp * v.Nmax + pos) * D + lane * E;
 #pragma unroll
         for (int k = 0; k < E; ++k) dc[k] = sc[k];
-        if (lane == 0) (kv ? v.hs2v : v.hs2k)[grp * v.Nmax + pos] = (kv ? v.s2v[nxt] : v.s2k[nxt])[grp * v.cap2 + j];
+        if (lane == 0) (kv ? v.hs2v : v.hs2k)[grp * v.Nmax + pos] = (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + j];
       }
     }
     rows += 2;
@@ -464,10 +646,48 @@ __global__ void __launch_bounds__(256) k_offload_host(const DevView v, const int
   if (lane == 0 && rows) atomicAdd(&v.st->d2h_rows, rows);
 }
 
+// Incremental variant: only the moves into T1 / T2 from another tier, from the staging
+// buffer of the moves (still intact: the next migrate waits for this kernel).
+template <int D>
+__global__ void __launch_bounds__(256) k_offload_moves(const DevView v, const int cur) {
+  constexpr int E = D / 32;
+  if (v.st->last_full) return;
+  const int b = blockIdx.z, lg = blockIdx.y, l = lg / v.Hkv, g = lg % v.Hkv;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = blockIdx.x * 8 + w;
+  if (m >= v.mcount[b]) return;
+  const int4 mv = v.moves[(size_t)b * v.mcap + m];
+  const int st = mv.x, dt = mv.z & 3, pos = mv.w;
+  if (st == dt || dt == T0) return;
+  if (dt == T2 && v.hc2k == nullptr) return;
+  const size_t grp = grp_of(v, l, b, g);
+  const uint16_t* tmp = reinterpret_cast<const uint16_t*>(v.mtemp) + ((((size_t)b * v.mcap + m) * v.L + l) * v.Hkv + g) * 2 * D;
+  for (int kv = 0; kv < 2; ++kv) {
+    const uint16_t* tk = tmp + kv * D;
+    if (dt == T1) {
+      uint16_t x[E];
+      load_bits(x, tk + lane * E, E);
+      uint16_t* dst = reinterpret_cast<uint16_t*>(kv ? v.hv1 : v.hk1) + (grp * v.Nmax + pos) * D;
+      store_bits(dst + lane * E, x, E);
+    } else {
+      const int8_t* c = reinterpret_cast<const int8_t*>(tk) + lane * E;
+      int8_t* dc = (kv ? v.hc2v : v.hc2k) + (grp * v.Nmax + pos) * D + lane * E;
+#pragma unroll
+      for (int k = 0; k < E; ++k) dc[k] = c[k];
+      if (lane == 0) (kv ? v.hs2v : v.hs2k)[grp * v.Nmax + pos] = *reinterpret_cast<const float*>(reinterpret_cast<const int8_t*>(tk) + D);
+    }
+  }
+  if (lane == 0) atomicAdd(&v.st->d2h_rows, 2ull);
+}
+
 __global__ void k_commit(const DevView v) {
   if (threadIdx.x == 0) {
-    v.st->cur ^= 1;
-    v.st->n_event = v.st->n;
+    DevState* s = v.st;
+    s->cur ^= 1;
+    s->n_event = s->n;
+    s->last_full = s->use_full;
+    if (s->use_full) s->scur ^= 1;
+    s->use_full = 0;
   }
 }
 
@@ -544,6 +764,27 @@ cudaError_t launch_offload_host(const DevView& v, int cur, cudaStream_t s) {
   dim3 grid((capmax + 31) / 32, v.L * v.B * v.Hkv, 2);
   if (v.D == 128) k_offload_host<128><<<grid, 256, 0, s>>>(v, cur);
   else k_offload_host<64><<<grid, 256, 0, s>>>(v, cur);
+  return cudaGetLastError();
+}
+cudaError_t launch_plan(const DevView& v, cudaStream_t s) {
+  k_plan<<<v.B, PLAN_THREADS, 0, s>>>(v);
+  return cudaGetLastError();
+}
+cudaError_t launch_moves(const DevView& v, int cur, cudaStream_t s) {
+  dim3 grid((v.mcap + 7) / 8, v.L * v.Hkv, v.B);
+  if (v.D == 128) {
+    k_move_gather<128><<<grid, 256, 0, s>>>(v, cur);
+    k_move_scatter<128><<<grid, 256, 0, s>>>(v, cur);
+  } else {
+    k_move_gather<64><<<grid, 256, 0, s>>>(v, cur);
+    k_move_scatter<64><<<grid, 256, 0, s>>>(v, cur);
+  }
+  return cudaGetLastError();
+}
+cudaError_t launch_offload_moves(const DevView& v, int cur, cudaStream_t s) {
+  dim3 grid((v.mcap + 7) / 8, v.L * v.Hkv, v.B);
+  if (v.D == 128) k_offload_moves<128><<<grid, 256, 0, s>>>(v, cur);
+  else k_offload_moves<64><<<grid, 256, 0, s>>>(v, cur);
   return cudaGetLastError();
 }
 cudaError_t launch_commit(const DevView& v, cudaStream_t s) {

@@ -119,6 +119,12 @@ def test_tiny_t2_half():                      # f2 = 50 %: int8 T2 rows in atten
     _run_pair(H.workload("tiny", interval=8, t2_bp=5000))
 
 
+@pytest.mark.parametrize("mcap", ["4", "0"])
+def test_tiny_migrate_paths(mcap, monkeypatch):   # full rebuild (tiny move budget) vs incremental moves
+    monkeypatch.setenv("KVTIER_MCAP", mcap)
+    _run_pair(H.workload("tiny", interval=8, t2_bp=3000, B=2, L=2), graph=True)
+
+
 def test_tiny_per_event_mode():               # AMB-9 literal Alg. 1
     _run_pair(H.workload("tiny", interval=8, evict_mode=kt.EVICT_PER_EVENT, evict_bp=1000))
 
