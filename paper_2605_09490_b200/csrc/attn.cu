@@ -570,6 +570,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     for (int x = 0; x < NW; ++x) a += fw[x * 8 + h] * ow[(x * 8 + h) * OWS + dd];
     part[16 + e] = a;
   }
+  if (tr && tid == 0) tr[4] = gtimer();
   __threadfence();
   named_sync(1, NCONS);
   int* sflag = reinterpret_cast<int*>(zn);
@@ -579,11 +580,10 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     if (last) v.unit_ctr[unit] = 0;     // reset for the next launch (nobody else touches it now)
     *sflag = last;
   }
-  if (tr && tid == 0) tr[4] = gtimer();
   named_sync(1, NCONS);
+  if (tr && tid == 0) tr[5] = gtimer();
   if (!*sflag) return;                 // another CTA of the unit finishes the merge
   __threadfence();
-  if (tr && tid == 0) tr[5] = gtimer();
 
   // ---- last CTA: merge the C partials in rank order (deterministic), write o and (M, 1/L).
   //      Partials are staged into shared memory (the free ring) with parallel 16-B loads, in
@@ -616,6 +616,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       ml[8 + tid] = 1.0f / Ls;
     }
   }
+  if (tr && tid == 0) tr[6] = gtimer();
   float acc[8];
   const int nel = (tot + NCONS - 1) / NCONS;          // <= 8 outputs per thread (G*D <= 1024)
 #pragma unroll
@@ -649,7 +650,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(val);
     }
   }
-  if (tr && tid == 0) { tr[6] = gtimer(); tr[7] = tr[6]; }
+  if (tr && tid == 0) tr[7] = gtimer();
 }
 
 // End-of-step flush of the last layer's deferred score update.

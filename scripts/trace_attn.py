@@ -28,14 +28,18 @@ for _ in range(3):
     run.step()
 run.sync()
 tr = run.kv.debug_trace().astype(np.int64)        # [L][CTAs][8], last step
-names = ["start", "pdl_wait", "first_tile", "loop_done", "pushed", "merge_sync", "o_written"]
+names = ["start", "pdl_wait", "first_tile", "loop_done", "partial_written", "after_atomic", "merge_ML", "o_written"]
 t0 = tr[0, :, 0].min()
 rel = (tr - t0) / 1e3
 out = {"config": a.config, "split": a.split, "variant": a.variant, "ctas": int(tr.shape[1])}
 for l in (0, 1, 2, tr.shape[0] // 2, tr.shape[0] - 1):
-    out[f"L{l}"] = {n: [round(float(rel[l, :, i].min()), 2), round(float(np.median(rel[l, :, i])), 2),
-                        round(float(rel[l, :, i].max()), 2)] for i, n in enumerate(names)}
-ends = [float(rel[l, :, 6].max()) for l in range(tr.shape[0])]
+    d = {}
+    for i, n in enumerate(names):
+        col = rel[l, :, i]
+        col = col[tr[l, :, i] > 0]          # merge checkpoints exist only on the last CTA of a unit
+        d[n] = [round(float(col.min()), 2), round(float(np.median(col)), 2), round(float(col.max()), 2)] if col.size else None
+    out[f"L{l}"] = d
+ends = [float(rel[l, :, 7].max()) for l in range(tr.shape[0])]
 out["layer_end_deltas_us"] = [round(ends[l] - ends[l - 1], 2) for l in range(1, len(ends))]
 print(json.dumps(out))
 run.close()
