@@ -552,48 +552,52 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     if (ww == 0) xm[h] = M;
   }
   named_sync(1, NCONS);
+  // CTA partial, staged in shared memory as it goes to global: [m 8 | l 8 | o G*D]
+  const int tot = G * D;
+  const int ps4 = (16 + tot + 3) / 4;                 // float4s per partial
+  float* xp = xo;                                      // [16 + G*D] (xo has room for 8*D)
   if (tid < 8) {
     float Ls = 0.f;
 #pragma unroll
     for (int x = 0; x < NW; ++x) Ls += redl[x * 8 + tid] * fw[x * 8 + tid];
-    xl[tid] = Ls;
+    xp[tid] = xm[tid];
+    xp[8 + tid] = Ls;
   }
-  // ---- CTA partial -> global slot [unit][rank]: (m[8], l[8], o[G][D])
-  const int tot = G * D;
-  float* part = v.part + ((size_t)unit * C + r) * v.part_stride;
-  named_sync(1, NCONS);                // xm, xl ready
-  if (tid < 16) part[tid] = tid < 8 ? xm[tid] : xl[tid - 8];
   for (int e = tid; e < tot; e += NCONS) {
     const int h = e / D, dd = e - h * D;
     float a = 0.f;
 #pragma unroll
     for (int x = 0; x < NW; ++x) a += fw[x * 8 + h] * ow[(x * 8 + h) * OWS + dd];
-    part[16 + e] = a;
+    xp[16 + e] = a;
   }
   if (tr && tid == 0) tr[4] = gtimer();
-  __threadfence();
   named_sync(1, NCONS);
+  // warp 0 publishes it (one warp's 16-B stores, one fence) and takes the unit ticket
   int* sflag = reinterpret_cast<int*>(zn);
-  if (tid == 0) {
-    const int old = atomicAdd(v.unit_ctr + unit, 1);
-    const int last = old == C - 1;
-    if (last) v.unit_ctr[unit] = 0;     // reset for the next launch (nobody else touches it now)
-    *sflag = last;
+  if (w == 0) {
+    float4* part = reinterpret_cast<float4*>(v.part + ((size_t)unit * C + r) * v.part_stride);
+    for (int i = lane; i < ps4; i += 32) part[i] = reinterpret_cast<const float4*>(xp)[i];
+    __threadfence();
+    int last = 0;
+    if (lane == 0) {
+      last = atomicAdd(v.unit_ctr + unit, 1) == C - 1;
+      if (last) v.unit_ctr[unit] = 0;   // reset for the next launch (nobody else touches it now)
+      *sflag = last;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) __threadfence();          // acquire side: the other partials are in L2
   }
   named_sync(1, NCONS);
   if (tr && tid == 0) tr[5] = gtimer();
   if (!*sflag) return;                 // another CTA of the unit finishes the merge
-  __threadfence();
 
   // ---- last CTA: merge the C partials in rank order (deterministic), write o and (M, 1/L).
-  //      Partials are staged into shared memory (the free ring) with parallel 16-B loads, in
-  //      batches of CB ranks, so the merge costs ~one L2 round trip per batch.
+  //      Every partial is staged into shared memory with cp.async (one L2 round trip).
   const float* P = v.part + (size_t)unit * C * v.part_stride;
-  const int ps4 = (16 + tot + 3) / 4;                 // float4s per partial actually used
   const int ringf = NST * STAGEB / 4;                 // ring capacity in floats
   const int CB = max(1, min(C, (ringf - 64 * 8 - 16 - 64 * 16) / (ps4 * 4)));
   float* stg = reinterpret_cast<float*>(ring);        // [CB][ps4*4]
-  float* gmf = stg + CB * ps4 * 4;                    // [C <= 64][8] merge factors (fits: checked on host)
+  float* gmf = stg + CB * ps4 * 4;                    // [C <= 64][8] merge factors
   float* Mh = gmf + 64 * 8;                           // [16] M, 1/L
   float* hd = Mh + 16;                                // [C][16] (m, l) of every partial
   for (int i = tid; i < 16 * C; i += NCONS) hd[i] = __ldcg(P + (size_t)(i >> 4) * v.part_stride + (i & 15));
@@ -624,11 +628,14 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   for (int c0 = 0; c0 < C; c0 += CB) {
     const int cb = min(CB, C - c0);
     named_sync(1, NCONS);                             // previous batch consumed
-    const float4* src = reinterpret_cast<const float4*>(P + (size_t)c0 * v.part_stride);
+    const float* src = P + (size_t)c0 * v.part_stride;
     for (int i = tid; i < cb * ps4; i += NCONS) {
       const int c = i / ps4, j = i - c * ps4;
-      reinterpret_cast<float4*>(stg)[i] = __ldcg(src + (size_t)c * (v.part_stride / 4) + j);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(stg + 4 * (size_t)i)),
+                   "l"(src + (size_t)c * v.part_stride + 4 * j));
     }
+    cp_commit();
+    cp_wait<0>();
     named_sync(1, NCONS);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
