@@ -272,6 +272,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     if (lane == 0) {
       for (int i = 0;; ++i) {
         const int s2 = i % NST;
+        if (i == v.pdl_pre) pdl_wait();   // at most pdl_pre stages in flight before the previous layer ends
         if (i >= NST) mbar_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
         const int k = r + i * C;
         const uint32_t full = full0 + 8 * s2, dst = ring_s + s2 * STAGEB;
@@ -555,7 +556,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   // CTA partial, staged in shared memory as it goes to global: [m 8 | l 8 | o G*D]
   const int tot = G * D;
   const int ps4 = (16 + tot + 3) / 4;                 // float4s per partial
-  float* xp = xo;                                      // [16 + G*D] (xo has room for 8*D)
+  float* xp = fw + 8 * NW;                            // [16 + G*D] in the free ring (16-B aligned)
   if (tid < 8) {
     float Ls = 0.f;
 #pragma unroll

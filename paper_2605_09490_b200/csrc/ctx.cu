@@ -241,6 +241,8 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.out_fp32 = cfg->out_fp32;
   v.split = auto_split(*cfg);
   v.variant = cfg->variant;
+  v.pdl_pre = getenv("KVTIER_PDL_PRE") ? atoi(getenv("KVTIER_PDL_PRE")) : 1 << 30;
+  v.use_pdl = getenv("KVTIER_NOPDL") ? 0 : 1;
   v.chunk_max = 0;
   for (int i = 0; i < 2; ++i) {
     v.k0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_k0[i]);
@@ -550,7 +552,7 @@ kv_tier_status kv_tier_step(kv_tier_ctx* ctx, const void* q, const void* k_new, 
   // dependent launch (each kernel's prologue overlaps the previous layer's tail)
   for (int l = 0; l < v.L && !st; ++l) {
     st = decode_attention_impl(ctx, l, qb + l * qs * 2, kb + l * ks * 2, vb + l * ks * 2, ob + l * os,
-                               fuse_score_update, stream, l > 0 && !v.stream_mode);
+                               fuse_score_update, stream, v.use_pdl && l > 0 && !v.stream_mode);
     if (!st && v.stream_mode && l + 2 < v.L) st = kv_tier_prefetch(ctx, l + 2, side);
   }
   if (st) return st;

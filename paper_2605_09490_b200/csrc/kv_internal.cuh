@@ -32,6 +32,8 @@ struct DevView {
   int split;            // CTAs per (b, g) cluster
   int chunk_max;        // max tokens per CTA (logit buffer rows)
   int variant;          // decode-attention kernel variant (warps x pipeline stages)
+  int pdl_pre;          // stages the producer may load before griddepcontrol.wait
+  int use_pdl;          // chain consecutive layers with programmatic dependent launch
   unsigned long long* trace;   // debug: per-CTA %globaltimer checkpoints (null = off)
   float* zbuf;          // [2][B*Hkv][zrows][8] logits (log2 domain) of the last two launches
   float* ml;            // [2][B*Hkv][16] per-head (max, 1/sum) of the last two launches

@@ -19,8 +19,12 @@ ap.add_argument("--config", default="7b")
 ap.add_argument("--steps", type=int, default=48)
 ap.add_argument("--splits", default="1,2,3,4,6,8")
 ap.add_argument("--variants", default="0,1,2,3,4,5")
+ap.add_argument("--env", default="", help="KEY=VAL,... set before each ctx (e.g. KVTIER_PDL_PRE=1)")
 a = ap.parse_args()
 res = []
+for kv_ in [x for x in a.env.split(",") if x]:
+    k_, v_ = kv_.split("=")
+    os.environ[k_] = v_
 for split in [int(x) for x in a.splits.split(",")]:
     for var in [int(x) for x in a.variants.split(",")]:
         w = H.workload(a.config, steps=2 + a.steps)
