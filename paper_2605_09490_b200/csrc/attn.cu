@@ -571,94 +571,75 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     for (int x = 0; x < NW; ++x) a += fw[x * 8 + h] * ow[(x * 8 + h) * OWS + dd];
     xp[16 + e] = a;
   }
-  if (tr && tid == 0) tr[4] = gtimer();
   named_sync(1, NCONS);
-  // warp 0 publishes it (one warp's 16-B stores, one fence) and takes the unit ticket
-  int* sflag = reinterpret_cast<int*>(zn);
-  if (w == 0) {
+  {   // publish: visible to the merge kernel once this grid completes (no fence needed)
     float4* part = reinterpret_cast<float4*>(v.part + ((size_t)unit * C + r) * v.part_stride);
-    for (int i = lane; i < ps4; i += 32) part[i] = reinterpret_cast<const float4*>(xp)[i];
-    __threadfence();
-    int last = 0;
-    if (lane == 0) {
-      last = atomicAdd(v.unit_ctr + unit, 1) == C - 1;
-      if (last) v.unit_ctr[unit] = 0;   // reset for the next launch (nobody else touches it now)
-      *sflag = last;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) __threadfence();          // acquire side: the other partials are in L2
+    for (int i = tid; i < ps4; i += NCONS) part[i] = reinterpret_cast<const float4*>(xp)[i];
   }
-  named_sync(1, NCONS);
-  if (tr && tid == 0) tr[5] = gtimer();
-  if (!*sflag) return;                 // another CTA of the unit finishes the merge
+  if (tr && tid == 0) tr[4] = gtimer();
+}
 
-  // ---- last CTA: merge the C partials in rank order (deterministic), write o and (M, 1/L).
-  //      Every partial is staged into shared memory with cp.async (one L2 round trip).
+// Merge of the C per-CTA partials of every unit, in rank order (deterministic): o and the
+// per-head (max, 1/sum) for the deferred score pass.  Launched right behind the decode kernel
+// with programmatic dependent launch: its CTAs are resident early and start when it completes.
+template <int D>
+__global__ void __launch_bounds__(256) k_decode_merge(const DevView v, const int layer, void* __restrict__ o,
+                                                      const int zpar) {
+  const int unit = blockIdx.x, tid = threadIdx.x;
+  const int b = unit / v.Hkv, g = unit - b * v.Hkv;
+  const int G = v.G, C = v.split, tot = G * D;
+  const int ps4 = (16 + tot + 3) / 4;
+  extern __shared__ __align__(16) float msm[];
+  float* stg = msm;                                   // [C][ps4*4]
+  float* gmf = stg + (size_t)C * ps4 * 4;             // [C][8]
+  float* Mh = gmf + 8 * C;                            // [16]
+  unsigned long long* tr = v.trace ? v.trace + (((size_t)layer * v.B * v.Hkv + unit) * v.split) * 8 : nullptr;
+  pdl_trigger();
+  pdl_wait();
+  if (tr && tid == 0) tr[5] = gtimer();
   const float* P = v.part + (size_t)unit * C * v.part_stride;
-  const int ringf = NST * STAGEB / 4;                 // ring capacity in floats
-  const int CB = max(1, min(C, (ringf - 64 * 8 - 16 - 64 * 16) / (ps4 * 4)));
-  float* stg = reinterpret_cast<float*>(ring);        // [CB][ps4*4]
-  float* gmf = stg + CB * ps4 * 4;                    // [C <= 64][8] merge factors
-  float* Mh = gmf + 64 * 8;                           // [16] M, 1/L
-  float* hd = Mh + 16;                                // [C][16] (m, l) of every partial
-  for (int i = tid; i < 16 * C; i += NCONS) hd[i] = __ldcg(P + (size_t)(i >> 4) * v.part_stride + (i & 15));
-  named_sync(1, NCONS);
-  if (tid < 8) {                                      // M and 1/L per head, merge factors
+  for (int i = tid; i < C * ps4; i += blockDim.x) {
+    const int c = i / ps4, j = i - c * ps4;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(stg + 4 * (size_t)i)),
+                 "l"(P + (size_t)c * v.part_stride + 4 * j));
+  }
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  if (tid < 8) {
     float M = -INFINITY;
-    for (int c = 0; c < C; ++c) M = fmaxf(M, hd[c * 16 + tid]);
+    for (int c = 0; c < C; ++c) M = fmaxf(M, stg[c * ps4 * 4 + tid]);
     float Ls = 0.f;
     for (int c = 0; c < C; ++c) {
-      const float mc = hd[c * 16 + tid];
+      const float mc = stg[c * ps4 * 4 + tid];
       const float f = mc == -INFINITY ? 0.f : exp2f(mc - M);
-      gmf[c * 8 + tid] = f;                           // exp2(m_c - M), before 1/L
-      Ls += f * hd[c * 16 + 8 + tid];
+      gmf[c * 8 + tid] = f;
+      Ls += f * stg[c * ps4 * 4 + 8 + tid];
     }
     Mh[tid] = M;
     Mh[8 + tid] = 1.0f / Ls;
-    if (zpar >= 0) {                   // publish (M, 1/L) for the deferred score pass
+    if (zpar >= 0) {
       float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
       ml[tid] = M;
       ml[8 + tid] = 1.0f / Ls;
     }
   }
-  if (tr && tid == 0) tr[6] = gtimer();
-  float acc[8];
-  const int nel = (tot + NCONS - 1) / NCONS;          // <= 8 outputs per thread (G*D <= 1024)
-#pragma unroll
-  for (int k = 0; k < 8; ++k) acc[k] = 0.f;
-  for (int c0 = 0; c0 < C; c0 += CB) {
-    const int cb = min(CB, C - c0);
-    named_sync(1, NCONS);                             // previous batch consumed
-    const float* src = P + (size_t)c0 * v.part_stride;
-    for (int i = tid; i < cb * ps4; i += NCONS) {
-      const int c = i / ps4, j = i - c * ps4;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(stg + 4 * (size_t)i)),
-                   "l"(src + (size_t)c * v.part_stride + 4 * j));
-    }
-    cp_commit();
-    cp_wait<0>();
-    named_sync(1, NCONS);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int e = tid + k * NCONS;
-      if (k < nel && e < tot) {
-        const int h = e / D;
-        for (int c = 0; c < cb; ++c) acc[k] += gmf[(c0 + c) * 8 + h] * stg[c * ps4 * 4 + 16 + e];
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int e = tid + k * NCONS;
-    if (k < nel && e < tot) {
-      const int h = e / D, dd = e - h * D;
-      const float val = acc[k] * Mh[8 + h];
-      const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
-      if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = val;
-      else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(val);
-    }
+  __syncthreads();
+  for (int e = tid; e < tot; e += blockDim.x) {
+    const int h = e / D, dd = e - h * D;
+    float acc = 0.f;
+    for (int c = 0; c < C; ++c) acc += gmf[c * 8 + h] * stg[c * ps4 * 4 + 16 + e];
+    const float val = acc * Mh[8 + h];
+    const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
+    if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = val;
+    else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(val);
   }
   if (tr && tid == 0) tr[7] = gtimer();
+}
+
+size_t merge_smem_bytes(const DevView& v) {
+  const int ps4 = (16 + v.G * v.D + 3) / 4;
+  return ((size_t)v.split * ps4 * 4 + 8 * v.split + 16) * 4;
 }
 
 // End-of-step flush of the last layer's deferred score update.
@@ -714,6 +695,13 @@ static cudaError_t launch_k(const DevView& v, cudaLaunchConfig_t& cfg, int layer
 
 cudaError_t attn_configure(const DevView& v) {
   if (v.variant < 0 || v.variant >= kNumVariants) return cudaErrorInvalidValue;
+  {
+    cudaError_t e = v.D == 128 ? cudaFuncSetAttribute(k_decode_merge<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      (int)merge_smem_bytes(v))
+                               : cudaFuncSetAttribute(k_decode_merge<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      (int)merge_smem_bytes(v));
+    if (e != cudaSuccess) return e;
+  }
   const Variant vr = kVariants[v.variant];
 #define KVT_CONF(DD, NWW, NSS) \
   if (v.D == DD && vr.nw == NWW && vr.nst == NSS) return configure_k<DD, NWW, NSS>(v);
@@ -723,8 +711,8 @@ cudaError_t attn_configure(const DevView& v) {
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
-                               void* o, int zpar, int prev_zpar, int pdl, cudaStream_t s) {
+static cudaError_t launch_decode_main(const DevView& v, int layer, const void* q, const void* knew,
+                                      const void* vnew, void* o, int zpar, int prev_zpar, int pdl, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(v.split, v.B * v.Hkv, 1);
   cfg.dynamicSmemBytes = attn_smem_bytes(v);
@@ -742,6 +730,28 @@ cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const
   KVT_VARIANTS(KVT_LAUNCH, 64)
 #undef KVT_LAUNCH
   return cudaErrorInvalidValue;
+}
+
+static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, int pdl, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(v.B * v.Hkv, 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = merge_smem_bytes(v);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  if (v.D == 128) return cudaLaunchKernelEx(&cfg, k_decode_merge<128>, v, layer, o, zpar);
+  return cudaLaunchKernelEx(&cfg, k_decode_merge<64>, v, layer, o, zpar);
+}
+
+cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
+                               void* o, int zpar, int prev_zpar, int pdl, cudaStream_t s) {
+  cudaError_t e = launch_decode_main(v, layer, q, knew, vnew, o, zpar, prev_zpar, pdl, s);
+  if (e != cudaSuccess) return e;
+  return launch_merge(v, layer, o, zpar, v.use_pdl, s);
 }
 
 }  // namespace kvt

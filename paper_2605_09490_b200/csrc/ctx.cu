@@ -298,8 +298,8 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     const size_t tb = (size_t)v.L * v.split * v.B * v.Hkv * 8 * sizeof(unsigned long long);
     if (cudaMalloc(&ctx->trace, tb) == cudaSuccess) { cudaMemset(ctx->trace, 0, tb); v.trace = ctx->trace; }
   }
-  if (attn_smem_bytes(v) > 227 * 1024) {
-    const size_t need = attn_smem_bytes(v);
+  if (attn_smem_bytes(v) > 227 * 1024 || merge_smem_bytes(v) > 227 * 1024) {
+    const size_t need = std::max(attn_smem_bytes(v), merge_smem_bytes(v));
     if (ctx->host_t1) cudaFreeHost(ctx->host_t1);
     if (ctx->host_t2) cudaFreeHost(ctx->host_t2);
     delete ctx;

@@ -105,5 +105,6 @@ cudaError_t launch_offload_host(const DevView& v, int cur, cudaStream_t s);
 cudaError_t launch_commit(const DevView& v, cudaStream_t s);
 cudaError_t launch_prefetch(const DevView& v, int layer, cudaStream_t s);
 size_t attn_smem_bytes(const DevView& v);
+size_t merge_smem_bytes(const DevView& v);
 cudaError_t attn_configure(const DevView& v);
 }  // namespace kvt
