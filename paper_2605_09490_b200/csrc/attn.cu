@@ -320,7 +320,49 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   if (tr && tid == 0) tr[1] = gtimer();
 
   if (w == WSCORE) {
-    // ============================ score warp: previous layer's S_part update ============================
+    // ============================ side warp ============================
+    // (1) rank 0: the new token (a1 fused): append its K/V row to T0 row n0-1 (swizzled) and
+    //     publish its attention term as the unit's partial number C: m = z, l = 1, o = v_new.
+    if (has_new) {
+      uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[sb]) + (grp * v.cap0 + sg.n0o) * D;
+      uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[sb]) + (grp * v.cap0 + sg.n0o) * D;
+      const uint16_t* kin = knew ? reinterpret_cast<const uint16_t*>(knew) + ((size_t)b * v.Hkv + g) * D : nullptr;
+      const uint16_t* vin = vnew ? reinterpret_cast<const uint16_t*>(vnew) + ((size_t)b * v.Hkv + g) * D : nullptr;
+      float* part = v.part + ((size_t)unit * (C + 1) + C) * v.part_stride;
+      float kf[D / 32];
+      const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));
+#pragma unroll
+      for (int k = 0; k < D / 32; ++k) {
+        const int e = lane + 32 * k;
+        const int se = swz_off(sg.n0o, e);
+        const uint16_t kb = kin ? kin[e] : K0w[se];
+        const uint16_t vb = vin ? vin[e] : V0w[se];
+        if (kin) K0w[se] = kb;
+        if (vin) V0w[se] = vb;
+        kf[k] = bf16_bits_to_f(kb);
+        const float vf = bf16_bits_to_f(vb);
+        for (int h = 0; h < G; ++h) part[16 + h * D + e] = vf;
+      }
+      float* zrow = zpar >= 0 ? v.zbuf + ((size_t)zpar * v.B * v.Hkv + unit) * v.zrows * 8 : nullptr;
+      for (int h = 0; h < G; ++h) {
+        const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + ((size_t)b * v.Hq + g * G + h) * D;
+        float dot = 0.f;
+#pragma unroll
+        for (int k = 0; k < D / 32; ++k) dot += bf16_bits_to_f(qh[lane + 32 * k]) * kf[k];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+        if (lane == 0) {
+          part[h] = dot * sl2;
+          part[8 + h] = 1.f;
+          if (zrow) zrow[(size_t)sg.a3 * 8 + h] = dot * sl2;
+        }
+      }
+      if (lane >= G && lane < 8) {       // unused heads of the partial
+        part[lane] = -INFINITY;
+        part[8 + lane] = 0.f;
+      }
+    }
+    // (2) the previous launch's deferred S_part update, this CTA's share
     bool bad = false;
     if (prev_zpar >= 0) {
       const long long tot = (long long)v.B * v.Hkv * sg.nvirt;
@@ -355,51 +397,6 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   }
   const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));   // log2(e)/sqrt(d)
   float* zrow = zpar >= 0 ? v.zbuf + ((size_t)zpar * v.B * v.Hkv + unit) * v.zrows * 8 : nullptr;
-
-  // ---- new token (a1 + its own attention term), warp 0 of rank 0, before the tiles:
-  //      append the row to T0 row n0-1 (swizzled); logits on CUDA cores in fp32
-  if (has_new && w == 0) {
-    uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[sb]) + (grp * v.cap0 + sg.n0o) * D;
-    uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[sb]) + (grp * v.cap0 + sg.n0o) * D;
-    const uint16_t* kin = knew ? reinterpret_cast<const uint16_t*>(knew) + ((size_t)b * v.Hkv + g) * D : nullptr;
-    const uint16_t* vin = vnew ? reinterpret_cast<const uint16_t*>(vnew) + ((size_t)b * v.Hkv + g) * D : nullptr;
-    for (int e = lane; e < D; e += 32) {
-      const int se = swz_off(sg.n0o, e);
-      const uint16_t kb = kin ? kin[e] : K0w[se];
-      const uint16_t vb = vin ? vin[e] : V0w[se];
-      nrow[e] = bf16_bits_to_f(kb);
-      nrow[D + e] = bf16_bits_to_f(vb);
-      if (kin) K0w[se] = kb;
-      if (vin) V0w[se] = vb;
-    }
-    __syncwarp();
-    float part = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int d0 = ks * 16 + 2 * tq;
-      part += bf16lo(qf[ks][0]) * nrow[d0] + bf16hi(qf[ks][0]) * nrow[d0 + 1];
-      part += bf16lo(qf[ks][1]) * nrow[d0 + 8] + bf16hi(qf[ks][1]) * nrow[d0 + 9];
-    }
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    if (tq == 0) {
-      zn[gq] = part * sl2;
-      if (zrow) zrow[(size_t)sg.a3 * 8 + gq] = part * sl2;
-    }
-    __syncwarp();
-    mxa = zn[2 * tq];
-    mxb = zn[2 * tq + 1];
-    la = gq == 0 ? 1.f : 0.f;                // p = exp2(z - max) = 1, counted once per head
-    lb = la;
-#pragma unroll
-    for (int mt = 0; mt < KS; ++mt) {
-      const float va = nrow[D + mt * 16 + gq], vb = nrow[D + mt * 16 + gq + 8];
-      oacc[mt][0] = va;
-      oacc[mt][1] = va;
-      oacc[mt][2] = vb;
-      oacc[mt][3] = vb;
-    }
-  }
 
   // one warp-slice (16 rows) of a tile: logits, online softmax, P.V
   auto online = [&](float z00, float z01, float z10, float z11, float& p00, float& p01, float& p10, float& p11) {
@@ -573,7 +570,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   }
   named_sync(1, NCONS);
   {   // publish: visible to the merge kernel once this grid completes (no fence needed)
-    float4* part = reinterpret_cast<float4*>(v.part + ((size_t)unit * C + r) * v.part_stride);
+    float4* part = reinterpret_cast<float4*>(v.part + ((size_t)unit * (C + 1) + r) * v.part_stride);
     for (int i = tid; i < ps4; i += NCONS) part[i] = reinterpret_cast<const float4*>(xp)[i];
   }
   if (tr && tid == 0) tr[4] = gtimer();
@@ -585,62 +582,62 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
 template <int D>
 __global__ void __launch_bounds__(256) k_decode_merge(const DevView v, const int layer, void* __restrict__ o,
                                                       const int zpar) {
+  // one CTA per unit; every thread loads, for its output element, the (m, l) of its head and
+  // the o value of all C+1 partials at once (independent loads: one L2 round trip), then
+  // merges them in rank order (deterministic).  C+1 <= 65.
   const int unit = blockIdx.x, tid = threadIdx.x;
   const int b = unit / v.Hkv, g = unit - b * v.Hkv;
-  const int G = v.G, C = v.split, tot = G * D;
-  const int ps4 = (16 + tot + 3) / 4;
-  extern __shared__ __align__(16) float msm[];
-  float* stg = msm;                                   // [C][ps4*4]
-  float* gmf = stg + (size_t)C * ps4 * 4;             // [C][8]
-  float* Mh = gmf + 8 * C;                            // [16]
+  const int G = v.G, NP = v.split + 1, tot = G * D;
   unsigned long long* tr = v.trace ? v.trace + (((size_t)layer * v.B * v.Hkv + unit) * v.split) * 8 : nullptr;
   pdl_trigger();
   pdl_wait();
   if (tr && tid == 0) tr[5] = gtimer();
-  const float* P = v.part + (size_t)unit * C * v.part_stride;
-  for (int i = tid; i < C * ps4; i += blockDim.x) {
-    const int c = i / ps4, j = i - c * ps4;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(stg + 4 * (size_t)i)),
-                 "l"(P + (size_t)c * v.part_stride + 4 * j));
-  }
-  cp_commit();
-  cp_wait<0>();
-  __syncthreads();
-  if (tid < 8) {
-    float M = -INFINITY;
-    for (int c = 0; c < C; ++c) M = fmaxf(M, stg[c * ps4 * 4 + tid]);
-    float Ls = 0.f;
-    for (int c = 0; c < C; ++c) {
-      const float mc = stg[c * ps4 * 4 + tid];
-      const float f = mc == -INFINITY ? 0.f : exp2f(mc - M);
-      gmf[c * 8 + tid] = f;
-      Ls += f * stg[c * ps4 * 4 + 8 + tid];
-    }
-    Mh[tid] = M;
-    Mh[8 + tid] = 1.0f / Ls;
-    if (zpar >= 0) {
-      float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
-      ml[tid] = M;
-      ml[8 + tid] = 1.0f / Ls;
-    }
-  }
-  __syncthreads();
+  const float* P = v.part + (size_t)unit * NP * v.part_stride;
   for (int e = tid; e < tot; e += blockDim.x) {
     const int h = e / D, dd = e - h * D;
-    float acc = 0.f;
-    for (int c = 0; c < C; ++c) acc += gmf[c * 8 + h] * stg[c * ps4 * 4 + 16 + e];
-    const float val = acc * Mh[8 + h];
+    constexpr int MAXP = 17;
+    float m[MAXP], l[MAXP], x[MAXP];
+    float M = -INFINITY, Ls = 0.f, acc = 0.f;
+    for (int c0 = 0; c0 < NP; c0 += MAXP) {          // one batch for split <= 16
+#pragma unroll
+      for (int c = 0; c < MAXP; ++c) {
+        if (c0 + c < NP) {
+          const float* pc = P + (size_t)(c0 + c) * v.part_stride;
+          m[c] = __ldcg(pc + h);
+          l[c] = __ldcg(pc + 8 + h);
+          x[c] = __ldcg(pc + 16 + e);
+        }
+      }
+      float Mn = M;
+#pragma unroll
+      for (int c = 0; c < MAXP; ++c)
+        if (c0 + c < NP) Mn = fmaxf(Mn, m[c]);
+      const float sc = M == -INFINITY ? 0.f : exp2f(M - Mn);
+      Ls *= sc;
+      acc *= sc;
+#pragma unroll
+      for (int c = 0; c < MAXP; ++c)
+        if (c0 + c < NP) {
+          const float f = m[c] == -INFINITY ? 0.f : exp2f(m[c] - Mn);
+          Ls += f * l[c];
+          acc += f * x[c];
+        }
+      M = Mn;
+    }
+    const float invL = 1.0f / Ls;
     const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
-    if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = val;
-    else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(val);
+    if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = acc * invL;
+    else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(acc * invL);
+    if (dd == 0 && zpar >= 0) {        // publish (M, 1/L) for the deferred score pass
+      float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
+      ml[h] = M;
+      ml[8 + h] = invL;
+    }
   }
   if (tr && tid == 0) tr[7] = gtimer();
 }
 
-size_t merge_smem_bytes(const DevView& v) {
-  const int ps4 = (16 + v.G * v.D + 3) / 4;
-  return ((size_t)v.split * ps4 * 4 + 8 * v.split + 16) * 4;
-}
+size_t merge_smem_bytes(const DevView& v) { (void)v; return 0; }
 
 // End-of-step flush of the last layer's deferred score update.
 __global__ void __launch_bounds__(256) k_score_flush(const DevView v, const int zpar) {

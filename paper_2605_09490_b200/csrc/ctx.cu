@@ -151,7 +151,7 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   L.off_S = take(BH * N * 4);
   L.off_z = take(2 * BH * (N + 64) * 8 * 4);     // deferred-score logits (two launches)
   L.off_ml = take(2 * BH * 16 * 4);
-  L.off_part = take(BH * 64 * (16 + 8 * D) * 4);   // per-CTA partials (split <= 64)
+  L.off_part = take(BH * 65 * (16 + 8 * D) * 4);   // per-CTA partials (split <= 64) + the new token
   L.off_uctr = take(BH * 4);
   const size_t mcap = mcap_of(c);
   L.off_moves = take(B * mcap * 16);
