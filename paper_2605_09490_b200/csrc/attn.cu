@@ -369,9 +369,11 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       const long long ncta = (long long)gridDim.x * gridDim.y;
       const long long cid = (long long)blockIdx.y * gridDim.x + blockIdx.x;
       const long long per = (tot + ncta - 1) / ncta;
+      if (tr && lane == 0) tr[5] = gtimer();
       score_range(v, sg, cur, prev_zpar, cid * per, min(tot, (cid + 1) * per), lane, 32, bad);
     }
     if (bad) atomicOr(&v.st->err, 1);
+    if (tr && lane == 0) tr[6] = gtimer();
     return;
   }
 
@@ -591,7 +593,6 @@ __global__ void __launch_bounds__(256) k_decode_merge(const DevView v, const int
   unsigned long long* tr = v.trace ? v.trace + (((size_t)layer * v.B * v.Hkv + unit) * v.split) * 8 : nullptr;
   pdl_trigger();
   pdl_wait();
-  if (tr && tid == 0) tr[5] = gtimer();
   const float* P = v.part + (size_t)unit * NP * v.part_stride;
   for (int e = tid; e < tot; e += blockDim.x) {
     const int h = e / D, dd = e - h * D;
