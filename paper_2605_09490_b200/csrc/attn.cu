@@ -191,14 +191,14 @@ __device__ __forceinline__ void score_range(const DevView& v, const Seg& sg, int
 }
 
 template <int D, int NW, int NST>
-__global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
+__global__ void __launch_bounds__((NW + 3) * 32, (NW == 4 ? 2 : 1))
     k_decode_attn(const DevView v, const int layer, const __nv_bfloat16* __restrict__ q,
                   const __nv_bfloat16* __restrict__ knew, const __nv_bfloat16* __restrict__ vnew,
                   void* __restrict__ o, const int zpar, const int prev_zpar) {
   // zpar: logits buffer of this launch (-1: no score update); prev_zpar: pending score pass
   // of the previous launch to apply in the background (-1: none)
   constexpr int NCONS = NW * 32;              // consumer threads
-  constexpr int WPROD = NW, WSCORE = NW + 1;
+  constexpr int WPROD = NW, WSCORE = NW + 1;     // + warp NW + 2: second score-pass warp
   constexpr int TILE = NW * 16;
   constexpr int ROWB = D * 2;
   constexpr int TILEB = TILE * ROWB;
@@ -319,43 +319,57 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   pdl_wait();
   if (tr && tid == 0) tr[1] = gtimer();
 
-  if (w == WSCORE) {
-    // ============================ side warp ============================
+  if (w >= WSCORE) {
+    // ============================ side warps ============================
     // (1) rank 0: the new token (a1 fused): append its K/V row to T0 row n0-1 (swizzled) and
     //     publish its attention term as the unit's partial number C: m = z, l = 1, o = v_new.
-    if (has_new) {
+    if (has_new && w == WSCORE) {
       uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[sb]) + (grp * v.cap0 + sg.n0o) * D;
       uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[sb]) + (grp * v.cap0 + sg.n0o) * D;
       const uint16_t* kin = knew ? reinterpret_cast<const uint16_t*>(knew) + ((size_t)b * v.Hkv + g) * D : nullptr;
       const uint16_t* vin = vnew ? reinterpret_cast<const uint16_t*>(vnew) + ((size_t)b * v.Hkv + g) * D : nullptr;
       float* part = v.part + ((size_t)unit * (C + 1) + C) * v.part_stride;
-      float kf[D / 32];
+      constexpr int EL = D / 32;
       const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));
+      uint16_t kb[EL], vb[EL], qb[8][EL];
+      const uint16_t* qbase = reinterpret_cast<const uint16_t*>(q) + ((size_t)b * v.Hq + g * G) * D;
 #pragma unroll
-      for (int k = 0; k < D / 32; ++k) {
+      for (int k = 0; k < EL; ++k) {          // every load of the new-token work issued at once
         const int e = lane + 32 * k;
         const int se = swz_off(sg.n0o, e);
-        const uint16_t kb = kin ? kin[e] : K0w[se];
-        const uint16_t vb = vin ? vin[e] : V0w[se];
-        if (kin) K0w[se] = kb;
-        if (vin) V0w[se] = vb;
-        kf[k] = bf16_bits_to_f(kb);
-        const float vf = bf16_bits_to_f(vb);
-        for (int h = 0; h < G; ++h) part[16 + h * D + e] = vf;
+        kb[k] = kin ? kin[e] : K0w[se];
+        vb[k] = vin ? vin[e] : V0w[se];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) qb[h][k] = h < G ? qbase[(size_t)h * D + e] : (uint16_t)0;
       }
       float* zrow = zpar >= 0 ? v.zbuf + ((size_t)zpar * v.B * v.Hkv + unit) * v.zrows * 8 : nullptr;
-      for (int h = 0; h < G; ++h) {
-        const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + ((size_t)b * v.Hq + g * G + h) * D;
-        float dot = 0.f;
+      float dot[8];
 #pragma unroll
-        for (int k = 0; k < D / 32; ++k) dot += bf16_bits_to_f(qh[lane + 32 * k]) * kf[k];
+      for (int h = 0; h < 8; ++h) {
+        dot[h] = 0.f;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
-        if (lane == 0) {
-          part[h] = dot * sl2;
-          part[8 + h] = 1.f;
-          if (zrow) zrow[(size_t)sg.a3 * 8 + h] = dot * sl2;
-        }
+        for (int k = 0; k < EL; ++k) dot[h] += bf16_bits_to_f(qb[h][k]) * bf16_bits_to_f(kb[k]);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int h = 0; h < 8; ++h) dot[h] += __shfl_xor_sync(0xffffffffu, dot[h], off);
+#pragma unroll
+      for (int k = 0; k < EL; ++k) {
+        const int e = lane + 32 * k;
+        const int se = swz_off(sg.n0o, e);
+        if (kin) K0w[se] = kb[k];
+        if (vin) V0w[se] = vb[k];
+        const float vf = bf16_bits_to_f(vb[k]);
+        for (int h = 0; h < G; ++h) part[16 + h * D + e] = vf;
+      }
+      if (lane < G) {
+        float z = 0.f;
+#pragma unroll
+        for (int h = 0; h < 8; ++h) z = lane == h ? dot[h] * sl2 : z;
+        part[lane] = z;
+        part[8 + lane] = 1.f;
+        if (zrow) zrow[(size_t)sg.a3 * 8 + lane] = z;
       }
       if (lane >= G && lane < 8) {       // unused heads of the partial
         part[lane] = -INFINITY;
@@ -366,14 +380,14 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     bool bad = false;
     if (prev_zpar >= 0) {
       const long long tot = (long long)v.B * v.Hkv * sg.nvirt;
-      const long long ncta = (long long)gridDim.x * gridDim.y;
-      const long long cid = (long long)blockIdx.y * gridDim.x + blockIdx.x;
-      const long long per = (tot + ncta - 1) / ncta;
-      if (tr && lane == 0) tr[5] = gtimer();
-      score_range(v, sg, cur, prev_zpar, cid * per, min(tot, (cid + 1) * per), lane, 32, bad);
+      const long long nw = 2LL * gridDim.x * gridDim.y;          // two score warps per CTA
+      const long long wid = 2LL * ((long long)blockIdx.y * gridDim.x + blockIdx.x) + (w - WSCORE);
+      const long long per = (tot + nw - 1) / nw;
+      if (tr && lane == 0 && w == WSCORE) tr[5] = gtimer();
+      score_range(v, sg, cur, prev_zpar, wid * per, min(tot, (wid + 1) * per), lane, 32, bad);
     }
     if (bad) atomicOr(&v.st->err, 1);
-    if (tr && lane == 0) tr[6] = gtimer();
+    if (tr && lane == 0 && w == WSCORE) tr[6] = gtimer();
     return;
   }
 
@@ -582,7 +596,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
 // per-head (max, 1/sum) for the deferred score pass.  Launched right behind the decode kernel
 // with programmatic dependent launch: its CTAs are resident early and start when it completes.
 template <int D>
-__global__ void __launch_bounds__(256) k_decode_merge(const DevView v, const int layer, void* __restrict__ o,
+__global__ void __launch_bounds__(1024) k_decode_merge(const DevView v, const int layer, void* __restrict__ o,
                                                       const int zpar) {
   // one CTA per unit; every thread loads, for its output element, the (m, l) of its head and
   // the o value of all C+1 partials at once (independent loads: one L2 round trip), then
@@ -683,7 +697,7 @@ static cudaError_t configure_k(const DevView& v) {
 template <int D, int NW, int NST>
 static cudaError_t launch_k(const DevView& v, cudaLaunchConfig_t& cfg, int layer, const void* q, const void* knew,
                             const void* vnew, void* o, int zpar, int prev_zpar) {
-  cfg.blockDim = dim3((NW + 2) * 32, 1, 1);
+  cfg.blockDim = dim3((NW + 3) * 32, 1, 1);
   return cudaLaunchKernelEx(&cfg, k_decode_attn<D, NW, NST>, v, layer, reinterpret_cast<const __nv_bfloat16*>(q),
                             reinterpret_cast<const __nv_bfloat16*>(knew), reinterpret_cast<const __nv_bfloat16*>(vnew),
                             o, zpar, prev_zpar);
@@ -733,7 +747,7 @@ static cudaError_t launch_decode_main(const DevView& v, int layer, const void* q
 static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, int pdl, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(v.B * v.Hkv, 1, 1);
-  cfg.blockDim = dim3(256, 1, 1);
+  cfg.blockDim = dim3(1024, 1, 1);
   cfg.dynamicSmemBytes = merge_smem_bytes(v);
   cfg.stream = s;
   cudaLaunchAttribute at[1];
