@@ -54,6 +54,16 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
 }
+// streamed K/V rows are read once per layer: evict them first so the hot data stays in L2
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_ef(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar, uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src));
 }
@@ -270,6 +280,7 @@ __global__ void __launch_bounds__((NW + 3) * 32, (NW == 4 ? 2 : 1))
     // tiles are dealt round-robin to the unit's CTAs (tile k -> rank k mod C): balanced,
     // and deterministic (the fp32 summation order never depends on timing)
     if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
       for (int i = 0;; ++i) {
         const int s2 = i % NST;
         if (i == v.pdl_pre) pdl_wait();   // at most pdl_pre stages in flight before the previous layer ends
@@ -287,15 +298,15 @@ __global__ void __launch_bounds__((NW + 3) * 32, (NW == 4 ? 2 : 1))
           mbar_expect_tx(full, STAGEB);
           if (ts < sg.a1) {           // T0 rows (pad rows beyond n0o are stale but finite)
             const int nrows = min(TILE, sg.a1 - ts);
-            bulk_g2s(dst, K0 + (size_t)ts * D, nrows * ROWB, full);
-            bulk_g2s(dst + TILEB, V0 + (size_t)ts * D, nrows * ROWB, full);
+            bulk_g2s_ef(dst, K0 + (size_t)ts * D, nrows * ROWB, full, pol);
+            bulk_g2s_ef(dst + TILEB, V0 + (size_t)ts * D, nrows * ROWB, full, pol);
             if (nrows < TILE) {
-              bulk_g2s(dst + nrows * ROWB, K1, (TILE - nrows) * ROWB, full);
-              bulk_g2s(dst + TILEB + nrows * ROWB, V1, (TILE - nrows) * ROWB, full);
+              bulk_g2s_ef(dst + nrows * ROWB, K1, (TILE - nrows) * ROWB, full, pol);
+              bulk_g2s_ef(dst + TILEB + nrows * ROWB, V1, (TILE - nrows) * ROWB, full, pol);
             }
           } else {
-            bulk_g2s(dst, K1 + (size_t)(ts - sg.a1) * D, TILEB, full);
-            bulk_g2s(dst + TILEB, V1 + (size_t)(ts - sg.a1) * D, TILEB, full);
+            bulk_g2s_ef(dst, K1 + (size_t)(ts - sg.a1) * D, TILEB, full, pol);
+            bulk_g2s_ef(dst + TILEB, V1 + (size_t)(ts - sg.a1) * D, TILEB, full, pol);
           }
         } else {                      // T2: int8 codes + fp32 scales (canonical layout)
           const int j0 = (k - ntb) * TILE;
@@ -729,11 +740,24 @@ static cudaError_t launch_decode_main(const DevView& v, int layer, const void* q
   cfg.gridDim = dim3(v.split, v.B * v.Hkv, 1);
   cfg.dynamicSmemBytes = attn_smem_bytes(v);
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (v.hot_bytes > 0) {
+    at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[na].val.accessPolicyWindow.base_ptr = v.hot_base;
+    at[na].val.accessPolicyWindow.num_bytes = v.hot_bytes;
+    at[na].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   const Variant vr = kVariants[v.variant];
 #define KVT_LAUNCH(DD, NWW, NSS)                          \
   if (v.D == DD && vr.nw == NWW && vr.nst == NSS)         \
@@ -750,11 +774,24 @@ static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, 
   cfg.blockDim = dim3(1024, 1, 1);
   cfg.dynamicSmemBytes = merge_smem_bytes(v);
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (v.hot_bytes > 0) {
+    at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[na].val.accessPolicyWindow.base_ptr = v.hot_base;
+    at[na].val.accessPolicyWindow.num_bytes = v.hot_bytes;
+    at[na].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   if (v.D == 128) return cudaLaunchKernelEx(&cfg, k_decode_merge<128>, v, layer, o, zpar);
   return cudaLaunchKernelEx(&cfg, k_decode_merge<64>, v, layer, o, zpar);
 }

@@ -65,6 +65,12 @@ kv_tier_status cuda_check(kv_tier_ctx* ctx, cudaError_t e, const char* what) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 int round16(long long x) { return (int)((x + 15) / 16 * 16); }
 
+int split_of(const kv_tier_config& c) {
+  if (c.split > 0) return c.split;
+  const int units = c.num_requests * c.num_kv_heads;
+  return std::max(1, std::min(8, (2 * 148 + units - 1) / units));
+}
+
 int auto_split(const kv_tier_config& c) {
   if (c.split > 0) return c.split;
   const int units = c.num_requests * c.num_kv_heads;
@@ -113,9 +119,11 @@ void capacities(const kv_tier_config& c, int* cap0, int* cap1, int* cap2) {
 struct Layout {
   size_t off_k0[2], off_v0[2], off_k1[2], off_v1[2], off_c2k[2], off_c2v[2], off_s2k[2], off_s2v[2];
   size_t off_idx[2][3], off_vis[2], off_tier[2], off_row[2], off_cnt[2], off_S, off_fS, off_st, off_z, off_ml;
-  size_t off_part, off_uctr, off_moves, off_mcount, off_scratch, off_mtemp, total;
+  size_t off_part, off_uctr, off_moves, off_mcount, off_scratch, off_mtemp, total, hot_begin;
   size_t b_t0, b_t1, b_t2, b_scores, b_meta;
 };
+
+int split_of(const kv_tier_config& c);
 
 // Rows an incremental migrate may move per request; more -> full rebuild (first event).
 size_t mcap_of(const kv_tier_config& c) {
@@ -148,16 +156,18 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
     L.off_s2k[i] = take(LBH * cap2 * 4); L.off_s2v[i] = take(LBH * cap2 * 4);
   }
   L.b_t2 = o - s0; s0 = o;
-  L.off_S = take(BH * N * 4);
-  L.off_z = take(2 * BH * (N + 64) * 8 * 4);     // deferred-score logits (two launches)
-  L.off_ml = take(2 * BH * 16 * 4);
-  L.off_part = take(BH * 65 * (16 + 8 * D) * 4);   // per-CTA partials (split <= 64) + the new token
-  L.off_uctr = take(BH * 4);
+  // migrate staging (cold)
   const size_t mcap = mcap_of(c);
   L.off_moves = take(B * mcap * 16);
   L.off_mcount = take(B * 4);
   L.off_scratch = take(B * N * 4);
   L.off_mtemp = take(B * mcap * LBH / B * 2 * D * 2);
+  // hot, small: kept resident in L2 (access-policy window from off_S to the end)
+  L.off_S = take(BH * N * 4);
+  L.off_z = take(2 * BH * (N + 64) * 8 * 4);     // deferred-score logits (two launches)
+  L.off_ml = take(2 * BH * 16 * 4);
+  L.off_part = take(BH * (split_of(c) + 1) * (16 + 8 * D) * 4);   // per-CTA partials + the new token
+  L.off_uctr = take(BH * 4);
   L.b_scores = o - s0; s0 = o;
   for (int i = 0; i < 2; ++i) {
     L.off_idx[i][0] = take(B * cap0 * 4);
@@ -170,6 +180,7 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   }
   L.off_fS = take(B * N * 4);
   L.off_st = take(sizeof(DevState));
+  L.hot_begin = L.off_S;
   L.b_meta = o - s0;
   L.total = o;
   return L;
@@ -266,6 +277,8 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.part = reinterpret_cast<float*>(A + L.off_part);
   v.part_stride = 16 + 8 * v.D;
   v.unit_ctr = reinterpret_cast<int*>(A + L.off_uctr);
+  v.hot_base = A + L.hot_begin;
+  v.hot_bytes = L.total - L.hot_begin;
   v.moves = reinterpret_cast<int4*>(A + L.off_moves);
   v.mcount = reinterpret_cast<int*>(A + L.off_mcount);
   v.mcap = (int)mcap_of(*cfg);
@@ -306,6 +319,19 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     return fail(nullptr, KV_TIER_E_INVAL, "decode kernel needs %zu B shared memory (> 227 KB): raise split or pick a smaller variant", need);
   }
   e = cudaMemset(buf->device_arena, 0, ctx->sz.device_arena);   // stale rows read as masked padding stay finite
+  if (e == cudaSuccess) {
+    // scores, logits, partials and index lists stay L2-resident while K/V streams past them
+    int maxp = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, cfg->device);
+    size_t want = std::min<size_t>(v.hot_bytes, (size_t)maxp);
+    size_t cur_lim = 0;
+    cudaDeviceGetLimit(&cur_lim, cudaLimitPersistingL2CacheSize);
+    if (want > cur_lim) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    int maxw = 0;
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, cfg->device);
+    v.hot_bytes = std::min<size_t>(v.hot_bytes, (size_t)maxw);
+    cudaGetLastError();                  // persistence is an optimisation: ignore if unsupported
+  }
   if (e == cudaSuccess) e = attn_configure(v);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_step_begin, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_migrated, cudaEventDisableTiming);

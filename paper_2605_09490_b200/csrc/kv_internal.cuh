@@ -40,7 +40,9 @@ struct DevView {
   int zrows;            // virtual rows per unit (N_max + padding)
   float* part;          // [B*Hkv][split][part_stride] per-CTA partials (m[8], l[8], o[G][D])
   int part_stride;
-  int* unit_ctr;        // [B*Hkv] CTAs of the current launch that finished (reset by the last)
+  int* unit_ctr;        // [B*Hkv] (unused by the current decode path)
+  void* hot_base;       // L2 access-policy window over the small hot buffers
+  size_t hot_bytes;
   int4* moves;          // [B][mcap] {src tier, src row, dst tier | dst row << 2, position}
   int* mcount;          // [B] moves of the last plan (<= mcap)
   int mcap;
