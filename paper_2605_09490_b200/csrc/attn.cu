@@ -201,14 +201,13 @@ __device__ __forceinline__ void score_range(const DevView& v, const Seg& sg, int
 }
 
 template <int D, int NW, int NST>
-__global__ void __launch_bounds__((NW + 3) * 32, (NW == 4 ? 2 : 1))
+__global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     k_decode_attn(const DevView v, const int layer, const __nv_bfloat16* __restrict__ q,
                   const __nv_bfloat16* __restrict__ knew, const __nv_bfloat16* __restrict__ vnew,
-                  void* __restrict__ o, const int zpar, const int prev_zpar) {
-  // zpar: logits buffer of this launch (-1: no score update); prev_zpar: pending score pass
-  // of the previous launch to apply in the background (-1: none)
+                  void* __restrict__ o, const int zpar) {
+  // zpar: logits/ML ring slot of this launch (-1: no score update)
   constexpr int NCONS = NW * 32;              // consumer threads
-  constexpr int WPROD = NW, WSCORE = NW + 1;     // + warp NW + 2: second score-pass warp
+  constexpr int WPROD = NW, WSCORE = NW + 1;
   constexpr int TILE = NW * 16;
   constexpr int ROWB = D * 2;
   constexpr int TILEB = TILE * ROWB;
@@ -330,11 +329,11 @@ __global__ void __launch_bounds__((NW + 3) * 32, (NW == 4 ? 2 : 1))
   pdl_wait();
   if (tr && tid == 0) tr[1] = gtimer();
 
-  if (w >= WSCORE) {
-    // ============================ side warps ============================
+  if (w == WSCORE) {
+    // ============================ side warp ============================
     // (1) rank 0: the new token (a1 fused): append its K/V row to T0 row n0-1 (swizzled) and
     //     publish its attention term as the unit's partial number C: m = z, l = 1, o = v_new.
-    if (has_new && w == WSCORE) {
+    if (has_new) {
       uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[sb]) + (grp * v.cap0 + sg.n0o) * D;
       uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[sb]) + (grp * v.cap0 + sg.n0o) * D;
       const uint16_t* kin = knew ? reinterpret_cast<const uint16_t*>(knew) + ((size_t)b * v.Hkv + g) * D : nullptr;
@@ -387,18 +386,6 @@ __global__ void __launch_bounds__((NW + 3) * 32, (NW == 4 ? 2 : 1))
         part[8 + lane] = 0.f;
       }
     }
-    // (2) the previous launch's deferred S_part update, this CTA's share
-    bool bad = false;
-    if (prev_zpar >= 0) {
-      const long long tot = (long long)v.B * v.Hkv * sg.nvirt;
-      const long long nw = 2LL * gridDim.x * gridDim.y;          // two score warps per CTA
-      const long long wid = 2LL * ((long long)blockIdx.y * gridDim.x + blockIdx.x) + (w - WSCORE);
-      const long long per = (tot + nw - 1) / nw;
-      if (tr && lane == 0 && w == WSCORE) tr[5] = gtimer();
-      score_range(v, sg, cur, prev_zpar, wid * per, min(tot, (wid + 1) * per), lane, 32, bad);
-    }
-    if (bad) atomicOr(&v.st->err, 1);
-    if (tr && lane == 0 && w == WSCORE) tr[6] = gtimer();
     return;
   }
 
@@ -665,7 +652,8 @@ __global__ void __launch_bounds__(1024) k_decode_merge(const DevView v, const in
 
 size_t merge_smem_bytes(const DevView& v) { (void)v; return 0; }
 
-// End-of-step flush of the last layer's deferred score update.
+// a4: the score update of one decode_attention launch (ring slot zpar), on the library's
+// score stream, off the attention critical path.
 __global__ void __launch_bounds__(256) k_score_flush(const DevView v, const int zpar) {
   const int cur = v.st->cur;
   Seg sg;
@@ -677,7 +665,7 @@ __global__ void __launch_bounds__(256) k_score_flush(const DevView v, const int 
 }
 
 cudaError_t launch_score_flush(const DevView& v, int zpar, cudaStream_t s) {
-  k_score_flush<<<2 * 148, 256, 0, s>>>(v, zpar);
+  k_score_flush<<<148, 256, 0, s>>>(v, zpar);
   return cudaGetLastError();
 }
 
@@ -707,11 +695,11 @@ static cudaError_t configure_k(const DevView& v) {
 
 template <int D, int NW, int NST>
 static cudaError_t launch_k(const DevView& v, cudaLaunchConfig_t& cfg, int layer, const void* q, const void* knew,
-                            const void* vnew, void* o, int zpar, int prev_zpar) {
-  cfg.blockDim = dim3((NW + 3) * 32, 1, 1);
+                            const void* vnew, void* o, int zpar) {
+  cfg.blockDim = dim3((NW + 2) * 32, 1, 1);
   return cudaLaunchKernelEx(&cfg, k_decode_attn<D, NW, NST>, v, layer, reinterpret_cast<const __nv_bfloat16*>(q),
                             reinterpret_cast<const __nv_bfloat16*>(knew), reinterpret_cast<const __nv_bfloat16*>(vnew),
-                            o, zpar, prev_zpar);
+                            o, zpar);
 }
 
 #define KVT_VARIANTS(X, D) X(D, 4, 3) X(D, 4, 4) X(D, 8, 2) X(D, 8, 3) X(D, 4, 2) X(D, 4, 6)
@@ -735,7 +723,7 @@ cudaError_t attn_configure(const DevView& v) {
 }
 
 static cudaError_t launch_decode_main(const DevView& v, int layer, const void* q, const void* knew,
-                                      const void* vnew, void* o, int zpar, int prev_zpar, int pdl, cudaStream_t s) {
+                                      const void* vnew, void* o, int zpar, int pdl, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(v.split, v.B * v.Hkv, 1);
   cfg.dynamicSmemBytes = attn_smem_bytes(v);
@@ -761,7 +749,7 @@ static cudaError_t launch_decode_main(const DevView& v, int layer, const void* q
   const Variant vr = kVariants[v.variant];
 #define KVT_LAUNCH(DD, NWW, NSS)                          \
   if (v.D == DD && vr.nw == NWW && vr.nst == NSS)         \
-    return launch_k<DD, NWW, NSS>(v, cfg, layer, q, knew, vnew, o, zpar, prev_zpar);
+    return launch_k<DD, NWW, NSS>(v, cfg, layer, q, knew, vnew, o, zpar);
   KVT_VARIANTS(KVT_LAUNCH, 128)
   KVT_VARIANTS(KVT_LAUNCH, 64)
 #undef KVT_LAUNCH
@@ -797,8 +785,8 @@ static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, 
 }
 
 cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
-                               void* o, int zpar, int prev_zpar, int pdl, cudaStream_t s) {
-  cudaError_t e = launch_decode_main(v, layer, q, knew, vnew, o, zpar, prev_zpar, pdl, s);
+                               void* o, int zpar, int pdl, cudaStream_t s) {
+  cudaError_t e = launch_decode_main(v, layer, q, knew, vnew, o, zpar, pdl, s);
   if (e != cudaSuccess) return e;
   return launch_merge(v, layer, o, zpar, v.use_pdl, s);
 }

@@ -33,8 +33,11 @@ struct kv_tier_ctx {
   std::vector<int> appended_step;          // step in which layer l's new row was written
   bool offload_pending = false;
   bool capturing = false;
-  int zpar_next = 0;                       // logits buffer of the next fused decode_attention
-  int pending_zpar = -1;                   // deferred score pass not yet applied
+  int zslot_next = 0;                      // logits/ML ring slot of the next fused decode_attention
+  bool slot_busy[ZRING] = {false, false, false, false};   // a score kernel may still read the slot
+  bool scores_pending = false;             // score kernels not yet joined back into the main stream
+  cudaStream_t score_stream = nullptr;     // a4 score updates run here, off the attention chain
+  cudaEvent_t ev_merged[ZRING] = {}, ev_scored[ZRING] = {}, ev_score_tail = nullptr;
   bool slot_recorded[2] = {false, false};   // ev_slot_free[x] recorded within the open step
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -164,8 +167,8 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   L.off_mtemp = take(B * mcap * LBH / B * 2 * D * 2);
   // hot, small: kept resident in L2 (access-policy window from off_S to the end)
   L.off_S = take(BH * N * 4);
-  L.off_z = take(2 * BH * (N + 64) * 8 * 4);     // deferred-score logits (two launches)
-  L.off_ml = take(2 * BH * 16 * 4);
+  L.off_z = take(ZRING * BH * (N + 64) * 8 * 4);     // logits of recent launches (score update)
+  L.off_ml = take(ZRING * BH * 16 * 4);
   L.off_part = take(BH * (split_of(c) + 1) * (16 + 8 * D) * 4);   // per-CTA partials + the new token
   L.off_uctr = take(BH * 4);
   L.b_scores = o - s0; s0 = o;
@@ -337,6 +340,12 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_migrated, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_offload_done, cudaEventDisableTiming);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ctx->ev_slot_free[i], cudaEventDisableTiming);
+  for (int i = 0; i < ZRING && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&ctx->ev_merged[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_scored[i], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_score_tail, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->score_stream, cudaStreamNonBlocking);
   ctx->ev_prefetched.assign(v.L, nullptr);
   for (int l = 0; l < v.L && e == cudaSuccess; ++l) e = cudaEventCreateWithFlags(&ctx->ev_prefetched[l], cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -364,6 +373,12 @@ kv_tier_status kv_tier_destroy(kv_tier_ctx* ctx) {
   if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
   if (ctx->graph) cudaGraphDestroy(ctx->graph);
   if (ctx->trace) cudaFree(ctx->trace);
+  for (int i = 0; i < ZRING; ++i) {
+    if (ctx->ev_merged[i]) cudaEventDestroy(ctx->ev_merged[i]);
+    if (ctx->ev_scored[i]) cudaEventDestroy(ctx->ev_scored[i]);
+  }
+  if (ctx->ev_score_tail) cudaEventDestroy(ctx->ev_score_tail);
+  if (ctx->score_stream) cudaStreamDestroy(ctx->score_stream);
   delete ctx;
   return KV_TIER_OK;
 }
@@ -460,11 +475,21 @@ static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, con
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
   if (ctx->v.stream_mode) e = cudaStreamWaitEvent(s, ctx->ev_prefetched[layer], 0);
-  const int zpar = fuse_score_update ? ctx->zpar_next : -1;
-  if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, zpar, ctx->pending_zpar, pdl, s);
-  if (e == cudaSuccess) {
-    ctx->pending_zpar = zpar;
-    if (zpar >= 0) ctx->zpar_next ^= 1;
+  const int zpar = fuse_score_update ? ctx->zslot_next : -1;
+  // the ring slot's previous score kernel must be done before its logits are overwritten
+  if (e == cudaSuccess && zpar >= 0 && ctx->slot_busy[zpar]) e = cudaStreamWaitEvent(s, ctx->ev_scored[zpar], 0);
+  if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, zpar, pdl, s);
+  if (e == cudaSuccess && zpar >= 0) {
+    // a4 on the score stream: S_part += sum_h exp2(z - M)/L once this launch's merge is done
+    e = cudaEventRecord(ctx->ev_merged[zpar], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->score_stream, ctx->ev_merged[zpar], 0);
+    if (e == cudaSuccess) e = launch_score_flush(ctx->v, zpar, ctx->score_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_scored[zpar], ctx->score_stream);
+    if (e == cudaSuccess) {
+      ctx->slot_busy[zpar] = true;
+      ctx->scores_pending = true;
+      ctx->zslot_next = (zpar + 1) % ZRING;
+    }
   }
   if (e == cudaSuccess && ctx->v.stream_mode) {
     e = cudaEventRecord(ctx->ev_slot_free[layer & 1], s);
@@ -496,11 +521,16 @@ kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (!ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "end_step without begin_step");
   cudaError_t e = cudaSuccess;
-  if (ctx->pending_zpar >= 0) e = launch_score_flush(ctx->v, ctx->pending_zpar, reinterpret_cast<cudaStream_t>(stream));
-  if (e == cudaSuccess) e = launch_end_step(ctx->v, reinterpret_cast<cudaStream_t>(stream));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (ctx->scores_pending) {     // join the score stream: S_part is complete for this step
+    e = cudaEventRecord(ctx->ev_score_tail, ctx->score_stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->ev_score_tail, 0);
+  }
+  if (e == cudaSuccess) e = launch_end_step(ctx->v, s);
   kv_tier_status st = cuda_check(ctx, e, "end_step");
   if (st) return st;
-  ctx->pending_zpar = -1;
+  ctx->scores_pending = false;
+  for (auto& b : ctx->slot_busy) b = false;
   ctx->step_open = false;
   ctx->t += 1;
   return KV_TIER_OK;
@@ -599,7 +629,7 @@ kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const
   const bool classified = ctx->classified;
   const std::vector<int> pstep = ctx->prefetched_step;
   const std::vector<int> astep = ctx->appended_step;
-  const int zpn = ctx->zpar_next, pzp = ctx->pending_zpar;
+  const int zpn = ctx->zslot_next;
   cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return cuda_check(ctx, e, "begin capture");
   ctx->capturing = true;
@@ -610,8 +640,9 @@ kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const
   ctx->n = n; ctx->t = t; ctx->c[0] = c0; ctx->classified = classified; ctx->step_open = false;
   ctx->prefetched_step = pstep;
   ctx->appended_step = astep;
-  ctx->zpar_next = zpn;
-  ctx->pending_zpar = pzp;
+  ctx->zslot_next = zpn;
+  for (auto& b : ctx->slot_busy) b = false;
+  ctx->scores_pending = false;
   if (st) { if (g) cudaGraphDestroy(g); return st; }
   if (e != cudaSuccess) return cuda_check(ctx, e, "end capture");
   e = cudaGraphInstantiate(&ctx->graph_exec, g, 0);
@@ -636,8 +667,7 @@ kv_tier_status kv_tier_step_graph_launch(kv_tier_ctx* ctx, void* stream) {
   ctx->c[0] += 1;
   ctx->t += 1;
   ctx->classified = false;
-  ctx->zpar_next ^= (ctx->v.L & 1);        // same transitions as kv_tier_step
-  ctx->pending_zpar = -1;
+  ctx->zslot_next = (ctx->zslot_next + ctx->v.L) % ZRING;   // same transitions as kv_tier_step
   return KV_TIER_OK;
 }
 

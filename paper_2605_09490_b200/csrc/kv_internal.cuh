@@ -7,7 +7,8 @@
 namespace kvt {
 
 constexpr int T0 = 0, T1 = 1, T2 = 2, T3 = 3;
-constexpr int CNT_STRIDE = 8;   // cnt[buf][b][8]: |T0| |T1| |T2| |T3| |visible at event| pad..
+constexpr int CNT_STRIDE = 8;
+constexpr int ZRING = 4;          // logits/ML ring slots (score kernels lag the decode chain)   // cnt[buf][b][8]: |T0| |T1| |T2| |T3| |visible at event| pad..
 
 // Mutable device state (graph-static kernels read it instead of taking args).
 struct DevState {
@@ -35,8 +36,8 @@ struct DevView {
   int pdl_pre;          // stages the producer may load before griddepcontrol.wait
   int use_pdl;          // chain consecutive layers with programmatic dependent launch
   unsigned long long* trace;   // debug: per-CTA %globaltimer checkpoints (null = off)
-  float* zbuf;          // [2][B*Hkv][zrows][8] logits (log2 domain) of the last two launches
-  float* ml;            // [2][B*Hkv][16] per-head (max, 1/sum) of the last two launches
+  float* zbuf;          // [ZRING][B*Hkv][zrows][8] logits (log2 domain) of recent launches
+  float* ml;            // [ZRING][B*Hkv][16] per-head (max, 1/sum) of recent launches
   int zrows;            // virtual rows per unit (N_max + padding)
   float* part;          // [B*Hkv][split][part_stride] per-CTA partials (m[8], l[8], o[G][D])
   int part_stride;
@@ -94,7 +95,7 @@ cudaError_t launch_append(const DevView& v, int layer, const void* k, const void
 cudaError_t launch_load_prefix(const DevView& v, int layer, const void* k, const void* vv, int n0, cudaStream_t s);
 cudaError_t launch_init_meta(const DevView& v, int n0, cudaStream_t s);
 cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
-                               void* o, int zpar, int prev_zpar, int pdl, cudaStream_t s);
+                               void* o, int zpar, int pdl, cudaStream_t s);
 cudaError_t launch_score_flush(const DevView& v, int zpar, cudaStream_t s);
 cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s);
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);
