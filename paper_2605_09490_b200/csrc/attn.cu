@@ -603,8 +603,10 @@ __global__ void __launch_bounds__(1024) k_decode_merge(const DevView v, const in
   const int b = unit / v.Hkv, g = unit - b * v.Hkv;
   const int G = v.G, NP = v.split + 1, tot = G * D;
   unsigned long long* tr = v.trace ? v.trace + (((size_t)layer * v.B * v.Hkv + unit) * v.split) * 8 : nullptr;
+  if (tr && tid == 0) tr[6] = gtimer();
   pdl_trigger();
   pdl_wait();
+  if (tr && tid == 0) tr[5] = gtimer();
   const float* P = v.part + (size_t)unit * NP * v.part_stride;
   for (int e = tid; e < tot; e += blockDim.x) {
     const int h = e / D, dd = e - h * D;

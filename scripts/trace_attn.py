@@ -28,7 +28,7 @@ for _ in range(3):
     run.step()
 run.sync()
 tr = run.kv.debug_trace().astype(np.int64)        # [L][CTAs][8], last step
-names = ["start", "pdl_wait", "first_tile", "loop_done", "partial_written", "side_newtok_done", "side_done", "merge_end"]
+names = ["start", "pdl_wait", "first_tile", "loop_done", "partial_written", "merge_released", "merge_resident", "merge_end"]
 t0 = tr[0, :, 0].min()
 rel = (tr - t0) / 1e3
 out = {"config": a.config, "split": a.split, "variant": a.variant, "ctas": int(tr.shape[1])}
