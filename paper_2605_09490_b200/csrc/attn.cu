@@ -594,23 +594,23 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
 // per-head (max, 1/sum) for the deferred score pass.  Launched right behind the decode kernel
 // with programmatic dependent launch: its CTAs are resident early and start when it completes.
 template <int D>
-__global__ void __launch_bounds__(1024) k_decode_merge(const DevView v, const int layer, void* __restrict__ o,
+__global__ void __launch_bounds__(512) k_decode_merge(const DevView v, const int layer, void* __restrict__ o,
                                                       const int zpar) {
   // one CTA per unit; every thread loads, for its output element, the (m, l) of its head and
   // the o value of all C+1 partials at once (independent loads: one L2 round trip), then
   // merges them in rank order (deterministic).  C+1 <= 65.
-  const int unit = blockIdx.x, tid = threadIdx.x;
+  const int unit = blockIdx.x, tid = threadIdx.x + blockIdx.y * blockDim.x;
   const int b = unit / v.Hkv, g = unit - b * v.Hkv;
   const int G = v.G, NP = v.split + 1, tot = G * D;
   unsigned long long* tr = v.trace ? v.trace + (((size_t)layer * v.B * v.Hkv + unit) * v.split) * 8 : nullptr;
-  if (tr && tid == 0) tr[6] = gtimer();
+  if (tr && tid == 0 && blockIdx.y == 0) tr[6] = gtimer();
   pdl_trigger();
   pdl_wait();
-  if (tr && tid == 0) tr[5] = gtimer();
+  if (tr && tid == 0 && blockIdx.y == 0) tr[5] = gtimer();
   const float* P = v.part + (size_t)unit * NP * v.part_stride;
-  for (int e = tid; e < tot; e += blockDim.x) {
+  for (int e = tid; e < tot; e += blockDim.x * gridDim.y) {
     const int h = e / D, dd = e - h * D;
-    constexpr int MAXP = 17;
+    constexpr int MAXP = 16;                        // registers only (512 threads -> <= 128 regs)
     float m[MAXP], l[MAXP], x[MAXP];
     float M = -INFINITY, Ls = 0.f, acc = 0.f;
     for (int c0 = 0; c0 < NP; c0 += MAXP) {          // one batch for split <= 16
@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(1024) k_decode_merge(const DevView v, const in
       ml[8 + h] = invL;
     }
   }
-  if (tr && tid == 0) tr[7] = gtimer();
+  if (tr && tid == 0 && blockIdx.y == 0) tr[7] = gtimer();
 }
 
 size_t merge_smem_bytes(const DevView& v) { (void)v; return 0; }
@@ -760,8 +760,8 @@ static cudaError_t launch_decode_main(const DevView& v, int layer, const void* q
 
 static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, int pdl, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(v.B * v.Hkv, 1, 1);
-  cfg.blockDim = dim3(1024, 1, 1);
+  cfg.gridDim = dim3(v.B * v.Hkv, 2, 1);
+  cfg.blockDim = dim3(512, 1, 1);
   cfg.dynamicSmemBytes = merge_smem_bytes(v);
   cfg.stream = s;
   cudaLaunchAttribute at[2];
