@@ -54,6 +54,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
 }
+// L2 prefetch of a contiguous byte range (no shared-memory destination)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 // streamed K/V rows are read once per layer: evict them first so the hot data stays in L2
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
@@ -289,6 +293,31 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
         if (k >= ntiles) {
           stile[s2] = -1;
           mbar_arrive(full);          // sentinel stage (no data)
+          // This CTA's rows of the NEXT layer (same unit, same tiles) go to L2 now, so HBM keeps
+          // streaming through this layer's merge and the next launch; the next layer's bulk
+          // copies then hit L2.  Nothing of the next layer is computed before its q exists.
+          if (v.l2_prefetch && layer + 1 < v.L) {
+            const size_t ngrp = grp_of(v, layer + 1, b, g);
+            const __nv_bfloat16* nK0 = v.k0[sb] + ngrp * v.cap0 * D;
+            const __nv_bfloat16* nV0 = v.v0[sb] + ngrp * v.cap0 * D;
+            const __nv_bfloat16* nK1 = v.k1[sb] + ngrp * v.cap1 * D;
+            const __nv_bfloat16* nV1 = v.v1[sb] + ngrp * v.cap1 * D;
+            for (int kk = r; kk < ntb; kk += C) {
+              const int ts = kk * TILE;
+              if (ts < sg.a1) {
+                const int nrows = min(TILE, sg.a1 - ts);
+                bulk_prefetch_l2(nK0 + (size_t)ts * D, nrows * ROWB);
+                bulk_prefetch_l2(nV0 + (size_t)ts * D, nrows * ROWB);
+                if (nrows < TILE && !v.stream_mode) {
+                  bulk_prefetch_l2(nK1, (TILE - nrows) * ROWB);
+                  bulk_prefetch_l2(nV1, (TILE - nrows) * ROWB);
+                }
+              } else if (!v.stream_mode) {
+                bulk_prefetch_l2(nK1 + (size_t)(ts - sg.a1) * D, TILEB);
+                bulk_prefetch_l2(nV1 + (size_t)(ts - sg.a1) * D, TILEB);
+              }
+            }
+          }
           break;
         }
         stile[s2] = k;
