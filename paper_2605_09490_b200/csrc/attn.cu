@@ -26,7 +26,10 @@
 //
 // HBM traffic per launch = algorithmic bytes: every visible K/V row once, q, o, the new row,
 // and the 8 B score read+write per visible token per kv head (of the previous layer).
+#include <cooperative_groups.h>
 #include "kv_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace kvt {
 
@@ -242,6 +245,10 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   float* sML = redl + 8 * NW;                                             // [16] merged M, 1/L
   float* nrow = sML + 16;                                                 // [2][D] new token K, V
   float* zn = nrow + 2 * D;                                               // [8] new token logits
+  float* rbuf = zn + 8;                  // cluster merge: [C+1][m 8 | l 8 | o slice] (16-B aligned)
+  const int cm_per = (((v.G * D + C - 1) / C) + 3) & ~3;                  // o floats per rank slice
+  const int cm_rb = cm_per + 16;
+  const bool cm = v.cluster_merge != 0;
 
   // ---------------------------------------------------------------- prologue (pre-PDL-wait)
   const int cur = v.st->cur;
@@ -277,6 +284,9 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  // cluster merge: phase 0 = every CTA of the cluster has started (its shared memory may be
+  // written remotely after the matching wait); phase 1 = every partial has been pushed
+  if (cm) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
 
   if (w == WPROD) {
     // ============================ producer ============================
@@ -351,6 +361,10 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       }
     }
     __syncwarp();
+    if (cm) {
+      asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    }
     return;
   }
   pdl_trigger();
@@ -360,6 +374,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
 
   if (w == WSCORE) {
     // ============================ side warp ============================
+    if (cm) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
     // (1) rank 0: the new token (a1 fused): append its K/V row to T0 row n0-1 (swizzled) and
     //     publish its attention term as the unit's partial number C: m = z, l = 1, o = v_new.
     if (has_new) {
@@ -414,7 +429,38 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
         part[lane] = -INFINITY;
         part[8 + lane] = 0.f;
       }
+      if (cm) {                          // partial number C of every rank's slice
+#pragma unroll
+        for (int k = 0; k < EL; ++k) nrow[lane + 32 * k] = bf16_bits_to_f(vb[k]);
+        if (lane < 8) {
+          zn[lane] = lane < G ? part[lane] : -INFINITY;
+        }
+        __syncwarp();
+        cg::cluster_group cluster = cg::this_cluster();
+        const int tot = G * D, q4 = cm_rb / 4;
+        for (int e = lane; e < C * q4; e += 32) {
+          const int c = e / q4, j4 = e - c * q4;
+          float4 val;
+          if (j4 < 2) {
+            const int h0 = 4 * j4;
+            val = make_float4(zn[h0], zn[h0 + 1], zn[h0 + 2], zn[h0 + 3]);
+          } else if (j4 < 4) {
+            const int h0 = 4 * (j4 - 2);
+            val = make_float4(h0 < G ? 1.f : 0.f, h0 + 1 < G ? 1.f : 0.f, h0 + 2 < G ? 1.f : 0.f, h0 + 3 < G ? 1.f : 0.f);
+          } else {
+            const int idx = c * cm_per + 4 * (j4 - 4);
+            if (idx < tot) {
+              const int dd = idx % D;
+              val = make_float4(nrow[dd], nrow[dd + 1], nrow[dd + 2], nrow[dd + 3]);
+            } else {
+              val = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+          reinterpret_cast<float4*>(cluster.map_shared_rank(rbuf, c) + C * cm_rb)[j4] = val;
+        }
+      }
     }
+    if (cm) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
     return;
   }
 
@@ -612,11 +658,60 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     xp[16 + e] = a;
   }
   named_sync(1, NCONS);
-  {   // publish: visible to the merge kernel once this grid completes (no fence needed)
+  if (!cm) {   // publish: visible to the merge kernel once this grid completes (no fence needed)
     float4* part = reinterpret_cast<float4*>(v.part + ((size_t)unit * (C + 1) + r) * v.part_stride);
     for (int i = tid; i < ps4; i += NCONS) part[i] = reinterpret_cast<const float4*>(xp)[i];
+    if (tr && tid == 0) tr[4] = gtimer();
+    return;
+  }
+  // ---- cluster merge: push (m, l) and slice c of o to rank c, one barrier, merge own slice
+  cg::cluster_group cluster = cg::this_cluster();
+  asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");     // phase 0 (long complete)
+  {
+    const int q4 = cm_rb / 4;
+    const float4* xp4 = reinterpret_cast<const float4*>(xp);
+    for (int e = tid; e < C * q4; e += NCONS) {
+      const int c = e / q4, j4 = e - c * q4;
+      float4 val;
+      if (j4 < 4) {
+        val = xp4[j4];
+      } else {
+        const int idx = c * cm_per + 4 * (j4 - 4);
+        val = idx < tot ? xp4[4 + idx / 4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      reinterpret_cast<float4*>(cluster.map_shared_rank(rbuf, c) + r * cm_rb)[j4] = val;
+    }
   }
   if (tr && tid == 0) tr[4] = gtimer();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (tr && tid == 0) tr[5] = gtimer();
+  {
+    // same arithmetic, same order as k_decode_merge (rank order, new token last)
+    const int NP = C + 1, e0 = r * cm_per;
+    for (int j = tid; j < cm_per && e0 + j < tot; j += NCONS) {
+      const int e = e0 + j, h = e / D, dd = e - h * D;
+      float M = -INFINITY;
+      for (int c = 0; c < NP; ++c) M = fmaxf(M, rbuf[c * cm_rb + h]);
+      float Ls = 0.f, acc = 0.f;
+      for (int c = 0; c < NP; ++c) {
+        const float mc = rbuf[c * cm_rb + h];
+        const float f = mc == -INFINITY ? 0.f : exp2f(mc - M);
+        Ls += f * rbuf[c * cm_rb + 8 + h];
+        acc += f * rbuf[c * cm_rb + 16 + j];
+      }
+      const float invL = 1.0f / Ls;
+      const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
+      if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = acc * invL;
+      else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(acc * invL);
+      if (dd == 0 && zpar >= 0) {        // publish (M, 1/L) for the deferred score pass
+        float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
+        ml[h] = M;
+        ml[8 + h] = invL;
+      }
+    }
+  }
+  if (tr && tid == 0) { tr[6] = gtimer(); tr[7] = tr[6]; }
 }
 
 // Merge of the C per-CTA partials of every unit, in rank order (deterministic): o and the
@@ -712,6 +807,10 @@ size_t attn_smem_bytes(const DevView& v) {
   const size_t xob = (size_t)8 * v.D * 4 + (8 + 8 + 16 * vr.nw + 16 + 2 * v.D + 8) * 4;
   const size_t t2 = (v.cap2 > 0) ? (size_t)vr.nw * 16 * v.D * 2 : 0;
   size_t total = ringb + xob + t2;
+  if (v.cluster_merge) {
+    const int C = v.split, per = (((v.G * v.D + C - 1) / C) + 3) & ~3;
+    total += (size_t)(C + 1) * (per + 16) * 4 + 16;
+  }
   const size_t ow = (size_t)vr.nw * 8 * (v.D + 4) * 4 + vr.nw * 8 * 4;   // end-of-kernel reuse of the ring
   if (ow > (size_t)vr.nst * 2 * tile * v.D * 2) total += ow;   // (never for the shipped variants)
   return total;
@@ -759,7 +858,7 @@ static cudaError_t launch_decode_main(const DevView& v, int layer, const void* q
   cfg.gridDim = dim3(v.split, v.B * v.Hkv, 1);
   cfg.dynamicSmemBytes = attn_smem_bytes(v);
   cfg.stream = s;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   int na = 0;
   if (v.hot_bytes > 0) {
     at[na].id = cudaLaunchAttributeAccessPolicyWindow;
@@ -773,6 +872,13 @@ static cudaError_t launch_decode_main(const DevView& v, int layer, const void* q
   if (pdl) {
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (v.cluster_merge) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = v.split;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
     ++na;
   }
   cfg.attrs = at;
@@ -818,7 +924,7 @@ static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, 
 cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
                                void* o, int zpar, int pdl, cudaStream_t s) {
   cudaError_t e = launch_decode_main(v, layer, q, knew, vnew, o, zpar, pdl, s);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || v.cluster_merge) return e;
   return launch_merge(v, layer, o, zpar, v.use_pdl, s);
 }
 

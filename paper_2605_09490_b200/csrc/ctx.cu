@@ -258,6 +258,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.pdl_pre = getenv("KVTIER_PDL_PRE") ? atoi(getenv("KVTIER_PDL_PRE")) : 1 << 30;
   v.use_pdl = getenv("KVTIER_NOPDL") ? 0 : 1;
   v.l2_prefetch = getenv("KVTIER_L2PF") ? 1 : 0;   // measured: no gain at 7B
+  v.cluster_merge = (getenv("KVTIER_CLUSTER") && atoi(getenv("KVTIER_CLUSTER")) && v.split <= 8) ? 1 : 0;
   v.chunk_max = 0;
   for (int i = 0; i < 2; ++i) {
     v.k0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_k0[i]);

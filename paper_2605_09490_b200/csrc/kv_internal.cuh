@@ -36,6 +36,7 @@ struct DevView {
   int pdl_pre;          // stages the producer may load before griddepcontrol.wait
   int use_pdl;          // chain consecutive layers with programmatic dependent launch
   int l2_prefetch;      // prefetch the next layer's rows into L2 at the end of a layer
+  int cluster_merge;    // merge the unit's partials in distributed shared memory (cluster of split CTAs)
   unsigned long long* trace;   // debug: per-CTA %globaltimer checkpoints (null = off)
   float* zbuf;          // [ZRING][B*Hkv][zrows][8] logits (log2 domain) of recent launches
   float* ml;            // [ZRING][B*Hkv][16] per-head (max, 1/sum) of recent launches

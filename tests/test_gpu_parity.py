@@ -280,3 +280,33 @@ def test_abi_errors():
         run.kv.step(run.Q[1], run.Kn[1], run.Vn[1], run.O, 1, stream=run.main, side=run.side)
     assert e.value.status == -5
     run.close()
+
+
+# --------------------------------------------------------------------- cluster (DSMEM) merge
+@pytest.mark.parametrize("split", [1, 3, 8])
+def test_cluster_merge_parity(split, monkeypatch):
+    monkeypatch.setenv("KVTIER_CLUSTER", "1")
+    w = H.workload("tiny", B=3, L=2, Hq=12, Hkv=2, d=128, N=700, P=40, interval=16, steps=34,
+                   hbm_bp=3000, evict_bp=1000, t2_bp=2500)
+    _run_pair(w, graph=True, check_every=5, split=split)
+
+
+def test_cluster_merge_equals_merge_kernel_bitwise(monkeypatch):
+    # same partials, same merge order and arithmetic -> same bits (o and scores)
+    w = H.workload("tiny", B=2, L=3, Hq=12, Hkv=2, d=128, N=500, P=40, interval=8, steps=24,
+                   hbm_bp=3000, evict_bp=1000, t2_bp=2500)
+    outs, scores = [], []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("KVTIER_CLUSTER", mode)
+        run = H.TieredDecode(w, split=4)
+        run.capture()
+        seq = []
+        for _ in range(w["steps"]):
+            run.step()
+            seq.append(run.output().copy())
+        run.sync()
+        outs.append(np.stack(seq))
+        scores.append(run.kv.export(kt.X_SCORES).copy())
+        run.close()
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(scores[0], scores[1])
