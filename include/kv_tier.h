@@ -213,8 +213,10 @@ KV_TIER_API kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_
 /* Overwrite S_part with host fp32 [B][H_kv][n] (classify cross-feed, AMB-18). Synchronises. */
 KV_TIER_API kv_tier_status kv_tier_import_scores(kv_tier_ctx* ctx, const float* host_S, size_t bytes);
 
-/* Debug: %globaltimer checkpoints [L][B*H_kv][split][8] of the last launch of every layer
- * (start, after PDL wait, first tile, end of K phase, end of V phase, merge, score, end);
+/* Debug: %globaltimer checkpoints [L][B*H_kv][split][16] of the last launch of every layer:
+ * 16 slots per CTA: (start, after PDL wait, first stage, loop done, partial written, merge
+ * released, merge resident, merge end, consumer wait ns, consumer busy ns, stages, producer
+ * empty-wait ns, producer done, -, -, -);
  * only with KVTIER_TRACE=1 in the environment at kv_tier_init. */
 KV_TIER_API kv_tier_status kv_tier_debug_trace(kv_tier_ctx* ctx, uint64_t* host_dst, size_t n);
 

@@ -12,6 +12,8 @@ LIB_DIR = os.path.join(HERE, "lib")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-Xcompiler", "-fvisibility=hidden"]
+if os.environ.get("KVT_TRACE_LOOP"):        # debug: per-stage wait/busy accounting in the trace
+    FLAGS += ["-DKVT_TRACE_LOOP=1"]
 
 TARGETS = {
     "libkvtier.so": ["csrc/ctx.cu", "csrc/attn.cu", "csrc/tiers.cu"],

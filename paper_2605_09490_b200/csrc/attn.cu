@@ -3,31 +3,37 @@
 //
 // C CTAs per unit (request b, kv head g).  The unit's visible rows are laid out virtually as
 // [T0 rows except the new token | pad | T1 staging | pad | T2 int8 | pad | new token],
-// segments starting at multiples of 16, cut into tiles of TILE tokens dealt round-robin to
-// the unit's CTAs (tile k -> CTA k mod C: balanced and deterministic).
+// segments starting at multiples of 16.  Each CTA owns a contiguous range of whole stages
+// (NW 16-row groups) of the bf16 part and one of the int8 part (stage counts differ by <= 1).
 //
-//   producer warp   streams its tiles' K rows and V rows with 1-D bulk async copies
-//                   (cp.async.bulk) into an NST-deep shared-memory ring guarded by full/empty
-//                   mbarriers.  Rows are stored pre-swizzled in HBM (16-B chunk c of store
-//                   row j at c ^ (j & 7)), so a linear copy is the conflict-free layout.
-//   consumer warps  each owns 16 rows of a tile: S^T = K q^T on the tensor cores (mma.sync
+//   producer warp   streams its stages (NW groups = one per consumer warp) with 1-D bulk async
+//                   copies (cp.async.bulk) into an NST-deep shared-memory ring guarded by
+//                   full/empty mbarriers.  Rows are stored pre-swizzled in HBM (16-B chunk c of
+//                   store row j at c ^ (j & 7)), so a linear copy is the conflict-free layout.
+//                   Up to pdl_pre stages are issued before griddepcontrol.wait: they overlap
+//                   the previous kernel's tail.
+//   consumer warps  each owns 16 rows of a stage: S^T = K q^T on the tensor cores (mma.sync
 //                   m16n8k16 bf16, swap-AB: tokens = M, the G <= 8 heads of the group = N),
 //                   per-warp online softmax in fp32, o^T += V^T p^T (movmatrix.trans turns the
 //                   C fragment into the B fragment).  Logits (log2 domain) go to an
 //                   L2-resident buffer for the score update.
-//   merge           warps -> CTA partial (shared memory) -> global partial slot; the LAST CTA
-//                   of the unit to finish (atomic counter) merges the C partials in rank order
-//                   (deterministic), writes o and the per-head (max, 1/sum).  Nobody waits for
-//                   a straggler: finished CTAs exit and free their SM for the next layer.
-//   score warp      meanwhile applies the PREVIOUS layer's cumulative score update:
-//                   S_part[b][g][pos] += sum_{h in g} exp2(z - M_h) / L_h (one fp32 add per
-//                   layer in layer order, AMB-14; every (b, g, pos) written by one thread ->
-//                   no atomics, bit-reproducible).  The last layer's update runs in end_step.
+//   side warp       rank 0: appends the new token's K/V row (a1) and computes its attention
+//                   term on the CUDA cores as one more partial (m = z, l = 1, o = v_new).
+//   merge           warps -> CTA partial (m, l, o) in shared memory, then either
+//                   (default) a global partial slot, merged in rank order by the PDL-chained
+//                   k_decode_merge, which also publishes the per-head (M, 1/L); the score update
+//                   (a4) then runs as k_score_flush on the library's score stream;
+//                   or (KVTIER_CLUSTER=1) one thread-block cluster per unit: partials pushed
+//                   over distributed shared memory (rank c receives slice c of o and every
+//                   (m, l)), one cluster barrier, each rank merges its slice in the same order,
+//                   and applies the score update of its own tokens in the epilogue.
 //
-// HBM traffic per launch = algorithmic bytes: every visible K/V row once, q, o, the new row,
-// and the 8 B score read+write per visible token per kv head (of the previous layer).
 #include <cooperative_groups.h>
 #include "kv_internal.cuh"
+
+#ifndef KVT_TRACE_LOOP
+#define KVT_TRACE_LOOP 0
+#endif
 
 namespace cg = cooperative_groups;
 
@@ -57,10 +63,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
 }
-// L2 prefetch of a contiguous byte range (no shared-memory destination)
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
-}
 // streamed K/V rows are read once per layer: evict them first so the hot data stays in L2
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
@@ -83,7 +85,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-constexpr int NTRACE = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -157,15 +158,15 @@ struct Seg {
   }
 };
 
-// Score pass of one layer over virtual tokens [i0, i1) of the flattened (unit, token) space
-// (called by the score warp of the next layer's kernel and by the end-of-step flush).
-// Batches of SB tokens per thread with every load hoisted (three dependent round trips per
-// batch: position, then S_part + logits, then the store).
-__device__ __forceinline__ void score_range(const DevView& v, const Seg& sg, int cur, int zpar, long long i0,
-                                            long long i1, int lane0, int stride, bool& bad) {
-  constexpr int SB = 8;
-  const float* zb = v.zbuf + (size_t)zpar * v.B * v.Hkv * v.zrows * 8;
-  const float* ML = v.ml + (size_t)zpar * v.B * v.Hkv * 16;
+// Score pass over virtual tokens [i0, i1) of the flattened (unit, token) space for nz <= ZBATCH
+// consecutive launches (ring slots zfirst, zfirst+1, ...), applied in launch (= layer) order:
+// S <- fp32(S + inc_l) per launch, the same adds one pass per launch would do.  Every load of a
+// token batch is hoisted (three dependent round trips: position, then S_part + logits, then
+// the store).
+__device__ __forceinline__ void score_range(const DevView& v, const Seg& sg, int cur, int zfirst, int nz,
+                                            long long i0, long long i1, int lane0, int stride, bool& bad) {
+  constexpr int SB = 8 / ZBATCH;
+  const size_t zslot = (size_t)v.B * v.Hkv * v.zrows * 8, mslot = (size_t)v.B * v.Hkv * 16;
   for (long long base = i0 + lane0; base < i1; base += (long long)stride * SB) {
     int pos[SB], uu[SB], tt[SB];
 #pragma unroll
@@ -182,27 +183,41 @@ __device__ __forceinline__ void score_range(const DevView& v, const Seg& sg, int
       }
     }
     float sv[SB];
-    float4 z0[SB], z1[SB];
+    float4 z0[SB][ZBATCH], z1[SB][ZBATCH];
 #pragma unroll
     for (int k = 0; k < SB; ++k) {
       if (pos[k] >= 0) {
         sv[k] = v.S[(size_t)uu[k] * v.Nmax + pos[k]];     // S_part[b][g] rows are unit-major
-        const float* z = zb + ((size_t)uu[k] * v.zrows + tt[k]) * 8;
-        z0[k] = *reinterpret_cast<const float4*>(z);
-        z1[k] = *reinterpret_cast<const float4*>(z + 4);
+#pragma unroll
+        for (int j = 0; j < ZBATCH; ++j) {
+          if (j < nz) {
+            const int slot = (zfirst + j) % ZRING;
+            const float* z = v.zbuf + slot * zslot + ((size_t)uu[k] * v.zrows + tt[k]) * 8;
+            z0[k][j] = *reinterpret_cast<const float4*>(z);
+            z1[k][j] = *reinterpret_cast<const float4*>(z + 4);
+          }
+        }
       }
     }
 #pragma unroll
     for (int k = 0; k < SB; ++k) {
       if (pos[k] < 0) continue;
-      const float* ml = ML + (size_t)uu[k] * 16;
-      const float zz[8] = {z0[k].x, z0[k].y, z0[k].z, z0[k].w, z1[k].x, z1[k].y, z1[k].z, z1[k].w};
-      float inc = 0.f;
+      float s = sv[k];
 #pragma unroll
-      for (int h = 0; h < 8; ++h)
-        if (h < v.G) inc += exp2f(zz[h] - ml[h]) * ml[8 + h];
-      v.S[(size_t)uu[k] * v.Nmax + pos[k]] = sv[k] + inc;
-      bad |= !isfinite(inc);
+      for (int j = 0; j < ZBATCH; ++j) {
+        if (j >= nz) break;
+        const int slot = (zfirst + j) % ZRING;
+        const float* ml = v.ml + slot * mslot + (size_t)uu[k] * 16;
+        const float zz[8] = {z0[k][j].x, z0[k][j].y, z0[k][j].z, z0[k][j].w,
+                             z1[k][j].x, z1[k][j].y, z1[k][j].z, z1[k][j].w};
+        float inc = 0.f;
+#pragma unroll
+        for (int h = 0; h < 8; ++h)
+          if (h < v.G) inc += exp2f(zz[h] - ml[h]) * ml[8 + h];
+        s = s + inc;
+        bad |= !isfinite(inc);
+      }
+      v.S[(size_t)uu[k] * v.Nmax + pos[k]] = s;
     }
   }
 }
@@ -229,7 +244,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   const int gq = lane >> 2, tq = lane & 3;
   const int G = v.G;
   unsigned long long* tr = v.trace ? v.trace + (((size_t)layer * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * NTRACE : nullptr;
-  if (tr && tid == 0) tr[0] = gtimer();
+  if (tr && tid == 0) { tr[0] = gtimer(); for (int x = 8; x < NTRACE; ++x) tr[x] = 0; }
 
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;                                             // [NST][K tile | V tile]
@@ -245,7 +260,8 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   float* sML = redl + 8 * NW;                                             // [16] merged M, 1/L
   float* nrow = sML + 16;                                                 // [2][D] new token K, V
   float* zn = nrow + 2 * D;                                               // [8] new token logits
-  float* rbuf = zn + 8;                  // cluster merge: [C+1][m 8 | l 8 | o slice] (16-B aligned)
+  float* rbuf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(zn + 8) + 15) & ~(uintptr_t)15);
+                                         // cluster merge: [C+1][m 8 | l 8 | o slice] (16-B aligned)
   const int cm_per = (((v.G * D + C - 1) / C) + 3) & ~3;                  // o floats per rank slice
   const int cm_rb = cm_per + 16;
   const bool cm = v.cluster_merge != 0;
@@ -254,9 +270,28 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   const int cur = v.st->cur;
   Seg sg;
   sg.init(v.cnt[cur] + b * CNT_STRIDE);
-  const int ntb = (sg.a2 + TILE - 1) / TILE;                 // bf16 tiles [0, a2)
-  const int nt2 = (sg.n2 + TILE - 1) / TILE;                 // int8 tiles [a2, a2 + n2)
-  const int ntiles = ntb + nt2;
+  // This CTA's work: stages of NW 16-row groups (one per consumer warp) from the unit's stage
+  // list [bf16 segment [0, a2) | int8 segment [a2, a2 + n2)], dealt round-robin (stage k ->
+  // rank k mod C, default) or as contiguous ranges (KVTIER_RR=0).  Static either way, so the
+  // fp32 summation order never depends on timing.
+  const int gbf = sg.a2 >> 4, gq2 = (sg.n2 + 15) >> 4;
+  const int sbf = (gbf + NW - 1) / NW, ns_all = sbf + (gq2 + NW - 1) / NW;
+  int cs0, cstr, nstage;
+  if (v.stage_rr) {
+    cs0 = r;
+    cstr = C;
+    nstage = ns_all > r ? (ns_all - r + C - 1) / C : 0;
+  } else {
+    cs0 = (int)((long long)ns_all * r / C);
+    cstr = 1;
+    nstage = (int)((long long)ns_all * (r + 1) / C) - cs0;
+  }
+  auto stage_at = [&](int i, bool& t2, int& g0, int& ng) {   // this CTA's i-th stage
+    const int gs = cs0 + i * cstr;
+    t2 = gs >= sbf;
+    g0 = (t2 ? gs - sbf : gs) * NW;
+    ng = min(NW, (t2 ? gq2 : gbf) - g0);
+  };
   const bool has_new = r == 0;                               // rank 0 handles the new token
 
   const int sb = v.st->scur;                                 // row-store buffer
@@ -290,73 +325,59 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
 
   if (w == WPROD) {
     // ============================ producer ============================
-    // tiles are dealt round-robin to the unit's CTAs (tile k -> rank k mod C): balanced,
-    // and deterministic (the fp32 summation order never depends on timing)
+    // streams this CTA's stages (static ranges: the fp32 summation order never depends on timing)
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
       for (int i = 0;; ++i) {
         const int s2 = i % NST;
         if (i == v.pdl_pre) pdl_wait();   // at most pdl_pre stages in flight before the previous layer ends
-        if (i >= NST) mbar_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
-        const int k = r + i * C;
+        if (i >= NST) {
+#if KVT_TRACE_LOOP
+          const unsigned long long tw = tr ? gtimer() : 0;
+          mbar_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
+          if (tr) tr[11] += gtimer() - tw;
+#else
+          mbar_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
+#endif
+        }
         const uint32_t full = full0 + 8 * s2, dst = ring_s + s2 * STAGEB;
-        if (k >= ntiles) {
+        if (i >= nstage) {
+          if (tr) tr[12] = gtimer();
           stile[s2] = -1;
           mbar_arrive(full);          // sentinel stage (no data)
-          // This CTA's rows of the NEXT layer (same unit, same tiles) go to L2 now, so HBM keeps
-          // streaming through this layer's merge and the next launch; the next layer's bulk
-          // copies then hit L2.  Nothing of the next layer is computed before its q exists.
-          if (v.l2_prefetch && layer + 1 < v.L) {
-            const size_t ngrp = grp_of(v, layer + 1, b, g);
-            const __nv_bfloat16* nK0 = v.k0[sb] + ngrp * v.cap0 * D;
-            const __nv_bfloat16* nV0 = v.v0[sb] + ngrp * v.cap0 * D;
-            const __nv_bfloat16* nK1 = v.k1[sb] + ngrp * v.cap1 * D;
-            const __nv_bfloat16* nV1 = v.v1[sb] + ngrp * v.cap1 * D;
-            for (int kk = r; kk < ntb; kk += C) {
-              const int ts = kk * TILE;
-              if (ts < sg.a1) {
-                const int nrows = min(TILE, sg.a1 - ts);
-                bulk_prefetch_l2(nK0 + (size_t)ts * D, nrows * ROWB);
-                bulk_prefetch_l2(nV0 + (size_t)ts * D, nrows * ROWB);
-                if (nrows < TILE && !v.stream_mode) {
-                  bulk_prefetch_l2(nK1, (TILE - nrows) * ROWB);
-                  bulk_prefetch_l2(nV1, (TILE - nrows) * ROWB);
-                }
-              } else if (!v.stream_mode) {
-                bulk_prefetch_l2(nK1 + (size_t)(ts - sg.a1) * D, TILEB);
-                bulk_prefetch_l2(nV1 + (size_t)(ts - sg.a1) * D, TILEB);
-              }
-            }
-          }
           break;
         }
-        stile[s2] = k;
-        if (k < ntb) {
-          const int ts = k * TILE;
-          mbar_expect_tx(full, STAGEB);
-          if (ts < sg.a1) {           // T0 rows (pad rows beyond n0o are stale but finite)
-            const int nrows = min(TILE, sg.a1 - ts);
-            bulk_g2s_ef(dst, K0 + (size_t)ts * D, nrows * ROWB, full, pol);
-            bulk_g2s_ef(dst + TILEB, V0 + (size_t)ts * D, nrows * ROWB, full, pol);
-            if (nrows < TILE) {
-              bulk_g2s_ef(dst + nrows * ROWB, K1, (TILE - nrows) * ROWB, full, pol);
-              bulk_g2s_ef(dst + TILEB + nrows * ROWB, V1, (TILE - nrows) * ROWB, full, pol);
+        stile[s2] = i;
+        bool st2;
+        int g0, ng;
+        stage_at(i, st2, g0, ng);
+        const int nrows = 16 * ng;
+        if (!st2) {                   // bf16 rows: T0 (pad rows beyond n0o are stale but finite), T1
+          const int ts = 16 * g0;
+          mbar_expect_tx(full, 2 * nrows * ROWB);
+          if (ts < sg.a1) {           // a1 is a multiple of 16: the T1 part starts at T1 row 0
+            const int n0r = min(nrows, sg.a1 - ts);
+            bulk_g2s_ef(dst, K0 + (size_t)ts * D, n0r * ROWB, full, pol);
+            bulk_g2s_ef(dst + TILEB, V0 + (size_t)ts * D, n0r * ROWB, full, pol);
+            if (n0r < nrows) {
+              bulk_g2s_ef(dst + n0r * ROWB, K1, (nrows - n0r) * ROWB, full, pol);
+              bulk_g2s_ef(dst + TILEB + n0r * ROWB, V1, (nrows - n0r) * ROWB, full, pol);
             }
           } else {
-            bulk_g2s_ef(dst, K1 + (size_t)(ts - sg.a1) * D, TILEB, full, pol);
-            bulk_g2s_ef(dst + TILEB, V1 + (size_t)(ts - sg.a1) * D, TILEB, full, pol);
+            bulk_g2s_ef(dst, K1 + (size_t)(ts - sg.a1) * D, nrows * ROWB, full, pol);
+            bulk_g2s_ef(dst + TILEB, V1 + (size_t)(ts - sg.a1) * D, nrows * ROWB, full, pol);
           }
-        } else {                      // T2: int8 codes + fp32 scales (canonical layout)
-          const int j0 = (k - ntb) * TILE;
+        } else {                      // T2: int8 codes + fp32 scales (canonical layout; rows < cap2)
+          const int j0 = 16 * g0;
           const int8_t* CK = v.c2k[sb] + (grp * v.cap2 + j0) * D;
           const int8_t* CV = v.c2v[sb] + (grp * v.cap2 + j0) * D;
           const float* SK = v.s2k[sb] + grp * v.cap2 + j0;
           const float* SV = v.s2v[sb] + grp * v.cap2 + j0;
-          mbar_expect_tx(full, 2 * (TILE * D + TILE * 4));
-          bulk_g2s(dst, CK, TILE * D, full);
-          bulk_g2s(dst + TILE * D, SK, TILE * 4, full);
-          bulk_g2s(dst + TILEB, CV, TILE * D, full);
-          bulk_g2s(dst + TILEB + TILE * D, SV, TILE * 4, full);
+          mbar_expect_tx(full, 2 * (nrows * D + nrows * 4));
+          bulk_g2s(dst, CK, nrows * D, full);
+          bulk_g2s(dst + TILE * D, SK, nrows * 4, full);
+          bulk_g2s(dst + TILEB, CV, nrows * D, full);
+          bulk_g2s(dst + TILEB + TILE * D, SV, nrows * 4, full);
         }
       }
     }
@@ -487,31 +508,41 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));   // log2(e)/sqrt(d)
   float* zrow = zpar >= 0 ? v.zbuf + ((size_t)zpar * v.B * v.Hkv + unit) * v.zrows * 8 : nullptr;
 
-  // one warp-slice (16 rows) of a tile: logits, online softmax, P.V
+  // one warp-slice (16 rows) of a stage: logits, online softmax, P.V.  Lazy rescale: the running
+  // max of a head only moves (warp reduction + rescale of o and l) when some logit exceeds it
+  // by more than RESCALE_SLACK (log2 units); otherwise p = exp2(z - m) <= 2^RESCALE_SLACK is
+  // accumulated against the stale max -- the same softmax, without the shuffle chain.
+  constexpr float RESCALE_SLACK = 8.f;
   auto online = [&](float z00, float z01, float z10, float z11, float& p00, float& p01, float& p10, float& p11) {
-    float ta = fmaxf(z00, z10), tb = fmaxf(z01, z11);
+    const bool grow = z00 > mxa + RESCALE_SLACK || z10 > mxa + RESCALE_SLACK ||
+                      z01 > mxb + RESCALE_SLACK || z11 > mxb + RESCALE_SLACK;
+    if (__any_sync(0xffffffffu, grow)) {
+      float ta = fmaxf(z00, z10), tb = fmaxf(z01, z11);
 #pragma unroll
-    for (int off = 4; off < 32; off <<= 1) {
-      ta = fmaxf(ta, __shfl_xor_sync(0xffffffffu, ta, off));
-      tb = fmaxf(tb, __shfl_xor_sync(0xffffffffu, tb, off));
-    }
-    const float na = fmaxf(mxa, ta), nb = fmaxf(mxb, tb);     // finite: some row is valid
-    const float ca = exp2f(mxa - na), cb = exp2f(mxb - nb);   // 0 when the old max is -inf
-    mxa = na;
-    mxb = nb;
+      for (int off = 4; off < 32; off <<= 1) {
+        ta = fmaxf(ta, __shfl_xor_sync(0xffffffffu, ta, off));
+        tb = fmaxf(tb, __shfl_xor_sync(0xffffffffu, tb, off));
+      }
+      const float na = fmaxf(mxa, ta), nb = fmaxf(mxb, tb);     // finite: some row is valid
+      const float ca = exp2f(mxa - na), cb = exp2f(mxb - nb);   // 0 when the old max is -inf
+      mxa = na;
+      mxb = nb;
 #pragma unroll
-    for (int mt = 0; mt < KS; ++mt) {
-      oacc[mt][0] *= ca;
-      oacc[mt][2] *= ca;
-      oacc[mt][1] *= cb;
-      oacc[mt][3] *= cb;
+      for (int mt = 0; mt < KS; ++mt) {
+        oacc[mt][0] *= ca;
+        oacc[mt][2] *= ca;
+        oacc[mt][1] *= cb;
+        oacc[mt][3] *= cb;
+      }
+      la *= ca;
+      lb *= cb;
     }
-    p00 = exp2f(z00 - na);
-    p01 = exp2f(z01 - nb);
-    p10 = exp2f(z10 - na);
-    p11 = exp2f(z11 - nb);
-    la = la * ca + p00 + p10;
-    lb = lb * cb + p01 + p11;
+    p00 = exp2f(z00 - mxa);
+    p01 = exp2f(z01 - mxb);
+    p10 = exp2f(z10 - mxa);
+    p11 = exp2f(z11 - mxb);
+    la += p00 + p10;
+    lb += p01 + p11;
   };
   const int mi = lane >> 3, ii = lane & 7;
   auto qk = [&](uint32_t sK, int rowbase, float* acc) {
@@ -555,19 +586,33 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     __syncwarp();
   };
 
+#if KVT_TRACE_LOOP
+  unsigned long long tprev = 0;
+#endif
   for (int i = 0;; ++i) {
     const int s2 = i % NST;
+#if KVT_TRACE_LOOP   // per-stage wait / busy accounting (debug builds: -DKVT_TRACE_LOOP=1)
+    const unsigned long long tw = (tr && tid == 0) ? gtimer() : 0;
+    if (tr && tid == 0 && i > 0) tr[9] += tw - tprev;
+    if (tr && tid == 0 && i == 1) tr[13] = tw - tprev;       // first stage (includes the q load)
     mbar_wait(full0 + 8 * s2, (i / NST) & 1);
+    if (tr && tid == 0) { tprev = gtimer(); tr[8] += tprev - tw; tr[10] += 1; }
+#else
+    mbar_wait(full0 + 8 * s2, (i / NST) & 1);
+#endif
     const int k = stile[s2];
     if (k < 0) break;
     if (tr && tid == 0 && i == 0) tr[2] = gtimer();
     const uint32_t sK = ring_s + s2 * STAGEB, sV = sK + TILEB;
-    const bool t2 = k >= ntb;
-    const int tv0 = t2 ? sg.a2 + (k - ntb) * TILE : k * TILE;
+    bool t2;
+    int g0, ng;
+    stage_at(k, t2, g0, ng);
+    const bool wact = w < ng;                                 // this warp's group is in the stage
+    const int tv0 = t2 ? sg.a2 + 16 * g0 : 16 * g0;
     const int r0 = w * 16 + gq, r1 = r0 + 8;
     const int t0 = tv0 + r0, t1 = tv0 + r1;
-    const bool v0 = t2 ? (t0 - sg.a2 < sg.n2) : sg.bf16_valid(t0);
-    const bool v1 = t2 ? (t1 - sg.a2 < sg.n2) : sg.bf16_valid(t1);
+    const bool v0 = wact && (t2 ? (t0 - sg.a2 < sg.n2) : sg.bf16_valid(t0));
+    const bool v1 = wact && (t2 ? (t1 - sg.a2 < sg.n2) : sg.bf16_valid(t1));
     if (__any_sync(0xffffffffu, v0 || v1)) {
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
       float fk0 = sl2, fk1 = sl2, fv0 = 1.f, fv1 = 1.f;
@@ -704,14 +749,80 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
       if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = acc * invL;
       else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(acc * invL);
-      if (dd == 0 && zpar >= 0) {        // publish (M, 1/L) for the deferred score pass
-        float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
-        ml[h] = M;
-        ml[8 + h] = invL;
-      }
     }
   }
-  if (tr && tid == 0) { tr[6] = gtimer(); tr[7] = tr[6]; }
+  if (tr && tid == 0) tr[6] = gtimer();
+  if (zpar < 0) return;
+  // ---- a4 fused: every rank holds the (m, l) of all partials, hence the unit's global (M, 1/L)
+  //      per head (bitwise the merge's); the exact probabilities of this CTA's own tokens
+  //      update S_part[b][g][pos] (one fp32 add per (step, layer), AMB-14; one writer per entry)
+  if (tid < 8) {
+    float M = -INFINITY;
+    for (int c = 0; c <= C; ++c) M = fmaxf(M, rbuf[c * cm_rb + tid]);
+    float Ls = 0.f;
+    for (int c = 0; c <= C; ++c) {
+      const float mc = rbuf[c * cm_rb + tid];
+      const float f = mc == -INFINITY ? 0.f : exp2f(mc - M);
+      Ls += f * rbuf[c * cm_rb + 8 + tid];
+    }
+    sML[tid] = M;
+    sML[8 + tid] = 1.0f / Ls;
+  }
+  named_sync(1, NCONS);
+  {
+    constexpr int SBE = 4;
+    const int ntok = nstage * TILE + (has_new ? 1 : 0);   // + the new token (rank 0, last)
+    float* S = v.S + (size_t)unit * v.Nmax;
+    bool bad = false;
+    for (int j0 = tid; j0 < ntok; j0 += NCONS * SBE) {
+      int pos[SBE], tt[SBE];
+      float4 z0[SBE], z1[SBE];
+#pragma unroll
+      for (int k = 0; k < SBE; ++k) {
+        const int j = j0 + k * NCONS;
+        pos[k] = -1;
+        tt[k] = 0;
+        if (j < ntok) {
+          int t;
+          bool ok;
+          if (j < nstage * TILE) {        // stage rows: T0/T1 or T2 rows only (never pads)
+            bool jt2;
+            int jg0, jng;
+            stage_at(j / TILE, jt2, jg0, jng);
+            const int row = j % TILE;
+            t = (jt2 ? sg.a2 : 0) + 16 * jg0 + row;
+            ok = row < 16 * jng && (jt2 ? t < sg.a2 + sg.n2 : sg.bf16_valid(t));
+          } else {                        // the new token (rank 0)
+            t = sg.a3;
+            ok = true;
+          }
+          if (ok) {
+            tt[k] = t;
+            pos[k] = sg.pos(v, cur, b, t);
+            z0[k] = *reinterpret_cast<const float4*>(zrow + (size_t)t * 8);
+            z1[k] = *reinterpret_cast<const float4*>(zrow + (size_t)t * 8 + 4);
+          }
+        }
+      }
+      float sv[SBE];
+#pragma unroll
+      for (int k = 0; k < SBE; ++k)
+        if (pos[k] >= 0) sv[k] = S[pos[k]];
+#pragma unroll
+      for (int k = 0; k < SBE; ++k) {
+        if (pos[k] < 0) continue;
+        const float zz[8] = {z0[k].x, z0[k].y, z0[k].z, z0[k].w, z1[k].x, z1[k].y, z1[k].z, z1[k].w};
+        float inc = 0.f;
+#pragma unroll
+        for (int h = 0; h < 8; ++h)
+          if (h < G) inc += exp2f(zz[h] - sML[h]) * sML[8 + h];
+        S[pos[k]] = sv[k] + inc;
+        bad |= !isfinite(inc);
+      }
+    }
+    if (bad) atomicOr(&v.st->err, 1);
+  }
+  if (tr && tid == 0) tr[7] = gtimer();
 }
 
 // Merge of the C per-CTA partials of every unit, in rank order (deterministic): o and the
@@ -726,7 +837,7 @@ __global__ void __launch_bounds__(512) k_decode_merge(const DevView v, const int
   const int unit = blockIdx.x, tid = threadIdx.x + blockIdx.y * blockDim.x;
   const int b = unit / v.Hkv, g = unit - b * v.Hkv;
   const int G = v.G, NP = v.split + 1, tot = G * D;
-  unsigned long long* tr = v.trace ? v.trace + (((size_t)layer * v.B * v.Hkv + unit) * v.split) * 8 : nullptr;
+  unsigned long long* tr = v.trace ? v.trace + (((size_t)layer * v.B * v.Hkv + unit) * v.split) * NTRACE : nullptr;
   if (tr && tid == 0 && blockIdx.y == 0) tr[6] = gtimer();
   pdl_trigger();
   pdl_wait();
@@ -778,20 +889,20 @@ __global__ void __launch_bounds__(512) k_decode_merge(const DevView v, const int
 
 size_t merge_smem_bytes(const DevView& v) { (void)v; return 0; }
 
-// a4: the score update of one decode_attention launch (ring slot zpar), on the library's
-// score stream, off the attention critical path.
-__global__ void __launch_bounds__(256) k_score_flush(const DevView v, const int zpar) {
+// a4: the score update of nz consecutive decode_attention launches (ring slots zfirst..), on
+// the library's score stream, off the attention critical path.
+__global__ void __launch_bounds__(256) k_score_flush(const DevView v, const int zfirst, const int nz) {
   const int cur = v.st->cur;
   Seg sg;
   sg.init(v.cnt[cur]);          // counts are uniform across requests
   const long long tot = (long long)v.B * v.Hkv * sg.nvirt;
   bool bad = false;
-  score_range(v, sg, cur, zpar, 0, tot, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, bad);
+  score_range(v, sg, cur, zfirst, nz, 0, tot, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, bad);
   if (bad) atomicOr(&v.st->err, 1);
 }
 
-cudaError_t launch_score_flush(const DevView& v, int zpar, cudaStream_t s) {
-  k_score_flush<<<148, 256, 0, s>>>(v, zpar);
+cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_t s) {
+  k_score_flush<<<148, 256, 0, s>>>(v, zfirst, nz);
   return cudaGetLastError();
 }
 

@@ -33,8 +33,9 @@ struct kv_tier_ctx {
   std::vector<int> appended_step;          // step in which layer l's new row was written
   bool offload_pending = false;
   bool capturing = false;
-  int zslot_next = 0;                      // logits/ML ring slot of the next fused decode_attention
-  bool slot_busy[ZRING] = {false, false, false, false};   // a score kernel may still read the slot
+  int zslot_next = 0;                      // logits/ML ring slot of the next fused decode_attention (0 at step start)
+  int zpend_first = 0, zpend_n = 0;        // launches whose score update is not yet issued
+  bool slot_busy[ZRING] = {};              // a score kernel may still read the slot
   bool scores_pending = false;             // score kernels not yet joined back into the main stream
   cudaStream_t score_stream = nullptr;     // a4 score updates run here, off the attention chain
   cudaEvent_t ev_merged[ZRING] = {}, ev_scored[ZRING] = {}, ev_score_tail = nullptr;
@@ -257,7 +258,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.variant = cfg->variant;
   v.pdl_pre = getenv("KVTIER_PDL_PRE") ? atoi(getenv("KVTIER_PDL_PRE")) : 1 << 30;
   v.use_pdl = getenv("KVTIER_NOPDL") ? 0 : 1;
-  v.l2_prefetch = getenv("KVTIER_L2PF") ? 1 : 0;   // measured: no gain at 7B
+  v.stage_rr = getenv("KVTIER_RR") ? atoi(getenv("KVTIER_RR")) : 1;
   v.cluster_merge = (getenv("KVTIER_CLUSTER") && atoi(getenv("KVTIER_CLUSTER")) && v.split <= 8) ? 1 : 0;
   v.chunk_max = 0;
   for (int i = 0; i < 2; ++i) {
@@ -313,7 +314,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     v.hs2v = reinterpret_cast<float*>(h + 2 * rows * v.D + rows * 4);
   }
   if (getenv("KVTIER_TRACE") && atoi(getenv("KVTIER_TRACE")) > 0) {
-    const size_t tb = (size_t)v.L * v.split * v.B * v.Hkv * 8 * sizeof(unsigned long long);
+    const size_t tb = (size_t)v.L * v.split * v.B * v.Hkv * NTRACE * sizeof(unsigned long long);
     if (cudaMalloc(&ctx->trace, tb) == cudaSuccess) { cudaMemset(ctx->trace, 0, tb); v.trace = ctx->trace; }
   }
   if (attn_smem_bytes(v) > 227 * 1024 || merge_smem_bytes(v) > 227 * 1024) {
@@ -430,6 +431,8 @@ kv_tier_status kv_tier_begin_step(kv_tier_ctx* ctx, void* stream) {
   ctx->step_open = true;
   ctx->classified = false;
   ctx->slot_recorded[0] = ctx->slot_recorded[1] = false;
+  ctx->zslot_next = 0;
+  ctx->zpend_n = 0;
   return KV_TIER_OK;
 }
 
@@ -461,6 +464,24 @@ kv_tier_status kv_tier_prefetch(kv_tier_ctx* ctx, int32_t layer, void* side) {
   return cuda_check(ctx, e, "prefetch");
 }
 
+// a4 on the score stream: S_part += sum_h exp2(z - M)/L for the pending launches (layer order),
+// once the last of them has merged.  Slots are batched ZBATCH-aligned from slot 0 each step.
+static cudaError_t issue_scores(kv_tier_ctx* ctx, cudaStream_t s) {
+  const int z0 = ctx->zpend_first, nz = ctx->zpend_n;
+  (void)s;
+  cudaError_t e = cudaSuccess;
+  for (int j = 0; j < nz && e == cudaSuccess; ++j)    // launches may sit on different streams
+    e = cudaStreamWaitEvent(ctx->score_stream, ctx->ev_merged[(z0 + j) % ZRING], 0);
+  if (e == cudaSuccess) e = launch_score_flush(ctx->v, z0, nz, ctx->score_stream);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_scored[z0], ctx->score_stream);
+  if (e == cudaSuccess) {
+    for (int j = 0; j < nz; ++j) ctx->slot_busy[(z0 + j) % ZRING] = true;
+    ctx->scores_pending = true;
+    ctx->zpend_n = 0;
+  }
+  return e;
+}
+
 static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, const void* q, const void* k_new,
                                             const void* v_new, void* o, int32_t fuse_score_update, void* stream,
                                             int pdl) {
@@ -477,21 +498,27 @@ static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, con
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
   if (ctx->v.stream_mode) e = cudaStreamWaitEvent(s, ctx->ev_prefetched[layer], 0);
+  if (ctx->v.cluster_merge) {   // a4 fused into the kernel's epilogue (one logits slot, no score stream)
+    const int zp = fuse_score_update ? 0 : -1;
+    if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, zp, pdl, s);
+    if (e == cudaSuccess && ctx->v.stream_mode) {
+      e = cudaEventRecord(ctx->ev_slot_free[layer & 1], s);
+      ctx->slot_recorded[layer & 1] = true;
+    }
+    if (e == cudaSuccess && k_new) ctx->appended_step[layer] = ctx->t;
+    return cuda_check(ctx, e, "decode_attention");
+  }
   const int zpar = fuse_score_update ? ctx->zslot_next : -1;
   // the ring slot's previous score kernel must be done before its logits are overwritten
-  if (e == cudaSuccess && zpar >= 0 && ctx->slot_busy[zpar]) e = cudaStreamWaitEvent(s, ctx->ev_scored[zpar], 0);
+  if (e == cudaSuccess && zpar >= 0 && ctx->slot_busy[zpar])
+    e = cudaStreamWaitEvent(s, ctx->ev_scored[zpar - zpar % ZBATCH], 0);
   if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, zpar, pdl, s);
+  if (e == cudaSuccess && zpar >= 0) e = cudaEventRecord(ctx->ev_merged[zpar], s);
   if (e == cudaSuccess && zpar >= 0) {
-    // a4 on the score stream: S_part += sum_h exp2(z - M)/L once this launch's merge is done
-    e = cudaEventRecord(ctx->ev_merged[zpar], s);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->score_stream, ctx->ev_merged[zpar], 0);
-    if (e == cudaSuccess) e = launch_score_flush(ctx->v, zpar, ctx->score_stream);
-    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_scored[zpar], ctx->score_stream);
-    if (e == cudaSuccess) {
-      ctx->slot_busy[zpar] = true;
-      ctx->scores_pending = true;
-      ctx->zslot_next = (zpar + 1) % ZRING;
-    }
+    if (ctx->zpend_n == 0) ctx->zpend_first = zpar;
+    ctx->zpend_n += 1;
+    ctx->zslot_next = (zpar + 1) % ZRING;
+    if (ctx->zpend_n == ZBATCH) e = issue_scores(ctx, s);
   }
   if (e == cudaSuccess && ctx->v.stream_mode) {
     e = cudaEventRecord(ctx->ev_slot_free[layer & 1], s);
@@ -524,7 +551,8 @@ kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream) {
   if (!ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "end_step without begin_step");
   cudaError_t e = cudaSuccess;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (ctx->scores_pending) {     // join the score stream: S_part is complete for this step
+  if (ctx->zpend_n > 0) e = issue_scores(ctx, s);
+  if (e == cudaSuccess && ctx->scores_pending) {     // join the score stream: S_part is complete for this step
     e = cudaEventRecord(ctx->ev_score_tail, ctx->score_stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->ev_score_tail, 0);
   }
@@ -533,6 +561,8 @@ kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream) {
   if (st) return st;
   ctx->scores_pending = false;
   for (auto& b : ctx->slot_busy) b = false;
+  ctx->zslot_next = 0;
+  ctx->zpend_n = 0;
   ctx->step_open = false;
   ctx->t += 1;
   return KV_TIER_OK;
@@ -631,7 +661,6 @@ kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const
   const bool classified = ctx->classified;
   const std::vector<int> pstep = ctx->prefetched_step;
   const std::vector<int> astep = ctx->appended_step;
-  const int zpn = ctx->zslot_next;
   cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return cuda_check(ctx, e, "begin capture");
   ctx->capturing = true;
@@ -642,7 +671,8 @@ kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const
   ctx->n = n; ctx->t = t; ctx->c[0] = c0; ctx->classified = classified; ctx->step_open = false;
   ctx->prefetched_step = pstep;
   ctx->appended_step = astep;
-  ctx->zslot_next = zpn;
+  ctx->zslot_next = 0;
+  ctx->zpend_n = 0;
   for (auto& b : ctx->slot_busy) b = false;
   ctx->scores_pending = false;
   if (st) { if (g) cudaGraphDestroy(g); return st; }
@@ -669,7 +699,6 @@ kv_tier_status kv_tier_step_graph_launch(kv_tier_ctx* ctx, void* stream) {
   ctx->c[0] += 1;
   ctx->t += 1;
   ctx->classified = false;
-  ctx->zslot_next = (ctx->zslot_next + ctx->v.L) % ZRING;   // same transitions as kv_tier_step
   return KV_TIER_OK;
 }
 
@@ -850,7 +879,7 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
 
 kv_tier_status kv_tier_debug_trace(kv_tier_ctx* ctx, uint64_t* host_dst, size_t n) {
   if (!ctx || !host_dst) return fail(ctx, KV_TIER_E_INVAL, "null arg");
-  const size_t need = (size_t)ctx->v.L * ctx->v.split * ctx->v.B * ctx->v.Hkv * 8;
+  const size_t need = (size_t)ctx->v.L * ctx->v.split * ctx->v.B * ctx->v.Hkv * NTRACE;
   if (!ctx->trace) return fail(ctx, KV_TIER_E_STATE, "tracing off (set KVTIER_TRACE=1 before kv_tier_init)");
   if (n != need) return fail(ctx, KV_TIER_E_INVAL, "trace needs %zu entries", need);
   cudaError_t e = cudaDeviceSynchronize();

@@ -7,8 +7,11 @@
 namespace kvt {
 
 constexpr int T0 = 0, T1 = 1, T2 = 2, T3 = 3;
-constexpr int CNT_STRIDE = 8;
-constexpr int ZRING = 4;          // logits/ML ring slots (score kernels lag the decode chain)   // cnt[buf][b][8]: |T0| |T1| |T2| |T3| |visible at event| pad..
+constexpr int NTRACE = 16;        // debug trace slots per CTA (KVTIER_TRACE=1)
+constexpr int CNT_STRIDE = 8;     // cnt[buf][b][8]: |T0| |T1| |T2| |T3| |visible at event| pad..
+constexpr int ZRING = 4;          // logits/ML ring slots (score kernels lag the decode chain)
+constexpr int ZBATCH = 1;         // launches whose score updates one score kernel applies (layer order;
+                                  // measured: batching 4 made the kernel too big to share SMs with the chain)
 
 // Mutable device state (graph-static kernels read it instead of taking args).
 struct DevState {
@@ -35,7 +38,7 @@ struct DevView {
   int variant;          // decode-attention kernel variant (warps x pipeline stages)
   int pdl_pre;          // stages the producer may load before griddepcontrol.wait
   int use_pdl;          // chain consecutive layers with programmatic dependent launch
-  int l2_prefetch;      // prefetch the next layer's rows into L2 at the end of a layer
+  int stage_rr;         // stages dealt round-robin to the unit's CTAs (else contiguous ranges)
   int cluster_merge;    // merge the unit's partials in distributed shared memory (cluster of split CTAs)
   unsigned long long* trace;   // debug: per-CTA %globaltimer checkpoints (null = off)
   float* zbuf;          // [ZRING][B*Hkv][zrows][8] logits (log2 domain) of recent launches
@@ -98,7 +101,7 @@ cudaError_t launch_load_prefix(const DevView& v, int layer, const void* k, const
 cudaError_t launch_init_meta(const DevView& v, int n0, cudaStream_t s);
 cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
                                void* o, int zpar, int pdl, cudaStream_t s);
-cudaError_t launch_score_flush(const DevView& v, int zpar, cudaStream_t s);
+cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_t s);
 cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s);
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);
 cudaError_t launch_classify(const DevView& v, cudaStream_t s);

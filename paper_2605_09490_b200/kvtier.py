@@ -241,11 +241,11 @@ class KvTier:
         return buf.view(np.float32).reshape(B, H, -1, 2)
 
     def debug_trace(self):
-        """[split*B*H_kv][8] %globaltimer ns checkpoints of the last decode_attention (KVTIER_TRACE=1)."""
-        n = self.cfg.num_layers * self.cfg.num_requests * self.cfg.num_kv_heads * 8 * max(1, self._split())
+        """[L][split*B*H_kv][16] %globaltimer ns checkpoints of the last step (KVTIER_TRACE=1)."""
+        n = self.cfg.num_layers * self.cfg.num_requests * self.cfg.num_kv_heads * 16 * max(1, self._split())
         buf = np.zeros(n, dtype=np.uint64)
         _check(load().kv_tier_debug_trace(self.ctx, buf.ctypes.data_as(C.c_void_p), n), self.ctx)
-        return buf.reshape(self.cfg.num_layers, -1, 8)
+        return buf.reshape(self.cfg.num_layers, -1, 16)
 
     def _split(self):
         if self.cfg.split:

@@ -39,6 +39,10 @@ for l in (0, 1, 2, tr.shape[0] // 2, tr.shape[0] - 1):
         col = col[tr[l, :, i] > 0]          # merge checkpoints exist only on the last CTA of a unit
         d[n] = [round(float(col.min()), 2), round(float(np.median(col)), 2), round(float(col.max()), 2)] if col.size else None
     out[f"L{l}"] = d
+    for i, n in ((8, "cons_wait_us"), (9, "cons_busy_us"), (10, "stages"), (11, "prod_empty_wait_us"), (13, "first_stage_busy_us")):
+        col = tr[l, :, i].astype(np.float64) / (1.0 if i == 10 else 1e3)
+        d[n] = [round(float(col.min()), 2), round(float(np.median(col)), 2), round(float(col.max()), 2)]
+    d["prod_done"] = [round(float(x), 2) for x in np.percentile(rel[l, :, 12], [0, 50, 100])]
 ends = [float(rel[l, :, 7].max()) for l in range(tr.shape[0])]
 out["layer_end_deltas_us"] = [round(ends[l] - ends[l - 1], 2) for l in range(1, len(ends))]
 print(json.dumps(out))

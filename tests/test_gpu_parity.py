@@ -310,3 +310,12 @@ def test_cluster_merge_equals_merge_kernel_bitwise(monkeypatch):
         run.close()
     assert np.array_equal(outs[0], outs[1])
     assert np.array_equal(scores[0], scores[1])
+
+
+def test_contiguous_stage_ranges(monkeypatch):   # KVTIER_RR=0: contiguous stage ranges per CTA
+    monkeypatch.setenv("KVTIER_RR", "0")
+    w = H.workload("tiny", B=3, L=2, Hq=12, Hkv=2, d=128, N=700, P=40, interval=16, steps=34,
+                   hbm_bp=3000, evict_bp=1000, t2_bp=2500)
+    _run_pair(w, graph=True, check_every=5, split=3)
+    monkeypatch.setenv("KVTIER_CLUSTER", "1")
+    _run_pair(w, graph=True, check_every=5, split=5)
