@@ -63,6 +63,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
 }
+// L2 prefetch of a contiguous byte range (no shared-memory destination)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 // streamed K/V rows are read once per layer: evict them first so the hot data stays in L2
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
@@ -115,6 +119,13 @@ __device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uin
       "{%0,%1,%2,%3};\n"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// 2^x on the SFU without the subnormal range fix-up exp2f adds (results below 2^-126 flush to
+// 0: p of a token 126 log2 units under the running max is below fp32 resolution of l anyway)
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 __device__ __forceinline__ uint32_t movm_t(uint32_t x) {
   uint32_t y;
@@ -328,21 +339,58 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     // streams this CTA's stages (static ranges: the fp32 summation order never depends on timing)
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
+#if KVT_TRACE_LOOP
+      unsigned long long pwait = 0;
+#endif
       for (int i = 0;; ++i) {
         const int s2 = i % NST;
-        if (i == v.pdl_pre) pdl_wait();   // at most pdl_pre stages in flight before the previous layer ends
+        if (i == v.pdl_pre) {
+          // Before blocking on the previous kernel: this CTA's remaining stages go to L2 now, so
+          // HBM streams them during the previous layer's tail instead of idling (K/V rows do
+          // not depend on the previous kernel; only their consumption does).
+          if (v.l2_prefetch) {
+            for (int j = i; j < nstage; ++j) {
+              bool pt2;
+              int pg0, png;
+              stage_at(j, pt2, pg0, png);
+              const int nrows = 16 * png;
+              if (!pt2) {
+                const int ts = 16 * pg0;
+                if (ts < sg.a1) {
+                  const int n0r = min(nrows, sg.a1 - ts);
+                  bulk_prefetch_l2(K0 + (size_t)ts * D, n0r * ROWB);
+                  bulk_prefetch_l2(V0 + (size_t)ts * D, n0r * ROWB);
+                  if (n0r < nrows) {
+                    bulk_prefetch_l2(K1, (nrows - n0r) * ROWB);
+                    bulk_prefetch_l2(V1, (nrows - n0r) * ROWB);
+                  }
+                } else {
+                  bulk_prefetch_l2(K1 + (size_t)(ts - sg.a1) * D, nrows * ROWB);
+                  bulk_prefetch_l2(V1 + (size_t)(ts - sg.a1) * D, nrows * ROWB);
+                }
+              } else {
+                const size_t j0 = 16 * (size_t)pg0;
+                bulk_prefetch_l2(v.c2k[sb] + (grp * v.cap2 + j0) * D, nrows * D);
+                bulk_prefetch_l2(v.c2v[sb] + (grp * v.cap2 + j0) * D, nrows * D);
+              }
+            }
+          }
+          pdl_wait();   // at most pdl_pre stages in flight before the previous layer ends
+        }
         if (i >= NST) {
 #if KVT_TRACE_LOOP
-          const unsigned long long tw = tr ? gtimer() : 0;
+          const unsigned long long tw = gtimer();
           mbar_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
-          if (tr) tr[11] += gtimer() - tw;
+          pwait += gtimer() - tw;
 #else
           mbar_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
 #endif
         }
         const uint32_t full = full0 + 8 * s2, dst = ring_s + s2 * STAGEB;
         if (i >= nstage) {
-          if (tr) tr[12] = gtimer();
+#if KVT_TRACE_LOOP
+          if (tr) { tr[12] = gtimer(); tr[11] = pwait; }
+#endif
           stile[s2] = -1;
           mbar_arrive(full);          // sentinel stage (no data)
           break;
@@ -524,7 +572,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
         tb = fmaxf(tb, __shfl_xor_sync(0xffffffffu, tb, off));
       }
       const float na = fmaxf(mxa, ta), nb = fmaxf(mxb, tb);     // finite: some row is valid
-      const float ca = exp2f(mxa - na), cb = exp2f(mxb - nb);   // 0 when the old max is -inf
+      const float ca = ex2_ftz(mxa - na), cb = ex2_ftz(mxb - nb);   // 0 when the old max is -inf
       mxa = na;
       mxb = nb;
 #pragma unroll
@@ -537,27 +585,35 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       la *= ca;
       lb *= cb;
     }
-    p00 = exp2f(z00 - mxa);
-    p01 = exp2f(z01 - mxb);
-    p10 = exp2f(z10 - mxa);
-    p11 = exp2f(z11 - mxb);
+    p00 = ex2_ftz(z00 - mxa);
+    p01 = ex2_ftz(z01 - mxb);
+    p10 = ex2_ftz(z10 - mxa);
+    p11 = ex2_ftz(z11 - mxb);
     la += p00 + p10;
     lb += p01 + p11;
   };
   const int mi = lane >> 3, ii = lane & 7;
+  // K slice . q^T: KS independent-ish MMAs in NCH accumulator chains (short dependency depth:
+  // the per-stage critical path is latency, not tensor throughput)
   auto qk = [&](uint32_t sK, int rowbase, float* acc) {
-    float acc2[4] = {0.f, 0.f, 0.f, 0.f};
+    constexpr int NCH = KS >= 4 ? 4 : KS;
+    float ch[NCH][4];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) ch[c][0] = ch[c][1] = ch[c][2] = ch[c][3] = 0.f;
     const int row = rowbase + ii + ((mi & 1) << 3);
 #pragma unroll
-    for (int ks = 0; ks < KS; ks += 2) {
+    for (int ks = 0; ks < KS; ++ks) {
       uint32_t a0, a1_, a2_, a3_;
       ldsm_x4(a0, a1_, a2_, a3_, sK + row * ROWB + (((2 * ks + (mi >> 1)) ^ (row & 7)) << 4));
-      mma16816(acc, a0, a1_, a2_, a3_, qf[ks][0], qf[ks][1]);
-      ldsm_x4(a0, a1_, a2_, a3_, sK + row * ROWB + (((2 * ks + 2 + (mi >> 1)) ^ (row & 7)) << 4));
-      mma16816(acc2, a0, a1_, a2_, a3_, qf[ks + 1][0], qf[ks + 1][1]);
+      mma16816(ch[ks % NCH], a0, a1_, a2_, a3_, qf[ks][0], qf[ks][1]);
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j] += acc2[j];
+    for (int j = 0; j < 4; ++j) {
+      float x = ch[0][j];
+#pragma unroll
+      for (int c = 1; c < NCH; ++c) x += ch[c][j];
+      acc[j] += x;
+    }
   };
   auto pv = [&](uint32_t sV, int rowbase, float p00, float p01, float p10, float p11) {
     const uint32_t b0 = movm_t(pack_bf16(p00, p01));
@@ -587,16 +643,18 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   };
 
 #if KVT_TRACE_LOOP
-  unsigned long long tprev = 0;
+  unsigned long long tprev = 0, acc_wait = 0, acc_busy = 0, first_busy = 0, nst_seen = 0;
 #endif
   for (int i = 0;; ++i) {
     const int s2 = i % NST;
 #if KVT_TRACE_LOOP   // per-stage wait / busy accounting (debug builds: -DKVT_TRACE_LOOP=1)
-    const unsigned long long tw = (tr && tid == 0) ? gtimer() : 0;
-    if (tr && tid == 0 && i > 0) tr[9] += tw - tprev;
-    if (tr && tid == 0 && i == 1) tr[13] = tw - tprev;       // first stage (includes the q load)
+    const unsigned long long tw = gtimer();                   // registers only in the loop
+    if (i > 0) acc_busy += tw - tprev;
+    if (i == 1) first_busy = tw - tprev;                      // first stage (includes the q load)
     mbar_wait(full0 + 8 * s2, (i / NST) & 1);
-    if (tr && tid == 0) { tprev = gtimer(); tr[8] += tprev - tw; tr[10] += 1; }
+    tprev = gtimer();
+    acc_wait += tprev - tw;
+    nst_seen += 1;
 #else
     mbar_wait(full0 + 8 * s2, (i / NST) & 1);
 #endif
@@ -648,6 +706,9 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     if (lane == 0) mbar_arrive(empty0 + 8 * s2);
   }
   if (tr && tid == 0) tr[3] = gtimer();
+#if KVT_TRACE_LOOP
+  if (tr && tid == 0) { tr[8] = acc_wait; tr[9] = acc_busy; tr[10] = nst_seen; tr[13] = first_busy; }
+#endif
 
   // ---- warps -> CTA partial (ring reused as [NW][8][D+4] fp32)
 #pragma unroll

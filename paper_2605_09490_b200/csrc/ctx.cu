@@ -258,6 +258,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.variant = cfg->variant;
   v.pdl_pre = getenv("KVTIER_PDL_PRE") ? atoi(getenv("KVTIER_PDL_PRE")) : 1 << 30;
   v.use_pdl = getenv("KVTIER_NOPDL") ? 0 : 1;
+  v.l2_prefetch = getenv("KVTIER_L2PF") ? atoi(getenv("KVTIER_L2PF")) : 0;   // measured: no gain at 7B
   v.stage_rr = getenv("KVTIER_RR") ? atoi(getenv("KVTIER_RR")) : 1;
   v.cluster_merge = (getenv("KVTIER_CLUSTER") && atoi(getenv("KVTIER_CLUSTER")) && v.split <= 8) ? 1 : 0;
   v.chunk_max = 0;
@@ -498,6 +499,7 @@ static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, con
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
   if (ctx->v.stream_mode) e = cudaStreamWaitEvent(s, ctx->ev_prefetched[layer], 0);
+  if (getenv("KVTIER_NOSCORE")) fuse_score_update = 0;   // experiment hook: attention without a4
   if (ctx->v.cluster_merge) {   // a4 fused into the kernel's epilogue (one logits slot, no score stream)
     const int zp = fuse_score_update ? 0 : -1;
     if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, zp, pdl, s);

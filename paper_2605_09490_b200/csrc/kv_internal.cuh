@@ -38,6 +38,7 @@ struct DevView {
   int variant;          // decode-attention kernel variant (warps x pipeline stages)
   int pdl_pre;          // stages the producer may load before griddepcontrol.wait
   int use_pdl;          // chain consecutive layers with programmatic dependent launch
+  int l2_prefetch;      // pre-wait L2 prefetch of the CTA's stages beyond the shared-memory ring
   int stage_rr;         // stages dealt round-robin to the unit's CTAs (else contiguous ranges)
   int cluster_merge;    // merge the unit's partials in distributed shared memory (cluster of split CTAs)
   unsigned long long* trace;   // debug: per-CTA %globaltimer checkpoints (null = off)
