@@ -60,8 +60,16 @@ typedef enum {
  * PER_EVENT: literal Alg. 1, n_evict = floor(r * |U|) at every event. */
 typedef enum { KV_TIER_EVICT_TOTAL = 0, KV_TIER_EVICT_PER_EVENT = 1 } kv_tier_evict_mode;
 
-/* Multi-GPU partitioning.  REQUEST: each rank owns B requests (no
- * collective in the step).  KVHEAD / SEQUENCE are reserved for later rounds. */
+/* Multi-GPU partitioning.  The library itself runs no collective; the caller
+ * (paper_2605_09490_b200/dist.py, torch.distributed over NCCL) moves the bytes.
+ *   REQUEST  each rank owns B requests; no collective anywhere on the path.
+ *   KVHEAD   each rank owns H_kv / world kv heads (num_q_heads / num_kv_heads in the config
+ *            are the rank's LOCAL counts; its global kv heads are rank*H_kv .. +H_kv-1).
+ *            The step is local.  Tiers are per token across all heads (AMB-3, Alg. 1),
+ *            so at an event every rank all-gathers S_part (kv_tier_scores_device) and calls
+ *            kv_tier_classify_gathered: identical S -> identical tiers on every rank, summed
+ *            in ascending global head order exactly as unsharded (bit-exact).
+ *   SEQUENCE reserved. */
 typedef enum { KV_TIER_SHARD_REQUEST = 0, KV_TIER_SHARD_KVHEAD = 1, KV_TIER_SHARD_SEQUENCE = 2 } kv_tier_shard;
 
 #define KV_TIER_STAGING_ALL 0xFFFFFFFFu   /* differential mode: staging holds all of T1 (§3.4) */
@@ -175,7 +183,8 @@ KV_TIER_API kv_tier_status kv_tier_step_graph_launch(kv_tier_ctx* ctx, void* str
 /* a5: per request, protected set P = [0,P) u [P,P+k_s) u [n-k_w,n); the live
  * non-protected tokens ordered by the unique key (fp32 bits of S_i, i) ascending
  * (AMB-7); n_new = bottom -> T3 (AMB-8/9), top floor(beta|surv|) -> T0, lowest
- * floor(f2 * rest) -> T2, remainder -> T1 (Alg. 1).  Idempotent until migrate. */
+ * floor(f2 * rest) -> T2, remainder -> T1 (Alg. 1).  Idempotent until migrate.
+ * E_STATE under KV-head sharding with world > 1 (use kv_tier_classify_gathered). */
 KV_TIER_API kv_tier_status kv_tier_classify(kv_tier_ctx* ctx, void* stream);
 
 /* a6: apply the transitions of the last classify: T0<->T1 copies, ->T2 int8
@@ -212,6 +221,18 @@ KV_TIER_API kv_tier_status kv_tier_export_size(kv_tier_ctx* ctx, int32_t what, s
 KV_TIER_API kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, void* host_dst, size_t bytes);
 /* Overwrite S_part with host fp32 [B][H_kv][n] (classify cross-feed, AMB-18). Synchronises. */
 KV_TIER_API kv_tier_status kv_tier_import_scores(kv_tier_ctx* ctx, const float* host_S, size_t bytes);
+
+/* Device pointer and size of this ctx's per-kv-head partial scores S_part [B][H_kv][N_max]
+ * fp32 (owned by the ctx; valid until kv_tier_destroy).  For the caller's collectives. */
+KV_TIER_API kv_tier_status kv_tier_scores_device(kv_tier_ctx* ctx, void** ptr, size_t* bytes);
+
+/* a5 from gathered scores (KV-head sharding): S_all is device memory
+ * [parts][B][H_kv][N_max] fp32 -- the all-gather over ranks of every rank's S_part, rank
+ * order = global kv head order.  S_i = fp32 sum over the parts*H_kv heads in ascending
+ * global order (AMB-1/14), then the same selection as kv_tier_classify.  S_all must stay
+ * valid until the classify has run on `stream`.  E_INVAL on a null/misaligned pointer. */
+KV_TIER_API kv_tier_status kv_tier_classify_gathered(kv_tier_ctx* ctx, const float* S_all, int32_t parts,
+                                                     void* stream);
 
 /* Debug: %globaltimer checkpoints [L][B*H_kv][split][16] of the last launch of every layer:
  * 16 slots per CTA: (start, after PDL wait, first stage, loop done, partial written, merge

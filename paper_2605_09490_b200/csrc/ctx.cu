@@ -98,7 +98,9 @@ kv_tier_status validate(const kv_tier_config* c) {
   if (c->evict_mode != 0 && c->evict_mode != 1) return fail(nullptr, KV_TIER_E_INVAL, "bad evict_mode");
   if (c->staging_tokens != 0 && c->staging_tokens != KV_TIER_STAGING_ALL)
     return fail(nullptr, KV_TIER_E_INVAL, "staging_tokens must be 0 (stream) or KV_TIER_STAGING_ALL (differential)");
-  if (c->shard != KV_TIER_SHARD_REQUEST) return fail(nullptr, KV_TIER_E_INVAL, "only request sharding is implemented");
+  if (c->shard != KV_TIER_SHARD_REQUEST && c->shard != KV_TIER_SHARD_KVHEAD)
+    return fail(nullptr, KV_TIER_E_INVAL, "shard must be REQUEST or KVHEAD");
+  if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(nullptr, KV_TIER_E_INVAL, "need 0 <= rank < world");
   if (c->split < 0 || c->split > 64) return fail(nullptr, KV_TIER_E_INVAL, "split must be in [0, 64]");
   if (c->variant < 0 || c->variant > 5) return fail(nullptr, KV_TIER_E_INVAL, "variant must be in [0, 5]");
   return KV_TIER_OK;
@@ -234,7 +236,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   kv_tier_status st = validate(cfg);
   if (st != KV_TIER_OK) return st;
   if (!buf || !buf->device_arena || !out) return fail(nullptr, KV_TIER_E_INVAL, "null buffers/out");
-  if (nccl_unique_id) return fail(nullptr, KV_TIER_E_INVAL, "request sharding has no collective: pass NULL");
+  if (nccl_unique_id) return fail(nullptr, KV_TIER_E_INVAL, "the library runs no collective (the caller does): pass NULL");
   if (((uintptr_t)buf->device_arena) & 255) return fail(nullptr, KV_TIER_E_INVAL, "device_arena must be 256-B aligned");
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e != cudaSuccess) return fail(nullptr, KV_TIER_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
@@ -570,8 +572,30 @@ kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream) {
   return KV_TIER_OK;
 }
 
+static kv_tier_status classify_impl(kv_tier_ctx* ctx, const float* Sx, int parts, void* stream);
+
 kv_tier_status kv_tier_classify(kv_tier_ctx* ctx, void* stream) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (ctx->cfg.shard == KV_TIER_SHARD_KVHEAD && ctx->cfg.world > 1)
+    return fail(ctx, KV_TIER_E_STATE, "KV-head sharding: classify needs every shard's scores (kv_tier_classify_gathered)");
+  return classify_impl(ctx, nullptr, 1, stream);
+}
+
+kv_tier_status kv_tier_classify_gathered(kv_tier_ctx* ctx, const float* S_all, int32_t parts, void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!S_all || parts < 1) return fail(ctx, KV_TIER_E_INVAL, "S_all must be a device pointer and parts >= 1");
+  if (((uintptr_t)S_all) & 3) return fail(ctx, KV_TIER_E_INVAL, "S_all must be 4-B aligned");
+  return classify_impl(ctx, S_all, parts, stream);
+}
+
+kv_tier_status kv_tier_scores_device(kv_tier_ctx* ctx, void** ptr, size_t* bytes) {
+  if (!ctx || !ptr || !bytes) return fail(ctx, KV_TIER_E_INVAL, "null arg");
+  *ptr = ctx->v.S;
+  *bytes = (size_t)ctx->v.B * ctx->v.Hkv * ctx->v.Nmax * sizeof(float);
+  return KV_TIER_OK;
+}
+
+static kv_tier_status classify_impl(kv_tier_ctx* ctx, const float* Sx, int parts, void* stream) {
   if (!ctx->loaded) return fail(ctx, KV_TIER_E_STATE, "no prefix loaded");
   if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "classify inside a step (call after the last layer's score update)");
   const kv_tier_config& c = ctx->cfg;
@@ -589,7 +613,7 @@ kv_tier_status kv_tier_classify(kv_tier_ctx* ctx, void* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
   if (ctx->offload_pending) e = cudaStreamWaitEvent(s, ctx->ev_offload_done, 0);
-  if (e == cudaSuccess) e = launch_classify(ctx->v, s);
+  if (e == cudaSuccess) e = launch_classify(ctx->v, Sx, parts, s);
   kv_tier_status st = cuda_check(ctx, e, "classify");
   if (st) return st;
   ctx->pend[0] = p0; ctx->pend[1] = p1; ctx->pend[2] = p2; ctx->pend[3] = p3;

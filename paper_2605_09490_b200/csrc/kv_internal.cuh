@@ -105,7 +105,7 @@ cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const
 cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_t s);
 cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s);
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);
-cudaError_t launch_classify(const DevView& v, cudaStream_t s);
+cudaError_t launch_classify(const DevView& v, const float* Sx, int parts, cudaStream_t s);
 cudaError_t launch_migrate(const DevView& v, int cur, cudaStream_t s);
 cudaError_t launch_plan(const DevView& v, cudaStream_t s);
 cudaError_t launch_moves(const DevView& v, int cur, cudaStream_t s);

@@ -123,7 +123,9 @@ __global__ void k_score_update(const DevView v, const float* __restrict__ probs)
 // ranks, found by an 8-pass MSB radix select (histograms in shared memory).
 constexpr int CLS_THREADS = 1024;
 
-__global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v) {
+// Sx: per-kv-head partial scores [parts][B][H_kv][N_max] -- the ctx's own S_part (parts = 1)
+// or the all-gathered S_part of `parts` KV-head shards (global kv head = part * H_kv + g).
+__global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const float* __restrict__ Sx, const int parts) {
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int cur = v.st->cur, nxt = cur ^ 1, n = v.st->n;
   const uint8_t* told = v.tier[cur] + (size_t)b * v.Nmax;
@@ -146,8 +148,11 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v) {
   int c_live = 0, c_t3 = 0;
   bool bad = false;
   for (int pos = tid; pos < n; pos += CLS_THREADS) {
-    float s = v.S[((size_t)b * v.Hkv) * v.Nmax + pos];
-    for (int g = 1; g < v.Hkv; ++g) s = __fadd_rn(s, v.S[((size_t)b * v.Hkv + g) * v.Nmax + pos]);
+    float s = Sx[((size_t)b * v.Hkv) * v.Nmax + pos];
+    for (int gg = 1; gg < parts * v.Hkv; ++gg) {     // ascending global kv head
+      const int part = gg / v.Hkv, g = gg - part * v.Hkv;
+      s = __fadd_rn(s, Sx[(((size_t)part * v.B + b) * v.Hkv + g) * v.Nmax + pos]);
+    }
     fS[pos] = s;
     bad |= !(s >= 0.f) || isinf(s);
     if (told[pos] == T3) ++c_t3;
@@ -747,8 +752,8 @@ cudaError_t launch_score_update(const DevView& v, int layer, const float* probs,
   k_score_update<<<grid, 256, 0, s>>>(v, probs);
   return cudaGetLastError();
 }
-cudaError_t launch_classify(const DevView& v, cudaStream_t s) {
-  k_classify<<<v.B, CLS_THREADS, 0, s>>>(v);
+cudaError_t launch_classify(const DevView& v, const float* Sx, int parts, cudaStream_t s) {
+  k_classify<<<v.B, CLS_THREADS, 0, s>>>(v, Sx ? Sx : v.S, Sx ? parts : 1);
   return cudaGetLastError();
 }
 cudaError_t launch_migrate(const DevView& v, int cur, cudaStream_t s) {

@@ -1,6 +1,12 @@
-"""Multi-GPU plumbing for request sharding: one process per GPU,
-each rank owns its own batch of B requests (global request ids rank*B + b, seeds offset
-per rank), no collective inside the decode step; timing is the max over ranks."""
+"""Multi-GPU plumbing: one process per GPU, torch.distributed for the bytes.
+
+* Request sharding (row 1): every rank owns its own batch of B requests (global request
+  ids rank*B + b, seeds offset per rank); no collective inside the decode step.
+* KV-head sharding (row 2): rank r owns kv heads [r*H_l, (r+1)*H_l) and their q heads;
+  the step is local; at a manage event the ranks all-gather S_part (B*H_kv*N_max fp32 in
+  total) and each classifies the identical gathered scores (kv_tier_classify_gathered),
+  so tiers agree bit-for-bit across ranks and with the unsharded run.
+Timing is the max over ranks."""
 from __future__ import annotations
 
 import os
@@ -50,3 +56,43 @@ def barrier_sync():
         dist.barrier()
     if torch.cuda.is_available():
         torch.cuda.synchronize()
+
+
+def kvhead_plan(world, rank, Hq, Hkv):
+    """KV-head sharding: (first kv head, kv heads, first q head, q heads) of `rank`."""
+    if not (0 <= rank < world) or Hkv % world or Hq % Hkv:
+        raise ValueError("H_kv must divide evenly over the ranks and H_q over H_kv")
+    hl = Hkv // world
+    G = Hq // Hkv
+    return rank * hl, hl, rank * hl * G, hl * G
+
+
+def gather_scores(S_local, group=None):
+    """All-gather every rank's S_part [B][H_l][N] into [world][B][H_l][N] (rank order =
+    global kv head order).  Works on CUDA (NCCL) and CPU (gloo) tensors."""
+    world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+    x = S_local.contiguous()
+    if world == 1:
+        return x.unsqueeze(0)
+    out = torch.empty((world,) + tuple(x.shape), dtype=x.dtype, device=x.device)
+    if x.is_cuda:
+        dist.all_gather_into_tensor(out, x, group=group)
+    else:
+        dist.all_gather(list(out.unbind(0)), x, group=group)
+    return out
+
+
+def kvhead_classify(kv, stream=None, group=None):
+    """a5 under KV-head sharding: all-gather S_part, then classify the gathered scores."""
+    with torch.cuda.stream(stream) if stream is not None else _null():
+        S_all = gather_scores(kv.scores_tensor(), group)
+        kv.classify_gathered(S_all, S_all.shape[0], stream=stream)
+    return S_all
+
+
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False

@@ -29,24 +29,36 @@ class TieredDecode:
     The chain holds n0 = N - 1 prefix tokens; step 0 appends position N - 1, so the
     first manage event (t = 0) sees exactly N tokens (reading AMB-22)."""
 
-    def __init__(self, w, device="cuda:0", out_fp32=True, split=0, seed_offset=0, keep_inputs=False, variant=0):
+    def __init__(self, w, device="cuda:0", out_fp32=True, split=0, seed_offset=0, keep_inputs=False, variant=0,
+                 heads=None, classify_fn=None, shard=kt.SHARD_REQUEST, rank=0, world=1):
+        """heads = (first kv head, count): this ctx holds only those kv heads and their q
+        heads (KV-head sharding); classify_fn(run, stream) replaces kv.classify at events
+        (e.g. dist.kvhead_classify, or a single-process gather over several ctxs)."""
         self.w = w
         self.dev = torch.device(device)
         torch.cuda.set_device(self.dev)
         B, L, Hq, Hkv, d, N, P, T = (w[k] for k in ("B", "L", "Hq", "Hkv", "d", "N", "P", "steps"))
+        G = Hq // Hkv
+        h0, hl = heads if heads is not None else (0, Hkv)
+        self.heads = (h0, hl)
+        self.classify_fn = classify_fn
         self.seed = w["seed"] + seed_offset
         self.n0 = N - 1
         self.T = T
-        self.cfg = kt.make_config(B, L, Hq, Hkv, d, self.n0 + T, P, hbm_bp=w["hbm_bp"], evict_bp=w["evict_bp"],
+        self.cfg = kt.make_config(B, L, hl * G, hl, d, self.n0 + T, P, hbm_bp=w["hbm_bp"], evict_bp=w["evict_bp"],
                                   t2_bp=w["t2_bp"], manage_interval=w["interval"], evict_mode=w["evict_mode"],
                                   staging=w["staging"], device=self.dev.index or 0, out_fp32=int(out_fp32),
-                                  split=split, variant=variant)
+                                  split=split, variant=variant, shard=shard, rank=rank, world=world)
+        hs = slice(h0, h0 + hl)
+        qs = slice(h0 * G, (h0 + hl) * G)
         self.kv = kt.KvTier(self.cfg)
         self.main = torch.cuda.Stream(self.dev)
         self.side = torch.cuda.Stream(self.dev)
         with torch.cuda.stream(self.main):
             K = SG.gen_kv(self.seed, "k", L, B, Hkv, d, 0, self.n0, P, S.SINK_SIZE, self.dev, stream=self.main)
             V = SG.gen_kv(self.seed, "v", L, B, Hkv, d, 0, self.n0, P, S.SINK_SIZE, self.dev, stream=self.main)
+            if heads is not None:
+                K, V = K[:, :, hs].contiguous(), V[:, :, hs].contiguous()
             for l in range(L):
                 self.kv.load_prefix(l, K[l], V[l], self.n0, stream=self.main)
             self.main.synchronize()
@@ -56,12 +68,12 @@ class TieredDecode:
             kn = SG.gen_kv(self.seed, "k", L, B, Hkv, d, self.n0, T, P, S.SINK_SIZE, self.dev, stream=self.main)
             vn = SG.gen_kv(self.seed, "v", L, B, Hkv, d, self.n0, T, P, S.SINK_SIZE, self.dev, stream=self.main)
             # [L][B][Hkv][T][d] -> [T][L][B][Hkv][d] (per-step append rows)
-            self.Kn = kn.permute(3, 0, 1, 2, 4).contiguous()
-            self.Vn = vn.permute(3, 0, 1, 2, 4).contiguous()
+            self.Kn = kn[:, :, hs].permute(3, 0, 1, 2, 4).contiguous()
+            self.Vn = vn[:, :, hs].permute(3, 0, 1, 2, 4).contiguous()
             del kn, vn
-            self.Q = SG.gen_q(self.seed, 0, T, L, B, Hq, Hkv, d, self.dev, stream=self.main)
+            self.Q = SG.gen_q(self.seed, 0, T, L, B, Hq, Hkv, d, self.dev, stream=self.main)[:, :, :, qs].contiguous()
             odt = torch.float32 if out_fp32 else torch.bfloat16
-            self.O = torch.empty((L, B, Hq, d), dtype=odt, device=self.dev)
+            self.O = torch.empty((L, B, hl * G, d), dtype=odt, device=self.dev)
             # fixed buffers for the captured step graph
             self.qbuf = torch.empty_like(self.Q[0])
             self.kbuf = torch.empty_like(self.Kn[0])
@@ -84,9 +96,9 @@ class TieredDecode:
         self.main.synchronize()
         return self.O.cpu().numpy()
 
-    def step(self):
-        """One decode step t (+ manage event when t mod Delta == 0).  Asynchronous on
-        self.main: read results through output()."""
+    def step(self, manage=True):
+        """One decode step t (+ manage event when t mod Delta == 0 unless manage=False).
+        Asynchronous on self.main: read results through output()."""
         t = self.t
         with torch.cuda.stream(self.main):
             if self.graph:
@@ -96,11 +108,17 @@ class TieredDecode:
                 self.kv.step_graph_launch(stream=self.main)
             else:
                 self.kv.step(self.Q[t], self.Kn[t], self.Vn[t], self.O, 1, stream=self.main, side=self.side)
-            if self.is_event(t):
-                self.kv.classify(stream=self.main)
+            if manage and self.is_event(t):
+                self.classify()
                 self.kv.migrate(stream=self.main, side=self.side)
         self.t += 1
         return self.O
+
+    def classify(self):
+        if self.classify_fn is not None:
+            self.classify_fn(self, self.main)
+        else:
+            self.kv.classify(stream=self.main)
 
     def step_layers(self):
         """Same step through the per-layer ABI calls (append / prefetch / decode_attention)."""
@@ -119,7 +137,7 @@ class TieredDecode:
                     self.kv.prefetch(l + 2, side=self.side)
             self.kv.end_step(stream=self.main)
             if self.is_event(t):
-                self.kv.classify(stream=self.main)
+                self.classify()
                 self.kv.migrate(stream=self.main, side=self.side)
         self.t += 1
         return self.O
@@ -132,3 +150,66 @@ class TieredDecode:
     def close(self):
         self.sync()
         self.kv.close()
+
+
+class KvHeadShardedDecode:
+    """KV-head sharding simulated in one process: `world` ctxs on one
+    device, ctx r holding kv heads [r*H_l, (r+1)*H_l).  At an event the ctxs' S_part are
+    gathered in rank order (the bytes an NCCL all-gather moves) and every ctx classifies the
+    same gathered scores.  Outputs are concatenated over q heads."""
+
+    def __init__(self, w, world, device="cuda:0", **kw):
+        Hkv = w["Hkv"]
+        assert Hkv % world == 0
+        hl = Hkv // world
+        self.world = world
+        self.runs = []
+        for r in range(world):
+            self.runs.append(TieredDecode(w, device=device, heads=(r * hl, hl), shard=kt.SHARD_KVHEAD,
+                                          rank=r, world=world, **kw))
+        self.w = w
+
+    def is_event(self, t):
+        return t % self.w["interval"] == 0
+
+    @property
+    def t(self):
+        return self.runs[0].t
+
+    def capture(self):
+        for r in self.runs:
+            r.capture()
+
+    def step(self):
+        t = self.t
+        for r in self.runs:
+            r.step(manage=False)
+        if self.is_event(t):
+            for r in self.runs:
+                r.main.synchronize()
+            gathered = torch.stack([r.kv.scores_tensor() for r in self.runs]).contiguous()   # the all-gather
+            torch.cuda.current_stream(self.runs[0].dev).synchronize()
+            for r in self.runs:
+                with torch.cuda.stream(r.main):
+                    r.kv.classify_gathered(gathered, self.world, stream=r.main)
+                    r.kv.migrate(stream=r.main, side=r.side)
+            for r in self.runs:
+                r.main.synchronize()
+
+    def output(self):
+        import numpy as np
+        return np.concatenate([r.output() for r in self.runs], axis=2)
+
+    def scores(self):
+        import numpy as np
+        for r in self.runs:
+            r.sync()
+        return np.concatenate([r.kv.export(kt.X_SCORES) for r in self.runs], axis=1)
+
+    def sync(self):
+        for r in self.runs:
+            r.sync()
+
+    def close(self):
+        for r in self.runs:
+            r.close()

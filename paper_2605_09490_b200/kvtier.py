@@ -18,6 +18,7 @@ KV_TIER_OK = 0
 STATUS = {0: "OK", -1: "E_INVAL", -2: "E_CUDA", -3: "E_NCCL", -4: "E_STATE", -5: "E_CAPACITY",
           -6: "E_OOM", -7: "E_NUMERIC"}
 EVICT_TOTAL, EVICT_PER_EVENT = 0, 1
+SHARD_REQUEST, SHARD_KVHEAD, SHARD_SEQUENCE = 0, 1, 2
 STAGING_ALL = 0xFFFFFFFF
 X_SCORES, X_TIERS, X_IDX_T0, X_IDX_T1, X_IDX_T2, X_T0_ROWS, X_T1_ROWS, X_STAGING, X_T2_CODES, X_T2_SCALES = range(10)
 
@@ -66,6 +67,8 @@ _SIGS = {
     "kv_tier_step_graph_capture": [C.c_void_p] + [C.c_void_p] * 4 + [C.c_int32, C.c_void_p, C.c_void_p],
     "kv_tier_step_graph_launch": [C.c_void_p, C.c_void_p],
     "kv_tier_classify": [C.c_void_p, C.c_void_p],
+    "kv_tier_classify_gathered": [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p],
+    "kv_tier_scores_device": [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)],
     "kv_tier_migrate": [C.c_void_p, C.c_void_p, C.c_void_p],
     "kv_tier_sync": [C.c_void_p],
     "kv_tier_census": [C.c_void_p, C.c_void_p, C.c_void_p],
@@ -117,12 +120,13 @@ def _stream_ptr(stream):
 
 def make_config(B, L, Hq, Hkv, d, max_tokens, prompt_len, hbm_bp=5000, evict_bp=500, t2_bp=0,
                 sink_size=4, window_size=128, manage_interval=64, evict_mode=EVICT_TOTAL,
-                staging=STAGING_ALL, device=0, out_fp32=1, split=0, rank=0, world=1, variant=0):
+                staging=STAGING_ALL, device=0, out_fp32=1, split=0, rank=0, world=1, variant=0,
+                shard=0):
     return Config(num_requests=B, num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=d,
                   max_tokens=max_tokens, prompt_len=prompt_len, sink_size=sink_size,
                   window_size=window_size, manage_interval=manage_interval, hbm_ratio_bp=hbm_bp,
                   evict_ratio_bp=evict_bp, t2_fraction_bp=t2_bp, evict_mode=evict_mode,
-                  staging_tokens=staging, device=device, rank=rank, world=world, shard=0,
+                  staging_tokens=staging, device=device, rank=rank, world=world, shard=shard,
                   out_fp32=out_fp32, split=split, variant=variant)
 
 
@@ -204,6 +208,22 @@ class KvTier:
 
     def classify(self, stream=None):
         _check(load().kv_tier_classify(self.ctx, _stream_ptr(stream)), self.ctx)
+
+    def classify_gathered(self, S_all, parts, stream=None):
+        """a5 from all-gathered scores: S_all is a contiguous fp32 CUDA tensor
+        [parts][B][H_kv][N_max] (KV-head sharding, rank order = global head order)."""
+        assert S_all.is_cuda and S_all.dtype.itemsize == 4 and S_all.is_contiguous()
+        _check(load().kv_tier_classify_gathered(self.ctx, C.c_void_p(S_all.data_ptr()), parts, _stream_ptr(stream)),
+               self.ctx)
+
+    def scores_tensor(self):
+        """Zero-copy torch view [B][H_kv][N_max] fp32 of this ctx's S_part (inside the arena)."""
+        ptr, nbytes = C.c_void_p(), C.c_size_t()
+        _check(load().kv_tier_scores_device(self.ctx, C.byref(ptr), C.byref(nbytes)), self.ctx)
+        off = ptr.value - self.arena.data_ptr()
+        assert 0 <= off and off + nbytes.value <= self.arena.numel()
+        B, H = self.cfg.num_requests, self.cfg.num_kv_heads
+        return self.arena[off:off + nbytes.value].view(dtype=__import__("torch").float32).view(B, H, -1)
 
     def migrate(self, stream=None, side=None):
         _check(load().kv_tier_migrate(self.ctx, _stream_ptr(stream), _stream_ptr(side)), self.ctx)

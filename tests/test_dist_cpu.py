@@ -53,3 +53,53 @@ def test_shard_plan_rejects_bad_rank():
     with pytest.raises(ValueError):
         D.shard_plan(2, 2, 8)
     assert D.max_over_ranks(3.0) == 3.0      # no process group: identity
+
+
+def _kvhead_worker(rank, world, port, q):
+    import numpy as np
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        B, Hkv, N = 3, 4, 50
+        h0, hl, q0, ql = D.kvhead_plan(world, rank, 16, Hkv)
+        full = np.random.default_rng(7).random((B, Hkv, N), dtype=np.float32) * 100
+        S_local = torch.from_numpy(full[:, h0:h0 + hl].copy())
+        g = D.gather_scores(S_local)                       # [world][B][hl][N]
+        q.put((rank, (h0, hl, q0, ql), g.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_kvhead_gather_gloo_world2():
+    """KV-head sharding host logic: the all-gather puts shards in global head order, and the
+    ascending-head fp32 sum over the gathered parts is bitwise the unsharded S_i (AMB-14)."""
+    import numpy as np
+    from oracle import kvtier_oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_kvhead_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted((q.get(timeout=120) for _ in procs), key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, plan0, g0), (r1, plan1, g1) = out
+    assert plan0 == (0, 2, 0, 8) and plan1 == (2, 2, 8, 8)
+    assert np.array_equal(g0, g1)                          # every rank sees the same bytes
+    full = np.random.default_rng(7).random((3, 4, 50), dtype=np.float32) * 100
+    glob = np.concatenate(list(g0), axis=1)                # [B][H_kv][N] in global head order
+    assert np.array_equal(glob, full)
+    # the classify kernel's order: global head 0, 1, 2, 3 (ascending), fp32 adds
+    s = glob[:, 0].copy()
+    for h in range(1, 4):
+        s = (s + glob[:, h]).astype(np.float32)
+    for b in range(3):
+        assert np.array_equal(s[b], O.total_score_fp32(full[b]))
+
+
+def test_kvhead_plan_rejects_uneven():
+    with pytest.raises(ValueError):
+        D.kvhead_plan(3, 0, 16, 4)

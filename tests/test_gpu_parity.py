@@ -30,8 +30,11 @@ def _bf16_bits(a):
 
 
 def _check_event_state(run, orc, reqs_gpu, layers=(0,)):
-    """Tiers, index lists, census and store bytes after a manage event."""
+    """Tiers, index lists, census and store bytes after a manage event (store rows of the
+    ctx's own kv heads when it holds a KV-head shard)."""
     kv = run.kv
+    h0, hl = getattr(run, "heads", (0, run.w["Hkv"]))
+    hs = slice(h0, h0 + hl)
     st = orc.st
     n = st.n
     tiers = kv.export(kt.X_TIERS)
@@ -50,8 +53,8 @@ def _check_event_state(run, orc, reqs_gpu, layers=(0,)):
         for bo, bg in enumerate(reqs_gpu):
             for T, rows in ((0, t0), (1, t1)):
                 pos = O.export_index(st, bo, T)
-                wk = _bf16_bits(st.rowK[l, bo, :, pos].transpose(1, 0, 2))
-                wv = _bf16_bits(st.rowV[l, bo, :, pos].transpose(1, 0, 2))
+                wk = _bf16_bits(st.rowK[l, bo, hs][:, pos])            # [H_l][npos][d]
+                wv = _bf16_bits(st.rowV[l, bo, hs][:, pos])
                 assert np.array_equal(rows[bg][:, :, 0, :], wk), f"T{T} K rows layer {l} req {bg}"
                 assert np.array_equal(rows[bg][:, :, 1, :], wv), f"T{T} V rows layer {l} req {bg}"
             if stg is not None:
@@ -61,10 +64,10 @@ def _check_event_state(run, orc, reqs_gpu, layers=(0,)):
             scales = kv.export(kt.X_T2_SCALES, l)
             for bo, bg in enumerate(reqs_gpu):
                 pos = O.export_index(st, bo, 2)
-                assert np.array_equal(codes[bg][:, :, 0, :], st.codeK[l, bo, :, pos].transpose(1, 0, 2))
-                assert np.array_equal(codes[bg][:, :, 1, :], st.codeV[l, bo, :, pos].transpose(1, 0, 2))
-                assert np.array_equal(scales[bg][:, :, 0], st.scaleK[l, bo, :, pos].T)
-                assert np.array_equal(scales[bg][:, :, 1], st.scaleV[l, bo, :, pos].T)
+                assert np.array_equal(codes[bg][:, :, 0, :], st.codeK[l, bo, hs][:, pos])
+                assert np.array_equal(codes[bg][:, :, 1, :], st.codeV[l, bo, hs][:, pos])
+                assert np.array_equal(scales[bg][:, :, 0], st.scaleK[l, bo, hs][:, pos])
+                assert np.array_equal(scales[bg][:, :, 1], st.scaleV[l, bo, hs][:, pos])
 
 
 def _run_pair(w, reqs=None, graph=False, check_every=1, layers_api=False, split=0, variant=0):
@@ -319,3 +322,38 @@ def test_contiguous_stage_ranges(monkeypatch):   # KVTIER_RR=0: contiguous stage
     _run_pair(w, graph=True, check_every=5, split=3)
     monkeypatch.setenv("KVTIER_CLUSTER", "1")
     _run_pair(w, graph=True, check_every=5, split=5)
+
+
+# --------------------------------------------------------------------- KV-head sharding (§8e row 2)
+@pytest.mark.parametrize("world", [2, 4])
+def test_kvhead_sharding_matches_unsharded_oracle(world):
+    # world ctxs on one GPU, each owning H_kv/world kv heads; gathered scores at events
+    w = H.workload("tiny", B=2, L=2, Hq=16, Hkv=4, d=64, N=400, P=16, interval=8, steps=26,
+                   hbm_bp=4000, evict_bp=800, t2_bp=3000)
+    sh = H.KvHeadShardedDecode(w, world)
+    orc = OracleRun(w)
+    sh.capture()
+    for t in range(w["steps"]):
+        sh.step()
+        o_ref = orc.step()
+        ok, mabs, _ = o_close(sh.output()[:, orc.reqs], o_ref)
+        assert ok, (t, mabs)
+        if sh.is_event(t) or t == w["steps"] - 1:
+            S_gpu = sh.scores()
+            ok, mrel = s_close(S_gpu[orc.reqs], orc.st.S_part[:, :, :orc.st.n])
+            assert ok, (t, mrel)
+            tiers = [r.kv.export(kt.X_TIERS) for r in sh.runs]
+            for x in tiers[1:]:
+                assert np.array_equal(x, tiers[0])            # every shard holds the same tiers
+            for r in sh.runs:
+                _check_event_state(r, orc, orc.reqs, layers=(0, 1))
+    sh.close()
+
+
+def test_kvhead_plain_classify_refused():
+    w = H.workload("tiny", Hq=4, Hkv=2, steps=2)
+    run = H.TieredDecode(w, heads=(0, 1), shard=kt.SHARD_KVHEAD, rank=0, world=2)
+    run.step(manage=False)
+    with pytest.raises(RuntimeError):
+        run.kv.classify(stream=run.main)
+    run.close()
