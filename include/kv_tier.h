@@ -234,12 +234,15 @@ KV_TIER_API kv_tier_status kv_tier_scores_device(kv_tier_ctx* ctx, void** ptr, s
 KV_TIER_API kv_tier_status kv_tier_classify_gathered(kv_tier_ctx* ctx, const float* S_all, int32_t parts,
                                                      void* stream);
 
-/* Debug: %globaltimer checkpoints [L][B*H_kv][split][16] of the last launch of every layer:
- * 16 slots per CTA: (start, after PDL wait, first stage, loop done, partial written, merge
- * released, merge resident, merge end, consumer wait ns, consumer busy ns, stages, producer
- * empty-wait ns, producer done, -, -, -);
- * only with KVTIER_TRACE=1 in the environment at kv_tier_init. */
+/* Debug: %globaltimer checkpoints [L][CTAs][16] of the last launch of every layer; n must be
+ * kv_tier_debug_trace_len().  Split kernel (CTAs = B*H_kv*split): (start, after PDL wait, first
+ * stage, loop done, partial written, merge released, merge resident, merge end, consumer wait
+ * ns, consumer busy ns, stages, producer empty-wait ns, producer done, -, -, -).  Flat kernel
+ * (CTAs = grid): (start, after PDL wait, first stage, loop done, side warp new tokens done,
+ * side warp score pass done, last partial released, last unit finished, merges done, ns in
+ * unit epilogues, units finished, -, ...).  Only with KVTIER_TRACE=1 at kv_tier_init. */
 KV_TIER_API kv_tier_status kv_tier_debug_trace(kv_tier_ctx* ctx, uint64_t* host_dst, size_t n);
+KV_TIER_API kv_tier_status kv_tier_debug_trace_len(const kv_tier_ctx* ctx, size_t* n);
 
 KV_TIER_API const char* kv_tier_last_error(const kv_tier_ctx* ctx);
 KV_TIER_API const char* kv_tier_version(void);

@@ -14,12 +14,14 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-Xcompiler", "-fvisibility=hidden"]
 if os.environ.get("KVT_TRACE_LOOP"):        # debug: per-stage wait/busy accounting in the trace
     FLAGS += ["-DKVT_TRACE_LOOP=1"]
+if os.environ.get("KVT_FLAT_TRACE"):        # debug: per-unit epilogue timing in the flat kernel's trace
+    FLAGS += ["-DKVT_FLAT_TRACE=1"]
 
 TARGETS = {
-    "libkvtier.so": ["csrc/ctx.cu", "csrc/attn.cu", "csrc/tiers.cu"],
+    "libkvtier.so": ["csrc/ctx.cu", "csrc/attn.cu", "csrc/attn_flat.cu", "csrc/tiers.cu"],
     "libkvsynth.so": ["synth/synth.cu"],
 }
-DEPS = ["csrc/kv_internal.cuh", "../include/kv_tier.h", "../include/kv_synth.h"]
+DEPS = ["csrc/kv_internal.cuh", "csrc/decode_common.cuh", "../include/kv_tier.h", "../include/kv_synth.h"]
 
 
 def _stale(out, srcs):

@@ -40,6 +40,7 @@ struct kv_tier_ctx {
   cudaStream_t score_stream = nullptr;     // a4 score updates run here, off the attention chain
   cudaEvent_t ev_merged[ZRING] = {}, ev_scored[ZRING] = {}, ev_score_tail = nullptr;
   bool slot_recorded[2] = {false, false};   // ev_slot_free[x] recorded within the open step
+  int zflat_pending = -1;                  // flat kernel: slot whose score update the next launch applies
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   unsigned long long* trace = nullptr;     // debug timeline buffer (KVTIER_TRACE=1)
@@ -131,6 +132,13 @@ struct Layout {
 
 int split_of(const kv_tier_config& c);
 
+// Flat decode grid: one CTA per SM, more when a CTA would cover > 6 units (new-token slots).
+int flat_grid(const kv_tier_config& c, int nsm) {
+  const int units = c.num_requests * c.num_kv_heads;
+  return std::max(nsm, (units + 5) / 6);
+}
+constexpr int FLAT_GRID_MAX_SM = 296;     // partial slots reserved for grids up to this size
+
 // Rows an incremental migrate may move per request; more -> full rebuild (first event).
 size_t mcap_of(const kv_tier_config& c) {
   const char* ov = getenv("KVTIER_MCAP");                    // test hook: force the full-rebuild path
@@ -172,7 +180,9 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   L.off_S = take(BH * N * 4);
   L.off_z = take(ZRING * BH * (N + 64) * 8 * 4);     // logits of recent launches (score update)
   L.off_ml = take(ZRING * BH * 16 * 4);
-  L.off_part = take(BH * (split_of(c) + 1) * (16 + 8 * D) * 4);   // per-CTA partials + the new token
+  const size_t nslots = std::max(BH * (split_of(c) + 1),                 // split kernel: per-CTA partials + new token
+                                  (size_t)flat_grid(c, FLAT_GRID_MAX_SM) + 2 * BH);   // flat: <= grid + 2 units
+  L.off_part = take(nslots * (16 + 8 * D) * 4);
   L.off_uctr = take(BH * 4);
   L.b_scores = o - s0; s0 = o;
   for (int i = 0; i < 2; ++i) {
@@ -264,6 +274,28 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.stage_rr = getenv("KVTIER_RR") ? atoi(getenv("KVTIER_RR")) : 1;
   v.cluster_merge = (getenv("KVTIER_CLUSTER") && atoi(getenv("KVTIER_CLUSTER")) && v.split <= 8) ? 1 : 0;
   v.chunk_max = 0;
+  {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device);
+    v.nc = flat_grid(*cfg, std::min(nsm, FLAT_GRID_MAX_SM));
+    v.flat = getenv("KVTIER_FLAT") ? atoi(getenv("KVTIER_FLAT")) : 0;   // measured slower than split
+    // default: 8 consumer warps, 3 x 64 KB stages (2 stages when the T2 scratch needs room)
+    v.fvariant = getenv("KVTIER_FVAR") ? atoi(getenv("KVTIER_FVAR")) : (cfg->t2_fraction_bp > 0 ? 1 : 0);
+    if (v.cluster_merge) v.flat = 0;
+    // the flat kernel's partition arithmetic is 32-bit: cost space (<= 3 per 16 rows per unit)
+    // times the grid must fit
+    const unsigned long long units = (unsigned long long)cfg->num_requests * cfg->num_kv_heads;
+    if (units * 3ull * ((unsigned long long)cfg->max_tokens / 16 + 8) * (unsigned long long)v.nc >= (1ull << 32))
+      v.flat = 0;
+    // merging CTAs wait for their unit's other CTAs: the whole grid must be co-resident (one CTA
+    // per SM), and a CTA owns at most 8 new-token terms (units per CTA <= units/grid + 2)
+    if (v.nc > nsm || units > 6ull * (unsigned long long)v.nc) v.flat = 0;
+    v.spin_hint = getenv("KVTIER_SPIN") ? atoi(getenv("KVTIER_SPIN")) : 0;
+    // L2 prefetch budget: about a third of the 126 MB L2 per layer in flight, split over the grid
+    const long long l2mb = getenv("KVTIER_L2PF_MB") ? atoll(getenv("KVTIER_L2PF_MB")) : 0;   // measured: no gain
+    v.l2pf_bytes = l2mb * (1LL << 20) / std::max(1, v.nc);
+    v.inflight = getenv("KVTIER_INFLIGHT") ? atoi(getenv("KVTIER_INFLIGHT")) : 0;
+  }
   for (int i = 0; i < 2; ++i) {
     v.k0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_k0[i]);
     v.v0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_v0[i]);
@@ -317,11 +349,16 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     v.hs2v = reinterpret_cast<float*>(h + 2 * rows * v.D + rows * 4);
   }
   if (getenv("KVTIER_TRACE") && atoi(getenv("KVTIER_TRACE")) > 0) {
-    const size_t tb = (size_t)v.L * v.split * v.B * v.Hkv * NTRACE * sizeof(unsigned long long);
+    const size_t tb = (size_t)v.L * std::max(v.split * v.B * v.Hkv, v.nc) * NTRACE * sizeof(unsigned long long);
     if (cudaMalloc(&ctx->trace, tb) == cudaSuccess) { cudaMemset(ctx->trace, 0, tb); v.trace = ctx->trace; }
   }
-  if (attn_smem_bytes(v) > 227 * 1024 || merge_smem_bytes(v) > 227 * 1024) {
-    const size_t need = std::max(attn_smem_bytes(v), merge_smem_bytes(v));
+  if (v.flat && (v.fvariant < 0 || v.fvariant > 4)) {
+    delete ctx;
+    return fail(nullptr, KV_TIER_E_INVAL, "KVTIER_FVAR must be in [0, 4]");
+  }
+  const size_t smem_need = v.flat ? flat_smem_bytes(v) : std::max(attn_smem_bytes(v), merge_smem_bytes(v));
+  if (smem_need > 227 * 1024) {
+    const size_t need = smem_need;
     if (ctx->host_t1) cudaFreeHost(ctx->host_t1);
     if (ctx->host_t2) cudaFreeHost(ctx->host_t2);
     delete ctx;
@@ -341,7 +378,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     v.hot_bytes = std::min<size_t>(v.hot_bytes, (size_t)maxw);
     cudaGetLastError();                  // persistence is an optimisation: ignore if unsupported
   }
-  if (e == cudaSuccess) e = attn_configure(v);
+  if (e == cudaSuccess) e = v.flat ? flat_configure(v) : attn_configure(v);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_step_begin, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_migrated, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_offload_done, cudaEventDisableTiming);
@@ -502,6 +539,21 @@ static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, con
   cudaError_t e = cudaSuccess;
   if (ctx->v.stream_mode) e = cudaStreamWaitEvent(s, ctx->ev_prefetched[layer], 0);
   if (getenv("KVTIER_NOSCORE")) fuse_score_update = 0;   // experiment hook: attention without a4
+  if (ctx->v.flat) {
+    // a4: this launch writes its logits to slot zpar and applies the previous launch's pending
+    // update (slot zprev) in its side warp; end_step flushes the last one (launches of a ctx
+    // are stream-ordered, so the adds stay in layer order)
+    const int zpar = fuse_score_update ? (ctx->zflat_pending == 0 ? 1 : 0) : -1;
+    if (e == cudaSuccess)
+      e = launch_decode_flat(ctx->v, layer, q, k_new, v_new, o, zpar, ctx->zflat_pending, pdl, s);
+    if (e == cudaSuccess) ctx->zflat_pending = zpar;
+    if (e == cudaSuccess && ctx->v.stream_mode) {
+      e = cudaEventRecord(ctx->ev_slot_free[layer & 1], s);
+      ctx->slot_recorded[layer & 1] = true;
+    }
+    if (e == cudaSuccess && k_new) ctx->appended_step[layer] = ctx->t;
+    return cuda_check(ctx, e, "decode_attention");
+  }
   if (ctx->v.cluster_merge) {   // a4 fused into the kernel's epilogue (one logits slot, no score stream)
     const int zp = fuse_score_update ? 0 : -1;
     if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, zp, pdl, s);
@@ -547,7 +599,14 @@ kv_tier_status kv_tier_score_update(kv_tier_ctx* ctx, int32_t layer, const float
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (!probs) return fail(ctx, KV_TIER_E_INVAL, "null probs");
   if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
-  return cuda_check(ctx, launch_score_update(ctx->v, layer, probs, reinterpret_cast<cudaStream_t>(stream)), "score_update");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  if (ctx->zflat_pending >= 0) {          // keep layer order: the pending fused update goes first
+    e = launch_score_flush(ctx->v, ctx->zflat_pending, 1, s);
+    ctx->zflat_pending = -1;
+  }
+  if (e == cudaSuccess) e = launch_score_update(ctx->v, layer, probs, s);
+  return cuda_check(ctx, e, "score_update");
 }
 
 kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream) {
@@ -555,7 +614,11 @@ kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream) {
   if (!ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "end_step without begin_step");
   cudaError_t e = cudaSuccess;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (ctx->zpend_n > 0) e = issue_scores(ctx, s);
+  if (ctx->zflat_pending >= 0) {           // flat kernel: the last fused launch's score update
+    e = launch_score_flush(ctx->v, ctx->zflat_pending, 1, s);
+    ctx->zflat_pending = -1;
+  }
+  if (e == cudaSuccess && ctx->zpend_n > 0) e = issue_scores(ctx, s);
   if (e == cudaSuccess && ctx->scores_pending) {     // join the score stream: S_part is complete for this step
     e = cudaEventRecord(ctx->ev_score_tail, ctx->score_stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->ev_score_tail, 0);
@@ -699,6 +762,7 @@ kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const
   ctx->appended_step = astep;
   ctx->zslot_next = 0;
   ctx->zpend_n = 0;
+  ctx->zflat_pending = -1;
   for (auto& b : ctx->slot_busy) b = false;
   ctx->scores_pending = false;
   if (st) { if (g) cudaGraphDestroy(g); return st; }
@@ -903,9 +967,15 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
   return cuda_check(ctx, e, "export");
 }
 
+kv_tier_status kv_tier_debug_trace_len(const kv_tier_ctx* ctx, size_t* n) {
+  if (!ctx || !n) return fail(nullptr, KV_TIER_E_INVAL, "null arg");
+  *n = (size_t)ctx->v.L * (ctx->v.flat ? ctx->v.nc : ctx->v.split * ctx->v.B * ctx->v.Hkv) * NTRACE;
+  return KV_TIER_OK;
+}
+
 kv_tier_status kv_tier_debug_trace(kv_tier_ctx* ctx, uint64_t* host_dst, size_t n) {
   if (!ctx || !host_dst) return fail(ctx, KV_TIER_E_INVAL, "null arg");
-  const size_t need = (size_t)ctx->v.L * ctx->v.split * ctx->v.B * ctx->v.Hkv * NTRACE;
+  const size_t need = (size_t)ctx->v.L * (ctx->v.flat ? ctx->v.nc : ctx->v.split * ctx->v.B * ctx->v.Hkv) * NTRACE;
   if (!ctx->trace) return fail(ctx, KV_TIER_E_STATE, "tracing off (set KVTIER_TRACE=1 before kv_tier_init)");
   if (n != need) return fail(ctx, KV_TIER_E_INVAL, "trace needs %zu entries", need);
   cudaError_t e = cudaDeviceSynchronize();

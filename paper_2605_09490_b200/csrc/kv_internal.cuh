@@ -7,7 +7,7 @@
 namespace kvt {
 
 constexpr int T0 = 0, T1 = 1, T2 = 2, T3 = 3;
-constexpr int NTRACE = 16;        // debug trace slots per CTA (KVTIER_TRACE=1)
+constexpr int NTRACE = 24;        // debug trace slots per CTA (KVTIER_TRACE=1)
 constexpr int CNT_STRIDE = 8;     // cnt[buf][b][8]: |T0| |T1| |T2| |T3| |visible at event| pad..
 constexpr int ZRING = 4;          // logits/ML ring slots (score kernels lag the decode chain)
 constexpr int ZBATCH = 1;         // launches whose score updates one score kernel applies (layer order;
@@ -41,13 +41,19 @@ struct DevView {
   int l2_prefetch;      // pre-wait L2 prefetch of the CTA's stages beyond the shared-memory ring
   int stage_rr;         // stages dealt round-robin to the unit's CTAs (else contiguous ranges)
   int cluster_merge;    // merge the unit's partials in distributed shared memory (cluster of split CTAs)
+  int flat;             // flat decode kernel (attn_flat.cu; default) instead of split-per-unit
+  int fvariant;         // flat kernel variant (consumer warps x stages)
+  int nc;               // flat kernel grid (CTAs; one per SM)
+  int spin_hint;        // mbarrier try_wait suspend-time hint in ns (0: plain polling)
+  long long l2pf_bytes; // flat kernel: K/V bytes per CTA requested into L2 at kernel start (0: off)
+  int inflight;         // flat kernel: max ring stages requested but not landed (0: the whole ring)
   unsigned long long* trace;   // debug: per-CTA %globaltimer checkpoints (null = off)
   float* zbuf;          // [ZRING][B*Hkv][zrows][8] logits (log2 domain) of recent launches
   float* ml;            // [ZRING][B*Hkv][16] per-head (max, 1/sum) of recent launches
   int zrows;            // virtual rows per unit (N_max + padding)
   float* part;          // [B*Hkv][split][part_stride] per-CTA partials (m[8], l[8], o[G][D])
   int part_stride;
-  int* unit_ctr;        // [B*Hkv] (unused by the current decode path)
+  int* unit_ctr;        // [B*Hkv] partials published per unit (flat kernel; reset by the merging CTA)
   void* hot_base;       // L2 access-policy window over the small hot buffers
   size_t hot_bytes;
   int4* moves;          // [B][mcap] {src tier, src row, dst tier | dst row << 2, position}
@@ -114,6 +120,10 @@ cudaError_t launch_offload_host(const DevView& v, int cur, cudaStream_t s);
 cudaError_t launch_commit(const DevView& v, cudaStream_t s);
 cudaError_t launch_prefetch(const DevView& v, int layer, cudaStream_t s);
 size_t attn_smem_bytes(const DevView& v);
+size_t flat_smem_bytes(const DevView& v);
+cudaError_t flat_configure(const DevView& v);
+cudaError_t launch_decode_flat(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
+                               void* o, int zpar, int zprev, int pdl, cudaStream_t s);
 size_t merge_smem_bytes(const DevView& v);
 cudaError_t attn_configure(const DevView& v);
 }  // namespace kvt

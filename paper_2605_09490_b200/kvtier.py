@@ -77,6 +77,7 @@ _SIGS = {
     "kv_tier_export": [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t],
     "kv_tier_import_scores": [C.c_void_p, C.c_void_p, C.c_size_t],
     "kv_tier_debug_trace": [C.c_void_p, C.c_void_p, C.c_size_t],
+    "kv_tier_debug_trace_len": [C.c_void_p, C.POINTER(C.c_size_t)],
     "kv_tier_last_error": [C.c_void_p],
     "kv_tier_version": [],
 }
@@ -261,11 +262,13 @@ class KvTier:
         return buf.view(np.float32).reshape(B, H, -1, 2)
 
     def debug_trace(self):
-        """[L][split*B*H_kv][16] %globaltimer ns checkpoints of the last step (KVTIER_TRACE=1)."""
-        n = self.cfg.num_layers * self.cfg.num_requests * self.cfg.num_kv_heads * 16 * max(1, self._split())
+        """[L][CTAs][NTRACE] %globaltimer ns checkpoints of the last step (KVTIER_TRACE=1)."""
+        ln = C.c_size_t(0)
+        _check(load().kv_tier_debug_trace_len(self.ctx, C.byref(ln)), self.ctx)
+        n = ln.value
         buf = np.zeros(n, dtype=np.uint64)
         _check(load().kv_tier_debug_trace(self.ctx, buf.ctypes.data_as(C.c_void_p), n), self.ctx)
-        return buf.reshape(self.cfg.num_layers, -1, 16)
+        return buf.reshape(self.cfg.num_layers, -1, NTRACE)
 
     def _split(self):
         if self.cfg.split:
@@ -276,6 +279,9 @@ class KvTier:
     def import_scores(self, S):
         S = np.ascontiguousarray(S, dtype=np.float32)
         _check(load().kv_tier_import_scores(self.ctx, S.ctypes.data_as(C.c_void_p), S.nbytes), self.ctx)
+
+
+NTRACE = 24            # trace slots per CTA (kv_internal.cuh)
 
 
 def version():

@@ -315,6 +315,34 @@ def test_cluster_merge_equals_merge_kernel_bitwise(monkeypatch):
     assert np.array_equal(scores[0], scores[1])
 
 
+# --------------------------------------------------------------------- flat work distribution
+@pytest.mark.parametrize("fvar,t2", [("0", 0), ("1", 2500), ("2", 2500)])
+def test_flat_kernel_parity(fvar, t2, monkeypatch):
+    # one CTA per SM over the flat (unit, 16-row group) list; units span several CTAs, merged
+    # by the CTA that owns their first group (attn_flat.cu).  Events every 16 steps.
+    monkeypatch.setenv("KVTIER_FLAT", "1")
+    monkeypatch.setenv("KVTIER_FVAR", fvar)
+    w = H.workload("tiny", B=3, L=2, Hq=12, Hkv=2, d=128, N=700, P=40, interval=16, steps=34,
+                   hbm_bp=3000, evict_bp=1000, t2_bp=t2)
+    _run_pair(w, graph=True, check_every=5)
+
+
+@pytest.mark.parametrize("shape", [dict(B=1, Hq=4, Hkv=1, d=64, N=300, P=16),      # 1 unit over many CTAs
+                                   dict(B=24, Hq=8, Hkv=4, d=64, N=120, P=16)])    # many units per CTA
+def test_flat_kernel_partition_extremes(shape, monkeypatch):
+    monkeypatch.setenv("KVTIER_FLAT", "1")
+    w = H.workload("tiny", L=2, interval=8, steps=18, hbm_bp=5000, evict_bp=500, t2_bp=0, **shape)
+    _run_pair(w, graph=True, check_every=3)
+
+
+def test_flat_kernel_7b_sampled(monkeypatch):
+    # BASELINE.json configs[1] shape, launch configuration of bench.py (graph, PDL), sampled
+    # requests against the oracle
+    monkeypatch.setenv("KVTIER_FLAT", "1")
+    w = H.workload("7b", steps=3)
+    _run_pair(w, reqs=[0, 5], graph=True, check_every=1)
+
+
 def test_contiguous_stage_ranges(monkeypatch):   # KVTIER_RR=0: contiguous stage ranges per CTA
     monkeypatch.setenv("KVTIER_RR", "0")
     w = H.workload("tiny", B=3, L=2, Hq=12, Hkv=2, d=128, N=700, P=40, interval=16, steps=34,
