@@ -89,14 +89,24 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   const int cur = v.st->cur;
   Seg sg;
   sg.init(v.cnt[cur] + b * CNT_STRIDE);
-  // This CTA's work: stages of NW 16-row groups (one per consumer warp) from the unit's stage
-  // list [bf16 segment [0, a2) | int8 segment [a2, a2 + n2)], dealt round-robin (stage k ->
-  // rank k mod C, default) or as contiguous ranges (KVTIER_RR=0).  Static either way, so the
-  // fp32 summation order never depends on timing.
+  // This CTA's work: stages of up to NW 16-row groups (one per consumer warp) from the unit's
+  // groups [bf16 segment [0, a2) | int8 segment [a2, a2 + n2)].  Default (KVTIER_RR=2): the
+  // groups themselves are dealt round-robin over the unit's C CTAs (bf16 then int8, continuing
+  // the deal), so CTAs differ by at most one group; KVTIER_RR=1 deals whole stages, 0 cuts
+  // contiguous stage ranges.  Static in every mode, so the fp32 summation order never depends
+  // on timing.  stage_at(i) -> kind, groups in the stage; group_of(i, w) -> the segment-relative
+  // index of warp w's group.
   const int gbf = sg.a2 >> 4, gq2 = (sg.n2 + 15) >> 4;
   const int sbf = (gbf + NW - 1) / NW, ns_all = sbf + (gq2 + NW - 1) / NW;
-  int cs0, cstr, nstage;
-  if (v.stage_rr) {
+  const int mode = v.stage_rr;
+  int cs0 = 0, cstr = 1, nstage, nb = 0, nq = 0, q0 = 0, sbr = 0;
+  if (mode == 2) {
+    nb = gbf > r ? (gbf - r + C - 1) / C : 0;              // bf16 groups r, r + C, ...
+    q0 = ((r - gbf) % C + C) % C;                          // int8 groups q0, q0 + C, ...
+    nq = gq2 > q0 ? (gq2 - q0 + C - 1) / C : 0;
+    sbr = (nb + NW - 1) / NW;
+    nstage = sbr + (nq + NW - 1) / NW;
+  } else if (mode == 1) {
     cs0 = r;
     cstr = C;
     nstage = ns_all > r ? (ns_all - r + C - 1) / C : 0;
@@ -105,11 +115,22 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     cstr = 1;
     nstage = (int)((long long)ns_all * (r + 1) / C) - cs0;
   }
-  auto stage_at = [&](int i, bool& t2, int& g0, int& ng) {   // this CTA's i-th stage
+  auto stage_at = [&](int i, bool& t2, int& ng) {          // this CTA's i-th stage
+    if (mode == 2) {
+      t2 = i >= sbr;
+      const int l0 = (t2 ? i - sbr : i) * NW;
+      ng = min(NW, (t2 ? nq : nb) - l0);
+    } else {
+      const int gs = cs0 + i * cstr;
+      t2 = gs >= sbf;
+      const int g0 = (t2 ? gs - sbf : gs) * NW;
+      ng = min(NW, (t2 ? gq2 : gbf) - g0);
+    }
+  };
+  auto group_of = [&](int i, int wi) {                      // segment-relative group index
+    if (mode == 2) return i >= sbr ? q0 + C * ((i - sbr) * NW + wi) : r + C * (i * NW + wi);
     const int gs = cs0 + i * cstr;
-    t2 = gs >= sbf;
-    g0 = (t2 ? gs - sbf : gs) * NW;
-    ng = min(NW, (t2 ? gq2 : gbf) - g0);
+    return (gs >= sbf ? gs - sbf : gs) * NW + wi;
   };
   const bool has_new = r == 0;                               // rank 0 handles the new token
 
@@ -159,27 +180,19 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
           if (v.l2_prefetch) {
             for (int j = i; j < nstage; ++j) {
               bool pt2;
-              int pg0, png;
-              stage_at(j, pt2, pg0, png);
-              const int nrows = 16 * png;
-              if (!pt2) {
-                const int ts = 16 * pg0;
-                if (ts < sg.a1) {
-                  const int n0r = min(nrows, sg.a1 - ts);
-                  bulk_prefetch_l2(K0 + (size_t)ts * D, n0r * ROWB);
-                  bulk_prefetch_l2(V0 + (size_t)ts * D, n0r * ROWB);
-                  if (n0r < nrows) {
-                    bulk_prefetch_l2(K1, (nrows - n0r) * ROWB);
-                    bulk_prefetch_l2(V1, (nrows - n0r) * ROWB);
-                  }
+              int png;
+              stage_at(j, pt2, png);
+              for (int wi = 0; wi < png; ++wi) {
+                const int gi = group_of(j, wi);
+                if (!pt2) {
+                  const int ts = 16 * gi;             // a1 is a multiple of 16: one store per group
+                  bulk_prefetch_l2((ts < sg.a1 ? K0 + (size_t)ts * D : K1 + (size_t)(ts - sg.a1) * D), 16 * ROWB);
+                  bulk_prefetch_l2((ts < sg.a1 ? V0 + (size_t)ts * D : V1 + (size_t)(ts - sg.a1) * D), 16 * ROWB);
                 } else {
-                  bulk_prefetch_l2(K1 + (size_t)(ts - sg.a1) * D, nrows * ROWB);
-                  bulk_prefetch_l2(V1 + (size_t)(ts - sg.a1) * D, nrows * ROWB);
+                  const size_t j0 = 16 * (size_t)gi;
+                  bulk_prefetch_l2(v.c2k[sb] + (grp * v.cap2 + j0) * D, 16 * D);
+                  bulk_prefetch_l2(v.c2v[sb] + (grp * v.cap2 + j0) * D, 16 * D);
                 }
-              } else {
-                const size_t j0 = 16 * (size_t)pg0;
-                bulk_prefetch_l2(v.c2k[sb] + (grp * v.cap2 + j0) * D, nrows * D);
-                bulk_prefetch_l2(v.c2v[sb] + (grp * v.cap2 + j0) * D, nrows * D);
               }
             }
           }
@@ -205,35 +218,31 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
         }
         stile[s2] = i;
         bool st2;
-        int g0, ng;
-        stage_at(i, st2, g0, ng);
+        int ng;
+        stage_at(i, st2, ng);
         const int nrows = 16 * ng;
         if (!st2) {                   // bf16 rows: T0 (pad rows beyond n0o are stale but finite), T1
-          const int ts = 16 * g0;
           mbar_expect_tx(full, 2 * nrows * ROWB);
-          if (ts < sg.a1) {           // a1 is a multiple of 16: the T1 part starts at T1 row 0
-            const int n0r = min(nrows, sg.a1 - ts);
-            bulk_g2s_ef(dst, K0 + (size_t)ts * D, n0r * ROWB, full, pol);
-            bulk_g2s_ef(dst + TILEB, V0 + (size_t)ts * D, n0r * ROWB, full, pol);
-            if (n0r < nrows) {
-              bulk_g2s_ef(dst + n0r * ROWB, K1, (nrows - n0r) * ROWB, full, pol);
-              bulk_g2s_ef(dst + TILEB + n0r * ROWB, V1, (nrows - n0r) * ROWB, full, pol);
-            }
-          } else {
-            bulk_g2s_ef(dst, K1 + (size_t)(ts - sg.a1) * D, nrows * ROWB, full, pol);
-            bulk_g2s_ef(dst + TILEB, V1 + (size_t)(ts - sg.a1) * D, nrows * ROWB, full, pol);
+          for (int wi = 0; wi < ng;) {               // runs of consecutive groups in one store
+            const int gi = group_of(i, wi);
+            const int ts = 16 * gi;                  // a1 is a multiple of 16: no group straddles
+            int run = 1;
+            while (wi + run < ng && group_of(i, wi + run) == gi + run && (ts < sg.a1) == (ts + 16 * run < sg.a1)) ++run;
+            const __nv_bfloat16* ks = ts < sg.a1 ? K0 + (size_t)ts * D : K1 + (size_t)(ts - sg.a1) * D;
+            const __nv_bfloat16* vs = ts < sg.a1 ? V0 + (size_t)ts * D : V1 + (size_t)(ts - sg.a1) * D;
+            bulk_g2s_ef(dst + wi * 16 * ROWB, ks, run * 16 * ROWB, full, pol);
+            bulk_g2s_ef(dst + TILEB + wi * 16 * ROWB, vs, run * 16 * ROWB, full, pol);
+            wi += run;
           }
         } else {                      // T2: int8 codes + fp32 scales (canonical layout; rows < cap2)
-          const int j0 = 16 * g0;
-          const int8_t* CK = v.c2k[sb] + (grp * v.cap2 + j0) * D;
-          const int8_t* CV = v.c2v[sb] + (grp * v.cap2 + j0) * D;
-          const float* SK = v.s2k[sb] + grp * v.cap2 + j0;
-          const float* SV = v.s2v[sb] + grp * v.cap2 + j0;
           mbar_expect_tx(full, 2 * (nrows * D + nrows * 4));
-          bulk_g2s(dst, CK, nrows * D, full);
-          bulk_g2s(dst + TILE * D, SK, nrows * 4, full);
-          bulk_g2s(dst + TILEB, CV, nrows * D, full);
-          bulk_g2s(dst + TILEB + TILE * D, SV, nrows * 4, full);
+          for (int wi = 0; wi < ng; ++wi) {
+            const int j0 = 16 * group_of(i, wi);
+            bulk_g2s(dst + wi * 16 * D, v.c2k[sb] + (grp * v.cap2 + j0) * D, 16 * D, full);
+            bulk_g2s(dst + TILE * D + wi * 16 * 4, v.s2k[sb] + grp * v.cap2 + j0, 16 * 4, full);
+            bulk_g2s(dst + TILEB + wi * 16 * D, v.c2v[sb] + (grp * v.cap2 + j0) * D, 16 * D, full);
+            bulk_g2s(dst + TILEB + TILE * D + wi * 16 * 4, v.s2v[sb] + grp * v.cap2 + j0, 16 * 4, full);
+          }
         }
       }
     }
@@ -475,12 +484,12 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     if (tr && tid == 0 && i == 0) tr[2] = gtimer();
     const uint32_t sK = ring_s + s2 * STAGEB, sV = sK + TILEB;
     bool t2;
-    int g0, ng;
-    stage_at(k, t2, g0, ng);
+    int ng;
+    stage_at(k, t2, ng);
     const bool wact = w < ng;                                 // this warp's group is in the stage
-    const int tv0 = t2 ? sg.a2 + 16 * g0 : 16 * g0;
-    const int r0 = w * 16 + gq, r1 = r0 + 8;
-    const int t0 = tv0 + r0, t1 = tv0 + r1;
+    const int tv0 = (t2 ? sg.a2 : 0) + 16 * (wact ? group_of(k, w) : 0);   // warp's first virtual row
+    const int r0 = w * 16 + gq, r1 = r0 + 8;                  // rows within the stage tile
+    const int t0 = tv0 + gq, t1 = tv0 + gq + 8;
     const bool v0 = wact && (t2 ? (t0 - sg.a2 < sg.n2) : sg.bf16_valid(t0));
     const bool v1 = wact && (t2 ? (t1 - sg.a2 < sg.n2) : sg.bf16_valid(t1));
     if (__any_sync(0xffffffffu, v0 || v1)) {
@@ -614,7 +623,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       float Ls = 0.f, acc = 0.f;
       for (int c = 0; c < NP; ++c) {
         const float mc = rbuf[c * cm_rb + h];
-        const float f = mc == -INFINITY ? 0.f : exp2f(mc - M);
+        const float f = mc == -INFINITY ? 0.f : ex2_ftz(mc - M);
         Ls += f * rbuf[c * cm_rb + 8 + h];
         acc += f * rbuf[c * cm_rb + 16 + j];
       }
@@ -635,7 +644,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     float Ls = 0.f;
     for (int c = 0; c <= C; ++c) {
       const float mc = rbuf[c * cm_rb + tid];
-      const float f = mc == -INFINITY ? 0.f : exp2f(mc - M);
+      const float f = mc == -INFINITY ? 0.f : ex2_ftz(mc - M);
       Ls += f * rbuf[c * cm_rb + 8 + tid];
     }
     sML[tid] = M;
@@ -660,11 +669,12 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
           bool ok;
           if (j < nstage * TILE) {        // stage rows: T0/T1 or T2 rows only (never pads)
             bool jt2;
-            int jg0, jng;
-            stage_at(j / TILE, jt2, jg0, jng);
+            int jng;
+            stage_at(j / TILE, jt2, jng);
             const int row = j % TILE;
-            t = (jt2 ? sg.a2 : 0) + 16 * jg0 + row;
-            ok = row < 16 * jng && (jt2 ? t < sg.a2 + sg.n2 : sg.bf16_valid(t));
+            ok = row < 16 * jng;
+            t = ok ? (jt2 ? sg.a2 : 0) + 16 * group_of(j / TILE, row >> 4) + (row & 15) : 0;
+            ok = ok && (jt2 ? t < sg.a2 + sg.n2 : sg.bf16_valid(t));
           } else {                        // the new token (rank 0)
             t = sg.a3;
             ok = true;
@@ -688,7 +698,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
         float inc = 0.f;
 #pragma unroll
         for (int h = 0; h < 8; ++h)
-          if (h < G) inc += exp2f(zz[h] - sML[h]) * sML[8 + h];
+          if (h < G) inc += ex2_ftz(zz[h] - sML[h]) * sML[8 + h];
         S[pos[k]] = sv[k] + inc;
         bad |= !isfinite(inc);
       }
@@ -698,66 +708,88 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   if (tr && tid == 0) tr[7] = gtimer();
 }
 
-// Merge of the C per-CTA partials of every unit, in rank order (deterministic): o and the
-// per-head (max, 1/sum) for the deferred score pass.  Launched right behind the decode kernel
-// with programmatic dependent launch: its CTAs are resident early and start when it completes.
+// Merge of the C per-CTA partials (+ the new-token partial) of every unit, in rank order
+// (deterministic): o and the per-head (max, 1/sum) for the deferred score pass.  Launched right
+// behind the decode kernel with programmatic dependent launch: its CTAs are resident early and
+// start when it completes.  One CTA per unit, one float4 of o per thread; each thread issues its
+// partial loads right after the wait, the per-head (M, 1/L) and the factors exp2(m_c - M) are
+// computed once (shared memory) in the same round trip, and o goes out as one vector store.
 template <int D>
-__global__ void __launch_bounds__(512) k_decode_merge(const DevView v, const int layer, void* __restrict__ o,
+__global__ void __launch_bounds__(256) k_decode_merge(const DevView v, const int layer, void* __restrict__ o,
                                                       const int zpar) {
-  // one CTA per unit; every thread loads, for its output element, the (m, l) of its head and
-  // the o value of all C+1 partials at once (independent loads: one L2 round trip), then
-  // merges them in rank order (deterministic).  C+1 <= 65.
-  const int unit = blockIdx.x, tid = threadIdx.x + blockIdx.y * blockDim.x;
+  constexpr int MAXP = 16, MAXNP = 65;
+  __shared__ float sf[MAXNP * 8], sl[MAXNP * 8], sI[8];
+  const int unit = blockIdx.x, tid = threadIdx.x;
   const int b = unit / v.Hkv, g = unit - b * v.Hkv;
-  const int G = v.G, NP = v.split + 1, tot = G * D;
+  const int G = v.G, NP = v.split + 1, tot4 = G * D / 4;
   unsigned long long* tr = v.trace ? v.trace + (((size_t)layer * v.B * v.Hkv + unit) * v.split) * NTRACE : nullptr;
-  if (tr && tid == 0 && blockIdx.y == 0) tr[6] = gtimer();
+  if (tr && tid == 0) tr[6] = gtimer();
   pdl_trigger();
   pdl_wait();
-  if (tr && tid == 0 && blockIdx.y == 0) tr[5] = gtimer();
+  if (tr && tid == 0) tr[5] = gtimer();
   const float* P = v.part + (size_t)unit * NP * v.part_stride;
-  for (int e = tid; e < tot; e += blockDim.x * gridDim.y) {
-    const int h = e / D, dd = e - h * D;
-    constexpr int MAXP = 16;                        // registers only (512 threads -> <= 128 regs)
-    float m[MAXP], l[MAXP], x[MAXP];
-    float M = -INFINITY, Ls = 0.f, acc = 0.f;
-    for (int c0 = 0; c0 < NP; c0 += MAXP) {          // one batch for split <= 16
+  const bool act = tid < tot4;
+  float4 x[MAXP];
 #pragma unroll
-      for (int c = 0; c < MAXP; ++c) {
-        if (c0 + c < NP) {
-          const float* pc = P + (size_t)(c0 + c) * v.part_stride;
-          m[c] = __ldcg(pc + h);
-          l[c] = __ldcg(pc + 8 + h);
-          x[c] = __ldcg(pc + 16 + e);
-        }
-      }
-      float Mn = M;
-#pragma unroll
-      for (int c = 0; c < MAXP; ++c)
-        if (c0 + c < NP) Mn = fmaxf(Mn, m[c]);
-      const float sc = M == -INFINITY ? 0.f : exp2f(M - Mn);
-      Ls *= sc;
-      acc *= sc;
-#pragma unroll
-      for (int c = 0; c < MAXP; ++c)
-        if (c0 + c < NP) {
-          const float f = m[c] == -INFINITY ? 0.f : exp2f(m[c] - Mn);
-          Ls += f * l[c];
-          acc += f * x[c];
-        }
-      M = Mn;
+  for (int c = 0; c < MAXP; ++c)
+    if (act && c < NP) x[c] = __ldcg(reinterpret_cast<const float4*>(P + (size_t)c * v.part_stride + 16) + tid);
+  for (int i = tid; i < NP * 8; i += blockDim.x) {
+    sf[i] = __ldcg(P + (size_t)(i >> 3) * v.part_stride + (i & 7));
+    sl[i] = __ldcg(P + (size_t)(i >> 3) * v.part_stride + 8 + (i & 7));
+  }
+  __syncthreads();
+  if (tid < 8) {
+    const int h = tid;
+    float M = -INFINITY;
+    for (int c = 0; c < NP; ++c) M = fmaxf(M, sf[c * 8 + h]);
+    float Ls = 0.f;
+    for (int c = 0; c < NP; ++c) {
+      const float mc = sf[c * 8 + h];
+      const float f = mc == -INFINITY ? 0.f : ex2_ftz(mc - M);
+      sf[c * 8 + h] = f;
+      Ls += f * sl[c * 8 + h];
     }
     const float invL = 1.0f / Ls;
-    const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
-    if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = acc * invL;
-    else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(acc * invL);
-    if (dd == 0 && zpar >= 0) {        // publish (M, 1/L) for the deferred score pass
+    sI[h] = invL;
+    if (h < G && zpar >= 0) {          // publish (M, 1/L) for the deferred score pass
       float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
       ml[h] = M;
       ml[8 + h] = invL;
     }
   }
-  if (tr && tid == 0 && blockIdx.y == 0) tr[7] = gtimer();
+  __syncthreads();
+  if (act) {
+    const int h = (4 * tid) / D;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = 0; c0 < NP; c0 += MAXP) {
+      if (c0 > 0) {                    // split > 15: next batch of partials
+#pragma unroll
+        for (int c = 0; c < MAXP; ++c)
+          if (c0 + c < NP) x[c] = __ldcg(reinterpret_cast<const float4*>(P + (size_t)(c0 + c) * v.part_stride + 16) + tid);
+      }
+#pragma unroll
+      for (int c = 0; c < MAXP; ++c)
+        if (c0 + c < NP) {
+          const float f = sf[(c0 + c) * 8 + h];
+          acc.x += f * x[c].x;
+          acc.y += f * x[c].y;
+          acc.z += f * x[c].z;
+          acc.w += f * x[c].w;
+        }
+    }
+    const float il = sI[h];
+    const size_t oi = ((size_t)b * v.Hq + g * G) * D + 4 * tid;
+    if (v.out_fp32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(o) + oi) = make_float4(acc.x * il, acc.y * il, acc.z * il, acc.w * il);
+    } else {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * il, acc.y * il), hi = __floats2bfloat162_rn(acc.z * il, acc.w * il);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o) + oi) = pk;
+    }
+  }
+  if (tr && tid == 0) tr[7] = gtimer();
 }
 
 size_t merge_smem_bytes(const DevView& v) { (void)v; return 0; }
@@ -879,8 +911,8 @@ static cudaError_t launch_decode_main(const DevView& v, int layer, const void* q
 
 static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, int pdl, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(v.B * v.Hkv, 2, 1);
-  cfg.blockDim = dim3(512, 1, 1);
+  cfg.gridDim = dim3(v.B * v.Hkv, 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
   cfg.dynamicSmemBytes = merge_smem_bytes(v);
   cfg.stream = s;
   cudaLaunchAttribute at[2];

@@ -210,7 +210,7 @@ __device__ __forceinline__ void score_range(const DevView& v, const Seg& sg, int
         float inc = 0.f;
 #pragma unroll
         for (int h = 0; h < 8; ++h)
-          if (h < v.G) inc += exp2f(zz[h] - ml[h]) * ml[8 + h];
+          if (h < v.G) inc += ex2_ftz(zz[h] - ml[h]) * ml[8 + h];
         s = s + inc;
         bad |= !isfinite(inc);
       }

@@ -39,7 +39,7 @@ struct DevView {
   int pdl_pre;          // stages the producer may load before griddepcontrol.wait
   int use_pdl;          // chain consecutive layers with programmatic dependent launch
   int l2_prefetch;      // pre-wait L2 prefetch of the CTA's stages beyond the shared-memory ring
-  int stage_rr;         // stages dealt round-robin to the unit's CTAs (else contiguous ranges)
+  int stage_rr;         // 2: 16-row groups dealt round-robin to the unit's CTAs, 1: whole stages, 0: contiguous
   int cluster_merge;    // merge the unit's partials in distributed shared memory (cluster of split CTAs)
   int flat;             // flat decode kernel (attn_flat.cu; default) instead of split-per-unit
   int fvariant;         // flat kernel variant (consumer warps x stages)
