@@ -46,6 +46,7 @@ def _args():
     ap.add_argument("--hbm", type=int, default=5000, help="beta in basis points")
     ap.add_argument("--evict", type=int, default=500, help="r in basis points")
     ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=0, help="decode kernel variant (consumer warps x stages)")
     ap.add_argument("--no-extras", action="store_true", help="skip control/e2e/stream/cpu legs")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -208,7 +209,7 @@ def main():
     seed_off, _ = shard_plan(world, rank, 1)
 
     # ---- leg 1: tiered, differential staging, device-resident inputs -> value
-    run = H.TieredDecode(w, device=dev, out_fp32=False, split=args.split, seed_offset=seed_off)
+    run = H.TieredDecode(w, device=dev, out_fp32=False, split=args.split, seed_offset=seed_off, variant=args.variant)
     run.capture()
     for _ in range(W):
         run.step()
@@ -339,7 +340,8 @@ def main():
     control_ms = None
     stream_leg = None
     if not args.no_extras:
-        ctl = H.TieredDecode(dict(w, steps=W + K), device=dev, out_fp32=False, split=args.split, seed_offset=seed_off)
+        ctl = H.TieredDecode(dict(w, steps=W + K), device=dev, out_fp32=False, split=args.split, seed_offset=seed_off,
+                             variant=args.variant)
         ctl.capture()
         for _ in range(W):
             ctl.step()
@@ -362,7 +364,7 @@ def main():
         # ---- stream mode (S = 0): T1 rows cross the host link every step (AMB-13)
         Ks, Ws = 8, 2
         ws = dict(w, staging=0, steps=Ws + Ks)
-        sr = H.TieredDecode(ws, device=dev, out_fp32=False, split=args.split, seed_offset=seed_off)
+        sr = H.TieredDecode(ws, device=dev, out_fp32=False, split=args.split, seed_offset=seed_off, variant=args.variant)
         sr.capture()
         for _ in range(Ws):
             sr.step()
