@@ -69,7 +69,19 @@ typedef enum { KV_TIER_EVICT_TOTAL = 0, KV_TIER_EVICT_PER_EVENT = 1 } kv_tier_ev
  *            so at an event every rank all-gathers S_part (kv_tier_scores_device) and calls
  *            kv_tier_classify_gathered: identical S -> identical tiers on every rank, summed
  *            in ascending global head order exactly as unsharded (bit-exact).
- *   SEQUENCE reserved. */
+ *   SEQUENCE positions are owned block-cyclically: block k = positions [64k, 64k+64) belongs
+ *            to rank k % world.  A rank's tier stores, index lists and
+ *            census hold its own positions only; the tier array and S_part cover every
+ *            position.  load_prefix takes the FULL prefix and keeps the rank's rows; the new
+ *            token of a step is stored by its owner only.  Per layer the rank calls
+ *            kv_tier_decode_attention_lse (o normalised by its own partial sum, plus its
+ *            (max, sum) per head), the caller combines the ranks' partials (o = sum_r w_r o_r
+ *            / sum_r w_r, w_r = 2^(m_r - M) l_r, M = max_r m_r: the LSE merge of Eq. 3 split
+ *            by position) and hands the global (M, L) back through kv_tier_score_update_lse,
+ *            which completes the fused score update with the exact global probabilities.
+ *            At an event: all-gather S_part, kv_tier_classify_gathered (sum over ranks is
+ *            exact: every position has one owner), migrate.  kv_tier_step / the step graph
+ *            and kv_tier_score_update are E_STATE (the exchange sits between the layers). */
 typedef enum { KV_TIER_SHARD_REQUEST = 0, KV_TIER_SHARD_KVHEAD = 1, KV_TIER_SHARD_SEQUENCE = 2 } kv_tier_shard;
 
 #define KV_TIER_STAGING_ALL 0xFFFFFFFFu   /* differential mode: staging holds all of T1 (§3.4) */
@@ -156,6 +168,22 @@ KV_TIER_API kv_tier_status kv_tier_prefetch(kv_tier_ctx* ctx, int32_t layer, voi
 KV_TIER_API kv_tier_status kv_tier_decode_attention(kv_tier_ctx* ctx, int32_t layer, const void* q,
                                                     const void* k_new, const void* v_new, void* o,
                                                     int32_t fuse_score_update, void* stream);
+
+/* a3 with the partial softmax statistics (sequence sharding; any mode): as
+ * kv_tier_decode_attention, but o is normalised by this ctx's own partial sum and lse
+ * (device fp32 [B][H_q][2]) receives (m, l) per head: m = max_i z_i in the log2 domain
+ * (z = q.k / sqrt(d) * log2(e)) and l = sum_i 2^(z_i - m) over this ctx's visible tokens.
+ * With fuse_score_update the score update of this launch waits for
+ * kv_tier_score_update_lse (E_STATE if another decode/end_step comes first). */
+KV_TIER_API kv_tier_status kv_tier_decode_attention_lse(kv_tier_ctx* ctx, int32_t layer, const void* q,
+                                                        const void* k_new, const void* v_new, void* o, float* lse,
+                                                        int32_t fuse_score_update, void* stream);
+
+/* Completes the pending fused score update of the last kv_tier_decode_attention_lse with the
+ * GLOBAL per-head (M, L) (device fp32 [B][H_q][2], same encoding; the combination of every
+ * rank's lse): S_part += sum_h 2^(z - M) / L over this ctx's tokens.  lse_global must stay
+ * valid until the update has run on `stream`. */
+KV_TIER_API kv_tier_status kv_tier_score_update_lse(kv_tier_ctx* ctx, const float* lse_global, void* stream);
 
 /* a4 standalone (external probabilities, e.g. from another attention kernel):
  * probs: device fp32 [B][H_q][n_vis] over the visible tokens in ascending position

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   // ---------------------------------------------------------------- prologue (pre-PDL-wait)
   const int cur = v.st->cur;
   Seg sg;
-  sg.init(v.cnt[cur] + b * CNT_STRIDE);
+  sg.init(v.cnt[cur] + b * CNT_STRIDE, v.st->nn);
   // This CTA's work: stages of up to NW 16-row groups (one per consumer warp) from the unit's
   // groups [bf16 segment [0, a2) | int8 segment [a2, a2 + n2)].  Default (KVTIER_RR=2): the
   // groups themselves are dealt round-robin over the unit's C CTAs (bf16 then int8, continuing
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     const int gs = cs0 + i * cstr;
     return (gs >= sbf ? gs - sbf : gs) * NW + wi;
   };
-  const bool has_new = r == 0;                               // rank 0 handles the new token
+  const bool has_new = r == 0 && sg.nn;                      // rank 0 handles the new token
 
   const int sb = v.st->scur;                                 // row-store buffer
   const size_t grp = grp_of(v, layer, b, g);
@@ -345,6 +345,10 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
           reinterpret_cast<float4*>(cluster.map_shared_rank(rbuf, c) + C * cm_rb)[j4] = val;
         }
       }
+    }
+    if (r == 0 && !sg.nn && !cm) {     // sequence shard without the new token: neutral partial C
+      float* part = v.part + ((size_t)unit * (C + 1) + C) * v.part_stride;
+      for (int e = lane; e < 16 + G * D; e += 32) part[e] = e < 8 ? -INFINITY : 0.f;
     }
     if (cm) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
     return;
@@ -716,7 +720,8 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
 // computed once (shared memory) in the same round trip, and o goes out as one vector store.
 template <int D>
 __global__ void __launch_bounds__(256) k_decode_merge(const DevView v, const int layer, void* __restrict__ o,
-                                                      const int zpar) {
+                                                      const int zpar, float* __restrict__ lse) {
+  // lse (optional) [B][Hq][2]: this ctx's (max, sum) per head, log2 domain (sequence sharding)
   constexpr int MAXP = 16, MAXNP = 65;
   __shared__ float sf[MAXNP * 8], sl[MAXNP * 8], sI[8];
   const int unit = blockIdx.x, tid = threadIdx.x;
@@ -749,9 +754,14 @@ __global__ void __launch_bounds__(256) k_decode_merge(const DevView v, const int
       sf[c * 8 + h] = f;
       Ls += f * sl[c * 8 + h];
     }
-    const float invL = 1.0f / Ls;
+    const float invL = Ls > 0.f ? 1.0f / Ls : 0.f;   // 0: a sequence shard with no visible token
     sI[h] = invL;
-    if (h < G && zpar >= 0) {          // publish (M, 1/L) for the deferred score pass
+    if (h < G && lse) {
+      lse[(((size_t)b * v.Hq + g * G + h) << 1)] = M;
+      lse[(((size_t)b * v.Hq + g * G + h) << 1) + 1] = Ls;
+    }
+    if (h < G && zpar >= 0 && !lse) {  // publish (M, 1/L) for the deferred score pass (with lse:
+                                       // the caller's global values, kv_tier_score_update_lse)
       float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
       ml[h] = M;
       ml[8 + h] = invL;
@@ -799,15 +809,44 @@ size_t merge_smem_bytes(const DevView& v) { (void)v; return 0; }
 __global__ void __launch_bounds__(256) k_score_flush(const DevView v, const int zfirst, const int nz) {
   const int cur = v.st->cur;
   Seg sg;
-  sg.init(v.cnt[cur]);          // counts are uniform across requests
+  sg.init(v.cnt[cur], v.st->nn);   // counts are uniform across requests
   const long long tot = (long long)v.B * v.Hkv * sg.nvirt;
   bool bad = false;
   score_range(v, sg, cur, zfirst, nz, 0, tot, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, bad);
   if (bad) atomicOr(&v.st->err, 1);
 }
 
+// Sequence shards: a shard's tier counts differ per request, so every unit decodes its own
+// virtual layout (one thread per (unit, virtual row) over the zrows-wide logit rows).
+__global__ void __launch_bounds__(256) k_score_flush_req(const DevView v, const int zfirst, const int nz) {
+  const int cur = v.st->cur, nn = v.st->nn;
+  const size_t zslot = (size_t)v.B * v.Hkv * v.zrows * 8, mslot = (size_t)v.B * v.Hkv * 16;
+  const long long tot = (long long)v.B * v.Hkv * v.zrows;
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+    const int u = (int)(i / v.zrows), t = (int)(i - (long long)u * v.zrows), b = u / v.Hkv;
+    Seg sg;
+    sg.init(v.cnt[cur] + b * CNT_STRIDE, nn);
+    if (t >= sg.nvirt || !sg.valid(t)) continue;
+    const int pos = sg.pos(v, cur, b, t);
+    float s = v.S[(size_t)u * v.Nmax + pos];
+    for (int j = 0; j < nz; ++j) {                 // launches in layer order
+      const int slot = (zfirst + j) % ZRING;
+      const float* z = v.zbuf + slot * zslot + ((size_t)u * v.zrows + t) * 8;
+      const float* ml = v.ml + slot * mslot + (size_t)u * 16;
+      float inc = 0.f;
+      for (int h = 0; h < v.G; ++h) inc += ex2_ftz(z[h] - ml[h]) * ml[8 + h];
+      s = s + inc;
+      bad |= !isfinite(inc);
+    }
+    v.S[(size_t)u * v.Nmax + pos] = s;
+  }
+  if (bad) atomicOr(&v.st->err, 1);
+}
+
 cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_t s) {
-  k_score_flush<<<148, 256, 0, s>>>(v, zfirst, nz);
+  if (v.seq_w > 1) k_score_flush_req<<<148, 256, 0, s>>>(v, zfirst, nz);
+  else k_score_flush<<<148, 256, 0, s>>>(v, zfirst, nz);
   return cudaGetLastError();
 }
 
@@ -909,7 +948,7 @@ static cudaError_t launch_decode_main(const DevView& v, int layer, const void* q
   return cudaErrorInvalidValue;
 }
 
-static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, int pdl, cudaStream_t s) {
+static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, int pdl, cudaStream_t s, float* lse) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(v.B * v.Hkv, 1, 1);
   cfg.blockDim = dim3(256, 1, 1);
@@ -933,15 +972,37 @@ static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, 
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  if (v.D == 128) return cudaLaunchKernelEx(&cfg, k_decode_merge<128>, v, layer, o, zpar);
-  return cudaLaunchKernelEx(&cfg, k_decode_merge<64>, v, layer, o, zpar);
+  if (v.D == 128) return cudaLaunchKernelEx(&cfg, k_decode_merge<128>, v, layer, o, zpar, lse);
+  return cudaLaunchKernelEx(&cfg, k_decode_merge<64>, v, layer, o, zpar, lse);
 }
 
 cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
-                               void* o, int zpar, int pdl, cudaStream_t s) {
+                               void* o, int zpar, int pdl, cudaStream_t s, float* lse) {
   cudaError_t e = launch_decode_main(v, layer, q, knew, vnew, o, zpar, pdl, s);
   if (e != cudaSuccess || v.cluster_merge) return e;
-  return launch_merge(v, layer, o, zpar, v.use_pdl, s);
+  return launch_merge(v, layer, o, zpar, v.use_pdl, s, lse);
+}
+
+// (M, 1/L) of every (unit, head) for score slot zslot from the caller's global (M, L)
+// [B][Hq][2] (sequence sharding: the ranks' partial sums combined, kv_tier_score_update_lse)
+__global__ void k_set_ml(const DevView v, const int zslot, const float* __restrict__ lse) {
+  const int unit = blockIdx.x, h = threadIdx.x;
+  const int b = unit / v.Hkv, g = unit - b * v.Hkv;
+  if (h >= 8) return;
+  float* ml = v.ml + ((size_t)zslot * v.B * v.Hkv + unit) * 16;
+  if (h < v.G) {
+    const size_t i = ((size_t)b * v.Hq + g * v.G + h) << 1;
+    ml[h] = lse[i];
+    ml[8 + h] = 1.0f / lse[i + 1];
+  } else {
+    ml[h] = -INFINITY;
+    ml[8 + h] = 0.f;
+  }
+}
+
+cudaError_t launch_set_ml(const DevView& v, int zslot, const float* lse, cudaStream_t s) {
+  k_set_ml<<<v.B * v.Hkv, 32, 0, s>>>(v, zslot, lse);
+  return cudaGetLastError();
 }
 
 }  // namespace kvt

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__((NW + 3) * 32, 1)
   pdl_trigger();                              // the next layer's grid may be scheduled now
   const int cur = v.st->cur;
   Seg sg;
-  sg.init(v.cnt[cur]);                        // counts are uniform across requests
+  sg.init(v.cnt[cur], v.st->nn);              // counts are uniform across requests
   Flat F;
   F.init(sg, v.B * v.Hkv, (int)gridDim.x);
   if ((uint32_t)c >= F.nce) return;

@@ -40,6 +40,7 @@ struct kv_tier_ctx {
   cudaStream_t score_stream = nullptr;     // a4 score updates run here, off the attention chain
   cudaEvent_t ev_merged[ZRING] = {}, ev_scored[ZRING] = {}, ev_score_tail = nullptr;
   bool slot_recorded[2] = {false, false};   // ev_slot_free[x] recorded within the open step
+  int lse_pending = -1;                    // score slot of a decode_attention_lse awaiting the global (M, L)
   int zflat_pending = -1;                  // flat kernel: slot whose score update the next launch applies
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -99,8 +100,8 @@ kv_tier_status validate(const kv_tier_config* c) {
   if (c->evict_mode != 0 && c->evict_mode != 1) return fail(nullptr, KV_TIER_E_INVAL, "bad evict_mode");
   if (c->staging_tokens != 0 && c->staging_tokens != KV_TIER_STAGING_ALL)
     return fail(nullptr, KV_TIER_E_INVAL, "staging_tokens must be 0 (stream) or KV_TIER_STAGING_ALL (differential)");
-  if (c->shard != KV_TIER_SHARD_REQUEST && c->shard != KV_TIER_SHARD_KVHEAD)
-    return fail(nullptr, KV_TIER_E_INVAL, "shard must be REQUEST or KVHEAD");
+  if (c->shard != KV_TIER_SHARD_REQUEST && c->shard != KV_TIER_SHARD_KVHEAD && c->shard != KV_TIER_SHARD_SEQUENCE)
+    return fail(nullptr, KV_TIER_E_INVAL, "shard must be REQUEST, KVHEAD or SEQUENCE");
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(nullptr, KV_TIER_E_INVAL, "need 0 <= rank < world");
   if (c->split < 0 || c->split > 64) return fail(nullptr, KV_TIER_E_INVAL, "split must be in [0, 64]");
   if (c->variant < 0 || c->variant > 5) return fail(nullptr, KV_TIER_E_INVAL, "variant must be in [0, 5]");
@@ -272,7 +273,8 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.use_pdl = getenv("KVTIER_NOPDL") ? 0 : 1;
   v.l2_prefetch = getenv("KVTIER_L2PF") ? atoi(getenv("KVTIER_L2PF")) : 0;   // measured: no gain at 7B
   v.stage_rr = getenv("KVTIER_RR") ? atoi(getenv("KVTIER_RR")) : 1;   // 2 (groups round-robin) measured slower
-  v.cluster_merge = (getenv("KVTIER_CLUSTER") && atoi(getenv("KVTIER_CLUSTER")) && v.split <= 8) ? 1 : 0;
+  v.cluster_merge = (getenv("KVTIER_CLUSTER") && atoi(getenv("KVTIER_CLUSTER")) && v.split <= 8 &&
+                     cfg->shard != KV_TIER_SHARD_SEQUENCE) ? 1 : 0;
   v.chunk_max = 0;
   {
     int nsm = 148;
@@ -282,6 +284,9 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     // default: 8 consumer warps, 3 x 64 KB stages (2 stages when the T2 scratch needs room)
     v.fvariant = getenv("KVTIER_FVAR") ? atoi(getenv("KVTIER_FVAR")) : (cfg->t2_fraction_bp > 0 ? 1 : 0);
     if (v.cluster_merge) v.flat = 0;
+    v.seq_w = cfg->shard == KV_TIER_SHARD_SEQUENCE ? cfg->world : 1;
+    v.seq_r = cfg->shard == KV_TIER_SHARD_SEQUENCE ? cfg->rank : 0;
+    if (v.seq_w > 1) v.flat = 0;            // sequence shards run the split kernel
     // the flat kernel's partition arithmetic is 32-bit: cost space (<= 3 per 16 rows per unit)
     // times the grid must fit
     const unsigned long long units = (unsigned long long)cfg->num_requests * cfg->num_kv_heads;
@@ -441,9 +446,9 @@ kv_tier_status kv_tier_load_prefix(kv_tier_ctx* ctx, int32_t layer, const void* 
     if (st) return st;
     ctx->n0 = n0;
     ctx->n = n0;
-    ctx->c[0] = n0; ctx->c[1] = ctx->c[2] = ctx->c[3] = 0;
+    ctx->c[0] = seq_owned_below(ctx->v.seq_w, ctx->v.seq_r, n0); ctx->c[1] = ctx->c[2] = ctx->c[3] = 0;
     ctx->n_event = n0;
-    ctx->nvis_event = n0;
+    ctx->nvis_event = ctx->c[0];
   }
   if (n0 > 0) {
     kv_tier_status st = cuda_check(ctx, launch_load_prefix(ctx->v, layer, k, v, n0, s), "load_prefix");
@@ -466,8 +471,8 @@ kv_tier_status kv_tier_begin_step(kv_tier_ctx* ctx, void* stream) {
   if (st) return st;
   st = cuda_check(ctx, cudaEventRecord(ctx->ev_step_begin, s), "event");
   if (st) return st;
+  ctx->c[0] += seq_own(ctx->v.seq_w, ctx->v.seq_r, ctx->n) ? 1 : 0;
   ctx->n += 1;
-  ctx->c[0] += 1;
   ctx->step_open = true;
   ctx->classified = false;
   ctx->slot_recorded[0] = ctx->slot_recorded[1] = false;
@@ -524,8 +529,13 @@ static cudaError_t issue_scores(kv_tier_ctx* ctx, cudaStream_t s) {
 
 static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, const void* q, const void* k_new,
                                             const void* v_new, void* o, int32_t fuse_score_update, void* stream,
-                                            int pdl) {
+                                            int pdl, float* lse = nullptr) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (ctx->v.seq_w > 1 && !lse)
+    return fail(ctx, KV_TIER_E_STATE, "sequence shard: use kv_tier_decode_attention_lse (partial softmax statistics)");
+  if (ctx->lse_pending >= 0)
+    return fail(ctx, KV_TIER_E_STATE, "the previous decode_attention_lse still waits for kv_tier_score_update_lse");
+  if (lse && ((uintptr_t)lse & 7)) return fail(ctx, KV_TIER_E_INVAL, "lse must be 8-B aligned");
   if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
   if (!q || !o) return fail(ctx, KV_TIER_E_INVAL, "null q/o");
   if ((k_new == nullptr) != (v_new == nullptr)) return fail(ctx, KV_TIER_E_INVAL, "k_new and v_new go together");
@@ -568,7 +578,13 @@ static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, con
   // the ring slot's previous score kernel must be done before its logits are overwritten
   if (e == cudaSuccess && zpar >= 0 && ctx->slot_busy[zpar])
     e = cudaStreamWaitEvent(s, ctx->ev_scored[zpar - zpar % ZBATCH], 0);
-  if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, zpar, pdl, s);
+  if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, zpar, pdl, s, lse);
+  if (e == cudaSuccess && zpar >= 0 && lse) {   // the update waits for the global (M, L)
+    ctx->lse_pending = zpar;
+    ctx->zslot_next = (zpar + 1) % ZRING;
+    if (k_new) ctx->appended_step[layer] = ctx->t;
+    return cuda_check(ctx, e, "decode_attention_lse");
+  }
   if (e == cudaSuccess && zpar >= 0) e = cudaEventRecord(ctx->ev_merged[zpar], s);
   if (e == cudaSuccess && zpar >= 0) {
     if (ctx->zpend_n == 0) ctx->zpend_first = zpar;
@@ -589,15 +605,43 @@ kv_tier_status kv_tier_decode_attention(kv_tier_ctx* ctx, int32_t layer, const v
   return decode_attention_impl(ctx, layer, q, k_new, v_new, o, fuse_score_update, stream, 0);
 }
 
+kv_tier_status kv_tier_decode_attention_lse(kv_tier_ctx* ctx, int32_t layer, const void* q, const void* k_new,
+                                            const void* v_new, void* o, float* lse, int32_t fuse_score_update,
+                                            void* stream) {
+  if (!lse) return fail(ctx, KV_TIER_E_INVAL, "null lse");
+  if (ctx && ctx->v.flat) return fail(ctx, KV_TIER_E_STATE, "decode_attention_lse runs the split kernel (KVTIER_FLAT=0)");
+  if (ctx && ctx->v.cluster_merge) return fail(ctx, KV_TIER_E_STATE, "decode_attention_lse needs the merge kernel (KVTIER_CLUSTER=0)");
+  return decode_attention_impl(ctx, layer, q, k_new, v_new, o, fuse_score_update, stream, 0, lse);
+}
+
+kv_tier_status kv_tier_score_update_lse(kv_tier_ctx* ctx, const float* lse_global, void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!lse_global || ((uintptr_t)lse_global & 7)) return fail(ctx, KV_TIER_E_INVAL, "lse_global must be an 8-B aligned device pointer");
+  if (ctx->lse_pending < 0) return fail(ctx, KV_TIER_E_STATE, "no decode_attention_lse awaits its score update");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int z = ctx->lse_pending;
+  cudaError_t e = launch_set_ml(ctx->v, z, lse_global, s);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_merged[z], s);
+  if (e == cudaSuccess) {
+    if (ctx->zpend_n == 0) ctx->zpend_first = z;
+    ctx->zpend_n += 1;
+    if (ctx->zpend_n == ZBATCH) e = issue_scores(ctx, s);
+  }
+  if (e == cudaSuccess) ctx->lse_pending = -1;
+  return cuda_check(ctx, e, "score_update_lse");
+}
+
 kv_tier_status kv_tier_visible_count(const kv_tier_ctx* ctx, int32_t* n_vis) {
   if (!ctx || !n_vis) return fail(nullptr, KV_TIER_E_INVAL, "null arg");
-  *n_vis = ctx->nvis_event + (ctx->n - ctx->n_event);
+  *n_vis = ctx->nvis_event + seq_owned_below(ctx->v.seq_w, ctx->v.seq_r, ctx->n) -
+           seq_owned_below(ctx->v.seq_w, ctx->v.seq_r, ctx->n_event);
   return KV_TIER_OK;
 }
 
 kv_tier_status kv_tier_score_update(kv_tier_ctx* ctx, int32_t layer, const float* probs, void* stream) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (!probs) return fail(ctx, KV_TIER_E_INVAL, "null probs");
+  if (ctx->v.seq_w > 1) return fail(ctx, KV_TIER_E_STATE, "standalone score update is not defined for sequence shards");
   if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
@@ -612,6 +656,7 @@ kv_tier_status kv_tier_score_update(kv_tier_ctx* ctx, int32_t layer, const float
 kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (!ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "end_step without begin_step");
+  if (ctx->lse_pending >= 0) return fail(ctx, KV_TIER_E_STATE, "end_step before kv_tier_score_update_lse");
   cudaError_t e = cudaSuccess;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (ctx->zflat_pending >= 0) {           // flat kernel: the last fused launch's score update
@@ -639,7 +684,7 @@ static kv_tier_status classify_impl(kv_tier_ctx* ctx, const float* Sx, int parts
 
 kv_tier_status kv_tier_classify(kv_tier_ctx* ctx, void* stream) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
-  if (ctx->cfg.shard == KV_TIER_SHARD_KVHEAD && ctx->cfg.world > 1)
+  if ((ctx->cfg.shard == KV_TIER_SHARD_KVHEAD || ctx->cfg.shard == KV_TIER_SHARD_SEQUENCE) && ctx->cfg.world > 1)
     return fail(ctx, KV_TIER_E_STATE, "KV-head sharding: classify needs every shard's scores (kv_tier_classify_gathered)");
   return classify_impl(ctx, nullptr, 1, stream);
 }
@@ -706,6 +751,16 @@ kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side) 
   ctx->cur ^= 1;
   ctx->n_event = ctx->n;
   ctx->nvis_event = ctx->n - ctx->c[3];
+  if (ctx->v.seq_w > 1) {                  // a shard's own counts are decided on the device
+    int cn[CNT_STRIDE];
+    e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaMemcpy(cn, ctx->v.cnt[ctx->cur], sizeof(cn), cudaMemcpyDeviceToHost);
+    st = cuda_check(ctx, e, "migrate (sequence shard counts)");
+    if (st) return st;
+    for (int i = 0; i < 3; ++i) ctx->c[i] = cn[i];
+    ctx->c[3] = seq_owned_below(ctx->v.seq_w, ctx->v.seq_r, ctx->n) - cn[4];
+    ctx->nvis_event = cn[4];
+  }
   ctx->classified = false;
   return KV_TIER_OK;
 }
@@ -713,6 +768,7 @@ kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side) 
 kv_tier_status kv_tier_step(kv_tier_ctx* ctx, const void* q, const void* k_new, const void* v_new, void* o,
                             int32_t fuse_score_update, void* stream, void* side) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (ctx->v.seq_w > 1) return fail(ctx, KV_TIER_E_STATE, "sequence shards combine every layer: drive decode_attention_lse per layer");
   if (!q || !k_new || !v_new || !o) return fail(ctx, KV_TIER_E_INVAL, "null step buffer");
   const DevView& v = ctx->v;
   const size_t qs = (size_t)v.B * v.Hq * v.D, ks = (size_t)v.B * v.Hkv * v.D;
@@ -785,8 +841,8 @@ kv_tier_status kv_tier_step_graph_launch(kv_tier_ctx* ctx, void* stream) {
   if (e == cudaSuccess) e = cudaGraphLaunch(ctx->graph_exec, s);
   kv_tier_status st = cuda_check(ctx, e, "graph launch");
   if (st) return st;
+  ctx->c[0] += seq_own(ctx->v.seq_w, ctx->v.seq_r, ctx->n) ? 1 : 0;
   ctx->n += 1;
-  ctx->c[0] += 1;
   ctx->t += 1;
   ctx->classified = false;
   return KV_TIER_OK;
@@ -815,7 +871,8 @@ kv_tier_status kv_tier_census(kv_tier_ctx* ctx, int32_t* counts, int64_t* d2h_ro
     for (int b = 0; b < ctx->v.B; ++b) {
       // counts over [0, n): T3 is n - |visible| (positions appended since the event are T0)
       for (int i = 0; i < 3; ++i) counts[b * 4 + i] = cn[b * CNT_STRIDE + i];
-      counts[b * 4 + 3] = ctx->n - cn[b * CNT_STRIDE + 0] - cn[b * CNT_STRIDE + 1] - cn[b * CNT_STRIDE + 2];
+      counts[b * 4 + 3] = seq_owned_below(ctx->v.seq_w, ctx->v.seq_r, ctx->n) - cn[b * CNT_STRIDE + 0] -
+                          cn[b * CNT_STRIDE + 1] - cn[b * CNT_STRIDE + 2];
     }
   }
   if (d2h_rows) {
@@ -833,22 +890,50 @@ kv_tier_status kv_tier_position(const kv_tier_ctx* ctx, int32_t* n, int32_t* t) 
   return KV_TIER_OK;
 }
 
+// Per-request tier counts |T0| |T1| |T2| of the live buffer (uniform across requests except
+// under sequence sharding, where a shard's own counts depend on the request's tiers).
+static kv_tier_status req_counts(kv_tier_ctx* ctx, std::vector<int>& cb) {
+  kv_tier_status st = kv_tier_sync(ctx);
+  if (st) return st;
+  std::vector<int> cn((size_t)ctx->v.B * CNT_STRIDE);
+  cudaError_t e = cudaMemcpy(cn.data(), ctx->v.cnt[ctx->cur], cn.size() * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_check(ctx, e, "export counts");
+  cb.assign((size_t)ctx->v.B * 3, 0);
+  for (int b = 0; b < ctx->v.B; ++b)
+    for (int T = 0; T < 3; ++T) cb[(size_t)b * 3 + T] = cn[(size_t)b * CNT_STRIDE + T];
+  return KV_TIER_OK;
+}
+
+// Bytes of one request's export `what` given its counts c[3].
+static size_t export_bytes_req(const kv_tier_ctx* ctx, int32_t what, const int* c) {
+  const size_t H = ctx->v.Hkv, D = ctx->v.D, n = ctx->n;
+  switch (what) {
+    case KV_TIER_X_SCORES: return H * n * 4;
+    case KV_TIER_X_TIERS: return n;
+    case KV_TIER_X_IDX_T0: return (size_t)c[0] * 4;
+    case KV_TIER_X_IDX_T1: return (size_t)c[1] * 4;
+    case KV_TIER_X_IDX_T2: return (size_t)c[2] * 4;
+    case KV_TIER_X_T0_ROWS: return H * c[0] * 2 * D * 2;
+    case KV_TIER_X_T1_ROWS: case KV_TIER_X_STAGING: return H * c[1] * 2 * D * 2;
+    case KV_TIER_X_T2_CODES: return H * c[2] * 2 * D;
+    case KV_TIER_X_T2_SCALES: return H * c[2] * 2 * 4;
+    default: return (size_t)-1;
+  }
+}
+
 kv_tier_status kv_tier_export_size(kv_tier_ctx* ctx, int32_t what, size_t* bytes) {
   if (!ctx || !bytes) return fail(nullptr, KV_TIER_E_INVAL, "null arg");
-  const size_t B = ctx->v.B, H = ctx->v.Hkv, D = ctx->v.D, n = ctx->n;
-  const size_t c0 = ctx->c[0], c1 = ctx->c[1], c2 = ctx->c[2];
-  switch (what) {
-    case KV_TIER_X_SCORES: *bytes = B * H * n * 4; break;
-    case KV_TIER_X_TIERS: *bytes = B * n; break;
-    case KV_TIER_X_IDX_T0: *bytes = B * c0 * 4; break;
-    case KV_TIER_X_IDX_T1: *bytes = B * c1 * 4; break;
-    case KV_TIER_X_IDX_T2: *bytes = B * c2 * 4; break;
-    case KV_TIER_X_T0_ROWS: *bytes = B * H * c0 * 2 * D * 2; break;
-    case KV_TIER_X_T1_ROWS: case KV_TIER_X_STAGING: *bytes = B * H * c1 * 2 * D * 2; break;
-    case KV_TIER_X_T2_CODES: *bytes = B * H * c2 * 2 * D; break;
-    case KV_TIER_X_T2_SCALES: *bytes = B * H * c2 * 2 * 4; break;
-    default: return fail(ctx, KV_TIER_E_INVAL, "unknown export %d", what);
+  if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "export inside a step");
+  std::vector<int> cb;
+  kv_tier_status st = req_counts(ctx, cb);
+  if (st) return st;
+  size_t tot = 0;
+  for (int b = 0; b < ctx->v.B; ++b) {
+    const size_t x = export_bytes_req(ctx, what, &cb[(size_t)b * 3]);
+    if (x == (size_t)-1) return fail(ctx, KV_TIER_E_INVAL, "unknown export %d", what);
+    tot += x;
   }
+  *bytes = tot;
   return KV_TIER_OK;
 }
 
@@ -858,8 +943,8 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
   if (st) return st;
   if (!host_dst || bytes != need) return fail(ctx, KV_TIER_E_INVAL, "export %d needs %zu bytes, got %zu", what, need, bytes);
   if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
-  if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "export inside a step");
-  st = kv_tier_sync(ctx);
+  std::vector<int> cb;
+  st = req_counts(ctx, cb);                 // (synchronised)
   if (st) return st;
   const DevView& v = ctx->v;
   const int cur = ctx->cur;
@@ -872,45 +957,47 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
   auto d2h = [&](void* dst, const void* src, size_t nbytes) {
     return cudaMemcpy(dst, src, nbytes, cudaMemcpyDeviceToHost);
   };
-  const int cnts[3] = {ctx->c[0], ctx->c[1], ctx->c[2]};
   const int caps[3] = {v.cap0, v.cap1, v.cap2};
   // store-order index list of tier T for request b and the permutation to ascending positions
   auto order = [&](int T, size_t b, std::vector<int>& pos, std::vector<int>& perm) {
-    pos.assign((size_t)std::max(cnts[T], 1), 0);
-    cudaError_t ee = d2h(pos.data(), v.idx[cur][T] + b * caps[T], (size_t)cnts[T] * 4);
-    perm.resize(cnts[T]);
-    for (int j = 0; j < cnts[T]; ++j) perm[j] = j;
+    const int cnt = cb[b * 3 + T];
+    pos.assign((size_t)std::max(cnt, 1), 0);
+    cudaError_t ee = d2h(pos.data(), v.idx[cur][T] + b * caps[T], (size_t)cnt * 4);
+    perm.resize(cnt);
+    for (int j = 0; j < cnt; ++j) perm[j] = j;
     std::sort(perm.begin(), perm.end(), [&](int x, int y) { return pos[x] < pos[y]; });
     return ee;
   };
   std::vector<int> pos, perm;
-  if (what == KV_TIER_X_SCORES) {
-    for (size_t bg = 0; bg < B * H && e == cudaSuccess; ++bg) e = d2h(out + bg * n * 4, v.S + bg * N, n * 4);
-  } else if (what == KV_TIER_X_TIERS) {
-    for (size_t b = 0; b < B && e == cudaSuccess; ++b) e = d2h(out + b * n, v.tier[cur] + b * N, n);
-  } else if (what >= KV_TIER_X_IDX_T0 && what <= KV_TIER_X_IDX_T2) {
-    const int T = what - KV_TIER_X_IDX_T0;
-    for (size_t b = 0; b < B && e == cudaSuccess; ++b) {
+  size_t off = 0;                      // this request's byte offset in host_dst
+  for (size_t b = 0; b < B && e == cudaSuccess; ++b) {
+    const int* c = &cb[b * 3];
+    char* ob = out + off;
+    off += export_bytes_req(ctx, what, c);
+    if (what == KV_TIER_X_SCORES) {
+      for (size_t g = 0; g < H && e == cudaSuccess; ++g) e = d2h(ob + g * n * 4, v.S + (b * H + g) * N, n * 4);
+    } else if (what == KV_TIER_X_TIERS) {
+      e = d2h(ob, v.tier[cur] + b * N, n);
+    } else if (what >= KV_TIER_X_IDX_T0 && what <= KV_TIER_X_IDX_T2) {
+      const int T = what - KV_TIER_X_IDX_T0;
       e = order(T, b, pos, perm);
-      int* o32 = reinterpret_cast<int*>(out) + b * cnts[T];
-      for (int j = 0; j < cnts[T]; ++j) o32[j] = pos[perm[j]];
-    }
-  } else if (what == KV_TIER_X_T0_ROWS || what == KV_TIER_X_STAGING) {
-    const bool t0 = what == KV_TIER_X_T0_ROWS;
-    if (!t0 && v.stream_mode) return fail(ctx, KV_TIER_E_STATE, "no persistent staging in stream mode");
-    const int T = t0 ? 0 : 1;
-    const int cnt = cnts[T];
-    const int cap = caps[T];
-    const __nv_bfloat16* Ks = t0 ? v.k0[sb] : v.k1[sb];
-    const __nv_bfloat16* Vs = t0 ? v.v0[sb] : v.v1[sb];
-    std::vector<uint16_t> tk((size_t)cnt * D), tv((size_t)cnt * D);
-    for (size_t b = 0; b < B && e == cudaSuccess; ++b) {
+      int* o32 = reinterpret_cast<int*>(ob);
+      for (int j = 0; j < c[T]; ++j) o32[j] = pos[perm[j]];
+    } else if (what == KV_TIER_X_T0_ROWS || what == KV_TIER_X_STAGING) {
+      const bool t0 = what == KV_TIER_X_T0_ROWS;
+      if (!t0 && v.stream_mode) return fail(ctx, KV_TIER_E_STATE, "no persistent staging in stream mode");
+      const int T = t0 ? 0 : 1;
+      const int cnt = c[T];
+      const int cap = caps[T];
+      const __nv_bfloat16* Ks = t0 ? v.k0[sb] : v.k1[sb];
+      const __nv_bfloat16* Vs = t0 ? v.v0[sb] : v.v1[sb];
+      std::vector<uint16_t> tk((size_t)cnt * D), tv((size_t)cnt * D);
       e = order(T, b, pos, perm);
       for (size_t g = 0; g < H && e == cudaSuccess; ++g) {
         const size_t grp = ((size_t)layer * B + b) * H + g;
         e = d2h(tk.data(), Ks + grp * cap * D, tk.size() * 2);
         if (e == cudaSuccess) e = d2h(tv.data(), Vs + grp * cap * D, tv.size() * 2);
-        uint16_t* o16 = reinterpret_cast<uint16_t*>(out) + ((b * H + g) * cnt) * 2 * D;
+        uint16_t* o16 = reinterpret_cast<uint16_t*>(ob) + (g * cnt) * 2 * D;
         for (int jj = 0; jj < cnt; ++jj) {
           const int j = perm[jj];
           for (size_t el = 0; el < D; ++el) {     // undo the store swizzle
@@ -919,38 +1006,34 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
           }
         }
       }
-    }
-  } else if (what == KV_TIER_X_T1_ROWS) {
-    const int cnt = cnts[1];
-    const size_t rows = (size_t)v.L * B * H * N;
-    const uint16_t* hk = reinterpret_cast<const uint16_t*>(ctx->host_t1);
-    const uint16_t* hv = hk ? hk + rows * D : nullptr;
-    if (cnt > 0 && !hk) return fail(ctx, KV_TIER_E_STATE, "no host T1 store");
-    for (size_t b = 0; b < B && e == cudaSuccess; ++b) {
+    } else if (what == KV_TIER_X_T1_ROWS) {
+      const int cnt = c[1];
+      const size_t rows = (size_t)v.L * B * H * N;
+      const uint16_t* hk = reinterpret_cast<const uint16_t*>(ctx->host_t1);
+      const uint16_t* hv = hk ? hk + rows * D : nullptr;
+      if (cnt > 0 && !hk) return fail(ctx, KV_TIER_E_STATE, "no host T1 store");
       e = order(1, b, pos, perm);
       for (size_t g = 0; g < H && e == cudaSuccess; ++g) {
         const size_t grp = ((size_t)layer * B + b) * H + g;
-        uint16_t* o16 = reinterpret_cast<uint16_t*>(out) + ((b * H + g) * cnt) * 2 * D;
+        uint16_t* o16 = reinterpret_cast<uint16_t*>(ob) + (g * cnt) * 2 * D;
         for (int jj = 0; jj < cnt; ++jj) {
           const int p = pos[perm[jj]];
           memcpy(o16 + (size_t)jj * 2 * D, hk + (grp * N + p) * D, D * 2);
           memcpy(o16 + (size_t)jj * 2 * D + D, hv + (grp * N + p) * D, D * 2);
         }
       }
-    }
-  } else if (what == KV_TIER_X_T2_CODES || what == KV_TIER_X_T2_SCALES) {
-    const int cnt = cnts[2];
-    const bool codes = what == KV_TIER_X_T2_CODES;
-    std::vector<int8_t> ck((size_t)cnt * D + 1), cv((size_t)cnt * D + 1);
-    std::vector<float> sk((size_t)cnt + 1), sv((size_t)cnt + 1);
-    for (size_t b = 0; b < B && e == cudaSuccess; ++b) {
+    } else if (what == KV_TIER_X_T2_CODES || what == KV_TIER_X_T2_SCALES) {
+      const int cnt = c[2];
+      const bool codes = what == KV_TIER_X_T2_CODES;
+      std::vector<int8_t> ck((size_t)cnt * D + 1), cv((size_t)cnt * D + 1);
+      std::vector<float> sk((size_t)cnt + 1), sv((size_t)cnt + 1);
       e = order(2, b, pos, perm);
       for (size_t g = 0; g < H && e == cudaSuccess; ++g) {
         const size_t grp = ((size_t)layer * B + b) * H + g;
         if (codes) {
           e = d2h(ck.data(), v.c2k[sb] + grp * v.cap2 * D, (size_t)cnt * D);
           if (e == cudaSuccess) e = d2h(cv.data(), v.c2v[sb] + grp * v.cap2 * D, (size_t)cnt * D);
-          int8_t* o8 = reinterpret_cast<int8_t*>(out) + ((b * H + g) * cnt) * 2 * D;
+          int8_t* o8 = reinterpret_cast<int8_t*>(ob) + (g * cnt) * 2 * D;
           for (int jj = 0; jj < cnt; ++jj) {
             memcpy(o8 + (size_t)jj * 2 * D, ck.data() + (size_t)perm[jj] * D, D);
             memcpy(o8 + (size_t)jj * 2 * D + D, cv.data() + (size_t)perm[jj] * D, D);
@@ -958,7 +1041,7 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
         } else {
           e = d2h(sk.data(), v.s2k[sb] + grp * v.cap2, (size_t)cnt * 4);
           if (e == cudaSuccess) e = d2h(sv.data(), v.s2v[sb] + grp * v.cap2, (size_t)cnt * 4);
-          float* of = reinterpret_cast<float*>(out) + ((b * H + g) * cnt) * 2;
+          float* of = reinterpret_cast<float*>(ob) + (g * cnt) * 2;
           for (int jj = 0; jj < cnt; ++jj) { of[2 * jj] = sk[perm[jj]]; of[2 * jj + 1] = sv[perm[jj]]; }
         }
       }

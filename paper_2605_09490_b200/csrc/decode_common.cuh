@@ -132,9 +132,11 @@ __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w &
 
 // Virtual-token bookkeeping shared by the decode kernel and the score pass.
 struct Seg {
-  int n0o, n1, n2, a1, a2, a3, nvirt;
-  __device__ __forceinline__ void init(const int* cn) {
-    n0o = cn[0] - 1;
+  int n0o, n1, n2, a1, a2, a3, nvirt, nn;
+  // nn: the step's new token is the last T0 row of this ctx (DevState::nn)
+  __device__ __forceinline__ void init(const int* cn, int nn_ = 1) {
+    nn = nn_;
+    n0o = cn[0] - nn;
     n1 = cn[1];
     n2 = cn[2];
     a1 = ru16(n0o);
@@ -144,7 +146,7 @@ struct Seg {
   }
   __device__ __forceinline__ bool bf16_valid(int t) const { return t < n0o || (t >= a1 && t < a1 + n1); }
   __device__ __forceinline__ bool valid(int t) const {
-    return t < n0o || (t >= a1 && t < a1 + n1) || (t >= a2 && t < a2 + n2) || t == a3;
+    return t < n0o || (t >= a1 && t < a1 + n1) || (t >= a2 && t < a2 + n2) || (nn && t == a3);
   }
   // position of virtual token t (valid t only)
   __device__ __forceinline__ int pos(const DevView& v, int cur, int b, int t) const {

@@ -24,6 +24,7 @@ struct DevState {
   int use_full;     // set by the migrate plan when the move list overflows -> full rebuild
   int last_full;    // use_full of the last committed migrate (read by the offload kernels)
   unsigned long long d2h_rows;   // rows written to the pinned host stores
+  int nn;           // 1: this rank holds the step's new token (always 1 unless sequence-sharded)
 };
 
 struct DevView {
@@ -44,6 +45,7 @@ struct DevView {
   int flat;             // flat decode kernel (attn_flat.cu; default) instead of split-per-unit
   int fvariant;         // flat kernel variant (consumer warps x stages)
   int nc;               // flat kernel grid (CTAs; one per SM)
+  int seq_w, seq_r;     // sequence sharding: positions in 64-blocks, block k owned by rank k % seq_w
   int spin_hint;        // mbarrier try_wait suspend-time hint in ns (0: plain polling)
   long long l2pf_bytes; // flat kernel: K/V bytes per CTA requested into L2 at kernel start (0: off)
   int inflight;         // flat kernel: max ring stages requested but not landed (0: the whole ring)
@@ -77,6 +79,27 @@ struct DevView {
   int8_t* hc2k; int8_t* hc2v; float* hs2k; float* hs2v;   // pinned host T2 (mapped, may be null)
 };
 
+// Sequence sharding: block-cyclic ownership of SEQ_BLOCK-position blocks.
+// A rank's tier stores and index lists hold only its own positions; the tier array and the
+// scores cover every position (tiers are identical on every rank).
+constexpr int SEQ_BLOCK = 64;
+__host__ __device__ __forceinline__ bool seq_own(int seq_w, int seq_r, int pos) {
+  return seq_w <= 1 || (pos / SEQ_BLOCK) % seq_w == seq_r;
+}
+// owned positions below n
+__host__ __device__ __forceinline__ int seq_owned_below(int seq_w, int seq_r, int n) {
+  if (seq_w <= 1) return n;
+  const int full = n / SEQ_BLOCK, rem = n % SEQ_BLOCK;
+  int c = (full / seq_w) * SEQ_BLOCK + (full % seq_w > seq_r ? SEQ_BLOCK : 0);
+  if (full % seq_w == seq_r) c += rem;
+  return c;
+}
+// position of the j-th owned position (ascending)
+__host__ __device__ __forceinline__ int seq_pos_of(int seq_w, int seq_r, int j) {
+  if (seq_w <= 1) return j;
+  return ((j / SEQ_BLOCK) * seq_w + seq_r) * SEQ_BLOCK + j % SEQ_BLOCK;
+}
+
 __device__ __forceinline__ size_t grp_of(const DevView& v, int l, int b, int g) {
   return ((size_t)l * v.B + b) * v.Hkv + g;
 }
@@ -107,7 +130,8 @@ cudaError_t launch_append(const DevView& v, int layer, const void* k, const void
 cudaError_t launch_load_prefix(const DevView& v, int layer, const void* k, const void* vv, int n0, cudaStream_t s);
 cudaError_t launch_init_meta(const DevView& v, int n0, cudaStream_t s);
 cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
-                               void* o, int zpar, int pdl, cudaStream_t s);
+                               void* o, int zpar, int pdl, cudaStream_t s, float* lse = nullptr);
+cudaError_t launch_set_ml(const DevView& v, int zslot, const float* lse, cudaStream_t s);
 cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_t s);
 cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s);
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);

@@ -9,20 +9,29 @@ namespace kvt {
 // ------------------------------------------------------------------ step bookkeeping
 // New position n joins T0 at the end of the T0 list (ascending order is kept since
 // n exceeds every stored position); it is inside the window, hence protected.
+// Sequence sharding: only the rank owning position n stores it; every rank marks it T0.
 __global__ void k_begin_step(const DevView v) {
   const int b = threadIdx.x;
   const int cur = v.st->cur;
   const int n = v.st->n;
+  const bool own = seq_own(v.seq_w, v.seq_r, n);
   if (b < v.B) {
     int* cn = v.cnt[cur] + b * CNT_STRIDE;
-    const int r = cn[0];
-    v.idx[cur][0][(size_t)b * v.cap0 + r] = n;
     v.tier[cur][(size_t)b * v.Nmax + n] = T0;
-    v.rowof[cur][(size_t)b * v.Nmax + n] = r;
-    cn[0] = r + 1;
+    if (own) {
+      const int r = cn[0];
+      v.idx[cur][0][(size_t)b * v.cap0 + r] = n;
+      v.rowof[cur][(size_t)b * v.Nmax + n] = r;
+      cn[0] = r + 1;
+    } else {
+      v.rowof[cur][(size_t)b * v.Nmax + n] = -1;
+    }
   }
   __syncthreads();
-  if (threadIdx.x == 0) v.st->n = n + 1;
+  if (threadIdx.x == 0) {
+    v.st->n = n + 1;
+    v.st->nn = own ? 1 : 0;
+  }
 }
 
 __global__ void k_end_step(const DevView v) {
@@ -35,6 +44,7 @@ __global__ void k_append(const DevView v, const int layer, const uint16_t* __res
   const int unit = blockIdx.x;               // b * Hkv + g
   const int b = unit / v.Hkv, g = unit % v.Hkv;
   const int cur = v.st->cur;
+  if (!v.st->nn) return;                     // another sequence shard holds the new token
   const int row = v.cnt[cur][b * CNT_STRIDE + 0] - 1;
   const size_t dst = (grp_of(v, layer, b, g) * v.cap0 + row) * v.D;
   const int sb = v.st->scur;
@@ -46,7 +56,8 @@ __global__ void k_append(const DevView v, const int layer, const uint16_t* __res
   }
 }
 
-// Prefill rows [0, n0) of one layer into T0 (Alg. 1).
+// Prefill rows [0, n0) of one layer into T0 (Alg. 1); a sequence shard keeps its own
+// positions only (store row j = its j-th owned position).
 __global__ void k_load_prefix(const DevView v, const int layer, const uint16_t* __restrict__ k,
                               const uint16_t* __restrict__ vv, const int n0) {
   const int unit = blockIdx.y;
@@ -54,33 +65,38 @@ __global__ void k_load_prefix(const DevView v, const int layer, const uint16_t* 
   const size_t base = grp_of(v, layer, b, g) * v.cap0 * v.D;
   uint16_t* K = reinterpret_cast<uint16_t*>(v.k0[0]);
   uint16_t* V = reinterpret_cast<uint16_t*>(v.v0[0]);
-  const size_t tot = (size_t)n0 * v.D;
+  const size_t tot = (size_t)seq_owned_below(v.seq_w, v.seq_r, n0) * v.D;
+  const size_t in_tot = (size_t)n0 * v.D;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
     const int j = (int)(e / v.D), el = (int)(e % v.D);
+    const int p = seq_pos_of(v.seq_w, v.seq_r, j);
     const size_t dst = base + (size_t)j * v.D + swz_off(j, el);
-    K[dst] = k[(size_t)unit * tot + e];
-    V[dst] = vv[(size_t)unit * tot + e];
+    K[dst] = k[(size_t)unit * in_tot + (size_t)p * v.D + el];
+    V[dst] = vv[(size_t)unit * in_tot + (size_t)p * v.D + el];
   }
 }
 
 // All n0 prefix tokens in T0 with S = 0 (Alg. 1).
 __global__ void k_init_meta(const DevView v, const int n0) {
   const int b = blockIdx.y;
+  const int n0own = seq_owned_below(v.seq_w, v.seq_r, n0);
   for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < v.Nmax; pos += gridDim.x * blockDim.x) {
+    const bool own = seq_own(v.seq_w, v.seq_r, pos);
+    const int j = seq_owned_below(v.seq_w, v.seq_r, pos);      // owned index of pos (if owned)
     for (int buf = 0; buf < 2; ++buf) {
       v.tier[buf][(size_t)b * v.Nmax + pos] = pos < n0 ? T0 : T3;
-      v.rowof[buf][(size_t)b * v.Nmax + pos] = pos < n0 ? pos : -1;
-      v.idxvis[buf][(size_t)b * v.Nmax + pos] = pos;
+      v.rowof[buf][(size_t)b * v.Nmax + pos] = pos < n0 && own ? j : -1;
+      v.idxvis[buf][(size_t)b * v.Nmax + pos] = seq_pos_of(v.seq_w, v.seq_r, pos);
     }
-    if (pos < n0) v.idx[0][0][(size_t)b * v.cap0 + pos] = pos;
+    if (pos < n0 && own) v.idx[0][0][(size_t)b * v.cap0 + j] = pos;
     for (int g = 0; g < v.Hkv; ++g) v.S[((size_t)b * v.Hkv + g) * v.Nmax + pos] = 0.f;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int buf = 0; buf < 2; ++buf) {
       int* cn = v.cnt[buf] + b * CNT_STRIDE;
-      cn[0] = buf == 0 ? n0 : 0;
+      cn[0] = buf == 0 ? n0own : 0;
       cn[1] = cn[2] = cn[3] = 0;
-      cn[4] = buf == 0 ? n0 : 0;
+      cn[4] = buf == 0 ? n0own : 0;
       cn[5] = cn[6] = cn[7] = 0;
     }
     if (b == 0) {
@@ -93,6 +109,7 @@ __global__ void k_init_meta(const DevView v, const int n0) {
       v.st->use_full = 0;
       v.st->last_full = 0;
       v.st->d2h_rows = 0ull;
+      v.st->nn = 1;
     }
   }
 }
@@ -253,12 +270,13 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
         t = key < thr_e ? T3 : key < thr_2 ? T2 : key < thr_1 ? T1 : T0;
       }
       tnew[pos] = (uint8_t)t;
-      if (t == T3) rnew[pos] = -1;
+      if (t == T3 || !seq_own(v.seq_w, v.seq_r, pos)) rnew[pos] = -1;
     }
+    const bool own = pos < n && seq_own(v.seq_w, v.seq_r, pos);   // lists hold own positions only
     unsigned m[4];
 #pragma unroll
     for (int L4 = 0; L4 < 4; ++L4) {
-      const bool f = L4 < 3 ? (t == L4) : (t >= 0 && t != T3);
+      const bool f = own && (L4 < 3 ? (t == L4) : (t >= 0 && t != T3));
       m[L4] = __ballot_sync(0xffffffffu, f);
       if (lane == 0) s_wsum[L4][w] = __popc(m[L4]);
     }
@@ -297,7 +315,7 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
     cn[0] = s_base[0];
     cn[1] = s_base[1];
     cn[2] = s_base[2];
-    cn[3] = n - s_base[3];
+    cn[3] = seq_owned_below(v.seq_w, v.seq_r, n) - s_base[3];
     cn[4] = s_base[3];
   }
 }
@@ -453,7 +471,8 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(const DevView v) {
                                     if (m0 + k < v.mcap) mv[m0 + k] = make_int4(X, r, X | (dst << 2), pos);
                                   });
     // tokens entering the store -> remaining holes
-    const int nin = block_compact(0, n, s_wsum, &s_tot, [&](int p) { return tnew[p] == X && told[p] != X; },
+    const int nin = block_compact(0, n, s_wsum, &s_tot,
+                                  [&](int p) { return tnew[p] == X && told[p] != X && seq_own(v.seq_w, v.seq_r, p); },
                                   [&](int p, int k) {
                                     const int dst = hole[ntk + k];
                                     inew[dst] = p;

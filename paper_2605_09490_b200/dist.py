@@ -6,6 +6,13 @@
   the step is local; at a manage event the ranks all-gather S_part (B*H_kv*N_max fp32 in
   total) and each classifies the identical gathered scores (kv_tier_classify_gathered),
   so tiers agree bit-for-bit across ranks and with the unsharded run.
+* Sequence sharding (row 3): positions are owned block-cyclically (64-position blocks, block
+  k on rank k % world).  Per layer every rank attends its own visible tokens
+  (kv_tier_decode_attention_lse: o normalised by its partial sum + (m, l) per head), the
+  ranks all-gather (o, m, l) and combine them in rank order (lse_combine: the LSE merge of
+  Eq. 3 split by position), and each rank completes its fused score update with the global
+  (M, L) (kv_tier_score_update_lse).  At an event the summed S_part (all-gather; each
+  position has one owner, so the sum is exact) feeds kv_tier_classify_gathered on every rank.
 Timing is the max over ranks."""
 from __future__ import annotations
 
@@ -96,3 +103,48 @@ class _null:
 
     def __exit__(self, *a):
         return False
+
+
+# ------------------------------------------------------------------ sequence sharding
+SEQ_BLOCK = 64          # kv_internal.cuh
+
+
+def seq_owner(pos, world):
+    """Rank owning position `pos` (block-cyclic, SEQ_BLOCK positions per block)."""
+    return (pos // SEQ_BLOCK) % world
+
+
+def seq_owned_positions(n, world, rank):
+    """Ascending positions below n owned by `rank` (host twin of seq_owned_below / seq_pos_of)."""
+    return [p for p in range(n) if seq_owner(p, world) == rank]
+
+
+def lse_combine(o_parts, lse_parts):
+    """Combine per-rank partial attention results (rank order, deterministic).
+
+    o_parts [W][B][H][d]: each rank's o normalised by its own partial sum; lse_parts
+    [W][B][H][2]: (m, l) per head, m in the log2 domain, l = sum 2^(z - m) (a rank without
+    visible tokens has m = -inf, l = 0, o = 0).  Returns (o [B][H][d], lse [B][H][2]) with
+    M = max_r m_r, w_r = 2^(m_r - M) l_r, L = sum_r w_r, o = sum_r w_r o_r / L."""
+    m, l = lse_parts[..., 0], lse_parts[..., 1]
+    M = m.max(dim=0).values
+    w = torch.where(torch.isinf(m), torch.zeros_like(l), torch.exp2(m - M) * l)
+    L = w.sum(dim=0)
+    o = (w.unsqueeze(-1) * o_parts).sum(dim=0) / L.unsqueeze(-1)
+    return o, torch.stack([M, L], dim=-1)
+
+
+def seq_combine(o_local, lse_local, group=None):
+    """All-gather (o, lse) over the group (NCCL on CUDA tensors, gloo on CPU) and combine."""
+    og = gather_scores(o_local.float(), group)
+    lg = gather_scores(lse_local, group)
+    return lse_combine(og, lg)
+
+
+def seq_classify(kv, stream=None, group=None):
+    """a5 under sequence sharding: sum of every rank's S_part (exact: one owner per position)
+    via the all-gather, then the identical classify on every rank."""
+    with torch.cuda.stream(stream) if stream is not None else _null():
+        S_all = gather_scores(kv.scores_tensor(), group)
+        kv.classify_gathered(S_all, S_all.shape[0], stream=stream)
+    return S_all

@@ -213,3 +213,76 @@ class KvHeadShardedDecode:
     def close(self):
         for r in self.runs:
             r.close()
+
+
+class SeqShardedDecode:
+    """Sequence sharding simulated in one process: `world` ctxs on one
+    device, ctx r owning the 64-position blocks k with k % world == r.  Every layer: each ctx
+    attends its own tokens (decode_attention_lse), the partials are combined in rank order
+    (dist.lse_combine -- the bytes an NCCL all-gather moves), and each ctx finishes its
+    score update with the global (M, L).  Events: summed S_part -> classify_gathered."""
+
+    def __init__(self, w, world, device="cuda:0", out_fp32=True, **kw):
+        self.w, self.world = w, world
+        self.runs = [TieredDecode(w, device=device, out_fp32=out_fp32, shard=kt.SHARD_SEQUENCE, rank=r,
+                                  world=world, **kw) for r in range(world)]
+        r0 = self.runs[0]
+        self.dev = r0.dev
+        self.stream = r0.main
+        B, L, Hq, d = w["B"], w["L"], w["Hq"], w["d"]
+        self.Ol = [torch.empty((L, B, Hq, d), dtype=torch.float32, device=self.dev) for _ in range(world)]
+        self.LSE = [torch.empty((L, B, Hq, 2), dtype=torch.float32, device=self.dev) for _ in range(world)]
+        self.O = torch.empty((L, B, Hq, d), dtype=torch.float32, device=self.dev)
+        self.LSEg = torch.empty((L, B, Hq, 2), dtype=torch.float32, device=self.dev)
+        self.t = 0
+
+    def is_event(self, t):
+        return t % self.w["interval"] == 0
+
+    def step(self):
+        from . import dist as D
+        t, s = self.t, self.stream
+        r0 = self.runs[0]
+        with torch.cuda.stream(s):
+            for r in self.runs:
+                r.kv.begin_step(stream=s)
+            for l in range(self.w["L"]):
+                for i, r in enumerate(self.runs):
+                    r.kv.decode_attention_lse(l, r0.Q[t, l], self.Ol[i][l], self.LSE[i][l], 1, stream=s,
+                                              k_new=r0.Kn[t, l], v_new=r0.Vn[t, l])
+                o, lse = D.lse_combine(torch.stack([x[l] for x in self.Ol]), torch.stack([x[l] for x in self.LSE]))
+                self.O[l].copy_(o)
+                self.LSEg[l].copy_(lse)
+                for r in self.runs:
+                    r.kv.score_update_lse(self.LSEg[l], stream=s)
+            for r in self.runs:
+                r.kv.end_step(stream=s)
+            if self.is_event(t):
+                S_all = torch.stack([r.kv.scores_tensor() for r in self.runs]).contiguous()   # the all-gather
+                for r in self.runs:
+                    r.kv.classify_gathered(S_all, self.world, stream=s)
+                    r.kv.migrate(stream=s, side=r.side)
+                s.synchronize()
+        self.t += 1
+        for r in self.runs:
+            r.t = self.t
+        return self.O
+
+    def output(self):
+        self.stream.synchronize()
+        return self.O.cpu().numpy()
+
+    def scores(self):
+        """Summed S_part [B][H_kv][n] (every position has exactly one owner)."""
+        import numpy as np
+        self.sync()
+        return np.sum([r.kv.export(kt.X_SCORES) for r in self.runs], axis=0)
+
+    def sync(self):
+        self.stream.synchronize()
+        for r in self.runs:
+            r.sync()
+
+    def close(self):
+        for r in self.runs:
+            r.close()

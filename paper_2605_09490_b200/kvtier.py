@@ -60,6 +60,9 @@ _SIGS = {
     "kv_tier_prefetch": [C.c_void_p, C.c_int32, C.c_void_p],
     "kv_tier_decode_attention": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_int32, C.c_void_p],
+    "kv_tier_decode_attention_lse": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_int32, C.c_void_p],
+    "kv_tier_score_update_lse": [C.c_void_p, C.c_void_p, C.c_void_p],
     "kv_tier_score_update": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p],
     "kv_tier_visible_count": [C.c_void_p, C.POINTER(C.c_int32)],
     "kv_tier_end_step": [C.c_void_p, C.c_void_p],
@@ -184,6 +187,19 @@ class KvTier:
                                                C.c_void_p(o.data_ptr()), fuse_score_update, _stream_ptr(stream)),
                self.ctx)
 
+    def decode_attention_lse(self, layer, q, o, lse, fuse_score_update=1, stream=None, k_new=None, v_new=None):
+        """As decode_attention, o normalised by this ctx's partial sum; lse [B][H_q][2] fp32 gets
+        (max in the log2 domain, sum) per head (sequence sharding)."""
+        kp = C.c_void_p(k_new.data_ptr()) if k_new is not None else None
+        vp = C.c_void_p(v_new.data_ptr()) if v_new is not None else None
+        _check(load().kv_tier_decode_attention_lse(self.ctx, layer, C.c_void_p(q.data_ptr()), kp, vp,
+                                                   C.c_void_p(o.data_ptr()), C.c_void_p(lse.data_ptr()),
+                                                   fuse_score_update, _stream_ptr(stream)), self.ctx)
+
+    def score_update_lse(self, lse_global, stream=None):
+        _check(load().kv_tier_score_update_lse(self.ctx, C.c_void_p(lse_global.data_ptr()), _stream_ptr(stream)),
+               self.ctx)
+
     def score_update(self, layer, probs, stream=None):
         _check(load().kv_tier_score_update(self.ctx, layer, C.c_void_p(probs.data_ptr()), _stream_ptr(stream)),
                self.ctx)
@@ -244,6 +260,9 @@ class KvTier:
         return n.value, t.value
 
     def export(self, what, layer=0):
+        """Canonical (ascending-position) export.  Per-request results are stacked into one
+        array when every request has the same counts (always, except under sequence sharding,
+        where a list of per-request arrays is returned)."""
         nbytes = C.c_size_t()
         _check(load().kv_tier_export_size(self.ctx, what, C.byref(nbytes)), self.ctx)
         buf = np.zeros(nbytes.value, dtype=np.uint8)
@@ -253,13 +272,24 @@ class KvTier:
             return buf.view(np.float32).reshape(B, H, -1)
         if what == X_TIERS:
             return buf.reshape(B, -1)
+        counts, _ = self.census()
+        T = {X_IDX_T0: 0, X_IDX_T1: 1, X_IDX_T2: 2, X_T0_ROWS: 0, X_T1_ROWS: 1, X_STAGING: 1,
+             X_T2_CODES: 2, X_T2_SCALES: 2}[what]
         if what in (X_IDX_T0, X_IDX_T1, X_IDX_T2):
-            return buf.view(np.int32).reshape(B, -1)
-        if what in (X_T0_ROWS, X_T1_ROWS, X_STAGING):
-            return buf.view(np.uint16).reshape(B, H, -1, 2, D)
-        if what == X_T2_CODES:
-            return buf.view(np.int8).reshape(B, H, -1, 2, D)
-        return buf.view(np.float32).reshape(B, H, -1, 2)
+            per, dt, shape = 4, np.int32, lambda c: (c,)
+        elif what in (X_T0_ROWS, X_T1_ROWS, X_STAGING):
+            per, dt, shape = H * 2 * D * 2, np.uint16, lambda c: (H, c, 2, D)
+        elif what == X_T2_CODES:
+            per, dt, shape = H * 2 * D, np.int8, lambda c: (H, c, 2, D)
+        else:
+            per, dt, shape = H * 2 * 4, np.float32, lambda c: (H, c, 2)
+        out, off = [], 0
+        for b in range(B):
+            c = int(counts[b][T])
+            out.append(buf[off:off + c * per].view(dt).reshape(shape(c)))
+            off += c * per
+        assert off == buf.size
+        return np.stack(out) if len({x.shape for x in out}) == 1 else out
 
     def debug_trace(self):
         """[L][CTAs][NTRACE] %globaltimer ns checkpoints of the last step (KVTIER_TRACE=1)."""

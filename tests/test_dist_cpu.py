@@ -103,3 +103,74 @@ def test_kvhead_gather_gloo_world2():
 def test_kvhead_plan_rejects_uneven():
     with pytest.raises(ValueError):
         D.kvhead_plan(3, 0, 16, 4)
+
+
+# --------------------------------------------------------------------- sequence sharding
+def _seq_worker(rank, world, port, q):
+    """Each rank holds the keys/values of its own 64-position blocks; the all-gathered LSE
+    combine must equal softmax attention over the whole sequence (float64 reference)."""
+    import numpy as np
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(5)
+        n, B, H, d = 300, 2, 3, 16
+        qv = torch.randn(B, H, d, generator=g, dtype=torch.float64)
+        K = torch.randn(B, n, d, generator=g, dtype=torch.float64)
+        V = torch.randn(B, n, d, generator=g, dtype=torch.float64)
+        z = torch.einsum("bhd,bnd->bhn", qv, K) / np.sqrt(d) * np.log2(np.e)      # log2 domain
+        ref = torch.einsum("bhn,bnd->bhd", torch.softmax(z * np.log(2), dim=-1), V)
+        own = torch.tensor(D.seq_owned_positions(n, world, rank))
+        zl = z[:, :, own]
+        m = zl.max(dim=-1).values
+        p = torch.exp2(zl - m.unsqueeze(-1))
+        l = p.sum(dim=-1)
+        o_local = torch.einsum("bhn,bnd->bhd", p, V[:, own]) / l.unsqueeze(-1)
+        o, lse = D.seq_combine(o_local, torch.stack([m, l], dim=-1))
+        M_ref = z.max(dim=-1).values
+        L_ref = torch.exp2(z - M_ref.unsqueeze(-1)).sum(dim=-1)
+        q.put((rank, float((o.double() - ref).abs().max()), float((lse[..., 0].double() - M_ref).abs().max()),
+               float(((lse[..., 1].double() - L_ref) / L_ref).abs().max()), own.tolist()[:3]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sequence_sharding_lse_combine_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_seq_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, err_o, err_m, err_l, first in out:
+        assert err_o < 1e-5 and err_m < 1e-6 and err_l < 1e-6, (rank, err_o, err_m, err_l)   # fp32 gather
+        assert first == [64 * rank, 64 * rank + 1, 64 * rank + 2]
+
+
+def test_sequence_ownership_formulas():
+    # host twins of seq_owned_below / seq_pos_of (kv_internal.cuh) against brute force
+    for world in (1, 2, 3, 8):
+        for rank in range(world):
+            owned = D.seq_owned_positions(1000, world, rank)
+            for n in (0, 1, 63, 64, 65, 200, 999, 1000):
+                assert sum(1 for p in owned if p < n) == _owned_below(world, rank, n)
+            for j, p in enumerate(owned):
+                assert _pos_of(world, rank, j) == p
+
+
+def _owned_below(w, r, n):        # transcription of seq_owned_below
+    if w <= 1:
+        return n
+    full, rem = n // 64, n % 64
+    c = (full // w) * 64 + (64 if full % w > r else 0)
+    return c + (rem if full % w == r else 0)
+
+
+def _pos_of(w, r, j):             # transcription of seq_pos_of
+    return j if w <= 1 else ((j // 64) * w + r) * 64 + j % 64

@@ -385,3 +385,86 @@ def test_kvhead_plain_classify_refused():
     with pytest.raises(RuntimeError):
         run.kv.classify(stream=run.main)
     run.close()
+
+
+# --------------------------------------------------------------------- sequence sharding (§8e row 3)
+def _check_seq_event_state(sh, orc, layers=(0, 1)):
+    """Every shard holds the global tiers; its index lists, census and T0/T1 rows (and T2
+    codes) are exactly the oracle's restricted to the positions it owns."""
+    from paper_2605_09490_b200 import dist as D
+    st = orc.st
+    n = st.n
+    for r, run in enumerate(sh.runs):
+        kv = run.kv
+        own = set(D.seq_owned_positions(n, sh.world, r))
+        tiers = kv.export(kt.X_TIERS)
+        idx = [kv.export(x) for x in (kt.X_IDX_T0, kt.X_IDX_T1, kt.X_IDX_T2)]
+        counts, _ = kv.census()
+        for bo, bg in enumerate(orc.reqs):
+            assert np.array_equal(tiers[bg], st.tier[bo, :n]), f"shard {r}: tiers differ"
+            want = [[p for p in O.export_index(st, bo, T) if p in own] for T in range(3)]
+            for T in range(3):
+                assert idx[T][bg].tolist() == want[T], f"shard {r}: idx T{T}"
+            n_own = sum(1 for p in range(n) if p in own)
+            assert counts[bg].tolist() == [len(want[0]), len(want[1]), len(want[2]),
+                                           n_own - len(want[0]) - len(want[1]) - len(want[2])]
+        for l in layers:
+            for T, x in ((0, kt.X_T0_ROWS), (1, kt.X_T1_ROWS)):
+                rows = kv.export(x, l)
+                for bo, bg in enumerate(orc.reqs):
+                    pos = [p for p in O.export_index(st, bo, T) if p in own]
+                    assert np.array_equal(rows[bg][:, :, 0, :], _bf16_bits(st.rowK[l, bo][:, pos]))
+                    assert np.array_equal(rows[bg][:, :, 1, :], _bf16_bits(st.rowV[l, bo][:, pos]))
+            if run.w["t2_bp"]:
+                codes = kv.export(kt.X_T2_CODES, l)
+                for bo, bg in enumerate(orc.reqs):
+                    pos = [p for p in O.export_index(st, bo, 2) if p in own]
+                    assert np.array_equal(codes[bg][:, :, 0, :], st.codeK[l, bo][:, pos])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sequence_sharding_matches_unsharded_oracle(world):
+    # world ctxs on one GPU, block-cyclic 64-position ownership; per-layer LSE combine of the
+    # ranks' partials, global (M, L) back into the fused score update, summed scores at events
+    w = H.workload("tiny", B=2, L=2, Hq=8, Hkv=2, d=64, N=400, P=16, interval=8, steps=26,
+                   hbm_bp=4000, evict_bp=800, t2_bp=3000)
+    sh = H.SeqShardedDecode(w, world)
+    orc = OracleRun(w)
+    for t in range(w["steps"]):
+        sh.step()
+        o = sh.output()
+        ref = orc.step()
+        ok, mabs, _ = o_close(o[:, orc.reqs], ref)
+        assert ok, (t, mabs)
+        if sh.is_event(t) or t == w["steps"] - 1:
+            ok, mrel = s_close(sh.scores()[orc.reqs], orc.st.S_part[:, :, :orc.st.n])
+            assert ok, (t, mrel)
+            if sh.is_event(t):
+                _check_seq_event_state(sh, orc)
+    sh.close()
+
+
+def test_sequence_shard_without_visible_tokens():
+    # a shard owning no position yet (n < 64 * rank) contributes an empty partial (m = -inf, l = 0)
+    w = H.workload("tiny", B=1, L=1, Hq=4, Hkv=2, d=64, N=60, P=8, interval=4, steps=6,
+                   hbm_bp=5000, evict_bp=500, t2_bp=0)
+    sh = H.SeqShardedDecode(w, 2)
+    orc = OracleRun(w)
+    for t in range(w["steps"]):
+        sh.step()
+        ok, mabs, _ = o_close(sh.output()[:, orc.reqs], orc.step())
+        assert ok, (t, mabs)
+    ok, mrel = s_close(sh.scores()[orc.reqs], orc.st.S_part[:, :, :orc.st.n])
+    assert ok, mrel
+    sh.close()
+
+
+def test_sequence_shard_refuses_plain_paths():
+    w = H.workload("tiny", steps=2)
+    run = H.TieredDecode(w, shard=kt.SHARD_SEQUENCE, rank=1, world=2)
+    with pytest.raises(kt.KvTierError):
+        run.kv.step(run.Q[0], run.Kn[0], run.Vn[0], run.O, 1, stream=run.main, side=run.side)
+    run.kv.begin_step(stream=run.main)
+    with pytest.raises(kt.KvTierError):
+        run.kv.decode_attention(0, run.Q[0, 0], run.O[0], 1, stream=run.main, k_new=run.Kn[0, 0], v_new=run.Vn[0, 0])
+    run.close()
