@@ -82,8 +82,13 @@ def gather_scores(S_local, group=None):
     if world == 1:
         return x.unsqueeze(0)
     out = torch.empty((world,) + tuple(x.shape), dtype=x.dtype, device=x.device)
-    if x.is_cuda:
+    if x.is_cuda and dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, x, group=group)
+    elif x.is_cuda:                         # gloo: stage through host memory
+        hx = x.cpu()
+        ho = torch.empty(out.shape, dtype=x.dtype)
+        dist.all_gather(list(ho.unbind(0)), hx, group=group)
+        out.copy_(ho)
     else:
         dist.all_gather(list(out.unbind(0)), x, group=group)
     return out

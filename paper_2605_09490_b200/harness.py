@@ -286,3 +286,60 @@ class SeqShardedDecode:
     def close(self):
         for r in self.runs:
             r.close()
+
+
+class SeqShardRank:
+    """One rank of a sequence-sharded decode in its own process: the ctx
+    owns the 64-position blocks k with k % world == rank; every layer the ranks all-gather
+    (o, m, l) over the process group (NCCL, or gloo staged through host memory) and combine
+    them in rank order; events classify the all-gathered scores.  Every rank ends each step
+    with the full o of all layers."""
+
+    def __init__(self, w, rank, world, device="cuda:0", group=None, **kw):
+        self.w, self.rank, self.world, self.group = w, rank, world, group
+        self.run = TieredDecode(w, device=device, out_fp32=True, shard=kt.SHARD_SEQUENCE, rank=rank, world=world, **kw)
+        B, L, Hq, d = w["B"], w["L"], w["Hq"], w["d"]
+        dev = self.run.dev
+        self.Ol = torch.empty((L, B, Hq, d), dtype=torch.float32, device=dev)
+        self.LSE = torch.empty((L, B, Hq, 2), dtype=torch.float32, device=dev)
+        self.O = torch.empty((L, B, Hq, d), dtype=torch.float32, device=dev)
+        self.LSEg = torch.empty((L, B, Hq, 2), dtype=torch.float32, device=dev)
+        self.t = 0
+
+    def is_event(self, t):
+        return t % self.w["interval"] == 0
+
+    def step(self):
+        from . import dist as D
+        r, t = self.run, self.t
+        s = r.main
+        with torch.cuda.stream(s):
+            r.kv.begin_step(stream=s)
+            for l in range(self.w["L"]):
+                r.kv.decode_attention_lse(l, r.Q[t, l], self.Ol[l], self.LSE[l], 1, stream=s,
+                                          k_new=r.Kn[t, l], v_new=r.Vn[t, l])
+                o, lse = D.seq_combine(self.Ol[l], self.LSE[l], self.group)
+                self.O[l].copy_(o)
+                self.LSEg[l].copy_(lse)
+                r.kv.score_update_lse(self.LSEg[l], stream=s)
+            r.kv.end_step(stream=s)
+            if self.is_event(t):
+                D.seq_classify(r.kv, stream=s, group=self.group)
+                r.kv.migrate(stream=s, side=r.side)
+        self.t += 1
+        r.t = self.t
+        return self.O
+
+    def output(self):
+        self.run.main.synchronize()
+        return self.O.cpu().numpy()
+
+    def scores(self):
+        """Summed S_part over the ranks [B][H_kv][n] (exact: one owner per position)."""
+        from . import dist as D
+        self.run.sync()
+        S = torch.from_numpy(self.run.kv.export(kt.X_SCORES).copy())
+        return D.gather_scores(S, self.group).sum(dim=0).numpy()
+
+    def close(self):
+        self.run.close()

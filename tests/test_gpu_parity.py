@@ -468,3 +468,53 @@ def test_sequence_shard_refuses_plain_paths():
     with pytest.raises(kt.KvTierError):
         run.kv.decode_attention(0, run.Q[0, 0], run.O[0], 1, stream=run.main, k_new=run.Kn[0, 0], v_new=run.Vn[0, 0])
     run.close()
+
+
+def _seq_proc_worker(rank, world, port, q):
+    import os
+    import torch.distributed as tdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)   # one GPU: gloo via host memory
+    try:
+        w = H.workload("tiny", B=2, L=2, Hq=8, Hkv=2, d=64, N=400, P=16, interval=8, steps=18,
+                       hbm_bp=4000, evict_bp=800, t2_bp=3000)
+        sr = H.SeqShardRank(w, rank, world)
+        orc = OracleRun(w)
+        worst_o, worst_s = 0.0, 0.0
+        for t in range(w["steps"]):
+            sr.step()
+            ok, mabs, _ = o_close(sr.output()[:, orc.reqs], orc.step())
+            worst_o = max(worst_o, mabs)
+            assert ok, (rank, t, mabs)
+            if sr.is_event(t) or t == w["steps"] - 1:
+                ok, mrel = s_close(sr.scores()[orc.reqs], orc.st.S_part[:, :, :orc.st.n])
+                worst_s = max(worst_s, mrel)
+                assert ok, (rank, t, mrel)
+                assert np.array_equal(sr.run.kv.export(kt.X_TIERS)[orc.reqs], orc.st.tier[:, :orc.st.n])
+        sr.close()
+        q.put((rank, "ok", worst_o, worst_s))
+    except Exception as e:                      # report to the parent
+        q.put((rank, repr(e), 0.0, 0.0))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_sequence_sharding_two_processes():
+    # the multi-process driver (one ctx per process, per-layer all-gather of (o, m, l) over a
+    # process group) against the unsharded oracle; two processes share the one GPU of this box
+    import socket
+    import torch.multiprocessing as mp
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_seq_proc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    for rank, status, wo, ws in res:
+        assert status == "ok", (rank, status)
