@@ -543,7 +543,6 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   }
   named_sync(1, NCONS);                // every consumer is done with the ring
   float* ow = reinterpret_cast<float*>(ring);
-  float* fw = ow + NW * 8 * OWS;       // [NW][8] warp factors exp2(m_w - M)
   if (lane < 4) {
     redm[w * 8 + 2 * lane] = mxa;
     redm[w * 8 + 2 * lane + 1] = mxb;
@@ -560,19 +559,52 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     o1[8] = oacc[mt][3];
   }
   named_sync(1, NCONS);
+  const int tot = G * D;
+  if (!cm) {
+    // publish straight to the global slot (visible to the merge kernel once this grid
+    // completes): every thread forms its elements' per-head max and warp factors itself
+    float* part = v.part + ((size_t)unit * (C + 1) + r) * v.part_stride;
+    if (tid < 8) {
+      float M = -INFINITY;
+#pragma unroll
+      for (int x = 0; x < NW; ++x) M = fmaxf(M, redm[x * 8 + tid]);
+      float Ls = 0.f;
+#pragma unroll
+      for (int x = 0; x < NW; ++x) {
+        const float m = redm[x * 8 + tid];
+        Ls += (m == -INFINITY ? 0.f : ex2_ftz(m - M)) * redl[x * 8 + tid];
+      }
+      part[tid] = M;
+      part[8 + tid] = Ls;
+    }
+    for (int e = tid; e < tot; e += NCONS) {
+      const int h = e / D, dd = e - h * D;
+      float mw[NW], M = -INFINITY;
+#pragma unroll
+      for (int x = 0; x < NW; ++x) {
+        mw[x] = redm[x * 8 + h];
+        M = fmaxf(M, mw[x]);
+      }
+      float a = 0.f;
+#pragma unroll
+      for (int x = 0; x < NW; ++x) a += (mw[x] == -INFINITY ? 0.f : ex2_ftz(mw[x] - M)) * ow[(x * 8 + h) * OWS + dd];
+      part[16 + e] = a;
+    }
+    if (tr && tid == 0) tr[4] = gtimer();
+    return;
+  }
+  float* fw = ow + NW * 8 * OWS;       // [NW][8] warp factors exp2(m_w - M)
   if (tid < 8 * NW) {                  // factors of every (warp, head)
     const int ww = tid >> 3, h = tid & 7;
     float M = -INFINITY;
 #pragma unroll
     for (int x = 0; x < NW; ++x) M = fmaxf(M, redm[x * 8 + h]);
     const float m = redm[ww * 8 + h];
-    fw[tid] = m == -INFINITY ? 0.f : exp2f(m - M);
+    fw[tid] = m == -INFINITY ? 0.f : ex2_ftz(m - M);
     if (ww == 0) xm[h] = M;
   }
   named_sync(1, NCONS);
-  // CTA partial, staged in shared memory as it goes to global: [m 8 | l 8 | o G*D]
-  const int tot = G * D;
-  const int ps4 = (16 + tot + 3) / 4;                 // float4s per partial
+  // CTA partial, staged in shared memory for the cluster exchange: [m 8 | l 8 | o G*D]
   float* xp = fw + 8 * NW;                            // [16 + G*D] in the free ring (16-B aligned)
   if (tid < 8) {
     float Ls = 0.f;
@@ -589,12 +621,6 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     xp[16 + e] = a;
   }
   named_sync(1, NCONS);
-  if (!cm) {   // publish: visible to the merge kernel once this grid completes (no fence needed)
-    float4* part = reinterpret_cast<float4*>(v.part + ((size_t)unit * (C + 1) + r) * v.part_stride);
-    for (int i = tid; i < ps4; i += NCONS) part[i] = reinterpret_cast<const float4*>(xp)[i];
-    if (tr && tid == 0) tr[4] = gtimer();
-    return;
-  }
   // ---- cluster merge: push (m, l) and slice c of o to rank c, one barrier, merge own slice
   cg::cluster_group cluster = cg::this_cluster();
   asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");     // phase 0 (long complete)
