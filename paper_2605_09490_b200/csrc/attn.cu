@@ -748,7 +748,7 @@ template <int D>
 __global__ void __launch_bounds__(256) k_decode_merge(const DevView v, const int layer, void* __restrict__ o,
                                                       const int zpar, float* __restrict__ lse) {
   // lse (optional) [B][Hq][2]: this ctx's (max, sum) per head, log2 domain (sequence sharding)
-  constexpr int MAXP = 16, MAXNP = 65;
+  constexpr int MAXP = 9, MAXNP = 65;      // split <= 8: one batch
   __shared__ float sf[MAXNP * 8], sl[MAXNP * 8], sI[8];
   const int unit = blockIdx.x, tid = threadIdx.x;
   const int b = unit / v.Hkv, g = unit - b * v.Hkv;
