@@ -25,6 +25,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+CONFIG_INDEX = {"tiny": 0, "7b": 1, "14b": 2, "32b": 3, "70b": 4}      # BASELINE.json configs[i]
 
 
 def _peaks():
@@ -397,7 +398,7 @@ def main():
             "value": sps, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{args.config}-shaped (BASELINE.json configs[1]): B={B}/GPU L={L} "
+            "config": {"workload": f"{args.config}-shaped (BASELINE.json configs[{CONFIG_INDEX.get(args.config, '?')}]): B={B}/GPU L={L} "
                                    f"Hq/Hkv={w['Hq']}/{Hkv} d={d} N={w['N']} beta={args.hbm}bp r={args.evict}bp "
                                    f"Delta={w['interval']} differential staging",
                        "global_batch": B * world, "parallelism": f"request-sharded x{world}",

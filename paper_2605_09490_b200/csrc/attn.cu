@@ -842,6 +842,39 @@ __global__ void __launch_bounds__(256) k_score_flush(const DevView v, const int 
   if (bad) atomicOr(&v.st->err, 1);
 }
 
+// Register-lean variant (default): it runs beside the decode chain, so its CTAs must fit next
+// to two decode CTAs in an SM's register file (128 threads x <= 32 registers); one (unit,
+// token) entry per thread per pass, same arithmetic and order as score_range.
+__global__ void __launch_bounds__(128, 16) k_score_flush_lean(const DevView v, const int zfirst, const int nz) {
+  const int cur = v.st->cur;
+  Seg sg;
+  sg.init(v.cnt[cur], v.st->nn);
+  const long long tot = (long long)v.B * v.Hkv * sg.nvirt;
+  const size_t zslot = (size_t)v.B * v.Hkv * v.zrows * 8, mslot = (size_t)v.B * v.Hkv * 16;
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+    const int u = (int)(i / sg.nvirt), t = (int)(i - (long long)u * sg.nvirt);
+    if (!sg.valid(t)) continue;
+    const int pos = sg.pos(v, cur, u / v.Hkv, t);
+    float s = v.S[(size_t)u * v.Nmax + pos];
+    for (int j = 0; j < nz; ++j) {
+      const int slot = (zfirst + j) % ZRING;
+      const float4* z = reinterpret_cast<const float4*>(v.zbuf + slot * zslot + ((size_t)u * v.zrows + t) * 8);
+      const float* ml = v.ml + slot * mslot + (size_t)u * 16;
+      const float4 za = z[0], zc = z[1];
+      const float zz[8] = {za.x, za.y, za.z, za.w, zc.x, zc.y, zc.z, zc.w};
+      float inc = 0.f;
+#pragma unroll
+      for (int h = 0; h < 8; ++h)
+        if (h < v.G) inc += ex2_ftz(zz[h] - ml[h]) * ml[8 + h];
+      s = s + inc;
+      bad |= !isfinite(inc);
+    }
+    v.S[(size_t)u * v.Nmax + pos] = s;
+  }
+  if (bad) atomicOr(&v.st->err, 1);
+}
+
 // Sequence shards: a shard's tier counts differ per request, so every unit decodes its own
 // virtual layout (one thread per (unit, virtual row) over the zrows-wide logit rows).
 __global__ void __launch_bounds__(256) k_score_flush_req(const DevView v, const int zfirst, const int nz) {
@@ -872,7 +905,8 @@ __global__ void __launch_bounds__(256) k_score_flush_req(const DevView v, const 
 
 cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_t s) {
   if (v.seq_w > 1) k_score_flush_req<<<148, 256, 0, s>>>(v, zfirst, nz);
-  else k_score_flush<<<148, 256, 0, s>>>(v, zfirst, nz);
+  else if (v.score_lean) k_score_flush_lean<<<v.score_grid, 128, 0, s>>>(v, zfirst, nz);
+  else k_score_flush<<<v.score_grid, 256, 0, s>>>(v, zfirst, nz);
   return cudaGetLastError();
 }
 

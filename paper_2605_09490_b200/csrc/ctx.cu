@@ -300,6 +300,8 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     const long long l2mb = getenv("KVTIER_L2PF_MB") ? atoll(getenv("KVTIER_L2PF_MB")) : 0;   // measured: no gain
     v.l2pf_bytes = l2mb * (1LL << 20) / std::max(1, v.nc);
     v.inflight = getenv("KVTIER_INFLIGHT") ? atoi(getenv("KVTIER_INFLIGHT")) : 0;
+    v.score_lean = getenv("KVTIER_SCORE_LEAN") ? atoi(getenv("KVTIER_SCORE_LEAN")) : 0;   // measured slower
+    v.score_grid = getenv("KVTIER_SCORE_GRID") ? atoi(getenv("KVTIER_SCORE_GRID")) : (v.score_lean ? 296 : 148);
   }
   for (int i = 0; i < 2; ++i) {
     v.k0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_k0[i]);

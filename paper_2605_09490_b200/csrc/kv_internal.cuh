@@ -9,7 +9,7 @@ namespace kvt {
 constexpr int T0 = 0, T1 = 1, T2 = 2, T3 = 3;
 constexpr int NTRACE = 24;        // debug trace slots per CTA (KVTIER_TRACE=1)
 constexpr int CNT_STRIDE = 8;     // cnt[buf][b][8]: |T0| |T1| |T2| |T3| |visible at event| pad..
-constexpr int ZRING = 4;          // logits/ML ring slots (score kernels lag the decode chain)
+constexpr int ZRING = 8;          // logits/ML ring slots (score kernels lag the decode chain)
 constexpr int ZBATCH = 1;         // launches whose score updates one score kernel applies (layer order;
                                   // measured: batching 4 made the kernel too big to share SMs with the chain)
 
@@ -45,7 +45,9 @@ struct DevView {
   int flat;             // flat decode kernel (attn_flat.cu; default) instead of split-per-unit
   int fvariant;         // flat kernel variant (consumer warps x stages)
   int nc;               // flat kernel grid (CTAs; one per SM)
-  int seq_w, seq_r;     // sequence sharding: positions in 64-blocks, block k owned by rank k % seq_w
+  int seq_w, seq_r;
+  int score_grid;       // CTAs of the score-flush kernel (runs beside the attention chain)
+  int score_lean;       // 1: register-lean score-flush kernel (fits beside two decode CTAs)     // sequence sharding: positions in 64-blocks, block k owned by rank k % seq_w
   int spin_hint;        // mbarrier try_wait suspend-time hint in ns (0: plain polling)
   long long l2pf_bytes; // flat kernel: K/V bytes per CTA requested into L2 at kernel start (0: off)
   int inflight;         // flat kernel: max ring stages requested but not landed (0: the whole ring)
