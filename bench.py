@@ -26,6 +26,7 @@ sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
 CONFIG_INDEX = {"tiny": 0, "7b": 1, "14b": 2, "32b": 3, "70b": 4}      # BASELINE.json configs[i]
+POLICIES = {"hierarchy": 0, "streaming": 1, "h2o": 2, "random": 3}       # kv_tier_policy
 
 
 def _peaks():
@@ -48,6 +49,9 @@ def _args():
     ap.add_argument("--evict", type=int, default=500, help="r in basis points")
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--variant", type=int, default=0, help="decode kernel variant (consumer warps x stages)")
+    ap.add_argument("--policy", default="hierarchy", choices=list(POLICIES),
+                    help="tier policy: the paper's hierarchy or a pure-eviction baseline (P:276-280)")
+    ap.add_argument("--budget", type=int, default=1024, help="kept tokens per request (h2o / random)")
     ap.add_argument("--no-extras", action="store_true", help="skip control/e2e/stream/cpu legs")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -203,7 +207,9 @@ def main():
 
     W, K = args.warmup, args.steps
     E = 0 if args.no_extras else min(K, 64)
-    w = H.workload(args.config, hbm_bp=args.hbm, evict_bp=args.evict, steps=W + K + E + 1)
+    pol = POLICIES[args.policy]
+    w = H.workload(args.config, hbm_bp=args.hbm, evict_bp=args.evict, steps=W + K + E + 1, policy=pol,
+                   budget=args.budget if pol in (2, 3) else 0, policy_seed=7)
     dev = f"cuda:{local}"
     peaks = _peaks()
     from paper_2605_09490_b200.dist import shard_plan
@@ -400,7 +406,9 @@ def main():
             "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{args.config}-shaped (BASELINE.json configs[{CONFIG_INDEX.get(args.config, '?')}]): B={B}/GPU L={L} "
                                    f"Hq/Hkv={w['Hq']}/{Hkv} d={d} N={w['N']} beta={args.hbm}bp r={args.evict}bp "
-                                   f"Delta={w['interval']} differential staging",
+                                   f"Delta={w['interval']} differential staging"
+                                   + ("" if pol == 0 else f" policy={args.policy}"
+                                      + (f" budget={args.budget}" if pol in (2, 3) else "")),
                        "global_batch": B * world, "parallelism": f"request-sharded x{world}",
                        "l2": "no flush: per-step K/V traffic > 126 MB L2", "split": run_split(w, args)},
             "hbm_gbs": hbm_gbs, "hbm_frac_of_measured_peak": hbm_gbs / peaks["hbm_gbs"],

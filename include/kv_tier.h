@@ -84,6 +84,18 @@ typedef enum { KV_TIER_EVICT_TOTAL = 0, KV_TIER_EVICT_PER_EVENT = 1 } kv_tier_ev
  *            and kv_tier_score_update are E_STATE (the exchange sits between the layers). */
 typedef enum { KV_TIER_SHARD_REQUEST = 0, KV_TIER_SHARD_KVHEAD = 1, KV_TIER_SHARD_SEQUENCE = 2 } kv_tier_shard;
 
+/* Tier policy of a5 (the paper's pure-eviction baselines, §4.1, on
+ * the same classify/migrate/decode path).  P = the protected set (prompt, sinks, window).
+ *   HIERARCHY  the paper's four tiers (Alg. 1): beta / r / f2 as configured.
+ *   STREAMING  StreamingLLM-style: every live non-protected token -> T3 (keep sinks + window).
+ *   H2O        heavy hitters: keep P + the top max(0, budget - |P|) live tokens by cumulative
+ *              score (ties: the newer token), the rest -> T3; no T1/T2.
+ *   RANDOM     as H2O but ranked by a seeded hash of (policy_seed, request, position)
+ *              (splitmix64, high 32 bits) instead of the score: uniform random removal.
+ * budget (H2O/RANDOM) counts kept tokens per request, protected ones included. */
+typedef enum { KV_TIER_POLICY_HIERARCHY = 0, KV_TIER_POLICY_STREAMING = 1, KV_TIER_POLICY_H2O = 2,
+               KV_TIER_POLICY_RANDOM = 3 } kv_tier_policy;
+
 #define KV_TIER_STAGING_ALL 0xFFFFFFFFu   /* differential mode: staging holds all of T1 (§3.4) */
 
 typedef struct {
@@ -110,6 +122,9 @@ typedef struct {
   int32_t  split;            /* CTAs per (request, kv head), <= 64; 0 = auto            */
   int32_t  variant;          /* decode kernel (consumer warps, stages): 0 (4,3) 1 (4,4)
                                 2 (8,2) 3 (8,3) 4 (4,2) 5 (4,6)                        */
+  int32_t  policy;           /* kv_tier_policy (0 = the paper's hierarchy)             */
+  int32_t  budget;           /* kept tokens per request (H2O / RANDOM)                 */
+  uint32_t policy_seed;      /* RANDOM                                                 */
 } kv_tier_config;
 
 typedef struct kv_tier_ctx kv_tier_ctx;

@@ -22,6 +22,9 @@ import numpy as np
 
 T0, T1, T2, T3 = 0, 1, 2, 3
 EVICT_TOTAL, EVICT_PER_EVENT = 0, 1
+# tier policies: the paper's hierarchy and its pure-eviction baselines (§4.1 P:276-280;
+# SPEC §baselines)
+POLICY_HIERARCHY, POLICY_STREAMING, POLICY_H2O, POLICY_RANDOM = 0, 1, 2, 3
 
 
 # ----------------------------------------------------------------- attention
@@ -165,7 +168,40 @@ def tier_counts(n_protected, n_live, n_t3, hbm_bp, evict_bp, t2_bp, mode=EVICT_T
     return n_new, n_hbm, n_t2, surv - n_hbm - n_t2
 
 
-def classify_request(S_part_b, tier_b, n, cfg):
+_M64 = (1 << 64) - 1
+
+
+def splitmix64(x):
+    """SplitMix64 finaliser on a Python int (mod 2^64): the counter-based generator the
+    RANDOM policy draws its keys from (each side of the parity test implements it)."""
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def random_key32(seed, req, pos):
+    """RANDOM policy rank key of (request, position): high 32 bits of
+    splitmix64(splitmix64(seed << 32 | req) ^ pos)."""
+    return splitmix64(splitmix64(((seed & 0xFFFFFFFF) << 32) | (req & 0xFFFFFFFF)) ^ pos) >> 32
+
+
+def policy_counts(policy, budget, n_protected, n_live, n_t3, cfg):
+    """(n_new_evict, n_hbm, n_t2, n_t1) of a manage event under a tier policy.
+
+    HIERARCHY: Alg. 1 (tier_counts).  STREAMING (StreamingLLM): keep only the
+    protected sinks + window, every live non-protected token is evicted.  H2O / RANDOM
+    (P:279-280): keep the protected set plus max(0, budget - |P|) live tokens,
+    all in HBM (pure eviction: no T1/T2)."""
+    if policy == POLICY_HIERARCHY:
+        return tier_counts(n_protected, n_live, n_t3, cfg.hbm_bp, cfg.evict_bp, cfg.t2_bp, cfg.evict_mode)
+    if policy == POLICY_STREAMING:
+        return n_live, 0, 0, 0
+    keep = min(n_live, max(0, budget - n_protected))
+    return n_live - keep, keep, 0, 0
+
+
+def classify_request(S_part_b, tier_b, n, cfg, req=0):
     """One manage event for one request (Alg. 1 lines P:189-197; §3.3).
 
     S_part_b: [H_kv][>=n] fp32, tier_b: [>=n] u8 current tiers (T3 sticky, AMB-16/24).
@@ -176,11 +212,15 @@ def classify_request(S_part_b, tier_b, n, cfg):
     t3 = old == T3
     live = ~prot & ~t3
     pos_live = np.nonzero(live)[0]
-    # order U_live by the unique key (bits(S_i), i) ascending (AMB-7)
-    order = np.lexsort((pos_live, S[pos_live].view(np.uint32)))
+    # order U_live by the unique key (bits(S_i), i) ascending (AMB-7); RANDOM: (hash, i)
+    if cfg.policy == POLICY_RANDOM:
+        primary = np.array([random_key32(cfg.policy_seed, req, int(p)) for p in pos_live], dtype=np.uint64)
+    else:
+        primary = S[pos_live].view(np.uint32)
+    order = np.lexsort((pos_live, primary))
     sorted_pos = pos_live[order]
-    n_new, n_hbm, n_t2, n_t1 = tier_counts(int(prot.sum()), len(pos_live), int(t3.sum()),
-                                           cfg.hbm_bp, cfg.evict_bp, cfg.t2_bp, cfg.evict_mode)
+    n_new, n_hbm, n_t2, n_t1 = policy_counts(cfg.policy, cfg.budget, int(prot.sum()), len(pos_live),
+                                             int(t3.sum()), cfg)
     new = np.full(n, T0, dtype=np.uint8)          # protected -> T0
     new[t3] = T3
     new[sorted_pos[:n_new]] = T3
@@ -207,6 +247,10 @@ class OracleConfig:
     evict_bp: int = 500
     t2_bp: int = 0
     evict_mode: int = EVICT_TOTAL
+    policy: int = POLICY_HIERARCHY
+    budget: int = 0
+    policy_seed: int = 0
+    req_ids: list = None       # the library's request index of each oracle request (RANDOM keys)
 
     @property
     def G(self):
@@ -322,7 +366,7 @@ def manage_event(st):
     B = st.tier.shape[0]
     for b in range(B):
         old = st.tier[b, :st.n].copy()
-        new = classify_request(st.S_part[b], old, st.n, cfg)
+        new = classify_request(st.S_part[b], old, st.n, cfg, req=cfg.req_ids[b] if cfg.req_ids else b)
         to_t2 = (new == T2) & (old != T2)
         from_t2 = (old == T2) & ((new == T0) | (new == T1))
         for p in np.nonzero(to_t2)[0]:

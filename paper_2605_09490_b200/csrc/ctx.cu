@@ -105,6 +105,10 @@ kv_tier_status validate(const kv_tier_config* c) {
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(nullptr, KV_TIER_E_INVAL, "need 0 <= rank < world");
   if (c->split < 0 || c->split > 64) return fail(nullptr, KV_TIER_E_INVAL, "split must be in [0, 64]");
   if (c->variant < 0 || c->variant > 5) return fail(nullptr, KV_TIER_E_INVAL, "variant must be in [0, 5]");
+  if (c->policy < KV_TIER_POLICY_HIERARCHY || c->policy > KV_TIER_POLICY_RANDOM)
+    return fail(nullptr, KV_TIER_E_INVAL, "policy must be a kv_tier_policy");
+  if ((c->policy == KV_TIER_POLICY_H2O || c->policy == KV_TIER_POLICY_RANDOM) && c->budget < 1)
+    return fail(nullptr, KV_TIER_E_INVAL, "H2O / RANDOM need budget >= 1 kept tokens per request");
   return KV_TIER_OK;
 }
 
@@ -265,6 +269,9 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.P = cfg->prompt_len; v.ks = cfg->sink_size; v.kw = cfg->window_size;
   v.hbm_bp = (int)cfg->hbm_ratio_bp; v.evict_bp = (int)cfg->evict_ratio_bp; v.t2_bp = (int)cfg->t2_fraction_bp;
   v.evict_mode = cfg->evict_mode;
+  v.policy = cfg->policy;
+  v.budget = cfg->budget;
+  v.policy_seed = cfg->policy_seed;
   v.stream_mode = cfg->staging_tokens == 0;
   v.out_fp32 = cfg->out_fp32;
   v.split = auto_split(*cfg);
@@ -711,11 +718,10 @@ static kv_tier_status classify_impl(kv_tier_ctx* ctx, const float* Sx, int parts
   const kv_tier_config& c = ctx->cfg;
   const long long n = ctx->n, np = n_protected(c, ctx->n), n3 = ctx->c[3];
   const long long nl = n - np - n3;
-  long long n_new = c.evict_mode == 0 ? std::max(0LL, ((long long)c.evict_ratio_bp * (nl + n3)) / 10000 - n3)
-                                      : ((long long)c.evict_ratio_bp * nl) / 10000;
+  long long n_new, n_hbm, n_t2;
+  policy_counts(c.policy, c.budget, (int)c.hbm_ratio_bp, (int)c.evict_ratio_bp, (int)c.t2_fraction_bp, c.evict_mode,
+                np, nl, n3, &n_new, &n_hbm, &n_t2);
   const long long surv = nl - n_new;
-  const long long n_hbm = ((long long)c.hbm_ratio_bp * surv) / 10000;
-  const long long n_t2 = ((long long)c.t2_fraction_bp * (surv - n_hbm)) / 10000;
   const int p0 = (int)(np + n_hbm), p1 = (int)(surv - n_hbm - n_t2), p2 = (int)n_t2, p3 = (int)(n3 + n_new);
   if (p0 > ctx->v.cap0 || p1 > ctx->v.cap1 || p2 > ctx->v.cap2)
     return fail(ctx, KV_TIER_E_CAPACITY, "tier counts %d/%d/%d exceed capacities %d/%d/%d", p0, p1, p2,

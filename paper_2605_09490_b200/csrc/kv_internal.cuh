@@ -32,6 +32,8 @@ struct DevView {
   int cap0, cap1, cap2;
   int P, ks, kw;
   int hbm_bp, evict_bp, t2_bp, evict_mode;
+  int policy, budget;   // kv_tier_policy (tier policy of a5), kept tokens (H2O / RANDOM)
+  unsigned policy_seed;
   int stream_mode;      // staging_tokens == 0
   int out_fp32;
   int split;            // CTAs per (b, g) cluster
@@ -80,6 +82,44 @@ struct DevView {
   __nv_bfloat16* hk1; __nv_bfloat16* hv1;            // pinned host T1 [L][B][Hkv][Nmax][D] (mapped)
   int8_t* hc2k; int8_t* hc2v; float* hs2k; float* hs2v;   // pinned host T2 (mapped, may be null)
 };
+
+// RANDOM tier policy: rank key of (request, position) = high 32 bits of
+// splitmix64(splitmix64(seed << 32 | req) ^ pos) (the oracle implements the same generator).
+__host__ __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__host__ __device__ __forceinline__ unsigned random_key32(unsigned seed, int req, int pos) {
+  return (unsigned)(splitmix64(splitmix64(((unsigned long long)seed << 32) | (unsigned)req) ^ (unsigned)pos) >> 32);
+}
+// (n_new, n_hbm, n_t2) of a manage event under the tier policy (kv_tier.h kv_tier_policy)
+__host__ __device__ __forceinline__ void policy_counts(int policy, int budget, int hbm_bp, int evict_bp, int t2_bp,
+                                                       int evict_mode, long long n_prot, long long nl, long long n3,
+                                                       long long* n_new, long long* n_hbm, long long* n_t2) {
+  if (policy == 1) {                 // STREAMING: only the protected sinks + window stay
+    *n_new = nl; *n_hbm = 0; *n_t2 = 0;
+    return;
+  }
+  if (policy == 2 || policy == 3) {  // H2O / RANDOM: protected + the top budget - |P| live tokens
+    long long keep = budget - n_prot;
+    keep = keep < 0 ? 0 : (keep > nl ? nl : keep);
+    *n_new = nl - keep; *n_hbm = keep; *n_t2 = 0;
+    return;
+  }
+  long long nn;                      // HIERARCHY: Alg. 1 floors in basis points (AMB-8/9/11)
+  if (evict_mode == 0) {
+    nn = ((long long)evict_bp * (nl + n3)) / 10000 - n3;
+    if (nn < 0) nn = 0;
+  } else {
+    nn = ((long long)evict_bp * nl) / 10000;
+  }
+  const long long surv = nl - nn;
+  *n_new = nn;
+  *n_hbm = ((long long)hbm_bp * surv) / 10000;
+  *n_t2 = ((long long)t2_bp * (surv - *n_hbm)) / 10000;
+}
 
 // Sequence sharding: block-cyclic ownership of SEQ_BLOCK-position blocks.
 // A rank's tier stores and index lists hold only its own positions; the tier array and the

@@ -187,18 +187,12 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
   if (bad) atomicOr(&v.st->err, 1);
   __syncthreads();
   if (tid == 0) {
-    // Alg. 1 floor arithmetic in integer basis points (AMB-8/9/11)
+    // Alg. 1 floor arithmetic in integer basis points (AMB-8/9/11), or the
+    // pure-eviction baselines' counts (tier policy)
     const long long nl = s_cnt[0], n3 = s_cnt[1];
-    long long n_new;
-    if (v.evict_mode == 0) {
-      n_new = ((long long)v.evict_bp * (nl + n3)) / 10000 - n3;
-      if (n_new < 0) n_new = 0;
-    } else {
-      n_new = ((long long)v.evict_bp * nl) / 10000;
-    }
-    const long long surv = nl - n_new;
-    const long long n_hbm = ((long long)v.hbm_bp * surv) / 10000;
-    const long long n_t2 = ((long long)v.t2_bp * (surv - n_hbm)) / 10000;
+    const long long n_prot = (long long)min(prot_lo, n) + (n - max(max(prot_hi, 0), min(prot_lo, n)));
+    long long n_new, n_hbm, n_t2;
+    policy_counts(v.policy, v.budget, v.hbm_bp, v.evict_bp, v.t2_bp, v.evict_mode, n_prot, nl, n3, &n_new, &n_hbm, &n_t2);
     const long long rk[3] = {n_new, n_new + n_t2, nl - n_hbm};
     for (int k = 0; k < 3; ++k) {
       s_active[k] = rk[k] < nl;
@@ -214,7 +208,8 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
     __syncthreads();
     for (int pos = tid; pos < n; pos += CLS_THREADS) {
       if (told[pos] == T3 || pos < prot_lo || pos >= prot_hi) continue;
-      const unsigned long long key = ((unsigned long long)__float_as_uint(fS[pos]) << 32) | (unsigned)pos;
+      const unsigned long long key = ((unsigned long long)(v.policy == 3 ? random_key32(v.policy_seed, b, pos)
+                                                                          : __float_as_uint(fS[pos])) << 32) | (unsigned)pos;
       const unsigned dig = (unsigned)(key >> shift) & 255u;
 #pragma unroll
       for (int k = 0; k < 3; ++k)
@@ -266,7 +261,8 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
       if (to == T3) t = T3;
       else if (pos < prot_lo || pos >= prot_hi) t = T0;
       else {
-        const unsigned long long key = ((unsigned long long)__float_as_uint(fS[pos]) << 32) | (unsigned)pos;
+        const unsigned long long key = ((unsigned long long)(v.policy == 3 ? random_key32(v.policy_seed, b, pos)
+                                                                            : __float_as_uint(fS[pos])) << 32) | (unsigned)pos;
         t = key < thr_e ? T3 : key < thr_2 ? T2 : key < thr_1 ? T1 : T0;
       }
       tnew[pos] = (uint8_t)t;

@@ -48,7 +48,9 @@ class TieredDecode:
         self.cfg = kt.make_config(B, L, hl * G, hl, d, self.n0 + T, P, hbm_bp=w["hbm_bp"], evict_bp=w["evict_bp"],
                                   t2_bp=w["t2_bp"], manage_interval=w["interval"], evict_mode=w["evict_mode"],
                                   staging=w["staging"], device=self.dev.index or 0, out_fp32=int(out_fp32),
-                                  split=split, variant=variant, shard=shard, rank=rank, world=world)
+                                  split=split, variant=variant, shard=shard, rank=rank, world=world,
+                                  policy=w.get("policy", 0), budget=w.get("budget", 0),
+                                  policy_seed=w.get("policy_seed", 0))
         hs = slice(h0, h0 + hl)
         qs = slice(h0 * G, (h0 + hl) * G)
         self.kv = kt.KvTier(self.cfg)

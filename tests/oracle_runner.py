@@ -19,7 +19,9 @@ class OracleRun:
         self.Q = S.gen_q(seed, 0, T, L, B, Hq, Hkv, d, reqs=self.reqs)
         self.cfg = O.OracleConfig(B=len(self.reqs), L=L, Hq=Hq, Hkv=Hkv, d=d, prompt_len=P,
                                   manage_interval=w["interval"], hbm_bp=w["hbm_bp"], evict_bp=w["evict_bp"],
-                                  t2_bp=w.get("t2_bp", 0), evict_mode=w.get("evict_mode", 0))
+                                  t2_bp=w.get("t2_bp", 0), evict_mode=w.get("evict_mode", 0),
+                                  policy=w.get("policy", 0), budget=w.get("budget", 0),
+                                  policy_seed=w.get("policy_seed", 0), req_ids=self.reqs)
         self.st = O.init_state(self.cfg, self.K, self.V, n0)
 
     def step(self):

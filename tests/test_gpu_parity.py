@@ -518,3 +518,19 @@ def test_sequence_sharding_two_processes():
         p.join(timeout=120)
     for rank, status, wo, ws in res:
         assert status == "ok", (rank, status)
+
+
+# --------------------------------------------------------------------- tier policies (§8f N3)
+@pytest.mark.parametrize("policy,budget", [(kt.POLICY_STREAMING, 0), (kt.POLICY_H2O, 300), (kt.POLICY_RANDOM, 300)])
+def test_tier_policy_parity(policy, budget):
+    # the paper's pure-eviction baselines on the same classify/migrate/decode path
+    w = H.workload("tiny", B=3, L=2, Hq=8, Hkv=2, d=128, N=640, P=32, interval=8, steps=26,
+                   hbm_bp=5000, evict_bp=500, t2_bp=0, policy=policy, budget=budget, policy_seed=11)
+    _run_pair(w, graph=True, check_every=4)
+
+
+def test_random_policy_request_keys_sampled_requests():
+    # RANDOM keys depend on the request index: the oracle runs only requests 1 and 3
+    w = H.workload("tiny", B=4, L=1, Hq=4, Hkv=2, d=64, N=500, P=16, interval=8, steps=18,
+                   hbm_bp=5000, evict_bp=500, t2_bp=0, policy=kt.POLICY_RANDOM, budget=250, policy_seed=5)
+    _run_pair(w, reqs=[1, 3], graph=True, check_every=8)

@@ -424,3 +424,84 @@ def test_generator_long_tail_calibration():                     # P:76 (top-20% 
     s = np.sort(O.total_score_fp32(st.S_part[0][:, :st.n]))[::-1]
     share = s[: len(s) // 5].sum() / s.sum()
     assert 0.50 < share < 0.66, share
+
+
+# --------------------------------------------------------------------- tier policies
+def _pol_cfg(policy, budget=0, seed=0, P=4, ks=2, kw=3):
+    return O.OracleConfig(B=1, L=1, Hq=1, Hkv=1, d=2, prompt_len=P, sink_size=ks, window_size=kw,
+                          policy=policy, budget=budget, policy_seed=seed)
+
+
+def test_splitmix64_reference_value():
+    # first output of SplitMix64 from state 0 (the published reference value)
+    assert O.splitmix64(0) == 0xE220A8397B1DCDAF
+
+
+def test_streaming_keeps_exactly_the_protected_set():
+    # StreamingLLM: sinks + window (+ prompt) survive, everything else is evicted
+    n = 30
+    cfg = _pol_cfg(O.POLICY_STREAMING)
+    S = np.random.default_rng(1).random((1, n)).astype(np.float32)
+    new = O.classify_request(S, np.zeros(n, np.uint8), n, cfg)
+    prot = O.protected_mask(n, cfg.prompt_len, cfg.sink_size, cfg.window_size)
+    assert np.array_equal(new == O.T0, prot) and np.array_equal(new == O.T3, ~prot)
+
+
+def test_h2o_uniform_scores_reduce_to_recency():
+    # uniform scores -> the tie-break keeps the newest tokens
+    n, budget = 40, 15
+    cfg = _pol_cfg(O.POLICY_H2O, budget=budget)
+    new = O.classify_request(np.ones((1, n), np.float32), np.zeros(n, np.uint8), n, cfg)
+    prot = O.protected_mask(n, cfg.prompt_len, cfg.sink_size, cfg.window_size)
+    live = [p for p in range(n) if not prot[p]]
+    keep = budget - int(prot.sum())
+    assert [p for p in live if new[p] == O.T0] == live[-keep:]
+    assert int((new == O.T0).sum()) == budget and set(np.unique(new)) <= {O.T0, O.T3}
+
+
+def test_h2o_sort_and_take_brute_force():
+    # distinct scores -> keep P plus the top budget - |P| live tokens by score
+    rng = np.random.default_rng(7)
+    for trial in range(20):
+        n = int(rng.integers(12, 60))
+        budget = int(rng.integers(1, n + 5))
+        cfg = _pol_cfg(O.POLICY_H2O, budget=budget, P=int(rng.integers(0, 5)))
+        S = rng.permutation(n).astype(np.float32)[None] * 0.25
+        new = O.classify_request(S, np.zeros(n, np.uint8), n, cfg)
+        prot = O.protected_mask(n, cfg.prompt_len, cfg.sink_size, cfg.window_size)
+        live = [p for p in range(n) if not prot[p]]
+        keep = min(len(live), max(0, budget - int(prot.sum())))
+        top = sorted(live, key=lambda p: -S[0, p])[:keep]
+        want = set(np.nonzero(prot)[0]) | set(top)
+        assert set(np.nonzero(new == O.T0)[0]) == want and int((new == O.T3).sum()) == n - len(want)
+
+
+def test_random_policy_determinism_and_uniformity():
+    # deterministic given the seed; every live position kept with frequency keep/|U|
+    n, budget = 40, 20
+    cfg = _pol_cfg(O.POLICY_RANDOM, budget=budget, seed=3)
+    S = np.zeros((1, n), np.float32)
+    a = O.classify_request(S, np.zeros(n, np.uint8), n, cfg)
+    b = O.classify_request(S, np.zeros(n, np.uint8), n, cfg)
+    assert np.array_equal(a, b)
+    prot = O.protected_mask(n, cfg.prompt_len, cfg.sink_size, cfg.window_size)
+    live = np.nonzero(~prot)[0]
+    keep = budget - int(prot.sum())
+    freq = np.zeros(n)
+    trials = 600
+    for seed in range(trials):
+        c = _pol_cfg(O.POLICY_RANDOM, budget=budget, seed=seed)
+        freq += O.classify_request(S, np.zeros(n, np.uint8), n, c) == O.T0
+    f = freq[live] / trials
+    assert np.all(freq[prot] == trials)
+    assert abs(f.mean() - keep / len(live)) < 1e-9                 # exactly `keep` per draw
+    assert np.all(np.abs(f - keep / len(live)) < 0.1)              # uniform over positions
+
+
+def test_policy_budget_covers_everything():
+    # budget >= n keeps all
+    n = 25
+    for pol in (O.POLICY_H2O, O.POLICY_RANDOM):
+        new = O.classify_request(np.random.default_rng(2).random((1, n)).astype(np.float32),
+                                 np.zeros(n, np.uint8), n, _pol_cfg(pol, budget=n + 3, seed=1))
+        assert np.all(new == O.T0)
