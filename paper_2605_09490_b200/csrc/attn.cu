@@ -41,7 +41,7 @@ namespace kvt {
 
 // Variants (consumer warps NW, pipeline stages NST): a tile is 16 tokens per consumer warp.
 
-template <int D, int NW, int NST>
+template <int D, int NW, int NST, bool CM>
 __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     k_decode_attn(const DevView v, const int layer, const __nv_bfloat16* __restrict__ q,
                   const __nv_bfloat16* __restrict__ knew, const __nv_bfloat16* __restrict__ vnew,
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
                                          // cluster merge: [C+1][m 8 | l 8 | o slice] (16-B aligned)
   const int cm_per = (((v.G * D + C - 1) / C) + 3) & ~3;                  // o floats per rank slice
   const int cm_rb = cm_per + 16;
-  const bool cm = v.cluster_merge != 0;
+  constexpr bool cm = CM;   // cluster-merge instantiation (KVTIER_CLUSTER=1); the default kernel carries no cluster code
 
   // ---------------------------------------------------------------- prologue (pre-PDL-wait)
   const int cur = v.st->cur;
@@ -933,7 +933,10 @@ size_t attn_smem_bytes(const DevView& v) {
 
 template <int D, int NW, int NST>
 static cudaError_t configure_k(const DevView& v) {
-  cudaError_t e = cudaFuncSetAttribute(k_decode_attn<D, NW, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (v.cluster_merge)
+    return cudaFuncSetAttribute(k_decode_attn<D, NW, NST, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)attn_smem_bytes(v));
+  cudaError_t e = cudaFuncSetAttribute(k_decode_attn<D, NW, NST, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)attn_smem_bytes(v));
   return e;
 }
@@ -942,7 +945,11 @@ template <int D, int NW, int NST>
 static cudaError_t launch_k(const DevView& v, cudaLaunchConfig_t& cfg, int layer, const void* q, const void* knew,
                             const void* vnew, void* o, int zpar) {
   cfg.blockDim = dim3((NW + 2) * 32, 1, 1);
-  return cudaLaunchKernelEx(&cfg, k_decode_attn<D, NW, NST>, v, layer, reinterpret_cast<const __nv_bfloat16*>(q),
+  if (v.cluster_merge)
+    return cudaLaunchKernelEx(&cfg, k_decode_attn<D, NW, NST, true>, v, layer, reinterpret_cast<const __nv_bfloat16*>(q),
+                              reinterpret_cast<const __nv_bfloat16*>(knew), reinterpret_cast<const __nv_bfloat16*>(vnew),
+                              o, zpar);
+  return cudaLaunchKernelEx(&cfg, k_decode_attn<D, NW, NST, false>, v, layer, reinterpret_cast<const __nv_bfloat16*>(q),
                             reinterpret_cast<const __nv_bfloat16*>(knew), reinterpret_cast<const __nv_bfloat16*>(vnew),
                             o, zpar);
 }

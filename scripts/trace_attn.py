@@ -19,12 +19,14 @@ ap.add_argument("--config", default="7b")
 ap.add_argument("--split", type=int, default=0)
 ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--graph", type=int, default=1)
+ap.add_argument("--policy", type=int, default=0, help="kv_tier_policy (1 = streaming: tiny layers, the chain's latency floor)")
+ap.add_argument("--budget", type=int, default=0)
 a = ap.parse_args()
-w = H.workload(a.config, steps=4)
+w = H.workload(a.config, steps=70 if a.policy else 4, policy=a.policy, budget=a.budget)
 run = H.TieredDecode(w, out_fp32=False, split=a.split, variant=a.variant)
 if a.graph:
     run.capture()
-for _ in range(3):
+for _ in range(w["steps"] - 1):
     run.step()
 run.sync()
 tr = run.kv.debug_trace().astype(np.int64)        # [L][CTAs][8], last step
