@@ -41,6 +41,100 @@ namespace kvt {
 
 // Variants (consumer warps NW, pipeline stages NST): a tile is 16 tokens per consumer warp.
 
+__device__ __forceinline__ int atom_add_acqrel_gpu(int* p, int x) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(x) : "memory");
+  return old;
+}
+
+// KVTIER_LASTMERGE=1: the unit's C partials + the new-token partial are merged by the CTA whose
+// release-add completes the unit's count (no merge kernel, one kernel boundary per layer
+// fewer).  Same arithmetic and order as k_decode_merge.  Called by the NCONS consumer threads
+// after their partial stores; rank 0 first waits (named barrier 3) for its side warp's partial.
+template <int D, int NCONS>
+__device__ __forceinline__ void last_cta_merge(const DevView& v, int unit, int b, int g, int C, int zpar, void* o,
+                                               unsigned char* scratch, int tid, bool rank0) {
+  if (rank0) asm volatile("bar.sync 3, %0;\n" ::"r"(NCONS + 32) : "memory");
+  else named_sync(1, NCONS);
+  float* sf = reinterpret_cast<float*>(scratch);      // [NP][8] m -> factors
+  float* sl = sf + 65 * 8;                            // [NP][8] l
+  float* sI = sl + 65 * 8;                            // [8] 1/L
+  int* sflag = reinterpret_cast<int*>(sI + 8);
+  if (tid == 0) sflag[0] = atom_add_acqrel_gpu(v.unit_ctr + unit, 1) == C - 1;
+  named_sync(1, NCONS);
+  if (!sflag[0]) return;
+  const int G = v.G, NP = C + 1, tot4 = G * D / 4;
+  const float* P = v.part + (size_t)unit * NP * v.part_stride;
+  constexpr int NE = (8 * D / 4 + NCONS - 1) / NCONS, MAXP = 9;
+  float4 x[NE][MAXP];
+#pragma unroll
+  for (int k = 0; k < NE; ++k)
+#pragma unroll
+    for (int c = 0; c < MAXP; ++c)
+      if (c < NP && tid + k * NCONS < tot4)
+        x[k][c] = __ldcg(reinterpret_cast<const float4*>(P + (size_t)c * v.part_stride + 16) + tid + k * NCONS);
+  for (int i = tid; i < NP * 8; i += NCONS) {
+    sf[i] = __ldcg(P + (size_t)(i >> 3) * v.part_stride + (i & 7));
+    sl[i] = __ldcg(P + (size_t)(i >> 3) * v.part_stride + 8 + (i & 7));
+  }
+  named_sync(1, NCONS);
+  if (tid < 8) {
+    const int h = tid;
+    float M = -INFINITY;
+    for (int c = 0; c < NP; ++c) M = fmaxf(M, sf[c * 8 + h]);
+    float Ls = 0.f;
+    for (int c = 0; c < NP; ++c) {
+      const float mc = sf[c * 8 + h];
+      const float f = mc == -INFINITY ? 0.f : ex2_ftz(mc - M);
+      sf[c * 8 + h] = f;
+      Ls += f * sl[c * 8 + h];
+    }
+    const float invL = Ls > 0.f ? 1.0f / Ls : 0.f;
+    sI[h] = invL;
+    if (h < G && zpar >= 0) {
+      float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
+      ml[h] = M;
+      ml[8 + h] = invL;
+    }
+  }
+  named_sync(1, NCONS);
+#pragma unroll
+  for (int k = 0; k < NE; ++k) {
+    const int j = tid + k * NCONS;
+    if (j >= tot4) continue;
+    const int h = (4 * j) / D;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = 0; c0 < NP; c0 += MAXP) {
+      if (c0 > 0) {
+#pragma unroll
+        for (int c = 0; c < MAXP; ++c)
+          if (c0 + c < NP) x[k][c] = __ldcg(reinterpret_cast<const float4*>(P + (size_t)(c0 + c) * v.part_stride + 16) + j);
+      }
+#pragma unroll
+      for (int c = 0; c < MAXP; ++c)
+        if (c0 + c < NP) {
+          const float f = sf[(c0 + c) * 8 + h];
+          acc.x += f * x[k][c].x;
+          acc.y += f * x[k][c].y;
+          acc.z += f * x[k][c].z;
+          acc.w += f * x[k][c].w;
+        }
+    }
+    const float il = sI[h];
+    const size_t oi = ((size_t)b * v.Hq + g * G) * D + 4 * j;
+    if (v.out_fp32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(o) + oi) = make_float4(acc.x * il, acc.y * il, acc.z * il, acc.w * il);
+    } else {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * il, acc.y * il), hi = __floats2bfloat162_rn(acc.z * il, acc.w * il);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o) + oi) = pk;
+    }
+  }
+  if (tid == 0) v.unit_ctr[unit] = 0;                 // next launch touches it after this grid completes
+}
+
 template <int D, int NW, int NST, bool CM>
 __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     k_decode_attn(const DevView v, const int layer, const __nv_bfloat16* __restrict__ q,
@@ -350,6 +444,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       float* part = v.part + ((size_t)unit * (C + 1) + C) * v.part_stride;
       for (int e = lane; e < 16 + G * D; e += 32) part[e] = e < 8 ? -INFINITY : 0.f;
     }
+    if (!cm && v.last_merge && r == 0) asm volatile("bar.arrive 3, %0;\n" ::"r"(NCONS + 32) : "memory");
     if (cm) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
     return;
   }
@@ -591,6 +686,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       part[16 + e] = a;
     }
     if (tr && tid == 0) tr[4] = gtimer();
+    if (v.last_merge) last_cta_merge<D, NCONS>(v, unit, b, g, C, zpar, o, ring + NW * 8 * OWS * 4, tid, r == 0);
     return;
   }
   float* fw = ow + NW * 8 * OWS;       // [NW][8] warp factors exp2(m_w - M)
@@ -1046,7 +1142,7 @@ static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, 
 cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
                                void* o, int zpar, int pdl, cudaStream_t s, float* lse) {
   cudaError_t e = launch_decode_main(v, layer, q, knew, vnew, o, zpar, pdl, s);
-  if (e != cudaSuccess || v.cluster_merge) return e;
+  if (e != cudaSuccess || v.cluster_merge || (v.last_merge && !lse)) return e;
   return launch_merge(v, layer, o, zpar, v.use_pdl, s, lse);
 }
 

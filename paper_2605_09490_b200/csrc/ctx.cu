@@ -308,6 +308,8 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     v.l2pf_bytes = l2mb * (1LL << 20) / std::max(1, v.nc);
     v.inflight = getenv("KVTIER_INFLIGHT") ? atoi(getenv("KVTIER_INFLIGHT")) : 0;
     v.score_lean = getenv("KVTIER_SCORE_LEAN") ? atoi(getenv("KVTIER_SCORE_LEAN")) : 0;   // measured slower
+    v.last_merge = getenv("KVTIER_LASTMERGE") ? atoi(getenv("KVTIER_LASTMERGE")) : 0;
+    if (v.seq_w > 1) v.last_merge = 0;      // sequence shards need the merge kernel's (m, l) output
     v.score_grid = getenv("KVTIER_SCORE_GRID") ? atoi(getenv("KVTIER_SCORE_GRID")) : (v.score_lean ? 296 : 148);
   }
   for (int i = 0; i < 2; ++i) {
@@ -619,7 +621,8 @@ kv_tier_status kv_tier_decode_attention_lse(kv_tier_ctx* ctx, int32_t layer, con
                                             void* stream) {
   if (!lse) return fail(ctx, KV_TIER_E_INVAL, "null lse");
   if (ctx && ctx->v.flat) return fail(ctx, KV_TIER_E_STATE, "decode_attention_lse runs the split kernel (KVTIER_FLAT=0)");
-  if (ctx && ctx->v.cluster_merge) return fail(ctx, KV_TIER_E_STATE, "decode_attention_lse needs the merge kernel (KVTIER_CLUSTER=0)");
+  if (ctx && (ctx->v.cluster_merge || ctx->v.last_merge))
+    return fail(ctx, KV_TIER_E_STATE, "decode_attention_lse needs the merge kernel (KVTIER_CLUSTER=0, KVTIER_LASTMERGE=0)");
   return decode_attention_impl(ctx, layer, q, k_new, v_new, o, fuse_score_update, stream, 0, lse);
 }
 

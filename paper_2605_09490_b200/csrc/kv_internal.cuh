@@ -49,7 +49,8 @@ struct DevView {
   int nc;               // flat kernel grid (CTAs; one per SM)
   int seq_w, seq_r;
   int score_grid;       // CTAs of the score-flush kernel (runs beside the attention chain)
-  int score_lean;       // 1: register-lean score-flush kernel (fits beside two decode CTAs)     // sequence sharding: positions in 64-blocks, block k owned by rank k % seq_w
+  int score_lean;       // 1: register-lean score-flush kernel (fits beside two decode CTAs)
+  int last_merge;       // 1: the CTA completing a unit merges its partials (no merge kernel)     // sequence sharding: positions in 64-blocks, block k owned by rank k % seq_w
   int spin_hint;        // mbarrier try_wait suspend-time hint in ns (0: plain polling)
   long long l2pf_bytes; // flat kernel: K/V bytes per CTA requested into L2 at kernel start (0: off)
   int inflight;         // flat kernel: max ring stages requested but not landed (0: the whole ring)
