@@ -163,6 +163,16 @@ def test_7b_sampled_requests():               # BASELINE.json configs[1], bench 
     _run_pair(w, reqs=[0, 5], graph=True, check_every=16)
 
 
+# --------------------------------------------------------------------- larger BASELINE shapes, sampled
+@pytest.mark.parametrize("name,B,req,steps", [("14b", 2, 1, 2), ("32b", 1, 0, 2), ("70b", 1, 0, 1)])
+def test_large_shapes_sampled_requests(name, B, req, steps):
+    # BASELINE.json configs[2..4] per-request shapes (all layers, heads and tokens; fewer
+    # requests so one GPU and the CPU oracle fit): the t = 0 event (+ one step) through the
+    # bench's launch configuration (step graph, PDL chain), one request checked
+    w = H.workload(name, B=B, steps=steps)
+    _run_pair(w, reqs=[req], graph=True, check_every=1)
+
+
 # --------------------------------------------------------------------- classify cross-fed
 @pytest.mark.parametrize("kind", ["ties", "cont"])
 def test_classify_crossfed_bit_exact(kind):   # AMB-18 (i): identical S -> identical tiers
