@@ -434,7 +434,7 @@ def run_split(w, args):
     if args.split:
         return args.split
     units = w["B"] * w["Hkv"]
-    return max(1, min(8, (2 * 148 + units - 1) // units))
+    return max(1, min(8, (2 * 148) // units))
 
 
 if __name__ == "__main__":

@@ -1082,7 +1082,7 @@ static cudaError_t launch_decode_main(const DevView& v, int layer, const void* q
     at[na].id = cudaLaunchAttributeAccessPolicyWindow;
     at[na].val.accessPolicyWindow.base_ptr = v.hot_base;
     at[na].val.accessPolicyWindow.num_bytes = v.hot_bytes;
-    at[na].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[na].val.accessPolicyWindow.hitRatio = v.hot_hit;
     at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     ++na;
@@ -1123,7 +1123,7 @@ static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, 
     at[na].id = cudaLaunchAttributeAccessPolicyWindow;
     at[na].val.accessPolicyWindow.base_ptr = v.hot_base;
     at[na].val.accessPolicyWindow.num_bytes = v.hot_bytes;
-    at[na].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[na].val.accessPolicyWindow.hitRatio = v.hot_hit;
     at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     ++na;

@@ -919,7 +919,7 @@ cudaError_t launch_decode_flat(const DevView& v, int layer, const void* q, const
     at[na].id = cudaLaunchAttributeAccessPolicyWindow;
     at[na].val.accessPolicyWindow.base_ptr = v.hot_base;
     at[na].val.accessPolicyWindow.num_bytes = v.hot_bytes;
-    at[na].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[na].val.accessPolicyWindow.hitRatio = v.hot_hit;
     at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     ++na;

@@ -71,18 +71,15 @@ kv_tier_status cuda_check(kv_tier_ctx* ctx, cudaError_t e, const char* what) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 int round16(long long x) { return (int)((x + 15) / 16 * 16); }
 
+// CTAs per unit: one wave of at most 2 decode CTAs per SM (rounding up would start a second,
+// partial wave: measured at 14B, 3 -> 2 CTAs per unit took 382 -> 401 steps/s)
 int split_of(const kv_tier_config& c) {
   if (c.split > 0) return c.split;
   const int units = c.num_requests * c.num_kv_heads;
-  return std::max(1, std::min(8, (2 * 148 + units - 1) / units));
+  return std::max(1, std::min(8, (2 * 148) / units));
 }
 
-int auto_split(const kv_tier_config& c) {
-  if (c.split > 0) return c.split;
-  const int units = c.num_requests * c.num_kv_heads;
-  int s = (2 * 148 + units - 1) / units;
-  return std::max(1, std::min(8, s));
-}
+int auto_split(const kv_tier_config& c) { return split_of(c); }
 
 kv_tier_status validate(const kv_tier_config* c) {
   if (!c) return fail(nullptr, KV_TIER_E_INVAL, "null config");
@@ -392,6 +389,10 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     int maxw = 0;
     cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, cfg->device);
     v.hot_bytes = std::min<size_t>(v.hot_bytes, (size_t)maxw);
+    // the persisting share of the window must fit the carve-out, or the hot lines evict each other
+    size_t lim = 0;
+    cudaDeviceGetLimit(&lim, cudaLimitPersistingL2CacheSize);
+    v.hot_hit = v.hot_bytes > 0 ? (float)std::min(1.0, (double)lim / (double)v.hot_bytes) : 0.f;
     cudaGetLastError();                  // persistence is an optimisation: ignore if unsupported
   }
   if (e == cudaSuccess) e = v.flat ? flat_configure(v) : attn_configure(v);

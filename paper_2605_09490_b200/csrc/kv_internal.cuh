@@ -9,7 +9,7 @@ namespace kvt {
 constexpr int T0 = 0, T1 = 1, T2 = 2, T3 = 3;
 constexpr int NTRACE = 24;        // debug trace slots per CTA (KVTIER_TRACE=1)
 constexpr int CNT_STRIDE = 8;     // cnt[buf][b][8]: |T0| |T1| |T2| |T3| |visible at event| pad..
-constexpr int ZRING = 8;          // logits/ML ring slots (score kernels lag the decode chain)
+constexpr int ZRING = 4;          // logits/ML ring slots (score kernels lag the decode chain)
 constexpr int ZBATCH = 1;         // launches whose score updates one score kernel applies (layer order;
                                   // measured: batching 4 made the kernel too big to share SMs with the chain)
 
@@ -63,6 +63,7 @@ struct DevView {
   int* unit_ctr;        // [B*Hkv] partials published per unit (flat kernel; reset by the merging CTA)
   void* hot_base;       // L2 access-policy window over the small hot buffers
   size_t hot_bytes;
+  float hot_hit;        // hitRatio of the window: persisting carve-out / window bytes (<= 1)
   int4* moves;          // [B][mcap] {src tier, src row, dst tier | dst row << 2, position}
   int* mcount;          // [B] moves of the last plan (<= mcap)
   int mcap;

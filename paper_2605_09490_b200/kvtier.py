@@ -307,7 +307,7 @@ class KvTier:
         if self.cfg.split:
             return self.cfg.split
         units = self.cfg.num_requests * self.cfg.num_kv_heads
-        return max(1, min(8, (2 * 148 + units - 1) // units))
+        return max(1, min(8, (2 * 148) // units))
 
     def import_scores(self, S):
         S = np.ascontiguousarray(S, dtype=np.float32)
