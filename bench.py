@@ -52,6 +52,8 @@ def _args():
     ap.add_argument("--policy", default="hierarchy", choices=list(POLICIES),
                     help="tier policy: the paper's hierarchy or a pure-eviction baseline (P:276-280)")
     ap.add_argument("--budget", type=int, default=1024, help="kept tokens per request (h2o / random)")
+    ap.add_argument("--scorer", default="attention", choices=["attention", "vatp"],
+                    help="a4 token scorer: Eq. 1 attention or VATP (attention x ||v||, P:712)""")
     ap.add_argument("--no-extras", action="store_true", help="skip control/e2e/stream/cpu legs")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -209,7 +211,8 @@ def main():
     E = 0 if args.no_extras else min(K, 64)
     pol = POLICIES[args.policy]
     w = H.workload(args.config, hbm_bp=args.hbm, evict_bp=args.evict, steps=W + K + E + 1, policy=pol,
-                   budget=args.budget if pol in (2, 3) else 0, policy_seed=7)
+                   budget=args.budget if pol in (2, 3) else 0, policy_seed=7,
+                   scorer=1 if args.scorer == "vatp" else 0)
     dev = f"cuda:{local}"
     peaks = _peaks()
     from paper_2605_09490_b200.dist import shard_plan
@@ -408,7 +411,8 @@ def main():
                                    f"Hq/Hkv={w['Hq']}/{Hkv} d={d} N={w['N']} beta={args.hbm}bp r={args.evict}bp "
                                    f"Delta={w['interval']} differential staging"
                                    + ("" if pol == 0 else f" policy={args.policy}"
-                                      + (f" budget={args.budget}" if pol in (2, 3) else "")),
+                                      + (f" budget={args.budget}" if pol in (2, 3) else ""))
+                                   + ("" if args.scorer == "attention" else f" scorer={args.scorer}"),
                        "global_batch": B * world, "parallelism": f"request-sharded x{world}",
                        "l2": "no flush: per-step K/V traffic > 126 MB L2", "split": run_split(w, args)},
             "hbm_gbs": hbm_gbs, "hbm_frac_of_measured_peak": hbm_gbs / peaks["hbm_gbs"],

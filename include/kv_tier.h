@@ -96,6 +96,13 @@ typedef enum { KV_TIER_SHARD_REQUEST = 0, KV_TIER_SHARD_KVHEAD = 1, KV_TIER_SHAR
 typedef enum { KV_TIER_POLICY_HIERARCHY = 0, KV_TIER_POLICY_STREAMING = 1, KV_TIER_POLICY_H2O = 2,
                KV_TIER_POLICY_RANDOM = 3 } kv_tier_policy;
 
+/* Token scorer of a4 ("better scoring methods are plugins").
+ *   ATTENTION  Eq. 1: S_i += sum_h p_{l,h,i}.
+ *   VATP       value-aware attention: S_i += fp32(sum_h p_{l,h,i}) * ||v_{l,g,i}||_2, the
+ *              fp32 L2 norm of the token's bf16 V row of layer l, kv head g, fixed when the row
+ *              is loaded / appended.  Split decode kernel only (not KVTIER_FLAT / KVTIER_CLUSTER). */
+typedef enum { KV_TIER_SCORER_ATTENTION = 0, KV_TIER_SCORER_VATP = 1 } kv_tier_scorer;
+
 #define KV_TIER_STAGING_ALL 0xFFFFFFFFu   /* differential mode: staging holds all of T1 (§3.4) */
 
 typedef struct {
@@ -125,6 +132,7 @@ typedef struct {
   int32_t  policy;           /* kv_tier_policy (0 = the paper's hierarchy)             */
   int32_t  budget;           /* kept tokens per request (H2O / RANDOM)                 */
   uint32_t policy_seed;      /* RANDOM                                                 */
+  int32_t  scorer;           /* kv_tier_scorer (0 = Eq. 1 attention score)             */
 } kv_tier_config;
 
 typedef struct kv_tier_ctx kv_tier_ctx;

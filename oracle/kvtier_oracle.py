@@ -25,6 +25,8 @@ EVICT_TOTAL, EVICT_PER_EVENT = 0, 1
 # tier policies: the paper's hierarchy and its pure-eviction baselines (§4.1 P:276-280;
 # SPEC §baselines)
 POLICY_HIERARCHY, POLICY_STREAMING, POLICY_H2O, POLICY_RANDOM = 0, 1, 2, 3
+# token scorers of the score update: Eq. 1 attention or VATP, attention x ||v||
+SCORER_ATTENTION, SCORER_VATP = 0, 1
 
 
 # ----------------------------------------------------------------- attention
@@ -251,6 +253,7 @@ class OracleConfig:
     budget: int = 0
     policy_seed: int = 0
     req_ids: list = None       # the library's request index of each oracle request (RANDOM keys)
+    scorer: int = SCORER_ATTENTION
 
     @property
     def G(self):
@@ -272,6 +275,7 @@ class OracleState:
     scaleV: np.ndarray
     t: int = 0
     events: list = field(default_factory=list)
+    vnorm: np.ndarray = None   # VATP: [L][B][Hkv][Nmax] fp32 ||v|| of every token's original V row
 
 
 def init_state(cfg, Kbits, Vbits, n0):
@@ -281,8 +285,11 @@ def init_state(cfg, Kbits, Vbits, n0):
     will ever generate (the never-migrated originals)."""
     from paper_2605_09490_b200.synth.synth import bf16_bits_to_f32   # input decoding only
     L, B, Hkv, Nmax, d = Kbits.shape
+    vnorm = None
+    if getattr(cfg, "scorer", SCORER_ATTENTION) == SCORER_VATP:
+        vnorm = value_norms(bf16_bits_to_f32(Vbits))
     return OracleState(
-        cfg=cfg, n=n0,
+        cfg=cfg, n=n0, vnorm=vnorm,
         tier=np.full((B, Nmax), T0, dtype=np.uint8),
         S_part=np.zeros((B, Hkv, Nmax), dtype=np.float32),
         rowK=bf16_bits_to_f32(Kbits).copy(), rowV=bf16_bits_to_f32(Vbits).copy(),
@@ -291,6 +298,20 @@ def init_state(cfg, Kbits, Vbits, n0):
         scaleK=np.ones((L, B, Hkv, Nmax), dtype=np.float32),
         scaleV=np.ones((L, B, Hkv, Nmax), dtype=np.float32),
     )
+
+
+def value_norms(V):
+    """VATP weights: fp32 L2 norm of each V row (last axis), summed in float64."""
+    return np.sqrt(np.sum(np.asarray(V, dtype=np.float64) ** 2, axis=-1)).astype(np.float32)
+
+
+def score_increment(psum, st, l, b, g, vis):
+    """fp32 increment of S_part for positions vis: fp32(sum_h p) (Eq. 1, AMB-14), times the
+    token's V-row norm under VATP: fp32(fp32(sum_h p) * ||v||)."""
+    inc = psum.astype(np.float32)
+    if st.vnorm is not None:
+        inc = (inc * st.vnorm[l, b, g, vis]).astype(np.float32)
+    return inc
 
 
 def effective_rows(st, l, b, g, vis):
@@ -335,7 +356,7 @@ def decode_layer(st, l, qbits_l):
                 psum += p
             if not np.all(np.isfinite(psum)):
                 raise FloatingPointError("non-finite probability (E_NUMERIC)")
-            st.S_part[b, g, vis] = (st.S_part[b, g, vis] + psum.astype(np.float32)).astype(np.float32)
+            st.S_part[b, g, vis] = (st.S_part[b, g, vis] + score_increment(psum, st, l, b, g, vis)).astype(np.float32)
     return o
 
 

@@ -397,6 +397,14 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
         const float vf = bf16_bits_to_f(vb[k]);
         for (int h = 0; h < G; ++h) part[16 + h * D + e] = vf;
       }
+      if (v.scorer == 1) {             // VATP: the new token's V-row norm for this layer
+        float ss = 0.f;
+#pragma unroll
+        for (int k = 0; k < EL; ++k) ss += bf16_bits_to_f(vb[k]) * bf16_bits_to_f(vb[k]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+        if (lane == 0) v.vnorm[((size_t)layer * v.B * v.Hkv + unit) * v.Nmax + (v.st->n - 1)] = sqrtf(ss);
+      }
       if (lane < G) {
         float z = 0.f;
 #pragma unroll
@@ -865,6 +873,7 @@ __global__ void __launch_bounds__(256) k_decode_merge(const DevView v, const int
     sl[i] = __ldcg(P + (size_t)(i >> 3) * v.part_stride + 8 + (i & 7));
   }
   __syncthreads();
+  if (unit == 0 && tid == 0 && zpar >= 0) v.zlayer[zpar] = layer;   // the slot's layer (VATP weights)
   if (tid < 8) {
     const int h = tid;
     float M = -INFINITY;
@@ -963,7 +972,7 @@ __global__ void __launch_bounds__(128, 16) k_score_flush_lean(const DevView v, c
 #pragma unroll
       for (int h = 0; h < 8; ++h)
         if (h < v.G) inc += ex2_ftz(zz[h] - ml[h]) * ml[8 + h];
-      s = s + inc;
+      s = s + inc * score_weight(v, v.scorer ? v.zlayer[slot] : 0, u, pos);
       bad |= !isfinite(inc);
     }
     v.S[(size_t)u * v.Nmax + pos] = s;
@@ -991,7 +1000,7 @@ __global__ void __launch_bounds__(256) k_score_flush_req(const DevView v, const 
       const float* ml = v.ml + slot * mslot + (size_t)u * 16;
       float inc = 0.f;
       for (int h = 0; h < v.G; ++h) inc += ex2_ftz(z[h] - ml[h]) * ml[8 + h];
-      s = s + inc;
+      s = s + inc * score_weight(v, v.scorer ? v.zlayer[slot] : 0, u, pos);
       bad |= !isfinite(inc);
     }
     v.S[(size_t)u * v.Nmax + pos] = s;

@@ -104,6 +104,8 @@ kv_tier_status validate(const kv_tier_config* c) {
   if (c->variant < 0 || c->variant > 5) return fail(nullptr, KV_TIER_E_INVAL, "variant must be in [0, 5]");
   if (c->policy < KV_TIER_POLICY_HIERARCHY || c->policy > KV_TIER_POLICY_RANDOM)
     return fail(nullptr, KV_TIER_E_INVAL, "policy must be a kv_tier_policy");
+  if (c->scorer != KV_TIER_SCORER_ATTENTION && c->scorer != KV_TIER_SCORER_VATP)
+    return fail(nullptr, KV_TIER_E_INVAL, "scorer must be a kv_tier_scorer");
   if ((c->policy == KV_TIER_POLICY_H2O || c->policy == KV_TIER_POLICY_RANDOM) && c->budget < 1)
     return fail(nullptr, KV_TIER_E_INVAL, "H2O / RANDOM need budget >= 1 kept tokens per request");
   return KV_TIER_OK;
@@ -128,7 +130,7 @@ void capacities(const kv_tier_config& c, int* cap0, int* cap1, int* cap2) {
 struct Layout {
   size_t off_k0[2], off_v0[2], off_k1[2], off_v1[2], off_c2k[2], off_c2v[2], off_s2k[2], off_s2v[2];
   size_t off_idx[2][3], off_vis[2], off_tier[2], off_row[2], off_cnt[2], off_S, off_fS, off_st, off_z, off_ml;
-  size_t off_part, off_uctr, off_moves, off_mcount, off_scratch, off_mtemp, total, hot_begin;
+  size_t off_part, off_uctr, off_moves, off_mcount, off_scratch, off_mtemp, total, hot_begin, off_vnorm, off_zlayer;
   size_t b_t0, b_t1, b_t2, b_scores, b_meta;
 };
 
@@ -186,6 +188,8 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
                                   (size_t)flat_grid(c, FLAT_GRID_MAX_SM) + 2 * BH);   // flat: <= grid + 2 units
   L.off_part = take(nslots * (16 + 8 * D) * 4);
   L.off_uctr = take(BH * 4);
+  L.off_zlayer = take(ZRING * 4);
+  L.off_vnorm = take(c.scorer == KV_TIER_SCORER_VATP ? LBH * N * 4 : 0);   // VATP: V-row norms
   L.b_scores = o - s0; s0 = o;
   for (int i = 0; i < 2; ++i) {
     L.off_idx[i][0] = take(B * cap0 * 4);
@@ -331,6 +335,10 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.part = reinterpret_cast<float*>(A + L.off_part);
   v.part_stride = 16 + 8 * v.D;
   v.unit_ctr = reinterpret_cast<int*>(A + L.off_uctr);
+  v.zlayer = reinterpret_cast<int*>(A + L.off_zlayer);
+  v.scorer = cfg->scorer;
+  v.vnorm = cfg->scorer == KV_TIER_SCORER_VATP ? reinterpret_cast<float*>(A + L.off_vnorm) : nullptr;
+  if (v.scorer == KV_TIER_SCORER_VATP) { v.flat = 0; v.cluster_merge = 0; }   // VATP: split kernel + merge kernel
   v.hot_base = A + L.hot_begin;
   v.hot_bytes = L.total - L.hot_begin;
   v.moves = reinterpret_cast<int4*>(A + L.off_moves);
@@ -464,6 +472,8 @@ kv_tier_status kv_tier_load_prefix(kv_tier_ctx* ctx, int32_t layer, const void* 
   }
   if (n0 > 0) {
     kv_tier_status st = cuda_check(ctx, launch_load_prefix(ctx->v, layer, k, v, n0, s), "load_prefix");
+    if (!st && ctx->v.scorer == KV_TIER_SCORER_VATP)
+      st = cuda_check(ctx, launch_vnorm_prefix(ctx->v, layer, v, n0, s), "load_prefix (V norms)");
     if (st) return st;
   }
   ctx->loaded_layers[layer] = 1;

@@ -206,6 +206,7 @@ __device__ __forceinline__ void score_range(const DevView& v, const Seg& sg, int
       for (int j = 0; j < ZBATCH; ++j) {
         if (j >= nz) break;
         const int slot = (zfirst + j) % ZRING;
+        const float wgt = score_weight(v, v.scorer ? v.zlayer[slot] : 0, uu[k], pos[k]);
         const float* ml = v.ml + slot * mslot + (size_t)uu[k] * 16;
         const float zz[8] = {z0[k][j].x, z0[k][j].y, z0[k][j].z, z0[k][j].w,
                              z1[k][j].x, z1[k][j].y, z1[k][j].z, z1[k][j].w};
@@ -213,7 +214,7 @@ __device__ __forceinline__ void score_range(const DevView& v, const Seg& sg, int
 #pragma unroll
         for (int h = 0; h < 8; ++h)
           if (h < v.G) inc += ex2_ftz(zz[h] - ml[h]) * ml[8 + h];
-        s = s + inc;
+        s = s + inc * wgt;
         bad |= !isfinite(inc);
       }
       v.S[(size_t)uu[k] * v.Nmax + pos[k]] = s;

@@ -33,6 +33,9 @@ struct DevView {
   int P, ks, kw;
   int hbm_bp, evict_bp, t2_bp, evict_mode;
   int policy, budget;   // kv_tier_policy (tier policy of a5), kept tokens (H2O / RANDOM)
+  int scorer;           // kv_tier_scorer (a4 increment: attention, or attention x ||v|| for VATP)
+  float* vnorm;         // VATP: [L][B][Hkv][Nmax] fp32 L2 norm of each token's V row (null otherwise)
+  int* zlayer;          // [ZRING] layer of the launch that filled each logit slot
   unsigned policy_seed;
   int stream_mode;      // staging_tokens == 0
   int out_fp32;
@@ -123,6 +126,11 @@ __host__ __device__ __forceinline__ void policy_counts(int policy, int budget, i
   *n_t2 = ((long long)t2_bp * (surv - *n_hbm)) / 10000;
 }
 
+// a4 weight of token (layer, unit, pos): 1 (Eq. 1) or its V-row norm (VATP)
+__device__ __forceinline__ float score_weight(const DevView& v, int layer, int unit, int pos) {
+  return v.scorer == 1 ? v.vnorm[((size_t)layer * v.B * v.Hkv + unit) * v.Nmax + pos] : 1.f;
+}
+
 // Sequence sharding: block-cyclic ownership of SEQ_BLOCK-position blocks.
 // A rank's tier stores and index lists hold only its own positions; the tier array and the
 // scores cover every position (tiers are identical on every rank).
@@ -176,6 +184,7 @@ cudaError_t launch_init_meta(const DevView& v, int n0, cudaStream_t s);
 cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
                                void* o, int zpar, int pdl, cudaStream_t s, float* lse = nullptr);
 cudaError_t launch_set_ml(const DevView& v, int zslot, const float* lse, cudaStream_t s);
+cudaError_t launch_vnorm_prefix(const DevView& v, int layer, const void* vv, int n0, cudaStream_t s);
 cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_t s);
 cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s);
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);

@@ -3,6 +3,7 @@
 //   (radix select + compaction), a6 migrate (gather / quantise / offload), a2 stream
 //   prefetch.  Citations: PAPER.md Alg. 1, §3.2-3.4 P:143-211.
 #include "kv_internal.cuh"
+#include <algorithm>
 
 namespace kvt {
 
@@ -54,6 +55,39 @@ __global__ void k_append(const DevView v, const int layer, const uint16_t* __res
     K[dst + swz_off(row, e)] = k[(size_t)unit * v.D + e];
     V[dst + swz_off(row, e)] = vv[(size_t)unit * v.D + e];
   }
+  if (v.scorer == 1 && threadIdx.x < 32) {   // VATP: V-row norm of the appended token
+    float ss = 0.f;
+    for (int e = threadIdx.x; e < v.D; e += 32) {
+      const float x = bf16_bits_to_f(vv[(size_t)unit * v.D + e]);
+      ss += x * x;
+    }
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if (threadIdx.x == 0) v.vnorm[((size_t)layer * v.B * v.Hkv + unit) * v.Nmax + (v.st->n - 1)] = sqrtf(ss);
+  }
+}
+
+// VATP: fp32 L2 norm of every prefix token's V row of one layer (one warp per row); positions
+// of a sequence shard's own rows only.
+__global__ void k_vnorm_prefix(const DevView v, const int layer, const uint16_t* __restrict__ vv, const int n0) {
+  const int unit = blockIdx.y, lane = threadIdx.x & 31;
+  const int nown = seq_owned_below(v.seq_w, v.seq_r, n0);
+  for (int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); j < nown; j += gridDim.x * (blockDim.x / 32)) {
+    const int p = seq_pos_of(v.seq_w, v.seq_r, j);
+    const uint16_t* row = vv + ((size_t)unit * n0 + p) * v.D;
+    float ss = 0.f;
+    for (int e = lane; e < v.D; e += 32) {
+      const float x = bf16_bits_to_f(row[e]);
+      ss += x * x;
+    }
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if (lane == 0) v.vnorm[((size_t)layer * v.B * v.Hkv + unit) * v.Nmax + p] = sqrtf(ss);
+  }
+}
+
+cudaError_t launch_vnorm_prefix(const DevView& v, int layer, const void* vv, int n0, cudaStream_t s) {
+  dim3 grid((unsigned)std::max(1, std::min(1024, (n0 + 7) / 8)), v.B * v.Hkv);
+  k_vnorm_prefix<<<grid, 256, 0, s>>>(v, layer, reinterpret_cast<const uint16_t*>(vv), n0);
+  return cudaGetLastError();
 }
 
 // Prefill rows [0, n0) of one layer into T0 (Alg. 1); a sequence shard keeps its own
@@ -117,7 +151,7 @@ __global__ void k_init_meta(const DevView v, const int n0) {
 // ------------------------------------------------------------------ a4 standalone
 // probs [B][Hq][n_vis] in ascending visible order; visible list = idxvis at the last
 // event followed by the positions appended since (all T0, ascending).
-__global__ void k_score_update(const DevView v, const float* __restrict__ probs) {
+__global__ void k_score_update(const DevView v, const int layer, const float* __restrict__ probs) {
   const int unit = blockIdx.y;
   const int b = unit / v.Hkv, g = unit % v.Hkv;
   const int cur = v.st->cur;
@@ -130,7 +164,7 @@ __global__ void k_score_update(const DevView v, const float* __restrict__ probs)
   float inc = 0.f;
   for (int h = g * v.G; h < (g + 1) * v.G; ++h) inc += probs[((size_t)b * v.Hq + h) * nvis + j];
   float* S = v.S + ((size_t)b * v.Hkv + g) * v.Nmax + pos;
-  *S = *S + inc;
+  *S = *S + inc * score_weight(v, layer, unit, pos);
   if (!isfinite(inc)) atomicOr(&v.st->err, 1);
 }
 
@@ -762,9 +796,8 @@ cudaError_t launch_init_meta(const DevView& v, int n0, cudaStream_t s) {
   return cudaGetLastError();
 }
 cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s) {
-  (void)layer;
   dim3 grid((v.Nmax + 255) / 256, v.B * v.Hkv);
-  k_score_update<<<grid, 256, 0, s>>>(v, probs);
+  k_score_update<<<grid, 256, 0, s>>>(v, layer, probs);
   return cudaGetLastError();
 }
 cudaError_t launch_classify(const DevView& v, const float* Sx, int parts, cudaStream_t s) {

@@ -50,7 +50,7 @@ class TieredDecode:
                                   staging=w["staging"], device=self.dev.index or 0, out_fp32=int(out_fp32),
                                   split=split, variant=variant, shard=shard, rank=rank, world=world,
                                   policy=w.get("policy", 0), budget=w.get("budget", 0),
-                                  policy_seed=w.get("policy_seed", 0))
+                                  policy_seed=w.get("policy_seed", 0), scorer=w.get("scorer", 0))
         hs = slice(h0, h0 + hl)
         qs = slice(h0 * G, (h0 + hl) * G)
         self.kv = kt.KvTier(self.cfg)

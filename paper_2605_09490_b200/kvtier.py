@@ -20,6 +20,7 @@ STATUS = {0: "OK", -1: "E_INVAL", -2: "E_CUDA", -3: "E_NCCL", -4: "E_STATE", -5:
 EVICT_TOTAL, EVICT_PER_EVENT = 0, 1
 SHARD_REQUEST, SHARD_KVHEAD, SHARD_SEQUENCE = 0, 1, 2
 POLICY_HIERARCHY, POLICY_STREAMING, POLICY_H2O, POLICY_RANDOM = 0, 1, 2, 3
+SCORER_ATTENTION, SCORER_VATP = 0, 1
 STAGING_ALL = 0xFFFFFFFF
 X_SCORES, X_TIERS, X_IDX_T0, X_IDX_T1, X_IDX_T2, X_T0_ROWS, X_T1_ROWS, X_STAGING, X_T2_CODES, X_T2_SCALES = range(10)
 
@@ -38,7 +39,7 @@ class Config(C.Structure):
         ("evict_mode", C.c_int32), ("staging_tokens", C.c_uint32),
         ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("shard", C.c_int32),
         ("out_fp32", C.c_int32), ("split", C.c_int32), ("variant", C.c_int32),
-        ("policy", C.c_int32), ("budget", C.c_int32), ("policy_seed", C.c_uint32)]
+        ("policy", C.c_int32), ("budget", C.c_int32), ("policy_seed", C.c_uint32), ("scorer", C.c_int32)]
 
 
 class Sizes(C.Structure):
@@ -127,14 +128,14 @@ def _stream_ptr(stream):
 def make_config(B, L, Hq, Hkv, d, max_tokens, prompt_len, hbm_bp=5000, evict_bp=500, t2_bp=0,
                 sink_size=4, window_size=128, manage_interval=64, evict_mode=EVICT_TOTAL,
                 staging=STAGING_ALL, device=0, out_fp32=1, split=0, rank=0, world=1, variant=0,
-                shard=0, policy=0, budget=0, policy_seed=0):
+                shard=0, policy=0, budget=0, policy_seed=0, scorer=0):
     return Config(num_requests=B, num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=d,
                   max_tokens=max_tokens, prompt_len=prompt_len, sink_size=sink_size,
                   window_size=window_size, manage_interval=manage_interval, hbm_ratio_bp=hbm_bp,
                   evict_ratio_bp=evict_bp, t2_fraction_bp=t2_bp, evict_mode=evict_mode,
                   staging_tokens=staging, device=device, rank=rank, world=world, shard=shard,
                   out_fp32=out_fp32, split=split, variant=variant, policy=policy, budget=budget,
-                  policy_seed=policy_seed)
+                  policy_seed=policy_seed, scorer=scorer)
 
 
 def query_sizes(cfg):

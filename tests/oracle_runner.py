@@ -21,7 +21,8 @@ class OracleRun:
                                   manage_interval=w["interval"], hbm_bp=w["hbm_bp"], evict_bp=w["evict_bp"],
                                   t2_bp=w.get("t2_bp", 0), evict_mode=w.get("evict_mode", 0),
                                   policy=w.get("policy", 0), budget=w.get("budget", 0),
-                                  policy_seed=w.get("policy_seed", 0), req_ids=self.reqs)
+                                  policy_seed=w.get("policy_seed", 0), req_ids=self.reqs,
+                                  scorer=w.get("scorer", 0))
         self.st = O.init_state(self.cfg, self.K, self.V, n0)
 
     def step(self):

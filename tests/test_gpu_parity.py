@@ -544,3 +544,12 @@ def test_random_policy_request_keys_sampled_requests():
     w = H.workload("tiny", B=4, L=1, Hq=4, Hkv=2, d=64, N=500, P=16, interval=8, steps=18,
                    hbm_bp=5000, evict_bp=500, t2_bp=0, policy=kt.POLICY_RANDOM, budget=250, policy_seed=5)
     _run_pair(w, reqs=[1, 3], graph=True, check_every=8)
+
+
+# --------------------------------------------------------------------- VATP scorer (§8f N2)
+@pytest.mark.parametrize("api", ["graph", "layers"])
+def test_vatp_scorer_parity(api):
+    # value-aware scores: S += fp32(sum_h p) * ||v|| with the norms of the appended rows
+    w = H.workload("tiny", B=3, L=2, Hq=8, Hkv=2, d=128, N=600, P=32, interval=8, steps=26,
+                   hbm_bp=4000, evict_bp=800, t2_bp=3000, scorer=kt.SCORER_VATP)
+    _run_pair(w, graph=api == "graph", layers_api=api == "layers", check_every=4)

@@ -505,3 +505,40 @@ def test_policy_budget_covers_everything():
         new = O.classify_request(np.random.default_rng(2).random((1, n)).astype(np.float32),
                                  np.zeros(n, np.uint8), n, _pol_cfg(pol, budget=n + 3, seed=1))
         assert np.all(new == O.T0)
+
+
+# --------------------------------------------------------------------- VATP scorer
+def _vatp_run(scale_v):
+    from tests.oracle_runner import OracleRun
+    from paper_2605_09490_b200 import harness as Hh
+    w = Hh.workload("tiny", L=2, steps=4, interval=2, scorer=O.SCORER_VATP)
+    r = OracleRun(w)
+    if scale_v != 1.0:                       # scale every V row exactly (power of two)
+        r.st.rowV *= scale_v
+        r.st.vnorm *= scale_v
+    outs = [r.step() for _ in range(w["steps"])]
+    return r, outs
+
+
+def test_vatp_scales_with_value_norms():
+    # property pin: doubling every value row (exact in bf16/fp32) doubles every VATP increment
+    # and the attention output, and leaves the tiers unchanged; a wrong weight (K norm, no
+    # weight, squared norm) breaks it
+    r1, o1 = _vatp_run(1.0)
+    r2, o2 = _vatp_run(2.0)
+    assert np.array_equal(r2.st.S_part, 2 * r1.st.S_part)
+    assert np.array_equal(r2.st.tier, r1.st.tier)
+    for a, b in zip(o1, o2):
+        assert np.allclose(b, 2 * a, rtol=1e-12, atol=0)
+
+
+def test_vatp_weights_are_value_row_norms():
+    # one layer, one kv head, unit probability mass on a single token: the increment is that
+    # token's ||v|| (brute force on a hand-built state)
+    V = np.array([[3.0, 4.0], [0.0, 1.0], [6.0, 8.0]], np.float32)
+    vn = O.value_norms(V)
+    assert vn.tolist() == [5.0, 1.0, 10.0]
+    class St:
+        vnorm = vn[None, None, None, :]
+    inc = O.score_increment(np.array([0.25, 0.5, 0.25]), St, 0, 0, 0, np.arange(3))
+    assert inc.tolist() == [1.25, 0.5, 2.5]
