@@ -47,5 +47,14 @@ for l in (0, 1, 2, tr.shape[0] // 2, tr.shape[0] - 1):
     d["prod_done"] = [round(float(x), 2) for x in np.percentile(rel[l, :, 12], [0, 50, 100])]
 ends = [float(rel[l, :, 7].max()) for l in range(tr.shape[0])]
 out["layer_end_deltas_us"] = [round(ends[l] - ends[l - 1], 2) for l in range(1, len(ends))]
+mt = tr[:, :, :].astype(np.int64)
+sel = mt[:, :, 16] > 0
+if sel.any():
+    l = tr.shape[0] // 2
+    x = mt[l]
+    x = x[x[:, 16] > 0]
+    out["merge_loads_us"] = [round(float(v), 2) for v in np.percentile((x[:, 16] - x[:, 5]) / 1e3, [0, 50, 100])]
+    out["merge_factors_us"] = [round(float(v), 2) for v in np.percentile((x[:, 17] - x[:, 16]) / 1e3, [0, 50, 100])]
+    out["merge_tail_us"] = [round(float(v), 2) for v in np.percentile((x[:, 7] - x[:, 17]) / 1e3, [0, 50, 100])]
 print(json.dumps(out))
 run.close()
