@@ -245,13 +245,20 @@ class SeqShardedDecode:
         from . import dist as D
         t, s = self.t, self.stream
         r0 = self.runs[0]
+        stream_mode = self.w["staging"] == 0
+        L = self.w["L"]
         with torch.cuda.stream(s):
             for r in self.runs:
                 r.kv.begin_step(stream=s)
-            for l in range(self.w["L"]):
+                if stream_mode:                      # T1 rows of the first layers, layer-ahead
+                    for l in range(min(2, L)):
+                        r.kv.prefetch(l, side=r.side)
+            for l in range(L):
                 for i, r in enumerate(self.runs):
                     r.kv.decode_attention_lse(l, r0.Q[t, l], self.Ol[i][l], self.LSE[i][l], 1, stream=s,
                                               k_new=r0.Kn[t, l], v_new=r0.Vn[t, l])
+                    if stream_mode and l + 2 < L:
+                        r.kv.prefetch(l + 2, side=r.side)
                 o, lse = D.lse_combine(torch.stack([x[l] for x in self.Ol]), torch.stack([x[l] for x in self.LSE]))
                 self.O[l].copy_(o)
                 self.LSEg[l].copy_(lse)
@@ -315,11 +322,18 @@ class SeqShardRank:
         from . import dist as D
         r, t = self.run, self.t
         s = r.main
+        stream_mode = self.w["staging"] == 0
+        L = self.w["L"]
         with torch.cuda.stream(s):
             r.kv.begin_step(stream=s)
-            for l in range(self.w["L"]):
+            if stream_mode:                          # T1 rows of the first layers, layer-ahead
+                for l in range(min(2, L)):
+                    r.kv.prefetch(l, side=r.side)
+            for l in range(L):
                 r.kv.decode_attention_lse(l, r.Q[t, l], self.Ol[l], self.LSE[l], 1, stream=s,
                                           k_new=r.Kn[t, l], v_new=r.Vn[t, l])
+                if stream_mode and l + 2 < L:
+                    r.kv.prefetch(l + 2, side=r.side)
                 o, lse = D.seq_combine(self.Ol[l], self.LSE[l], self.group)
                 self.O[l].copy_(o)
                 self.LSEg[l].copy_(lse)

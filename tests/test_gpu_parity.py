@@ -432,12 +432,13 @@ def _check_seq_event_state(sh, orc, layers=(0, 1)):
                     assert np.array_equal(codes[bg][:, :, 0, :], st.codeK[l, bo][:, pos])
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sequence_sharding_matches_unsharded_oracle(world):
+@pytest.mark.parametrize("world,staging", [(2, kt.STAGING_ALL), (3, kt.STAGING_ALL), (2, 0)])
+def test_sequence_sharding_matches_unsharded_oracle(world, staging):
     # world ctxs on one GPU, block-cyclic 64-position ownership; per-layer LSE combine of the
-    # ranks' partials, global (M, L) back into the fused score update, summed scores at events
+    # ranks' partials, global (M, L) back into the fused score update, summed scores at events;
+    # staging 0: each shard re-fetches its own T1 rows from pinned host memory every step
     w = H.workload("tiny", B=2, L=2, Hq=8, Hkv=2, d=64, N=400, P=16, interval=8, steps=26,
-                   hbm_bp=4000, evict_bp=800, t2_bp=3000)
+                   hbm_bp=4000, evict_bp=800, t2_bp=3000, staging=staging)
     sh = H.SeqShardedDecode(w, world)
     orc = OracleRun(w)
     for t in range(w["steps"]):
