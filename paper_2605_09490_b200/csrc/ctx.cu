@@ -118,10 +118,20 @@ void capacities(const kv_tier_config& c, int* cap0, int* cap1, int* cap2) {
   const long long prot = (long long)c.prompt_len + c.sink_size + c.window_size;
   const long long hbm = ((long long)c.hbm_ratio_bp * N + 9999) / 10000;
   (void)prot; (void)hbm;   // v1: T0 sized for the whole chain (the prefix starts all-T0)
-  long long c0 = N;
+  // a sequence shard stores only its own positions: every store is bounded by that count
+  const long long own = c.shard == KV_TIER_SHARD_SEQUENCE
+                            ? seq_owned_below(c.world, c.rank, (int)N) + SEQ_BLOCK : N;
+  const long long Nc = std::min<long long>(N, own);
+  long long c0 = Nc;
   const long long off = ((long long)(10000 - c.hbm_ratio_bp) * N + 9999) / 10000 + 2;
-  long long c1 = std::min<long long>(N, off);
-  long long c2 = c.t2_fraction_bp ? std::min<long long>(N, (off * c.t2_fraction_bp + 9999) / 10000 + 2) : 0;
+  long long c1 = std::min<long long>(Nc, off);
+  long long c2 = c.t2_fraction_bp ? std::min<long long>(Nc, (off * c.t2_fraction_bp + 9999) / 10000 + 2) : 0;
+  if (c.shard == KV_TIER_SHARD_SEQUENCE && c.world > 1) {
+    // a shard's T1/T2 share tracks the global fraction (block-cyclic ownership): 1.25x its fair
+    // share + one block; a classify that would exceed it sets the device capacity flag (E_CAPACITY)
+    c1 = std::min<long long>(c1, (off * 5 + 4 * c.world - 1) / (4 * c.world) + SEQ_BLOCK);
+    if (c2) c2 = std::min<long long>(c2, (c2 * 5 + 4 * c.world - 1) / (4 * c.world) + SEQ_BLOCK);
+  }
   *cap0 = round16(c0);
   *cap1 = round16(c1);
   *cap2 = round16(c2);
@@ -147,7 +157,9 @@ constexpr int FLAT_GRID_MAX_SM = 296;     // partial slots reserved for grids up
 size_t mcap_of(const kv_tier_config& c) {
   const char* ov = getenv("KVTIER_MCAP");                    // test hook: force the full-rebuild path
   if (ov && atoi(ov) > 0) return (size_t)atoi(ov);
-  return std::max<size_t>(256, ((size_t)c.max_tokens / 8 + 15) / 16 * 16);
+  const size_t n = c.shard == KV_TIER_SHARD_SEQUENCE ? (size_t)seq_owned_below(c.world, c.rank, c.max_tokens) + SEQ_BLOCK
+                                                    : (size_t)c.max_tokens;
+  return std::max<size_t>(256, (n / 8 + 15) / 16 * 16);
 }
 
 Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
@@ -457,7 +469,7 @@ kv_tier_status kv_tier_load_prefix(kv_tier_ctx* ctx, int32_t layer, const void* 
   if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
   if (!k || !v) return fail(ctx, KV_TIER_E_INVAL, "null k/v");
   if (ctx->t > 0 || ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "load_prefix after decoding started");
-  if (n0 < 0 || n0 + 1 > ctx->v.cap0 || n0 + 1 > ctx->v.Nmax)
+  if (n0 < 0 || seq_owned_below(ctx->v.seq_w, ctx->v.seq_r, n0) + 1 > ctx->v.cap0 || n0 + 1 > ctx->v.Nmax)
     return fail(ctx, KV_TIER_E_CAPACITY, "prefix of %d tokens exceeds T0 capacity %d / N_max %d", n0, ctx->v.cap0, ctx->v.Nmax);
   if (ctx->n0 >= 0 && ctx->n0 != n0) return fail(ctx, KV_TIER_E_INVAL, "n0 differs between layers");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -737,7 +749,7 @@ static kv_tier_status classify_impl(kv_tier_ctx* ctx, const float* Sx, int parts
                 np, nl, n3, &n_new, &n_hbm, &n_t2);
   const long long surv = nl - n_new;
   const int p0 = (int)(np + n_hbm), p1 = (int)(surv - n_hbm - n_t2), p2 = (int)n_t2, p3 = (int)(n3 + n_new);
-  if (p0 > ctx->v.cap0 || p1 > ctx->v.cap1 || p2 > ctx->v.cap2)
+  if (ctx->v.seq_w <= 1 && (p0 > ctx->v.cap0 || p1 > ctx->v.cap1 || p2 > ctx->v.cap2))   // shards: own counts <= caps
     return fail(ctx, KV_TIER_E_CAPACITY, "tier counts %d/%d/%d exceed capacities %d/%d/%d", p0, p1, p2,
                 ctx->v.cap0, ctx->v.cap1, ctx->v.cap2);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -877,6 +889,7 @@ kv_tier_status kv_tier_sync(kv_tier_ctx* ctx) {
   DevState h;
   e = cudaMemcpy(&h, ctx->v.st, sizeof(h), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return fail(ctx, KV_TIER_E_CUDA, "state read: %s", cudaGetErrorString(e));
+  if (h.err & 2) return fail(ctx, KV_TIER_E_CAPACITY, "a tier store of this sequence shard overflowed at classify (its share of T1/T2 exceeded 1.25x the fair share)");
   if (h.err) return fail(ctx, KV_TIER_E_NUMERIC, "non-finite probability or score detected on device");
   if (h.n != ctx->n || h.cur != ctx->cur)
     return fail(ctx, KV_TIER_E_STATE, "device/host state diverged (n %d/%d cur %d/%d)", h.n, ctx->n, h.cur, ctx->cur);

@@ -19,7 +19,7 @@ struct DevState {
   int t;            // decode step
   int cur;          // ping-pong buffer holding the live stores / lists
   int n_event;      // n at the last committed manage event
-  int err;          // sticky error bits: 1 = non-finite probability/score
+  int err;          // sticky error bits: 1 = non-finite probability/score, 2 = tier store overflow (shard)
   int scur;         // buffer holding the bf16/int8 row stores (flips only on a full rebuild)
   int use_full;     // set by the migrate plan when the move list overflows -> full rebuild
   int last_full;    // use_full of the last committed migrate (read by the offload kernels)

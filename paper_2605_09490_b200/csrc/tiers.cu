@@ -329,8 +329,12 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
       if (m[L4] & (1u << lane)) {
         const int off = s_base[L4] + s_wsum[L4][w] + __popc(m[L4] & lt);
         if (L4 < 3) {
-          v.idx[nxt][L4][(size_t)b * caps[L4] + off] = pos;
-          rnew[pos] = off;
+          if (off < caps[L4]) {           // never past a store (sequence shards size T1/T2 by share)
+            v.idx[nxt][L4][(size_t)b * caps[L4] + off] = pos;
+            rnew[pos] = off;
+          } else {
+            atomicOr(&v.st->err, 2);
+          }
         } else {
           v.idxvis[nxt][(size_t)b * v.Nmax + off] = pos;
         }
@@ -342,9 +346,9 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
   }
   if (tid == 0) {
     int* cn = v.cnt[nxt] + b * CNT_STRIDE;
-    cn[0] = s_base[0];
-    cn[1] = s_base[1];
-    cn[2] = s_base[2];
+    cn[0] = min(s_base[0], caps[0]);   // an overflow (flagged above) stays inside the stores
+    cn[1] = min(s_base[1], caps[1]);
+    cn[2] = min(s_base[2], caps[2]);
     cn[3] = seq_owned_below(v.seq_w, v.seq_r, n) - s_base[3];
     cn[4] = s_base[3];
   }
