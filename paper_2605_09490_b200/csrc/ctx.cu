@@ -146,6 +146,12 @@ struct Layout {
 
 int split_of(const kv_tier_config& c);
 
+// Rows per group of the pinned host stores: every position, or a sequence shard's own ones.
+int host_rows_of(const kv_tier_config& c) {
+  return c.shard == KV_TIER_SHARD_SEQUENCE && c.world > 1 ? seq_owned_below(c.world, c.rank, c.max_tokens) + SEQ_BLOCK
+                                                         : c.max_tokens;
+}
+
 // Flat decode grid: one CTA per SM, more when a CTA would cover > 6 units (new-token slots).
 int flat_grid(const kv_tier_config& c, int nsm) {
   const int units = c.num_requests * c.num_kv_heads;
@@ -250,7 +256,7 @@ kv_tier_status kv_tier_query_sizes(const kv_tier_config* cfg, kv_tier_sizes* out
   out->t2_store = L.b_t2;
   out->scores = L.b_scores;
   out->meta = L.b_meta;
-  const size_t rows = (size_t)cfg->num_layers * cfg->num_requests * cfg->num_kv_heads * cfg->max_tokens;
+  const size_t rows = (size_t)cfg->num_layers * cfg->num_requests * cfg->num_kv_heads * host_rows_of(*cfg);
   out->host_t1 = cfg->hbm_ratio_bp < 10000 ? rows * cfg->head_dim * 2 * 2 : 0;
   out->host_t2 = cfg->t2_fraction_bp ? rows * (cfg->head_dim + 4) * 2 : 0;
   out->cap_t0 = cap0;
@@ -361,7 +367,8 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.fS = reinterpret_cast<float*>(A + L.off_fS);
   v.st = reinterpret_cast<DevState*>(A + L.off_st);
   // pinned, mapped host stores (NUMA placement follows the calling thread's node)
-  const size_t rows = (size_t)v.L * v.B * v.Hkv * v.Nmax;
+  v.hN = host_rows_of(*cfg);
+  const size_t rows = (size_t)v.L * v.B * v.Hkv * v.hN;
   if (ctx->sz.host_t1) {
     e = cudaHostAlloc(&ctx->host_t1, ctx->sz.host_t1, cudaHostAllocMapped | cudaHostAllocPortable);
     if (e != cudaSuccess) { delete ctx; return fail(nullptr, KV_TIER_E_OOM, "cudaHostAlloc(T1 %zu B): %s", (size_t)0, cudaGetErrorString(e)); }
@@ -1043,7 +1050,7 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
       }
     } else if (what == KV_TIER_X_T1_ROWS) {
       const int cnt = c[1];
-      const size_t rows = (size_t)v.L * B * H * N;
+      const size_t rows = (size_t)v.L * B * H * v.hN;
       const uint16_t* hk = reinterpret_cast<const uint16_t*>(ctx->host_t1);
       const uint16_t* hv = hk ? hk + rows * D : nullptr;
       if (cnt > 0 && !hk) return fail(ctx, KV_TIER_E_STATE, "no host T1 store");
@@ -1053,8 +1060,8 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
         uint16_t* o16 = reinterpret_cast<uint16_t*>(ob) + (g * cnt) * 2 * D;
         for (int jj = 0; jj < cnt; ++jj) {
           const int p = pos[perm[jj]];
-          memcpy(o16 + (size_t)jj * 2 * D, hk + (grp * N + p) * D, D * 2);
-          memcpy(o16 + (size_t)jj * 2 * D + D, hv + (grp * N + p) * D, D * 2);
+          memcpy(o16 + (size_t)jj * 2 * D, hk + host_row(v, grp, p) * D, D * 2);
+          memcpy(o16 + (size_t)jj * 2 * D + D, hv + host_row(v, grp, p) * D, D * 2);
         }
       }
     } else if (what == KV_TIER_X_T2_CODES || what == KV_TIER_X_T2_SCALES) {

@@ -47,13 +47,14 @@ struct DevView {
   int l2_prefetch;      // pre-wait L2 prefetch of the CTA's stages beyond the shared-memory ring
   int stage_rr;         // 2: 16-row groups dealt round-robin to the unit's CTAs, 1: whole stages, 0: contiguous
   int cluster_merge;    // merge the unit's partials in distributed shared memory (cluster of split CTAs)
-  int flat;             // flat decode kernel (attn_flat.cu; default) instead of split-per-unit
+  int flat;             // flat decode kernel (attn_flat.cu, KVTIER_FLAT=1) instead of the split kernel
   int fvariant;         // flat kernel variant (consumer warps x stages)
   int nc;               // flat kernel grid (CTAs; one per SM)
-  int seq_w, seq_r;
+  int seq_w, seq_r;     // sequence sharding: positions in 64-blocks, block k owned by rank k % seq_w
+  int hN;               // rows per group of the pinned host stores (N_max, or a shard's own positions)
   int score_grid;       // CTAs of the score-flush kernel (runs beside the attention chain)
   int score_lean;       // 1: register-lean score-flush kernel (fits beside two decode CTAs)
-  int last_merge;       // 1: the CTA completing a unit merges its partials (no merge kernel)     // sequence sharding: positions in 64-blocks, block k owned by rank k % seq_w
+  int last_merge;       // 1: the CTA completing a unit merges its partials (no merge kernel)
   int spin_hint;        // mbarrier try_wait suspend-time hint in ns (0: plain polling)
   long long l2pf_bytes; // flat kernel: K/V bytes per CTA requested into L2 at kernel start (0: off)
   int inflight;         // flat kernel: max ring stages requested but not landed (0: the whole ring)
@@ -63,7 +64,7 @@ struct DevView {
   int zrows;            // virtual rows per unit (N_max + padding)
   float* part;          // [B*Hkv][split][part_stride] per-CTA partials (m[8], l[8], o[G][D])
   int part_stride;
-  int* unit_ctr;        // [B*Hkv] partials published per unit (flat kernel; reset by the merging CTA)
+  int* unit_ctr;        // [B*Hkv] partials published per unit (flat kernel, KVTIER_LASTMERGE; reset by the merger)
   void* hot_base;       // L2 access-policy window over the small hot buffers
   size_t hot_bytes;
   float hot_hit;        // hitRatio of the window: persisting carve-out / window bytes (<= 1)
@@ -84,7 +85,7 @@ struct DevView {
   float* S;                                            // S_part [B][Hkv][Nmax]
   float* fS;                                           // scratch [B][Nmax]
   DevState* st;
-  __nv_bfloat16* hk1; __nv_bfloat16* hv1;            // pinned host T1 [L][B][Hkv][Nmax][D] (mapped)
+  __nv_bfloat16* hk1; __nv_bfloat16* hv1;            // pinned host T1 [L][B][Hkv][hN][D] (mapped; host_row)
   int8_t* hc2k; int8_t* hc2v; float* hs2k; float* hs2v;   // pinned host T2 (mapped, may be null)
 };
 
@@ -150,6 +151,12 @@ __host__ __device__ __forceinline__ int seq_owned_below(int seq_w, int seq_r, in
 __host__ __device__ __forceinline__ int seq_pos_of(int seq_w, int seq_r, int j) {
   if (seq_w <= 1) return j;
   return ((j / SEQ_BLOCK) * seq_w + seq_r) * SEQ_BLOCK + j % SEQ_BLOCK;
+}
+
+// Row of position pos of group grp in the pinned host T1/T2 stores ([L][B][H_kv][hN] rows): a
+// sequence shard keeps only its own positions there too (row = owned index).
+__host__ __device__ __forceinline__ size_t host_row(const DevView& v, size_t grp, int pos) {
+  return grp * (size_t)v.hN + (size_t)(v.seq_w > 1 ? seq_owned_below(v.seq_w, v.seq_r, pos) : pos);
 }
 
 __device__ __forceinline__ size_t grp_of(const DevView& v, int l, int b, int g) {

@@ -391,7 +391,7 @@ __device__ __forceinline__ void source_row(const DevView& v, int sb, int kv, siz
     load_bits(x, s + swz_off(orow, lane * E), E);
   } else if (ot == T1) {
     if (v.stream_mode) {
-      const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.hv1 : v.hk1) + (grp * v.Nmax + pos) * D;
+      const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.hv1 : v.hk1) + host_row(v, grp, pos) * D;
       load_bits(x, s + lane * E, E);   // pinned host store: canonical layout
     } else {
       const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v1[sb] : v.k1[sb]) + (grp * v.cap1 + orow) * D;
@@ -689,14 +689,14 @@ __global__ void __launch_bounds__(256) k_offload_host(const DevView v, const int
         } else {
           source_row<D>(v, sb ^ 1, kv, grp, ot, orow, pos, lane, x);   // pre-rebuild buffer
         }
-        uint16_t* dst = reinterpret_cast<uint16_t*>(kv ? v.hv1 : v.hk1) + (grp * v.Nmax + pos) * D;
+        uint16_t* dst = reinterpret_cast<uint16_t*>(kv ? v.hv1 : v.hk1) + host_row(v, grp, pos) * D;
         store_bits(dst + lane * E, x, E);
       } else {
         const int8_t* sc = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + j) * D + lane * E;
-        int8_t* dc = (kv ? v.hc2v : v.hc2k) + (grp * v.Nmax + pos) * D + lane * E;
+        int8_t* dc = (kv ? v.hc2v : v.hc2k) + host_row(v, grp, pos) * D + lane * E;
 #pragma unroll
         for (int k = 0; k < E; ++k) dc[k] = sc[k];
-        if (lane == 0) (kv ? v.hs2v : v.hs2k)[grp * v.Nmax + pos] = (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + j];
+        if (lane == 0) (kv ? v.hs2v : v.hs2k)[host_row(v, grp, pos)] = (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + j];
       }
     }
     rows += 2;
@@ -725,14 +725,14 @@ __global__ void __launch_bounds__(256) k_offload_moves(const DevView v, const in
     if (dt == T1) {
       uint16_t x[E];
       load_bits(x, tk + lane * E, E);
-      uint16_t* dst = reinterpret_cast<uint16_t*>(kv ? v.hv1 : v.hk1) + (grp * v.Nmax + pos) * D;
+      uint16_t* dst = reinterpret_cast<uint16_t*>(kv ? v.hv1 : v.hk1) + host_row(v, grp, pos) * D;
       store_bits(dst + lane * E, x, E);
     } else {
       const int8_t* c = reinterpret_cast<const int8_t*>(tk) + lane * E;
-      int8_t* dc = (kv ? v.hc2v : v.hc2k) + (grp * v.Nmax + pos) * D + lane * E;
+      int8_t* dc = (kv ? v.hc2v : v.hc2k) + host_row(v, grp, pos) * D + lane * E;
 #pragma unroll
       for (int k = 0; k < E; ++k) dc[k] = c[k];
-      if (lane == 0) (kv ? v.hs2v : v.hs2k)[grp * v.Nmax + pos] = *reinterpret_cast<const float*>(reinterpret_cast<const int8_t*>(tk) + D);
+      if (lane == 0) (kv ? v.hs2v : v.hs2k)[host_row(v, grp, pos)] = *reinterpret_cast<const float*>(reinterpret_cast<const int8_t*>(tk) + D);
     }
   }
   if (lane == 0) atomicAdd(&v.st->d2h_rows, 2ull);
@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(256) k_prefetch(const DevView v, const int lay
   for (int j = j0 + w; j < j1; j += 8) {
     const int pos = v.idx[cur][1][(size_t)b * v.cap1 + j];
     for (int kv = 0; kv < 2; ++kv) {
-      const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.hv1 : v.hk1) + (grp * v.Nmax + pos) * D;
+      const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.hv1 : v.hk1) + host_row(v, grp, pos) * D;
       uint16_t* d = reinterpret_cast<uint16_t*>(kv ? v.v1[0] : v.k1[0]) + (sg * v.cap1 + j) * D;
       uint16_t x[E];
       load_bits(x, s + lane * E, E);
