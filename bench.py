@@ -52,6 +52,9 @@ def _args():
     ap.add_argument("--policy", default="hierarchy", choices=list(POLICIES),
                     help="tier policy: the paper's hierarchy or a pure-eviction baseline (P:276-280)")
     ap.add_argument("--budget", type=int, default=1024, help="kept tokens per request (h2o / random)")
+    ap.add_argument("--shard", default="request", choices=["request", "sequence"],
+                    help="N>1 partitioning: requests per rank (weak scaling, default) or one batch's "
+                         "positions split over the ranks with a per-layer LSE combine (strong scaling)")
     ap.add_argument("--scorer", default="attention", choices=["attention", "vatp"],
                     help="a4 token scorer: Eq. 1 attention or VATP (attention x ||v||, P:712)""")
     ap.add_argument("--no-extras", action="store_true", help="skip control/e2e/stream/cpu legs")
@@ -234,6 +237,8 @@ def main():
                    scorer=1 if args.scorer == "vatp" else 0)
     dev = f"cuda:{local}"
     peaks = _peaks()
+    if args.shard == "sequence":
+        return run_sequence_sharded(args, w, world, rank, local, dev, peaks)
     from paper_2605_09490_b200.dist import shard_plan
     seed_off, _ = shard_plan(world, rank, 1)
 
@@ -456,6 +461,59 @@ def main():
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_sequence_sharded(args, w, world, rank, local, dev, peaks):
+    """--shard sequence: the ranks share ONE batch, each owning the 64-position blocks
+    k % world == rank; per layer decode_attention_lse + an all-gather of (o, m, l) over NCCL +
+    the rank-order LSE combine + score_update_lse.  Strong scaling: the
+    value is full-batch steps/s.  Per-layer host-driven launches (no step graph)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_09490_b200 import harness as H
+    from paper_2605_09490_b200 import kvtier as kt
+    W, K = args.warmup, args.steps
+    sr = H.SeqShardRank(w, rank, world, device=dev)
+    for _ in range(W):
+        sr.step()
+    _barrier_sync()
+    with ClockSampler(local) as clk:
+        el = timed(sr.step, sr.run.main, K)
+    _barrier_sync()
+    el_max = _max_over_ranks(el)
+    sr.run.sync()
+    counts, _ = sr.run.kv.census()
+    own = [int(x) for x in counts[0]]
+    n_vis_own = own[0] + own[1] + own[2]
+    per_layer = attn_bytes_per_layer(w, own, n_vis_own)          # this rank's bytes per layer
+    L = w["L"]
+    step_bytes = _sum_over_ranks(L * per_layer)
+    sps = K / el_max
+    if rank == 0:
+        hbm = step_bytes * sps / 1e9
+        print(json.dumps({
+            "metric": "tiered decode steps/sec (+ HBM GB/s vs roofline, T1 prefetch overhead %)",
+            "value": sps, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": 1e3 / sps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.config}-shaped (BASELINE.json configs[{CONFIG_INDEX.get(args.config, '?')}]): "
+                                   f"B={w['B']} (whole batch) L={L} Hq/Hkv={w['Hq']}/{w['Hkv']} d={w['d']} N={w['N']} "
+                                   f"beta={args.hbm}bp r={args.evict}bp, sequence-sharded",
+                       "global_batch": w["B"], "parallelism": f"sequence-sharded x{world} (64-position blocks, "
+                                                            f"per-layer NCCL all-gather + LSE combine)"},
+            "hbm_gbs": hbm, "hbm_frac_of_measured_peak": hbm / (peaks["hbm_gbs"] * world),
+            "step_bytes": int(step_bytes), "census_rank0_b0": own,
+            "clocks": clk.summary(), "gpu_launches": K * (3 * L + 2),
+            "note": "per-layer host-driven launches and collectives (no step graph): the combine sits between layers",
+        }), flush=True)
+    sr.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _sum_over_ranks(x):
+    from paper_2605_09490_b200.dist import sum_over_ranks
+    return sum_over_ranks(x)
 
 
 def run_split(w, args):
