@@ -202,6 +202,15 @@ KV_TIER_API kv_tier_status kv_tier_decode_attention_lse(kv_tier_ctx* ctx, int32_
                                                         const void* k_new, const void* v_new, void* o, float* lse,
                                                         int32_t fuse_score_update, void* stream);
 
+/* Rank combine of sequence-shard partials (the LSE merge of Eq. 3 split by position; no ctx):
+ * o_parts device fp32 [world][rows][d] (each rank's o normalised by its own partial sum),
+ * lse_parts [world][rows][2] (m in the log2 domain, l); writes o_out [rows][d] and
+ * lse_out [rows][2] = (M, L) with M = max_r m_r, w_r = 2^(m_r - M) l_r (0 for m_r = -inf),
+ * L = sum_r w_r and o = sum_r w_r o_r / L (0 if L = 0), summed in rank order (deterministic).
+ * rows = B * H_q.  d % 4 == 0 and 16-B aligned pointers, else E_INVAL. */
+KV_TIER_API kv_tier_status kv_tier_lse_combine(const float* o_parts, const float* lse_parts, int32_t world,
+                                               int32_t rows, int32_t d, float* o_out, float* lse_out, void* stream);
+
 /* Completes the pending fused score update of the last kv_tier_decode_attention_lse with the
  * GLOBAL per-head (M, L) (device fp32 [B][H_q][2], same encoding; the combination of every
  * rank's lse): S_part += sum_h 2^(z - M) / L over this ctx's tokens.  lse_global must stay

@@ -1172,6 +1172,43 @@ __global__ void k_set_ml(const DevView v, const int zslot, const float* __restri
   }
 }
 
+// Rank combine of sequence-shard partials (kv_tier_lse_combine): one thread per (row, 4 lanes
+// of d), ranks in order.
+__global__ void k_lse_combine(const float* __restrict__ op, const float* __restrict__ lp, const int world,
+                              const int rows, const int d, float* __restrict__ oo, float* __restrict__ lo) {
+  const int d4 = d / 4;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)rows * d4) return;
+  const int row = (int)(i / d4), j = (int)(i - (long long)row * d4);
+  float M = -INFINITY;
+  for (int r = 0; r < world; ++r) M = fmaxf(M, lp[((size_t)r * rows + row) * 2]);
+  float L = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int r = 0; r < world; ++r) {
+    const float m = lp[((size_t)r * rows + row) * 2], l = lp[((size_t)r * rows + row) * 2 + 1];
+    const float wr = m == -INFINITY ? 0.f : ex2_ftz(m - M) * l;
+    const float4 x = reinterpret_cast<const float4*>(op + ((size_t)r * rows + row) * d)[j];
+    L += wr;
+    acc.x += wr * x.x;
+    acc.y += wr * x.y;
+    acc.z += wr * x.z;
+    acc.w += wr * x.w;
+  }
+  const float il = L > 0.f ? 1.0f / L : 0.f;
+  reinterpret_cast<float4*>(oo + (size_t)row * d)[j] = make_float4(acc.x * il, acc.y * il, acc.z * il, acc.w * il);
+  if (j == 0) {
+    lo[(size_t)row * 2] = M;
+    lo[(size_t)row * 2 + 1] = L;
+  }
+}
+
+cudaError_t launch_lse_combine(const float* op, const float* lp, int world, int rows, int d, float* oo, float* lo,
+                               cudaStream_t s) {
+  const long long n = (long long)rows * (d / 4);
+  k_lse_combine<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(op, lp, world, rows, d, oo, lo);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_set_ml(const DevView& v, int zslot, const float* lse, cudaStream_t s) {
   k_set_ml<<<v.B * v.Hkv, 32, 0, s>>>(v, zslot, lse);
   return cudaGetLastError();

@@ -656,6 +656,17 @@ kv_tier_status kv_tier_decode_attention_lse(kv_tier_ctx* ctx, int32_t layer, con
   return decode_attention_impl(ctx, layer, q, k_new, v_new, o, fuse_score_update, stream, 0, lse);
 }
 
+kv_tier_status kv_tier_lse_combine(const float* o_parts, const float* lse_parts, int32_t world, int32_t rows,
+                                   int32_t d, float* o_out, float* lse_out, void* stream) {
+  if (!o_parts || !lse_parts || !o_out || !lse_out || world < 1 || rows < 0 || d < 4 || d % 4)
+    return fail(nullptr, KV_TIER_E_INVAL, "lse_combine: null pointer or bad shape (world >= 1, d %% 4 == 0)");
+  if ((((uintptr_t)o_parts) | ((uintptr_t)o_out)) & 15 || (((uintptr_t)lse_parts) | ((uintptr_t)lse_out)) & 7)
+    return fail(nullptr, KV_TIER_E_INVAL, "lse_combine: o must be 16-B and lse 8-B aligned");
+  if (rows == 0) return KV_TIER_OK;
+  return cuda_check(nullptr, launch_lse_combine(o_parts, lse_parts, world, rows, d, o_out, lse_out,
+                                                reinterpret_cast<cudaStream_t>(stream)), "lse_combine");
+}
+
 kv_tier_status kv_tier_score_update_lse(kv_tier_ctx* ctx, const float* lse_global, void* stream) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (!lse_global || ((uintptr_t)lse_global & 7)) return fail(ctx, KV_TIER_E_INVAL, "lse_global must be an 8-B aligned device pointer");

@@ -192,6 +192,8 @@ cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const
                                void* o, int zpar, int pdl, cudaStream_t s, float* lse = nullptr);
 cudaError_t launch_set_ml(const DevView& v, int zslot, const float* lse, cudaStream_t s);
 cudaError_t launch_vnorm_prefix(const DevView& v, int layer, const void* vv, int n0, cudaStream_t s);
+cudaError_t launch_lse_combine(const float* op, const float* lp, int world, int rows, int d, float* oo, float* lo,
+                               cudaStream_t s);
 cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_t s);
 cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s);
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);

@@ -125,12 +125,17 @@ def seq_owned_positions(n, world, rank):
 
 
 def lse_combine(o_parts, lse_parts):
-    """Combine per-rank partial attention results (rank order, deterministic).
+    """Combine per-rank partial attention results (rank order, deterministic).  CUDA tensors run
+    the library kernel (kv_tier_lse_combine); CPU tensors (gloo host-logic tests only) the same
+    arithmetic in torch.
 
     o_parts [W][B][H][d]: each rank's o normalised by its own partial sum; lse_parts
     [W][B][H][2]: (m, l) per head, m in the log2 domain, l = sum 2^(z - m) (a rank without
     visible tokens has m = -inf, l = 0, o = 0).  Returns (o [B][H][d], lse [B][H][2]) with
     M = max_r m_r, w_r = 2^(m_r - M) l_r, L = sum_r w_r, o = sum_r w_r o_r / L."""
+    if o_parts.is_cuda:
+        from . import kvtier as kt
+        return kt.lse_combine(o_parts, lse_parts)
     m, l = lse_parts[..., 0], lse_parts[..., 1]
     M = m.max(dim=0).values
     w = torch.where(torch.isinf(m), torch.zeros_like(l), torch.exp2(m - M) * l)

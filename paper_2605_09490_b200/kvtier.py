@@ -66,6 +66,8 @@ _SIGS = {
     "kv_tier_decode_attention_lse": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_int32, C.c_void_p],
     "kv_tier_score_update_lse": [C.c_void_p, C.c_void_p, C.c_void_p],
+    "kv_tier_lse_combine": [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                            C.c_void_p],
     "kv_tier_score_update": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p],
     "kv_tier_visible_count": [C.c_void_p, C.POINTER(C.c_int32)],
     "kv_tier_end_step": [C.c_void_p, C.c_void_p],
@@ -316,6 +318,22 @@ class KvTier:
 
 
 NTRACE = 24            # trace slots per CTA (kv_internal.cuh)
+
+
+def lse_combine(o_parts, lse_parts, stream=None):
+    """Rank combine of sequence-shard partials on the GPU (kv_tier_lse_combine): o_parts
+    [W][..., d] fp32, lse_parts [W][..., 2] fp32 (contiguous CUDA tensors) -> (o, lse)."""
+    import torch
+    assert o_parts.is_cuda and o_parts.dtype == torch.float32 and lse_parts.dtype == torch.float32
+    o_parts, lse_parts = o_parts.contiguous(), lse_parts.contiguous()
+    W, d = o_parts.shape[0], o_parts.shape[-1]
+    rows = o_parts[0].numel() // d
+    o = torch.empty(o_parts.shape[1:], dtype=torch.float32, device=o_parts.device)
+    lse = torch.empty(lse_parts.shape[1:], dtype=torch.float32, device=o_parts.device)
+    s = stream if stream is not None else torch.cuda.current_stream(o_parts.device)
+    _check(load().kv_tier_lse_combine(C.c_void_p(o_parts.data_ptr()), C.c_void_p(lse_parts.data_ptr()), W, rows, d,
+                                      C.c_void_p(o.data_ptr()), C.c_void_p(lse.data_ptr()), _stream_ptr(s)))
+    return o, lse
 
 
 def version():

@@ -554,3 +554,35 @@ def test_vatp_scorer_parity(api):
     w = H.workload("tiny", B=3, L=2, Hq=8, Hkv=2, d=128, N=600, P=32, interval=8, steps=26,
                    hbm_bp=4000, evict_bp=800, t2_bp=3000, scorer=kt.SCORER_VATP)
     _run_pair(w, graph=api == "graph", layers_api=api == "layers", check_every=4)
+
+
+def test_lse_combine_kernel_matches_full_softmax():
+    # kv_tier_lse_combine: shards of a softmax-weighted sum, combined in rank order, equal the
+    # float64 softmax over the concatenation; an empty shard (m = -inf, l = 0) contributes nothing
+    g = torch.Generator().manual_seed(3)
+    W, rows, n, d = 4, 37, 90, 64
+    z = torch.randn(rows, n, generator=g, dtype=torch.float64) * 3
+    V = torch.randn(n, d, generator=g, dtype=torch.float64)
+    ref = torch.softmax(z * np.log(2), dim=-1) @ V
+    cuts = [0, 30, 30, 61, 90]                        # rank 1 owns nothing
+    o_parts, lse_parts = [], []
+    for r in range(W):
+        zz, vv = z[:, cuts[r]:cuts[r + 1]], V[cuts[r]:cuts[r + 1]]
+        if zz.shape[1] == 0:
+            o_parts.append(torch.zeros(rows, d, dtype=torch.float64))
+            lse_parts.append(torch.tensor([[-float("inf"), 0.0]] * rows, dtype=torch.float64))
+            continue
+        m = zz.max(dim=-1).values
+        p = torch.exp2(zz - m[:, None])
+        l = p.sum(dim=-1)
+        o_parts.append(p @ vv / l[:, None])
+        lse_parts.append(torch.stack([m, l], dim=-1))
+    op = torch.stack(o_parts).float().cuda()
+    lp = torch.stack(lse_parts).float().cuda()
+    o, lse = kt.lse_combine(op, lp)
+    torch.cuda.synchronize()
+    assert (o.double().cpu() - ref).abs().max() < 1e-5
+    M = z.max(dim=-1).values
+    assert torch.equal(lse[:, 0].double().cpu(), M.float().double())
+    L = torch.exp2(z - M[:, None]).sum(dim=-1)
+    assert ((lse[:, 1].double().cpu() - L) / L).abs().max() < 1e-5
