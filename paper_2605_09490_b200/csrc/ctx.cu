@@ -236,7 +236,7 @@ int n_protected(const kv_tier_config& c, int n) {
 
 extern "C" {
 
-const char* kv_tier_version(void) { return "kvtier-b200 0.1 (sm_100a, mma.sync+cluster decode)"; }
+const char* kv_tier_version(void) { return "kvtier-b200 0.2 (sm_100a: bulk-copy ring + mma.sync split decode, PDL merge chain)"; }
 
 const char* kv_tier_last_error(const kv_tier_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_err.c_str();
