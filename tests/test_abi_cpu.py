@@ -82,3 +82,37 @@ def test_init_without_gpu_fails_loudly():
     h = C.c_void_p()
     st = kt.load().kv_tier_init(C.byref(cfg), C.byref(buf), None, C.byref(h))
     assert st == -2                      # E_CUDA: there is no CPU fallback
+
+
+# --------------------------------------------------------------------- host logic without a GPU
+def test_sequence_shard_store_sizing():
+    # a sequence shard's stores hold its own positions only: T0 = owned rows
+    # (+ one block), T1 = 1.25x its share + one block, host stores by owned row
+    from paper_2605_09490_b200 import dist as D
+    N, W = 16640, 8
+    full = kt.query_sizes(kt.make_config(64, 80, 64, 8, 128, N, 64))
+    for r in (0, 3, 7):
+        s = kt.query_sizes(kt.make_config(64, 80, 64, 8, 128, N, 64, shard=kt.SHARD_SEQUENCE, rank=r, world=W))
+        own = len(D.seq_owned_positions(N, W, r))
+        assert own + 64 >= s.cap_t0 >= own and s.cap_t0 % 16 == 0
+        assert s.cap_t1 < full.cap_t1 and s.cap_t1 >= 1.25 * full.cap_t1 / W
+        assert s.host_t1 * W < 1.2 * full.host_t1
+        assert s.device_arena < 180e9 < full.device_arena          # 70B fits one B200 per shard
+
+
+def test_lse_combine_rejects_bad_arguments():
+    # argument errors are detected synchronously, before any launch
+    for args in ((None, None, 1, 1, 4, None, None), (1 << 20, 1 << 20, 1, 1, 6, 1 << 20, 1 << 20),
+                 (1 << 20, 1 << 20, 0, 1, 4, 1 << 20, 1 << 20), (0x10008, 1 << 20, 1, 1, 4, 1 << 20, 1 << 20)):
+        st = kt.load().kv_tier_lse_combine(*(C.c_void_p(a) if i in (0, 1, 5, 6) and a is not None else a
+                                             for i, a in enumerate(args)), None)
+        assert st == -1                                            # E_INVAL
+
+
+@pytest.mark.parametrize("field,value", [("policy", 9), ("scorer", 4), ("budget", 0)])
+def test_policy_and_scorer_validation(field, value):
+    kw = dict(policy=kt.POLICY_H2O, budget=100)
+    kw[field] = value
+    cfg = kt.make_config(2, 1, 4, 2, 64, 300, 16, **kw)
+    s = kt.Sizes()
+    assert kt.load().kv_tier_query_sizes(C.byref(cfg), C.byref(s)) == -1
