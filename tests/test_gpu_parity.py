@@ -586,3 +586,48 @@ def test_lse_combine_kernel_matches_full_softmax():
     assert torch.equal(lse[:, 0].double().cpu(), M.float().double())
     L = torch.exp2(z - M[:, None]).sum(dim=-1)
     assert ((lse[:, 1].double().cpu() - L) / L).abs().max() < 1e-5
+
+
+# --------------------------------------------------------------------- randomized configurations
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVT_FUZZ_SEEDS", "24"))))
+def test_randomized_configs(seed):
+    # seeded draws over the configuration space (shapes, ratios, T2, eviction mode, interval,
+    # staging, tier policy, scorer) against the oracle: catches interactions no fixed test covers
+    rng = np.random.default_rng(1000 + seed)
+    Hkv = int(rng.choice([1, 2, 4]))
+    G = int(rng.choice([1, 2, 5, 7, 8]))
+    d = int(rng.choice([64, 128]))
+    N = int(rng.integers(150, 900))
+    P = int(rng.integers(0, 48))
+    pol = int(rng.choice([kt.POLICY_HIERARCHY] * 4 + [kt.POLICY_STREAMING, kt.POLICY_H2O, kt.POLICY_RANDOM]))
+    w = H.workload("tiny", B=int(rng.integers(1, 5)), L=int(rng.integers(1, 4)), Hq=Hkv * G, Hkv=Hkv, d=d, N=N, P=P,
+                   interval=int(rng.choice([4, 8, 16])), steps=int(rng.integers(10, 22)),
+                   hbm_bp=int(rng.integers(0, 10001)), evict_bp=int(rng.integers(0, 2001)),
+                   t2_bp=int(rng.choice([0, 0, 2500, 10000])),
+                   evict_mode=int(rng.choice([kt.EVICT_TOTAL, kt.EVICT_PER_EVENT])),
+                   staging=int(rng.choice([kt.STAGING_ALL, kt.STAGING_ALL, 0])),
+                   policy=pol, budget=int(rng.integers(P + 140, N + 50)) if pol in (2, 3) else 0,
+                   policy_seed=seed, scorer=int(rng.choice([0, 0, kt.SCORER_VATP])))
+    _run_pair(w, graph=bool(rng.integers(0, 2)), check_every=3)
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVT_FUZZ_SEEDS_SEQ", "8"))))
+def test_randomized_sequence_shards(seed):
+    rng = np.random.default_rng(5000 + seed)
+    Hkv = int(rng.choice([1, 2]))
+    w = H.workload("tiny", B=int(rng.integers(1, 4)), L=int(rng.integers(1, 3)), Hq=Hkv * int(rng.choice([2, 4, 7])),
+                   Hkv=Hkv, d=int(rng.choice([64, 128])), N=int(rng.integers(100, 700)), P=int(rng.integers(0, 40)),
+                   interval=int(rng.choice([4, 8])), steps=int(rng.integers(8, 18)), hbm_bp=int(rng.integers(0, 10001)),
+                   evict_bp=int(rng.integers(0, 1500)), t2_bp=int(rng.choice([0, 3000])),
+                   staging=int(rng.choice([kt.STAGING_ALL, 0])))
+    sh = H.SeqShardedDecode(w, int(rng.integers(2, 5)))
+    orc = OracleRun(w)
+    for t in range(w["steps"]):
+        sh.step()
+        ok, mabs, _ = o_close(sh.output()[:, orc.reqs], orc.step())
+        assert ok, (t, mabs)
+        if sh.is_event(t):
+            ok, mrel = s_close(sh.scores()[orc.reqs], orc.st.S_part[:, :, :orc.st.n])
+            assert ok, (t, mrel)
+            _check_seq_event_state(sh, orc, layers=tuple(range(w["L"])))
+    sh.close()
