@@ -48,6 +48,8 @@ def _args():
     ap.add_argument("--hbm", type=int, default=5000, help="beta in basis points")
     ap.add_argument("--evict", type=int, default=500, help="r in basis points")
     ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=0,
+                    help="requests per GPU (0: the config's B); e.g. 16 = the 32B config's share on 2 GPUs")
     ap.add_argument("--variant", type=int, default=0, help="decode kernel variant (consumer warps x stages)")
     ap.add_argument("--policy", default="hierarchy", choices=list(POLICIES),
                     help="tier policy: the paper's hierarchy or a pure-eviction baseline (P:276-280)")
@@ -232,7 +234,8 @@ def main():
     W, K = args.warmup, args.steps
     E = 0 if args.no_extras else min(K, 64)
     pol = POLICIES[args.policy]
-    w = H.workload(args.config, hbm_bp=args.hbm, evict_bp=args.evict, steps=W + K + E + 1, policy=pol,
+    over = {"B": args.batch} if args.batch else {}
+    w = H.workload(args.config, hbm_bp=args.hbm, evict_bp=args.evict, steps=W + K + E + 1, policy=pol, **over,
                    budget=args.budget if pol in (2, 3) else 0, policy_seed=7,
                    scorer=1 if args.scorer == "vatp" else 0)
     dev = f"cuda:{local}"

@@ -25,8 +25,10 @@ EVICT_TOTAL, EVICT_PER_EVENT = 0, 1
 # tier policies: the paper's hierarchy and its pure-eviction baselines (§4.1 P:276-280;
 # SPEC §baselines)
 POLICY_HIERARCHY, POLICY_STREAMING, POLICY_H2O, POLICY_RANDOM = 0, 1, 2, 3
-# token scorers of the score update: Eq. 1 attention or VATP, attention x ||v||
-SCORER_ATTENTION, SCORER_VATP = 0, 1
+# token scorers (§4 ablation P:707-714): Eq. 1 attention; VATP, attention x ||v||
+# (P:712); redundancy, attention - neighbour cosine; combined, attention x ||v|| -
+# redundancy.  Readings AMB-30/31 in DESIGN.md.
+SCORER_ATTENTION, SCORER_VATP, SCORER_REDUNDANCY, SCORER_COMBINED = 0, 1, 2, 3
 
 
 # ----------------------------------------------------------------- attention
@@ -203,10 +205,56 @@ def policy_counts(policy, budget, n_protected, n_live, n_t3, cfg):
     return n_live - keep, keep, 0, 0
 
 
-def classify_request(S_part_b, tier_b, n, cfg, req=0):
+def ordered_bits(f):
+    """Order-preserving map fp32 -> uint32 (sign-magnitude to unsigned): for non-negative
+    values it orders exactly like the raw bits (AMB-7); negatives sort below every positive."""
+    u = np.asarray(f, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    return np.where(u & 0x80000000, 0xFFFFFFFF - u, u | 0x80000000).astype(np.uint64)
+
+
+def key_redundancy(K):
+    """Neighbour-cosine redundancy (reading AMB-30): per layer l and kv head g,
+    c_i = cos(k_i, k_{i-1}) of the ORIGINAL key rows (fp64, rounded to fp32), c_0 = 0, 0 when
+    either row is zero; R_part[b][g][i] = fp32 sum over layers in ascending l.
+    K: fp32 [L][B][H_kv][N][d].  Returns R_part fp32 [B][H_kv][N]."""
+    K = np.asarray(K, dtype=np.float64)
+    L, B, Hkv, N, d = K.shape
+    c = np.zeros((L, B, Hkv, N), dtype=np.float32)
+    if N > 1:
+        a, p = K[..., 1:, :], K[..., :-1, :]
+        dot = np.sum(a * p, axis=-1)
+        na, nb = np.sum(a * a, axis=-1), np.sum(p * p, axis=-1)
+        ok = (na > 0) & (nb > 0)
+        c[..., 1:] = np.where(ok, dot / np.sqrt(np.where(ok, na * nb, 1.0)), 0.0).astype(np.float32)
+    R = np.zeros((B, Hkv, N), dtype=np.float32)
+    for l in range(L):
+        R = (R + c[l]).astype(np.float32)
+    return R
+
+
+def classify_scores(S, R_part_b, live, cfg):
+    """The fp32 value ranked by classify (AMB-31).  Attention / VATP: S itself.  Redundancy /
+    combined ("attn - redundancy", P:713-714): I_i - rho_i with I_i = fp32(S_i / S_max)
+    (S_max = max of S over the live set, I = 0 if S_max = 0) and rho_i = fp32(fp32(sum_g
+    R_part[g][i]) / (L * H_kv)), the mean neighbour cosine over layers and kv heads."""
+    scorer = getattr(cfg, "scorer", SCORER_ATTENTION)
+    if scorer < SCORER_REDUNDANCY:
+        return S
+    n = S.shape[0]
+    smax = np.float32(S[live].max()) if live.any() else np.float32(0)
+    I = (S / smax).astype(np.float32) if smax > 0 else np.zeros(n, dtype=np.float32)
+    rsum = np.zeros(n, dtype=np.float32)
+    for g in range(R_part_b.shape[0]):
+        rsum = (rsum + R_part_b[g, :n]).astype(np.float32)
+    rho = (rsum / np.float32(cfg.L * cfg.Hkv)).astype(np.float32)
+    return (I - rho).astype(np.float32)
+
+
+def classify_request(S_part_b, tier_b, n, cfg, req=0, R_part_b=None):
     """One manage event for one request (Alg. 1 lines P:189-197; §3.3).
 
-    S_part_b: [H_kv][>=n] fp32, tier_b: [>=n] u8 current tiers (T3 sticky, AMB-16/24).
+    S_part_b: [H_kv][>=n] fp32, tier_b: [>=n] u8 current tiers (T3 sticky, AMB-16/24),
+    R_part_b: [H_kv][>=n] fp32 redundancy partials (redundancy / combined scorers only).
     Returns the new tier array [n] (uint8)."""
     S = total_score_fp32(np.asarray(S_part_b)[:, :n])
     prot = protected_mask(n, cfg.prompt_len, cfg.sink_size, cfg.window_size)
@@ -214,11 +262,11 @@ def classify_request(S_part_b, tier_b, n, cfg, req=0):
     t3 = old == T3
     live = ~prot & ~t3
     pos_live = np.nonzero(live)[0]
-    # order U_live by the unique key (bits(S_i), i) ascending (AMB-7); RANDOM: (hash, i)
+    # order U_live by the unique key (bits(score_i), i) ascending (AMB-7); RANDOM: (hash, i)
     if cfg.policy == POLICY_RANDOM:
         primary = np.array([random_key32(cfg.policy_seed, req, int(p)) for p in pos_live], dtype=np.uint64)
     else:
-        primary = S[pos_live].view(np.uint32)
+        primary = ordered_bits(classify_scores(S, R_part_b, live, cfg)[pos_live])
     order = np.lexsort((pos_live, primary))
     sorted_pos = pos_live[order]
     n_new, n_hbm, n_t2, n_t1 = policy_counts(cfg.policy, cfg.budget, int(prot.sum()), len(pos_live),
@@ -275,7 +323,8 @@ class OracleState:
     scaleV: np.ndarray
     t: int = 0
     events: list = field(default_factory=list)
-    vnorm: np.ndarray = None   # VATP: [L][B][Hkv][Nmax] fp32 ||v|| of every token's original V row
+    vnorm: np.ndarray = None   # VATP / combined: [L][B][Hkv][Nmax] fp32 ||v|| of every original V row
+    R_part: np.ndarray = None  # redundancy / combined: [B][Hkv][Nmax] fp32 (key_redundancy)
 
 
 def init_state(cfg, Kbits, Vbits, n0):
@@ -285,11 +334,14 @@ def init_state(cfg, Kbits, Vbits, n0):
     will ever generate (the never-migrated originals)."""
     from paper_2605_09490_b200.synth.synth import bf16_bits_to_f32   # input decoding only
     L, B, Hkv, Nmax, d = Kbits.shape
-    vnorm = None
-    if getattr(cfg, "scorer", SCORER_ATTENTION) == SCORER_VATP:
+    vnorm = R_part = None
+    scorer = getattr(cfg, "scorer", SCORER_ATTENTION)
+    if scorer in (SCORER_VATP, SCORER_COMBINED):
         vnorm = value_norms(bf16_bits_to_f32(Vbits))
+    if scorer in (SCORER_REDUNDANCY, SCORER_COMBINED):
+        R_part = key_redundancy(bf16_bits_to_f32(Kbits))
     return OracleState(
-        cfg=cfg, n=n0, vnorm=vnorm,
+        cfg=cfg, n=n0, vnorm=vnorm, R_part=R_part,
         tier=np.full((B, Nmax), T0, dtype=np.uint8),
         S_part=np.zeros((B, Hkv, Nmax), dtype=np.float32),
         rowK=bf16_bits_to_f32(Kbits).copy(), rowV=bf16_bits_to_f32(Vbits).copy(),
@@ -387,7 +439,8 @@ def manage_event(st):
     B = st.tier.shape[0]
     for b in range(B):
         old = st.tier[b, :st.n].copy()
-        new = classify_request(st.S_part[b], old, st.n, cfg, req=cfg.req_ids[b] if cfg.req_ids else b)
+        new = classify_request(st.S_part[b], old, st.n, cfg, req=cfg.req_ids[b] if cfg.req_ids else b,
+                               R_part_b=None if st.R_part is None else st.R_part[b])
         to_t2 = (new == T2) & (old != T2)
         from_t2 = (old == T2) & ((new == T0) | (new == T1))
         for p in np.nonzero(to_t2)[0]:

@@ -542,3 +542,112 @@ def test_vatp_weights_are_value_row_norms():
         vnorm = vn[None, None, None, :]
     inc = O.score_increment(np.array([0.25, 0.5, 0.25]), St, 0, 0, 0, np.arange(3))
     assert inc.tolist() == [1.25, 0.5, 2.5]
+
+
+# ------------------------------------------------ redundancy / combined scorers
+def test_ordered_bits_sorts_like_the_values():
+    # order pin: ranking by ordered_bits equals ranking by value for mixed signs, and equals
+    # the raw-bit order of AMB-7 on non-negative values
+    rng = np.random.default_rng(5)
+    f = np.concatenate([rng.standard_normal(500), [0.0, 1e-40, -1e-40, 3.4e38, -3.4e38]]).astype(np.float32)
+    ob = O.ordered_bits(f)
+    assert np.array_equal(np.argsort(ob, kind="stable"), np.argsort(f, kind="stable"))
+    pos = np.abs(f)
+    assert np.array_equal(np.argsort(O.ordered_bits(pos), kind="stable"),
+                          np.argsort(pos.view(np.uint32), kind="stable"))
+
+
+def test_key_redundancy_bruteforce_and_closed_forms():
+    # brute force in plain Python (math.fsum / math.sqrt) on a tiny random K, plus closed forms:
+    # a scaled copy of the previous key has cosine 1, its negation -1, a zero row 0, position 0 is 0
+    rng = np.random.default_rng(9)
+    L, B, Hkv, N, d = 3, 2, 2, 7, 5
+    K = rng.standard_normal((L, B, Hkv, N, d)).astype(np.float32)
+    K[:, 0, 0, 3] = 2.0 * K[:, 0, 0, 2]          # cos = 1 at i = 3
+    K[:, 0, 1, 4] = -K[:, 0, 1, 3]               # cos = -1 at i = 4
+    K[:, 1, 0, 5] = 0.0                          # zero row: cos(k5, k4) = cos(k6, k5) = 0
+    R = O.key_redundancy(K)
+    for b in range(B):
+        for g in range(Hkv):
+            for i in range(N):
+                acc = np.float32(0)
+                for l in range(L):
+                    c = 0.0
+                    if i > 0:
+                        a = [float(x) for x in K[l, b, g, i]]
+                        p = [float(x) for x in K[l, b, g, i - 1]]
+                        na, nb = math.fsum(x * x for x in a), math.fsum(x * x for x in p)
+                        if na > 0 and nb > 0:
+                            c = math.fsum(x * y for x, y in zip(a, p)) / math.sqrt(na * nb)
+                    acc = np.float32(acc + np.float32(c))
+                assert abs(float(R[b, g, i]) - float(acc)) <= 2e-6 * L, (b, g, i)
+    assert R[0, 0, 3] == pytest.approx(L, abs=1e-5)
+    assert R[0, 1, 4] == pytest.approx(-L, abs=1e-5)
+    assert R[1, 0, 5] == 0.0 and R[1, 0, 6] == 0.0
+    assert np.all(R[:, :, 0] == 0.0)
+
+
+def _red_cfg(scorer, L=2, Hkv=2, P=2, ks=1, kw=2, hbm_bp=5000, evict_bp=2500):
+    return O.OracleConfig(B=1, L=L, Hq=Hkv, Hkv=Hkv, d=4, prompt_len=P, sink_size=ks, window_size=kw,
+                          hbm_bp=hbm_bp, evict_bp=evict_bp, scorer=scorer)
+
+
+def test_redundancy_evicts_the_most_redundant_tokens_first():
+    # P:713 "penalizes tokens with high cosine similarity to neighbors": with equal attention
+    # scores the evicted tokens are exactly the live ones with the largest mean neighbour cosine
+    n, Hkv = 13, 2
+    cfg = _red_cfg(O.SCORER_REDUNDANCY, Hkv=Hkv)
+    S = np.full((Hkv, n), 0.5, np.float32)
+    rng = np.random.default_rng(3)
+    R = rng.uniform(-2, 2, size=(Hkv, n)).astype(np.float32)
+    new = O.classify_request(S, np.zeros(n, np.uint8), n, cfg, R_part_b=R)
+    prot = O.protected_mask(n, cfg.prompt_len, cfg.sink_size, cfg.window_size)
+    live = np.nonzero(~prot)[0]
+    rho = [float(np.float32(np.float32(R[0, i] + R[1, i]) / np.float32(cfg.L * Hkv))) for i in live]
+    order = [p for _, p in sorted(zip([-r for r in rho], live), key=lambda x: (x[0], x[1]))]
+    n3 = int(len(live) * cfg.evict_bp // 10000)
+    assert n3 >= 1
+    assert sorted(np.nonzero(new == O.T3)[0].tolist()) == sorted(order[:n3])
+
+
+def test_redundancy_reduces_to_attention_when_rho_is_constant():
+    # special case: a constant redundancy shifts every key by the same amount, and S/S_max is
+    # monotone in S, so the tiers equal the attention scorer's; the combined scorer likewise
+    # reduces to VATP (same S input -> same tiers as the attention ranking of that S)
+    n, Hkv = 40, 2
+    rng = np.random.default_rng(11)
+    S = rng.uniform(0.1, 3.0, size=(Hkv, n)).astype(np.float32)
+    R = np.full((Hkv, n), 0.25, np.float32)
+    base = O.classify_request(S, np.zeros(n, np.uint8), n, _red_cfg(O.SCORER_ATTENTION, hbm_bp=4000, evict_bp=1500))
+    for sc in (O.SCORER_REDUNDANCY, O.SCORER_COMBINED):
+        got = O.classify_request(S, np.zeros(n, np.uint8), n, _red_cfg(sc, hbm_bp=4000, evict_bp=1500), R_part_b=R)
+        assert np.array_equal(got, base)
+
+
+def test_classify_scores_closed_form():
+    # I = S / S_max over the live set (protected positions excluded from the max), rho = mean
+    # of R over layers x kv heads; a position whose S equals S_max and rho = 0 keys to 1
+    cfg = _red_cfg(O.SCORER_REDUNDANCY, L=2, Hkv=2)
+    S = np.array([100.0, 2.0, 4.0, 1.0], np.float32)
+    live = np.array([False, True, True, True])
+    R = np.array([[0.0, 0.5, 0.0, -1.0], [0.0, 0.5, 0.0, -1.0]], np.float32)
+    k = O.classify_scores(S, R, live, cfg)
+    assert k[2] == 1.0
+    assert k[1] == np.float32(0.5) - np.float32(0.25)
+    assert k[3] == np.float32(0.25) + np.float32(0.5)
+    assert k[0] == np.float32(25.0)
+
+
+def test_combined_increments_are_vatp_weighted():
+    # the combined scorer accumulates the VATP increment (attention x ||v||); r = 0 so
+    # the different rankings cannot change the visible set
+    from paper_2605_09490_b200 import harness as Hh
+    from tests.oracle_runner import OracleRun
+    outs = {}
+    for sc in (O.SCORER_VATP, O.SCORER_COMBINED):
+        w = Hh.workload("tiny", L=2, steps=3, interval=64, scorer=sc, evict_bp=0)
+        r = OracleRun(w)
+        for _ in range(3):
+            r.step()
+        outs[sc] = r.st.S_part.copy()
+    assert np.array_equal(outs[O.SCORER_VATP], outs[O.SCORER_COMBINED])
