@@ -27,6 +27,7 @@ sys.path.insert(0, ROOT)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
 CONFIG_INDEX = {"tiny": 0, "7b": 1, "14b": 2, "32b": 3, "70b": 4}      # BASELINE.json configs[i]
 POLICIES = {"hierarchy": 0, "streaming": 1, "h2o": 2, "random": 3}       # kv_tier_policy
+SCORERS = {"attention": 0, "vatp": 1, "redundancy": 2, "combined": 3}    # kv_tier_scorer
 
 
 def _peaks():
@@ -57,8 +58,8 @@ def _args():
     ap.add_argument("--shard", default="request", choices=["request", "sequence"],
                     help="N>1 partitioning: requests per rank (weak scaling, default) or one batch's "
                          "positions split over the ranks with a per-layer LSE combine (strong scaling)")
-    ap.add_argument("--scorer", default="attention", choices=["attention", "vatp"],
-                    help="a4 token scorer: Eq. 1 attention or VATP (attention x ||v||, P:712)""")
+    ap.add_argument("--scorer", default="attention", choices=list(SCORERS),
+                    help="token scorer: Eq. 1 attention, VATP (P:712), redundancy (P:713), combined (P:714)")
     ap.add_argument("--no-extras", action="store_true", help="skip control/e2e/stream/cpu legs")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -237,7 +238,7 @@ def main():
     over = {"B": args.batch} if args.batch else {}
     w = H.workload(args.config, hbm_bp=args.hbm, evict_bp=args.evict, steps=W + K + E + 1, policy=pol, **over,
                    budget=args.budget if pol in (2, 3) else 0, policy_seed=7,
-                   scorer=1 if args.scorer == "vatp" else 0)
+                   scorer=SCORERS[args.scorer])
     dev = f"cuda:{local}"
     peaks = _peaks()
     if args.shard == "sequence":

@@ -100,8 +100,17 @@ typedef enum { KV_TIER_POLICY_HIERARCHY = 0, KV_TIER_POLICY_STREAMING = 1, KV_TI
  *   ATTENTION  Eq. 1: S_i += sum_h p_{l,h,i}.
  *   VATP       value-aware attention: S_i += fp32(sum_h p_{l,h,i}) * ||v_{l,g,i}||_2, the
  *              fp32 L2 norm of the token's bf16 V row of layer l, kv head g, fixed when the row
- *              is loaded / appended.  Split decode kernel only (not KVTIER_FLAT / KVTIER_CLUSTER). */
-typedef enum { KV_TIER_SCORER_ATTENTION = 0, KV_TIER_SCORER_VATP = 1 } kv_tier_scorer;
+ *              is loaded / appended.  Split decode kernel only (not KVTIER_FLAT / KVTIER_CLUSTER).
+ *   REDUNDANCY "attn - redundancy" (R-KV): S as ATTENTION; classify ranks by
+ *              I_i - rho_i, I_i = fp32(S_i / S_max over the live set), rho_i the mean over layers
+ *              and kv heads of c_i = cos(k_i, k_{i-1}) of the original key rows (DESIGN AMB-30/31).
+ *              c is formed when a row is loaded / appended (the ctx keeps the previous key of
+ *              every layer and kv head), so prefix layers must be loaded in ascending order.
+ *   COMBINED   "attn x val - redundancy": S as VATP, ranked as REDUNDANCY.
+ *   REDUNDANCY / COMBINED: request or KV-head sharding without classify_gathered (E_INVAL for
+ *   sequence sharding; kv_tier_classify_gathered returns E_STATE). */
+typedef enum { KV_TIER_SCORER_ATTENTION = 0, KV_TIER_SCORER_VATP = 1, KV_TIER_SCORER_REDUNDANCY = 2,
+               KV_TIER_SCORER_COMBINED = 3 } kv_tier_scorer;
 
 #define KV_TIER_STAGING_ALL 0xFFFFFFFFu   /* differential mode: staging holds all of T1 (§3.4) */
 
@@ -274,7 +283,8 @@ enum {
   KV_TIER_X_T1_ROWS = 6,    /* bf16 [B][H_kv][|T1|][2][d]  from the pinned host store      */
   KV_TIER_X_STAGING = 7,    /* bf16 [B][H_kv][|T1|][2][d]  HBM staging (differential mode) */
   KV_TIER_X_T2_CODES = 8,   /* i8   [B][H_kv][|T2|][2][d]                                  */
-  KV_TIER_X_T2_SCALES = 9   /* f32  [B][H_kv][|T2|][2]                                     */
+  KV_TIER_X_T2_SCALES = 9,  /* f32  [B][H_kv][|T2|][2]                                     */
+  KV_TIER_X_REDUNDANCY = 10 /* fp32 [B][H_kv][n]   R_part (AMB-30; zeros unless REDUNDANCY/COMBINED) */
 };
 /* Bytes `what` needs (counts are uniform across requests). */
 KV_TIER_API kv_tier_status kv_tier_export_size(kv_tier_ctx* ctx, int32_t what, size_t* bytes);

@@ -81,6 +81,19 @@ int split_of(const kv_tier_config& c) {
 
 int auto_split(const kv_tier_config& c) { return split_of(c); }
 
+// Logit ring slots: as many as fit a 60 MB share of the L2 persisting carve-out (2..ZRING).  A
+// ring larger than that thrashes L2 against the KV stream; long layers need fewer slots (the
+// score kernel lags the chain by about a layer).  Measured (profiles/r01/zring_r01.md): 32B
+// B=16 2 slots 146 vs 4 slots 128 steps/s; 14B 3 slots 431, 4 slots 416, 2 slots 369; 7B 4
+// slots 3005 vs 2 slots 2499.
+int zring_of(const kv_tier_config& c) {
+  if (const char* e = getenv("KVTIER_ZRING")) return std::max(2, std::min(ZRING, atoi(e)));
+  const size_t slot = (size_t)c.num_requests * c.num_kv_heads * (c.max_tokens + 64) * 8 * 4;
+  int k = ZRING;
+  while (k > 2 && (size_t)k * slot > ((size_t)60 << 20)) --k;
+  return k;
+}
+
 kv_tier_status validate(const kv_tier_config* c) {
   if (!c) return fail(nullptr, KV_TIER_E_INVAL, "null config");
   if (c->num_requests < 1 || c->num_requests > 1024) return fail(nullptr, KV_TIER_E_INVAL, "num_requests out of range");
@@ -104,8 +117,10 @@ kv_tier_status validate(const kv_tier_config* c) {
   if (c->variant < 0 || c->variant > 5) return fail(nullptr, KV_TIER_E_INVAL, "variant must be in [0, 5]");
   if (c->policy < KV_TIER_POLICY_HIERARCHY || c->policy > KV_TIER_POLICY_RANDOM)
     return fail(nullptr, KV_TIER_E_INVAL, "policy must be a kv_tier_policy");
-  if (c->scorer != KV_TIER_SCORER_ATTENTION && c->scorer != KV_TIER_SCORER_VATP)
+  if (c->scorer < KV_TIER_SCORER_ATTENTION || c->scorer > KV_TIER_SCORER_COMBINED)
     return fail(nullptr, KV_TIER_E_INVAL, "scorer must be a kv_tier_scorer");
+  if (scorer_uses_red(c->scorer) && c->shard == KV_TIER_SHARD_SEQUENCE && c->world > 1)
+    return fail(nullptr, KV_TIER_E_INVAL, "redundancy scorers need each position's predecessor: not with sequence sharding");
   if ((c->policy == KV_TIER_POLICY_H2O || c->policy == KV_TIER_POLICY_RANDOM) && c->budget < 1)
     return fail(nullptr, KV_TIER_E_INVAL, "H2O / RANDOM need budget >= 1 kept tokens per request");
   return KV_TIER_OK;
@@ -141,10 +156,12 @@ struct Layout {
   size_t off_k0[2], off_v0[2], off_k1[2], off_v1[2], off_c2k[2], off_c2v[2], off_s2k[2], off_s2v[2];
   size_t off_idx[2][3], off_vis[2], off_tier[2], off_row[2], off_cnt[2], off_S, off_fS, off_st, off_z, off_ml;
   size_t off_part, off_uctr, off_moves, off_mcount, off_scratch, off_mtemp, total, hot_begin, off_vnorm, off_zlayer;
+  size_t off_red, off_lastk;
   size_t b_t0, b_t1, b_t2, b_scores, b_meta;
 };
 
 int split_of(const kv_tier_config& c);
+int zring_of(const kv_tier_config& c);
 
 // Rows per group of the pinned host stores: every position, or a sequence shard's own ones.
 int host_rows_of(const kv_tier_config& c) {
@@ -200,14 +217,16 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   L.off_mtemp = take(B * mcap * LBH / B * 2 * D * 2);
   // hot, small: kept resident in L2 (access-policy window from off_S to the end)
   L.off_S = take(BH * N * 4);
-  L.off_z = take(ZRING * BH * (N + 64) * 8 * 4);     // logits of recent launches (score update)
+  L.off_z = take(zring_of(c) * BH * (N + 64) * 8 * 4);   // logits of recent launches (score update)
   L.off_ml = take(ZRING * BH * 16 * 4);
   const size_t nslots = std::max(BH * (split_of(c) + 1),                 // split kernel: per-CTA partials + new token
                                   (size_t)flat_grid(c, FLAT_GRID_MAX_SM) + 2 * BH);   // flat: <= grid + 2 units
   L.off_part = take(nslots * (16 + 8 * D) * 4);
   L.off_uctr = take(BH * 4);
   L.off_zlayer = take(ZRING * 4);
-  L.off_vnorm = take(c.scorer == KV_TIER_SCORER_VATP ? LBH * N * 4 : 0);   // VATP: V-row norms
+  L.off_vnorm = take(scorer_uses_vnorm(c.scorer) ? LBH * N * 4 : 0);     // VATP / combined: V-row norms
+  L.off_red = take(scorer_uses_red(c.scorer) ? BH * N * 4 : 0);          // redundancy partials R_part
+  L.off_lastk = take(scorer_uses_red(c.scorer) ? LBH * D * 2 : 0);       // previous key per (layer, kv head)
   L.b_scores = o - s0; s0 = o;
   for (int i = 0; i < 2; ++i) {
     L.off_idx[i][0] = take(B * cap0 * 4);
@@ -350,13 +369,16 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.zbuf = reinterpret_cast<float*>(A + L.off_z);
   v.ml = reinterpret_cast<float*>(A + L.off_ml);
   v.zrows = cfg->max_tokens + 64;
+  v.zring = zring_of(*cfg);
   v.part = reinterpret_cast<float*>(A + L.off_part);
   v.part_stride = 16 + 8 * v.D;
   v.unit_ctr = reinterpret_cast<int*>(A + L.off_uctr);
   v.zlayer = reinterpret_cast<int*>(A + L.off_zlayer);
   v.scorer = cfg->scorer;
-  v.vnorm = cfg->scorer == KV_TIER_SCORER_VATP ? reinterpret_cast<float*>(A + L.off_vnorm) : nullptr;
-  if (v.scorer == KV_TIER_SCORER_VATP) { v.flat = 0; v.cluster_merge = 0; }   // VATP: split kernel + merge kernel
+  v.vnorm = scorer_uses_vnorm(cfg->scorer) ? reinterpret_cast<float*>(A + L.off_vnorm) : nullptr;
+  v.red = scorer_uses_red(cfg->scorer) ? reinterpret_cast<float*>(A + L.off_red) : nullptr;
+  v.lastk = scorer_uses_red(cfg->scorer) ? reinterpret_cast<uint16_t*>(A + L.off_lastk) : nullptr;
+  if (v.scorer != KV_TIER_SCORER_ATTENTION) { v.flat = 0; v.cluster_merge = 0; }   // split kernel + merge kernel
   v.hot_base = A + L.hot_begin;
   v.hot_bytes = L.total - L.hot_begin;
   v.moves = reinterpret_cast<int4*>(A + L.off_moves);
@@ -476,6 +498,9 @@ kv_tier_status kv_tier_load_prefix(kv_tier_ctx* ctx, int32_t layer, const void* 
   if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
   if (!k || !v) return fail(ctx, KV_TIER_E_INVAL, "null k/v");
   if (ctx->t > 0 || ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "load_prefix after decoding started");
+  if (scorer_uses_red(ctx->v.scorer) &&
+      layer != (int)std::count(ctx->loaded_layers.begin(), ctx->loaded_layers.end(), 1))
+    return fail(ctx, KV_TIER_E_STATE, "redundancy scorers: load prefix layers once each, in ascending order (AMB-30)");
   if (n0 < 0 || seq_owned_below(ctx->v.seq_w, ctx->v.seq_r, n0) + 1 > ctx->v.cap0 || n0 + 1 > ctx->v.Nmax)
     return fail(ctx, KV_TIER_E_CAPACITY, "prefix of %d tokens exceeds T0 capacity %d / N_max %d", n0, ctx->v.cap0, ctx->v.Nmax);
   if (ctx->n0 >= 0 && ctx->n0 != n0) return fail(ctx, KV_TIER_E_INVAL, "n0 differs between layers");
@@ -491,8 +516,10 @@ kv_tier_status kv_tier_load_prefix(kv_tier_ctx* ctx, int32_t layer, const void* 
   }
   if (n0 > 0) {
     kv_tier_status st = cuda_check(ctx, launch_load_prefix(ctx->v, layer, k, v, n0, s), "load_prefix");
-    if (!st && ctx->v.scorer == KV_TIER_SCORER_VATP)
+    if (!st && scorer_uses_vnorm(ctx->v.scorer))
       st = cuda_check(ctx, launch_vnorm_prefix(ctx->v, layer, v, n0, s), "load_prefix (V norms)");
+    if (!st && scorer_uses_red(ctx->v.scorer))
+      st = cuda_check(ctx, launch_redund_prefix(ctx->v, layer, k, n0, s), "load_prefix (key redundancy)");
     if (st) return st;
   }
   ctx->loaded_layers[layer] = 1;
@@ -557,11 +584,11 @@ static cudaError_t issue_scores(kv_tier_ctx* ctx, cudaStream_t s) {
   (void)s;
   cudaError_t e = cudaSuccess;
   for (int j = 0; j < nz && e == cudaSuccess; ++j)    // launches may sit on different streams
-    e = cudaStreamWaitEvent(ctx->score_stream, ctx->ev_merged[(z0 + j) % ZRING], 0);
+    e = cudaStreamWaitEvent(ctx->score_stream, ctx->ev_merged[(z0 + j) % ctx->v.zring], 0);
   if (e == cudaSuccess) e = launch_score_flush(ctx->v, z0, nz, ctx->score_stream);
   if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_scored[z0], ctx->score_stream);
   if (e == cudaSuccess) {
-    for (int j = 0; j < nz; ++j) ctx->slot_busy[(z0 + j) % ZRING] = true;
+    for (int j = 0; j < nz; ++j) ctx->slot_busy[(z0 + j) % ctx->v.zring] = true;
     ctx->scores_pending = true;
     ctx->zpend_n = 0;
   }
@@ -622,7 +649,7 @@ static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, con
   if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, zpar, pdl, s, lse);
   if (e == cudaSuccess && zpar >= 0 && lse) {   // the update waits for the global (M, L)
     ctx->lse_pending = zpar;
-    ctx->zslot_next = (zpar + 1) % ZRING;
+    ctx->zslot_next = (zpar + 1) % ctx->v.zring;
     if (k_new) ctx->appended_step[layer] = ctx->t;
     return cuda_check(ctx, e, "decode_attention_lse");
   }
@@ -630,7 +657,7 @@ static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, con
   if (e == cudaSuccess && zpar >= 0) {
     if (ctx->zpend_n == 0) ctx->zpend_first = zpar;
     ctx->zpend_n += 1;
-    ctx->zslot_next = (zpar + 1) % ZRING;
+    ctx->zslot_next = (zpar + 1) % ctx->v.zring;
     if (ctx->zpend_n == ZBATCH) e = issue_scores(ctx, s);
   }
   if (e == cudaSuccess && ctx->v.stream_mode) {
@@ -746,6 +773,8 @@ kv_tier_status kv_tier_classify_gathered(kv_tier_ctx* ctx, const float* S_all, i
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (!S_all || parts < 1) return fail(ctx, KV_TIER_E_INVAL, "S_all must be a device pointer and parts >= 1");
   if (((uintptr_t)S_all) & 3) return fail(ctx, KV_TIER_E_INVAL, "S_all must be 4-B aligned");
+  if (scorer_uses_red(ctx->v.scorer))
+    return fail(ctx, KV_TIER_E_STATE, "redundancy scorers classify from the ctx's own R_part (kv_tier_classify)");
   return classify_impl(ctx, S_all, parts, stream);
 }
 
@@ -961,7 +990,7 @@ static kv_tier_status req_counts(kv_tier_ctx* ctx, std::vector<int>& cb) {
 static size_t export_bytes_req(const kv_tier_ctx* ctx, int32_t what, const int* c) {
   const size_t H = ctx->v.Hkv, D = ctx->v.D, n = ctx->n;
   switch (what) {
-    case KV_TIER_X_SCORES: return H * n * 4;
+    case KV_TIER_X_SCORES: case KV_TIER_X_REDUNDANCY: return H * n * 4;
     case KV_TIER_X_TIERS: return n;
     case KV_TIER_X_IDX_T0: return (size_t)c[0] * 4;
     case KV_TIER_X_IDX_T1: return (size_t)c[1] * 4;
@@ -1029,6 +1058,9 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
     off += export_bytes_req(ctx, what, c);
     if (what == KV_TIER_X_SCORES) {
       for (size_t g = 0; g < H && e == cudaSuccess; ++g) e = d2h(ob + g * n * 4, v.S + (b * H + g) * N, n * 4);
+    } else if (what == KV_TIER_X_REDUNDANCY) {
+      if (!v.red) memset(ob, 0, H * n * 4);
+      for (size_t g = 0; g < H && v.red && e == cudaSuccess; ++g) e = d2h(ob + g * n * 4, v.red + (b * H + g) * N, n * 4);
     } else if (what == KV_TIER_X_TIERS) {
       e = d2h(ob, v.tier[cur] + b * N, n);
     } else if (what >= KV_TIER_X_IDX_T0 && what <= KV_TIER_X_IDX_T2) {

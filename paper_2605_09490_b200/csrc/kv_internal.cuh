@@ -9,9 +9,15 @@ namespace kvt {
 constexpr int T0 = 0, T1 = 1, T2 = 2, T3 = 3;
 constexpr int NTRACE = 24;        // debug trace slots per CTA (KVTIER_TRACE=1)
 constexpr int CNT_STRIDE = 8;     // cnt[buf][b][8]: |T0| |T1| |T2| |T3| |visible at event| pad..
-constexpr int ZRING = 4;          // logits/ML ring slots (score kernels lag the decode chain)
+constexpr int ZRING = 4;          // max logits/ML ring slots (score kernels lag the decode chain);
+                                  // DevView::zring <= ZRING are used (zring_of in ctx.cu)
 constexpr int ZBATCH = 1;         // launches whose score updates one score kernel applies (layer order;
                                   // measured: batching 4 made the kernel too big to share SMs with the chain)
+
+// kv_tier_scorer: VATP (1) and combined (3) weight increments by ||v||; redundancy (2) and
+// combined (3) rank by I - rho (DESIGN AMB-30/31)
+__host__ __device__ constexpr bool scorer_uses_vnorm(int s) { return s == 1 || s == 3; }
+__host__ __device__ constexpr bool scorer_uses_red(int s) { return s == 2 || s == 3; }
 
 // Mutable device state (graph-static kernels read it instead of taking args).
 struct DevState {
@@ -34,8 +40,11 @@ struct DevView {
   int hbm_bp, evict_bp, t2_bp, evict_mode;
   int policy, budget;   // kv_tier_policy (tier policy of a5), kept tokens (H2O / RANDOM)
   int scorer;           // kv_tier_scorer (a4 increment: attention, or attention x ||v|| for VATP)
-  float* vnorm;         // VATP: [L][B][Hkv][Nmax] fp32 L2 norm of each token's V row (null otherwise)
+  float* vnorm;         // VATP / combined: [L][B][Hkv][Nmax] fp32 L2 norm of each token's V row (else null)
+  float* red;           // redundancy / combined: [B][Hkv][Nmax] fp32 R_part = sum_l cos(k_i, k_{i-1})
+  uint16_t* lastk;      // redundancy / combined: [L][B][Hkv][D] bf16 key of the last appended token
   int* zlayer;          // [ZRING] layer of the launch that filled each logit slot
+  int zring;            // logit ring slots in use (2..ZRING): the ring stays inside the L2 carve-out
   unsigned policy_seed;
   int stream_mode;      // staging_tokens == 0
   int out_fp32;
@@ -129,7 +138,7 @@ __host__ __device__ __forceinline__ void policy_counts(int policy, int budget, i
 
 // a4 weight of token (layer, unit, pos): 1 (Eq. 1) or its V-row norm (VATP)
 __device__ __forceinline__ float score_weight(const DevView& v, int layer, int unit, int pos) {
-  return v.scorer == 1 ? v.vnorm[((size_t)layer * v.B * v.Hkv + unit) * v.Nmax + pos] : 1.f;
+  return scorer_uses_vnorm(v.scorer) ? v.vnorm[((size_t)layer * v.B * v.Hkv + unit) * v.Nmax + pos] : 1.f;
 }
 
 // Sequence sharding: block-cyclic ownership of SEQ_BLOCK-position blocks.
@@ -173,6 +182,35 @@ constexpr int STORE_SLACK_ROWS = 128;   // rows of slack after each bf16 store b
 
 __device__ __forceinline__ float bf16_bits_to_f(uint16_t h) { return __uint_as_float(((uint32_t)h) << 16); }
 
+// Redundancy (AMB-30), one full warp: c = cos(k_new, k_prev) of layer `layer`, unit (b, g), with
+// k_prev the unit's previous key (lastk, zero before the first row); R_part[unit][pos] += c
+// (layers append in ascending order, so the fp32 sum runs over l ascending); then k_new
+// becomes the previous key.  krow: the new key's bf16 row (global memory).
+__device__ __forceinline__ void redund_append(const DevView& v, int layer, int unit, int pos, const uint16_t* krow) {
+  const int lane = threadIdx.x & 31;
+  uint16_t* prev = v.lastk + ((size_t)layer * v.B * v.Hkv + unit) * v.D;
+  float dot = 0.f, na = 0.f, nb = 0.f;
+  for (int e = lane; e < v.D; e += 32) {
+    const float a = bf16_bits_to_f(krow[e]), p = bf16_bits_to_f(prev[e]);
+    dot = fmaf(a, p, dot);
+    na = fmaf(a, a, na);
+    nb = fmaf(p, p, nb);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    dot += __shfl_xor_sync(0xffffffffu, dot, off);
+    na += __shfl_xor_sync(0xffffffffu, na, off);
+    nb += __shfl_xor_sync(0xffffffffu, nb, off);
+  }
+  __syncwarp();
+  for (int e = lane; e < v.D; e += 32) prev[e] = krow[e];
+  if (lane == 0) {
+    const float c = (na > 0.f && nb > 0.f) ? __fdiv_rn(dot, __fsqrt_rn(__fmul_rn(na, nb))) : 0.f;
+    float* r = v.red + (size_t)unit * v.Nmax + pos;
+    *r = __fadd_rn(*r, c);
+  }
+}
+
 // fp32 -> bf16 round-to-nearest-even on the bit pattern (finite inputs)
 __device__ __forceinline__ uint16_t f_to_bf16_bits(float x) {
   uint32_t u = __float_as_uint(x);
@@ -192,6 +230,7 @@ cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const
                                void* o, int zpar, int pdl, cudaStream_t s, float* lse = nullptr);
 cudaError_t launch_set_ml(const DevView& v, int zslot, const float* lse, cudaStream_t s);
 cudaError_t launch_vnorm_prefix(const DevView& v, int layer, const void* vv, int n0, cudaStream_t s);
+cudaError_t launch_redund_prefix(const DevView& v, int layer, const void* k, int n0, cudaStream_t s);
 cudaError_t launch_lse_combine(const float* op, const float* lp, int world, int rows, int d, float* oo, float* lo,
                                cudaStream_t s);
 cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_t s);

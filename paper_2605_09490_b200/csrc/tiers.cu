@@ -55,7 +55,9 @@ __global__ void k_append(const DevView v, const int layer, const uint16_t* __res
     K[dst + swz_off(row, e)] = k[(size_t)unit * v.D + e];
     V[dst + swz_off(row, e)] = vv[(size_t)unit * v.D + e];
   }
-  if (v.scorer == 1 && threadIdx.x < 32) {   // VATP: V-row norm of the appended token
+  if (v.red && threadIdx.x >= 32 && threadIdx.x < 64)   // redundancy: cos with the previous key
+    redund_append(v, layer, unit, v.st->n - 1, k + (size_t)unit * v.D);
+  if (scorer_uses_vnorm(v.scorer) && threadIdx.x < 32) {   // VATP: V-row norm of the appended token
     float ss = 0.f;
     for (int e = threadIdx.x; e < v.D; e += 32) {
       const float x = bf16_bits_to_f(vv[(size_t)unit * v.D + e]);
@@ -82,6 +84,43 @@ __global__ void k_vnorm_prefix(const DevView v, const int layer, const uint16_t*
     for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
     if (lane == 0) v.vnorm[((size_t)layer * v.B * v.Hkv + unit) * v.Nmax + p] = sqrtf(ss);
   }
+}
+
+// Redundancy (AMB-30): c_p = cos(k_p, k_{p-1}) of every prefix row of one layer added to R_part
+// (one warp per row, c_0 = 0), and the last prefix key becomes the unit's previous key.
+__global__ void k_redund_prefix(const DevView v, const int layer, const uint16_t* __restrict__ k, const int n0) {
+  const int unit = blockIdx.y, lane = threadIdx.x & 31;
+  for (int p = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); p < n0; p += gridDim.x * (blockDim.x / 32)) {
+    const uint16_t* row = k + ((size_t)unit * n0 + p) * v.D;
+    float dot = 0.f, na = 0.f, nb = 0.f;
+    if (p > 0) {
+      for (int e = lane; e < v.D; e += 32) {
+        const float a = bf16_bits_to_f(row[e]), q = bf16_bits_to_f(row[e - v.D]);
+        dot = fmaf(a, q, dot);
+        na = fmaf(a, a, na);
+        nb = fmaf(q, q, nb);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        dot += __shfl_xor_sync(0xffffffffu, dot, off);
+        na += __shfl_xor_sync(0xffffffffu, na, off);
+        nb += __shfl_xor_sync(0xffffffffu, nb, off);
+      }
+    }
+    if (lane == 0) {
+      const float c = (na > 0.f && nb > 0.f) ? __fdiv_rn(dot, __fsqrt_rn(__fmul_rn(na, nb))) : 0.f;
+      float* r = v.red + (size_t)unit * v.Nmax + p;
+      *r = __fadd_rn(*r, c);
+    }
+    if (p == n0 - 1)
+      for (int e = lane; e < v.D; e += 32) v.lastk[((size_t)layer * v.B * v.Hkv + unit) * v.D + e] = row[e];
+  }
+}
+
+cudaError_t launch_redund_prefix(const DevView& v, int layer, const void* k, int n0, cudaStream_t s) {
+  dim3 grid((unsigned)std::max(1, std::min(1024, (n0 + 7) / 8)), v.B * v.Hkv);
+  k_redund_prefix<<<grid, 256, 0, s>>>(v, layer, reinterpret_cast<const uint16_t*>(k), n0);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_vnorm_prefix(const DevView& v, int layer, const void* vv, int n0, cudaStream_t s) {
@@ -174,6 +213,12 @@ __global__ void k_score_update(const DevView v, const int layer, const float* __
 // ranks, found by an 8-pass MSB radix select (histograms in shared memory).
 constexpr int CLS_THREADS = 1024;
 
+// order-preserving fp32 -> uint32 (negatives below positives; raw bits order on S >= 0, AMB-7/31)
+__device__ __forceinline__ unsigned ord_bits(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
 // Sx: per-kv-head partial scores [parts][B][H_kv][N_max] -- the ctx's own S_part (parts = 1)
 // or the all-gathered S_part of `parts` KV-head shards (global kv head = part * H_kv + g).
 __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const float* __restrict__ Sx, const int parts) {
@@ -185,6 +230,7 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
   const int prot_hi = n - v.kw;            // window [n-k_w, n)
 
   __shared__ int s_cnt[2];
+  __shared__ unsigned int s_smax;
   __shared__ unsigned int hist[3][256];
   __shared__ unsigned long long s_prefix[3];
   __shared__ long long s_rank[3];
@@ -194,9 +240,11 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
   __shared__ int s_base[4];
 
   if (tid < 2) s_cnt[tid] = 0;
+  if (tid == 0) s_smax = 0u;
   __syncthreads();
   // S_i = fp32 sum over kv heads in ascending order (AMB-1/14)
   int c_live = 0, c_t3 = 0;
+  unsigned smax = 0u;                      // max S over the live set (bits; S >= 0)
   bool bad = false;
   for (int pos = tid; pos < n; pos += CLS_THREADS) {
     float s = Sx[((size_t)b * v.Hkv) * v.Nmax + pos];
@@ -207,7 +255,10 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
     fS[pos] = s;
     bad |= !(s >= 0.f) || isinf(s);
     if (told[pos] == T3) ++c_t3;
-    else if (pos >= prot_lo && pos < prot_hi) ++c_live;
+    else if (pos >= prot_lo && pos < prot_hi) {
+      ++c_live;
+      smax = max(smax, __float_as_uint(s));
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -218,8 +269,22 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
     atomicAdd(&s_cnt[0], c_live);
     atomicAdd(&s_cnt[1], c_t3);
   }
+  if (v.red) atomicMax(&s_smax, smax);
   if (bad) atomicOr(&v.st->err, 1);
   __syncthreads();
+  if (v.red) {
+    // redundancy / combined (AMB-31): rank by I - rho, I = S / S_max, rho = mean_{l,g} cos
+    const float fmax = __uint_as_float(s_smax);
+    const float lh = (float)(v.L * v.Hkv);
+    for (int pos = tid; pos < n; pos += CLS_THREADS) {
+      const float* r = v.red + (size_t)b * v.Hkv * v.Nmax + pos;
+      float rs = r[0];
+      for (int g = 1; g < v.Hkv; ++g) rs = __fadd_rn(rs, r[(size_t)g * v.Nmax]);
+      const float I = fmax > 0.f ? __fdiv_rn(fS[pos], fmax) : 0.f;
+      fS[pos] = __fsub_rn(I, __fdiv_rn(rs, lh));
+    }
+    __syncthreads();
+  }
   if (tid == 0) {
     // Alg. 1 floor arithmetic in integer basis points (AMB-8/9/11), or the
     // pure-eviction baselines' counts (tier policy)
@@ -243,7 +308,7 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
     for (int pos = tid; pos < n; pos += CLS_THREADS) {
       if (told[pos] == T3 || pos < prot_lo || pos >= prot_hi) continue;
       const unsigned long long key = ((unsigned long long)(v.policy == 3 ? random_key32(v.policy_seed, b, pos)
-                                                                          : __float_as_uint(fS[pos])) << 32) | (unsigned)pos;
+                                                                          : ord_bits(fS[pos])) << 32) | (unsigned)pos;
       const unsigned dig = (unsigned)(key >> shift) & 255u;
 #pragma unroll
       for (int k = 0; k < 3; ++k)
@@ -296,7 +361,7 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
       else if (pos < prot_lo || pos >= prot_hi) t = T0;
       else {
         const unsigned long long key = ((unsigned long long)(v.policy == 3 ? random_key32(v.policy_seed, b, pos)
-                                                                            : __float_as_uint(fS[pos])) << 32) | (unsigned)pos;
+                                                                            : ord_bits(fS[pos])) << 32) | (unsigned)pos;
         t = key < thr_e ? T3 : key < thr_2 ? T2 : key < thr_1 ? T1 : T0;
       }
       tnew[pos] = (uint8_t)t;

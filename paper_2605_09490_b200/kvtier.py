@@ -20,9 +20,10 @@ STATUS = {0: "OK", -1: "E_INVAL", -2: "E_CUDA", -3: "E_NCCL", -4: "E_STATE", -5:
 EVICT_TOTAL, EVICT_PER_EVENT = 0, 1
 SHARD_REQUEST, SHARD_KVHEAD, SHARD_SEQUENCE = 0, 1, 2
 POLICY_HIERARCHY, POLICY_STREAMING, POLICY_H2O, POLICY_RANDOM = 0, 1, 2, 3
-SCORER_ATTENTION, SCORER_VATP = 0, 1
+SCORER_ATTENTION, SCORER_VATP, SCORER_REDUNDANCY, SCORER_COMBINED = 0, 1, 2, 3
 STAGING_ALL = 0xFFFFFFFF
-X_SCORES, X_TIERS, X_IDX_T0, X_IDX_T1, X_IDX_T2, X_T0_ROWS, X_T1_ROWS, X_STAGING, X_T2_CODES, X_T2_SCALES = range(10)
+(X_SCORES, X_TIERS, X_IDX_T0, X_IDX_T1, X_IDX_T2, X_T0_ROWS, X_T1_ROWS, X_STAGING, X_T2_CODES, X_T2_SCALES,
+ X_REDUNDANCY) = range(11)
 
 
 class KvTierError(RuntimeError):
@@ -274,7 +275,7 @@ class KvTier:
         buf = np.zeros(nbytes.value, dtype=np.uint8)
         _check(load().kv_tier_export(self.ctx, what, layer, buf.ctypes.data_as(C.c_void_p), nbytes.value), self.ctx)
         B, H, D = self.cfg.num_requests, self.cfg.num_kv_heads, self.cfg.head_dim
-        if what == X_SCORES:
+        if what in (X_SCORES, X_REDUNDANCY):
             return buf.view(np.float32).reshape(B, H, -1)
         if what == X_TIERS:
             return buf.reshape(B, -1)

@@ -116,3 +116,23 @@ def test_policy_and_scorer_validation(field, value):
     cfg = kt.make_config(2, 1, 4, 2, 64, 300, 16, **kw)
     s = kt.Sizes()
     assert kt.load().kv_tier_query_sizes(C.byref(cfg), C.byref(s)) == -1
+
+
+def test_redundancy_scorers_refused_under_sequence_sharding():
+    # neighbour cosine needs position i-1, which another sequence shard owns (AMB-31)
+    for sc, want in ((kt.SCORER_REDUNDANCY, -1), (kt.SCORER_COMBINED, -1), (kt.SCORER_VATP, 0)):
+        cfg = kt.make_config(2, 1, 4, 2, 64, 300, 16, scorer=sc, shard=kt.SHARD_SEQUENCE, world=2, rank=0)
+        s = kt.Sizes()
+        assert kt.load().kv_tier_query_sizes(C.byref(cfg), C.byref(s)) == want
+
+
+def test_redundancy_scorers_size_their_buffers():
+    # R_part [B][H_kv][N] fp32 + the previous key [L][B][H_kv][d] bf16 on top of the attention arena
+    sz = {}
+    for sc in (kt.SCORER_ATTENTION, kt.SCORER_REDUNDANCY):
+        cfg = kt.make_config(2, 3, 4, 2, 64, 300, 16, scorer=sc)
+        s = kt.Sizes()
+        assert kt.load().kv_tier_query_sizes(C.byref(cfg), C.byref(s)) == 0
+        sz[sc] = s.device_arena
+    extra = sz[kt.SCORER_REDUNDANCY] - sz[kt.SCORER_ATTENTION]
+    assert 2 * 2 * 300 * 4 + 3 * 2 * 2 * 64 * 2 <= extra <= 2 * 2 * 300 * 4 + 3 * 2 * 2 * 64 * 2 + 2 * 256

@@ -89,6 +89,10 @@ def _run_pair(w, reqs=None, graph=False, check_every=1, layers_api=False, split=
             S_gpu = run.kv.export(kt.X_SCORES)
             ok, mrel = s_close(S_gpu[reqs_gpu], orc.st.S_part[:, :, :orc.st.n])
             assert ok, f"scores mismatch at step {t}: max rel {mrel}"
+            if orc.st.R_part is not None:          # redundancy partials (AMB-30): fp32 cosines
+                R_gpu = run.kv.export(kt.X_REDUNDANCY)[reqs_gpu]
+                err = np.abs(R_gpu - orc.st.R_part[:, :, :orc.st.n]).max()
+                assert err <= 2e-6 * w["L"], f"redundancy mismatch at step {t}: {err}"
             if run.is_event(t):
                 _check_event_state(run, orc, reqs_gpu)
     run.close()
@@ -556,6 +560,23 @@ def test_vatp_scorer_parity(api):
     _run_pair(w, graph=api == "graph", layers_api=api == "layers", check_every=4)
 
 
+@pytest.mark.parametrize("scorer", ["redundancy", "combined"])
+@pytest.mark.parametrize("api", ["graph", "layers"])
+def test_redundancy_scorer_parity(scorer, api):
+    # "attn - redundancy" / "attn x val - redundancy": R_part from the loaded and
+    # appended keys, signed classify keys I - rho (AMB-30/31); T2 on so keys leave / re-enter HBM
+    sc = kt.SCORER_REDUNDANCY if scorer == "redundancy" else kt.SCORER_COMBINED
+    w = H.workload("tiny", B=3, L=3, Hq=8, Hkv=2, d=128, N=600, P=32, interval=8, steps=26,
+                   hbm_bp=4000, evict_bp=1200, t2_bp=3000, scorer=sc)
+    _run_pair(w, graph=api == "graph", layers_api=api == "layers", check_every=4)
+
+
+def test_redundancy_scorer_sampled_7b_requests():
+    # the 7B-shaped config (d = 128, 28 layers) with the combined scorer, requests 0 and 5
+    w = H.workload("7b", steps=10, interval=4, scorer=kt.SCORER_COMBINED)
+    _run_pair(w, reqs=[0, 5], check_every=3)
+
+
 def test_lse_combine_kernel_matches_full_softmax():
     # kv_tier_lse_combine: shards of a softmax-weighted sum, combined in rank order, equal the
     # float64 softmax over the concatenation; an empty shard (m = -inf, l = 0) contributes nothing
@@ -607,7 +628,8 @@ def test_randomized_configs(seed):
                    evict_mode=int(rng.choice([kt.EVICT_TOTAL, kt.EVICT_PER_EVENT])),
                    staging=int(rng.choice([kt.STAGING_ALL, kt.STAGING_ALL, 0])),
                    policy=pol, budget=int(rng.integers(P + 140, N + 50)) if pol in (2, 3) else 0,
-                   policy_seed=seed, scorer=int(rng.choice([0, 0, kt.SCORER_VATP])))
+                   policy_seed=seed, scorer=int(rng.choice([0, 0, kt.SCORER_VATP, kt.SCORER_REDUNDANCY,
+                                                             kt.SCORER_COMBINED])))
     _run_pair(w, graph=bool(rng.integers(0, 2)), check_every=3)
 
 
