@@ -226,6 +226,32 @@ KV_TIER_API kv_tier_status kv_tier_lse_combine(const float* o_parts, const float
  * valid until the update has run on `stream`. */
 KV_TIER_API kv_tier_status kv_tier_score_update_lse(kv_tier_ctx* ctx, const float* lse_global, void* stream);
 
+/* ---- N1: host-side T1 partial attention (ScoutAttention-style prior art P:120,
+ * P:215; strict DDR residency of T1).  With host-T1 mode on, kv_tier_decode_attention_lse
+ * attends T0 ∪ T2 ∪ {new token} only (T1 skipped; no kv_tier_prefetch needed in stream mode)
+ * and the host cores attend T1 in the pinned host store, so per layer only q goes down and
+ * (o, m, l) plus the T1 score increments come up, instead of |T1| rows.  One layer:
+ *   decode_attention_lse(o_gpu, lse_gpu) ; host_t1_attention(q_host -> o_host, lse_host) ;
+ *   lse_combine([o_gpu, o_host], [lse_gpu, lse_host]) -> o, lse ;
+ *   score_update_lse(lse) ; host_t1_score_update(lse copied to the host).
+ * Attention scorer, request / KV-head sharding, split kernel with the merge kernel only;
+ * kv_tier_decode_attention, kv_tier_step and graph capture return E_STATE in this mode. */
+KV_TIER_API kv_tier_status kv_tier_set_host_t1(kv_tier_ctx* ctx, int32_t on);   /* outside a step */
+/* Host T1 partial of `layer` in the open step.  q_host: bf16 [B][H_q][d] host memory (the step's
+ * query); writes o_part fp32 [B][H_q][d] = sum_j 2^(z_j - m) v_j / l and lse_part fp32 [B][H_q][2]
+ * = (m, l) over the request's T1 tokens j, z_j = fp32(q·k_j)·log2(e)/sqrt(d) (the decode kernel's
+ * encoding; m = -inf, l = 0, o = 0 when |T1| = 0).  OpenMP over (b, h); the first call after a
+ * migrate synchronises the device once to read the new T1 lists.  Keeps z for the score update. */
+KV_TIER_API kv_tier_status kv_tier_host_t1_attention(kv_tier_ctx* ctx, int32_t layer, const void* q_host,
+                                                     float* o_part, float* lse_part);
+/* Eq. 1 for the T1 tokens of the layer last passed to kv_tier_host_t1_attention (E_STATE
+ * otherwise): lse_global_host fp32 [B][H_q][2] host copy of the combined (M, L);
+ * S_part[b][g][i] += fp32(sum_{h in g} 2^(z_hi - M_h) / L_h), formed on the host and scattered
+ * by a kernel on `stream` from double-buffered mapped pinned memory (the call waits for the
+ * scatter two layers back before reusing its buffer). */
+KV_TIER_API kv_tier_status kv_tier_host_t1_score_update(kv_tier_ctx* ctx, int32_t layer, const float* lse_global_host,
+                                                        void* stream);
+
 /* a4 standalone (external probabilities, e.g. from another attention kernel):
  * probs: device fp32 [B][H_q][n_vis] over the visible tokens in ascending position
  * order; S_part[b][g][i] += fp32(sum_{h in g} probs[b][h][j(i)]).  n_vis is

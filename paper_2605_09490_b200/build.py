@@ -11,7 +11,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "lib")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-Xcompiler", "-fvisibility=hidden"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-Xcompiler", "-fvisibility=hidden",
+         "-Xcompiler", "-fopenmp", "-lgomp"]     # OpenMP: host-T1 attention (N1) on the host cores
 if os.environ.get("KVT_TRACE_LOOP"):        # debug: per-stage wait/busy accounting in the trace
     FLAGS += ["-DKVT_TRACE_LOOP=1"]
 if os.environ.get("KVT_FLAT_TRACE"):        # debug: per-unit epilogue timing in the flat kernel's trace

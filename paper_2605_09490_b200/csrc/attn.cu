@@ -182,7 +182,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   // ---------------------------------------------------------------- prologue (pre-PDL-wait)
   const int cur = v.st->cur;
   Seg sg;
-  sg.init(v.cnt[cur] + b * CNT_STRIDE, v.st->nn);
+  sg.init(v.cnt[cur] + b * CNT_STRIDE, v.st->nn, v.host_t1);
   // This CTA's work: stages of up to NW 16-row groups (one per consumer warp) from the unit's
   // groups [bf16 segment [0, a2) | int8 segment [a2, a2 + n2)].  Default (KVTIER_RR=2): the
   // groups themselves are dealt round-robin over the unit's C CTAs (bf16 then int8, continuing
@@ -941,7 +941,7 @@ size_t merge_smem_bytes(const DevView& v) { (void)v; return 0; }
 __global__ void __launch_bounds__(256) k_score_flush(const DevView v, const int zfirst, const int nz) {
   const int cur = v.st->cur;
   Seg sg;
-  sg.init(v.cnt[cur], v.st->nn);   // counts are uniform across requests
+  sg.init(v.cnt[cur], v.st->nn, v.host_t1);   // counts are uniform across requests
   const long long tot = (long long)v.B * v.Hkv * sg.nvirt;
   bool bad = false;
   score_range(v, sg, cur, zfirst, nz, 0, tot, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, bad);
@@ -954,7 +954,7 @@ __global__ void __launch_bounds__(256) k_score_flush(const DevView v, const int 
 __global__ void __launch_bounds__(128, 16) k_score_flush_lean(const DevView v, const int zfirst, const int nz) {
   const int cur = v.st->cur;
   Seg sg;
-  sg.init(v.cnt[cur], v.st->nn);
+  sg.init(v.cnt[cur], v.st->nn, v.host_t1);
   const long long tot = (long long)v.B * v.Hkv * sg.nvirt;
   const size_t zslot = (size_t)v.B * v.Hkv * v.zrows * 8, mslot = (size_t)v.B * v.Hkv * 16;
   bool bad = false;
@@ -991,7 +991,7 @@ __global__ void __launch_bounds__(256) k_score_flush_req(const DevView v, const 
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
     const int u = (int)(i / v.zrows), t = (int)(i - (long long)u * v.zrows), b = u / v.Hkv;
     Seg sg;
-    sg.init(v.cnt[cur] + b * CNT_STRIDE, nn);
+    sg.init(v.cnt[cur] + b * CNT_STRIDE, nn, v.host_t1);
     if (t >= sg.nvirt || !sg.valid(t)) continue;
     const int pos = sg.pos(v, cur, b, t);
     float s = v.S[(size_t)u * v.Nmax + pos];

@@ -4,6 +4,7 @@
 #include "kv_internal.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -45,6 +46,14 @@ struct kv_tier_ctx {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   unsigned long long* trace = nullptr;     // debug timeline buffer (KVTIER_TRACE=1)
+  // N1 host-T1 mode (kv_tier_set_host_t1)
+  int mig_epoch = 0, h1_epoch = -1;        // migrates issued / epoch of the host copy of the T1 lists
+  std::vector<int> h1_idx, h1_cnt;         // [B][cap1] T1 positions (store order), [B] |T1|
+  std::vector<float> h1_z;                 // [B][H_q][cap1] logits of the last host_t1_attention
+  int h1_layer = -1;                       // layer whose logits h1_z holds (-1: none pending)
+  float* h1_inc[2] = {nullptr, nullptr};   // pinned mapped score increments, double-buffered
+  cudaEvent_t ev_inc[2] = {nullptr, nullptr};
+  bool inc_used[2] = {false, false};
   std::string err;
 };
 
@@ -488,6 +497,10 @@ kv_tier_status kv_tier_destroy(kv_tier_ctx* ctx) {
   }
   if (ctx->ev_score_tail) cudaEventDestroy(ctx->ev_score_tail);
   if (ctx->score_stream) cudaStreamDestroy(ctx->score_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->h1_inc[i]) cudaFreeHost(ctx->h1_inc[i]);
+    if (ctx->ev_inc[i]) cudaEventDestroy(ctx->ev_inc[i]);
+  }
   delete ctx;
   return KV_TIER_OK;
 }
@@ -611,7 +624,9 @@ static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, con
   if (!ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "decode_attention outside begin_step/end_step");
   if (!k_new && ctx->appended_step[layer] != ctx->t)
     return fail(ctx, KV_TIER_E_STATE, "layer %d: no new-token row (pass k_new/v_new or call kv_tier_append)", layer);
-  if (ctx->v.stream_mode && ctx->prefetched_step[layer] != ctx->t)
+  if (ctx->v.host_t1 && !lse)
+    return fail(ctx, KV_TIER_E_STATE, "host-T1 mode: the GPU result is partial, use kv_tier_decode_attention_lse");
+  if (ctx->v.stream_mode && !ctx->v.host_t1 && ctx->prefetched_step[layer] != ctx->t)
     return fail(ctx, KV_TIER_E_STATE, "stream mode: kv_tier_prefetch(layer %d) must precede decode_attention in every step", layer);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
@@ -815,6 +830,7 @@ kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side) 
   if (!ctx->classified) return fail(ctx, KV_TIER_E_STATE, "migrate without a preceding classify");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(main_stream);
   cudaStream_t sd = reinterpret_cast<cudaStream_t>(side);
+  ctx->mig_epoch += 1;                       // host-T1 mode re-reads the T1 lists
   // plan the new row layout; move only the rows that change (or rebuild when too many move)
   cudaError_t e = launch_plan(ctx->v, s);
   if (e == cudaSuccess) e = launch_moves(ctx->v, ctx->cur, s);
@@ -1149,6 +1165,131 @@ kv_tier_status kv_tier_debug_trace(kv_tier_ctx* ctx, uint64_t* host_dst, size_t 
   cudaError_t e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaMemcpy(host_dst, ctx->trace, need * 8, cudaMemcpyDeviceToHost);
   return cuda_check(ctx, e, "trace");
+}
+
+// ------------------------------------------------------------------ N1: host-side T1 attention
+// SURVEY §8f N1 (ScoutAttention-style): T1 is attended where it lives.  Per layer
+// q goes down and (o, m, l) plus the T1 score increments come up -- O(B·H_q·d + B·H_kv·|T1|)
+// floats instead of |T1| rows.  The host loops are the same softmax as the decode kernel's
+// (log2 domain, fp32), split by tier and recombined by kv_tier_lse_combine (Eq. 3).
+kv_tier_status kv_tier_set_host_t1(kv_tier_ctx* ctx, int32_t on) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "set_host_t1 inside a step");
+  if (on && ctx->v.scorer != KV_TIER_SCORER_ATTENTION) return fail(ctx, KV_TIER_E_STATE, "host-T1 mode supports the attention scorer");
+  if (on && ctx->v.seq_w > 1) return fail(ctx, KV_TIER_E_STATE, "host-T1 mode: not with sequence sharding");
+  if (on && ctx->v.flat) return fail(ctx, KV_TIER_E_STATE, "host-T1 mode runs the split kernel (KVTIER_FLAT=0)");
+  if (on && (ctx->v.cluster_merge || ctx->v.last_merge))
+    return fail(ctx, KV_TIER_E_STATE, "host-T1 mode needs the merge kernel (KVTIER_CLUSTER=0, KVTIER_LASTMERGE=0)");
+  if (on && !ctx->host_t1 && ctx->v.cap1 > 0) return fail(ctx, KV_TIER_E_STATE, "no host T1 store");
+  const size_t ninc = (size_t)ctx->v.B * ctx->v.Hkv * std::max(ctx->v.cap1, 1);
+  for (int i = 0; on && i < 2; ++i) {
+    if (!ctx->h1_inc[i]) {
+      cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&ctx->h1_inc[i]), ninc * 4, cudaHostAllocMapped | cudaHostAllocPortable);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_inc[i], cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_check(ctx, e, "set_host_t1 (staging)");
+    }
+  }
+  ctx->v.host_t1 = on ? 1 : 0;
+  ctx->h1_epoch = -1;
+  ctx->h1_layer = -1;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_host_t1_attention(kv_tier_ctx* ctx, int32_t layer, const void* q_host, float* o_part,
+                                         float* lse_part) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!ctx->v.host_t1) return fail(ctx, KV_TIER_E_STATE, "host-T1 mode is off (kv_tier_set_host_t1)");
+  if (!ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "host_t1_attention outside begin_step/end_step");
+  if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
+  if (!q_host || !o_part || !lse_part) return fail(ctx, KV_TIER_E_INVAL, "null q/o/lse");
+  const DevView& v = ctx->v;
+  const int B = v.B, Hq = v.Hq, Hkv = v.Hkv, G = v.G, D = v.D, cap1 = std::max(v.cap1, 1);
+  if (ctx->h1_epoch != ctx->mig_epoch) {     // first call after a migrate: read the T1 lists
+    std::vector<int> cn((size_t)B * CNT_STRIDE);
+    ctx->h1_idx.assign((size_t)B * cap1, 0);
+    ctx->h1_cnt.assign(B, 0);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(cn.data(), v.cnt[ctx->cur], cn.size() * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && v.cap1 > 0)
+      e = cudaMemcpy(ctx->h1_idx.data(), v.idx[ctx->cur][1], (size_t)B * v.cap1 * 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_check(ctx, e, "host_t1_attention (T1 lists)");
+    for (int b = 0; b < B; ++b) ctx->h1_cnt[b] = cn[(size_t)b * CNT_STRIDE + 1];
+    ctx->h1_z.assign((size_t)B * Hq * cap1, 0.f);
+    ctx->h1_epoch = ctx->mig_epoch;
+  }
+  const size_t rows = (size_t)v.L * B * Hkv * v.hN;
+  const uint16_t* hk = reinterpret_cast<const uint16_t*>(ctx->host_t1);
+  const uint16_t* hv = hk ? hk + rows * D : nullptr;
+  const uint16_t* q = reinterpret_cast<const uint16_t*>(q_host);
+  const float sl2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+  auto bf = [](uint16_t h) { uint32_t u = (uint32_t)h << 16; float f; memcpy(&f, &u, 4); return f; };
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int bh = 0; bh < B * Hq; ++bh) {
+    const int b = bh / Hq, h = bh % Hq, g = h / G;
+    const int n1 = ctx->h1_cnt[b];
+    const size_t grp = ((size_t)layer * B + b) * Hkv + g;
+    float qf[128], acc[128];
+    for (int e = 0; e < D; ++e) { qf[e] = bf(q[(size_t)bh * D + e]); acc[e] = 0.f; }
+    float* z = ctx->h1_z.data() + (size_t)bh * cap1;
+    float m = -INFINITY;
+    for (int j = 0; j < n1; ++j) {
+      const uint16_t* kr = hk + host_row(v, grp, ctx->h1_idx[(size_t)b * cap1 + j]) * D;
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int e = 0; e < D; e += 4)
+        for (int u = 0; u < 4; ++u) s4[u] += qf[e + u] * bf(kr[e + u]);
+      z[j] = ((s4[0] + s4[1]) + (s4[2] + s4[3])) * sl2;
+      m = std::max(m, z[j]);
+    }
+    float l = 0.f;
+    for (int j = 0; j < n1; ++j) {
+      const float p = exp2f(z[j] - m);
+      l += p;
+      const uint16_t* vr = hv + host_row(v, grp, ctx->h1_idx[(size_t)b * cap1 + j]) * D;
+      for (int e = 0; e < D; ++e) acc[e] += p * bf(vr[e]);
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    for (int e = 0; e < D; ++e) o_part[(size_t)bh * D + e] = acc[e] * inv;
+    lse_part[(size_t)bh * 2] = m;
+    lse_part[(size_t)bh * 2 + 1] = l;
+  }
+  ctx->h1_layer = layer;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_host_t1_score_update(kv_tier_ctx* ctx, int32_t layer, const float* lse_global_host,
+                                            void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!lse_global_host) return fail(ctx, KV_TIER_E_INVAL, "null lse_global");
+  if (!ctx->v.host_t1 || ctx->h1_layer != layer)
+    return fail(ctx, KV_TIER_E_STATE, "host_t1_score_update(layer %d) must follow host_t1_attention of that layer", layer);
+  const DevView& v = ctx->v;
+  const int B = v.B, Hq = v.Hq, Hkv = v.Hkv, G = v.G, cap1 = std::max(v.cap1, 1);
+  const int buf = layer & 1;
+  cudaError_t e = cudaSuccess;
+  if (ctx->inc_used[buf]) e = cudaEventSynchronize(ctx->ev_inc[buf]);   // its previous scatter is done
+  if (e != cudaSuccess) return cuda_check(ctx, e, "host_t1_score_update (staging)");
+  float* inc = ctx->h1_inc[buf];
+#pragma omp parallel for schedule(static)
+  for (int bg = 0; bg < B * Hkv; ++bg) {
+    const int b = bg / Hkv, g = bg % Hkv;
+    const int n1 = ctx->h1_cnt[b];
+    for (int j = 0; j < n1; ++j) {
+      float s = 0.f;                   // Eq. 1: sum over the group's q heads of 2^(z - M) / L
+      for (int h = g * G; h < (g + 1) * G; ++h) {
+        const float M = lse_global_host[((size_t)b * Hq + h) * 2], L = lse_global_host[((size_t)b * Hq + h) * 2 + 1];
+        s += exp2f(ctx->h1_z[((size_t)b * Hq + h) * cap1 + j] - M) * (L > 0.f ? 1.f / L : 0.f);
+      }
+      inc[(size_t)bg * cap1 + j] = s;
+    }
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  float* dinc = nullptr;
+  e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dinc), inc, 0);
+  if (e == cudaSuccess) e = launch_t1_score_add(v, dinc, s);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_inc[buf], s);
+  if (e == cudaSuccess) ctx->inc_used[buf] = true;
+  ctx->h1_layer = -1;
+  return cuda_check(ctx, e, "host_t1_score_update");
 }
 
 kv_tier_status kv_tier_import_scores(kv_tier_ctx* ctx, const float* host_S, size_t bytes) {

@@ -134,10 +134,11 @@ __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w &
 struct Seg {
   int n0o, n1, n2, a1, a2, a3, nvirt, nn;
   // nn: the step's new token is the last T0 row of this ctx (DevState::nn)
-  __device__ __forceinline__ void init(const int* cn, int nn_ = 1) {
+  // skip1: host-T1 mode: the host cores attend T1, the GPU skips it
+  __device__ __forceinline__ void init(const int* cn, int nn_ = 1, int skip1 = 0) {
     nn = nn_;
     n0o = cn[0] - nn;
-    n1 = cn[1];
+    n1 = skip1 ? 0 : cn[1];
     n2 = cn[2];
     a1 = ru16(n0o);
     a2 = ru16(a1 + n1);

@@ -47,6 +47,7 @@ struct DevView {
   int zring;            // logit ring slots in use (2..ZRING): the ring stays inside the L2 carve-out
   unsigned policy_seed;
   int stream_mode;      // staging_tokens == 0
+  int host_t1;          // N1: T1 attended on the host (kv_tier_set_host_t1); kernels skip T1
   int out_fp32;
   int split;            // CTAs per (b, g) cluster
   int chunk_max;        // max tokens per CTA (logit buffer rows)
@@ -230,6 +231,7 @@ cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const
                                void* o, int zpar, int pdl, cudaStream_t s, float* lse = nullptr);
 cudaError_t launch_set_ml(const DevView& v, int zslot, const float* lse, cudaStream_t s);
 cudaError_t launch_vnorm_prefix(const DevView& v, int layer, const void* vv, int n0, cudaStream_t s);
+cudaError_t launch_t1_score_add(const DevView& v, const float* inc, cudaStream_t s);
 cudaError_t launch_redund_prefix(const DevView& v, int layer, const void* k, int n0, cudaStream_t s);
 cudaError_t launch_lse_combine(const float* op, const float* lp, int world, int rows, int d, float* oo, float* lo,
                                cudaStream_t s);

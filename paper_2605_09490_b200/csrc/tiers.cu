@@ -117,6 +117,26 @@ __global__ void k_redund_prefix(const DevView v, const int layer, const uint16_t
   }
 }
 
+// N1 host-T1 mode: S_part[b][g][idx1[b][j]] += inc[b][g][j] for the T1 tokens the host attended
+// (inc: [B][H_kv][cap1] fp32 in mapped pinned memory, store order of the T1 index list).
+__global__ void k_t1_score_add(const DevView v, const float* __restrict__ inc) {
+  const int unit = blockIdx.y, b = unit / v.Hkv;
+  const int cur = v.st->cur;
+  const int n1 = v.cnt[cur][b * CNT_STRIDE + 1];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n1; j += gridDim.x * blockDim.x) {
+    const float x = inc[(size_t)unit * v.cap1 + j];
+    float* S = v.S + (size_t)unit * v.Nmax + v.idx[cur][1][(size_t)b * v.cap1 + j];
+    *S = *S + x;
+    if (!isfinite(x)) atomicOr(&v.st->err, 1);
+  }
+}
+
+cudaError_t launch_t1_score_add(const DevView& v, const float* inc, cudaStream_t s) {
+  dim3 grid((unsigned)std::max(1, std::min(64, (v.cap1 + 255) / 256)), v.B * v.Hkv);
+  k_t1_score_add<<<grid, 256, 0, s>>>(v, inc);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_redund_prefix(const DevView& v, int layer, const void* k, int n0, cudaStream_t s) {
   dim3 grid((unsigned)std::max(1, std::min(1024, (n0 + 7) / 8)), v.B * v.Hkv);
   k_redund_prefix<<<grid, 256, 0, s>>>(v, layer, reinterpret_cast<const uint16_t*>(k), n0);

@@ -217,6 +217,77 @@ class KvHeadShardedDecode:
             r.close()
 
 
+class HostT1Decode:
+    """T1 attended on the host cores where it lives (kv_tier_set_host_t1).
+    Per layer: q goes down (D2H), the GPU attends T0 ∪ T2 ∪ {new} (decode_attention_lse) while
+    the host attends T1 (host_t1_attention, OpenMP), the two partials are combined on the GPU
+    (lse_combine, Eq. 3 split by tier), and the score update runs for the GPU's tokens
+    (score_update_lse) and for T1 on the host (host_t1_score_update) with the global (M, L)."""
+
+    def __init__(self, w, device="cuda:0", **kw):
+        self.w = w
+        self.run = TieredDecode(w, device=device, out_fp32=True, **kw)
+        self.run.kv.set_host_t1(True)
+        B, L, Hq, d = w["B"], w["L"], w["Hq"], w["d"]
+        dev = self.run.dev
+        self.parts_o = torch.empty((2, B, Hq, d), dtype=torch.float32, device=dev)
+        self.parts_l = torch.empty((2, B, Hq, 2), dtype=torch.float32, device=dev)
+        self.q_host = torch.empty((B, Hq, d), dtype=torch.bfloat16).pin_memory()
+        self.o_host = torch.empty((B, Hq, d), dtype=torch.float32).pin_memory()
+        self.l_host = torch.empty((B, Hq, 2), dtype=torch.float32).pin_memory()
+        self.lse_host = torch.empty((L, B, Hq, 2), dtype=torch.float32).pin_memory()
+        self.O = torch.empty((L, B, Hq, d), dtype=torch.float32, device=dev)
+        self.LSE = torch.empty((L, B, Hq, 2), dtype=torch.float32, device=dev)
+        self.t = 0
+
+    def is_event(self, t):
+        return t % self.w["interval"] == 0
+
+    def step(self, q=None):
+        """One decode step; q: optional [L][B][H_q][d] bf16 (default: the generated queries)."""
+        r, t = self.run, self.t
+        kv, s = r.kv, r.main
+        Q = r.Q[t] if q is None else q
+        with torch.cuda.stream(s):
+            kv.begin_step(stream=s)
+            for l in range(self.w["L"]):
+                self.q_host.copy_(Q[l], non_blocking=True)                  # q down
+                q_ready = torch.cuda.Event()
+                q_ready.record(s)
+                kv.decode_attention_lse(l, Q[l], self.parts_o[0], self.parts_l[0], 1, stream=s,
+                                        k_new=r.Kn[t, l], v_new=r.Vn[t, l])
+                q_ready.synchronize()
+                kv.host_t1_attention(l, self.q_host, self.o_host, self.l_host)   # overlaps the GPU partial
+                self.parts_o[1].copy_(self.o_host, non_blocking=True)            # (o, m, l) up
+                self.parts_l[1].copy_(self.l_host, non_blocking=True)
+                o, lse = kt.lse_combine(self.parts_o, self.parts_l)
+                self.O[l].copy_(o)
+                self.LSE[l].copy_(lse)
+                kv.score_update_lse(self.LSE[l], stream=s)
+                self.lse_host[l].copy_(self.LSE[l], non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(s)
+                done.synchronize()
+                kv.host_t1_score_update(l, self.lse_host[l], stream=s)
+            kv.end_step(stream=s)
+            if self.is_event(t):
+                kv.classify(stream=s)
+                kv.migrate(stream=s, side=r.side)
+        self.t += 1
+        r.t = self.t
+        return self.O
+
+    def output(self):
+        self.run.main.synchronize()
+        return self.O.cpu().numpy()
+
+    def sync(self):
+        self.run.sync()
+
+    def close(self):
+        self.run.close()
+
+
 class SeqShardedDecode:
     """Sequence sharding simulated in one process: `world` ctxs on one
     device, ctx r owning the 64-position blocks k with k % world == r.  Every layer: each ctx

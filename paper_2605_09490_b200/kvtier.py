@@ -67,6 +67,9 @@ _SIGS = {
     "kv_tier_decode_attention_lse": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_int32, C.c_void_p],
     "kv_tier_score_update_lse": [C.c_void_p, C.c_void_p, C.c_void_p],
+    "kv_tier_set_host_t1": [C.c_void_p, C.c_int32],
+    "kv_tier_host_t1_attention": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p],
+    "kv_tier_host_t1_score_update": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p],
     "kv_tier_lse_combine": [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                             C.c_void_p],
     "kv_tier_score_update": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p],
@@ -206,6 +209,26 @@ class KvTier:
     def score_update_lse(self, lse_global, stream=None):
         _check(load().kv_tier_score_update_lse(self.ctx, C.c_void_p(lse_global.data_ptr()), _stream_ptr(stream)),
                self.ctx)
+
+    # N1 host-T1 mode (kv_tier_set_host_t1): host tensors are CPU (ideally pinned) torch tensors
+    def set_host_t1(self, on=True):
+        _check(load().kv_tier_set_host_t1(self.ctx, 1 if on else 0), self.ctx)
+
+    def host_t1_attention(self, layer, q_host, o_part, lse_part):
+        """T1 partial of `layer` on the host cores: q_host bf16 [B][H_q][d] -> o_part fp32
+        [B][H_q][d], lse_part fp32 [B][H_q][2] (CPU tensors)."""
+        for x in (q_host, o_part, lse_part):
+            if x.is_cuda or not x.is_contiguous():
+                raise ValueError("host_t1_attention takes contiguous CPU tensors")
+        _check(load().kv_tier_host_t1_attention(self.ctx, layer, C.c_void_p(q_host.data_ptr()),
+                                                C.c_void_p(o_part.data_ptr()), C.c_void_p(lse_part.data_ptr())),
+               self.ctx)
+
+    def host_t1_score_update(self, layer, lse_global_host, stream=None):
+        if lse_global_host.is_cuda or not lse_global_host.is_contiguous():
+            raise ValueError("host_t1_score_update takes a contiguous CPU lse tensor")
+        _check(load().kv_tier_host_t1_score_update(self.ctx, layer, C.c_void_p(lse_global_host.data_ptr()),
+                                                   _stream_ptr(stream)), self.ctx)
 
     def score_update(self, layer, probs, stream=None):
         _check(load().kv_tier_score_update(self.ctx, layer, C.c_void_p(probs.data_ptr()), _stream_ptr(stream)),

@@ -577,6 +577,57 @@ def test_redundancy_scorer_sampled_7b_requests():
     _run_pair(w, reqs=[0, 5], check_every=3)
 
 
+# --------------------------------------------------------------------- N1: host-side T1 attention
+@pytest.mark.parametrize("staging,d", [(kt.STAGING_ALL, 128), (0, 128), (0, 64)])
+def test_host_t1_attention_matches_oracle(staging, d):
+    # T1 attended on the host cores, T0 ∪ T2 on the GPU, combined by LSE (Eq. 3):
+    # o, scores and every event's tiers / rows equal the oracle's full-attention run
+    w = H.workload("tiny", B=3, L=2, Hq=8, Hkv=2, d=d, N=600, P=32, interval=8, steps=26,
+                   hbm_bp=4000, evict_bp=800, t2_bp=3000, staging=staging)
+    h = H.HostT1Decode(w)
+    orc = OracleRun(w)
+    for t in range(w["steps"]):
+        h.step()
+        ok, mabs, _ = o_close(h.output()[:, orc.reqs], orc.step())
+        assert ok, (t, mabs)
+        if t % 4 == 0 or h.is_event(t):
+            h.sync()
+            ok, mrel = s_close(h.run.kv.export(kt.X_SCORES)[orc.reqs], orc.st.S_part[:, :, :orc.st.n])
+            assert ok, (t, mrel)
+            if h.is_event(t):
+                _check_event_state(h.run, orc, orc.reqs, layers=(0, 1))
+    h.close()
+
+
+def test_host_t1_sampled_7b_requests():
+    w = H.workload("7b", steps=6, interval=4, staging=0)
+    h = H.HostT1Decode(w)
+    orc = OracleRun(w, reqs=[0, 5])
+    for t in range(w["steps"]):
+        h.step()
+        ok, mabs, _ = o_close(h.output()[:, orc.reqs], orc.step())
+        assert ok, (t, mabs)
+    h.sync()
+    ok, mrel = s_close(h.run.kv.export(kt.X_SCORES)[orc.reqs], orc.st.S_part[:, :, :orc.st.n])
+    assert ok, mrel
+    h.close()
+
+
+def test_host_t1_mode_guards():
+    w = H.workload("tiny", steps=2)
+    run = H.TieredDecode(w)
+    run.kv.set_host_t1(True)
+    with torch.cuda.stream(run.main):
+        run.kv.begin_step(stream=run.main)
+        with pytest.raises(kt.KvTierError):      # the GPU result alone would miss T1
+            run.kv.decode_attention(0, run.Q[0, 0], run.O[0], 1, stream=run.main, k_new=run.Kn[0, 0], v_new=run.Vn[0, 0])
+    run.close()
+    r2 = H.TieredDecode(H.workload("tiny", steps=2, scorer=kt.SCORER_VATP))
+    with pytest.raises(kt.KvTierError):
+        r2.kv.set_host_t1(True)
+    r2.close()
+
+
 def test_lse_combine_kernel_matches_full_softmax():
     # kv_tier_lse_combine: shards of a softmax-weighted sum, combined in rank order, equal the
     # float64 softmax over the concatenation; an empty shard (m = -inf, l = 0) contributes nothing
