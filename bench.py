@@ -376,7 +376,7 @@ def main():
     # ---- control: same visible set, everything HBM-resident, no classify/migrate in window
     overhead = None
     control_ms = None
-    stream_leg = None
+    stream_leg = host_t1_leg = None
     if not args.no_extras:
         ctl = H.TieredDecode(dict(w, steps=W + K), device=dev, out_fp32=False, split=args.split, seed_offset=seed_off,
                              variant=args.variant)
@@ -425,6 +425,28 @@ def main():
         del sr
         torch.cuda.empty_cache()
 
+        # ---- N1: T1 attended on the host cores where it lives; per layer q goes
+        # down and (o, m, l) + T1 score increments come up instead of the T1 rows
+        Kh, Wh = 4, 1
+        hr = H.HostT1Decode(dict(w, staging=0, steps=Wh + Kh), device=dev, split=args.split,
+                            seed_offset=seed_off, variant=args.variant)
+        for _ in range(Wh):
+            hr.step()
+        hr.sync()
+        _barrier_sync()
+        el_h = _max_over_ranks(timed(hr.step, hr.run.main, Kh))
+        hq = w["Hq"]
+        link_b = L * B * (hq * d * 2 + hq * (d + 2) * 4 + hq * 2 * 4 + Hkv * cs[1] * 4)
+        host_t1_leg = {"steps_per_s": world * Kh / el_h, "ms_per_step": 1e3 * el_h / Kh,
+                       "link_bytes_per_step": int(link_b), "t1_row_bytes_avoided": int(t1_bytes),
+                       "vs_stream_mode": (Kh / el_h) / (Ks / el_s),
+                       "host_threads": os.cpu_count(),
+                       "note": "T1 never crosses the link; per layer the host loop (OpenMP over B*H_q) runs "
+                               "beside the GPU partial and two host round trips serialise the layer"}
+        hr.close()
+        del hr
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_extras:
         cpu = cpu_oracle_sample(w, args.cpu_seconds)
@@ -460,6 +482,7 @@ def main():
                          "peak_src": peaks["src"]},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
             "stream_mode": stream_leg,
+            "host_t1": host_t1_leg,
             "context": "paper: 5-7% transfer overhead on RTX 5080 PCIe Gen5, unpinned, 7B int8, batch 1 (P:642)",
         }
         print(json.dumps(out), flush=True)

@@ -57,6 +57,12 @@ struct kv_tier_ctx {
   std::string err;
 };
 
+static inline float __uint_as_float_host(uint32_t u) {
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -1172,6 +1178,57 @@ kv_tier_status kv_tier_debug_trace(kv_tier_ctx* ctx, uint64_t* host_dst, size_t 
 // q goes down and (o, m, l) plus the T1 score increments come up -- O(B·H_q·d + B·H_kv·|T1|)
 // floats instead of |T1| rows.  The host loops are the same softmax as the decode kernel's
 // (log2 domain, fp32), split by tier and recombined by kv_tier_lse_combine (Eq. 3).
+// One (request, kv head) of the host T1 partial: z[h][j] = fp32(q_h·k_j)·sl2 for the G heads of
+// the group (each K row converted once), m_h = max_j z, then p = 2^(z - m), l_h = sum p and
+// o_h = sum p v_j / l_h (each V row converted once).  omp simd lets the e-loops vectorise;
+// target_clones picks AVX-512 / AVX2 code at load time where the host has it.
+__attribute__((target_clones("avx512f", "avx2", "default")))
+static void h1_unit(int n1, int G, int D, float sl2, const uint16_t* q, const uint16_t* hk, const uint16_t* hv,
+                    const int* idx, size_t row0, int seq_w, int seq_r, float* z, size_t zst, float* o, float* lse) {
+  float qf[8][128], acc[8][128], row[128], m[8], l[8];
+  for (int h = 0; h < G; ++h) {
+    for (int e = 0; e < D; ++e) {
+      qf[h][e] = __uint_as_float_host((uint32_t)q[(size_t)h * D + e] << 16);
+      acc[h][e] = 0.f;
+    }
+    m[h] = -INFINITY;
+    l[h] = 0.f;
+  }
+  auto rowp = [&](int pos) {
+    return row0 + (size_t)(seq_w > 1 ? seq_owned_below(seq_w, seq_r, pos) : pos);
+  };
+  for (int j = 0; j < n1; ++j) {
+    const uint16_t* kr = hk + rowp(idx[j]) * D;
+#pragma omp simd
+    for (int e = 0; e < D; ++e) row[e] = __uint_as_float_host((uint32_t)kr[e] << 16);
+    for (int h = 0; h < G; ++h) {
+      float s = 0.f;
+#pragma omp simd reduction(+ : s)
+      for (int e = 0; e < D; ++e) s += qf[h][e] * row[e];
+      const float zz = s * sl2;
+      z[(size_t)h * zst + j] = zz;
+      m[h] = std::max(m[h], zz);
+    }
+  }
+  for (int j = 0; j < n1; ++j) {
+    const uint16_t* vr = hv + rowp(idx[j]) * D;
+#pragma omp simd
+    for (int e = 0; e < D; ++e) row[e] = __uint_as_float_host((uint32_t)vr[e] << 16);
+    for (int h = 0; h < G; ++h) {
+      const float p = exp2f(z[(size_t)h * zst + j] - m[h]);
+      l[h] += p;
+#pragma omp simd
+      for (int e = 0; e < D; ++e) acc[h][e] += p * row[e];
+    }
+  }
+  for (int h = 0; h < G; ++h) {
+    const float inv = l[h] > 0.f ? 1.f / l[h] : 0.f;
+    for (int e = 0; e < D; ++e) o[(size_t)h * D + e] = acc[h][e] * inv;
+    lse[(size_t)h * 2] = m[h];
+    lse[(size_t)h * 2 + 1] = l[h];
+  }
+}
+
 kv_tier_status kv_tier_set_host_t1(kv_tier_ctx* ctx, int32_t on) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "set_host_t1 inside a step");
@@ -1222,35 +1279,15 @@ kv_tier_status kv_tier_host_t1_attention(kv_tier_ctx* ctx, int32_t layer, const 
   const uint16_t* hv = hk ? hk + rows * D : nullptr;
   const uint16_t* q = reinterpret_cast<const uint16_t*>(q_host);
   const float sl2 = (float)(1.4426950408889634 / std::sqrt((double)D));
-  auto bf = [](uint16_t h) { uint32_t u = (uint32_t)h << 16; float f; memcpy(&f, &u, 4); return f; };
+  const size_t zst = (size_t)cap1;
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int bh = 0; bh < B * Hq; ++bh) {
-    const int b = bh / Hq, h = bh % Hq, g = h / G;
-    const int n1 = ctx->h1_cnt[b];
+  for (int bg = 0; bg < B * Hkv; ++bg) {       // one (request, kv head): each T1 row read once for its G heads
+    const int b = bg / Hkv, g = bg % Hkv;
     const size_t grp = ((size_t)layer * B + b) * Hkv + g;
-    float qf[128], acc[128];
-    for (int e = 0; e < D; ++e) { qf[e] = bf(q[(size_t)bh * D + e]); acc[e] = 0.f; }
-    float* z = ctx->h1_z.data() + (size_t)bh * cap1;
-    float m = -INFINITY;
-    for (int j = 0; j < n1; ++j) {
-      const uint16_t* kr = hk + host_row(v, grp, ctx->h1_idx[(size_t)b * cap1 + j]) * D;
-      float s4[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int e = 0; e < D; e += 4)
-        for (int u = 0; u < 4; ++u) s4[u] += qf[e + u] * bf(kr[e + u]);
-      z[j] = ((s4[0] + s4[1]) + (s4[2] + s4[3])) * sl2;
-      m = std::max(m, z[j]);
-    }
-    float l = 0.f;
-    for (int j = 0; j < n1; ++j) {
-      const float p = exp2f(z[j] - m);
-      l += p;
-      const uint16_t* vr = hv + host_row(v, grp, ctx->h1_idx[(size_t)b * cap1 + j]) * D;
-      for (int e = 0; e < D; ++e) acc[e] += p * bf(vr[e]);
-    }
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    for (int e = 0; e < D; ++e) o_part[(size_t)bh * D + e] = acc[e] * inv;
-    lse_part[(size_t)bh * 2] = m;
-    lse_part[(size_t)bh * 2 + 1] = l;
+    const size_t bh0 = (size_t)b * Hq + (size_t)g * G;
+    h1_unit(ctx->h1_cnt[b], G, D, sl2, q + bh0 * D, hk, hv, ctx->h1_idx.data() + (size_t)b * cap1,
+            grp * (size_t)v.hN, v.seq_w, v.seq_r, ctx->h1_z.data() + bh0 * zst, zst, o_part + bh0 * D,
+            lse_part + bh0 * 2);
   }
   ctx->h1_layer = layer;
   return KV_TIER_OK;
