@@ -15,6 +15,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-X
          "-Xcompiler", "-fopenmp", "-lgomp"]     # OpenMP: host-T1 attention (N1) on the host cores
 if os.environ.get("KVT_TRACE_LOOP"):        # debug: per-stage wait/busy accounting in the trace
     FLAGS += ["-DKVT_TRACE_LOOP=1"]
+if os.environ.get("KVT_NO_RED_DECODE"):     # experiment: no redundancy code in the decode kernel
+    FLAGS += ["-DKVT_NO_RED_DECODE=1"]
 if os.environ.get("KVT_FLAT_TRACE"):        # debug: per-unit epilogue timing in the flat kernel's trace
     FLAGS += ["-DKVT_FLAT_TRACE=1"]
 

@@ -397,7 +397,9 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
         const float vf = bf16_bits_to_f(vb[k]);
         for (int h = 0; h < G; ++h) part[16 + h * D + e] = vf;
       }
+#ifndef KVT_NO_RED_DECODE
       if (v.red && kin) redund_append(v, layer, unit, v.st->n - 1, kin);   // redundancy (fused append only)
+#endif
       if (scorer_uses_vnorm(v.scorer)) {   // VATP: the new token's V-row norm for this layer
         float ss = 0.f;
 #pragma unroll
@@ -964,7 +966,7 @@ __global__ void __launch_bounds__(128, 16) k_score_flush_lean(const DevView v, c
     const int pos = sg.pos(v, cur, u / v.Hkv, t);
     float s = v.S[(size_t)u * v.Nmax + pos];
     for (int j = 0; j < nz; ++j) {
-      const int slot = (zfirst + j) % v.zring;
+      const int slot = zslot_of(v, zfirst + j);
       const float4* z = reinterpret_cast<const float4*>(v.zbuf + slot * zslot + ((size_t)u * v.zrows + t) * 8);
       const float* ml = v.ml + slot * mslot + (size_t)u * 16;
       const float4 za = z[0], zc = z[1];
@@ -996,7 +998,7 @@ __global__ void __launch_bounds__(256) k_score_flush_req(const DevView v, const 
     const int pos = sg.pos(v, cur, b, t);
     float s = v.S[(size_t)u * v.Nmax + pos];
     for (int j = 0; j < nz; ++j) {                 // launches in layer order
-      const int slot = (zfirst + j) % v.zring;
+      const int slot = zslot_of(v, zfirst + j);
       const float* z = v.zbuf + slot * zslot + ((size_t)u * v.zrows + t) * 8;
       const float* ml = v.ml + slot * mslot + (size_t)u * 16;
       float inc = 0.f;

@@ -191,7 +191,7 @@ __device__ __forceinline__ void score_range(const DevView& v, const Seg& sg, int
 #pragma unroll
         for (int j = 0; j < ZBATCH; ++j) {
           if (j < nz) {
-            const int slot = (zfirst + j) % v.zring;
+            const int slot = zslot_of(v, zfirst + j);
             const float* z = v.zbuf + slot * zslot + ((size_t)uu[k] * v.zrows + tt[k]) * 8;
             z0[k][j] = *reinterpret_cast<const float4*>(z);
             z1[k][j] = *reinterpret_cast<const float4*>(z + 4);
@@ -206,7 +206,7 @@ __device__ __forceinline__ void score_range(const DevView& v, const Seg& sg, int
 #pragma unroll
       for (int j = 0; j < ZBATCH; ++j) {
         if (j >= nz) break;
-        const int slot = (zfirst + j) % v.zring;
+        const int slot = zslot_of(v, zfirst + j);
         const float wgt = score_weight(v, v.scorer ? v.zlayer[slot] : 0, uu[k], pos[k]);
         const float* ml = v.ml + slot * mslot + (size_t)uu[k] * 16;
         const float zz[8] = {z0[k][j].x, z0[k][j].y, z0[k][j].z, z0[k][j].w,

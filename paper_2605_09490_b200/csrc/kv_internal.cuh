@@ -137,6 +137,11 @@ __host__ __device__ __forceinline__ void policy_counts(int policy, int budget, i
   *n_t2 = ((long long)t2_bp * (surv - *n_hbm)) / 10000;
 }
 
+// ring slot of launch index i = zfirst + j: batches start ZBATCH-aligned and zring % ZBATCH == 0
+// (ZBATCH = 1), so a batch never wraps and the slot is i itself (no division in the score passes)
+__device__ __forceinline__ int zslot_of(const DevView&, int i) { return i; }
+static_assert(ZBATCH == 1, "zring_of must keep zring % ZBATCH == 0 if ZBATCH grows");
+
 // a4 weight of token (layer, unit, pos): 1 (Eq. 1) or its V-row norm (VATP)
 __device__ __forceinline__ float score_weight(const DevView& v, int layer, int unit, int pos) {
   return scorer_uses_vnorm(v.scorer) ? v.vnorm[((size_t)layer * v.B * v.Hkv + unit) * v.Nmax + pos] : 1.f;
