@@ -251,6 +251,12 @@ KV_TIER_API kv_tier_status kv_tier_host_t1_attention(kv_tier_ctx* ctx, int32_t l
  * scatter two layers back before reusing its buffer). */
 KV_TIER_API kv_tier_status kv_tier_host_t1_score_update(kv_tier_ctx* ctx, int32_t layer, const float* lse_global_host,
                                                         void* stream);
+/* The whole N1 sequence of one layer in one call (out_fp32 = 1): q device bf16 [B][H_q][d],
+ * k_new / v_new as kv_tier_decode_attention, o device fp32 [B][H_q][d] = exact attention over
+ * every visible token.  Uses ctx-owned pinned / device staging; blocks the calling thread twice
+ * (q on the host, combined (M, L) on the host). */
+KV_TIER_API kv_tier_status kv_tier_host_t1_layer(kv_tier_ctx* ctx, int32_t layer, const void* q, const void* k_new,
+                                                 const void* v_new, float* o, void* stream);
 
 /* a4 standalone (external probabilities, e.g. from another attention kernel):
  * probs: device fp32 [B][H_q][n_vis] over the visible tokens in ascending position

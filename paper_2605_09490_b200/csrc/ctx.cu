@@ -52,6 +52,11 @@ struct kv_tier_ctx {
   std::vector<float> h1_z;                 // [B][H_q][cap1] logits of the last host_t1_attention
   int h1_layer = -1;                       // layer whose logits h1_z holds (-1: none pending)
   float* h1_inc[2] = {nullptr, nullptr};   // pinned mapped score increments, double-buffered
+  // kv_tier_host_t1_layer: pinned q / partial / lse staging and device partials
+  uint16_t* h1_q = nullptr;
+  float* h1_o = nullptr;                   // [B][H_q][d] host partial o, then [B][H_q][2] lse, then lse_global
+  float* d1_parts = nullptr;               // device: o parts [2][B][H_q][d], lse parts [2][B][H_q][2], lse [B][H_q][2]
+  cudaEvent_t ev_q = nullptr;
   cudaEvent_t ev_inc[2] = {nullptr, nullptr};
   bool inc_used[2] = {false, false};
   std::string err;
@@ -507,6 +512,10 @@ kv_tier_status kv_tier_destroy(kv_tier_ctx* ctx) {
     if (ctx->h1_inc[i]) cudaFreeHost(ctx->h1_inc[i]);
     if (ctx->ev_inc[i]) cudaEventDestroy(ctx->ev_inc[i]);
   }
+  if (ctx->h1_q) cudaFreeHost(ctx->h1_q);
+  if (ctx->h1_o) cudaFreeHost(ctx->h1_o);
+  if (ctx->d1_parts) cudaFree(ctx->d1_parts);
+  if (ctx->ev_q) cudaEventDestroy(ctx->ev_q);
   delete ctx;
   return KV_TIER_OK;
 }
@@ -1246,6 +1255,14 @@ kv_tier_status kv_tier_set_host_t1(kv_tier_ctx* ctx, int32_t on) {
       if (e != cudaSuccess) return cuda_check(ctx, e, "set_host_t1 (staging)");
     }
   }
+  if (on && !ctx->h1_q) {
+    const size_t rows = (size_t)ctx->v.B * ctx->v.Hq, D = ctx->v.D;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&ctx->h1_q), rows * D * 2, cudaHostAllocPortable);
+    if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&ctx->h1_o), rows * (D + 4) * 4, cudaHostAllocPortable);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&ctx->d1_parts), rows * (2 * D + 6) * 4);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_q, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_check(ctx, e, "set_host_t1 (layer staging)");
+  }
   ctx->v.host_t1 = on ? 1 : 0;
   ctx->h1_epoch = -1;
   ctx->h1_layer = -1;
@@ -1327,6 +1344,46 @@ kv_tier_status kv_tier_host_t1_score_update(kv_tier_ctx* ctx, int32_t layer, con
   if (e == cudaSuccess) ctx->inc_used[buf] = true;
   ctx->h1_layer = -1;
   return cuda_check(ctx, e, "host_t1_score_update");
+}
+
+// One whole host-T1 layer (the sequence of kv_tier.h's N1 block) in a single call: q down,
+// GPU partial, host partial, combine, both score updates.  Two host waits per layer (q on the
+// host; the combined (M, L) on the host).
+kv_tier_status kv_tier_host_t1_layer(kv_tier_ctx* ctx, int32_t layer, const void* q, const void* k_new,
+                                     const void* v_new, float* o, void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!ctx->v.host_t1 || !ctx->h1_q) return fail(ctx, KV_TIER_E_STATE, "host-T1 mode is off (kv_tier_set_host_t1)");
+  if (!ctx->v.out_fp32) return fail(ctx, KV_TIER_E_STATE, "kv_tier_host_t1_layer needs out_fp32 = 1");
+  if (!q || !o || ((uintptr_t)o & 15)) return fail(ctx, KV_TIER_E_INVAL, "q / o (16-B aligned fp32) required");
+  const DevView& v = ctx->v;
+  const size_t rows = (size_t)v.B * v.Hq, D = v.D;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  float* po = ctx->d1_parts;                 // [2][rows][D]
+  float* pl = po + 2 * rows * D;             // [2][rows][2]
+  float* lg = pl + 4 * rows;                 // [rows][2]
+  float* ho = ctx->h1_o;                     // host o [rows][D], lse [rows][2], lse_global [rows][2]
+  float* hl = ho + rows * D;
+  float* hg = hl + 2 * rows;
+  cudaError_t e = cudaMemcpyAsync(ctx->h1_q, q, rows * D * 2, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_q, s);
+  if (e != cudaSuccess) return cuda_check(ctx, e, "host_t1_layer (q down)");
+  kv_tier_status st = decode_attention_impl(ctx, layer, q, k_new, v_new, po, 1, stream, 0, pl);
+  if (st) return st;
+  e = cudaEventSynchronize(ctx->ev_q);
+  if (e != cudaSuccess) return cuda_check(ctx, e, "host_t1_layer (q wait)");
+  st = kv_tier_host_t1_attention(ctx, layer, ctx->h1_q, ho, hl);
+  if (st) return st;
+  e = cudaMemcpyAsync(po + rows * D, ho, rows * D * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(pl + 2 * rows, hl, rows * 2 * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = launch_lse_combine(po, pl, 2, (int)rows, (int)D, o, lg, s);
+  if (e != cudaSuccess) return cuda_check(ctx, e, "host_t1_layer (combine)");
+  st = kv_tier_score_update_lse(ctx, lg, stream);
+  if (st) return st;
+  e = cudaMemcpyAsync(hg, lg, rows * 2 * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_q, s);
+  if (e == cudaSuccess) e = cudaEventSynchronize(ctx->ev_q);
+  if (e != cudaSuccess) return cuda_check(ctx, e, "host_t1_layer (lse up)");
+  return kv_tier_host_t1_score_update(ctx, layer, hg, stream);
 }
 
 kv_tier_status kv_tier_import_scores(kv_tier_ctx* ctx, const float* host_S, size_t bytes) {

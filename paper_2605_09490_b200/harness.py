@@ -224,8 +224,10 @@ class HostT1Decode:
     (lse_combine, Eq. 3 split by tier), and the score update runs for the GPU's tokens
     (score_update_lse) and for T1 on the host (host_t1_score_update) with the global (M, L)."""
 
-    def __init__(self, w, device="cuda:0", **kw):
-        self.w = w
+    def __init__(self, w, device="cuda:0", fused=True, **kw):
+        """fused: one kv_tier_host_t1_layer call per layer (the library sequences the copies,
+        the host loop and both score updates); else the same sequence from Python."""
+        self.w, self.fused = w, fused
         self.run = TieredDecode(w, device=device, out_fp32=True, **kw)
         self.run.kv.set_host_t1(True)
         B, L, Hq, d = w["B"], w["L"], w["Hq"], w["d"]
@@ -251,6 +253,9 @@ class HostT1Decode:
         with torch.cuda.stream(s):
             kv.begin_step(stream=s)
             for l in range(self.w["L"]):
+                if self.fused:
+                    kv.host_t1_layer(l, Q[l], self.O[l], stream=s, k_new=r.Kn[t, l], v_new=r.Vn[t, l])
+                    continue
                 self.q_host.copy_(Q[l], non_blocking=True)                  # q down
                 q_ready = torch.cuda.Event()
                 q_ready.record(s)

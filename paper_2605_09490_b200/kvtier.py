@@ -70,6 +70,7 @@ _SIGS = {
     "kv_tier_set_host_t1": [C.c_void_p, C.c_int32],
     "kv_tier_host_t1_attention": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p],
     "kv_tier_host_t1_score_update": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p],
+    "kv_tier_host_t1_layer": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     "kv_tier_lse_combine": [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                             C.c_void_p],
     "kv_tier_score_update": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p],
@@ -229,6 +230,13 @@ class KvTier:
             raise ValueError("host_t1_score_update takes a contiguous CPU lse tensor")
         _check(load().kv_tier_host_t1_score_update(self.ctx, layer, C.c_void_p(lse_global_host.data_ptr()),
                                                    _stream_ptr(stream)), self.ctx)
+
+    def host_t1_layer(self, layer, q, o, stream=None, k_new=None, v_new=None):
+        """One whole host-T1 layer (kv_tier_host_t1_layer): o fp32 [B][H_q][d] on the device."""
+        kp = C.c_void_p(k_new.data_ptr()) if k_new is not None else None
+        vp = C.c_void_p(v_new.data_ptr()) if v_new is not None else None
+        _check(load().kv_tier_host_t1_layer(self.ctx, layer, C.c_void_p(q.data_ptr()), kp, vp,
+                                            C.c_void_p(o.data_ptr()), _stream_ptr(stream)), self.ctx)
 
     def score_update(self, layer, probs, stream=None):
         _check(load().kv_tier_score_update(self.ctx, layer, C.c_void_p(probs.data_ptr()), _stream_ptr(stream)),

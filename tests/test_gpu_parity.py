@@ -578,13 +578,14 @@ def test_redundancy_scorer_sampled_7b_requests():
 
 
 # --------------------------------------------------------------------- N1: host-side T1 attention
-@pytest.mark.parametrize("staging,d", [(kt.STAGING_ALL, 128), (0, 128), (0, 64)])
-def test_host_t1_attention_matches_oracle(staging, d):
+@pytest.mark.parametrize("staging,d,fused", [(kt.STAGING_ALL, 128, False), (kt.STAGING_ALL, 128, True),
+                                              (0, 128, True), (0, 64, False)])
+def test_host_t1_attention_matches_oracle(staging, d, fused):
     # T1 attended on the host cores, T0 ∪ T2 on the GPU, combined by LSE (Eq. 3):
     # o, scores and every event's tiers / rows equal the oracle's full-attention run
     w = H.workload("tiny", B=3, L=2, Hq=8, Hkv=2, d=d, N=600, P=32, interval=8, steps=26,
                    hbm_bp=4000, evict_bp=800, t2_bp=3000, staging=staging)
-    h = H.HostT1Decode(w)
+    h = H.HostT1Decode(w, fused=fused)
     orc = OracleRun(w)
     for t in range(w["steps"]):
         h.step()
