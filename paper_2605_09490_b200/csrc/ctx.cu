@@ -1246,7 +1246,6 @@ kv_tier_status kv_tier_set_host_t1(kv_tier_ctx* ctx, int32_t on) {
   if (on && ctx->v.flat) return fail(ctx, KV_TIER_E_STATE, "host-T1 mode runs the split kernel (KVTIER_FLAT=0)");
   if (on && (ctx->v.cluster_merge || ctx->v.last_merge))
     return fail(ctx, KV_TIER_E_STATE, "host-T1 mode needs the merge kernel (KVTIER_CLUSTER=0, KVTIER_LASTMERGE=0)");
-  if (on && !ctx->host_t1 && ctx->v.cap1 > 0) return fail(ctx, KV_TIER_E_STATE, "no host T1 store");
   const size_t ninc = (size_t)ctx->v.B * ctx->v.Hkv * std::max(ctx->v.cap1, 1);
   for (int i = 0; on && i < 2; ++i) {
     if (!ctx->h1_inc[i]) {
@@ -1293,6 +1292,8 @@ kv_tier_status kv_tier_host_t1_attention(kv_tier_ctx* ctx, int32_t layer, const 
   }
   const size_t rows = (size_t)v.L * B * Hkv * v.hN;
   const uint16_t* hk = reinterpret_cast<const uint16_t*>(ctx->host_t1);
+  if (!hk && std::any_of(ctx->h1_cnt.begin(), ctx->h1_cnt.end(), [](int c) { return c > 0; }))
+    return fail(ctx, KV_TIER_E_STATE, "T1 tokens without a host T1 store");   // (beta = 100 % keeps T1 empty)
   const uint16_t* hv = hk ? hk + rows * D : nullptr;
   const uint16_t* q = reinterpret_cast<const uint16_t*>(q_host);
   const float sl2 = (float)(1.4426950408889634 / std::sqrt((double)D));

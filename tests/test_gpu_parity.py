@@ -600,6 +600,33 @@ def test_host_t1_attention_matches_oracle(staging, d, fused):
     h.close()
 
 
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVT_FUZZ_SEEDS_H1", "8"))))
+def test_randomized_host_t1(seed):
+    # seeded draws incl. the degenerate ratios: beta = 100 % (no T1: the host partial is empty,
+    # m = -inf) and beta = 0 (every live token in T1), T2 on/off, both staging modes, d = 64/128
+    rng = np.random.default_rng(7000 + seed)
+    Hkv = int(rng.choice([1, 2, 4]))
+    w = H.workload("tiny", B=int(rng.integers(1, 4)), L=int(rng.integers(1, 4)), Hq=Hkv * int(rng.choice([1, 3, 8])),
+                   Hkv=Hkv, d=int(rng.choice([64, 128])), N=int(rng.integers(150, 800)), P=int(rng.integers(0, 40)),
+                   interval=int(rng.choice([4, 8])), steps=int(rng.integers(8, 18)),
+                   hbm_bp=int(rng.choice([0, 10000, int(rng.integers(0, 10001))])), evict_bp=int(rng.integers(0, 2001)),
+                   t2_bp=int(rng.choice([0, 3000])), staging=int(rng.choice([kt.STAGING_ALL, 0])),
+                   evict_mode=int(rng.choice([kt.EVICT_TOTAL, kt.EVICT_PER_EVENT])))
+    h = H.HostT1Decode(w, fused=bool(rng.integers(0, 2)))
+    orc = OracleRun(w)
+    for t in range(w["steps"]):
+        h.step()
+        ok, mabs, _ = o_close(h.output()[:, orc.reqs], orc.step())
+        assert ok, (t, mabs)
+        if h.is_event(t) or t == w["steps"] - 1:
+            h.sync()
+            ok, mrel = s_close(h.run.kv.export(kt.X_SCORES)[orc.reqs], orc.st.S_part[:, :, :orc.st.n])
+            assert ok, (t, mrel)
+            if h.is_event(t):
+                _check_event_state(h.run, orc, orc.reqs, layers=tuple(range(w["L"])))
+    h.close()
+
+
 def test_host_t1_sampled_7b_requests():
     w = H.workload("7b", steps=6, interval=4, staging=0)
     h = H.HostT1Decode(w)
