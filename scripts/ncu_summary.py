@@ -60,7 +60,8 @@ def full(path, kid="0"):
             rd = float(d.get("dram__bytes_read.sum", "0").replace(",", "") or 0)
             wr = float(d.get("dram__bytes_write.sum", "0").replace(",", "") or 0)
             ur = units[hh.index("dram__bytes_read.sum")] if "dram__bytes_read.sum" in hh else ""
-            print(f"| dram__bytes_read.sum + write.sum | {rd:.4g} + {wr:.4g} {ur} |")
+            uw = units[hh.index("dram__bytes_write.sum")] if "dram__bytes_write.sum" in hh else ""
+            print(f"| dram__bytes_read.sum + write.sum | {rd:.4g} {ur} + {wr:.4g} {uw} |")
     src = subprocess.run([NCU, "-i", path, "--page", "source", "--csv", "--print-source=sass"],
                          capture_output=True, text=True).stdout
     sr = list(csv.reader(io.StringIO(src)))
