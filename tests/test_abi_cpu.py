@@ -136,3 +136,12 @@ def test_redundancy_scorers_size_their_buffers():
         sz[sc] = s.device_arena
     extra = sz[kt.SCORER_REDUNDANCY] - sz[kt.SCORER_ATTENTION]
     assert 2 * 2 * 300 * 4 + 3 * 2 * 2 * 64 * 2 <= extra <= 2 * 2 * 300 * 4 + 3 * 2 * 2 * 64 * 2 + 2 * 256
+
+
+def test_host_t1_entry_points_reject_null_ctx():
+    # N1 entry points check their arguments before touching a device
+    lib = kt.load()
+    assert lib.kv_tier_set_host_t1(None, 1) == -1
+    assert lib.kv_tier_host_t1_attention(None, 0, None, None, None) == -1
+    assert lib.kv_tier_host_t1_score_update(None, 0, None, None) == -1
+    assert lib.kv_tier_host_t1_layer(None, 0, None, None, None, None, None) == -1

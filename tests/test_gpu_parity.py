@@ -392,6 +392,15 @@ def test_kvhead_sharding_matches_unsharded_oracle(world):
     sh.close()
 
 
+def test_redundancy_scorer_refused_in_classify_gathered():
+    # R_part lives per shard, and the gathered classify would rank without it (AMB-31): refused
+    w = H.workload("tiny", Hq=4, Hkv=2, steps=2, scorer=kt.SCORER_REDUNDANCY)
+    sh = H.KvHeadShardedDecode(w, 2)
+    with pytest.raises(kt.KvTierError):
+        sh.step()                                    # t = 0 is an event
+    sh.close()
+
+
 def test_kvhead_plain_classify_refused():
     w = H.workload("tiny", Hq=4, Hkv=2, steps=2)
     run = H.TieredDecode(w, heads=(0, 1), shard=kt.SHARD_KVHEAD, rank=0, world=2)
