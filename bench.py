@@ -28,6 +28,7 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
 CONFIG_INDEX = {"tiny": 0, "7b": 1, "14b": 2, "32b": 3, "70b": 4}      # BASELINE.json configs[i]
 POLICIES = {"hierarchy": 0, "streaming": 1, "h2o": 2, "random": 3}       # kv_tier_policy
 SCORERS = {"attention": 0, "vatp": 1, "redundancy": 2, "combined": 3}    # kv_tier_scorer
+MODEL_DIMS = {"tiny": (256, 512), "7b": (3584, 18944)}                    # (hidden, intermediate): Qwen2-7B
 
 
 def _peaks():
@@ -376,7 +377,7 @@ def main():
     # ---- control: same visible set, everything HBM-resident, no classify/migrate in window
     overhead = None
     control_ms = None
-    stream_leg = host_t1_leg = None
+    stream_leg = host_t1_leg = model_leg = None
     if not args.no_extras:
         ctl = H.TieredDecode(dict(w, steps=W + K), device=dev, out_fp32=False, split=args.split, seed_offset=seed_off,
                              variant=args.variant)
@@ -447,6 +448,31 @@ def main():
         del hr
         torch.cuda.empty_cache()
 
+        # ---- N4 (partial): the same attention inside a decoder of the model's shape (random bf16
+        # weights, torch/cuBLAS for the non-attention layers): end-to-end decode tokens/s with
+        # no tiering (beta = 100 %, r = 0), the default hierarchy, and strict DDR residency
+        if args.config in MODEL_DIMS:
+            hidden, inter = MODEL_DIMS[args.config]
+            Km, Wm = 16, 3
+            model_leg = {"hidden": hidden, "intermediate": inter,
+                         "note": "random bf16 weights, RMSNorm + GEMMs + SiLU in torch/cuBLAS, no RoPE / LM head"}
+            for name, extra in (("all_hbm_no_eviction", dict(hbm_bp=10000, evict_bp=0)), ("hierarchy", {}),
+                                ("hierarchy_stream_mode", dict(staging=0))):
+                md = H.ModelDecode(dict(w, steps=Wm + Km, **extra), hidden=hidden, inter=inter, device=dev,
+                                   split=args.split, seed_offset=seed_off, variant=args.variant)
+                for _ in range(Wm):
+                    md.step()
+                md.sync()
+                _barrier_sync()
+                el_m = _max_over_ranks(timed(md.step, md.run.main, Km))
+                model_leg[name] = {"tokens_per_s": world * B * Km / el_m, "ms_per_step": 1e3 * el_m / Km}
+                md.close()
+                del md
+                torch.cuda.empty_cache()
+            b0 = model_leg["all_hbm_no_eviction"]["ms_per_step"]
+            for name in ("hierarchy", "hierarchy_stream_mode"):
+                model_leg[name]["overhead_pct_vs_all_hbm"] = 100.0 * (model_leg[name]["ms_per_step"] / b0 - 1.0)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_extras:
         cpu = cpu_oracle_sample(w, args.cpu_seconds)
@@ -483,6 +509,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
             "stream_mode": stream_leg,
             "host_t1": host_t1_leg,
+            "model_decode": model_leg,
             "context": "paper: 5-7% transfer overhead on RTX 5080 PCIe Gen5, unpinned, 7B int8, batch 1 (P:642)",
         }
         print(json.dumps(out), flush=True)

@@ -154,6 +154,73 @@ class TieredDecode:
         self.kv.close()
 
 
+class ModelDecode:
+    """the tiered attention inside a decoder of the 7B model's shape
+    (Qwen2-7B dims) with random bf16 weights, so the path runs with its real
+    per-layer dependency: q/k/v come from this layer's projections of the previous layer's
+    output, and the T1 prefetch of layer l+2 (stream mode) overlaps layer l's MLP.
+    Non-attention layers are plain torch/cuBLAS (RMSNorm, GEMMs, SiLU; no RoPE, no LM head):
+    they are the context, not the product.  The prefix K/V are the synthetic generator's."""
+
+    def __init__(self, w, hidden=3584, inter=18944, device="cuda:0", **kw):
+        import math
+        self.w, self.hidden, self.inter = w, hidden, inter
+        self.run = TieredDecode(w, device=device, out_fp32=False, **kw)
+        B, L, Hq, Hkv, d = w["B"], w["L"], w["Hq"], w["Hkv"], w["d"]
+        dev = self.run.dev
+        g = torch.Generator(device=dev).manual_seed(w["seed"] + 17)
+
+        def W(i, o):
+            return (torch.randn(i, o, generator=g, device=dev) / math.sqrt(i)).to(torch.bfloat16)
+
+        self.layers = [dict(wqkv=W(hidden, (Hq + 2 * Hkv) * d), wo=W(Hq * d, hidden), wgu=W(hidden, 2 * inter),
+                            wd=W(inter, hidden)) for _ in range(L)]
+        self.x = torch.randn(B, hidden, generator=g, device=dev).to(torch.bfloat16)
+        self.O = torch.empty((B, Hq, d), dtype=torch.bfloat16, device=dev)
+
+    @staticmethod
+    def _rms(x):
+        xf = x.float()
+        return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-6)).to(torch.bfloat16)
+
+    def step(self):
+        r, w = self.run, self.w
+        kv, s, t = r.kv, r.main, r.t
+        B, L, Hq, Hkv, d = w["B"], w["L"], w["Hq"], w["Hkv"], w["d"]
+        stream_mode = w["staging"] == 0
+        with torch.cuda.stream(s):
+            kv.begin_step(stream=s)
+            if stream_mode:
+                for l in range(min(2, L)):
+                    kv.prefetch(l, side=r.side)
+            x = self.x
+            for l, p in enumerate(self.layers):
+                qkv = self._rms(x) @ p["wqkv"]
+                q = qkv[:, :Hq * d].reshape(B, Hq, d).contiguous()
+                k = qkv[:, Hq * d:(Hq + Hkv) * d].reshape(B, Hkv, d).contiguous()
+                v = qkv[:, (Hq + Hkv) * d:].reshape(B, Hkv, d).contiguous()
+                kv.decode_attention(l, q, self.O, 1, stream=s, k_new=k, v_new=v)
+                if stream_mode and l + 2 < L:
+                    kv.prefetch(l + 2, side=r.side)
+                x = x + self.O.reshape(B, Hq * d) @ p["wo"]
+                gu = self._rms(x) @ p["wgu"]
+                x = x + (torch.nn.functional.silu(gu[:, :self.inter]) * gu[:, self.inter:]) @ p["wd"]
+            kv.end_step(stream=s)
+            if r.is_event(t):
+                r.classify()
+                kv.migrate(stream=s, side=r.side)
+            self.x = self._rms(x)
+        r.t += 1
+        return self.x
+
+    def sync(self):
+        self.run.sync()
+
+    def close(self):
+        self.run.close()
+        self.layers = None
+
+
 class KvHeadShardedDecode:
     """KV-head sharding simulated in one process: `world` ctxs on one
     device, ctx r holding kv heads [r*H_l, (r+1)*H_l).  At an event the ctxs' S_part are
