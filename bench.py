@@ -453,7 +453,9 @@ def main():
         # no tiering (beta = 100 %, r = 0), the default hierarchy, and strict DDR residency
         if args.config in MODEL_DIMS:
             hidden, inter = MODEL_DIMS[args.config]
-            Km, Wm = 16, 3
+            # Km = Delta: the timed window holds exactly one classify/migrate event (t = 64), so
+            # the hierarchy's cost is amortised over one full management interval
+            Km, Wm = 64, 3
             model_leg = {"hidden": hidden, "intermediate": inter,
                          "note": "random bf16 weights, RMSNorm + GEMMs + SiLU in torch/cuBLAS, no RoPE / LM head"}
             for name, extra in (("all_hbm_no_eviction", dict(hbm_bp=10000, evict_bp=0)), ("hierarchy", {}),
