@@ -609,7 +609,7 @@ def test_host_t1_attention_matches_oracle(staging, d, fused):
     h.close()
 
 
-@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVT_FUZZ_SEEDS_H1", "8"))))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVT_FUZZ_SEEDS_H1", "16"))))
 def test_randomized_host_t1(seed):
     # seeded draws incl. the degenerate ratios: beta = 100 % (no T1: the host partial is empty,
     # m = -inf) and beta = 0 (every live token in T1), T2 on/off, both staging modes, d = 64/128
@@ -723,7 +723,7 @@ def test_lse_combine_kernel_matches_full_softmax():
 
 
 # --------------------------------------------------------------------- randomized configurations
-@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVT_FUZZ_SEEDS", "24"))))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVT_FUZZ_SEEDS", "64"))))
 def test_randomized_configs(seed):
     # seeded draws over the configuration space (shapes, ratios, T2, eviction mode, interval,
     # staging, tier policy, scorer) against the oracle: catches interactions no fixed test covers
@@ -746,7 +746,7 @@ def test_randomized_configs(seed):
     _run_pair(w, graph=bool(rng.integers(0, 2)), check_every=3)
 
 
-@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVT_FUZZ_SEEDS_SEQ", "8"))))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVT_FUZZ_SEEDS_SEQ", "24"))))
 def test_randomized_sequence_shards(seed):
     rng = np.random.default_rng(5000 + seed)
     Hkv = int(rng.choice([1, 2]))
