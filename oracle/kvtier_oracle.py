@@ -11,7 +11,10 @@ reading fixes fp32 (scores, AMB-14; T2 codec, AMB-12).  Citations: P:n =
 PAPER.md line n, S:n = SPEC.md line n, AMB-k = ambiguity reading k.
 
 Pinned by tests/test_oracle_pins.py (-m "not gpu"); every function below has a
-pin there.  No function is "parity unpinned".
+pin there.  tests/test_oracle_mutants.py checks that those pins fail on plausible
+mistakes (T3 attended, T2 at full precision, one head per group in the external
+update, lossless T2 exit, window/floor/scale/T2-order errors).  No function is
+"parity unpinned".
 """
 from __future__ import annotations
 

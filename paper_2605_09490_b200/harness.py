@@ -94,9 +94,9 @@ class TieredDecode:
         return t % self.w["interval"] == 0
 
     def output(self):
-        """Host copy of the last step's o [L][B][Hq][d] (waits for the main stream)."""
+        """Host copy of the last step's o [L][B][Hq][d] as fp32 (waits for the main stream)."""
         self.main.synchronize()
-        return self.O.cpu().numpy()
+        return self.O.float().cpu().numpy()
 
     def step(self, manage=True):
         """One decode step t (+ manage event when t mod Delta == 0 unless manage=False).

@@ -70,8 +70,8 @@ def _check_event_state(run, orc, reqs_gpu, layers=(0,)):
                 assert np.array_equal(scales[bg][:, :, 1], st.scaleV[l, bo, hs][:, pos])
 
 
-def _run_pair(w, reqs=None, graph=False, check_every=1, layers_api=False, split=0, variant=0):
-    run = H.TieredDecode(w, split=split, variant=variant)
+def _run_pair(w, reqs=None, graph=False, check_every=1, layers_api=False, split=0, variant=0, out_fp32=True):
+    run = H.TieredDecode(w, split=split, variant=variant, out_fp32=out_fp32)
     orc = OracleRun(w, reqs=reqs)
     reqs_gpu = orc.reqs
     if graph:
@@ -167,6 +167,11 @@ def test_7b_sampled_requests():               # BASELINE.json configs[1], bench 
     _run_pair(w, reqs=[0, 5], graph=True, check_every=16)
 
 
+def test_7b_sampled_requests_bf16_out():      # the bench's exact launch configuration: o stored as bf16
+    w = H.workload("7b", steps=66)
+    _run_pair(w, reqs=[2, 7], graph=True, check_every=16, out_fp32=False)
+
+
 # --------------------------------------------------------------------- larger BASELINE shapes, sampled
 @pytest.mark.parametrize("name,B,req,steps", [("14b", 2, 1, 2), ("32b", 1, 0, 2), ("70b", 1, 0, 1)])
 def test_large_shapes_sampled_requests(name, B, req, steps):
@@ -222,9 +227,10 @@ def test_prop1_gpu_outputs_independent_of_beta():
     for k in (1, 2):
         assert np.array_equal(t3[k], t3[0])
         # bitwise equality holds in the oracle (ascending-position sums); on the GPU the
-        # T0/T1 split changes the chunking, hence the bf16 rounding of p -> tolerance only
-        ok, mabs, _ = o_close(outs[k], outs[0].astype(np.float64))
-        assert ok, mabs
+        # T0/T1 split changes the chunking and so the fp32 summation order (p enters the P.V
+        # MMA as hi + lo bf16 terms): equal to fp32 rounding, far inside the parity tolerance
+        mabs = float(np.abs(outs[k] - outs[0]).max())
+        assert mabs < 1e-4, mabs
 
 
 def test_graph_equals_layer_calls_bitwise():

@@ -651,3 +651,121 @@ def test_combined_increments_are_vatp_weighted():
             r.step()
         outs[sc] = r.st.S_part.copy()
     assert np.array_equal(outs[O.SCORER_VATP], outs[O.SCORER_COMBINED])
+
+
+# --------------------------------------------------------------------- the decode loop at r > 0, T2, external
+# update, lossy T2 exit (round-2 pins: each kills a plausible mutation of the oracle)
+def _sdpa_masked(q, k, v, keep, G):
+    """torch SDPA in float64 with a boolean mask: q [Hq][d], k/v [Hkv][n][d], keep [n]."""
+    q = torch.as_tensor(q, dtype=torch.float64)
+    k = torch.as_tensor(k, dtype=torch.float64).repeat_interleave(G, 0)
+    v = torch.as_tensor(v, dtype=torch.float64).repeat_interleave(G, 0)
+    mask = torch.as_tensor(keep)[None, None, :].expand(q.shape[0], 1, keep.shape[0])
+    return torch.nn.functional.scaled_dot_product_attention(q[:, None, :], k, v, attn_mask=mask)[:, 0].numpy()
+
+
+def test_decode_loop_masks_t3_at_r_gt_0():                    # Eq. 3 P:233-236 inside Alg. 1's loop
+    """At r = 10 % the loop's o equals float64 SDPA over ALL positions with only the oracle's T3
+    set masked (original generator rows: f2 = 0), and differs from full attention -- so an
+    oracle that attends every position, or drops a live one, fails.  Brute force on one head."""
+    st, outs, t3s, (K, V, Q) = _tiny_run(hbm_bp=3000, evict_bp=1000, interval=8, steps=20)
+    Kf, Vf, Qf = (S.bf16_bits_to_f32(x).astype(np.float64) for x in (K, V, Q))
+    n0, checked = 255, 0
+    for t in (1, 8, 9, 16, 19):                                # steps after (and at) events
+        n = n0 + t + 1
+        ev = set(int(i) for i in t3s[t - 1])                   # T3 as the step's attention saw it
+        assert len(ev) > 0
+        keep = np.ones(n, dtype=bool)
+        keep[list(ev)] = False
+        ref = _sdpa_masked(Qf[t, 0, 0], Kf[0, 0, :, :n], Vf[0, 0, :, :n], keep, G=2)
+        assert np.allclose(outs[t][0, 0], ref, rtol=0, atol=1e-12), t
+        full = _sdpa_masked(Qf[t, 0, 0], Kf[0, 0, :, :n], Vf[0, 0, :, :n], np.ones(n, bool), G=2)
+        assert np.abs(full - ref).max() > 1e-6                  # the mask matters at this step
+        h = 3
+        bf = _brute_attention(list(Qf[t, 0, 0, h]), Kf[0, 0, h // 2, :n].tolist(), Vf[0, 0, h // 2, :n].tolist(),
+                              skip=ev)
+        assert np.allclose(outs[t][0, 0, h], bf, rtol=0, atol=1e-12)
+        checked += 1
+    assert checked == 5
+
+
+def test_decode_loop_attends_t2_as_code_times_scale():        # P:151, AMB-12
+    """With f2 = 50 % the loop's o equals float64 SDPA over rows in which every T2 token is
+    fp32(code x scale) of its stored codes (the codec is pinned above), T3 masked; and it
+    differs measurably from SDPA over the full-precision rows."""
+    w = S.WORKLOADS["tiny"]
+    n0, steps = w["N"] - 1, 10
+    K = S.gen_kv(w["seed"], "k", 1, 1, 2, 64, 0, n0 + steps, w["P"], 4)
+    V = S.gen_kv(w["seed"], "v", 1, 1, 2, 64, 0, n0 + steps, w["P"], 4)
+    Q = S.gen_q(w["seed"], 0, steps, 1, 1, 4, 2, 64)
+    cfg = O.OracleConfig(B=1, L=1, Hq=4, Hkv=2, d=64, prompt_len=w["P"], manage_interval=8,
+                         hbm_bp=5000, evict_bp=500, t2_bp=5000)
+    st = O.init_state(cfg, K, V, n0)
+    for t in range(9):                                         # events at t = 0 and 8
+        O.decode_step(st, Q[t])
+    t, n_att = 9, st.n + 1                                     # step 9 appends position st.n (T0)
+    tier = st.tier[0, :n_att].copy()
+    t2 = np.nonzero(tier == 2)[0]
+    assert t2.size > 0 and tier[-1] == 0
+    Kr = st.rowK[0, 0, :, :n_att].astype(np.float64)           # [Hkv][n][d] full-precision rows
+    Vr = st.rowV[0, 0, :, :n_att].astype(np.float64)
+    Kq, Vq = Kr.copy(), Vr.copy()
+    for g in range(2):
+        ck = torch.from_numpy(st.codeK[0, 0, g, t2].astype(np.float32))
+        cv = torch.from_numpy(st.codeV[0, 0, g, t2].astype(np.float32))
+        Kq[g, t2] = (ck * torch.from_numpy(st.scaleK[0, 0, g, t2])[:, None]).double().numpy()
+        Vq[g, t2] = (cv * torch.from_numpy(st.scaleV[0, 0, g, t2])[:, None]).double().numpy()
+    keep = tier != 3
+    o = O.decode_step(st, Q[t])
+    Qf = S.bf16_bits_to_f32(Q).astype(np.float64)
+    ref = _sdpa_masked(Qf[t, 0, 0], Kq, Vq, keep, G=2)
+    assert np.allclose(o[0, 0], ref, rtol=0, atol=1e-12)
+    hi = _sdpa_masked(Qf[t, 0, 0], Kr, Vr, keep, G=2)
+    assert np.abs(hi - ref).max() > 1e-5                      # dequantisation changes the output
+
+
+def test_score_update_external_nested_loop():                 # Eq. 1 P:184-187, AMB-14
+    rng = np.random.default_rng(11)
+    Hkv, G, N = 3, 4, 40
+    vis = np.array(sorted(rng.choice(N, size=25, replace=False)))
+    probs = rng.random((Hkv * G, vis.size))
+    S0 = rng.random((Hkv, N)).astype(np.float32)
+    got = O.score_update_external(S0.copy(), vis, probs, G)
+    want = S0.copy()
+    for g in range(Hkv):
+        for j, p in enumerate(vis):
+            acc = 0.0
+            for h in range(g * G, g * G + G):                  # every head of the group
+                acc += float(probs[h, j])
+            want[g, p] = np.float32(np.float32(want[g, p]) + np.float32(acc))
+    assert np.array_equal(got, want)
+    untouched = np.setdiff1d(np.arange(N), vis)
+    assert np.array_equal(got[:, untouched], S0[:, untouched])
+
+
+def test_row_leaving_t2_keeps_bf16_of_dequant():              # AMB-12 (lossy T2 exit)
+    """Two crafted events: positions 3..6 go to T2 at the first, 3..5 return to T0 at the
+    second.  Their stored rows must be bf16(code x scale) of the first quantisation
+    (torch's bf16 rounding) -- not the original rows, which they differ from."""
+    L, Hkv, d, n = 2, 1, 8, 12
+    g = torch.Generator().manual_seed(3)
+    Kb = (torch.randn((L, 1, Hkv, n, d), generator=g) * 1.7).to(torch.bfloat16)
+    Vb = (torch.randn((L, 1, Hkv, n, d), generator=g) * 0.9).to(torch.bfloat16)
+    bits = lambda x: x.view(torch.int16).numpy().view(np.uint16)
+    cfg = O.OracleConfig(B=1, L=L, Hq=2, Hkv=Hkv, d=d, prompt_len=2, sink_size=1, window_size=2,
+                         hbm_bp=5000, evict_bp=0, t2_bp=10000)
+    st = O.init_state(cfg, bits(Kb), bits(Vb), n)
+    st.S_part[0, 0, :n] = np.arange(n, dtype=np.float32)       # ascending: 3..6 lowest -> T2
+    O.manage_event(st)
+    assert np.nonzero(st.tier[0, :n] == 2)[0].tolist() == [3, 4, 5, 6]
+    st.S_part[0, 0, :n] = np.arange(n, 0, -1, dtype=np.float32)   # descending: 3..5 highest -> T0
+    O.manage_event(st)
+    assert st.tier[0, 3:6].tolist() == [0, 0, 0]
+    Kf, Vf = Kb.float().numpy(), Vb.float().numpy()
+    for src, row in ((Kf, st.rowK), (Vf, st.rowV)):
+        for p in (3, 4, 5):
+            for l in range(L):
+                c, s = O.quantize_int8(src[l, 0, 0, p])
+                want = (torch.from_numpy(c.astype(np.float32)) * float(s)).to(torch.bfloat16).float().numpy()
+                assert np.array_equal(row[l, 0, 0, p], want), (p, l)
+        assert not np.array_equal(row[:, 0, 0, 3:6], src[:, 0, 0, 3:6])
