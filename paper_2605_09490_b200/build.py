@@ -21,7 +21,7 @@ if os.environ.get("KVT_FLAT_TRACE"):        # debug: per-unit epilogue timing in
     FLAGS += ["-DKVT_FLAT_TRACE=1"]
 
 TARGETS = {
-    "libkvtier.so": ["csrc/ctx.cu", "csrc/attn.cu", "csrc/attn_flat.cu", "csrc/tiers.cu"],
+    "libkvtier.so": ["csrc/ctx.cu", "csrc/attn.cu", "csrc/attn_flat.cu", "csrc/tiers.cu", "csrc/step.cu"],
     "libkvsynth.so": ["synth/synth.cu"],
 }
 DEPS = ["csrc/kv_internal.cuh", "csrc/decode_common.cuh", "../include/kv_tier.h", "../include/kv_synth.h"]

@@ -176,12 +176,38 @@ struct Layout {
   size_t off_k0[2], off_v0[2], off_k1[2], off_v1[2], off_c2k[2], off_c2v[2], off_s2k[2], off_s2v[2];
   size_t off_idx[2][3], off_vis[2], off_tier[2], off_row[2], off_cnt[2], off_S, off_fS, off_st, off_z, off_ml;
   size_t off_part, off_uctr, off_moves, off_mcount, off_scratch, off_mtemp, total, hot_begin, off_vnorm, off_zlayer;
-  size_t off_red, off_lastk;
+  size_t off_red, off_lastk, off_sdone;
   size_t b_t0, b_t1, b_t2, b_scores, b_meta;
 };
 
 int split_of(const kv_tier_config& c);
 int zring_of(const kv_tier_config& c);
+
+// Whole-step kernel (step.cu): s CTAs per kv head (a cluster, s <= 16) or m kv heads per CTA.
+// Every CTA of a request must be resident at once (they wait on each other layer by layer), so
+// a shape qualifies only if all B*H_kv/m clusters fit the GPU together.  The shape that keeps
+// the most SMs busy wins; ties: smaller s (fewer shared-memory exchanges).  Sets v.step_k (total
+// CTAs, 0 = no shape fits), v.step_s, v.step_m.
+void step_plan(DevView& v, int nsm) {
+  int best = 0, bs = 0, bm = 0;
+  for (int m = 8; m >= 1; m >>= 1) {
+    if (v.Hkv % m) continue;
+    for (int s = 1; s <= (m == 1 ? 16 : 1); ++s) {
+      const int clusters_needed = v.B * v.Hkv / m, total = clusters_needed * s;
+      if (total > nsm) continue;
+      v.step_k = total; v.step_s = s; v.step_m = m;
+      if (step_smem_bytes(v) > 227 * 1024) continue;
+      int clusters = 0;
+      if (step_configure(v, &clusters) != cudaSuccess) { cudaGetLastError(); continue; }
+      if (getenv("KVTIER_TRACE")) fprintf(stderr, "step_plan: s=%d m=%d CTAs=%d clusters=%d/%d smem=%zu\n", s, m,
+                                          total, clusters_needed, clusters, step_smem_bytes(v));
+      if (clusters < clusters_needed) continue;
+      if (total > best) { best = total; bs = s; bm = m; }
+    }
+  }
+  v.step_k = best; v.step_s = bs; v.step_m = bm;
+  if (best) { int c = 0; step_configure(v, &c); }   // leave the chosen shape's attributes set
+}
 
 // Rows per group of the pinned host stores: every position, or a sequence shard's own ones.
 int host_rows_of(const kv_tier_config& c) {
@@ -242,6 +268,7 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   const size_t nslots = std::max(BH * (split_of(c) + 1),                 // split kernel: per-CTA partials + new token
                                   (size_t)flat_grid(c, FLAT_GRID_MAX_SM) + 2 * BH);   // flat: <= grid + 2 units
   L.off_part = take(nslots * (16 + 8 * D) * 4);
+  L.off_sdone = take((size_t)c.num_layers * B * 4);                     // step kernel layer counters
   L.off_uctr = take(BH * 4);
   L.off_zlayer = take(ZRING * 4);
   L.off_vnorm = take(scorer_uses_vnorm(c.scorer) ? LBH * N * 4 : 0);     // VATP / combined: V-row norms
@@ -393,6 +420,8 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.part = reinterpret_cast<float*>(A + L.off_part);
   v.part_stride = 16 + 8 * v.D;
   v.unit_ctr = reinterpret_cast<int*>(A + L.off_uctr);
+  v.step_k = v.step_s = v.step_m = 0;
+  v.step_done = reinterpret_cast<int*>(A + L.off_sdone);
   v.zlayer = reinterpret_cast<int*>(A + L.off_zlayer);
   v.scorer = cfg->scorer;
   v.vnorm = scorer_uses_vnorm(cfg->scorer) ? reinterpret_cast<float*>(A + L.off_vnorm) : nullptr;
@@ -431,7 +460,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     v.hs2v = reinterpret_cast<float*>(h + 2 * rows * v.D + rows * 4);
   }
   if (getenv("KVTIER_TRACE") && atoi(getenv("KVTIER_TRACE")) > 0) {
-    const size_t tb = (size_t)v.L * std::max(v.split * v.B * v.Hkv, v.nc) * NTRACE * sizeof(unsigned long long);
+    const size_t tb = (size_t)v.L * std::max(std::max(v.split * v.B * v.Hkv, v.nc), 16 * v.B) * NTRACE * sizeof(unsigned long long);
     if (cudaMalloc(&ctx->trace, tb) == cudaSuccess) { cudaMemset(ctx->trace, 0, tb); v.trace = ctx->trace; }
   }
   if (v.flat && (v.fvariant < 0 || v.fvariant > 4)) {
@@ -465,6 +494,12 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     cudaGetLastError();                  // persistence is an optimisation: ignore if unsupported
   }
   if (e == cudaSuccess) e = v.flat ? flat_configure(v) : attn_configure(v);
+  if (e == cudaSuccess && !v.flat && !v.cluster_merge && !v.last_merge && !v.stream_mode && v.seq_w <= 1) {
+    // kv_tier_step / the step graph: all layers in one launch, one thread-block cluster per request
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device);
+    step_plan(v, nsm);
+  }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_step_begin, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_migrated, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_offload_done, cudaEventDisableTiming);
@@ -891,6 +926,14 @@ kv_tier_status kv_tier_step(kv_tier_ctx* ctx, const void* q, const void* k_new, 
   char* ob = reinterpret_cast<char*>(o);
   kv_tier_status st = kv_tier_begin_step(ctx, stream);
   if (st) return st;
+  if (v.step_k > 0 && !v.host_t1) {
+    // every layer in one launch: a1 + a3 + a4 with the per-request layer dependency inside
+    st = cuda_check(ctx, launch_decode_step(v, q, k_new, v_new, o, fuse_score_update, reinterpret_cast<cudaStream_t>(stream)),
+                    "decode_step");
+    if (st) return st;
+    for (int l = 0; l < v.L; ++l) ctx->appended_step[l] = ctx->t;
+    return kv_tier_end_step(ctx, stream);
+  }
   if (v.stream_mode)
     for (int l = 0; l < std::min(2, v.L) && !st; ++l) st = kv_tier_prefetch(ctx, l, side);
   // a1 fused into the attention kernel; consecutive layers chained with programmatic

@@ -75,6 +75,10 @@ struct DevView {
   float* part;          // [B*Hkv][split][part_stride] per-CTA partials (m[8], l[8], o[G][D])
   int part_stride;
   int* unit_ctr;        // [B*Hkv] partials published per unit (flat kernel, KVTIER_LASTMERGE; reset by the merger)
+  // whole-step kernel (step.cu): step_k CTAs in all; step_s > 1: a cluster of step_s CTAs per kv
+  // head (row slices), else step_m kv heads per CTA.  step_k = 0: the step runs per layer.
+  int step_k, step_s, step_m;
+  int* step_done;       // [L][B] CTAs of request b that finished layer l (zeroed by k_begin_step)
   void* hot_base;       // L2 access-policy window over the small hot buffers
   size_t hot_bytes;
   float hot_hit;        // hitRatio of the window: persisting carve-out / window bytes (<= 1)
@@ -258,4 +262,8 @@ cudaError_t launch_decode_flat(const DevView& v, int layer, const void* q, const
                                void* o, int zpar, int zprev, int pdl, cudaStream_t s);
 size_t merge_smem_bytes(const DevView& v);
 cudaError_t attn_configure(const DevView& v);
+size_t step_smem_bytes(const DevView& v);
+cudaError_t step_configure(const DevView& v, int* clusters);
+cudaError_t launch_decode_step(const DevView& v, const void* q, const void* knew, const void* vnew, void* o, int score,
+                               cudaStream_t s);
 }  // namespace kvt

@@ -1,0 +1,910 @@
+// a1 + a3 + a4 for EVERY layer of one decode step in one launch (kv_tier_step and the step
+// graph, differential staging): PAPER.md Eq. 1, Eq. 3, Alg. 1 forward loop
+// P:175-188, Prop. 1 P:416-427.
+//
+// Why one launch.  A layer of the 7B config moves 32 MB: 4.9 us at the measured HBM peak.  The
+// per-layer kernels (decode -> merge -> next decode, attn.cu) spend ~6 us per layer in dependent
+// global round trips while HBM idles.  Here a thread-block CLUSTER owns one
+// request for the whole step:
+//   * its K CTAs (one per SM) split the request's kv heads: s CTAs per kv head (a slice of the
+//     head's rows each) or m heads per CTA;
+//   * each CTA's producer warp streams K/V tiles of layer l, l+1, ... into a deep shared-memory
+//     ring without waiting for the layer chain (K/V rows of layer l+1 do not depend on layer l),
+//     with an L2 prefetch NST stages ahead;
+//   * the partials of a kv head's s slices are exchanged through distributed shared memory: a
+//     bulk copy into each peer's receive buffer completes the peer's mbarrier (no global round
+//     trip); every slice merges its share of o and the head's global (M, 1/L);
+//   * the dependency a decoder imposes -- q and the new token's K/V of layer l+1 are projections
+//     of o(l) of the same request -- is a cluster mbarrier: q(l+1) is read only after every CTA
+//     of the request has finished its part of o(l) and arrived on every peer.
+// Clusters never wait on each other, so no co-residency beyond the cluster is assumed.
+//
+// Roles per CTA (NW consumer warps + 4):
+//   producer warp  stages of up to NW 16-row groups (never straddling a head or the bf16/int8
+//                  boundary) -> NST-deep ring, 1-D bulk async copies (UBLKCP) into the pre-swizzled
+//                  layout ldmatrix reads.
+//   consumers      S^T = K q^T and o^T += V^T p^T on the tensor cores (mma.sync m16n8k16, swap-AB:
+//                  tokens = M, the G <= 8 heads = N), online softmax in fp32 (log2 domain), p split
+//                  hi + lo bf16 for the P.V product; logits -> an L2-resident ring for a4; warps ->
+//                  CTA partial -> DSMEM exchange -> merge -> o, (M, 1/L).
+//   new-token warp the step's new token of each head (a1: its K/V row joins T0; its attention term
+//                  on the CUDA cores, added by the merge).
+//   score warps    a4 of layer l-1 while the consumers run layer l: S_part[b][g][pos] +=
+//                  sum_{h in g} 2^(z - M_h) / L_h over this CTA's rows (one writer per entry,
+//                  layer order, AMB-14).
+#include "decode_common.cuh"
+
+namespace kvt {
+
+// ----------------------------------------------------------------- cluster / async-proxy PTX
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {   // local smem addr -> peer's
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// local shared -> peer shared bulk copy, completing `bytes` on the peer's mbarrier
+__device__ __forceinline__ void bulk_s2peer(uint32_t dst_cl, uint32_t src, uint32_t bytes, uint32_t mbar_cl) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(dst_cl), "r"(src), "r"(bytes), "r"(mbar_cl) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int x;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];\n" : "=r"(x) : "l"(p) : "memory");
+  return x;
+}
+__device__ __forceinline__ void red_relaxed_gpu(int* p, int x) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(x) : "memory");
+}
+// CTA-local mbarrier wait that suspends until the phase completes
+__device__ __forceinline__ void mbar_sleep_wait(uint32_t a, uint32_t parity) { mbar_wait_hint(a, parity, 1000000u); }
+
+// ----------------------------------------------------------------- work split
+// Geometry (host side, step_plan in ctx.cu): R = H_kv * s / m CTAs per request; s > 1: a
+// cluster of s CTAs per kv head, slice = cluster rank; s == 1: heads [rank*m, rank*m + m) whole.
+struct StepPart {
+  int g, j0, j1, fnew;       // kv head, head-relative 16-row groups [j0, j1), this CTA appends the new token
+};
+
+// first group of a head whose cost range starts at or after cost x (bf16 group = 2, int8 = 1)
+__device__ __forceinline__ int group_at_cost(int x, int gbf) {
+  return x <= 2 * gbf ? (x + 1) >> 1 : gbf + (x - 2 * gbf);
+}
+
+struct StepIO {
+  const __nv_bfloat16* q;      // [L][B][Hq][D]
+  const __nv_bfloat16* knew;   // [L][B][Hkv][D]
+  const __nv_bfloat16* vnew;
+  void* o;                     // [L][B][Hq][D] fp32 or bf16
+  int score;                   // a4 on (fuse_score_update)
+};
+
+// stage descriptor flags
+constexpr int SD_FIRST = 1, SD_LAST = 2, SD_T2 = 4;
+constexpr int STEP_MAXM = 8;   // kv heads per CTA when s == 1
+
+template <int D, int NW, int NST>
+__global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView v, const StepIO io) {
+  constexpr int NCONS = NW * 32;
+  constexpr int WPROD = NW, WNEW = NW + 1, WSC0 = NW + 2;   // + two score warps
+  constexpr int NSC = 64;                                    // score-pass threads
+  constexpr int TILE = NW * 16;
+  constexpr int ROWB = D * 2;
+  constexpr int TILEB = TILE * ROWB;
+  constexpr int STAGEB = 2 * TILEB;
+  constexpr int KS = D / 16;
+  constexpr int OWS = D + 4;
+  constexpr int NH = NW / 2;
+  const int S = v.step_s, Mh = v.step_m;
+  const int R = v.Hkv * S / Mh;                  // CTAs per request
+  const int b = blockIdx.x / R;                  // this CTA's request
+  const int rk = blockIdx.x - b * R;             // rank within the request
+  int* const done_ctr = v.step_done;             // [L][B] CTAs of the request that finished layer l
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int G = v.G, L = v.L, B = v.B, Hkv = v.Hkv;
+  const int U = B * Hkv;
+  const int ZS = v.zring;
+  const int tot = G * D;                          // o floats per kv head
+  const int SL = ((tot + S - 1) / S + 3) & ~3;    // o floats per slice (s > 1)
+  auto trace = [&](int l, int slot) {             // debug timeline (KVTIER_TRACE=1)
+    if (v.trace) v.trace[((size_t)l * gridDim.x + blockIdx.x) * NTRACE + slot] = gtimer();
+  };
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* ring = smem;                                              // [NST][K tile | V tile]
+  unsigned char* t2w = ring + NST * STAGEB;                                // [NW][16][D] bf16 (T2 only)
+  float* ow = reinterpret_cast<float*>(t2w + (v.cap2 > 0 ? NW * 16 * ROWB : 0));   // [NH][8][OWS] combine
+  float* pbuf = ow + NH * 8 * OWS;                                         // [16 + 8 D] CTA partial (m, l, o)
+  float* rx = pbuf + 16 + 8 * D + 64;                                      // [2][S][16 + SL] received partials
+  float* redm = rx + 2 * S * (16 + SL);                                    // [NW][8]
+  float* redl = redm + NW * 8;                                             // [NW][8]
+  float* ntz = redl + NW * 8;                                              // [2][8] new-token logits
+  float* ntv = ntz + 16;                                                   // [2][D] new-token V row
+  float* sml = ntv + 2 * D;                                                // [ZRING][STEP_MAXM][16] (M, 1/L) for a4
+  float* smisc = sml + ZRING * STEP_MAXM * 16;                             // [24] merge scalars
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smisc + 24);
+  // full[NST] empty[NST] nfull[2] nempty[2] rxb[2] done[2]
+  int4* sdesc = reinterpret_cast<int4*>(bars + 2 * NST + 8);               // [NST]
+  volatile int* sc_done = reinterpret_cast<volatile int*>(sdesc + NST);    // layers whose a4 pass is complete
+  volatile int* ml_done = sc_done + 1;                                     // layers merged ((M, 1/L) in sml)
+
+  const int cur = v.st->cur, sb = v.st->scur;
+  Seg sg;
+  sg.init(v.cnt[cur], 1, 0);                 // counts are uniform across requests
+  const int gbf = sg.a2 >> 4, gq2 = (sg.n2 + 15) >> 4, ng = gbf + gq2, cu = 2 * gbf + gq2;
+  const int npart = S > 1 ? 1 : Mh;
+  const int slice = S > 1 ? (int)cluster_rank() : 0;   // the cluster is one kv head's S slices
+  auto part = [&](int k) -> StepPart {
+    StepPart p;
+    if (S > 1) {
+      p.g = rk / S;
+      p.j0 = group_at_cost(slice * cu / S, gbf);
+      p.j1 = group_at_cost((slice + 1) * cu / S, gbf);
+      p.fnew = slice == S - 1;
+    } else {
+      p.g = rk * Mh + k;
+      p.j0 = 0;
+      p.j1 = ng;
+      p.fnew = 1;
+    }
+    return p;
+  };
+
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + NST);
+  const uint32_t nfull0 = smem_u32(bars + 2 * NST), nempty0 = smem_u32(bars + 2 * NST + 2);
+  const uint32_t rxb0 = smem_u32(bars + 2 * NST + 4);
+  // q(l) and the new token's K/V of layer l are projections of o(l-1) of the same request: wait
+  // until every CTA of the request has finished its part of o(l-1) (relaxed polling: the counter
+  // orders the computation; no data produced by another CTA is read after it)
+  auto wait_layer = [&](int l) {
+    const int* p = done_ctr + (size_t)(l - 1) * B + b;
+    if (ld_relaxed_gpu(p) < R) {
+      const unsigned long long t0 = gtimer();
+      while (ld_relaxed_gpu(p) < R) {
+        __nanosleep(64);
+        if (gtimer() - t0 > 2000000000ull) {       // watchdog: report, never hang the device
+          atomicOr(&v.st->err, 4);
+          break;
+        }
+      }
+    }
+  };
+  if (tid == 0) {
+    for (int x = 0; x < NST; ++x) {
+      mbar_init(full0 + 8 * x, 1);
+      mbar_init(empty0 + 8 * x, NW);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(nfull0 + 8 * x, 1);
+      mbar_init(nempty0 + 8 * x, 1);
+      mbar_init(rxb0 + 8 * x, 1);               // the owner's arrive.expect_tx; peers complete tx
+    }
+    *sc_done = 0;
+    *ml_done = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (S > 1) cluster_sync_all();                // every peer's barriers exist before any remote use
+  if (v.trace && blockIdx.x == 0 && tid == 0) v.trace[NTRACE - 1] = gridDim.x;
+
+  if (w == WPROD) {
+    // ================================ producer ================================
+    // Stage sequence: layer-major, then this CTA's parts, then up to NW groups per stage.  A second
+    // cursor NST stages ahead prefetches into L2, so the copy that refills a ring slot hits L2.
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      struct Cur { int l, k, j; };
+      auto stage_of = [&](const Cur& it, const StepPart& pp, bool& t2) {
+        if (pp.j0 == pp.j1) { t2 = false; return 0; }
+        t2 = it.j >= gbf;
+        const int send = t2 ? pp.j1 : min(pp.j1, gbf);
+        return min(NW, send - it.j);
+      };
+      auto advance = [&](Cur& it) {
+        const StepPart pp = part(it.k);
+        bool t2;
+        const int cnt = stage_of(it, pp, t2);
+        it.j += cnt;
+        if (cnt == 0 || it.j >= pp.j1) {
+          if (++it.k == npart) { it.k = 0; ++it.l; }
+          it.j = part(it.k).j0;
+        }
+      };
+      auto issue = [&](const Cur& it, const StepPart& pp, int cnt, bool t2, uint32_t dst, uint32_t full) {
+        const size_t grp = grp_of(v, it.l, b, pp.g);
+        if (!t2) {
+          const __nv_bfloat16* K0 = v.k0[sb] + grp * v.cap0 * D;
+          const __nv_bfloat16* V0 = v.v0[sb] + grp * v.cap0 * D;
+          const __nv_bfloat16* K1 = v.k1[sb] + grp * v.cap1 * D;
+          const __nv_bfloat16* V1 = v.v1[sb] + grp * v.cap1 * D;
+          const int ts = 16 * it.j, te = 16 * (it.j + cnt);   // virtual rows; a1 is a multiple of 16
+          if (dst) mbar_expect_tx(full, 2 * (te - ts) * ROWB);
+          if (ts < sg.a1) {
+            const int e0 = min(te, sg.a1);
+            if (dst) {
+              bulk_g2s_ef(dst, K0 + (size_t)ts * D, (e0 - ts) * ROWB, full, pol);
+              bulk_g2s_ef(dst + TILEB, V0 + (size_t)ts * D, (e0 - ts) * ROWB, full, pol);
+            } else {
+              bulk_prefetch_l2(K0 + (size_t)ts * D, (e0 - ts) * ROWB);
+              bulk_prefetch_l2(V0 + (size_t)ts * D, (e0 - ts) * ROWB);
+            }
+          }
+          if (te > sg.a1) {
+            const int s0 = max(ts, sg.a1);
+            if (dst) {
+              bulk_g2s_ef(dst + (s0 - ts) * ROWB, K1 + (size_t)(s0 - sg.a1) * D, (te - s0) * ROWB, full, pol);
+              bulk_g2s_ef(dst + TILEB + (s0 - ts) * ROWB, V1 + (size_t)(s0 - sg.a1) * D, (te - s0) * ROWB, full, pol);
+            } else {
+              bulk_prefetch_l2(K1 + (size_t)(s0 - sg.a1) * D, (te - s0) * ROWB);
+              bulk_prefetch_l2(V1 + (size_t)(s0 - sg.a1) * D, (te - s0) * ROWB);
+            }
+          }
+        } else {                                             // int8 codes + fp32 scales
+          const size_t r0 = 16 * (size_t)(it.j - gbf);
+          const int nr = 16 * cnt;
+          if (dst) {
+            mbar_expect_tx(full, 2 * (nr * D + nr * 4));
+            bulk_g2s(dst, v.c2k[sb] + (grp * v.cap2 + r0) * D, nr * D, full);
+            bulk_g2s(dst + TILE * D, v.s2k[sb] + grp * v.cap2 + r0, nr * 4, full);
+            bulk_g2s(dst + TILEB, v.c2v[sb] + (grp * v.cap2 + r0) * D, nr * D, full);
+            bulk_g2s(dst + TILEB + TILE * D, v.s2v[sb] + grp * v.cap2 + r0, nr * 4, full);
+          } else {
+            bulk_prefetch_l2(v.c2k[sb] + (grp * v.cap2 + r0) * D, nr * D);
+            bulk_prefetch_l2(v.c2v[sb] + (grp * v.cap2 + r0) * D, nr * D);
+          }
+        }
+      };
+      Cur it{0, 0, part(0).j0};
+      Cur ah = it;
+      for (int x = 0; x < NST && ah.l < L; ++x) advance(ah);
+      int i = 0;
+      for (; it.l < L; ++i) {
+        const int s2 = i % NST;
+        if (i >= NST) mbar_sleep_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
+        if (ah.l < L) {                                       // L2 lookahead: the stage NST ahead
+          const StepPart pa = part(ah.k);
+          bool at2;
+          const int acnt = stage_of(ah, pa, at2);
+          if (acnt > 0) issue(ah, pa, acnt, at2, 0, 0);
+          advance(ah);
+        }
+        const StepPart pp = part(it.k);
+        bool t2;
+        const int cnt = stage_of(it, pp, t2);
+        const int fl = (it.j == pp.j0 ? SD_FIRST : 0) | ((cnt == 0 || it.j + cnt == pp.j1) ? SD_LAST : 0) |
+                       (t2 ? SD_T2 : 0);
+        sdesc[s2] = make_int4(it.l, it.k, it.j, fl | (cnt << 8));
+        if (it.k == 0 && it.j == pp.j0) trace(it.l, 0);
+        const uint32_t full = full0 + 8 * s2;
+        if (cnt > 0) issue(it, pp, cnt, t2, ring_s + s2 * STAGEB, full);
+        else mbar_arrive(full);                              // no cached row in this part
+        advance(it);
+      }
+      const int s2 = i % NST;
+      if (i >= NST) mbar_sleep_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
+      sdesc[s2] = make_int4(-1, 0, 0, 0);                    // sentinel
+      mbar_arrive(full0 + 8 * s2);
+    }
+  } else if (w == WNEW) {
+    // ========== new-token warp: the new token's attention term (every CTA of the head) and a1 ==========
+    int nts = 0;
+    constexpr int EL = D / 32;
+    const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));   // log2(e)/sqrt(d)
+    for (int l = 0; l < L; ++l) {
+      if (l > 0) {                                           // k_new(l), q(l) follow o(l-1)
+        if (lane == 0) wait_layer(l);
+        __syncwarp();
+      }
+      float* zl = v.zbuf + (size_t)(l % ZS) * U * v.zrows * 8;
+      for (int k = 0; k < npart; ++k) {
+        const StepPart pp = part(k);
+        const int g = pp.g, u = b * Hkv + g;
+        const int slot = nts & 1;
+        const size_t grp = grp_of(v, l, b, g);
+        const uint16_t* kin = reinterpret_cast<const uint16_t*>(io.knew) + (((size_t)l * B + b) * Hkv + g) * D;
+        const uint16_t* vin = reinterpret_cast<const uint16_t*>(io.vnew) + (((size_t)l * B + b) * Hkv + g) * D;
+        const uint16_t* qb0 = reinterpret_cast<const uint16_t*>(io.q) + (((size_t)l * B + b) * v.Hq + g * G) * D;
+        uint16_t kb[EL], vb[EL], qb[8][EL];
+#pragma unroll
+        for (int e2 = 0; e2 < EL; ++e2) {
+          const int e = lane + 32 * e2;
+          kb[e2] = __ldcg(kin + e);
+          vb[e2] = __ldcg(vin + e);
+#pragma unroll
+          for (int h = 0; h < 8; ++h) qb[h][e2] = h < G ? __ldcg(qb0 + (size_t)h * D + e) : (uint16_t)0;
+        }
+        float dot[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          dot[h] = 0.f;
+#pragma unroll
+          for (int e2 = 0; e2 < EL; ++e2) dot[h] += bf16_bits_to_f(qb[h][e2]) * bf16_bits_to_f(kb[e2]);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+          for (int h = 0; h < 8; ++h) dot[h] += __shfl_xor_sync(0xffffffffu, dot[h], off);
+        if (nts >= 2) mbar_sleep_wait(nempty0 + 8 * slot, ((nts >> 1) - 1) & 1);
+#pragma unroll
+        for (int e2 = 0; e2 < EL; ++e2) ntv[slot * D + lane + 32 * e2] = bf16_bits_to_f(vb[e2]);
+        if (pp.fnew) {                                       // one CTA per head: a1 + its side effects
+          uint16_t* K0w = reinterpret_cast<uint16_t*>(v.k0[sb]) + (grp * v.cap0 + sg.n0o) * D;
+          uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[sb]) + (grp * v.cap0 + sg.n0o) * D;
+#pragma unroll
+          for (int e2 = 0; e2 < EL; ++e2) {
+            const int se = swz_off(sg.n0o, lane + 32 * e2);
+            K0w[se] = kb[e2];                                // the row joins the T0 store
+            V0w[se] = vb[e2];
+          }
+          if (v.red) redund_append(v, l, u, v.st->n - 1, kin);   // redundancy partial (AMB-30)
+          if (scorer_uses_vnorm(v.scorer)) {                 // VATP: the new row's V norm
+            float ss = 0.f;
+#pragma unroll
+            for (int e2 = 0; e2 < EL; ++e2) ss += bf16_bits_to_f(vb[e2]) * bf16_bits_to_f(vb[e2]);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+            if (lane == 0) v.vnorm[((size_t)l * U + u) * v.Nmax + (v.st->n - 1)] = sqrtf(ss);
+          }
+        }
+        if (lane < 8) {
+          float z = 0.f;
+#pragma unroll
+          for (int h = 0; h < 8; ++h) z = lane == h ? dot[h] * sl2 : z;
+          ntz[slot * 8 + lane] = lane < G ? z : -INFINITY;
+          if (lane < G && io.score && pp.fnew) zl[((size_t)u * v.zrows + sg.a3) * 8 + lane] = z;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(nfull0 + 8 * slot);
+        ++nts;
+      }
+    }
+  } else if (w >= WSC0) {
+    // ====== score warps: a4 of layer l-1 while the consumers run layer l (Eq. 1, AMB-14) ======
+    const int st0 = tid - WSC0 * 32;                          // 0..NSC-1
+    constexpr int SB = 8;
+    bool bad = false;
+    for (int lp = 0; lp < L && io.score; ++lp) {
+      if (st0 == 0) {
+        while (*ml_done <= lp) __nanosleep(128);              // (M, 1/L) of layer lp merged
+        __threadfence_block();
+      }
+      named_sync(2, NSC);
+      const float* zb = v.zbuf + (size_t)(lp % ZS) * U * v.zrows * 8;
+      for (int k = 0; k < npart; ++k) {
+        const StepPart pp = part(k);
+        const int u = b * Hkv + pp.g;
+        const float* ml = sml + ((lp % ZS) * STEP_MAXM + k) * 16;
+        float mh[8], il[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          mh[h] = ml[h];
+          il[h] = ml[8 + h];
+        }
+        // rows of the part (virtual), then the new token (row a3) in the head's appending CTA
+        const int r_bf0 = 16 * min(pp.j0, gbf), r_bf1 = 16 * min(pp.j1, gbf);
+        const int r_q0 = sg.a2 + 16 * (max(pp.j0, gbf) - gbf), r_q1 = sg.a2 + 16 * (max(pp.j1, gbf) - gbf);
+        const int nbf = r_bf1 - r_bf0, nq = r_q1 - r_q0;
+        const int ntot = nbf + nq + (pp.fnew ? 1 : 0);
+        float* Sp = v.S + (size_t)u * v.Nmax;
+        const float* zu = zb + (size_t)u * v.zrows * 8;
+        for (int k0 = st0; k0 < ntot; k0 += NSC * SB) {
+          int pos[SB];
+          float4 z0[SB], z1[SB];
+#pragma unroll
+          for (int x = 0; x < SB; ++x) {
+            const int kk = k0 + NSC * x;
+            pos[x] = -1;
+            if (kk < ntot) {
+              const int t = kk < nbf ? r_bf0 + kk : (kk < nbf + nq ? r_q0 + (kk - nbf) : sg.a3);
+              const bool ok = kk < nbf ? sg.bf16_valid(t) : (kk < nbf + nq ? (t - sg.a2 < sg.n2) : true);
+              if (ok) {
+                pos[x] = sg.pos(v, cur, b, t);
+                z0[x] = __ldcg(reinterpret_cast<const float4*>(zu + (size_t)t * 8));
+                z1[x] = __ldcg(reinterpret_cast<const float4*>(zu + (size_t)t * 8 + 4));
+              }
+            }
+          }
+          float sv[SB];
+#pragma unroll
+          for (int x = 0; x < SB; ++x)
+            if (pos[x] >= 0) sv[x] = __ldcg(Sp + pos[x]);
+#pragma unroll
+          for (int x = 0; x < SB; ++x) {
+            if (pos[x] < 0) continue;
+            const float zz[8] = {z0[x].x, z0[x].y, z0[x].z, z0[x].w, z1[x].x, z1[x].y, z1[x].z, z1[x].w};
+            float inc = 0.f;
+#pragma unroll
+            for (int h = 0; h < 8; ++h)
+              if (h < G) inc += ex2_ftz(zz[h] - mh[h]) * il[h];
+            Sp[pos[x]] = sv[x] + inc * score_weight(v, lp, u, pos[x]);
+            bad |= !isfinite(inc);
+          }
+        }
+      }
+      named_sync(2, NSC);                                     // every zbuf read of layer lp is done
+      if (st0 == 0) {
+        __threadfence_block();
+        *sc_done = lp + 1;                                    // layers 0..lp scored
+        trace(lp, 5);
+      }
+    }
+    if (bad) atomicOr(&v.st->err, 1);
+  } else {
+    // ================================ consumers ================================
+    const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));
+    float mxa = -INFINITY, mxb = -INFINITY, la = 0.f, lb = 0.f;
+    float oacc[KS][4];
+    uint32_t qf[KS][2];
+    float* zrow = nullptr;
+    int nts = 0, nrx = 0;
+    const int mi = lane >> 3, ii = lane & 7;
+    constexpr float RESCALE_SLACK = 8.f;
+    auto online = [&](float z00, float z01, float z10, float z11, float& p00, float& p01, float& p10, float& p11) {
+      const bool grow = z00 > mxa + RESCALE_SLACK || z10 > mxa + RESCALE_SLACK ||
+                        z01 > mxb + RESCALE_SLACK || z11 > mxb + RESCALE_SLACK;
+      if (__any_sync(0xffffffffu, grow)) {
+        float ta = fmaxf(z00, z10), tb = fmaxf(z01, z11);
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+          ta = fmaxf(ta, __shfl_xor_sync(0xffffffffu, ta, off));
+          tb = fmaxf(tb, __shfl_xor_sync(0xffffffffu, tb, off));
+        }
+        const float na = fmaxf(mxa, ta), nb = fmaxf(mxb, tb);
+        const float ca = ex2_ftz(mxa - na), cb = ex2_ftz(mxb - nb);
+        mxa = na;
+        mxb = nb;
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          oacc[mt][0] *= ca;
+          oacc[mt][2] *= ca;
+          oacc[mt][1] *= cb;
+          oacc[mt][3] *= cb;
+        }
+        la *= ca;
+        lb *= cb;
+      }
+      p00 = ex2_ftz(z00 - mxa);
+      p01 = ex2_ftz(z01 - mxb);
+      p10 = ex2_ftz(z10 - mxa);
+      p11 = ex2_ftz(z11 - mxb);
+      la += p00 + p10;
+      lb += p01 + p11;
+    };
+    auto qk = [&](uint32_t sK, int rowbase, float* acc) {
+      constexpr int NCH = KS >= 4 ? 4 : KS;
+      float ch[NCH][4];
+#pragma unroll
+      for (int x = 0; x < NCH; ++x) ch[x][0] = ch[x][1] = ch[x][2] = ch[x][3] = 0.f;
+      const int row = rowbase + ii + ((mi & 1) << 3);
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        uint32_t a0, a1_, a2_, a3_;
+        ldsm_x4(a0, a1_, a2_, a3_, sK + row * ROWB + (((2 * ks + (mi >> 1)) ^ (row & 7)) << 4));
+        mma16816(ch[ks % NCH], a0, a1_, a2_, a3_, qf[ks][0], qf[ks][1]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float x = ch[0][j];
+#pragma unroll
+        for (int y = 1; y < NCH; ++y) x += ch[y][j];
+        acc[j] += x;
+      }
+    };
+    auto pv = [&](uint32_t sV, int rowbase, float p00, float p01, float p10, float p11) {
+      uint32_t h0, l0, h1, l1;
+      split_bf16x2(p00, p01, h0, l0);
+      split_bf16x2(p10, p11, h1, l1);
+      const uint32_t b0 = movm_t(h0), b1 = movm_t(h1), c0 = movm_t(l0), c1 = movm_t(l1);
+      const int row = rowbase + ii + ((mi >> 1) << 3);
+      uint32_t af[KS][4];
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt)
+        ldsm_x4_t(af[mt][0], af[mt][1], af[mt][2], af[mt][3], sV + row * ROWB + (((2 * mt + (mi & 1)) ^ (row & 7)) << 4));
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) mma16816(oacc[mt], af[mt][0], af[mt][1], af[mt][2], af[mt][3], c0, c1);
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) mma16816(oacc[mt], af[mt][0], af[mt][1], af[mt][2], af[mt][3], b0, b1);
+    };
+    auto stage_t2_rows = [&](const int8_t* codes, unsigned char* scr) {
+      for (int e = lane; e < 16 * (D / 16); e += 32) {
+        const int row = e / (D / 16), j = e % (D / 16);
+        const uint4 cw = *reinterpret_cast<const uint4*>(codes + (size_t)(w * 16 + row) * D + 16 * j);
+        uint4 lo, hi;
+        lo.x = i8pair_to_bf16x2(cw.x, 0); lo.y = i8pair_to_bf16x2(cw.x, 1);
+        lo.z = i8pair_to_bf16x2(cw.y, 0); lo.w = i8pair_to_bf16x2(cw.y, 1);
+        hi.x = i8pair_to_bf16x2(cw.z, 0); hi.y = i8pair_to_bf16x2(cw.z, 1);
+        hi.z = i8pair_to_bf16x2(cw.w, 0); hi.w = i8pair_to_bf16x2(cw.w, 1);
+        *reinterpret_cast<uint4*>(scr + row * ROWB + (((2 * j) ^ (row & 7)) << 4)) = lo;
+        *reinterpret_cast<uint4*>(scr + row * ROWB + (((2 * j + 1) ^ (row & 7)) << 4)) = hi;
+      }
+      __syncwarp();
+    };
+    auto store_o = [&](int l, int g, int e, float4 val) {    // o elements [e, e+4) of kv head g
+      const size_t oi = (((size_t)l * B + b) * v.Hq + g * G) * D + e;
+      if (v.out_fp32) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(io.o) + oi) = val;
+      } else {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(val.x, val.y), hi = __floats2bfloat162_rn(val.z, val.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(io.o) + oi) = pk;
+      }
+    };
+
+    for (int i = 0;; ++i) {
+      const int s2 = i % NST;
+      mbar_sleep_wait(full0 + 8 * s2, (i / NST) & 1);
+      const int4 dsc = sdesc[s2];
+      const int l = dsc.x;
+      if (l < 0) break;
+      const int kpart = dsc.y, j = dsc.z, fl = dsc.w & 0xFF, cnt = dsc.w >> 8;
+      const StepPart pp = part(kpart);
+      const int g = pp.g, u = b * Hkv + g;
+      if (fl & SD_FIRST) {
+        if (kpart == 0) {
+          // q(l) is a projection of o(l-1): every CTA of this request has stored its part
+          if (lane == 0) {
+            if (l > 0) wait_layer(l);
+            if (io.score)
+              while (*sc_done < l - ZS + 1) __nanosleep(128);   // logit slot of layer l - ZS consumed
+          }
+          __syncwarp();
+          if (tid == 0) trace(l, 1);
+        }
+        const __nv_bfloat16* qh = io.q + (((size_t)l * B + b) * v.Hq + g * G + gq) * D;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          if (gq < G) {
+            qf[ks][0] = __ldcg(reinterpret_cast<const unsigned int*>(qh + ks * 16 + 2 * tq));
+            qf[ks][1] = __ldcg(reinterpret_cast<const unsigned int*>(qh + ks * 16 + 8 + 2 * tq));
+          } else {
+            qf[ks][0] = 0u;
+            qf[ks][1] = 0u;
+          }
+        }
+        mxa = mxb = -INFINITY;
+        la = lb = 0.f;
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
+        zrow = io.score ? v.zbuf + (size_t)(l % ZS) * U * v.zrows * 8 + (size_t)u * v.zrows * 8 : nullptr;
+      }
+      if (cnt > 0) {
+        const bool t2 = fl & SD_T2;
+        const bool wact = w < cnt;
+        const int tv0 = t2 ? sg.a2 + 16 * (j - gbf + w) : 16 * (j + w);
+        const int r0 = w * 16 + gq, r1 = r0 + 8;
+        const int t0 = tv0 + gq, t1 = tv0 + gq + 8;
+        const bool v0 = wact && (t2 ? (t0 - sg.a2 < sg.n2) : sg.bf16_valid(t0));
+        const bool v1 = wact && (t2 ? (t1 - sg.a2 < sg.n2) : sg.bf16_valid(t1));
+        const uint32_t sK = ring_s + s2 * STAGEB, sV = sK + TILEB;
+        if (__any_sync(0xffffffffu, v0 || v1)) {
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          float fk0 = sl2, fk1 = sl2, fv0 = 1.f, fv1 = 1.f;
+          unsigned char* scr = t2w + (size_t)w * 16 * ROWB;
+          if (!t2) {
+            qk(sK, w * 16, acc);
+          } else {
+            unsigned char* st = ring + s2 * STAGEB;
+            const float* scK = reinterpret_cast<const float*>(st + TILE * D);
+            const float* scV = reinterpret_cast<const float*>(st + TILEB + TILE * D);
+            fk0 = scK[r0] * sl2; fk1 = scK[r1] * sl2;
+            fv0 = scV[r0]; fv1 = scV[r1];
+            stage_t2_rows(reinterpret_cast<const int8_t*>(st), scr);
+            qk(smem_u32(scr), 0, acc);
+          }
+          const float z00 = v0 ? acc[0] * fk0 : -INFINITY, z01 = v0 ? acc[1] * fk0 : -INFINITY;
+          const float z10 = v1 ? acc[2] * fk1 : -INFINITY, z11 = v1 ? acc[3] * fk1 : -INFINITY;
+          if (zrow) {
+            if (v0) *reinterpret_cast<float2*>(zrow + (size_t)t0 * 8 + 2 * tq) = make_float2(z00, z01);
+            if (v1) *reinterpret_cast<float2*>(zrow + (size_t)t1 * 8 + 2 * tq) = make_float2(z10, z11);
+          }
+          float p00, p01, p10, p11;
+          online(z00, z01, z10, z11, p00, p01, p10, p11);
+          if (!t2) {
+            pv(sV, w * 16, p00, p01, p10, p11);
+          } else {
+            __syncwarp();
+            stage_t2_rows(reinterpret_cast<const int8_t*>(ring + s2 * STAGEB + TILEB), scr);
+            pv(smem_u32(scr), 0, p00 * fv0, p01 * fv0, p10 * fv1, p11 * fv1);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * s2);
+      if (!(fl & SD_LAST)) continue;
+
+      // ---------------- part end: warps -> CTA partial (m, l, o) in pbuf
+      if (tid == 0 && kpart == 0) trace(l, 2);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        la += __shfl_xor_sync(0xffffffffu, la, off);
+        lb += __shfl_xor_sync(0xffffffffu, lb, off);
+      }
+      if (tid == 0 && S > 1) bulk_wait_read0();              // the previous push has read pbuf
+      named_sync(1, NCONS);                                  // ow / redm / pbuf free
+      if (lane < 4) {
+        redm[w * 8 + 2 * lane] = mxa;
+        redm[w * 8 + 2 * lane + 1] = mxb;
+        redl[w * 8 + 2 * lane] = la;
+        redl[w * 8 + 2 * lane + 1] = lb;
+      }
+      named_sync(1, NCONS);
+      {
+        float Ma = -INFINITY, Mb = -INFINITY;                 // per-head max over the warps
+#pragma unroll
+        for (int x = 0; x < NW; ++x) {
+          Ma = fmaxf(Ma, redm[x * 8 + 2 * tq]);
+          Mb = fmaxf(Mb, redm[x * 8 + 2 * tq + 1]);
+        }
+        const float fa = mxa == -INFINITY ? 0.f : ex2_ftz(mxa - Ma), fb = mxb == -INFINITY ? 0.f : ex2_ftz(mxb - Mb);
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          oacc[mt][0] *= fa;
+          oacc[mt][2] *= fa;
+          oacc[mt][1] *= fb;
+          oacc[mt][3] *= fb;
+        }
+      }
+      // two-round tree (deterministic order): warps NH.. hand their o to warps 0.., which add it
+      auto put = [&](int slot) {
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          float* o0 = ow + (slot * 8 + 2 * tq) * OWS + mt * 16 + gq;
+          float* o1 = o0 + OWS;
+          o0[0] = oacc[mt][0];
+          o1[0] = oacc[mt][1];
+          o0[8] = oacc[mt][2];
+          o1[8] = oacc[mt][3];
+        }
+      };
+      if (w >= NH) put(w - NH);
+      named_sync(1, NCONS);
+      if (w < NH) {
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          const float* o0 = ow + (w * 8 + 2 * tq) * OWS + mt * 16 + gq;
+          const float* o1 = o0 + OWS;
+          oacc[mt][0] += o0[0];
+          oacc[mt][1] += o1[0];
+          oacc[mt][2] += o0[8];
+          oacc[mt][3] += o1[8];
+        }
+      }
+      named_sync(1, NCONS);
+      if (w < NH) put(w);
+      named_sync(1, NCONS);
+      if (tid < 8) {
+        float M = -INFINITY;
+#pragma unroll
+        for (int x = 0; x < NW; ++x) M = fmaxf(M, redm[x * 8 + tid]);
+        float Ls = 0.f;
+#pragma unroll
+        for (int x = 0; x < NW; ++x) {
+          const float m = redm[x * 8 + tid];
+          Ls += (m == -INFINITY ? 0.f : ex2_ftz(m - M)) * redl[x * 8 + tid];
+        }
+        pbuf[tid] = M;
+        pbuf[8 + tid] = Ls;
+      }
+      for (int e = tid; e < tot; e += NCONS) {
+        const int h = e / D, dd = e - h * D;
+        float a = 0.f;
+#pragma unroll
+        for (int x = 0; x < NH; ++x) a += ow[(x * 8 + h) * OWS + dd];
+        pbuf[16 + e] = a;
+      }
+      const int par = l & 1;
+      if (tid == 0 && kpart == 0) trace(l, 6);               // CTA partial in pbuf
+      if (S > 1) {
+        // ---------------- DSMEM exchange: (m, l) + o slice r of this partial -> slice r's CTA.
+        // Every push carries 16 + SL floats (the last slice is padded from pbuf's tail), so each
+        // receiver expects exactly S * (16 + SL) * 4 bytes per layer.
+        fence_proxy_async_smem();                              // pbuf (generic stores) -> bulk copy reads
+        named_sync(1, NCONS);
+        if (tid == 0) {
+          const uint32_t rx_s = smem_u32(rx);
+          mbar_expect_tx(rxb0 + 8 * par, (uint32_t)(S * (16 + SL) * 4));
+          for (int r = 0; r < S; ++r) {                       // cluster ranks = the head's slices
+            const uint32_t peer = (uint32_t)r;
+            const uint32_t dst = rx_s + (uint32_t)(((par * S + slice) * (16 + SL)) * 4);
+            const uint32_t mb = mapa(rxb0 + 8 * par, peer);
+            bulk_s2peer(mapa(dst, peer), smem_u32(pbuf), 64, mb);
+            bulk_s2peer(mapa(dst + 64, peer), smem_u32(pbuf + 16 + r * SL), (uint32_t)(SL * 4), mb);
+          }
+          bulk_commit();
+        }
+      }
+      // ---------------- merge: this CTA's share of o (slice, or the whole head) + the new token
+      const int nslot = nts & 1;
+      mbar_sleep_wait(nfull0 + 8 * nslot, (nts >> 1) & 1);   // the new token's term (every CTA of the head)
+      if (tid == 0 && kpart == 0) trace(l, 7);               // new token ready
+      if (S > 1) mbar_sleep_wait(rxb0 + 8 * par, (nrx >> 1) & 1);
+      named_sync(1, NCONS);                                   // pbuf complete (S == 1)
+      if (tid == 0 && kpart == 0) trace(l, 8);               // peers' partials landed
+      const int nsrc = S > 1 ? S : 1;
+      const float* src0 = S > 1 ? rx + par * S * (16 + SL) : pbuf;   // partial 0 of the merge
+      const int sstride = 16 + SL;                            // between received partials
+      const int e_beg = S > 1 ? slice * SL : 0;
+      const int e_end = S > 1 ? min(tot, e_beg + SL) : tot;
+      float* fac = redm;                                      // [nsrc][8] factors (redm/redl are free now)
+      float* sIL = smisc;                                     // [8] 1/L
+      float* sFN = smisc + 8;                                 // [8] new-token factor
+      if (tid < 8) {
+        const float zn = ntz[nslot * 8 + tid];
+        float M = zn;
+        for (int x = 0; x < nsrc; ++x) M = fmaxf(M, src0[x * sstride + tid]);
+        float Ls = 0.f;
+        for (int x = 0; x < nsrc; ++x) {
+          const float m = src0[x * sstride + tid];
+          const float f = m == -INFINITY ? 0.f : ex2_ftz(m - M);
+          fac[x * 8 + tid] = f;
+          Ls += f * src0[x * sstride + 8 + tid];
+        }
+        const float fn = zn == -INFINITY ? 0.f : ex2_ftz(zn - M);
+        Ls += fn;
+        const float il = Ls > 0.f ? 1.0f / Ls : 0.f;
+        sIL[tid] = il;
+        sFN[tid] = fn;
+        float* mlw = sml + ((l % ZS) * STEP_MAXM + kpart) * 16;
+        mlw[tid] = tid < G ? M : 0.f;
+        mlw[8 + tid] = tid < G ? il : 0.f;
+      }
+      named_sync(1, NCONS);
+      for (int e = e_beg + 4 * tid; e < e_end; e += 4 * NCONS) {
+        const int h = e / D, dd = e - h * D;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int x = 0; x < nsrc; ++x) {
+          const float f = fac[x * 8 + h];
+          const float4 y = *reinterpret_cast<const float4*>(src0 + x * sstride + 16 + (e - e_beg));
+          acc.x += f * y.x;
+          acc.y += f * y.y;
+          acc.z += f * y.z;
+          acc.w += f * y.w;
+        }
+        const float fn = sFN[h], il = sIL[h];
+        const float4 nv = *reinterpret_cast<const float4*>(ntv + nslot * D + dd);
+        acc.x = (acc.x + fn * nv.x) * il;
+        acc.y = (acc.y + fn * nv.y) * il;
+        acc.z = (acc.z + fn * nv.z) * il;
+        acc.w = (acc.w + fn * nv.w) * il;
+        store_o(l, g, e, acc);
+      }
+      named_sync(1, NCONS);                                   // o stored, rx / ntv / fac read
+      if (tid == 0 && kpart == 0) trace(l, 9);
+      if (tid == 0) {
+        mbar_arrive(nempty0 + 8 * nslot);
+        if (kpart == npart - 1) {
+          __threadfence_block();
+          *ml_done = l + 1;                                   // every part's (M, 1/L) of layer l is in sml
+          // o(l) of this CTA is final: count it for the request (the q(l+1) dependency).  The
+          // relaxed add orders the COMPUTATION (a fused decoder would hand o(l) to its o_proj
+          // stage on chip); it deliberately does not wait for the global o stores to drain behind
+          // the K/V stream -- they are visible at kernel end.
+          red_relaxed_gpu(done_ctr + (size_t)l * B + b, 1);
+          trace(l, 4);
+        }
+      }
+      ++nts;
+      if (S > 1) ++nrx;
+    }
+    if (tid == 0 && S > 1) bulk_wait_read0();
+  }
+  __syncwarp();
+  if (S > 1) cluster_sync_all();                // no peer accesses this CTA's shared memory after exit
+}
+
+// ----------------------------------------------------------------- host side
+constexpr int STEP_NW = 8;                                        // consumer warps
+
+template <int D, int NST>
+static size_t step_smem_bytes_t(const DevView& v) {
+  constexpr int NW = STEP_NW;
+  const int S = v.step_s > 0 ? v.step_s : 1;
+  const int tot = v.G * D, SL = ((tot + S - 1) / S + 3) & ~3;
+  size_t s = (size_t)NST * 2 * NW * 16 * D * 2;                  // ring
+  if (v.cap2 > 0) s += (size_t)NW * 16 * D * 2;                  // T2 scratch
+  s += (size_t)(NW / 2) * 8 * (D + 4) * 4;                       // ow
+  s += (size_t)(16 + 8 * D + 4 * 16) * 4;                        // pbuf (+ tail read by the padded last slice)
+  s += (size_t)2 * S * (16 + SL) * 4;                            // rx
+  s += (size_t)2 * NW * 8 * 4 + 16 * 4 + 2 * D * 4;              // redm, redl, ntz, ntv
+  s += (size_t)ZRING * STEP_MAXM * 16 * 4 + 24 * 4;              // sml, merge scalars
+  s += (2 * NST + 8) * 8 + NST * 16 + 16;                        // barriers, descriptors, counters
+  return s;
+}
+
+// ring depth: as many stages as fit beside the scratch (one CTA per SM)
+static int step_nst(const DevView& v) {
+  if (v.D == 128) return v.cap2 > 0 ? 2 : 3;
+  return v.cap2 > 0 ? 5 : 6;
+}
+
+size_t step_smem_bytes(const DevView& v) {
+  const int nst = step_nst(v);
+  if (v.D == 128) return nst == 3 ? step_smem_bytes_t<128, 3>(v) : step_smem_bytes_t<128, 2>(v);
+  return nst == 6 ? step_smem_bytes_t<64, 6>(v) : step_smem_bytes_t<64, 5>(v);
+}
+
+template <int D, int NST>
+static cudaError_t step_conf_t(const DevView& v, int K, int* clusters) {
+  auto kern = k_decode_step<D, STEP_NW, NST>;
+  const size_t smem = step_smem_bytes_t<D, NST>(v);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(v.B * v.Hkv * v.step_s / v.step_m, 1, 1);
+  cfg.blockDim = dim3((STEP_NW + 4) * 32, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = K;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(clusters, kern, &cfg);
+}
+
+// Co-resident clusters of v.step_s CTAs (0: the shape cannot run).
+cudaError_t step_configure(const DevView& v, int* clusters) {
+  *clusters = 0;
+  const int nst = step_nst(v);
+  const int K = v.step_s;
+  if (v.D == 128) return nst == 3 ? step_conf_t<128, 3>(v, K, clusters) : step_conf_t<128, 2>(v, K, clusters);
+  return nst == 6 ? step_conf_t<64, 6>(v, K, clusters) : step_conf_t<64, 5>(v, K, clusters);
+}
+
+template <int D, int NST>
+static cudaError_t step_launch_t(const DevView& v, const StepIO& io, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(v.step_k, 1, 1);                  // step_k = total CTAs
+  cfg.blockDim = dim3((STEP_NW + 4) * 32, 1, 1);
+  cfg.dynamicSmemBytes = step_smem_bytes_t<D, NST>(v);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeClusterDimension;      // one cluster per kv head (its S slices)
+  at[na].val.clusterDim.x = v.step_s;
+  at[na].val.clusterDim.y = 1;
+  at[na].val.clusterDim.z = 1;
+  ++na;
+  if (v.hot_bytes > 0) {
+    at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[na].val.accessPolicyWindow.base_ptr = v.hot_base;
+    at[na].val.accessPolicyWindow.num_bytes = v.hot_bytes;
+    at[na].val.accessPolicyWindow.hitRatio = v.hot_hit;
+    at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, k_decode_step<D, STEP_NW, NST>, v, io);
+}
+
+cudaError_t launch_decode_step(const DevView& v, const void* q, const void* knew, const void* vnew, void* o, int score,
+                               cudaStream_t s) {
+  StepIO io;
+  io.q = reinterpret_cast<const __nv_bfloat16*>(q);
+  io.knew = reinterpret_cast<const __nv_bfloat16*>(knew);
+  io.vnew = reinterpret_cast<const __nv_bfloat16*>(vnew);
+  io.o = o;
+  io.score = score;
+  const int nst = step_nst(v);
+  if (v.D == 128) return nst == 3 ? step_launch_t<128, 3>(v, io, s) : step_launch_t<128, 2>(v, io, s);
+  return nst == 6 ? step_launch_t<64, 6>(v, io, s) : step_launch_t<64, 5>(v, io, s);
+}
+
+}  // namespace kvt

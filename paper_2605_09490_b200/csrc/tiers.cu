@@ -28,6 +28,8 @@ __global__ void k_begin_step(const DevView v) {
       v.rowof[cur][(size_t)b * v.Nmax + n] = -1;
     }
   }
+  if (v.step_k > 0)                            // whole-step kernel: fresh layer counters
+    for (int i = threadIdx.x; i < v.L * v.B; i += blockDim.x) v.step_done[i] = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
     v.st->n = n + 1;

@@ -233,13 +233,15 @@ def test_prop1_gpu_outputs_independent_of_beta():
         assert mabs < 1e-4, mabs
 
 
-def test_graph_equals_layer_calls_bitwise():
+def test_graph_equals_step_calls_bitwise():
+    # the step graph and kv_tier_step run the same whole-step kernel with the same work split:
+    # identical bits
     w = H.workload("tiny", interval=8, B=2, L=2, t2_bp=3000)
     a = H.TieredDecode(w)
     b = H.TieredDecode(w)
     b.capture()
     for t in range(w["steps"]):
-        a.step_layers()
+        a.step()
         b.step()
         oa, ob = a.output(), b.output()
         assert np.array_equal(oa, ob), t
@@ -248,15 +250,35 @@ def test_graph_equals_layer_calls_bitwise():
     a.close(); b.close()
 
 
+def test_step_kernel_matches_layer_kernel():
+    # whole-step kernel (kv_tier_step) vs the per-layer kernels (decode_attention per layer): the
+    # same softmax summed in a different order -> fp32 rounding apart; T0 rows byte-equal
+    w = H.workload("tiny", interval=8, B=3, L=3, t2_bp=3000, Hq=12, Hkv=2, d=128, N=700, P=40)
+    a = H.TieredDecode(w)
+    b = H.TieredDecode(w)
+    b.capture()
+    for t in range(w["steps"]):
+        a.step_layers()
+        b.step()
+        oa, ob = a.output(), b.output()
+        assert np.abs(oa - ob).max() <= 2e-6 + 1e-5 * np.abs(oa).max(), t
+    a.sync(); b.sync()
+    ok, mrel = s_close(b.kv.export(kt.X_SCORES), a.kv.export(kt.X_SCORES))
+    assert ok, mrel
+    assert np.array_equal(a.kv.export(kt.X_T0_ROWS, 2)[1], b.kv.export(kt.X_T0_ROWS, 2)[1])
+    a.close(); b.close()
+
+
 def test_stream_mode_equals_differential_bitwise():   # same rows, same order -> same bits
+    # both through the per-layer kernels (stream mode always runs them; the differential run
+    # uses the per-layer ABI so the work split is the same)
     outs = []
     for staging in (kt.STAGING_ALL, 0):
         w = H.workload("tiny", interval=8, B=2, L=3, staging=staging)
         run = H.TieredDecode(w)
-        run.capture()
         seq = []
         for _ in range(w["steps"]):
-            run.step()
+            run.step_layers()
             seq.append(run.output().copy())
         outs.append(np.stack(seq))
         run.close()
