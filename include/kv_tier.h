@@ -135,7 +135,9 @@ typedef struct {
   int32_t  device;           /* CUDA device ordinal                                   */
   int32_t  rank, world, shard;
   int32_t  out_fp32;         /* 1: o is fp32 [B][H_q][d]; 0: bf16                      */
-  int32_t  split;            /* CTAs per (request, kv head), <= 64; 0 = auto            */
+  int32_t  split;            /* CTAs per (request, kv head), <= 64; 0 = auto.  The
+                                whole-step kernel (kv_tier_step) takes it as its cluster
+                                size when <= 16 and the shape fits, else runs per layer */
   int32_t  variant;          /* decode kernel (consumer warps, stages): 0 (4,3) 1 (4,4)
                                 2 (8,2) 3 (8,3) 4 (4,2) 5 (4,6)                        */
   int32_t  policy;           /* kv_tier_policy (0 = the paper's hierarchy)             */
@@ -264,6 +266,14 @@ KV_TIER_API kv_tier_status kv_tier_host_t1_layer(kv_tier_ctx* ctx, int32_t layer
  * returned by kv_tier_visible_count. */
 KV_TIER_API kv_tier_status kv_tier_score_update(kv_tier_ctx* ctx, int32_t layer, const float* probs, void* stream);
 KV_TIER_API kv_tier_status kv_tier_visible_count(const kv_tier_ctx* ctx, int32_t* n_vis);
+
+/* Tier counts of the current step's layout, per request [|T0|, |T1|, |T2|, |T3|] over positions
+ * [0, n) (the same for every request unless sequence-sharded: then this rank's request 0).  Host
+ * mirror, no device synchronisation (unlike kv_tier_census).  Also reports the step kernel's
+ * work split: shape[0] = CTAs of kv_tier_step's whole-step kernel (0: the step runs layer by
+ * layer), shape[1] = CTAs per kv head (a thread-block cluster), shape[2] = kv heads per CTA,
+ * shape[3] = consumer warps per CTA.  Either pointer may be NULL. */
+KV_TIER_API kv_tier_status kv_tier_layout(const kv_tier_ctx* ctx, int32_t* counts4, int32_t* shape4);
 
 KV_TIER_API kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream);
 

@@ -13,22 +13,29 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-Xcompiler", "-fvisibility=hidden",
          "-Xcompiler", "-fopenmp", "-lgomp"]     # OpenMP: host-T1 attention (N1) on the host cores
-if os.environ.get("KVT_TRACE_LOOP"):        # debug: per-stage wait/busy accounting in the trace
-    FLAGS += ["-DKVT_TRACE_LOOP=1"]
-if os.environ.get("KVT_NO_RED_DECODE"):     # experiment: no redundancy code in the decode kernel
-    FLAGS += ["-DKVT_NO_RED_DECODE=1"]
-if os.environ.get("KVT_FLAT_TRACE"):        # debug: per-unit epilogue timing in the flat kernel's trace
-    FLAGS += ["-DKVT_FLAT_TRACE=1"]
+if os.environ.get("KVT_TRACE"):             # debug builds: per-(layer, CTA) timeline buffer
+    FLAGS += ["-DKVT_TRACE=1"]
 
 TARGETS = {
-    "libkvtier.so": ["csrc/ctx.cu", "csrc/attn.cu", "csrc/attn_flat.cu", "csrc/tiers.cu", "csrc/step.cu"],
+    "libkvtier.so": ["csrc/ctx.cu", "csrc/attn.cu", "csrc/tiers.cu", "csrc/step.cu"],
     "libkvsynth.so": ["synth/synth.cu"],
 }
 DEPS = ["csrc/kv_internal.cuh", "csrc/decode_common.cuh", "../include/kv_tier.h", "../include/kv_synth.h"]
 
 
-def _stale(out, srcs):
+def _stamp(cmd):
+    """The nvcc command without absolute paths (the repo is checked out elsewhere on GPU boxes)."""
+    return " ".join(os.path.relpath(x, HERE) if os.path.isabs(x) and x.startswith(os.path.dirname(HERE)) else x
+                    for x in cmd[1:])
+
+
+def _stale(out, srcs, cmd):
+    """Out of date when missing, older than a source, or built with another nvcc command (the
+    flags stamp next to the library: a debug build never silently stands in for the product)."""
     if not os.path.exists(out):
+        return True
+    stamp = out + ".cmd"
+    if not os.path.exists(stamp) or open(stamp).read() != _stamp(cmd):
         return True
     t = os.path.getmtime(out)
     return any(os.path.getmtime(os.path.join(HERE, s)) > t for s in srcs + DEPS)
@@ -38,12 +45,14 @@ def build(force=False, verbose=False):
     os.makedirs(LIB_DIR, exist_ok=True)
     for name, srcs in TARGETS.items():
         out = os.path.join(LIB_DIR, name)
-        if not force and not _stale(out, srcs):
-            continue
         cmd = [NVCC, *ARCH, *FLAGS, "-o", out, *[os.path.join(HERE, s) for s in srcs]]
+        if not force and not _stale(out, srcs, cmd):
+            continue
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
+        with open(out + ".cmd", "w") as f:
+            f.write(_stamp(cmd))
     return LIB_DIR
 
 

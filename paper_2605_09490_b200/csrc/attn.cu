@@ -10,8 +10,8 @@
 //                   copies (cp.async.bulk) into an NST-deep shared-memory ring guarded by
 //                   full/empty mbarriers.  Rows are stored pre-swizzled in HBM (16-B chunk c of
 //                   store row j at c ^ (j & 7)), so a linear copy is the conflict-free layout.
-//                   Up to pdl_pre stages are issued before griddepcontrol.wait: they overlap
-//                   the previous kernel's tail.
+//                   The whole ring is issued before griddepcontrol.wait: it overlaps the
+//                   previous kernel's tail.
 //   consumer warps  each owns 16 rows of a stage: S^T = K q^T on the tensor cores (mma.sync
 //                   m16n8k16 bf16, swap-AB: tokens = M, the G <= 8 heads of the group = N),
 //                   per-warp online softmax in fp32, o^T += V^T p^T (movmatrix.trans turns the
@@ -19,23 +19,14 @@
 //                   L2-resident buffer for the score update.
 //   side warp       rank 0: appends the new token's K/V row (a1) and computes its attention
 //                   term on the CUDA cores as one more partial (m = z, l = 1, o = v_new).
-//   merge           warps -> CTA partial (m, l, o) in shared memory, then either
-//                   (default) a global partial slot, merged in rank order by the PDL-chained
-//                   k_decode_merge, which also publishes the per-head (M, 1/L); the score update
-//                   (a4) then runs as k_score_flush on the library's score stream;
-//                   or (KVTIER_CLUSTER=1) one thread-block cluster per unit: partials pushed
-//                   over distributed shared memory (rank c receives slice c of o and every
-//                   (m, l)), one cluster barrier, each rank merges its slice in the same order,
-//                   and applies the score update of its own tokens in the epilogue.
+//   merge           warps -> CTA partial (m, l, o) in shared memory -> a global partial slot,
+//                   merged in rank order by the PDL-chained k_decode_merge, which also publishes
+//                   the per-head (M, 1/L); the score update (a4) then runs as k_score_flush on the
+//                   library's score stream.
+// This is the per-layer path (kv_tier_decode_attention[_lse], sequence shards, stream mode,
+// host-T1); kv_tier_step runs every layer in one launch (step.cu).
 //
-#include <cooperative_groups.h>
 #include "decode_common.cuh"
-
-#ifndef KVT_TRACE_LOOP
-#define KVT_TRACE_LOOP 0
-#endif
-
-namespace cg = cooperative_groups;
 
 namespace kvt {
 
@@ -47,95 +38,7 @@ __device__ __forceinline__ int atom_add_acqrel_gpu(int* p, int x) {
   return old;
 }
 
-// KVTIER_LASTMERGE=1: the unit's C partials + the new-token partial are merged by the CTA whose
-// release-add completes the unit's count (no merge kernel, one kernel boundary per layer
-// fewer).  Same arithmetic and order as k_decode_merge.  Called by the NCONS consumer threads
-// after their partial stores; rank 0 first waits (named barrier 3) for its side warp's partial.
-template <int D, int NCONS>
-__device__ __forceinline__ void last_cta_merge(const DevView& v, int unit, int b, int g, int C, int zpar, void* o,
-                                               unsigned char* scratch, int tid, bool rank0) {
-  if (rank0) asm volatile("bar.sync 3, %0;\n" ::"r"(NCONS + 32) : "memory");
-  else named_sync(1, NCONS);
-  float* sf = reinterpret_cast<float*>(scratch);      // [NP][8] m -> factors
-  float* sl = sf + 65 * 8;                            // [NP][8] l
-  float* sI = sl + 65 * 8;                            // [8] 1/L
-  int* sflag = reinterpret_cast<int*>(sI + 8);
-  if (tid == 0) sflag[0] = atom_add_acqrel_gpu(v.unit_ctr + unit, 1) == C - 1;
-  named_sync(1, NCONS);
-  if (!sflag[0]) return;
-  const int G = v.G, NP = C + 1, tot4 = G * D / 4;
-  const float* P = v.part + (size_t)unit * NP * v.part_stride;
-  constexpr int NE = (8 * D / 4 + NCONS - 1) / NCONS, MAXP = 9;
-  float4 x[NE][MAXP];
-#pragma unroll
-  for (int k = 0; k < NE; ++k)
-#pragma unroll
-    for (int c = 0; c < MAXP; ++c)
-      if (c < NP && tid + k * NCONS < tot4)
-        x[k][c] = __ldcg(reinterpret_cast<const float4*>(P + (size_t)c * v.part_stride + 16) + tid + k * NCONS);
-  for (int i = tid; i < NP * 8; i += NCONS) {
-    sf[i] = __ldcg(P + (size_t)(i >> 3) * v.part_stride + (i & 7));
-    sl[i] = __ldcg(P + (size_t)(i >> 3) * v.part_stride + 8 + (i & 7));
-  }
-  named_sync(1, NCONS);
-  if (tid < 8) {
-    const int h = tid;
-    float M = -INFINITY;
-    for (int c = 0; c < NP; ++c) M = fmaxf(M, sf[c * 8 + h]);
-    float Ls = 0.f;
-    for (int c = 0; c < NP; ++c) {
-      const float mc = sf[c * 8 + h];
-      const float f = mc == -INFINITY ? 0.f : ex2_ftz(mc - M);
-      sf[c * 8 + h] = f;
-      Ls += f * sl[c * 8 + h];
-    }
-    const float invL = Ls > 0.f ? 1.0f / Ls : 0.f;
-    sI[h] = invL;
-    if (h < G && zpar >= 0) {
-      float* ml = v.ml + ((size_t)zpar * v.B * v.Hkv + unit) * 16;
-      ml[h] = M;
-      ml[8 + h] = invL;
-    }
-  }
-  named_sync(1, NCONS);
-#pragma unroll
-  for (int k = 0; k < NE; ++k) {
-    const int j = tid + k * NCONS;
-    if (j >= tot4) continue;
-    const int h = (4 * j) / D;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int c0 = 0; c0 < NP; c0 += MAXP) {
-      if (c0 > 0) {
-#pragma unroll
-        for (int c = 0; c < MAXP; ++c)
-          if (c0 + c < NP) x[k][c] = __ldcg(reinterpret_cast<const float4*>(P + (size_t)(c0 + c) * v.part_stride + 16) + j);
-      }
-#pragma unroll
-      for (int c = 0; c < MAXP; ++c)
-        if (c0 + c < NP) {
-          const float f = sf[(c0 + c) * 8 + h];
-          acc.x += f * x[k][c].x;
-          acc.y += f * x[k][c].y;
-          acc.z += f * x[k][c].z;
-          acc.w += f * x[k][c].w;
-        }
-    }
-    const float il = sI[h];
-    const size_t oi = ((size_t)b * v.Hq + g * G) * D + 4 * j;
-    if (v.out_fp32) {
-      *reinterpret_cast<float4*>(reinterpret_cast<float*>(o) + oi) = make_float4(acc.x * il, acc.y * il, acc.z * il, acc.w * il);
-    } else {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * il, acc.y * il), hi = __floats2bfloat162_rn(acc.z * il, acc.w * il);
-      uint2 pk;
-      pk.x = *reinterpret_cast<uint32_t*>(&lo);
-      pk.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o) + oi) = pk;
-    }
-  }
-  if (tid == 0) v.unit_ctr[unit] = 0;                 // next launch touches it after this grid completes
-}
-
-template <int D, int NW, int NST, bool CM>
+template <int D, int NW, int NST>
 __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     k_decode_attn(const DevView v, const int layer, const __nv_bfloat16* __restrict__ q,
                   const __nv_bfloat16* __restrict__ knew, const __nv_bfloat16* __restrict__ vnew,
@@ -165,64 +68,30 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   unsigned long long* bars =
       reinterpret_cast<unsigned long long*>(t2w + (v.cap2 > 0 ? NW * 16 * ROWB : 0));   // full, empty
   int* stile = reinterpret_cast<int*>(bars + 2 * NST);                    // [NST] tile of each stage
-  float* xo = reinterpret_cast<float*>(stile + NST + 4);                 // [8][D] CTA partial o
-  float* xm = xo + 8 * D;                                                 // [8]  exchange: max (log2)
-  float* xl = xm + 8;                                                     // [8]  exchange: sum
-  float* redm = xl + 8;                                                   // [NW][8] warp max
+  float* redm = reinterpret_cast<float*>(stile + NST + 4);               // [NW][8] warp max
   float* redl = redm + 8 * NW;                                            // [NW][8] warp sum
-  float* sML = redl + 8 * NW;                                             // [16] merged M, 1/L
-  float* nrow = sML + 16;                                                 // [2][D] new token K, V
-  float* zn = nrow + 2 * D;                                               // [8] new token logits
-  float* rbuf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(zn + 8) + 15) & ~(uintptr_t)15);
-                                         // cluster merge: [C+1][m 8 | l 8 | o slice] (16-B aligned)
-  const int cm_per = (((v.G * D + C - 1) / C) + 3) & ~3;                  // o floats per rank slice
-  const int cm_rb = cm_per + 16;
-  constexpr bool cm = CM;   // cluster-merge instantiation (KVTIER_CLUSTER=1); the default kernel carries no cluster code
 
   // ---------------------------------------------------------------- prologue (pre-PDL-wait)
   const int cur = v.st->cur;
   Seg sg;
   sg.init(v.cnt[cur] + b * CNT_STRIDE, v.st->nn, v.host_t1);
   // This CTA's work: stages of up to NW 16-row groups (one per consumer warp) from the unit's
-  // groups [bf16 segment [0, a2) | int8 segment [a2, a2 + n2)].  Default (KVTIER_RR=2): the
-  // groups themselves are dealt round-robin over the unit's C CTAs (bf16 then int8, continuing
-  // the deal), so CTAs differ by at most one group; KVTIER_RR=1 deals whole stages, 0 cuts
-  // contiguous stage ranges.  Static in every mode, so the fp32 summation order never depends
-  // on timing.  stage_at(i) -> kind, groups in the stage; group_of(i, w) -> the segment-relative
-  // index of warp w's group.
+  // groups [bf16 segment [0, a2) | int8 segment [a2, a2 + n2)]; whole stages are dealt round-robin
+  // over the unit's C CTAs (static: the fp32 summation order never depends on timing; measured
+  // faster than dealing single groups or cutting contiguous ranges).
+  // stage_at(i) -> kind, groups in the stage; group_of(i, w) -> the segment-relative index of
+  // warp w's group.
   const int gbf = sg.a2 >> 4, gq2 = (sg.n2 + 15) >> 4;
   const int sbf = (gbf + NW - 1) / NW, ns_all = sbf + (gq2 + NW - 1) / NW;
-  const int mode = v.stage_rr;
-  int cs0 = 0, cstr = 1, nstage, nb = 0, nq = 0, q0 = 0, sbr = 0;
-  if (mode == 2) {
-    nb = gbf > r ? (gbf - r + C - 1) / C : 0;              // bf16 groups r, r + C, ...
-    q0 = ((r - gbf) % C + C) % C;                          // int8 groups q0, q0 + C, ...
-    nq = gq2 > q0 ? (gq2 - q0 + C - 1) / C : 0;
-    sbr = (nb + NW - 1) / NW;
-    nstage = sbr + (nq + NW - 1) / NW;
-  } else if (mode == 1) {
-    cs0 = r;
-    cstr = C;
-    nstage = ns_all > r ? (ns_all - r + C - 1) / C : 0;
-  } else {
-    cs0 = (int)((long long)ns_all * r / C);
-    cstr = 1;
-    nstage = (int)((long long)ns_all * (r + 1) / C) - cs0;
-  }
+  const int cs0 = r, cstr = C;
+  const int nstage = ns_all > r ? (ns_all - r + C - 1) / C : 0;
   auto stage_at = [&](int i, bool& t2, int& ng) {          // this CTA's i-th stage
-    if (mode == 2) {
-      t2 = i >= sbr;
-      const int l0 = (t2 ? i - sbr : i) * NW;
-      ng = min(NW, (t2 ? nq : nb) - l0);
-    } else {
-      const int gs = cs0 + i * cstr;
-      t2 = gs >= sbf;
-      const int g0 = (t2 ? gs - sbf : gs) * NW;
-      ng = min(NW, (t2 ? gq2 : gbf) - g0);
-    }
+    const int gs = cs0 + i * cstr;
+    t2 = gs >= sbf;
+    const int g0 = (t2 ? gs - sbf : gs) * NW;
+    ng = min(NW, (t2 ? gq2 : gbf) - g0);
   };
   auto group_of = [&](int i, int wi) {                      // segment-relative group index
-    if (mode == 2) return i >= sbr ? q0 + C * ((i - sbr) * NW + wi) : r + C * (i * NW + wi);
     const int gs = cs0 + i * cstr;
     return (gs >= sbf ? gs - sbf : gs) * NW + wi;
   };
@@ -253,59 +122,19 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  // cluster merge: phase 0 = every CTA of the cluster has started (its shared memory may be
-  // written remotely after the matching wait); phase 1 = every partial has been pushed
-  if (cm) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
 
   if (w == WPROD) {
     // ============================ producer ============================
-    // streams this CTA's stages (static ranges: the fp32 summation order never depends on timing)
+    // streams this CTA's stages (static ranges: the fp32 summation order never depends on timing).
+    // It never waits for the previous kernel: K/V rows of this layer do not depend on it, only
+    // their consumption (q, the new token) does, and the consumers wait (griddepcontrol.wait).
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
-#if KVT_TRACE_LOOP
-      unsigned long long pwait = 0;
-#endif
       for (int i = 0;; ++i) {
         const int s2 = i % NST;
-        if (i == v.pdl_pre) {
-          // Before blocking on the previous kernel: this CTA's remaining stages go to L2 now, so
-          // HBM streams them during the previous layer's tail instead of idling (K/V rows do
-          // not depend on the previous kernel; only their consumption does).
-          if (v.l2_prefetch) {
-            for (int j = i; j < nstage; ++j) {
-              bool pt2;
-              int png;
-              stage_at(j, pt2, png);
-              for (int wi = 0; wi < png; ++wi) {
-                const int gi = group_of(j, wi);
-                if (!pt2) {
-                  const int ts = 16 * gi;             // a1 is a multiple of 16: one store per group
-                  bulk_prefetch_l2((ts < sg.a1 ? K0 + (size_t)ts * D : K1 + (size_t)(ts - sg.a1) * D), 16 * ROWB);
-                  bulk_prefetch_l2((ts < sg.a1 ? V0 + (size_t)ts * D : V1 + (size_t)(ts - sg.a1) * D), 16 * ROWB);
-                } else {
-                  const size_t j0 = 16 * (size_t)gi;
-                  bulk_prefetch_l2(v.c2k[sb] + (grp * v.cap2 + j0) * D, 16 * D);
-                  bulk_prefetch_l2(v.c2v[sb] + (grp * v.cap2 + j0) * D, 16 * D);
-                }
-              }
-            }
-          }
-          pdl_wait();   // at most pdl_pre stages in flight before the previous layer ends
-        }
-        if (i >= NST) {
-#if KVT_TRACE_LOOP
-          const unsigned long long tw = gtimer();
-          mbar_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
-          pwait += gtimer() - tw;
-#else
-          mbar_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
-#endif
-        }
+        if (i >= NST) mbar_wait(empty0 + 8 * s2, ((i / NST) - 1) & 1);
         const uint32_t full = full0 + 8 * s2, dst = ring_s + s2 * STAGEB;
         if (i >= nstage) {
-#if KVT_TRACE_LOOP
-          if (tr) { tr[12] = gtimer(); tr[11] = pwait; }
-#endif
           stile[s2] = -1;
           mbar_arrive(full);          // sentinel stage (no data)
           break;
@@ -341,10 +170,6 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       }
     }
     __syncwarp();
-    if (cm) {
-      asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
-      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-    }
     return;
   }
   pdl_trigger();
@@ -354,7 +179,6 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
 
   if (w == WSCORE) {
     // ============================ side warp ============================
-    if (cm) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
     // (1) rank 0: the new token (a1 fused): append its K/V row to T0 row n0-1 (swizzled) and
     //     publish its attention term as the unit's partial number C: m = z, l = 1, o = v_new.
     if (has_new) {
@@ -397,9 +221,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
         const float vf = bf16_bits_to_f(vb[k]);
         for (int h = 0; h < G; ++h) part[16 + h * D + e] = vf;
       }
-#ifndef KVT_NO_RED_DECODE
       if (v.red && kin) redund_append(v, layer, unit, v.st->n - 1, kin);   // redundancy (fused append only)
-#endif
       if (scorer_uses_vnorm(v.scorer)) {   // VATP: the new token's V-row norm for this layer
         float ss = 0.f;
 #pragma unroll
@@ -420,43 +242,11 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
         part[lane] = -INFINITY;
         part[8 + lane] = 0.f;
       }
-      if (cm) {                          // partial number C of every rank's slice
-#pragma unroll
-        for (int k = 0; k < EL; ++k) nrow[lane + 32 * k] = bf16_bits_to_f(vb[k]);
-        if (lane < 8) {
-          zn[lane] = lane < G ? part[lane] : -INFINITY;
-        }
-        __syncwarp();
-        cg::cluster_group cluster = cg::this_cluster();
-        const int tot = G * D, q4 = cm_rb / 4;
-        for (int e = lane; e < C * q4; e += 32) {
-          const int c = e / q4, j4 = e - c * q4;
-          float4 val;
-          if (j4 < 2) {
-            const int h0 = 4 * j4;
-            val = make_float4(zn[h0], zn[h0 + 1], zn[h0 + 2], zn[h0 + 3]);
-          } else if (j4 < 4) {
-            const int h0 = 4 * (j4 - 2);
-            val = make_float4(h0 < G ? 1.f : 0.f, h0 + 1 < G ? 1.f : 0.f, h0 + 2 < G ? 1.f : 0.f, h0 + 3 < G ? 1.f : 0.f);
-          } else {
-            const int idx = c * cm_per + 4 * (j4 - 4);
-            if (idx < tot) {
-              const int dd = idx % D;
-              val = make_float4(nrow[dd], nrow[dd + 1], nrow[dd + 2], nrow[dd + 3]);
-            } else {
-              val = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-          }
-          reinterpret_cast<float4*>(cluster.map_shared_rank(rbuf, c) + C * cm_rb)[j4] = val;
-        }
-      }
     }
-    if (r == 0 && !sg.nn && !cm) {     // sequence shard without the new token: neutral partial C
+    if (r == 0 && !sg.nn) {     // sequence shard without the new token: neutral partial C
       float* part = v.part + ((size_t)unit * (C + 1) + C) * v.part_stride;
       for (int e = lane; e < 16 + G * D; e += 32) part[e] = e < 8 ? -INFINITY : 0.f;
     }
-    if (!cm && v.last_merge && r == 0) asm volatile("bar.arrive 3, %0;\n" ::"r"(NCONS + 32) : "memory");
-    if (cm) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
     return;
   }
 
@@ -573,22 +363,9 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     __syncwarp();
   };
 
-#if KVT_TRACE_LOOP
-  unsigned long long tprev = 0, acc_wait = 0, acc_busy = 0, first_busy = 0, nst_seen = 0;
-#endif
   for (int i = 0;; ++i) {
     const int s2 = i % NST;
-#if KVT_TRACE_LOOP   // per-stage wait / busy accounting (debug builds: -DKVT_TRACE_LOOP=1)
-    const unsigned long long tw = gtimer();                   // registers only in the loop
-    if (i > 0) acc_busy += tw - tprev;
-    if (i == 1) first_busy = tw - tprev;                      // first stage (includes the q load)
     mbar_wait(full0 + 8 * s2, (i / NST) & 1);
-    tprev = gtimer();
-    acc_wait += tprev - tw;
-    nst_seen += 1;
-#else
-    mbar_wait(full0 + 8 * s2, (i / NST) & 1);
-#endif
     const int k = stile[s2];
     if (k < 0) break;
     if (tr && tid == 0 && i == 0) tr[2] = gtimer();
@@ -637,9 +414,6 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     if (lane == 0) mbar_arrive(empty0 + 8 * s2);
   }
   if (tr && tid == 0) tr[3] = gtimer();
-#if KVT_TRACE_LOOP
-  if (tr && tid == 0) { tr[8] = acc_wait; tr[9] = acc_busy; tr[10] = nst_seen; tr[13] = first_busy; }
-#endif
 
   // ---- warps -> CTA partial (ring reused as [NW][8][D+4] fp32)
 #pragma unroll
@@ -666,183 +440,36 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
   }
   named_sync(1, NCONS);
   const int tot = G * D;
-  if (!cm) {
-    // publish straight to the global slot (visible to the merge kernel once this grid
-    // completes): every thread forms its elements' per-head max and warp factors itself
-    float* part = v.part + ((size_t)unit * (C + 1) + r) * v.part_stride;
-    if (tid < 8) {
-      float M = -INFINITY;
-#pragma unroll
-      for (int x = 0; x < NW; ++x) M = fmaxf(M, redm[x * 8 + tid]);
-      float Ls = 0.f;
-#pragma unroll
-      for (int x = 0; x < NW; ++x) {
-        const float m = redm[x * 8 + tid];
-        Ls += (m == -INFINITY ? 0.f : ex2_ftz(m - M)) * redl[x * 8 + tid];
-      }
-      part[tid] = M;
-      part[8 + tid] = Ls;
-    }
-    for (int e = tid; e < tot; e += NCONS) {
-      const int h = e / D, dd = e - h * D;
-      float mw[NW], M = -INFINITY;
-#pragma unroll
-      for (int x = 0; x < NW; ++x) {
-        mw[x] = redm[x * 8 + h];
-        M = fmaxf(M, mw[x]);
-      }
-      float a = 0.f;
-#pragma unroll
-      for (int x = 0; x < NW; ++x) a += (mw[x] == -INFINITY ? 0.f : ex2_ftz(mw[x] - M)) * ow[(x * 8 + h) * OWS + dd];
-      part[16 + e] = a;
-    }
-    if (tr && tid == 0) tr[4] = gtimer();
-    if (v.last_merge) last_cta_merge<D, NCONS>(v, unit, b, g, C, zpar, o, ring + NW * 8 * OWS * 4, tid, r == 0);
-    return;
-  }
-  float* fw = ow + NW * 8 * OWS;       // [NW][8] warp factors exp2(m_w - M)
-  if (tid < 8 * NW) {                  // factors of every (warp, head)
-    const int ww = tid >> 3, h = tid & 7;
+  // publish straight to the global slot (visible to the merge kernel once this grid completes):
+  // every thread forms its elements' per-head max and warp factors itself
+  float* part = v.part + ((size_t)unit * (C + 1) + r) * v.part_stride;
+  if (tid < 8) {
     float M = -INFINITY;
 #pragma unroll
-    for (int x = 0; x < NW; ++x) M = fmaxf(M, redm[x * 8 + h]);
-    const float m = redm[ww * 8 + h];
-    fw[tid] = m == -INFINITY ? 0.f : ex2_ftz(m - M);
-    if (ww == 0) xm[h] = M;
-  }
-  named_sync(1, NCONS);
-  // CTA partial, staged in shared memory for the cluster exchange: [m 8 | l 8 | o G*D]
-  float* xp = fw + 8 * NW;                            // [16 + G*D] in the free ring (16-B aligned)
-  if (tid < 8) {
+    for (int x = 0; x < NW; ++x) M = fmaxf(M, redm[x * 8 + tid]);
     float Ls = 0.f;
 #pragma unroll
-    for (int x = 0; x < NW; ++x) Ls += redl[x * 8 + tid] * fw[x * 8 + tid];
-    xp[tid] = xm[tid];
-    xp[8 + tid] = Ls;
+    for (int x = 0; x < NW; ++x) {
+      const float m = redm[x * 8 + tid];
+      Ls += (m == -INFINITY ? 0.f : ex2_ftz(m - M)) * redl[x * 8 + tid];
+    }
+    part[tid] = M;
+    part[8 + tid] = Ls;
   }
   for (int e = tid; e < tot; e += NCONS) {
     const int h = e / D, dd = e - h * D;
+    float mw[NW], M = -INFINITY;
+#pragma unroll
+    for (int x = 0; x < NW; ++x) {
+      mw[x] = redm[x * 8 + h];
+      M = fmaxf(M, mw[x]);
+    }
     float a = 0.f;
 #pragma unroll
-    for (int x = 0; x < NW; ++x) a += fw[x * 8 + h] * ow[(x * 8 + h) * OWS + dd];
-    xp[16 + e] = a;
-  }
-  named_sync(1, NCONS);
-  // ---- cluster merge: push (m, l) and slice c of o to rank c, one barrier, merge own slice
-  cg::cluster_group cluster = cg::this_cluster();
-  asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");     // phase 0 (long complete)
-  {
-    const int q4 = cm_rb / 4;
-    const float4* xp4 = reinterpret_cast<const float4*>(xp);
-    for (int e = tid; e < C * q4; e += NCONS) {
-      const int c = e / q4, j4 = e - c * q4;
-      float4 val;
-      if (j4 < 4) {
-        val = xp4[j4];
-      } else {
-        const int idx = c * cm_per + 4 * (j4 - 4);
-        val = idx < tot ? xp4[4 + idx / 4] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      reinterpret_cast<float4*>(cluster.map_shared_rank(rbuf, c) + r * cm_rb)[j4] = val;
-    }
+    for (int x = 0; x < NW; ++x) a += (mw[x] == -INFINITY ? 0.f : ex2_ftz(mw[x] - M)) * ow[(x * 8 + h) * OWS + dd];
+    part[16 + e] = a;
   }
   if (tr && tid == 0) tr[4] = gtimer();
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-  if (tr && tid == 0) tr[5] = gtimer();
-  {
-    // same arithmetic, same order as k_decode_merge (rank order, new token last)
-    const int NP = C + 1, e0 = r * cm_per;
-    for (int j = tid; j < cm_per && e0 + j < tot; j += NCONS) {
-      const int e = e0 + j, h = e / D, dd = e - h * D;
-      float M = -INFINITY;
-      for (int c = 0; c < NP; ++c) M = fmaxf(M, rbuf[c * cm_rb + h]);
-      float Ls = 0.f, acc = 0.f;
-      for (int c = 0; c < NP; ++c) {
-        const float mc = rbuf[c * cm_rb + h];
-        const float f = mc == -INFINITY ? 0.f : ex2_ftz(mc - M);
-        Ls += f * rbuf[c * cm_rb + 8 + h];
-        acc += f * rbuf[c * cm_rb + 16 + j];
-      }
-      const float invL = 1.0f / Ls;
-      const size_t oi = ((size_t)b * v.Hq + g * G + h) * D + dd;
-      if (v.out_fp32) reinterpret_cast<float*>(o)[oi] = acc * invL;
-      else reinterpret_cast<__nv_bfloat16*>(o)[oi] = __float2bfloat16_rn(acc * invL);
-    }
-  }
-  if (tr && tid == 0) tr[6] = gtimer();
-  if (zpar < 0) return;
-  // ---- a4 fused: every rank holds the (m, l) of all partials, hence the unit's global (M, 1/L)
-  //      per head (bitwise the merge's); the exact probabilities of this CTA's own tokens
-  //      update S_part[b][g][pos] (one fp32 add per (step, layer), AMB-14; one writer per entry)
-  if (tid < 8) {
-    float M = -INFINITY;
-    for (int c = 0; c <= C; ++c) M = fmaxf(M, rbuf[c * cm_rb + tid]);
-    float Ls = 0.f;
-    for (int c = 0; c <= C; ++c) {
-      const float mc = rbuf[c * cm_rb + tid];
-      const float f = mc == -INFINITY ? 0.f : ex2_ftz(mc - M);
-      Ls += f * rbuf[c * cm_rb + 8 + tid];
-    }
-    sML[tid] = M;
-    sML[8 + tid] = 1.0f / Ls;
-  }
-  named_sync(1, NCONS);
-  {
-    constexpr int SBE = 4;
-    const int ntok = nstage * TILE + (has_new ? 1 : 0);   // + the new token (rank 0, last)
-    float* S = v.S + (size_t)unit * v.Nmax;
-    bool bad = false;
-    for (int j0 = tid; j0 < ntok; j0 += NCONS * SBE) {
-      int pos[SBE], tt[SBE];
-      float4 z0[SBE], z1[SBE];
-#pragma unroll
-      for (int k = 0; k < SBE; ++k) {
-        const int j = j0 + k * NCONS;
-        pos[k] = -1;
-        tt[k] = 0;
-        if (j < ntok) {
-          int t;
-          bool ok;
-          if (j < nstage * TILE) {        // stage rows: T0/T1 or T2 rows only (never pads)
-            bool jt2;
-            int jng;
-            stage_at(j / TILE, jt2, jng);
-            const int row = j % TILE;
-            ok = row < 16 * jng;
-            t = ok ? (jt2 ? sg.a2 : 0) + 16 * group_of(j / TILE, row >> 4) + (row & 15) : 0;
-            ok = ok && (jt2 ? t < sg.a2 + sg.n2 : sg.bf16_valid(t));
-          } else {                        // the new token (rank 0)
-            t = sg.a3;
-            ok = true;
-          }
-          if (ok) {
-            tt[k] = t;
-            pos[k] = sg.pos(v, cur, b, t);
-            z0[k] = *reinterpret_cast<const float4*>(zrow + (size_t)t * 8);
-            z1[k] = *reinterpret_cast<const float4*>(zrow + (size_t)t * 8 + 4);
-          }
-        }
-      }
-      float sv[SBE];
-#pragma unroll
-      for (int k = 0; k < SBE; ++k)
-        if (pos[k] >= 0) sv[k] = S[pos[k]];
-#pragma unroll
-      for (int k = 0; k < SBE; ++k) {
-        if (pos[k] < 0) continue;
-        const float zz[8] = {z0[k].x, z0[k].y, z0[k].z, z0[k].w, z1[k].x, z1[k].y, z1[k].z, z1[k].w};
-        float inc = 0.f;
-#pragma unroll
-        for (int h = 0; h < 8; ++h)
-          if (h < G) inc += ex2_ftz(zz[h] - sML[h]) * sML[8 + h];
-        S[pos[k]] = sv[k] + inc;
-        bad |= !isfinite(inc);
-      }
-    }
-    if (bad) atomicOr(&v.st->err, 1);
-  }
-  if (tr && tid == 0) tr[7] = gtimer();
 }
 
 // Merge of the C per-CTA partials (+ the new-token partial) of every unit, in rank order
@@ -950,39 +577,6 @@ __global__ void __launch_bounds__(256) k_score_flush(const DevView v, const int 
   if (bad) atomicOr(&v.st->err, 1);
 }
 
-// Register-lean variant (default): it runs beside the decode chain, so its CTAs must fit next
-// to two decode CTAs in an SM's register file (128 threads x <= 32 registers); one (unit,
-// token) entry per thread per pass, same arithmetic and order as score_range.
-__global__ void __launch_bounds__(128, 16) k_score_flush_lean(const DevView v, const int zfirst, const int nz) {
-  const int cur = v.st->cur;
-  Seg sg;
-  sg.init(v.cnt[cur], v.st->nn, v.host_t1);
-  const long long tot = (long long)v.B * v.Hkv * sg.nvirt;
-  const size_t zslot = (size_t)v.B * v.Hkv * v.zrows * 8, mslot = (size_t)v.B * v.Hkv * 16;
-  bool bad = false;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
-    const int u = (int)(i / sg.nvirt), t = (int)(i - (long long)u * sg.nvirt);
-    if (!sg.valid(t)) continue;
-    const int pos = sg.pos(v, cur, u / v.Hkv, t);
-    float s = v.S[(size_t)u * v.Nmax + pos];
-    for (int j = 0; j < nz; ++j) {
-      const int slot = zslot_of(v, zfirst + j);
-      const float4* z = reinterpret_cast<const float4*>(v.zbuf + slot * zslot + ((size_t)u * v.zrows + t) * 8);
-      const float* ml = v.ml + slot * mslot + (size_t)u * 16;
-      const float4 za = z[0], zc = z[1];
-      const float zz[8] = {za.x, za.y, za.z, za.w, zc.x, zc.y, zc.z, zc.w};
-      float inc = 0.f;
-#pragma unroll
-      for (int h = 0; h < 8; ++h)
-        if (h < v.G) inc += ex2_ftz(zz[h] - ml[h]) * ml[8 + h];
-      s = s + inc * score_weight(v, v.scorer ? v.zlayer[slot] : 0, u, pos);
-      bad |= !isfinite(inc);
-    }
-    v.S[(size_t)u * v.Nmax + pos] = s;
-  }
-  if (bad) atomicOr(&v.st->err, 1);
-}
-
 // Sequence shards: a shard's tier counts differ per request, so every unit decodes its own
 // virtual layout (one thread per (unit, virtual row) over the zrows-wide logit rows).
 __global__ void __launch_bounds__(256) k_score_flush_req(const DevView v, const int zfirst, const int nz) {
@@ -1013,7 +607,6 @@ __global__ void __launch_bounds__(256) k_score_flush_req(const DevView v, const 
 
 cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_t s) {
   if (v.seq_w > 1) k_score_flush_req<<<148, 256, 0, s>>>(v, zfirst, nz);
-  else if (v.score_lean) k_score_flush_lean<<<v.score_grid, 128, 0, s>>>(v, zfirst, nz);
   else k_score_flush<<<v.score_grid, 256, 0, s>>>(v, zfirst, nz);
   return cudaGetLastError();
 }
@@ -1030,10 +623,6 @@ size_t attn_smem_bytes(const DevView& v) {
   const size_t xob = (size_t)8 * v.D * 4 + (8 + 8 + 16 * vr.nw + 16 + 2 * v.D + 8) * 4;
   const size_t t2 = (v.cap2 > 0) ? (size_t)vr.nw * 16 * v.D * 2 : 0;
   size_t total = ringb + xob + t2;
-  if (v.cluster_merge) {
-    const int C = v.split, per = (((v.G * v.D + C - 1) / C) + 3) & ~3;
-    total += (size_t)(C + 1) * (per + 16) * 4 + 16;
-  }
   const size_t ow = (size_t)vr.nw * 8 * (v.D + 4) * 4 + vr.nw * 8 * 4;   // end-of-kernel reuse of the ring
   if (ow > (size_t)vr.nst * 2 * tile * v.D * 2) total += ow;   // (never for the shipped variants)
   return total;
@@ -1041,23 +630,15 @@ size_t attn_smem_bytes(const DevView& v) {
 
 template <int D, int NW, int NST>
 static cudaError_t configure_k(const DevView& v) {
-  if (v.cluster_merge)
-    return cudaFuncSetAttribute(k_decode_attn<D, NW, NST, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)attn_smem_bytes(v));
-  cudaError_t e = cudaFuncSetAttribute(k_decode_attn<D, NW, NST, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)attn_smem_bytes(v));
-  return e;
+  return cudaFuncSetAttribute(k_decode_attn<D, NW, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)attn_smem_bytes(v));
 }
 
 template <int D, int NW, int NST>
 static cudaError_t launch_k(const DevView& v, cudaLaunchConfig_t& cfg, int layer, const void* q, const void* knew,
                             const void* vnew, void* o, int zpar) {
   cfg.blockDim = dim3((NW + 2) * 32, 1, 1);
-  if (v.cluster_merge)
-    return cudaLaunchKernelEx(&cfg, k_decode_attn<D, NW, NST, true>, v, layer, reinterpret_cast<const __nv_bfloat16*>(q),
-                              reinterpret_cast<const __nv_bfloat16*>(knew), reinterpret_cast<const __nv_bfloat16*>(vnew),
-                              o, zpar);
-  return cudaLaunchKernelEx(&cfg, k_decode_attn<D, NW, NST, false>, v, layer, reinterpret_cast<const __nv_bfloat16*>(q),
+  return cudaLaunchKernelEx(&cfg, k_decode_attn<D, NW, NST>, v, layer, reinterpret_cast<const __nv_bfloat16*>(q),
                             reinterpret_cast<const __nv_bfloat16*>(knew), reinterpret_cast<const __nv_bfloat16*>(vnew),
                             o, zpar);
 }
@@ -1104,13 +685,6 @@ static cudaError_t launch_decode_main(const DevView& v, int layer, const void* q
     at[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
-  if (v.cluster_merge) {
-    at[na].id = cudaLaunchAttributeClusterDimension;
-    at[na].val.clusterDim.x = v.split;
-    at[na].val.clusterDim.y = 1;
-    at[na].val.clusterDim.z = 1;
-    ++na;
-  }
   cfg.attrs = at;
   cfg.numAttrs = na;
   const Variant vr = kVariants[v.variant];
@@ -1154,8 +728,8 @@ static cudaError_t launch_merge(const DevView& v, int layer, void* o, int zpar, 
 cudaError_t launch_decode_attn(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
                                void* o, int zpar, int pdl, cudaStream_t s, float* lse) {
   cudaError_t e = launch_decode_main(v, layer, q, knew, vnew, o, zpar, pdl, s);
-  if (e != cudaSuccess || v.cluster_merge || (v.last_merge && !lse)) return e;
-  return launch_merge(v, layer, o, zpar, v.use_pdl, s, lse);
+  if (e != cudaSuccess) return e;
+  return launch_merge(v, layer, o, zpar, 1, s, lse);
 }
 
 // (M, 1/L) of every (unit, head) for score slot zslot from the caller's global (M, L)

@@ -34,6 +34,11 @@ struct kv_tier_ctx {
   std::vector<int> appended_step;          // step in which layer l's new row was written
   bool offload_pending = false;
   bool capturing = false;
+  // per-layer ABI: may decode_attention chain to the previous library launch with programmatic
+  // dependent launch?  Only when that launch was this step's decode_attention / append on the
+  // same stream (begin_step, score flushes and migrate change state the kernel's prologue reads).
+  bool pdl_ok = false;
+  void* pdl_stream = nullptr;
   int zslot_next = 0;                      // logits/ML ring slot of the next fused decode_attention (0 at step start)
   int zpend_first = 0, zpend_n = 0;        // launches whose score update is not yet issued
   bool slot_busy[ZRING] = {};              // a score kernel may still read the slot
@@ -42,7 +47,6 @@ struct kv_tier_ctx {
   cudaEvent_t ev_merged[ZRING] = {}, ev_scored[ZRING] = {}, ev_score_tail = nullptr;
   bool slot_recorded[2] = {false, false};   // ev_slot_free[x] recorded within the open step
   int lse_pending = -1;                    // score slot of a decode_attention_lse awaiting the global (M, L)
-  int zflat_pending = -1;                  // flat kernel: slot whose score update the next launch applies
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   unsigned long long* trace = nullptr;     // debug timeline buffer (KVTIER_TRACE=1)
@@ -107,7 +111,6 @@ int auto_split(const kv_tier_config& c) { return split_of(c); }
 // B=16 2 slots 146 vs 4 slots 128 steps/s; 14B 3 slots 431, 4 slots 416, 2 slots 369; 7B 4
 // slots 3005 vs 2 slots 2499.
 int zring_of(const kv_tier_config& c) {
-  if (const char* e = getenv("KVTIER_ZRING")) return std::max(2, std::min(ZRING, atoi(e)));
   const size_t slot = (size_t)c.num_requests * c.num_kv_heads * (c.max_tokens + 64) * 8 * 4;
   int k = ZRING;
   while (k > 2 && (size_t)k * slot > ((size_t)60 << 20)) --k;
@@ -183,29 +186,35 @@ struct Layout {
 int split_of(const kv_tier_config& c);
 int zring_of(const kv_tier_config& c);
 
-// Whole-step kernel (step.cu): s CTAs per kv head (a cluster, s <= 16) or m kv heads per CTA.
-// Every CTA of a request must be resident at once (they wait on each other layer by layer), so
-// a shape qualifies only if all B*H_kv/m clusters fit the GPU together.  The shape that keeps
-// the most SMs busy wins; ties: smaller s (fewer shared-memory exchanges).  Sets v.step_k (total
-// CTAs, 0 = no shape fits), v.step_s, v.step_m.
+// Whole-step kernel (step.cu): s CTAs per kv head (a cluster, s <= 16) or m kv heads per CTA;
+// 8 consumer warps per CTA (one CTA per SM) or 4 (two per SM).  Every CTA of a request must be
+// resident at once (they wait on each other layer by layer), so a shape qualifies only if all
+// B*H_kv/m clusters fit the GPU together.  Among those, the one engaging the most SMs wins, then
+// the one-CTA-per-SM shape.  Sets v.step_k (total CTAs, 0 = no
+// shape fits), v.step_s, v.step_m, v.step_nw.
 void step_plan(DevView& v, int nsm) {
-  int best = 0, bs = 0, bm = 0;
-  for (int m = 8; m >= 1; m >>= 1) {
-    if (v.Hkv % m) continue;
-    for (int s = 1; s <= (m == 1 ? 16 : 1); ++s) {
-      const int clusters_needed = v.B * v.Hkv / m, total = clusters_needed * s;
-      if (total > nsm) continue;
-      v.step_k = total; v.step_s = s; v.step_m = m;
-      if (step_smem_bytes(v) > 227 * 1024) continue;
-      int clusters = 0;
-      if (step_configure(v, &clusters) != cudaSuccess) { cudaGetLastError(); continue; }
-      if (getenv("KVTIER_TRACE")) fprintf(stderr, "step_plan: s=%d m=%d CTAs=%d clusters=%d/%d smem=%zu\n", s, m,
-                                          total, clusters_needed, clusters, step_smem_bytes(v));
-      if (clusters < clusters_needed) continue;
-      if (total > best) { best = total; bs = s; bm = m; }
+  int best = 0, bs = 0, bm = 0, bnw = 0;
+  for (int nw : {8, 4}) {
+    const int per_sm = nw == 8 ? 1 : 2;
+    for (int m = 8; m >= 1; m >>= 1) {
+      if (v.Hkv % m) continue;
+      for (int s = 1; s <= (m == 1 ? 16 : 1); ++s) {
+        if (v.split_req > 0 && (s != v.split_req || m != 1)) continue;   // the config's split, if given
+        const int clusters_needed = v.B * v.Hkv / m, total = clusters_needed * s;
+        if (total > per_sm * nsm) continue;
+        v.step_k = total; v.step_s = s; v.step_m = m; v.step_nw = nw;
+        if (step_smem_bytes(v) > (nw == 8 ? 227 * 1024 : 113 * 1024)) continue;
+        int clusters = 0;
+        if (step_configure(v, &clusters) != cudaSuccess) { cudaGetLastError(); continue; }
+        if (clusters < clusters_needed) continue;
+        // SMs engaged; ties: one CTA per SM (measured at 7B: 8 warps x 128 CTAs 3593 steps/s,
+        // 4 warps x 256 CTAs 3353)
+        const int sms = total / per_sm, best_sms = best ? best / (bnw == 8 ? 1 : 2) : 0;
+        if (sms > best_sms || (sms == best_sms && nw > bnw)) { best = total; bs = s; bm = m; bnw = nw; }
+      }
     }
   }
-  v.step_k = best; v.step_s = bs; v.step_m = bm;
+  v.step_k = best; v.step_s = bs; v.step_m = bm; v.step_nw = bnw;
   if (best) { int c = 0; step_configure(v, &c); }   // leave the chosen shape's attributes set
 }
 
@@ -215,12 +224,6 @@ int host_rows_of(const kv_tier_config& c) {
                                                          : c.max_tokens;
 }
 
-// Flat decode grid: one CTA per SM, more when a CTA would cover > 6 units (new-token slots).
-int flat_grid(const kv_tier_config& c, int nsm) {
-  const int units = c.num_requests * c.num_kv_heads;
-  return std::max(nsm, (units + 5) / 6);
-}
-constexpr int FLAT_GRID_MAX_SM = 296;     // partial slots reserved for grids up to this size
 
 // Rows an incremental migrate may move per request; more -> full rebuild (first event).
 size_t mcap_of(const kv_tier_config& c) {
@@ -265,8 +268,7 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   L.off_S = take(BH * N * 4);
   L.off_z = take(zring_of(c) * BH * (N + 64) * 8 * 4);   // logits of recent launches (score update)
   L.off_ml = take(ZRING * BH * 16 * 4);
-  const size_t nslots = std::max(BH * (split_of(c) + 1),                 // split kernel: per-CTA partials + new token
-                                  (size_t)flat_grid(c, FLAT_GRID_MAX_SM) + 2 * BH);   // flat: <= grid + 2 units
+  const size_t nslots = BH * (split_of(c) + 1);                          // per-CTA partials + new token
   L.off_part = take(nslots * (16 + 8 * D) * 4);
   L.off_sdone = take((size_t)c.num_layers * B * 4);                     // step kernel layer counters
   L.off_uctr = take(BH * 4);
@@ -360,43 +362,11 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.stream_mode = cfg->staging_tokens == 0;
   v.out_fp32 = cfg->out_fp32;
   v.split = auto_split(*cfg);
+  v.split_req = cfg->split;
   v.variant = cfg->variant;
-  v.pdl_pre = getenv("KVTIER_PDL_PRE") ? atoi(getenv("KVTIER_PDL_PRE")) : 1 << 30;
-  v.use_pdl = getenv("KVTIER_NOPDL") ? 0 : 1;
-  v.l2_prefetch = getenv("KVTIER_L2PF") ? atoi(getenv("KVTIER_L2PF")) : 0;   // measured: no gain at 7B
-  v.stage_rr = getenv("KVTIER_RR") ? atoi(getenv("KVTIER_RR")) : 1;   // 2 (groups round-robin) measured slower
-  v.cluster_merge = (getenv("KVTIER_CLUSTER") && atoi(getenv("KVTIER_CLUSTER")) && v.split <= 8 &&
-                     cfg->shard != KV_TIER_SHARD_SEQUENCE) ? 1 : 0;
-  v.chunk_max = 0;
-  {
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device);
-    v.nc = flat_grid(*cfg, std::min(nsm, FLAT_GRID_MAX_SM));
-    v.flat = getenv("KVTIER_FLAT") ? atoi(getenv("KVTIER_FLAT")) : 0;   // measured slower than split
-    // default: 8 consumer warps, 3 x 64 KB stages (2 stages when the T2 scratch needs room)
-    v.fvariant = getenv("KVTIER_FVAR") ? atoi(getenv("KVTIER_FVAR")) : (cfg->t2_fraction_bp > 0 ? 1 : 0);
-    if (v.cluster_merge) v.flat = 0;
-    v.seq_w = cfg->shard == KV_TIER_SHARD_SEQUENCE ? cfg->world : 1;
-    v.seq_r = cfg->shard == KV_TIER_SHARD_SEQUENCE ? cfg->rank : 0;
-    if (v.seq_w > 1) v.flat = 0;            // sequence shards run the split kernel
-    // the flat kernel's partition arithmetic is 32-bit: cost space (<= 3 per 16 rows per unit)
-    // times the grid must fit
-    const unsigned long long units = (unsigned long long)cfg->num_requests * cfg->num_kv_heads;
-    if (units * 3ull * ((unsigned long long)cfg->max_tokens / 16 + 8) * (unsigned long long)v.nc >= (1ull << 32))
-      v.flat = 0;
-    // merging CTAs wait for their unit's other CTAs: the whole grid must be co-resident (one CTA
-    // per SM), and a CTA owns at most 8 new-token terms (units per CTA <= units/grid + 2)
-    if (v.nc > nsm || units > 6ull * (unsigned long long)v.nc) v.flat = 0;
-    v.spin_hint = getenv("KVTIER_SPIN") ? atoi(getenv("KVTIER_SPIN")) : 0;
-    // L2 prefetch budget: about a third of the 126 MB L2 per layer in flight, split over the grid
-    const long long l2mb = getenv("KVTIER_L2PF_MB") ? atoll(getenv("KVTIER_L2PF_MB")) : 0;   // measured: no gain
-    v.l2pf_bytes = l2mb * (1LL << 20) / std::max(1, v.nc);
-    v.inflight = getenv("KVTIER_INFLIGHT") ? atoi(getenv("KVTIER_INFLIGHT")) : 0;
-    v.score_lean = getenv("KVTIER_SCORE_LEAN") ? atoi(getenv("KVTIER_SCORE_LEAN")) : 0;   // measured slower
-    v.last_merge = getenv("KVTIER_LASTMERGE") ? atoi(getenv("KVTIER_LASTMERGE")) : 0;
-    if (v.seq_w > 1) v.last_merge = 0;      // sequence shards need the merge kernel's (m, l) output
-    v.score_grid = getenv("KVTIER_SCORE_GRID") ? atoi(getenv("KVTIER_SCORE_GRID")) : (v.score_lean ? 296 : 148);
-  }
+  v.seq_w = cfg->shard == KV_TIER_SHARD_SEQUENCE ? cfg->world : 1;
+  v.seq_r = cfg->shard == KV_TIER_SHARD_SEQUENCE ? cfg->rank : 0;
+  v.score_grid = 148;                       // score-flush CTAs beside the per-layer chain (measured best)
   for (int i = 0; i < 2; ++i) {
     v.k0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_k0[i]);
     v.v0[i] = reinterpret_cast<__nv_bfloat16*>(A + L.off_v0[i]);
@@ -419,15 +389,13 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.zring = zring_of(*cfg);
   v.part = reinterpret_cast<float*>(A + L.off_part);
   v.part_stride = 16 + 8 * v.D;
-  v.unit_ctr = reinterpret_cast<int*>(A + L.off_uctr);
-  v.step_k = v.step_s = v.step_m = 0;
+  v.step_k = v.step_s = v.step_m = v.step_nw = 0;
   v.step_done = reinterpret_cast<int*>(A + L.off_sdone);
   v.zlayer = reinterpret_cast<int*>(A + L.off_zlayer);
   v.scorer = cfg->scorer;
   v.vnorm = scorer_uses_vnorm(cfg->scorer) ? reinterpret_cast<float*>(A + L.off_vnorm) : nullptr;
   v.red = scorer_uses_red(cfg->scorer) ? reinterpret_cast<float*>(A + L.off_red) : nullptr;
   v.lastk = scorer_uses_red(cfg->scorer) ? reinterpret_cast<uint16_t*>(A + L.off_lastk) : nullptr;
-  if (v.scorer != KV_TIER_SCORER_ATTENTION) { v.flat = 0; v.cluster_merge = 0; }   // split kernel + merge kernel
   v.hot_base = A + L.hot_begin;
   v.hot_bytes = L.total - L.hot_begin;
   v.moves = reinterpret_cast<int4*>(A + L.off_moves);
@@ -459,15 +427,13 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     v.hs2k = reinterpret_cast<float*>(h + 2 * rows * v.D);
     v.hs2v = reinterpret_cast<float*>(h + 2 * rows * v.D + rows * 4);
   }
-  if (getenv("KVTIER_TRACE") && atoi(getenv("KVTIER_TRACE")) > 0) {
-    const size_t tb = (size_t)v.L * std::max(std::max(v.split * v.B * v.Hkv, v.nc), 16 * v.B) * NTRACE * sizeof(unsigned long long);
+#if KVT_TRACE
+  {                                         // debug builds: per-(layer, CTA) timeline buffer
+    const size_t tb = (size_t)v.L * std::max(v.split * v.B * v.Hkv, 2 * 148) * NTRACE * sizeof(unsigned long long);
     if (cudaMalloc(&ctx->trace, tb) == cudaSuccess) { cudaMemset(ctx->trace, 0, tb); v.trace = ctx->trace; }
   }
-  if (v.flat && (v.fvariant < 0 || v.fvariant > 4)) {
-    delete ctx;
-    return fail(nullptr, KV_TIER_E_INVAL, "KVTIER_FVAR must be in [0, 4]");
-  }
-  const size_t smem_need = v.flat ? flat_smem_bytes(v) : std::max(attn_smem_bytes(v), merge_smem_bytes(v));
+#endif
+  const size_t smem_need = std::max(attn_smem_bytes(v), merge_smem_bytes(v));
   if (smem_need > 227 * 1024) {
     const size_t need = smem_need;
     if (ctx->host_t1) cudaFreeHost(ctx->host_t1);
@@ -493,8 +459,8 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     v.hot_hit = v.hot_bytes > 0 ? (float)std::min(1.0, (double)lim / (double)v.hot_bytes) : 0.f;
     cudaGetLastError();                  // persistence is an optimisation: ignore if unsupported
   }
-  if (e == cudaSuccess) e = v.flat ? flat_configure(v) : attn_configure(v);
-  if (e == cudaSuccess && !v.flat && !v.cluster_merge && !v.last_merge && !v.stream_mode && v.seq_w <= 1) {
+  if (e == cudaSuccess) e = attn_configure(v);
+  if (e == cudaSuccess && !v.stream_mode && v.seq_w <= 1) {
     // kv_tier_step / the step graph: all layers in one launch, one thread-block cluster per request
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device);
@@ -605,6 +571,7 @@ kv_tier_status kv_tier_begin_step(kv_tier_ctx* ctx, void* stream) {
   ctx->c[0] += seq_own(ctx->v.seq_w, ctx->v.seq_r, ctx->n) ? 1 : 0;
   ctx->n += 1;
   ctx->step_open = true;
+  ctx->pdl_ok = false;
   ctx->classified = false;
   ctx->slot_recorded[0] = ctx->slot_recorded[1] = false;
   ctx->zslot_next = 0;
@@ -619,6 +586,8 @@ kv_tier_status kv_tier_append(kv_tier_ctx* ctx, int32_t layer, const void* k_new
   if (!k_new || !v_new) return fail(ctx, KV_TIER_E_INVAL, "null k/v");
   kv_tier_status st = cuda_check(ctx, launch_append(ctx->v, layer, k_new, v_new, reinterpret_cast<cudaStream_t>(stream)), "append");
   if (!st) ctx->appended_step[layer] = ctx->t;
+  // the append writes only the new row, which a following decode reads after its dependency wait
+  ctx->pdl_ok = !st && ctx->pdl_stream == stream && ctx->pdl_ok;
   return st;
 }
 
@@ -681,32 +650,6 @@ static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, con
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
   if (ctx->v.stream_mode) e = cudaStreamWaitEvent(s, ctx->ev_prefetched[layer], 0);
-  if (getenv("KVTIER_NOSCORE")) fuse_score_update = 0;   // experiment hook: attention without a4
-  if (ctx->v.flat) {
-    // a4: this launch writes its logits to slot zpar and applies the previous launch's pending
-    // update (slot zprev) in its side warp; end_step flushes the last one (launches of a ctx
-    // are stream-ordered, so the adds stay in layer order)
-    const int zpar = fuse_score_update ? (ctx->zflat_pending == 0 ? 1 : 0) : -1;
-    if (e == cudaSuccess)
-      e = launch_decode_flat(ctx->v, layer, q, k_new, v_new, o, zpar, ctx->zflat_pending, pdl, s);
-    if (e == cudaSuccess) ctx->zflat_pending = zpar;
-    if (e == cudaSuccess && ctx->v.stream_mode) {
-      e = cudaEventRecord(ctx->ev_slot_free[layer & 1], s);
-      ctx->slot_recorded[layer & 1] = true;
-    }
-    if (e == cudaSuccess && k_new) ctx->appended_step[layer] = ctx->t;
-    return cuda_check(ctx, e, "decode_attention");
-  }
-  if (ctx->v.cluster_merge) {   // a4 fused into the kernel's epilogue (one logits slot, no score stream)
-    const int zp = fuse_score_update ? 0 : -1;
-    if (e == cudaSuccess) e = launch_decode_attn(ctx->v, layer, q, k_new, v_new, o, zp, pdl, s);
-    if (e == cudaSuccess && ctx->v.stream_mode) {
-      e = cudaEventRecord(ctx->ev_slot_free[layer & 1], s);
-      ctx->slot_recorded[layer & 1] = true;
-    }
-    if (e == cudaSuccess && k_new) ctx->appended_step[layer] = ctx->t;
-    return cuda_check(ctx, e, "decode_attention");
-  }
   const int zpar = fuse_score_update ? ctx->zslot_next : -1;
   // the ring slot's previous score kernel must be done before its logits are overwritten
   if (e == cudaSuccess && zpar >= 0 && ctx->slot_busy[zpar])
@@ -735,16 +678,22 @@ static kv_tier_status decode_attention_impl(kv_tier_ctx* ctx, int32_t layer, con
 
 kv_tier_status kv_tier_decode_attention(kv_tier_ctx* ctx, int32_t layer, const void* q, const void* k_new,
                                         const void* v_new, void* o, int32_t fuse_score_update, void* stream) {
-  return decode_attention_impl(ctx, layer, q, k_new, v_new, o, fuse_score_update, stream, 0);
+  // consecutive layers chain with programmatic dependent launch (the prologue streams this layer's
+  // K/V while the previous kernel -- the previous layer's merge, or caller kernels in between --
+  // finishes; q and the new token are read after griddepcontrol.wait)
+  const int pdl = ctx && ctx->pdl_ok && ctx->pdl_stream == stream && !ctx->v.stream_mode ? 1 : 0;
+  kv_tier_status st = decode_attention_impl(ctx, layer, q, k_new, v_new, o, fuse_score_update, stream, pdl);
+  if (ctx) {
+    ctx->pdl_ok = st == KV_TIER_OK;
+    ctx->pdl_stream = stream;
+  }
+  return st;
 }
 
 kv_tier_status kv_tier_decode_attention_lse(kv_tier_ctx* ctx, int32_t layer, const void* q, const void* k_new,
                                             const void* v_new, void* o, float* lse, int32_t fuse_score_update,
                                             void* stream) {
   if (!lse) return fail(ctx, KV_TIER_E_INVAL, "null lse");
-  if (ctx && ctx->v.flat) return fail(ctx, KV_TIER_E_STATE, "decode_attention_lse runs the split kernel (KVTIER_FLAT=0)");
-  if (ctx && (ctx->v.cluster_merge || ctx->v.last_merge))
-    return fail(ctx, KV_TIER_E_STATE, "decode_attention_lse needs the merge kernel (KVTIER_CLUSTER=0, KVTIER_LASTMERGE=0)");
   return decode_attention_impl(ctx, layer, q, k_new, v_new, o, fuse_score_update, stream, 0, lse);
 }
 
@@ -783,6 +732,21 @@ kv_tier_status kv_tier_visible_count(const kv_tier_ctx* ctx, int32_t* n_vis) {
   return KV_TIER_OK;
 }
 
+kv_tier_status kv_tier_layout(const kv_tier_ctx* ctx, int32_t* counts4, int32_t* shape4) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (counts4) {
+    for (int i = 0; i < 3; ++i) counts4[i] = ctx->c[i];
+    counts4[3] = seq_owned_below(ctx->v.seq_w, ctx->v.seq_r, ctx->n) - ctx->c[0] - ctx->c[1] - ctx->c[2];
+  }
+  if (shape4) {
+    shape4[0] = ctx->v.step_k;
+    shape4[1] = ctx->v.step_s;
+    shape4[2] = ctx->v.step_m;
+    shape4[3] = ctx->v.step_nw;
+  }
+  return KV_TIER_OK;
+}
+
 kv_tier_status kv_tier_score_update(kv_tier_ctx* ctx, int32_t layer, const float* probs, void* stream) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (!probs) return fail(ctx, KV_TIER_E_INVAL, "null probs");
@@ -790,10 +754,6 @@ kv_tier_status kv_tier_score_update(kv_tier_ctx* ctx, int32_t layer, const float
   if (layer < 0 || layer >= ctx->v.L) return fail(ctx, KV_TIER_E_INVAL, "layer out of range");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
-  if (ctx->zflat_pending >= 0) {          // keep layer order: the pending fused update goes first
-    e = launch_score_flush(ctx->v, ctx->zflat_pending, 1, s);
-    ctx->zflat_pending = -1;
-  }
   if (e == cudaSuccess) e = launch_score_update(ctx->v, layer, probs, s);
   return cuda_check(ctx, e, "score_update");
 }
@@ -804,10 +764,6 @@ kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream) {
   if (ctx->lse_pending >= 0) return fail(ctx, KV_TIER_E_STATE, "end_step before kv_tier_score_update_lse");
   cudaError_t e = cudaSuccess;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (ctx->zflat_pending >= 0) {           // flat kernel: the last fused launch's score update
-    e = launch_score_flush(ctx->v, ctx->zflat_pending, 1, s);
-    ctx->zflat_pending = -1;
-  }
   if (e == cudaSuccess && ctx->zpend_n > 0) e = issue_scores(ctx, s);
   if (e == cudaSuccess && ctx->scores_pending) {     // join the score stream: S_part is complete for this step
     e = cudaEventRecord(ctx->ev_score_tail, ctx->score_stream);
@@ -821,6 +777,7 @@ kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream) {
   ctx->zslot_next = 0;
   ctx->zpend_n = 0;
   ctx->step_open = false;
+  ctx->pdl_ok = false;
   ctx->t += 1;
   return KV_TIER_OK;
 }
@@ -940,7 +897,7 @@ kv_tier_status kv_tier_step(kv_tier_ctx* ctx, const void* q, const void* k_new, 
   // dependent launch (each kernel's prologue overlaps the previous layer's tail)
   for (int l = 0; l < v.L && !st; ++l) {
     st = decode_attention_impl(ctx, l, qb + l * qs * 2, kb + l * ks * 2, vb + l * ks * 2, ob + l * os,
-                               fuse_score_update, stream, v.use_pdl && l > 0 && !v.stream_mode);
+                               fuse_score_update, stream, l > 0 && !v.stream_mode);
     if (!st && v.stream_mode && l + 2 < v.L) st = kv_tier_prefetch(ctx, l + 2, side);
   }
   if (st) return st;
@@ -973,7 +930,6 @@ kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const
   ctx->appended_step = astep;
   ctx->zslot_next = 0;
   ctx->zpend_n = 0;
-  ctx->zflat_pending = -1;
   for (auto& b : ctx->slot_busy) b = false;
   ctx->scores_pending = false;
   if (st) { if (g) cudaGraphDestroy(g); return st; }
@@ -1211,13 +1167,13 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
 
 kv_tier_status kv_tier_debug_trace_len(const kv_tier_ctx* ctx, size_t* n) {
   if (!ctx || !n) return fail(nullptr, KV_TIER_E_INVAL, "null arg");
-  *n = (size_t)ctx->v.L * (ctx->v.flat ? ctx->v.nc : ctx->v.split * ctx->v.B * ctx->v.Hkv) * NTRACE;
+  *n = (size_t)ctx->v.L * (std::max(ctx->v.split * ctx->v.B * ctx->v.Hkv, 2 * 148)) * NTRACE;
   return KV_TIER_OK;
 }
 
 kv_tier_status kv_tier_debug_trace(kv_tier_ctx* ctx, uint64_t* host_dst, size_t n) {
   if (!ctx || !host_dst) return fail(ctx, KV_TIER_E_INVAL, "null arg");
-  const size_t need = (size_t)ctx->v.L * (ctx->v.flat ? ctx->v.nc : ctx->v.split * ctx->v.B * ctx->v.Hkv) * NTRACE;
+  const size_t need = (size_t)ctx->v.L * (std::max(ctx->v.split * ctx->v.B * ctx->v.Hkv, 2 * 148)) * NTRACE;
   if (!ctx->trace) return fail(ctx, KV_TIER_E_STATE, "tracing off (set KVTIER_TRACE=1 before kv_tier_init)");
   if (n != need) return fail(ctx, KV_TIER_E_INVAL, "trace needs %zu entries", need);
   cudaError_t e = cudaDeviceSynchronize();
@@ -1368,9 +1324,6 @@ kv_tier_status kv_tier_set_host_t1(kv_tier_ctx* ctx, int32_t on) {
   if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "set_host_t1 inside a step");
   if (on && ctx->v.scorer != KV_TIER_SCORER_ATTENTION) return fail(ctx, KV_TIER_E_STATE, "host-T1 mode supports the attention scorer");
   if (on && ctx->v.seq_w > 1) return fail(ctx, KV_TIER_E_STATE, "host-T1 mode: not with sequence sharding");
-  if (on && ctx->v.flat) return fail(ctx, KV_TIER_E_STATE, "host-T1 mode runs the split kernel (KVTIER_FLAT=0)");
-  if (on && (ctx->v.cluster_merge || ctx->v.last_merge))
-    return fail(ctx, KV_TIER_E_STATE, "host-T1 mode needs the merge kernel (KVTIER_CLUSTER=0, KVTIER_LASTMERGE=0)");
   const size_t ninc = (size_t)ctx->v.B * ctx->v.Hkv * std::max(ctx->v.cap1, 1);
   for (int i = 0; on && i < 2; ++i) {
     if (!ctx->h1_inc[i]) {

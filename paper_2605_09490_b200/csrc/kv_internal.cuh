@@ -50,34 +50,21 @@ struct DevView {
   int host_t1;          // N1: T1 attended on the host (kv_tier_set_host_t1); kernels skip T1
   int out_fp32;
   int split;            // CTAs per (b, g) cluster
-  int chunk_max;        // max tokens per CTA (logit buffer rows)
   int variant;          // decode-attention kernel variant (warps x pipeline stages)
-  int pdl_pre;          // stages the producer may load before griddepcontrol.wait
-  int use_pdl;          // chain consecutive layers with programmatic dependent launch
-  int l2_prefetch;      // pre-wait L2 prefetch of the CTA's stages beyond the shared-memory ring
-  int stage_rr;         // 2: 16-row groups dealt round-robin to the unit's CTAs, 1: whole stages, 0: contiguous
-  int cluster_merge;    // merge the unit's partials in distributed shared memory (cluster of split CTAs)
-  int flat;             // flat decode kernel (attn_flat.cu, KVTIER_FLAT=1) instead of the split kernel
-  int fvariant;         // flat kernel variant (consumer warps x stages)
-  int nc;               // flat kernel grid (CTAs; one per SM)
   int seq_w, seq_r;     // sequence sharding: positions in 64-blocks, block k owned by rank k % seq_w
   int hN;               // rows per group of the pinned host stores (N_max, or a shard's own positions)
   int score_grid;       // CTAs of the score-flush kernel (runs beside the attention chain)
-  int score_lean;       // 1: register-lean score-flush kernel (fits beside two decode CTAs)
-  int last_merge;       // 1: the CTA completing a unit merges its partials (no merge kernel)
-  int spin_hint;        // mbarrier try_wait suspend-time hint in ns (0: plain polling)
-  long long l2pf_bytes; // flat kernel: K/V bytes per CTA requested into L2 at kernel start (0: off)
-  int inflight;         // flat kernel: max ring stages requested but not landed (0: the whole ring)
   unsigned long long* trace;   // debug: per-CTA %globaltimer checkpoints (null = off)
   float* zbuf;          // [ZRING][B*Hkv][zrows][8] logits (log2 domain) of recent launches
   float* ml;            // [ZRING][B*Hkv][16] per-head (max, 1/sum) of recent launches
   int zrows;            // virtual rows per unit (N_max + padding)
   float* part;          // [B*Hkv][split][part_stride] per-CTA partials (m[8], l[8], o[G][D])
   int part_stride;
-  int* unit_ctr;        // [B*Hkv] partials published per unit (flat kernel, KVTIER_LASTMERGE; reset by the merger)
   // whole-step kernel (step.cu): step_k CTAs in all; step_s > 1: a cluster of step_s CTAs per kv
   // head (row slices), else step_m kv heads per CTA.  step_k = 0: the step runs per layer.
   int step_k, step_s, step_m;
+  int split_req;        // kv_tier_config::split (0 = auto): also fixes the step kernel's CTAs per kv head
+  int step_nw;          // consumer warps per CTA: 8 (one CTA per SM) or 4 (two CTAs per SM)
   int* step_done;       // [L][B] CTAs of request b that finished layer l (zeroed by k_begin_step)
   void* hot_base;       // L2 access-policy window over the small hot buffers
   size_t hot_bytes;
@@ -256,10 +243,6 @@ cudaError_t launch_offload_host(const DevView& v, int cur, cudaStream_t s);
 cudaError_t launch_commit(const DevView& v, cudaStream_t s);
 cudaError_t launch_prefetch(const DevView& v, int layer, cudaStream_t s);
 size_t attn_smem_bytes(const DevView& v);
-size_t flat_smem_bytes(const DevView& v);
-cudaError_t flat_configure(const DevView& v);
-cudaError_t launch_decode_flat(const DevView& v, int layer, const void* q, const void* knew, const void* vnew,
-                               void* o, int zpar, int zprev, int pdl, cudaStream_t s);
 size_t merge_smem_bytes(const DevView& v);
 cudaError_t attn_configure(const DevView& v);
 size_t step_smem_bytes(const DevView& v);

@@ -34,6 +34,10 @@
 //                  layer order, AMB-14).
 #include "decode_common.cuh"
 
+#ifndef KVT_TRACE
+#define KVT_TRACE 0   // debug builds (-DKVT_TRACE=1): per-(layer, CTA) timeline in the ctx trace buffer
+#endif
+
 namespace kvt {
 
 // ----------------------------------------------------------------- cluster / async-proxy PTX
@@ -66,7 +70,7 @@ __device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
 __device__ __forceinline__ void red_relaxed_gpu(int* p, int x) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(x) : "memory");
 }
-// CTA-local mbarrier wait that suspends until the phase completes
+// CTA-local mbarrier wait that suspends until the phase completes (no issue slots while waiting)
 __device__ __forceinline__ void mbar_sleep_wait(uint32_t a, uint32_t parity) { mbar_wait_hint(a, parity, 1000000u); }
 
 // ----------------------------------------------------------------- work split
@@ -94,7 +98,7 @@ constexpr int SD_FIRST = 1, SD_LAST = 2, SD_T2 = 4;
 constexpr int STEP_MAXM = 8;   // kv heads per CTA when s == 1
 
 template <int D, int NW, int NST>
-__global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView v, const StepIO io) {
+__global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(const DevView v, const StepIO io) {
   constexpr int NCONS = NW * 32;
   constexpr int WPROD = NW, WNEW = NW + 1, WSC0 = NW + 2;   // + two score warps
   constexpr int NSC = 64;                                    // score-pass threads
@@ -117,8 +121,11 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
   const int ZS = v.zring;
   const int tot = G * D;                          // o floats per kv head
   const int SL = ((tot + S - 1) / S + 3) & ~3;    // o floats per slice (s > 1)
-  auto trace = [&](int l, int slot) {             // debug timeline (KVTIER_TRACE=1)
-    if (v.trace) v.trace[((size_t)l * gridDim.x + blockIdx.x) * NTRACE + slot] = gtimer();
+  auto trace = [&](int l, int slot) {             // debug timeline: %globaltimer
+    if (KVT_TRACE && v.trace) v.trace[((size_t)l * gridDim.x + blockIdx.x) * NTRACE + slot] = gtimer();
+  };
+  auto ctrace = [&](int l, int slot) {            // debug: SM clock (intra-CTA intervals)
+    if (KVT_TRACE && v.trace) v.trace[((size_t)l * gridDim.x + blockIdx.x) * NTRACE + slot] = clock64();
   };
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -133,10 +140,12 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
   float* ntv = ntz + 16;                                                   // [2][D] new-token V row
   float* sml = ntv + 2 * D;                                                // [ZRING][STEP_MAXM][16] (M, 1/L) for a4
   float* smisc = sml + ZRING * STEP_MAXM * 16;                             // [24] merge scalars
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smisc + 24);
+  float* fac = smisc + 24;                                                 // [16][8] merge factors (S <= 16)
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(fac + 16 * 8);
   // full[NST] empty[NST] nfull[2] nempty[2] rxb[2] done[2]
   int4* sdesc = reinterpret_cast<int4*>(bars + 2 * NST + 8);               // [NST]
-  volatile int* sc_done = reinterpret_cast<volatile int*>(sdesc + NST);    // layers whose a4 pass is complete
+  StepPart* ptab = reinterpret_cast<StepPart*>(sdesc + NST);               // [STEP_MAXM] this CTA's parts
+  volatile int* sc_done = reinterpret_cast<volatile int*>(ptab + STEP_MAXM);   // layers whose a4 pass is complete
   volatile int* ml_done = sc_done + 1;                                     // layers merged ((M, 1/L) in sml)
 
   const int cur = v.st->cur, sb = v.st->scur;
@@ -145,7 +154,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
   const int gbf = sg.a2 >> 4, gq2 = (sg.n2 + 15) >> 4, ng = gbf + gq2, cu = 2 * gbf + gq2;
   const int npart = S > 1 ? 1 : Mh;
   const int slice = S > 1 ? (int)cluster_rank() : 0;   // the cluster is one kv head's S slices
-  auto part = [&](int k) -> StepPart {
+  auto part_calc = [&](int k) -> StepPart {
     StepPart p;
     if (S > 1) {
       p.g = rk / S;
@@ -160,6 +169,8 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
     }
     return p;
   };
+  if (tid < npart) ptab[tid] = part_calc(tid);              // constant for the step: no per-stage division
+  auto part = [&](int k) -> StepPart { return ptab[k]; };
 
   const uint32_t ring_s = smem_u32(ring);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + NST);
@@ -195,8 +206,9 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
     *ml_done = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  __syncthreads();                              // part table, barriers, counters
   if (S > 1) cluster_sync_all();                // every peer's barriers exist before any remote use
-  if (v.trace && blockIdx.x == 0 && tid == 0) v.trace[NTRACE - 1] = gridDim.x;
+  if (KVT_TRACE && v.trace && blockIdx.x == 0 && tid == 0) v.trace[NTRACE - 1] = gridDim.x;
 
   if (w == WPROD) {
     // ================================ producer ================================
@@ -550,18 +562,20 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
       const int l = dsc.x;
       if (l < 0) break;
       const int kpart = dsc.y, j = dsc.z, fl = dsc.w & 0xFF, cnt = dsc.w >> 8;
+
       const StepPart pp = part(kpart);
       const int g = pp.g, u = b * Hkv + g;
       if (fl & SD_FIRST) {
         if (kpart == 0) {
           // q(l) is a projection of o(l-1): every CTA of this request has stored its part
+          if (tid == 0) ctrace(l, 12);
           if (lane == 0) {
             if (l > 0) wait_layer(l);
             if (io.score)
               while (*sc_done < l - ZS + 1) __nanosleep(128);   // logit slot of layer l - ZS consumed
           }
           __syncwarp();
-          if (tid == 0) trace(l, 1);
+          if (tid == 0) { trace(l, 1); ctrace(l, 13); }
         }
         const __nv_bfloat16* qh = io.q + (((size_t)l * B + b) * v.Hq + g * G + gq) * D;
 #pragma unroll
@@ -578,6 +592,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
         la = lb = 0.f;
 #pragma unroll
         for (int mt = 0; mt < KS; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
+        if (tid == 0 && kpart == 0) { asm volatile("" :: "r"(qf[KS - 1][1])); ctrace(l, 14); }   // q loaded
         zrow = io.score ? v.zbuf + (size_t)(l % ZS) * U * v.zrows * 8 + (size_t)u * v.zrows * 8 : nullptr;
       }
       if (cnt > 0) {
@@ -626,14 +641,14 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
       if (!(fl & SD_LAST)) continue;
 
       // ---------------- part end: warps -> CTA partial (m, l, o) in pbuf
-      if (tid == 0 && kpart == 0) trace(l, 2);
+      if (tid == 0 && kpart == 0) ctrace(l, 15);
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) {
         la += __shfl_xor_sync(0xffffffffu, la, off);
         lb += __shfl_xor_sync(0xffffffffu, lb, off);
       }
       if (tid == 0 && S > 1) bulk_wait_read0();              // the previous push has read pbuf
-      named_sync(1, NCONS);                                  // ow / redm / pbuf free
+      // (ow / redm are free: the previous merge ended with a barrier)
       if (lane < 4) {
         redm[w * 8 + 2 * lane] = mxa;
         redm[w * 8 + 2 * lane + 1] = mxb;
@@ -682,8 +697,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
           oacc[mt][3] += o1[8];
         }
       }
-      named_sync(1, NCONS);
-      if (w < NH) put(w);
+      if (w < NH) put(w);                                    // same slot this warp just read: no barrier
       named_sync(1, NCONS);
       if (tid < 8) {
         float M = -INFINITY;
@@ -706,7 +720,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
         pbuf[16 + e] = a;
       }
       const int par = l & 1;
-      if (tid == 0 && kpart == 0) trace(l, 6);               // CTA partial in pbuf
+      if (tid == 0 && kpart == 0) ctrace(l, 16);             // CTA partial in pbuf
       if (S > 1) {
         // ---------------- DSMEM exchange: (m, l) + o slice r of this partial -> slice r's CTA.
         // Every push carries 16 + SL floats (the last slice is padded from pbuf's tail), so each
@@ -729,37 +743,45 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
       // ---------------- merge: this CTA's share of o (slice, or the whole head) + the new token
       const int nslot = nts & 1;
       mbar_sleep_wait(nfull0 + 8 * nslot, (nts >> 1) & 1);   // the new token's term (every CTA of the head)
-      if (tid == 0 && kpart == 0) trace(l, 7);               // new token ready
+      if (tid == 0 && kpart == 0) ctrace(l, 17);             // new token ready
       if (S > 1) mbar_sleep_wait(rxb0 + 8 * par, (nrx >> 1) & 1);
       named_sync(1, NCONS);                                   // pbuf complete (S == 1)
-      if (tid == 0 && kpart == 0) trace(l, 8);               // peers' partials landed
+      if (tid == 0 && kpart == 0) ctrace(l, 18);             // peers' partials landed
       const int nsrc = S > 1 ? S : 1;
       const float* src0 = S > 1 ? rx + par * S * (16 + SL) : pbuf;   // partial 0 of the merge
       const int sstride = 16 + SL;                            // between received partials
       const int e_beg = S > 1 ? slice * SL : 0;
       const int e_end = S > 1 ? min(tot, e_beg + SL) : tot;
-      float* fac = redm;                                      // [nsrc][8] factors (redm/redl are free now)
       float* sIL = smisc;                                     // [8] 1/L
       float* sFN = smisc + 8;                                 // [8] new-token factor
-      if (tid < 8) {
-        const float zn = ntz[nslot * 8 + tid];
+      if (w == 0) {
+        // warp 0: lane = (source group j = lane >> 3, head h = lane & 7); sources j, j+4, ... ;
+        // max and sum over the source groups by shuffles (fixed order: deterministic)
+        const int h = lane & 7, j = lane >> 3;
+        const float zn = ntz[nslot * 8 + h];
         float M = zn;
-        for (int x = 0; x < nsrc; ++x) M = fmaxf(M, src0[x * sstride + tid]);
+        for (int x = j; x < nsrc; x += 4) M = fmaxf(M, src0[x * sstride + h]);
+        M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 8));
+        M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 16));
         float Ls = 0.f;
-        for (int x = 0; x < nsrc; ++x) {
-          const float m = src0[x * sstride + tid];
+        for (int x = j; x < nsrc; x += 4) {
+          const float m = src0[x * sstride + h];
           const float f = m == -INFINITY ? 0.f : ex2_ftz(m - M);
-          fac[x * 8 + tid] = f;
-          Ls += f * src0[x * sstride + 8 + tid];
+          fac[x * 8 + h] = f;
+          Ls += f * src0[x * sstride + 8 + h];
         }
-        const float fn = zn == -INFINITY ? 0.f : ex2_ftz(zn - M);
-        Ls += fn;
-        const float il = Ls > 0.f ? 1.0f / Ls : 0.f;
-        sIL[tid] = il;
-        sFN[tid] = fn;
-        float* mlw = sml + ((l % ZS) * STEP_MAXM + kpart) * 16;
-        mlw[tid] = tid < G ? M : 0.f;
-        mlw[8 + tid] = tid < G ? il : 0.f;
+        Ls += __shfl_xor_sync(0xffffffffu, Ls, 8);
+        Ls += __shfl_xor_sync(0xffffffffu, Ls, 16);
+        if (j == 0) {
+          const float fn = zn == -INFINITY ? 0.f : ex2_ftz(zn - M);
+          Ls += fn;
+          const float il = Ls > 0.f ? 1.0f / Ls : 0.f;
+          sIL[h] = il;
+          sFN[h] = fn;
+          float* mlw = sml + ((l % ZS) * STEP_MAXM + kpart) * 16;
+          mlw[h] = h < G ? M : 0.f;
+          mlw[8 + h] = h < G ? il : 0.f;
+        }
       }
       named_sync(1, NCONS);
       for (int e = e_beg + 4 * tid; e < e_end; e += 4 * NCONS) {
@@ -782,7 +804,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
         store_o(l, g, e, acc);
       }
       named_sync(1, NCONS);                                   // o stored, rx / ntv / fac read
-      if (tid == 0 && kpart == 0) trace(l, 9);
+      if (tid == 0 && kpart == 0) ctrace(l, 19);
       if (tid == 0) {
         mbar_arrive(nempty0 + 8 * nslot);
         if (kpart == npart - 1) {
@@ -793,7 +815,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
           // stage on chip); it deliberately does not wait for the global o stores to drain behind
           // the K/V stream -- they are visible at kernel end.
           red_relaxed_gpu(done_ctr + (size_t)l * B + b, 1);
-          trace(l, 4);
+          ctrace(l, 20);
         }
       }
       ++nts;
@@ -806,11 +828,11 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1) k_decode_step(const DevView 
 }
 
 // ----------------------------------------------------------------- host side
-constexpr int STEP_NW = 8;                                        // consumer warps
-
-template <int D, int NST>
+// Two shapes: 8 consumer warps, one CTA per SM (NW = 8), or 4 consumer warps, two CTAs per SM
+// (NW = 4: twice the CTAs, so a request's rows are cut into twice as many slices and two
+// requests' layer chains share each SM).  DevView::step_nw selects.
+template <int D, int NW, int NST>
 static size_t step_smem_bytes_t(const DevView& v) {
-  constexpr int NW = STEP_NW;
   const int S = v.step_s > 0 ? v.step_s : 1;
   const int tot = v.G * D, SL = ((tot + S - 1) / S + 3) & ~3;
   size_t s = (size_t)NST * 2 * NW * 16 * D * 2;                  // ring
@@ -819,33 +841,41 @@ static size_t step_smem_bytes_t(const DevView& v) {
   s += (size_t)(16 + 8 * D + 4 * 16) * 4;                        // pbuf (+ tail read by the padded last slice)
   s += (size_t)2 * S * (16 + SL) * 4;                            // rx
   s += (size_t)2 * NW * 8 * 4 + 16 * 4 + 2 * D * 4;              // redm, redl, ntz, ntv
-  s += (size_t)ZRING * STEP_MAXM * 16 * 4 + 24 * 4;              // sml, merge scalars
-  s += (2 * NST + 8) * 8 + NST * 16 + 16;                        // barriers, descriptors, counters
+  s += (size_t)ZRING * STEP_MAXM * 16 * 4 + 24 * 4 + 16 * 8 * 4; // sml, merge scalars, merge factors
+  s += (2 * NST + 8) * 8 + NST * 16 + STEP_MAXM * sizeof(StepPart) + 16;   // barriers, descriptors, parts, counters
   return s;
 }
 
-// ring depth: as many stages as fit beside the scratch (one CTA per SM)
+// ring depth: as many stages as fit beside the scratch
 static int step_nst(const DevView& v) {
+  if (v.step_nw == 4) return v.D == 128 ? 2 : 4;                 // two CTAs per SM
   if (v.D == 128) return v.cap2 > 0 ? 2 : 3;
   return v.cap2 > 0 ? 5 : 6;
 }
 
+#define KVT_STEP_SHAPES(X)                                          \
+  X(128, 8, 3) X(128, 8, 2) X(64, 8, 6) X(64, 8, 5) X(128, 4, 2) X(64, 4, 4)
+
 size_t step_smem_bytes(const DevView& v) {
   const int nst = step_nst(v);
-  if (v.D == 128) return nst == 3 ? step_smem_bytes_t<128, 3>(v) : step_smem_bytes_t<128, 2>(v);
-  return nst == 6 ? step_smem_bytes_t<64, 6>(v) : step_smem_bytes_t<64, 5>(v);
+#define KVT_SZ(DD, NWW, NSS) \
+  if (v.D == DD && v.step_nw == NWW && nst == NSS) return step_smem_bytes_t<DD, NWW, NSS>(v);
+  KVT_STEP_SHAPES(KVT_SZ)
+#undef KVT_SZ
+  return ~(size_t)0;
 }
 
-template <int D, int NST>
-static cudaError_t step_conf_t(const DevView& v, int K, int* clusters) {
-  auto kern = k_decode_step<D, STEP_NW, NST>;
-  const size_t smem = step_smem_bytes_t<D, NST>(v);
+template <int D, int NW, int NST>
+static cudaError_t step_conf_t(const DevView& v, int* clusters) {
+  auto kern = k_decode_step<D, NW, NST>;
+  const size_t smem = step_smem_bytes_t<D, NW, NST>(v);
+  const int K = v.step_s;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(v.B * v.Hkv * v.step_s / v.step_m, 1, 1);
-  cfg.blockDim = dim3((STEP_NW + 4) * 32, 1, 1);
+  cfg.blockDim = dim3((NW + 4) * 32, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -857,21 +887,23 @@ static cudaError_t step_conf_t(const DevView& v, int K, int* clusters) {
   return cudaOccupancyMaxActiveClusters(clusters, kern, &cfg);
 }
 
-// Co-resident clusters of v.step_s CTAs (0: the shape cannot run).
+// Co-resident clusters of v.step_s CTAs of the v.step_nw shape (0: it cannot run).
 cudaError_t step_configure(const DevView& v, int* clusters) {
   *clusters = 0;
   const int nst = step_nst(v);
-  const int K = v.step_s;
-  if (v.D == 128) return nst == 3 ? step_conf_t<128, 3>(v, K, clusters) : step_conf_t<128, 2>(v, K, clusters);
-  return nst == 6 ? step_conf_t<64, 6>(v, K, clusters) : step_conf_t<64, 5>(v, K, clusters);
+#define KVT_CF(DD, NWW, NSS) \
+  if (v.D == DD && v.step_nw == NWW && nst == NSS) return step_conf_t<DD, NWW, NSS>(v, clusters);
+  KVT_STEP_SHAPES(KVT_CF)
+#undef KVT_CF
+  return cudaErrorInvalidValue;
 }
 
-template <int D, int NST>
+template <int D, int NW, int NST>
 static cudaError_t step_launch_t(const DevView& v, const StepIO& io, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(v.step_k, 1, 1);                  // step_k = total CTAs
-  cfg.blockDim = dim3((STEP_NW + 4) * 32, 1, 1);
-  cfg.dynamicSmemBytes = step_smem_bytes_t<D, NST>(v);
+  cfg.blockDim = dim3((NW + 4) * 32, 1, 1);
+  cfg.dynamicSmemBytes = step_smem_bytes_t<D, NW, NST>(v);
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   int na = 0;
@@ -891,7 +923,7 @@ static cudaError_t step_launch_t(const DevView& v, const StepIO& io, cudaStream_
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, k_decode_step<D, STEP_NW, NST>, v, io);
+  return cudaLaunchKernelEx(&cfg, k_decode_step<D, NW, NST>, v, io);
 }
 
 cudaError_t launch_decode_step(const DevView& v, const void* q, const void* knew, const void* vnew, void* o, int score,
@@ -903,8 +935,11 @@ cudaError_t launch_decode_step(const DevView& v, const void* q, const void* knew
   io.o = o;
   io.score = score;
   const int nst = step_nst(v);
-  if (v.D == 128) return nst == 3 ? step_launch_t<128, 3>(v, io, s) : step_launch_t<128, 2>(v, io, s);
-  return nst == 6 ? step_launch_t<64, 6>(v, io, s) : step_launch_t<64, 5>(v, io, s);
+#define KVT_LN(DD, NWW, NSS) \
+  if (v.D == DD && v.step_nw == NWW && nst == NSS) return step_launch_t<DD, NWW, NSS>(v, io, s);
+  KVT_STEP_SHAPES(KVT_LN)
+#undef KVT_LN
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace kvt

@@ -75,6 +75,7 @@ _SIGS = {
                             C.c_void_p],
     "kv_tier_score_update": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p],
     "kv_tier_visible_count": [C.c_void_p, C.POINTER(C.c_int32)],
+    "kv_tier_layout": [C.c_void_p, C.c_void_p, C.c_void_p],
     "kv_tier_end_step": [C.c_void_p, C.c_void_p],
     "kv_tier_step": [C.c_void_p] + [C.c_void_p] * 4 + [C.c_int32, C.c_void_p, C.c_void_p],
     "kv_tier_step_graph_capture": [C.c_void_p] + [C.c_void_p] * 4 + [C.c_int32, C.c_void_p, C.c_void_p],
@@ -246,6 +247,14 @@ class KvTier:
         n = C.c_int32()
         _check(load().kv_tier_visible_count(self.ctx, C.byref(n)), self.ctx)
         return n.value
+
+    def layout(self):
+        """(tier counts [T0, T1, T2, T3] of the current layout, step-kernel shape [CTAs, CTAs per
+        kv head, kv heads per CTA, consumer warps]) from the host mirror (no device sync)."""
+        c = np.zeros(4, dtype=np.int32)
+        sh = np.zeros(4, dtype=np.int32)
+        _check(load().kv_tier_layout(self.ctx, c.ctypes.data_as(C.c_void_p), sh.ctypes.data_as(C.c_void_p)), self.ctx)
+        return c.tolist(), sh.tolist()
 
     def end_step(self, stream=None):
         _check(load().kv_tier_end_step(self.ctx, _stream_ptr(stream)), self.ctx)

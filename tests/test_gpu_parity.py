@@ -145,20 +145,20 @@ def test_tiny_graph_stream_mode():
 
 
 @pytest.mark.parametrize("split", [1, 3, 8])
-def test_tiny_cluster_splits(split):          # DSMEM merge at several cluster sizes
-    _run_pair(H.workload("tiny", interval=8, B=3, L=2, steps=17), split=split)
+def test_tiny_layer_kernel_splits(split):     # per-layer kernel: CTAs per unit, PDL merge
+    _run_pair(H.workload("tiny", interval=8, B=3, L=2, steps=17), split=split, layers_api=True)
 
 
 @pytest.mark.parametrize("variant", range(6))
-def test_multi_request_multi_layer_graph(variant):   # several tiles, ragged tails, B > 1, d = 128
+def test_multi_request_multi_layer_variants(variant):   # per-layer kernel variants: tiles, ragged tails, d = 128
     w = H.workload("tiny", B=3, L=2, Hq=12, Hkv=2, d=128, N=700, P=40, interval=16, steps=40,
                    hbm_bp=3000, evict_bp=1000, t2_bp=0 if variant == 3 else 2500)
-    _run_pair(w, graph=True, check_every=7, variant=variant, split=(0, 4, 2, 3, 1, 16)[variant])
+    _run_pair(w, layers_api=True, check_every=7, variant=variant, split=(0, 4, 2, 3, 1, 16)[variant])
 
 
 @pytest.mark.parametrize("variant", [0, 2, 5])
 def test_tiny_variants(variant):                      # d = 64 kernels
-    _run_pair(H.workload("tiny", interval=8, t2_bp=3000, B=2, L=2, steps=20), graph=True, variant=variant)
+    _run_pair(H.workload("tiny", interval=8, t2_bp=3000, B=2, L=2, steps=20), layers_api=True, variant=variant)
 
 
 # --------------------------------------------------------------------- 7B-shaped, sampled
@@ -327,71 +327,31 @@ def test_abi_errors():
     run.close()
 
 
-# --------------------------------------------------------------------- cluster (DSMEM) merge
-@pytest.mark.parametrize("split", [1, 3, 8])
-def test_cluster_merge_parity(split, monkeypatch):
-    monkeypatch.setenv("KVTIER_CLUSTER", "1")
-    w = H.workload("tiny", B=3, L=2, Hq=12, Hkv=2, d=128, N=700, P=40, interval=16, steps=34,
-                   hbm_bp=3000, evict_bp=1000, t2_bp=2500)
-    _run_pair(w, graph=True, check_every=5, split=split)
+# --------------------------------------------------------------------- whole-step kernel shapes
+# kv_tier_step picks (slices per kv head s, heads per CTA m, warps per CTA) from the config;
+# these shapes drive its extremes: one head cut into 16 slices, many heads per CTA, d = 64,
+# G = 1 and G = 8, a ragged T2 segment, events every 4 steps.
+@pytest.mark.parametrize("shape", [
+    dict(B=1, Hq=8, Hkv=1, d=128, N=900, P=16),         # 1 kv head over a 16-CTA cluster
+    dict(B=24, Hq=16, Hkv=8, d=64, N=120, P=16),        # 192 heads: several heads per CTA
+    dict(B=3, Hq=3, Hkv=3, d=128, N=333, P=20),         # G = 1
+    dict(B=2, Hq=16, Hkv=2, d=64, N=701, P=64)])        # G = 8, d = 64
+def test_step_kernel_shapes(shape):
+    w = H.workload("tiny", L=3, interval=4, steps=13, hbm_bp=4000, evict_bp=800, t2_bp=3000, **shape)
+    _run_pair(w, graph=True, check_every=2)
 
 
-def test_cluster_merge_equals_merge_kernel_bitwise(monkeypatch):
-    # same partials, same merge order and arithmetic -> same bits (o and scores)
-    w = H.workload("tiny", B=2, L=3, Hq=12, Hkv=2, d=128, N=500, P=40, interval=8, steps=24,
-                   hbm_bp=3000, evict_bp=1000, t2_bp=2500)
-    outs, scores = [], []
-    for mode in ("0", "1"):
-        monkeypatch.setenv("KVTIER_CLUSTER", mode)
-        run = H.TieredDecode(w, split=4)
-        run.capture()
-        seq = []
-        for _ in range(w["steps"]):
-            run.step()
-            seq.append(run.output().copy())
-        run.sync()
-        outs.append(np.stack(seq))
-        scores.append(run.kv.export(kt.X_SCORES).copy())
-        run.close()
-    assert np.array_equal(outs[0], outs[1])
-    assert np.array_equal(scores[0], scores[1])
-
-
-# --------------------------------------------------------------------- flat work distribution
-@pytest.mark.parametrize("fvar,t2", [("0", 0), ("1", 2500), ("2", 2500)])
-def test_flat_kernel_parity(fvar, t2, monkeypatch):
-    # one CTA per SM over the flat (unit, 16-row group) list; units span several CTAs, merged
-    # by the CTA that owns their first group (attn_flat.cu).  Events every 16 steps.
-    monkeypatch.setenv("KVTIER_FLAT", "1")
-    monkeypatch.setenv("KVTIER_FVAR", fvar)
-    w = H.workload("tiny", B=3, L=2, Hq=12, Hkv=2, d=128, N=700, P=40, interval=16, steps=34,
-                   hbm_bp=3000, evict_bp=1000, t2_bp=t2)
-    _run_pair(w, graph=True, check_every=5)
-
-
-@pytest.mark.parametrize("shape", [dict(B=1, Hq=4, Hkv=1, d=64, N=300, P=16),      # 1 unit over many CTAs
-                                   dict(B=24, Hq=8, Hkv=4, d=64, N=120, P=16)])    # many units per CTA
-def test_flat_kernel_partition_extremes(shape, monkeypatch):
-    monkeypatch.setenv("KVTIER_FLAT", "1")
-    w = H.workload("tiny", L=2, interval=8, steps=18, hbm_bp=5000, evict_bp=500, t2_bp=0, **shape)
-    _run_pair(w, graph=True, check_every=3)
-
-
-def test_flat_kernel_7b_sampled(monkeypatch):
-    # BASELINE.json configs[1] shape, launch configuration of bench.py (graph, PDL), sampled
-    # requests against the oracle
-    monkeypatch.setenv("KVTIER_FLAT", "1")
-    w = H.workload("7b", steps=3)
-    _run_pair(w, reqs=[0, 5], graph=True, check_every=1)
-
-
-def test_contiguous_stage_ranges(monkeypatch):   # KVTIER_RR=0: contiguous stage ranges per CTA
-    monkeypatch.setenv("KVTIER_RR", "0")
-    w = H.workload("tiny", B=3, L=2, Hq=12, Hkv=2, d=128, N=700, P=40, interval=16, steps=34,
-                   hbm_bp=3000, evict_bp=1000, t2_bp=2500)
-    _run_pair(w, graph=True, check_every=5, split=3)
-    monkeypatch.setenv("KVTIER_CLUSTER", "1")
-    _run_pair(w, graph=True, check_every=5, split=5)
+@pytest.mark.parametrize("s", [1, 2, 3, 5, 9, 16])
+def test_step_kernel_slices_per_head(s):
+    # the config's split fixes the cluster size (row slices per kv head): odd sizes, a 9-CTA and a
+    # 16-CTA cluster, G = 5 (14B/32B head ratio), a ragged T2 segment
+    w = H.workload("tiny", B=2, L=2, Hq=20, Hkv=4, d=128, N=900, P=64, interval=4, steps=9, hbm_bp=5000,
+                   evict_bp=300, t2_bp=2500)
+    run = H.TieredDecode(w, split=s)
+    shape = run.kv.layout()[1]
+    run.close()
+    assert shape[1] == s or shape[0] == 0
+    _run_pair(w, graph=True, check_every=2, split=s)
 
 
 # --------------------------------------------------------------------- KV-head sharding (§8e row 2)
@@ -771,7 +731,8 @@ def test_randomized_configs(seed):
                    policy=pol, budget=int(rng.integers(P + 140, N + 50)) if pol in (2, 3) else 0,
                    policy_seed=seed, scorer=int(rng.choice([0, 0, kt.SCORER_VATP, kt.SCORER_REDUNDANCY,
                                                              kt.SCORER_COMBINED])))
-    _run_pair(w, graph=bool(rng.integers(0, 2)), check_every=3)
+    api = int(rng.integers(0, 3))             # step graph / kv_tier_step (whole-step kernel) / per-layer ABI
+    _run_pair(w, graph=api == 0, layers_api=api == 2, check_every=3)
 
 
 @pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVT_FUZZ_SEEDS_SEQ", "24"))))
