@@ -149,20 +149,27 @@ kv_tier_status validate(const kv_tier_config* c) {
   return KV_TIER_OK;
 }
 
-// Capacities (rows per (l, b, g)).  T0 must hold the initial prefix (all T0 until the
-// first event) and, after an event, P u top-n_hbm plus Delta appends (AMB-25).
+// Capacities (rows per (l, b, g)).  T0 holds the steady state, not the whole chain: after an
+// event P u the top n_hbm survivors, plus the Delta tokens appended before the next event
+// (AMB-25), n_hbm <= beta * (N - |P|) (Alg. 1); a longer prefix starts partly in T1
+// (AMB-26).  T1 (staging / stream ring) and T2 hold the offloaded share.  Every store is single-
+// buffered: migrate moves rows in place (chunked through mtemp).
+int delta_slack(const kv_tier_config& c) { return std::max(16, c.manage_interval) + 16; }
 void capacities(const kv_tier_config& c, int* cap0, int* cap1, int* cap2) {
   const long long N = c.max_tokens;
-  const long long prot = (long long)c.prompt_len + c.sink_size + c.window_size;
-  const long long hbm = ((long long)c.hbm_ratio_bp * N + 9999) / 10000;
-  (void)prot; (void)hbm;   // v1: T0 sized for the whole chain (the prefix starts all-T0)
+  const long long prot = std::min<long long>(N, (long long)c.prompt_len + c.sink_size + c.window_size);
   // a sequence shard stores only its own positions: every store is bounded by that count
   const long long own = c.shard == KV_TIER_SHARD_SEQUENCE
                             ? seq_owned_below(c.world, c.rank, (int)N) + SEQ_BLOCK : N;
   const long long Nc = std::min<long long>(N, own);
-  long long c0 = Nc;
+  long long keep;                                            // live tokens an event may keep in T0
+  if (c.policy == KV_TIER_POLICY_STREAMING) keep = 0;
+  else if (c.policy == KV_TIER_POLICY_H2O || c.policy == KV_TIER_POLICY_RANDOM) keep = c.budget;
+  else keep = ((long long)c.hbm_ratio_bp * (N - prot) + 9999) / 10000;
+  long long c0 = std::min<long long>(Nc, prot + keep + delta_slack(c));
+  const long long load0 = std::max<long long>(0, c0 - delta_slack(c));     // prefix rows loaded into T0
   const long long off = ((long long)(10000 - c.hbm_ratio_bp) * N + 9999) / 10000 + 2;
-  long long c1 = std::min<long long>(Nc, off);
+  long long c1 = std::min<long long>(Nc, std::max<long long>(off, Nc - load0));
   long long c2 = c.t2_fraction_bp ? std::min<long long>(Nc, (off * c.t2_fraction_bp + 9999) / 10000 + 2) : 0;
   if (c.shard == KV_TIER_SHARD_SEQUENCE && c.world > 1) {
     // a shard's T1/T2 share tracks the global fraction (block-cyclic ownership): 1.25x its fair
@@ -225,13 +232,20 @@ int host_rows_of(const kv_tier_config& c) {
 }
 
 
-// Rows an incremental migrate may move per request; more -> full rebuild (first event).
+// Rows a migrate may move per request: every position at most once, so an event never overflows.
 size_t mcap_of(const kv_tier_config& c) {
-  const char* ov = getenv("KVTIER_MCAP");                    // test hook: force the full-rebuild path
-  if (ov && atoi(ov) > 0) return (size_t)atoi(ov);
   const size_t n = c.shard == KV_TIER_SHARD_SEQUENCE ? (size_t)seq_owned_below(c.world, c.rank, c.max_tokens) + SEQ_BLOCK
                                                     : (size_t)c.max_tokens;
-  return std::max<size_t>(256, (n / 8 + 15) / 16 * 16);
+  return (n + 15) / 16 * 16;
+}
+// (layer, kv head) pairs per migrate chunk: mtemp (B * mcap rows of 4d bytes per pair) stays
+// within 64 MB.  KVTIER_MCHUNK (test hook) forces smaller chunks; results never depend on it.
+int mchunk_of(const kv_tier_config& c) {
+  const size_t per = (size_t)c.num_requests * mcap_of(c) * 4 * c.head_dim;
+  int k = (int)std::max<size_t>(1, ((size_t)64 << 20) / per);
+  k = std::min(k, c.num_layers * c.num_kv_heads);
+  if (const char* ov = getenv("KVTIER_MCHUNK")) k = std::max(1, std::min(k, atoi(ov)));
+  return k;
 }
 
 Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
@@ -244,26 +258,24 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   const bool stream = c.staging_tokens == 0;
   size_t s0 = o;
   const size_t SL = STORE_SLACK_ROWS;
-  for (int i = 0; i < 2; ++i) { L.off_k0[i] = take((LBH * cap0 + SL) * D * 2); L.off_v0[i] = take((LBH * cap0 + SL) * D * 2); }
+  L.off_k0[0] = L.off_k0[1] = take((LBH * cap0 + SL) * D * 2);     // single-buffered row stores
+  L.off_v0[0] = L.off_v0[1] = take((LBH * cap0 + SL) * D * 2);
   L.b_t0 = o - s0; s0 = o;
-  if (stream) {
-    L.off_k1[0] = L.off_k1[1] = take((2 * BH * cap1 + SL) * D * 2);
-    L.off_v1[0] = L.off_v1[1] = take((2 * BH * cap1 + SL) * D * 2);
-  } else {
-    for (int i = 0; i < 2; ++i) { L.off_k1[i] = take((LBH * cap1 + SL) * D * 2); L.off_v1[i] = take((LBH * cap1 + SL) * D * 2); }
-  }
+  const size_t g1 = stream ? 2 * BH : LBH;                      // stream mode: a 2-layer ring
+  L.off_k1[0] = L.off_k1[1] = take((g1 * cap1 + SL) * D * 2);
+  L.off_v1[0] = L.off_v1[1] = take((g1 * cap1 + SL) * D * 2);
   L.b_t1 = o - s0; s0 = o;
-  for (int i = 0; i < 2; ++i) {
-    L.off_c2k[i] = take(LBH * cap2 * D); L.off_c2v[i] = take(LBH * cap2 * D);
-    L.off_s2k[i] = take(LBH * cap2 * 4); L.off_s2v[i] = take(LBH * cap2 * 4);
-  }
+  L.off_c2k[0] = L.off_c2k[1] = take(LBH * cap2 * D);
+  L.off_c2v[0] = L.off_c2v[1] = take(LBH * cap2 * D);
+  L.off_s2k[0] = L.off_s2k[1] = take(LBH * cap2 * 4);
+  L.off_s2v[0] = L.off_s2v[1] = take(LBH * cap2 * 4);
   L.b_t2 = o - s0; s0 = o;
-  // migrate staging (cold)
+  // migrate staging (cold): the move list and one chunk of (layer, kv head) pairs in flight
   const size_t mcap = mcap_of(c);
   L.off_moves = take(B * mcap * 16);
   L.off_mcount = take(B * 4);
   L.off_scratch = take(B * N * 4);
-  L.off_mtemp = take(B * mcap * LBH / B * 2 * D * 2);
+  L.off_mtemp = take(B * mcap * (size_t)mchunk_of(c) * 2 * D * 2);
   // hot, small: kept resident in L2 (access-policy window from off_S to the end)
   L.off_S = take(BH * N * 4);
   L.off_z = take(zring_of(c) * BH * (N + 64) * 8 * 4);   // logits of recent launches (score update)
@@ -325,7 +337,7 @@ kv_tier_status kv_tier_query_sizes(const kv_tier_config* cfg, kv_tier_sizes* out
   out->scores = L.b_scores;
   out->meta = L.b_meta;
   const size_t rows = (size_t)cfg->num_layers * cfg->num_requests * cfg->num_kv_heads * host_rows_of(*cfg);
-  out->host_t1 = cfg->hbm_ratio_bp < 10000 ? rows * cfg->head_dim * 2 * 2 : 0;
+  out->host_t1 = rows * cfg->head_dim * 2 * 2;     // T1 (and a prefix longer than T0's load share) lives here
   out->host_t2 = cfg->t2_fraction_bp ? rows * (cfg->head_dim + 4) * 2 : 0;
   out->cap_t0 = cap0;
   out->cap_t1 = cap1;
@@ -401,6 +413,8 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.moves = reinterpret_cast<int4*>(A + L.off_moves);
   v.mcount = reinterpret_cast<int*>(A + L.off_mcount);
   v.mcap = (int)mcap_of(*cfg);
+  v.mchunk = mchunk_of(*cfg);
+  v.c0_load = std::max(0, cap0 - delta_slack(*cfg));
   v.scratch = reinterpret_cast<int*>(A + L.off_scratch);
   v.mtemp = reinterpret_cast<__nv_bfloat16*>(A + L.off_mtemp);
   v.fS = reinterpret_cast<float*>(A + L.off_fS);
@@ -530,8 +544,13 @@ kv_tier_status kv_tier_load_prefix(kv_tier_ctx* ctx, int32_t layer, const void* 
   if (scorer_uses_red(ctx->v.scorer) &&
       layer != (int)std::count(ctx->loaded_layers.begin(), ctx->loaded_layers.end(), 1))
     return fail(ctx, KV_TIER_E_STATE, "redundancy scorers: load prefix layers once each, in ascending order (AMB-30)");
-  if (n0 < 0 || seq_owned_below(ctx->v.seq_w, ctx->v.seq_r, n0) + 1 > ctx->v.cap0 || n0 + 1 > ctx->v.Nmax)
-    return fail(ctx, KV_TIER_E_CAPACITY, "prefix of %d tokens exceeds T0 capacity %d / N_max %d", n0, ctx->v.cap0, ctx->v.Nmax);
+  {
+    const int own0 = n0 < 0 ? 0 : seq_owned_below(ctx->v.seq_w, ctx->v.seq_r, n0);
+    const int over = std::max(0, own0 - ctx->v.c0_load);       // prefix rows that start in T1 (AMB-26)
+    if (n0 < 0 || n0 + 1 > ctx->v.Nmax || over > ctx->v.cap1 || (over > 0 && ctx->sz.host_t1 == 0))
+      return fail(ctx, KV_TIER_E_CAPACITY, "prefix of %d tokens exceeds T0 + T1 capacity %d + %d / N_max %d", n0,
+                  ctx->v.c0_load, ctx->v.cap1, ctx->v.Nmax);
+  }
   if (ctx->n0 >= 0 && ctx->n0 != n0) return fail(ctx, KV_TIER_E_INVAL, "n0 differs between layers");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (ctx->n0 < 0) {
@@ -539,7 +558,10 @@ kv_tier_status kv_tier_load_prefix(kv_tier_ctx* ctx, int32_t layer, const void* 
     if (st) return st;
     ctx->n0 = n0;
     ctx->n = n0;
-    ctx->c[0] = seq_owned_below(ctx->v.seq_w, ctx->v.seq_r, n0); ctx->c[1] = ctx->c[2] = ctx->c[3] = 0;
+    const int own0 = seq_owned_below(ctx->v.seq_w, ctx->v.seq_r, n0);
+    ctx->c[0] = std::min(own0, ctx->v.c0_load);
+    ctx->c[1] = own0 - ctx->c[0];
+    ctx->c[2] = ctx->c[3] = 0;
     ctx->n_event = n0;
     ctx->nvis_event = ctx->c[0];
   }
@@ -836,18 +858,17 @@ kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side) 
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (!ctx->classified) return fail(ctx, KV_TIER_E_STATE, "migrate without a preceding classify");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(main_stream);
-  cudaStream_t sd = reinterpret_cast<cudaStream_t>(side);
+  (void)side;                                // the offload runs in stream order with its chunk (mtemp reuse)
   ctx->mig_epoch += 1;                       // host-T1 mode re-reads the T1 lists
-  // plan the new row layout; move only the rows that change (or rebuild when too many move)
+  // plan the new row layout, then move only the rows that change, in place, one chunk of
+  // (layer, kv head) pairs at a time (gather -> scatter -> offload of rows entering T1/T2)
   cudaError_t e = launch_plan(ctx->v, s);
-  if (e == cudaSuccess) e = launch_moves(ctx->v, ctx->cur, s);
-  if (e == cudaSuccess) e = launch_migrate(ctx->v, ctx->cur, s);
+  const int npairs = ctx->v.L * ctx->v.Hkv;
+  for (int lg0 = 0; lg0 < npairs && e == cudaSuccess; lg0 += ctx->v.mchunk)
+    e = launch_move_chunk(ctx->v, ctx->cur, lg0, std::min(ctx->v.mchunk, npairs - lg0), s);
   if (e == cudaSuccess) e = launch_commit(ctx->v, s);
   if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_migrated, s);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, ctx->ev_migrated, 0);
-  if (e == cudaSuccess) e = launch_offload_moves(ctx->v, ctx->cur, sd);
-  if (e == cudaSuccess) e = launch_offload_host(ctx->v, ctx->cur, sd);
-  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_offload_done, sd);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_offload_done, s);
   kv_tier_status st = cuda_check(ctx, e, "migrate");
   if (st) return st;
   ctx->offload_pending = true;

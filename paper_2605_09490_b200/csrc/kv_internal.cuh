@@ -26,9 +26,8 @@ struct DevState {
   int cur;          // ping-pong buffer holding the live stores / lists
   int n_event;      // n at the last committed manage event
   int err;          // sticky error bits: 1 = non-finite probability/score, 2 = tier store overflow (shard)
-  int scur;         // buffer holding the bf16/int8 row stores (flips only on a full rebuild)
-  int use_full;     // set by the migrate plan when the move list overflows -> full rebuild
-  int last_full;    // use_full of the last committed migrate (read by the offload kernels)
+  int scur;         // row-store buffer (always 0: the stores are single-buffered, migrate works in place)
+  int pad0, pad1;
   unsigned long long d2h_rows;   // rows written to the pinned host stores
   int nn;           // 1: this rank holds the step's new token (always 1 unless sequence-sharded)
 };
@@ -71,9 +70,11 @@ struct DevView {
   float hot_hit;        // hitRatio of the window: persisting carve-out / window bytes (<= 1)
   int4* moves;          // [B][mcap] {src tier, src row, dst tier | dst row << 2, position}
   int* mcount;          // [B] moves of the last plan (<= mcap)
-  int mcap;
+  int mcap;             // moves per request (>= N: an event never overflows)
+  int mchunk;           // (layer, kv head) pairs per migrate chunk (mtemp holds one chunk)
+  int c0_load;          // prefix positions loaded into T0 (the rest start in T1, AMB-26)
   int* scratch;         // [B][Nmax] plan scratch (hole rows)
-  __nv_bfloat16* mtemp; // [B][mcap][L][Hkv][2][D] rows in flight during an incremental migrate
+  __nv_bfloat16* mtemp; // [B][mcap][mchunk][2][D] rows in flight during a migrate chunk
   __nv_bfloat16* k0[2]; __nv_bfloat16* v0[2];        // T0 store  [L][B][Hkv][cap0][D]
   __nv_bfloat16* k1[2]; __nv_bfloat16* v1[2];        // T1 staging [L][B][Hkv][cap1][D] (stream: [2][B][Hkv][cap1][D] in k1[0]/v1[0])
   int8_t* c2k[2]; int8_t* c2v[2];                      // T2 codes  [L][B][Hkv][cap2][D]
@@ -235,11 +236,8 @@ cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_
 cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s);
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);
 cudaError_t launch_classify(const DevView& v, const float* Sx, int parts, cudaStream_t s);
-cudaError_t launch_migrate(const DevView& v, int cur, cudaStream_t s);
 cudaError_t launch_plan(const DevView& v, cudaStream_t s);
-cudaError_t launch_moves(const DevView& v, int cur, cudaStream_t s);
-cudaError_t launch_offload_moves(const DevView& v, int cur, cudaStream_t s);
-cudaError_t launch_offload_host(const DevView& v, int cur, cudaStream_t s);
+cudaError_t launch_move_chunk(const DevView& v, int cur, int lg0, int nlg, cudaStream_t s);
 cudaError_t launch_commit(const DevView& v, cudaStream_t s);
 cudaError_t launch_prefetch(const DevView& v, int layer, cudaStream_t s);
 size_t attn_smem_bytes(const DevView& v);

@@ -151,46 +151,74 @@ cudaError_t launch_vnorm_prefix(const DevView& v, int layer, const void* vv, int
   return cudaGetLastError();
 }
 
-// Prefill rows [0, n0) of one layer into T0 (Alg. 1); a sequence shard keeps its own
-// positions only (store row j = its j-th owned position).
+// Prefill rows [0, n0) of one layer (Alg. 1).  The first c0_load owned positions fill the
+// T0 store; a prefix longer than that (T0 is sized for the steady state, |P| + n_hbm + Delta, not
+// for the whole chain: DESIGN.md AMB-26) places the rest in T1 -- the pinned host store and, in
+// differential mode, the HBM staging -- until the first manage event sorts the chain.  Attention
+// reads T0 and T1 alike, so step 0 is unchanged.  A sequence shard keeps its own positions only
+// (store row j = its j-th owned position).
 __global__ void k_load_prefix(const DevView v, const int layer, const uint16_t* __restrict__ k,
                               const uint16_t* __restrict__ vv, const int n0) {
   const int unit = blockIdx.y;
   const int b = unit / v.Hkv, g = unit % v.Hkv;
-  const size_t base = grp_of(v, layer, b, g) * v.cap0 * v.D;
+  const size_t grp = grp_of(v, layer, b, g);
   uint16_t* K = reinterpret_cast<uint16_t*>(v.k0[0]);
   uint16_t* V = reinterpret_cast<uint16_t*>(v.v0[0]);
-  const size_t tot = (size_t)seq_owned_below(v.seq_w, v.seq_r, n0) * v.D;
+  uint16_t* K1 = reinterpret_cast<uint16_t*>(v.k1[0]);
+  uint16_t* V1 = reinterpret_cast<uint16_t*>(v.v1[0]);
+  const int n0own = seq_owned_below(v.seq_w, v.seq_r, n0);
+  const size_t tot = (size_t)n0own * v.D;
   const size_t in_tot = (size_t)n0 * v.D;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
     const int j = (int)(e / v.D), el = (int)(e % v.D);
     const int p = seq_pos_of(v.seq_w, v.seq_r, j);
-    const size_t dst = base + (size_t)j * v.D + swz_off(j, el);
-    K[dst] = k[(size_t)unit * in_tot + (size_t)p * v.D + el];
-    V[dst] = vv[(size_t)unit * in_tot + (size_t)p * v.D + el];
+    const uint16_t kx = k[(size_t)unit * in_tot + (size_t)p * v.D + el];
+    const uint16_t vx = vv[(size_t)unit * in_tot + (size_t)p * v.D + el];
+    if (j < v.c0_load) {
+      const size_t dst = (grp * v.cap0 + j) * v.D + swz_off(j, el);
+      K[dst] = kx;
+      V[dst] = vx;
+    } else {
+      const int r = j - v.c0_load;                             // T1 row (store order = position order)
+      const size_t hdst = host_row(v, grp, p) * v.D + el;      // pinned host store: canonical layout
+      reinterpret_cast<uint16_t*>(v.hk1)[hdst] = kx;
+      reinterpret_cast<uint16_t*>(v.hv1)[hdst] = vx;
+      if (!v.stream_mode) {
+        const size_t dst = (grp * v.cap1 + r) * v.D + swz_off(r, el);
+        K1[dst] = kx;
+        V1[dst] = vx;
+      }
+    }
   }
 }
 
-// All n0 prefix tokens in T0 with S = 0 (Alg. 1).
+// The n0 prefix tokens with S = 0 (Alg. 1): the first c0_load owned positions in T0,
+// the rest in T1 (k_load_prefix).
 __global__ void k_init_meta(const DevView v, const int n0) {
   const int b = blockIdx.y;
   const int n0own = seq_owned_below(v.seq_w, v.seq_r, n0);
+  const int c0 = min(n0own, v.c0_load);
   for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < v.Nmax; pos += gridDim.x * blockDim.x) {
     const bool own = seq_own(v.seq_w, v.seq_r, pos);
     const int j = seq_owned_below(v.seq_w, v.seq_r, pos);      // owned index of pos (if owned)
+    const bool in1 = pos < n0 && own && j >= c0;
     for (int buf = 0; buf < 2; ++buf) {
-      v.tier[buf][(size_t)b * v.Nmax + pos] = pos < n0 ? T0 : T3;
-      v.rowof[buf][(size_t)b * v.Nmax + pos] = pos < n0 && own ? j : -1;
+      v.tier[buf][(size_t)b * v.Nmax + pos] = pos < n0 ? (in1 ? T1 : T0) : T3;
+      v.rowof[buf][(size_t)b * v.Nmax + pos] = pos < n0 && own ? (in1 ? j - c0 : j) : -1;
       v.idxvis[buf][(size_t)b * v.Nmax + pos] = seq_pos_of(v.seq_w, v.seq_r, pos);
     }
-    if (pos < n0 && own) v.idx[0][0][(size_t)b * v.cap0 + j] = pos;
+    if (pos < n0 && own) {
+      if (in1) v.idx[0][1][(size_t)b * v.cap1 + (j - c0)] = pos;
+      else v.idx[0][0][(size_t)b * v.cap0 + j] = pos;
+    }
     for (int g = 0; g < v.Hkv; ++g) v.S[((size_t)b * v.Hkv + g) * v.Nmax + pos] = 0.f;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int buf = 0; buf < 2; ++buf) {
       int* cn = v.cnt[buf] + b * CNT_STRIDE;
-      cn[0] = buf == 0 ? n0own : 0;
-      cn[1] = cn[2] = cn[3] = 0;
+      cn[0] = buf == 0 ? c0 : 0;
+      cn[1] = buf == 0 ? n0own - c0 : 0;
+      cn[2] = cn[3] = 0;
       cn[4] = buf == 0 ? n0own : 0;
       cn[5] = cn[6] = cn[7] = 0;
     }
@@ -201,8 +229,6 @@ __global__ void k_init_meta(const DevView v, const int n0) {
       v.st->n_event = n0;
       v.st->err = 0;
       v.st->scur = 0;
-      v.st->use_full = 0;
-      v.st->last_full = 0;
       v.st->d2h_rows = 0ull;
       v.st->nn = 1;
     }
@@ -608,17 +634,18 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(const DevView v) {
     if (tnew[p] == T3) rnew[p] = -1;
   if (tid == 0) {
     v.mcount[b] = min(s_nm, v.mcap);
-    if (s_nm > v.mcap) atomicOr(&v.st->use_full, 1);
+    if (s_nm > v.mcap) atomicOr(&v.st->err, 2);              // cannot happen: moves <= n <= mcap
   }
 }
 
-// Incremental migrate, phase 1: every moved row (all layers, K and V) -> staging buffer in
-// the destination's format (bf16 canonical, or int8 codes + scale for T2).
+// Migrate, phase 1: every moved row of the (layer, kv head) pairs [lg0, lg0 + gridDim.y), K and V
+// -> the staging buffer mtemp in the destination's format (bf16 canonical, or int8 codes + scale
+// for T2).  The stores are updated in place, so a chunk's rows are all gathered before any is
+// scattered; pairs are independent (a move never crosses layers or heads).
 template <int D>
-__global__ void __launch_bounds__(256) k_move_gather(const DevView v, const int cur) {
+__global__ void __launch_bounds__(256) k_move_gather(const DevView v, const int cur, const int lg0) {
   constexpr int E = D / 32;
-  if (v.st->use_full) return;
-  const int b = blockIdx.z, lg = blockIdx.y, l = lg / v.Hkv, g = lg % v.Hkv;
+  const int b = blockIdx.z, lg = lg0 + blockIdx.y, l = lg / v.Hkv, g = lg % v.Hkv;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = blockIdx.x * 8 + w;
   if (m >= v.mcount[b]) return;
@@ -627,7 +654,7 @@ __global__ void __launch_bounds__(256) k_move_gather(const DevView v, const int 
   if (st == T1 && dt == T1 && v.stream_mode) return;       // list-only move (rows live on the host)
   const int sb = v.st->scur;
   const size_t grp = grp_of(v, l, b, g);
-  uint16_t* tmp = reinterpret_cast<uint16_t*>(v.mtemp) + ((((size_t)b * v.mcap + m) * v.L + l) * v.Hkv + g) * 2 * D;
+  uint16_t* tmp = reinterpret_cast<uint16_t*>(v.mtemp) + (((size_t)b * v.mcap + m) * v.mchunk + blockIdx.y) * 2 * D;
   for (int kv = 0; kv < 2; ++kv) {
     uint16_t* tk = tmp + kv * D;
     if (dt == T2 && st == T2) {       // T2 -> T2: codes and scale verbatim
@@ -654,12 +681,11 @@ __global__ void __launch_bounds__(256) k_move_gather(const DevView v, const int 
   }
 }
 
-// Incremental migrate, phase 2: staging buffer -> destination rows (same row-store buffer).
+// Migrate, phase 2: staging buffer -> destination rows of the same chunk.
 template <int D>
-__global__ void __launch_bounds__(256) k_move_scatter(const DevView v, const int cur) {
+__global__ void __launch_bounds__(256) k_move_scatter(const DevView v, const int cur, const int lg0) {
   constexpr int E = D / 32;
-  if (v.st->use_full) return;
-  const int b = blockIdx.z, lg = blockIdx.y, l = lg / v.Hkv, g = lg % v.Hkv;
+  const int b = blockIdx.z, lg = lg0 + blockIdx.y, l = lg / v.Hkv, g = lg % v.Hkv;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = blockIdx.x * 8 + w;
   if (m >= v.mcount[b]) return;
@@ -668,7 +694,7 @@ __global__ void __launch_bounds__(256) k_move_scatter(const DevView v, const int
   if (dt == T1 && v.stream_mode) return;                     // T1 rows live on the host
   const int sb = v.st->scur;
   const size_t grp = grp_of(v, l, b, g);
-  const uint16_t* tmp = reinterpret_cast<const uint16_t*>(v.mtemp) + ((((size_t)b * v.mcap + m) * v.L + l) * v.Hkv + g) * 2 * D;
+  const uint16_t* tmp = reinterpret_cast<const uint16_t*>(v.mtemp) + (((size_t)b * v.mcap + m) * v.mchunk + blockIdx.y) * 2 * D;
   for (int kv = 0; kv < 2; ++kv) {
     const uint16_t* tk = tmp + kv * D;
     if (dt == T2) {
@@ -688,116 +714,12 @@ __global__ void __launch_bounds__(256) k_move_scatter(const DevView v, const int
   }
 }
 
-// Full rebuild (when the move list overflowed, e.g. the first event): every row of the
-// planned layout is written into the other row-store buffer.  One warp per (row, K|V).
+// Offload to the pinned host stores (zero-copy stores over the host link) of a chunk's moves:
+// rows newly in T1 (paper: "Offload T1 entries") and new T2 codes, from mtemp.
 template <int D>
-__global__ void __launch_bounds__(256) k_migrate(const DevView v, const int cur) {
+__global__ void __launch_bounds__(256) k_offload_moves(const DevView v, const int cur, const int lg0) {
   constexpr int E = D / 32;
-  if (!v.st->use_full) return;
-  const int T = blockIdx.z;
-  if (T == 1 && v.stream_mode) return;
-  if (T == 2 && v.cap2 == 0) return;
-  const int nxt = cur ^ 1;
-  const int sb = v.st->scur, db = sb ^ 1;
-  const int grpi = blockIdx.y;
-  const int b = (grpi / v.Hkv) % v.B;
-  const size_t grp = (size_t)grpi;
-  const int capT = T == 0 ? v.cap0 : (T == 1 ? v.cap1 : v.cap2);
-  const int cntT = v.cnt[nxt][b * CNT_STRIDE + T];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j0 = blockIdx.x * 32;
-  const int j1 = min(j0 + 32, cntT);
-  for (int j = j0 + w; j < j1; j += 8) {
-    const int pos = v.idx[nxt][T][(size_t)b * capT + j];
-    const int ot = v.tier[cur][(size_t)b * v.Nmax + pos];
-    const int orow = v.rowof[cur][(size_t)b * v.Nmax + pos];
-    for (int kv = 0; kv < 2; ++kv) {
-      if (T == 2) {
-        int8_t* dc = (kv ? v.c2v[db] : v.c2k[db]) + (grp * v.cap2 + j) * D + lane * E;
-        float* ds = (kv ? v.s2v[db] : v.s2k[db]) + grp * v.cap2 + j;
-        if (ot == T2) {
-          const int8_t* sc = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + orow) * D + lane * E;
-#pragma unroll
-          for (int k = 0; k < E; ++k) dc[k] = sc[k];
-          if (lane == 0) *ds = (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + orow];
-        } else {
-          uint16_t x[E];
-          source_row<D>(v, sb, kv, grp, ot, orow, pos, lane, x);
-          int8_t codes[E];
-          float sc;
-          quantize_row<D>(x, codes, &sc, lane);
-#pragma unroll
-          for (int k = 0; k < E; ++k) dc[k] = codes[k];
-          if (lane == 0) *ds = sc;
-        }
-      } else {
-        uint16_t x[E];
-        source_row<D>(v, sb, kv, grp, ot, orow, pos, lane, x);
-        uint16_t* dst = T == 0
-            ? reinterpret_cast<uint16_t*>(kv ? v.v0[db] : v.k0[db]) + (grp * v.cap0 + j) * D
-            : reinterpret_cast<uint16_t*>(kv ? v.v1[db] : v.k1[db]) + (grp * v.cap1 + j) * D;
-        store_bits(dst + swz_off(j, lane * E), x, E);
-      }
-    }
-  }
-}
-
-// Offload to the pinned host stores (zero-copy stores over the host link), on the side
-// stream after the commit: rows newly in T1 (paper: "Offload T1 entries") and new T2
-// codes.  Full-rebuild variant: scans the new T1/T2 lists.
-template <int D>
-__global__ void __launch_bounds__(256) k_offload_host(const DevView v, const int cur) {
-  constexpr int E = D / 32;
-  if (!v.st->last_full) return;
-  const int T = blockIdx.z + 1;            // 1: T1 rows, 2: T2 codes
-  if (T == 2 && (v.cap2 == 0 || v.hc2k == nullptr)) return;
-  const int nxt = cur ^ 1;
-  const int sb = v.st->scur;               // the rebuilt buffer (committed)
-  const int grpi = blockIdx.y;
-  const int b = (grpi / v.Hkv) % v.B;
-  const size_t grp = (size_t)grpi;
-  const int capT = T == 1 ? v.cap1 : v.cap2;
-  const int cntT = v.cnt[nxt][b * CNT_STRIDE + T];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j0 = blockIdx.x * 32;
-  const int j1 = min(j0 + 32, cntT);
-  unsigned long long rows = 0;
-  for (int j = j0 + w; j < j1; j += 8) {
-    const int pos = v.idx[nxt][T][(size_t)b * capT + j];
-    const int ot = v.tier[cur][(size_t)b * v.Nmax + pos];
-    if (ot == T) continue;          // already in this host store
-    const int orow = v.rowof[cur][(size_t)b * v.Nmax + pos];
-    for (int kv = 0; kv < 2; ++kv) {
-      if (T == 1) {
-        uint16_t x[E];
-        if (!v.stream_mode) {
-          const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v1[sb] : v.k1[sb]) + (grp * v.cap1 + j) * D;
-          load_bits(x, s + swz_off(j, lane * E), E);
-        } else {
-          source_row<D>(v, sb ^ 1, kv, grp, ot, orow, pos, lane, x);   // pre-rebuild buffer
-        }
-        uint16_t* dst = reinterpret_cast<uint16_t*>(kv ? v.hv1 : v.hk1) + host_row(v, grp, pos) * D;
-        store_bits(dst + lane * E, x, E);
-      } else {
-        const int8_t* sc = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + j) * D + lane * E;
-        int8_t* dc = (kv ? v.hc2v : v.hc2k) + host_row(v, grp, pos) * D + lane * E;
-#pragma unroll
-        for (int k = 0; k < E; ++k) dc[k] = sc[k];
-        if (lane == 0) (kv ? v.hs2v : v.hs2k)[host_row(v, grp, pos)] = (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + j];
-      }
-    }
-    rows += 2;
-  }
-  if (lane == 0 && rows) atomicAdd(&v.st->d2h_rows, rows);
-}
-
-// Incremental variant: only the moves into T1 / T2 from another tier, from the staging
-// buffer of the moves (still intact: the next migrate waits for this kernel).
-template <int D>
-__global__ void __launch_bounds__(256) k_offload_moves(const DevView v, const int cur) {
-  constexpr int E = D / 32;
-  if (v.st->last_full) return;
-  const int b = blockIdx.z, lg = blockIdx.y, l = lg / v.Hkv, g = lg % v.Hkv;
+  const int b = blockIdx.z, lg = lg0 + blockIdx.y, l = lg / v.Hkv, g = lg % v.Hkv;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = blockIdx.x * 8 + w;
   if (m >= v.mcount[b]) return;
@@ -806,7 +728,7 @@ __global__ void __launch_bounds__(256) k_offload_moves(const DevView v, const in
   if (st == dt || dt == T0) return;
   if (dt == T2 && v.hc2k == nullptr) return;
   const size_t grp = grp_of(v, l, b, g);
-  const uint16_t* tmp = reinterpret_cast<const uint16_t*>(v.mtemp) + ((((size_t)b * v.mcap + m) * v.L + l) * v.Hkv + g) * 2 * D;
+  const uint16_t* tmp = reinterpret_cast<const uint16_t*>(v.mtemp) + (((size_t)b * v.mcap + m) * v.mchunk + blockIdx.y) * 2 * D;
   for (int kv = 0; kv < 2; ++kv) {
     const uint16_t* tk = tmp + kv * D;
     if (dt == T1) {
@@ -830,9 +752,6 @@ __global__ void k_commit(const DevView v) {
     DevState* s = v.st;
     s->cur ^= 1;
     s->n_event = s->n;
-    s->last_full = s->use_full;
-    if (s->use_full) s->scur ^= 1;
-    s->use_full = 0;
   }
 }
 
@@ -895,40 +814,22 @@ cudaError_t launch_classify(const DevView& v, const float* Sx, int parts, cudaSt
   k_classify<<<v.B, CLS_THREADS, 0, s>>>(v, Sx ? Sx : v.S, Sx ? parts : 1);
   return cudaGetLastError();
 }
-cudaError_t launch_migrate(const DevView& v, int cur, cudaStream_t s) {
-  const int capmax = max(v.cap0, max(v.cap1, v.cap2));
-  dim3 grid((capmax + 31) / 32, v.L * v.B * v.Hkv, 3);
-  if (v.D == 128) k_migrate<128><<<grid, 256, 0, s>>>(v, cur);
-  else k_migrate<64><<<grid, 256, 0, s>>>(v, cur);
-  return cudaGetLastError();
-}
-cudaError_t launch_offload_host(const DevView& v, int cur, cudaStream_t s) {
-  const int capmax = max(v.cap1, v.cap2);
-  if (capmax == 0) return cudaSuccess;
-  dim3 grid((capmax + 31) / 32, v.L * v.B * v.Hkv, 2);
-  if (v.D == 128) k_offload_host<128><<<grid, 256, 0, s>>>(v, cur);
-  else k_offload_host<64><<<grid, 256, 0, s>>>(v, cur);
-  return cudaGetLastError();
-}
 cudaError_t launch_plan(const DevView& v, cudaStream_t s) {
   k_plan<<<v.B, PLAN_THREADS, 0, s>>>(v);
   return cudaGetLastError();
 }
-cudaError_t launch_moves(const DevView& v, int cur, cudaStream_t s) {
-  dim3 grid((v.mcap + 7) / 8, v.L * v.Hkv, v.B);
+// one chunk of (layer, kv head) pairs [lg0, lg0 + nlg): gather, scatter, host offload
+cudaError_t launch_move_chunk(const DevView& v, int cur, int lg0, int nlg, cudaStream_t s) {
+  dim3 grid((v.mcap + 7) / 8, nlg, v.B);
   if (v.D == 128) {
-    k_move_gather<128><<<grid, 256, 0, s>>>(v, cur);
-    k_move_scatter<128><<<grid, 256, 0, s>>>(v, cur);
+    k_move_gather<128><<<grid, 256, 0, s>>>(v, cur, lg0);
+    k_move_scatter<128><<<grid, 256, 0, s>>>(v, cur, lg0);
+    k_offload_moves<128><<<grid, 256, 0, s>>>(v, cur, lg0);
   } else {
-    k_move_gather<64><<<grid, 256, 0, s>>>(v, cur);
-    k_move_scatter<64><<<grid, 256, 0, s>>>(v, cur);
+    k_move_gather<64><<<grid, 256, 0, s>>>(v, cur, lg0);
+    k_move_scatter<64><<<grid, 256, 0, s>>>(v, cur, lg0);
+    k_offload_moves<64><<<grid, 256, 0, s>>>(v, cur, lg0);
   }
-  return cudaGetLastError();
-}
-cudaError_t launch_offload_moves(const DevView& v, int cur, cudaStream_t s) {
-  dim3 grid((v.mcap + 7) / 8, v.L * v.Hkv, v.B);
-  if (v.D == 128) k_offload_moves<128><<<grid, 256, 0, s>>>(v, cur);
-  else k_offload_moves<64><<<grid, 256, 0, s>>>(v, cur);
   return cudaGetLastError();
 }
 cudaError_t launch_commit(const DevView& v, cudaStream_t s) {

@@ -59,12 +59,23 @@ def _cfg(**kw):
 
 
 def test_query_sizes_7b():
+    # T0 holds the steady state (Alg. 1): |P| + top n_hbm + Delta appends, not the chain
+    N, P, ks, kw, delta = 2255, 64, 4, 128, 64
     s = kt.query_sizes(_cfg())
-    assert s.cap_t0 >= 2255 and s.cap_t1 >= 1128
-    # T0 ping-pong: 2 x K/V x L*B*Hkv*cap0*d*2 bytes
-    assert s.t0_store >= 2 * 2 * 28 * 8 * 4 * s.cap_t0 * 128 * 2
-    assert s.host_t1 == 28 * 8 * 4 * 2255 * 128 * 2 * 2
+    keep = (5000 * (N - (P + ks + kw)) + 9999) // 10000
+    slack = max(16, delta) + 16
+    assert s.cap_t0 == (P + ks + kw + keep + slack + 15) // 16 * 16
+    assert s.cap_t0 < 0.62 * N
+    assert s.cap_t1 >= N - (s.cap_t0 - slack)                   # a long prefix starts partly in T1 (AMB-26)
+    # single-buffered K/V stores: L*B*Hkv*cap0*d*2 bytes each
+    assert s.t0_store >= 2 * 28 * 8 * 4 * s.cap_t0 * 128 * 2
+    assert s.t0_store < 2 * 2 * 28 * 8 * 4 * s.cap_t0 * 128 * 2
+    assert s.host_t1 == 28 * 8 * 4 * N * 128 * 2 * 2
     assert s.device_arena >= s.t0_store + s.t1_staging + s.scores
+    plain = 28 * 8 * N * 4 * 4 * 128
+    assert s.device_arena < 1.25 * plain                        # T0 + all of T1 staged + metadata
+    st = kt.query_sizes(_cfg(staging=0))                        # strict DDR residency
+    assert st.device_arena < 0.8 * plain
 
 
 @pytest.mark.parametrize("bad", [dict(d=96), dict(Hq=30), dict(Hq=36, Hkv=4), dict(hbm_bp=10001),

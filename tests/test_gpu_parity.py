@@ -126,10 +126,10 @@ def test_tiny_t2_half():                      # f2 = 50 %: int8 T2 rows in atten
     _run_pair(H.workload("tiny", interval=8, t2_bp=5000))
 
 
-@pytest.mark.parametrize("mcap", ["4", "0"])
-def test_tiny_migrate_paths(mcap, monkeypatch):   # full rebuild (tiny move budget) vs incremental moves
-    monkeypatch.setenv("KVTIER_MCAP", mcap)
-    _run_pair(H.workload("tiny", interval=8, t2_bp=3000, B=2, L=2), graph=True)
+@pytest.mark.parametrize("mchunk", ["1", "3", "0"])
+def test_tiny_migrate_paths(mchunk, monkeypatch):   # in-place migrate in chunks of (layer, kv head) pairs
+    monkeypatch.setenv("KVTIER_MCHUNK", mchunk)
+    _run_pair(H.workload("tiny", interval=8, t2_bp=3000, B=2, L=2, Hkv=2, Hq=4), graph=True)
 
 
 def test_tiny_per_event_mode():               # AMB-9 literal Alg. 1
