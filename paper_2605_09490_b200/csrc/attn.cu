@@ -194,7 +194,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
 #pragma unroll
       for (int k = 0; k < EL; ++k) {          // every load of the new-token work issued at once
         const int e = lane + 32 * k;
-        const int se = swz_off(sg.n0o, e);
+        const int se = swz_off(sg.n0o, e, D);
         kb[k] = kin ? kin[e] : K0w[se];
         vb[k] = vin ? vin[e] : V0w[se];
 #pragma unroll
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
 #pragma unroll
       for (int k = 0; k < EL; ++k) {
         const int e = lane + 32 * k;
-        const int se = swz_off(sg.n0o, e);
+        const int se = swz_off(sg.n0o, e, D);
         if (kin) K0w[se] = kb[k];
         if (vin) V0w[se] = vb[k];
         const float vf = bf16_bits_to_f(vb[k]);
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       uint32_t a0, a1_, a2_, a3_;
-      ldsm_x4(a0, a1_, a2_, a3_, sK + row * ROWB + (((2 * ks + (mi >> 1)) ^ (row & 7)) << 4));
+      ldsm_x4(a0, a1_, a2_, a3_, sK + tile_off<D>(row, 2 * ks + (mi >> 1)));
       mma16816(ch[ks % NCH], a0, a1_, a2_, a3_, qf[ks][0], qf[ks][1]);
     }
 #pragma unroll
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     uint32_t af[KS][4];
 #pragma unroll
     for (int mt = 0; mt < KS; ++mt)
-      ldsm_x4_t(af[mt][0], af[mt][1], af[mt][2], af[mt][3], sV + row * ROWB + (((2 * mt + (mi & 1)) ^ (row & 7)) << 4));
+      ldsm_x4_t(af[mt][0], af[mt][1], af[mt][2], af[mt][3], sV + tile_off<D>(row, 2 * mt + (mi & 1)));
 #pragma unroll
     for (int mt = 0; mt < KS; ++mt) mma16816(oacc[mt], af[mt][0], af[mt][1], af[mt][2], af[mt][3], c0, c1);
 #pragma unroll
@@ -357,8 +357,8 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
       lo.z = i8pair_to_bf16x2(cw.y, 0); lo.w = i8pair_to_bf16x2(cw.y, 1);
       hi.x = i8pair_to_bf16x2(cw.z, 0); hi.y = i8pair_to_bf16x2(cw.z, 1);
       hi.z = i8pair_to_bf16x2(cw.w, 0); hi.w = i8pair_to_bf16x2(cw.w, 1);
-      *reinterpret_cast<uint4*>(scr + row * ROWB + (((2 * j) ^ (row & 7)) << 4)) = lo;
-      *reinterpret_cast<uint4*>(scr + row * ROWB + (((2 * j + 1) ^ (row & 7)) << 4)) = hi;
+      *reinterpret_cast<uint4*>(scr + tile_off<D>(row, 2 * j)) = lo;
+      *reinterpret_cast<uint4*>(scr + tile_off<D>(row, 2 * j + 1)) = hi;
     }
     __syncwarp();
   };

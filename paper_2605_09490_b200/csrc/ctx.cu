@@ -1127,7 +1127,7 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
       const int cap = caps[T];
       const __nv_bfloat16* Ks = t0 ? v.k0[sb] : v.k1[sb];
       const __nv_bfloat16* Vs = t0 ? v.v0[sb] : v.v1[sb];
-      std::vector<uint16_t> tk((size_t)cnt * D), tv((size_t)cnt * D);
+      std::vector<uint16_t> tk((size_t)((cnt + 7) & ~7) * D), tv((size_t)((cnt + 7) & ~7) * D);   // whole 8-row groups
       e = order(T, b, pos, perm);
       for (size_t g = 0; g < H && e == cudaSuccess; ++g) {
         const size_t grp = ((size_t)layer * B + b) * H + g;
@@ -1137,8 +1137,8 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
         for (int jj = 0; jj < cnt; ++jj) {
           const int j = perm[jj];
           for (size_t el = 0; el < D; ++el) {     // undo the store swizzle
-            o16[(size_t)jj * 2 * D + el] = tk[(size_t)j * D + swz_off(j, (int)el)];
-            o16[(size_t)jj * 2 * D + D + el] = tv[(size_t)j * D + swz_off(j, (int)el)];
+            o16[(size_t)jj * 2 * D + el] = tk[(size_t)j * D + swz_off(j, (int)el, (int)D)];
+            o16[(size_t)jj * 2 * D + D + el] = tv[(size_t)j * D + swz_off(j, (int)el, (int)D)];
           }
         }
       }

@@ -170,11 +170,27 @@ __device__ __forceinline__ size_t grp_of(const DevView& v, int l, int b, int g) 
   return ((size_t)l * v.B + b) * v.Hkv + g;
 }
 
-// bf16 K/V rows in the T0 store and the T1 staging are stored pre-swizzled: the 16-byte
-// chunk c of store row j sits at chunk position c ^ (j & 7).  A linear bulk copy of rows
-// into shared memory then lands in the bank-conflict-free layout ldmatrix reads.
-__host__ __device__ __forceinline__ int swz_off(int j, int e) {
-  return ((((e >> 3) ^ (j & 7)) << 3) | (e & 7));
+// bf16 K/V rows in the T0 store and the T1 staging are stored pre-swizzled in the 128-byte
+// swizzle atom of the tensor cores: every group of 8 rows holds its 128-byte column blocks one
+// after the other (d = 64: one block, plain rows; d = 128: [8 rows x cols 0..63 | 8 rows x cols
+// 64..127], 2 KB), and inside a block the 16-byte chunk c of row j sits at chunk c ^ (j & 7).  A
+// linear bulk copy of whole 8-row groups into shared memory therefore lands in the layout both
+// ldmatrix (bank-conflict-free) and a K-major / MN-major SWIZZLE_128B UMMA descriptor read.
+// swz_off(j, e, D): element e of row j relative to j * D.
+__host__ __device__ __forceinline__ int swz_off(int j, int e, int D) {
+  const int c = (e >> 3) & 7, r = j & 7;
+  return D == 128 ? ((e >> 6) << 9) + (r << 6) - (r << 7) + ((c ^ r) << 3) + (e & 7)
+                  : (((c ^ r) << 3) | (e & 7));
+}
+// byte offset of 16-byte chunk c (0 .. D/8-1) of row `row` inside a shared-memory tile of rows
+// (the same layout, tile starting at an 8-row boundary)
+template <int D>
+__device__ __forceinline__ uint32_t tile_off(int row, int c) {
+  if constexpr (D == 128)
+    return ((uint32_t)(row >> 3) << 11) + ((uint32_t)(c >> 3) << 10) + ((uint32_t)(row & 7) << 7) +
+           ((uint32_t)((c & 7) ^ (row & 7)) << 4);
+  else
+    return ((uint32_t)row << 7) + ((uint32_t)(c ^ (row & 7)) << 4);
 }
 constexpr int STORE_SLACK_ROWS = 128;   // rows of slack after each bf16 store buffer
 

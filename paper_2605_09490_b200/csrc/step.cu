@@ -355,7 +355,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
           uint16_t* V0w = reinterpret_cast<uint16_t*>(v.v0[sb]) + (grp * v.cap0 + sg.n0o) * D;
 #pragma unroll
           for (int e2 = 0; e2 < EL; ++e2) {
-            const int se = swz_off(sg.n0o, lane + 32 * e2);
+            const int se = swz_off(sg.n0o, lane + 32 * e2, D);
             K0w[se] = kb[e2];                                // the row joins the T0 store
             V0w[se] = vb[e2];
           }
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         uint32_t a0, a1_, a2_, a3_;
-        ldsm_x4(a0, a1_, a2_, a3_, sK + row * ROWB + (((2 * ks + (mi >> 1)) ^ (row & 7)) << 4));
+        ldsm_x4(a0, a1_, a2_, a3_, sK + tile_off<D>(row, 2 * ks + (mi >> 1)));
         mma16816(ch[ks % NCH], a0, a1_, a2_, a3_, qf[ks][0], qf[ks][1]);
       }
 #pragma unroll
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
       uint32_t af[KS][4];
 #pragma unroll
       for (int mt = 0; mt < KS; ++mt)
-        ldsm_x4_t(af[mt][0], af[mt][1], af[mt][2], af[mt][3], sV + row * ROWB + (((2 * mt + (mi & 1)) ^ (row & 7)) << 4));
+        ldsm_x4_t(af[mt][0], af[mt][1], af[mt][2], af[mt][3], sV + tile_off<D>(row, 2 * mt + (mi & 1)));
 #pragma unroll
       for (int mt = 0; mt < KS; ++mt) mma16816(oacc[mt], af[mt][0], af[mt][1], af[mt][2], af[mt][3], c0, c1);
 #pragma unroll
@@ -537,8 +537,8 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
         lo.z = i8pair_to_bf16x2(cw.y, 0); lo.w = i8pair_to_bf16x2(cw.y, 1);
         hi.x = i8pair_to_bf16x2(cw.z, 0); hi.y = i8pair_to_bf16x2(cw.z, 1);
         hi.z = i8pair_to_bf16x2(cw.w, 0); hi.w = i8pair_to_bf16x2(cw.w, 1);
-        *reinterpret_cast<uint4*>(scr + row * ROWB + (((2 * j) ^ (row & 7)) << 4)) = lo;
-        *reinterpret_cast<uint4*>(scr + row * ROWB + (((2 * j + 1) ^ (row & 7)) << 4)) = hi;
+        *reinterpret_cast<uint4*>(scr + tile_off<D>(row, 2 * j)) = lo;
+        *reinterpret_cast<uint4*>(scr + tile_off<D>(row, 2 * j + 1)) = hi;
       }
       __syncwarp();
     };

@@ -54,8 +54,8 @@ __global__ void k_append(const DevView v, const int layer, const uint16_t* __res
   uint16_t* K = reinterpret_cast<uint16_t*>(v.k0[sb]);
   uint16_t* V = reinterpret_cast<uint16_t*>(v.v0[sb]);
   for (int e = threadIdx.x; e < v.D; e += blockDim.x) {
-    K[dst + swz_off(row, e)] = k[(size_t)unit * v.D + e];
-    V[dst + swz_off(row, e)] = vv[(size_t)unit * v.D + e];
+    K[dst + swz_off(row, e, v.D)] = k[(size_t)unit * v.D + e];
+    V[dst + swz_off(row, e, v.D)] = vv[(size_t)unit * v.D + e];
   }
   if (v.red && threadIdx.x >= 32 && threadIdx.x < 64)   // redundancy: cos with the previous key
     redund_append(v, layer, unit, v.st->n - 1, k + (size_t)unit * v.D);
@@ -175,7 +175,7 @@ __global__ void k_load_prefix(const DevView v, const int layer, const uint16_t* 
     const uint16_t kx = k[(size_t)unit * in_tot + (size_t)p * v.D + el];
     const uint16_t vx = vv[(size_t)unit * in_tot + (size_t)p * v.D + el];
     if (j < v.c0_load) {
-      const size_t dst = (grp * v.cap0 + j) * v.D + swz_off(j, el);
+      const size_t dst = (grp * v.cap0 + j) * v.D + swz_off(j, el, v.D);
       K[dst] = kx;
       V[dst] = vx;
     } else {
@@ -184,7 +184,7 @@ __global__ void k_load_prefix(const DevView v, const int layer, const uint16_t* 
       reinterpret_cast<uint16_t*>(v.hk1)[hdst] = kx;
       reinterpret_cast<uint16_t*>(v.hv1)[hdst] = vx;
       if (!v.stream_mode) {
-        const size_t dst = (grp * v.cap1 + r) * v.D + swz_off(r, el);
+        const size_t dst = (grp * v.cap1 + r) * v.D + swz_off(r, el, v.D);
         K1[dst] = kx;
         V1[dst] = vx;
       }
@@ -501,14 +501,14 @@ __device__ __forceinline__ void source_row(const DevView& v, int sb, int kv, siz
   constexpr int E = D / 32;
   if (ot == T0) {
     const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v0[sb] : v.k0[sb]) + (grp * v.cap0 + orow) * D;
-    load_bits(x, s + swz_off(orow, lane * E), E);
+    load_bits(x, s + swz_off(orow, lane * E, D), E);
   } else if (ot == T1) {
     if (v.stream_mode) {
       const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.hv1 : v.hk1) + host_row(v, grp, pos) * D;
       load_bits(x, s + lane * E, E);   // pinned host store: canonical layout
     } else {
       const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v1[sb] : v.k1[sb]) + (grp * v.cap1 + orow) * D;
-      load_bits(x, s + swz_off(orow, lane * E), E);
+      load_bits(x, s + swz_off(orow, lane * E, D), E);
     }
   } else {
     const int8_t* c = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + orow) * D + lane * E;
@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(256) k_move_scatter(const DevView v, const int
       uint16_t* dst = dt == T0
           ? reinterpret_cast<uint16_t*>(kv ? v.v0[sb] : v.k0[sb]) + (grp * v.cap0 + drow) * D
           : reinterpret_cast<uint16_t*>(kv ? v.v1[sb] : v.k1[sb]) + (grp * v.cap1 + drow) * D;
-      store_bits(dst + swz_off(drow, lane * E), x, E);
+      store_bits(dst + swz_off(drow, lane * E, D), x, E);
     }
   }
 }
@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(256) k_prefetch(const DevView v, const int lay
       uint16_t* d = reinterpret_cast<uint16_t*>(kv ? v.v1[0] : v.k1[0]) + (sg * v.cap1 + j) * D;
       uint16_t x[E];
       load_bits(x, s + lane * E, E);
-      store_bits(d + swz_off(j, lane * E), x, E);
+      store_bits(d + swz_off(j, lane * E, D), x, E);
     }
   }
 }
