@@ -30,8 +30,15 @@ EVICT_TOTAL, EVICT_PER_EVENT = 0, 1
 POLICY_HIERARCHY, POLICY_STREAMING, POLICY_H2O, POLICY_RANDOM = 0, 1, 2, 3
 # token scorers (§4 ablation P:707-714): Eq. 1 attention; VATP, attention x ||v||
 # (P:712); redundancy, attention - neighbour cosine; combined, attention x ||v|| -
-# redundancy.  Readings AMB-30/31 in DESIGN.md.
+# redundancy.  Readings AMB-30/31 in DESIGN.md.  Windowed attention ("the last
+# alpha = 8 observation tokens", max-pooled with kernel 7, App. E) and R-KV's
+# Z = lambda I - (1 - lambda) R (App. E).  Readings AMB-32/33 in DESIGN.md.
 SCORER_ATTENTION, SCORER_VATP, SCORER_REDUNDANCY, SCORER_COMBINED = 0, 1, 2, 3
+SCORER_WINDOW, SCORER_RKV = 4, 5
+RKV_ALPHA = 8                      # observation tokens
+RKV_POOL = 7                       # max-pool kernel size
+RKV_LAMBDA = np.float32(0.07)      # lambda
+RKV_ONE_MINUS_LAMBDA = np.float32(0.93)
 
 
 # ----------------------------------------------------------------- attention
@@ -241,7 +248,7 @@ def classify_scores(S, R_part_b, live, cfg):
     (S_max = max of S over the live set, I = 0 if S_max = 0) and rho_i = fp32(fp32(sum_g
     R_part[g][i]) / (L * H_kv)), the mean neighbour cosine over layers and kv heads."""
     scorer = getattr(cfg, "scorer", SCORER_ATTENTION)
-    if scorer < SCORER_REDUNDANCY:
+    if scorer < SCORER_REDUNDANCY or scorer == SCORER_WINDOW:
         return S
     n = S.shape[0]
     smax = np.float32(S[live].max()) if live.any() else np.float32(0)
@@ -250,16 +257,57 @@ def classify_scores(S, R_part_b, live, cfg):
     for g in range(R_part_b.shape[0]):
         rsum = (rsum + R_part_b[g, :n]).astype(np.float32)
     rho = (rsum / np.float32(cfg.L * cfg.Hkv)).astype(np.float32)
+    if scorer == SCORER_RKV:   # Z = lambda I - (1 - lambda) R, each product rounded to fp32 (AMB-33)
+        return ((RKV_LAMBDA * I).astype(np.float32) - (RKV_ONE_MINUS_LAMBDA * rho).astype(np.float32)).astype(np.float32)
     return (I - rho).astype(np.float32)
 
 
-def classify_request(S_part_b, tier_b, n, cfg, req=0, R_part_b=None):
+def observation_window(cfg):
+    """Steps in the windowed scorers' observation window: alpha = 8, at most the
+    manage interval (AMB-32: a window never reaches back past the previous event)."""
+    return min(RKV_ALPHA, cfg.manage_interval)
+
+
+def snapshot_due(cfg, t):
+    """AMB-32: the windowed scorers snapshot S_part at the START of step t when t + w - 1 is a
+    multiple of Delta (w = observation_window), so that at the event of step t_e = t + w - 1 the
+    windowed score S(after t_e) - S(snapshot) sums the probabilities of steps t_e-w+1 .. t_e."""
+    w = observation_window(cfg)
+    return (t + w - 1) % cfg.manage_interval == 0
+
+
+def max_pool_visible(W, vis, k=RKV_POOL):
+    """R-KV's max-pool (kernel k, stride 1, (k-1)/2 padding that never wins) over the cache in
+    its stored order: the non-T3 positions ``vis`` ascending (AMB-32).  Returns an array like W
+    whose entries at ``vis`` are the pooled values (other entries 0)."""
+    out = np.zeros_like(W)
+    h = k // 2
+    m = len(vis)
+    for j in range(m):
+        out[vis[j]] = max(W[vis[x]] for x in range(max(0, j - h), min(m, j + h + 1)))
+    return out
+
+
+def windowed_scores(S_part_b, S_snap_b, tier_b, n):
+    """Windowed attention importance of the windowed / R-KV scorers (AMB-32):
+    W_i = fp32(S_i(now)) - fp32(S_i(snapshot)), each S the fp32 sum over kv heads in ascending
+    order, then max-pooled over the non-T3 positions in position order."""
+    W = (total_score_fp32(np.asarray(S_part_b)[:, :n]) - total_score_fp32(np.asarray(S_snap_b)[:, :n])).astype(np.float32)
+    vis = np.nonzero(np.asarray(tier_b[:n]) != T3)[0]
+    return max_pool_visible(W, vis)
+
+
+def classify_request(S_part_b, tier_b, n, cfg, req=0, R_part_b=None, S_snap_b=None):
     """One manage event for one request (Alg. 1 lines P:189-197; §3.3).
 
     S_part_b: [H_kv][>=n] fp32, tier_b: [>=n] u8 current tiers (T3 sticky, AMB-16/24),
-    R_part_b: [H_kv][>=n] fp32 redundancy partials (redundancy / combined scorers only).
+    R_part_b: [H_kv][>=n] fp32 redundancy partials (redundancy / combined / R-KV scorers only).
+    S_snap_b: [H_kv][>=n] fp32 snapshot of S_part (windowed / R-KV scorers only, AMB-32).
     Returns the new tier array [n] (uint8)."""
-    S = total_score_fp32(np.asarray(S_part_b)[:, :n])
+    if getattr(cfg, "scorer", SCORER_ATTENTION) in (SCORER_WINDOW, SCORER_RKV):
+        S = windowed_scores(S_part_b, S_snap_b, tier_b, n)
+    else:
+        S = total_score_fp32(np.asarray(S_part_b)[:, :n])
     prot = protected_mask(n, cfg.prompt_len, cfg.sink_size, cfg.window_size)
     old = np.asarray(tier_b[:n])
     t3 = old == T3
@@ -327,7 +375,8 @@ class OracleState:
     t: int = 0
     events: list = field(default_factory=list)
     vnorm: np.ndarray = None   # VATP / combined: [L][B][Hkv][Nmax] fp32 ||v|| of every original V row
-    R_part: np.ndarray = None  # redundancy / combined: [B][Hkv][Nmax] fp32 (key_redundancy)
+    R_part: np.ndarray = None  # redundancy / combined / R-KV: [B][Hkv][Nmax] fp32 (key_redundancy)
+    S_snap: np.ndarray = None  # windowed / R-KV: [B][Hkv][Nmax] fp32 S_part at the window start (AMB-32)
 
 
 def init_state(cfg, Kbits, Vbits, n0):
@@ -337,14 +386,16 @@ def init_state(cfg, Kbits, Vbits, n0):
     will ever generate (the never-migrated originals)."""
     from paper_2605_09490_b200.synth.synth import bf16_bits_to_f32   # input decoding only
     L, B, Hkv, Nmax, d = Kbits.shape
-    vnorm = R_part = None
+    vnorm = R_part = S_snap = None
     scorer = getattr(cfg, "scorer", SCORER_ATTENTION)
     if scorer in (SCORER_VATP, SCORER_COMBINED):
         vnorm = value_norms(bf16_bits_to_f32(Vbits))
-    if scorer in (SCORER_REDUNDANCY, SCORER_COMBINED):
+    if scorer in (SCORER_REDUNDANCY, SCORER_COMBINED, SCORER_RKV):
         R_part = key_redundancy(bf16_bits_to_f32(Kbits))
+    if scorer in (SCORER_WINDOW, SCORER_RKV):
+        S_snap = np.zeros((B, Hkv, Nmax), dtype=np.float32)
     return OracleState(
-        cfg=cfg, n=n0, vnorm=vnorm, R_part=R_part,
+        cfg=cfg, n=n0, vnorm=vnorm, R_part=R_part, S_snap=S_snap,
         tier=np.full((B, Nmax), T0, dtype=np.uint8),
         S_part=np.zeros((B, Hkv, Nmax), dtype=np.float32),
         rowK=bf16_bits_to_f32(Kbits).copy(), rowV=bf16_bits_to_f32(Vbits).copy(),
@@ -443,7 +494,8 @@ def manage_event(st):
     for b in range(B):
         old = st.tier[b, :st.n].copy()
         new = classify_request(st.S_part[b], old, st.n, cfg, req=cfg.req_ids[b] if cfg.req_ids else b,
-                               R_part_b=None if st.R_part is None else st.R_part[b])
+                               R_part_b=None if st.R_part is None else st.R_part[b],
+                               S_snap_b=None if st.S_snap is None else st.S_snap[b])
         to_t2 = (new == T2) & (old != T2)
         from_t2 = (old == T2) & ((new == T0) | (new == T1))
         for p in np.nonzero(to_t2)[0]:
@@ -463,7 +515,12 @@ def decode_step(st, qbits_t, manage=True):
     present in rowK/rowV from the generator) joins T0, attention + scores over all
     layers, then a manage event if t mod Delta == 0 (t = 0 included, AMB-10).
 
+    Windowed / R-KV scorers: S_part is snapshot first when the observation window of the next
+    event starts at this step (snapshot_due, AMB-32).
+
     qbits_t: [L][B][Hq][d] bf16 bits.  Returns o [L][B][Hq][d] fp64."""
+    if st.S_snap is not None and snapshot_due(st.cfg, st.t):
+        st.S_snap = st.S_part.copy()
     st.tier[:, st.n] = T0
     st.n += 1
     o = np.stack([decode_layer(st, l, qbits_t[l]) for l in range(st.cfg.L)])

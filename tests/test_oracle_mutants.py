@@ -41,6 +41,15 @@ MUTANTS = [
      "    new[surv[:n_t2]] = T2\n    new[surv[n_t2:len(surv) - n_hbm]] = T1",
      "    new[surv[len(surv) - n_hbm - n_t2:len(surv) - n_hbm]] = T2\n"
      "    new[surv[:len(surv) - n_hbm - n_t2]] = T1"),
+    ("observation window one step short",                                     # P:137, AMB-32
+     "    return (t + w - 1) % cfg.manage_interval == 0",
+     "    return (t + w - 2) % cfg.manage_interval == 0"),
+    ("max-pool over every position (T3 included)",                            # P:976, AMB-32
+     "    vis = np.nonzero(np.asarray(tier_b[:n]) != T3)[0]\n    return max_pool_visible(W, vis)",
+     "    vis = np.arange(n)\n    return max_pool_visible(W, vis)"),
+    ("R-KV weights swapped",
+     "        return ((RKV_LAMBDA * I).astype(np.float32) - (RKV_ONE_MINUS_LAMBDA * rho)",
+     "        return ((RKV_ONE_MINUS_LAMBDA * I).astype(np.float32) - (RKV_LAMBDA * rho)"),
 ]
 
 

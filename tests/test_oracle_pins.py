@@ -769,3 +769,155 @@ def test_row_leaving_t2_keeps_bf16_of_dequant():              # AMB-12 (lossy T2
                 want = (torch.from_numpy(c.astype(np.float32)) * float(s)).to(torch.bfloat16).float().numpy()
                 assert np.array_equal(row[l, 0, 0, p], want), (p, l)
         assert not np.array_equal(row[:, 0, 0, 3:6], src[:, 0, 0, 3:6])
+
+
+# --------------------------------------------------------------------- windowed / R-KV scorers
+# P:137 (R-KV's "last alpha = 8 observation tokens"), App. E P:972-978 (Z = lambda I - (1 - lambda) R,
+# softmax of the last 8 observation tokens max-pooled with kernel 7, lambda = 0.07); AMB-32/33.
+def test_max_pool_visible_matches_torch_max_pool1d():          # library routine on the compacted cache
+    rng = np.random.default_rng(21)
+    n = 60
+    W = rng.random(n).astype(np.float32)
+    tier = rng.integers(0, 4, size=n).astype(np.uint8)
+    vis = np.nonzero(tier != O.T3)[0]
+    got = O.max_pool_visible(W, vis)
+    ref = torch.nn.functional.max_pool1d(torch.from_numpy(W[vis])[None, None], kernel_size=7, stride=1,
+                                         padding=3)[0, 0].numpy()
+    assert np.array_equal(got[vis], ref)
+    # a T3 position is not a neighbour: the pool spans 3 non-T3 positions on each side
+    W2 = np.zeros(12, np.float32)
+    W2[5] = 9.0
+    t2 = np.zeros(12, np.uint8)
+    t2[[6, 7, 8]] = O.T3
+    v2 = np.nonzero(t2 != O.T3)[0]
+    p2 = O.max_pool_visible(W2, v2)
+    assert [int(i) for i in v2 if p2[i] == 9.0] == [2, 3, 4, 5, 9, 10, 11]
+
+
+def _event_inputs(scorer, interval, events, evict_bp=1000, L=2):
+    """Runs the tiny oracle through ``events`` manage events (t = 0, Delta, ...) and captures
+    (t, S_part, S_snap, tiers, n) of request 0 right before each classify (after the event
+    step's score update).  Returns (run, captures)."""
+    from paper_2605_09490_b200 import harness as Hh
+    from tests.oracle_runner import OracleRun
+    w = Hh.workload("tiny", L=L, steps=interval * (events - 1) + 1, interval=interval, scorer=scorer,
+                    evict_bp=evict_bp)
+    r = OracleRun(w)
+    caps = []
+    orig = O.manage_event
+
+    def spy(st):
+        caps.append((st.t, st.S_part[0].copy(), None if st.S_snap is None else st.S_snap[0].copy(),
+                     st.tier[0, :st.n].copy(), st.n))
+        orig(st)
+    O.manage_event = spy
+    try:
+        for _ in range(w["steps"]):
+            r.step()
+    finally:
+        O.manage_event = orig
+    return r, caps
+
+
+@pytest.mark.parametrize("interval", [4, 8, 16])
+def test_windowed_score_is_brute_force_sum_over_the_last_w_steps(interval):
+    """At an event t_e the windowed score of position i is the sum, over the last
+    w = min(8, Delta) steps t_e-w+1 .. t_e, over layers and q heads, of the softmax probability
+    of i (brute-force fp64 softmax over that step's visible set, original rows: f2 = 0), then
+    max-pooled (kernel 7) over the non-T3 positions in position order (AMB-32).
+    An off-by-one window moves every value by a whole step's mass and fails."""
+    r, caps = _event_inputs(O.SCORER_WINDOW, interval, events=3)
+    cfg = r.cfg
+    w = O.observation_window(cfg)
+    assert w == min(8, interval)
+    Kf = S.bf16_bits_to_f32(r.K).astype(np.float64)
+    inv = 1.0 / math.sqrt(cfg.d)
+    n0 = r.w["N"] - 1
+    for t_e, S_now, S_sn, tier, n in caps[1:]:
+        assert n == n0 + t_e + 1
+        keep = tier != O.T3                                     # T3 fixed since the last event (w <= Delta)
+        Wb = np.zeros(n)
+        for t in range(t_e - w + 1, t_e + 1):
+            n_t = n0 + t + 1
+            vis = np.nonzero(keep[:n_t])[0]
+            Qf = S.bf16_bits_to_f32(r.Q[t]).astype(np.float64)
+            for l in range(cfg.L):
+                for h in range(cfg.Hq):
+                    z = (Kf[l, 0, h // cfg.G, vis] @ Qf[l, 0, h]) * inv
+                    e = np.exp(z - z.max())
+                    Wb[vis] += e / e.sum()
+        vis = np.nonzero(keep)[0]
+        ref = np.zeros(n)
+        for j in range(len(vis)):
+            ref[vis[j]] = max(Wb[vis[x]] for x in range(max(0, j - 3), min(len(vis), j + 4)))
+        got = O.windowed_scores(S_now, S_sn, tier, n)
+        tol = 8 * np.finfo(np.float32).eps * float(S_now[:, :n].sum(0).max()) + 1e-6
+        assert np.abs(got[vis] - ref[vis]).max() <= tol, (t_e, np.abs(got[vis] - ref[vis]).max(), tol)
+        step_mass = cfg.L * cfg.Hq / n                          # mean mass of one step per position
+        assert step_mass > 50 * tol
+
+
+def test_windowed_score_at_the_first_event_is_the_cumulative_score():
+    # the window cannot reach back before step 0: at t = 0 the snapshot is the initial S = 0
+    _, caps = _event_inputs(O.SCORER_WINDOW, 16, events=1)
+    t_e, S_now, S_sn, tier, n = caps[0]
+    assert t_e == 0 and not S_sn.any()
+    vis = np.nonzero(tier != O.T3)[0]
+    assert np.array_equal(O.windowed_scores(S_now, S_sn, tier, n),
+                          O.max_pool_visible(O.total_score_fp32(S_now[:, :n]), vis))
+
+
+def test_rkv_closed_form():
+    # Z = fp32(lambda * I) - fp32((1 - lambda) * rho), I = pooled / max over the live set, rho the
+    # mean neighbour cosine over layers x kv heads (App. E P:975-977; AMB-33)
+    cfg = _red_cfg(O.SCORER_RKV, L=2, Hkv=2)
+    S = np.array([100.0, 2.0, 4.0, 1.0], np.float32)
+    live = np.array([False, True, True, True])
+    R = np.array([[0.0, 0.5, 0.0, -1.0], [0.0, 0.5, 0.0, -1.0]], np.float32)
+    k = O.classify_scores(S, R, live, cfg)
+    lam, lam1 = np.float32(0.07), np.float32(0.93)
+    assert k[2] == lam                                        # I = 1, rho = 0
+    assert k[1] == np.float32(lam * np.float32(0.5)) - np.float32(lam1 * np.float32(0.25))
+    assert k[3] == np.float32(lam * np.float32(0.25)) + np.float32(lam1 * np.float32(0.5))
+    assert k[0] == np.float32(lam * np.float32(25.0))
+
+
+def test_rkv_reduces_to_window_with_constant_redundancy_and_penalises_redundancy():
+    """Special cases of Z = lambda I - (1 - lambda) R: a constant R shifts every key equally, so
+    R-KV's tiers equal the windowed scorer's; a constant I leaves only -R, so the evicted tokens
+    are the most redundant live ones."""
+    n, Hkv = 40, 2
+    rng = np.random.default_rng(13)
+    S_now = rng.uniform(0.5, 3.0, size=(Hkv, n)).astype(np.float32)
+    S_sn = (S_now * rng.uniform(0.0, 0.9, size=(Hkv, n))).astype(np.float32)
+    tier = np.zeros(n, np.uint8)
+    tier[[7, 19]] = O.T3
+    Rc = np.full((Hkv, n), 0.3, np.float32)
+    base = O.classify_request(S_now, tier, n, _red_cfg(O.SCORER_WINDOW, hbm_bp=4000, evict_bp=1500),
+                              S_snap_b=S_sn)
+    got = O.classify_request(S_now, tier, n, _red_cfg(O.SCORER_RKV, hbm_bp=4000, evict_bp=1500),
+                             R_part_b=Rc, S_snap_b=S_sn)
+    assert np.array_equal(got, base)
+    # constant window mass: S_snap = S_now - c
+    S_sn2 = (S_now - np.float32(0.25)).astype(np.float32)
+    S_now2 = S_now.copy()
+    S_now2[:] = np.float32(1.0)
+    S_sn2[:] = np.float32(0.5)
+    R = rng.uniform(-2, 2, size=(Hkv, n)).astype(np.float32)
+    cfg = _red_cfg(O.SCORER_RKV, hbm_bp=4000, evict_bp=1500)
+    new = O.classify_request(S_now2, np.zeros(n, np.uint8), n, cfg, R_part_b=R, S_snap_b=S_sn2)
+    prot = O.protected_mask(n, cfg.prompt_len, cfg.sink_size, cfg.window_size)
+    live = np.nonzero(~prot)[0]
+    rho = {int(i): float(np.float32(np.float32(R[0, i] + R[1, i]) / np.float32(cfg.L * Hkv))) for i in live}
+    order = sorted(live.tolist(), key=lambda i: (-rho[i], i))
+    n3 = int(len(live) * cfg.evict_bp // 10000)
+    assert n3 >= 1
+    assert sorted(np.nonzero(new == O.T3)[0].tolist()) == sorted(order[:n3])
+
+
+def test_window_scorer_tiers_differ_from_cumulative():
+    """The windowed scorer is a different ranking from Eq. 1's cumulative one on the same run
+    (P:137-140 contrasts them): at the second event the two tier arrays differ."""
+    r_w, _ = _event_inputs(O.SCORER_WINDOW, 16, events=2, evict_bp=2000)
+    r_a, _ = _event_inputs(O.SCORER_ATTENTION, 16, events=2, evict_bp=2000)
+    assert not np.array_equal(r_w.st.tier, r_a.st.tier)
