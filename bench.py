@@ -598,19 +598,33 @@ def main():
 
 def run_sequence_sharded(args, w, world, rank, local, dev, peaks):
     """--shard sequence: the ranks share ONE batch, each owning the 64-position blocks
-    k % world == rank; per layer decode_attention_lse + an all-gather of (o, m, l) over NCCL +
-    the rank-order LSE combine + score_update_lse.  Strong scaling."""
+    k % world == rank.  The library owns the NCCL communicator (kv_tier_init with an
+    nccl_unique_id): per layer decode_attention_lse -> ncclAllGather of (o, m, l) -> the
+    rank-order LSE combine -> score_update_lse, the whole step captured as one CUDA graph;
+    events all-gather S_part inside kv_tier_classify.  Strong scaling."""
     from paper_2605_09490_b200 import harness as H
+    from paper_2605_09490_b200 import kvtier as kt
     W, K = args.warmup, args.steps
-    sr = H.SeqShardRank(w, rank, world, device=dev)
+    nid = [kt.nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        import torch.distributed as dist
+        dist.broadcast_object_list(nid, src=0)
+    run = H.TieredDecode(w, device=dev, out_fp32=True, shard=kt.SHARD_SEQUENCE, rank=rank, world=world,
+                         nccl_id=nid[0])
+    run.capture()
     for _ in range(W):
-        sr.step()
+        run.step()
     _barrier_sync()
     with ClockSampler(local) as clk:
-        el = timed(sr.step, sr.run.main, K)
+        el = timed(run.step, run.main, K)
     _barrier_sync()
     el_max = _max_over_ranks(el)
-    sr.run.sync()
+    run.sync()
+
+    class _Sr:                     # the census / close interface the report below uses
+        pass
+    sr = _Sr()
+    sr.run, sr.close = run, run.close
     counts, _ = sr.run.kv.census()
     own = [int(x) for x in counts[0]]
     n_vis_own = own[0] + own[1] + own[2]
@@ -627,11 +641,14 @@ def run_sequence_sharded(args, w, world, rank, local, dev, peaks):
                                    f"B={w['B']} (whole batch) L={L} Hq/Hkv={w['Hq']}/{w['Hkv']} d={w['d']} N={w['N']} "
                                    f"beta={args.hbm}bp r={args.evict}bp, sequence-sharded",
                        "global_batch": w["B"], "parallelism": f"sequence-sharded x{world} (64-position blocks, "
-                                                            f"per-layer NCCL all-gather + LSE combine)"},
+                                                            f"per-layer NCCL all-gather + LSE combine in the "
+                                                            f"step graph)"},
             "hbm_gbs": hbm, "hbm_frac_of_measured_peak": hbm / (peaks["hbm_gbs"] * world),
             "bytes_per_step": int(step_bytes), "census_rank0_b0": own,
-            "clocks": clk.summary(), "gpu_launches": K * (3 * L + 2),
-            "note": "per-layer host-driven launches and collectives: the combine sits between layers",
+            "clocks": clk.summary(), "gpu_launches": K * (4 * L + 2),
+            "note": "one CUDA graph per step: per layer decode + merge + NCCL all-gather + LSE combine + "
+                    "score rescale on the library's communicator; events (classify all-gathers S_part) "
+                    "inside the window",
         }), flush=True)
     sr.close()
     if world > 1:

@@ -49,7 +49,7 @@ typedef enum {
   KV_TIER_OK = 0,
   KV_TIER_E_INVAL = -1,     /* bad argument / shape mismatch, empty visible set */
   KV_TIER_E_CUDA = -2,      /* CUDA runtime error (possibly from an earlier async launch) */
-  KV_TIER_E_NCCL = -3,      /* reserved: collective failure */
+  KV_TIER_E_NCCL = -3,      /* NCCL missing, communicator creation or a collective failed */
   KV_TIER_E_STATE = -4,     /* call out of order (e.g. migrate without classify) */
   KV_TIER_E_CAPACITY = -5,  /* a tier store would overflow its capacity */
   KV_TIER_E_OOM = -6,       /* host pinned allocation failed */
@@ -80,8 +80,15 @@ typedef enum { KV_TIER_EVICT_TOTAL = 0, KV_TIER_EVICT_PER_EVENT = 1 } kv_tier_ev
  *            by position) and hands the global (M, L) back through kv_tier_score_update_lse,
  *            which completes the fused score update with the exact global probabilities.
  *            At an event: all-gather S_part, kv_tier_classify_gathered (sum over ranks is
- *            exact: every position has one owner), migrate.  kv_tier_step / the step graph
- *            and kv_tier_score_update are E_STATE (the exchange sits between the layers). */
+ *            exact: every position has one owner), migrate.  Without a communicator
+ *            kv_tier_step / the step graph and kv_tier_score_update are E_STATE (the exchange
+ *            sits between the layers).
+ *            WITH a communicator (kv_tier_init given an nccl_unique_id from
+ *            kv_tier_nccl_unique_id, one per job, every rank passing the same bytes): kv_tier_step
+ *            and the step graph run the whole step on the library's NCCL communicator -- per
+ *            layer decode_attention_lse -> ncclAllGather of every rank's (o, m, l) -> the LSE
+ *            combine (rank order, deterministic) into o -> kv_tier_score_update_lse -- captured
+ *            as one CUDA graph; kv_tier_classify all-gathers S_part itself.  out_fp32 must be 1. */
 typedef enum { KV_TIER_SHARD_REQUEST = 0, KV_TIER_SHARD_KVHEAD = 1, KV_TIER_SHARD_SEQUENCE = 2 } kv_tier_shard;
 
 /* Tier policy of a5 (the paper's pure-eviction baselines, §4.1, on
@@ -107,10 +114,21 @@ typedef enum { KV_TIER_POLICY_HIERARCHY = 0, KV_TIER_POLICY_STREAMING = 1, KV_TI
  *              c is formed when a row is loaded / appended (the ctx keeps the previous key of
  *              every layer and kv head), so prefix layers must be loaded in ascending order.
  *   COMBINED   "attn x val - redundancy": S as VATP, ranked as REDUNDANCY.
- *   REDUNDANCY / COMBINED: request or KV-head sharding without classify_gathered (E_INVAL for
- *   sequence sharding; kv_tier_classify_gathered returns E_STATE). */
+ *   WINDOW     windowed attention (R-KV's "last alpha = 8 observation tokens"; App. E
+ *              P:976): S as ATTENTION; classify ranks by W_i = fp32(sum_g S_part[g][i]) -
+ *              fp32(sum_g S_snap[g][i]), max-pooled (kernel 7, stride 1) over the non-T3
+ *              positions in ascending order.  S_snap is a copy of S_part the library takes at
+ *              kv_tier_begin_step of step t when (t + w - 1) % Delta == 0, w = min(8, Delta)
+ *              (cfg.manage_interval is then binding: call classify at steps t % Delta == 0 for
+ *              the window to be the last w steps; DESIGN AMB-32).
+ *   RKV        R-KV's Z = lambda I - (1 - lambda) R (App. E), lambda = 0.07:
+ *              I_i = fp32(Wpool_i / max of Wpool over the live set) (0 if that max is 0),
+ *              R_i = rho_i as REDUNDANCY; Z = fp32(0.07f * I) - fp32(0.93f * rho) (AMB-33).
+ *   REDUNDANCY / COMBINED / RKV: request or KV-head sharding without classify_gathered (E_INVAL
+ *   for sequence sharding; kv_tier_classify_gathered returns E_STATE).  WINDOW / RKV: no
+ *   sequence sharding (E_INVAL), no classify_gathered (E_STATE). */
 typedef enum { KV_TIER_SCORER_ATTENTION = 0, KV_TIER_SCORER_VATP = 1, KV_TIER_SCORER_REDUNDANCY = 2,
-               KV_TIER_SCORER_COMBINED = 3 } kv_tier_scorer;
+               KV_TIER_SCORER_COMBINED = 3, KV_TIER_SCORER_WINDOW = 4, KV_TIER_SCORER_RKV = 5 } kv_tier_scorer;
 
 #define KV_TIER_STAGING_ALL 0xFFFFFFFFu   /* differential mode: staging holds all of T1 (§3.4) */
 
@@ -166,10 +184,19 @@ typedef struct {
 KV_TIER_API kv_tier_status kv_tier_query_sizes(const kv_tier_config* cfg, kv_tier_sizes* out);
 
 /* Create a ctx over caller-owned device memory; pins host T1/T2 stores
- * (cudaHostAlloc, mapped).  nccl_unique_id must be NULL (request sharding has
- * no collective on the step). */
+ * (cudaHostAlloc, mapped).  nccl_unique_id: NULL, or (sequence sharding only, out_fp32 = 1) the
+ * 128 bytes of an ncclUniqueId every rank of the job passes: the ctx then owns an NCCL
+ * communicator of cfg->world ranks (collective: every rank must call kv_tier_init) plus its
+ * exchange buffers (cudaMalloc: 4 B x ((W + 1) B H_q (d + 2) + L B H_q 2 + W B H_kv N_max)),
+ * freed by kv_tier_destroy.  E_NCCL if NCCL is unavailable or the communicator fails;
+ * E_INVAL for an id with another shard mode. */
 KV_TIER_API kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* buf,
                             const void* nccl_unique_id, kv_tier_ctx** out);
+
+/* A fresh ncclUniqueId (rank 0 calls it and sends the bytes to the other ranks).  out: host,
+ * >= 128 bytes.  NCCL is resolved at run time from the process (torch's libnccl.so.2) or the
+ * loader path; E_NCCL if absent. */
+KV_TIER_API kv_tier_status kv_tier_nccl_unique_id(void* out, size_t bytes);
 KV_TIER_API kv_tier_status kv_tier_destroy(kv_tier_ctx* ctx);
 
 /* Initial chain (prefill result, Alg. 1): positions [0, n0) of layer `layer`
@@ -326,7 +353,8 @@ enum {
   KV_TIER_X_STAGING = 7,    /* bf16 [B][H_kv][|T1|][2][d]  HBM staging (differential mode) */
   KV_TIER_X_T2_CODES = 8,   /* i8   [B][H_kv][|T2|][2][d]                                  */
   KV_TIER_X_T2_SCALES = 9,  /* f32  [B][H_kv][|T2|][2]                                     */
-  KV_TIER_X_REDUNDANCY = 10 /* fp32 [B][H_kv][n]   R_part (AMB-30; zeros unless REDUNDANCY/COMBINED) */
+  KV_TIER_X_REDUNDANCY = 10,/* fp32 [B][H_kv][n]   R_part (AMB-30; zeros unless REDUNDANCY/COMBINED/RKV) */
+  KV_TIER_X_SNAPSHOT = 11   /* fp32 [B][H_kv][n]   S_snap (AMB-32; zeros unless WINDOW/RKV)   */
 };
 /* Bytes `what` needs (counts are uniform across requests). */
 KV_TIER_API kv_tier_status kv_tier_export_size(kv_tier_ctx* ctx, int32_t what, size_t* bytes);

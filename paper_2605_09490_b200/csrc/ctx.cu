@@ -12,7 +12,43 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>      // types only: the functions are resolved at run time (no link-time NCCL)
+
 using namespace kvt;
+
+// NCCL, resolved from the libnccl.so.2 already in the process (torch's), else dlopen'ed: the
+// library loads and runs without NCCL unless a ctx is created with an nccl_unique_id.
+namespace {
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+    a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+    a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.all_gather && a.group_start && a.group_end && a.error_string;
+    return a;
+  }();
+  return api;
+}
+}  // namespace
 
 struct kv_tier_ctx {
   kv_tier_config cfg;
@@ -63,6 +99,14 @@ struct kv_tier_ctx {
   cudaEvent_t ev_q = nullptr;
   cudaEvent_t ev_inc[2] = {nullptr, nullptr};
   bool inc_used[2] = {false, false};
+  // sequence sharding with a library-owned communicator (kv_tier_init with an nccl_unique_id):
+  // every layer's (o, m, l) all-gather + LSE combine + score rescale run inside kv_tier_step /
+  // the step graph; events all-gather S_part inside kv_tier_classify
+  ncclComm_t comm = nullptr;
+  float* x_send = nullptr;                 // [B][H_q][d] o partial, then [B][H_q][2] (m, l)
+  float* x_recv = nullptr;                 // [W][B][H_q][d] o parts, then [W][B][H_q][2] lse parts
+  float* x_lse = nullptr;                  // [L][B][H_q][2] global (M, L) per layer
+  float* x_scores = nullptr;               // [W][B][H_kv][N_max] all-gathered S_part (events)
   std::string err;
 };
 
@@ -140,8 +184,12 @@ kv_tier_status validate(const kv_tier_config* c) {
   if (c->variant < 0 || c->variant > 5) return fail(nullptr, KV_TIER_E_INVAL, "variant must be in [0, 5]");
   if (c->policy < KV_TIER_POLICY_HIERARCHY || c->policy > KV_TIER_POLICY_RANDOM)
     return fail(nullptr, KV_TIER_E_INVAL, "policy must be a kv_tier_policy");
-  if (c->scorer < KV_TIER_SCORER_ATTENTION || c->scorer > KV_TIER_SCORER_COMBINED)
+  if (c->scorer < KV_TIER_SCORER_ATTENTION || c->scorer > KV_TIER_SCORER_RKV)
     return fail(nullptr, KV_TIER_E_INVAL, "scorer must be a kv_tier_scorer");
+  if (scorer_uses_window(c->scorer) && c->shard == KV_TIER_SHARD_SEQUENCE && c->world > 1)
+    return fail(nullptr, KV_TIER_E_INVAL, "windowed scorers pool over the whole cache order: not with sequence sharding");
+  if (scorer_uses_window(c->scorer) && c->manage_interval < 1)
+    return fail(nullptr, KV_TIER_E_INVAL, "windowed scorers need manage_interval >= 1 (the observation window follows it)");
   if (scorer_uses_red(c->scorer) && c->shard == KV_TIER_SHARD_SEQUENCE && c->world > 1)
     return fail(nullptr, KV_TIER_E_INVAL, "redundancy scorers need each position's predecessor: not with sequence sharding");
   if ((c->policy == KV_TIER_POLICY_H2O || c->policy == KV_TIER_POLICY_RANDOM) && c->budget < 1)
@@ -186,7 +234,7 @@ struct Layout {
   size_t off_k0[2], off_v0[2], off_k1[2], off_v1[2], off_c2k[2], off_c2v[2], off_s2k[2], off_s2v[2];
   size_t off_idx[2][3], off_vis[2], off_tier[2], off_row[2], off_cnt[2], off_S, off_fS, off_st, off_z, off_ml;
   size_t off_part, off_uctr, off_moves, off_mcount, off_scratch, off_mtemp, total, hot_begin, off_vnorm, off_zlayer;
-  size_t off_red, off_lastk, off_sdone;
+  size_t off_red, off_lastk, off_snap, off_pool, off_sdone;
   size_t b_t0, b_t1, b_t2, b_scores, b_meta;
 };
 
@@ -283,11 +331,13 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   const size_t nslots = BH * (split_of(c) + 1);                          // per-CTA partials + new token
   L.off_part = take(nslots * (16 + 8 * D) * 4);
   L.off_sdone = take((size_t)c.num_layers * B * 4);                     // step kernel layer counters
-  L.off_uctr = take(BH * 4);
+  L.off_uctr = take(256);                                                 // migrate grid barrier
   L.off_zlayer = take(ZRING * 4);
   L.off_vnorm = take(scorer_uses_vnorm(c.scorer) ? LBH * N * 4 : 0);     // VATP / combined: V-row norms
   L.off_red = take(scorer_uses_red(c.scorer) ? BH * N * 4 : 0);          // redundancy partials R_part
   L.off_lastk = take(scorer_uses_red(c.scorer) ? LBH * D * 2 : 0);       // previous key per (layer, kv head)
+  L.off_snap = take(scorer_uses_window(c.scorer) ? BH * N * 4 : 0);      // windowed: S_part snapshot
+  L.off_pool = take(scorer_uses_window(c.scorer) ? B * N * 4 : 0);       // windowed: pooled scores
   L.b_scores = o - s0; s0 = o;
   for (int i = 0; i < 2; ++i) {
     L.off_idx[i][0] = take(B * cap0 * 4);
@@ -350,7 +400,12 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   kv_tier_status st = validate(cfg);
   if (st != KV_TIER_OK) return st;
   if (!buf || !buf->device_arena || !out) return fail(nullptr, KV_TIER_E_INVAL, "null buffers/out");
-  if (nccl_unique_id) return fail(nullptr, KV_TIER_E_INVAL, "the library runs no collective (the caller does): pass NULL");
+  if (nccl_unique_id && cfg->shard != KV_TIER_SHARD_SEQUENCE)
+    return fail(nullptr, KV_TIER_E_INVAL, "an nccl_unique_id is only used by sequence sharding (the other splits have no collective on the step)");
+  if (nccl_unique_id && !cfg->out_fp32)
+    return fail(nullptr, KV_TIER_E_INVAL, "sequence sharding with a communicator combines o in fp32: out_fp32 must be 1");
+  if (nccl_unique_id && !nccl_api().ok)
+    return fail(nullptr, KV_TIER_E_NCCL, "libnccl.so.2 not found in the process or on the loader path");
   if (((uintptr_t)buf->device_arena) & 255) return fail(nullptr, KV_TIER_E_INVAL, "device_arena must be 256-B aligned");
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e != cudaSuccess) return fail(nullptr, KV_TIER_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
@@ -408,6 +463,9 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.vnorm = scorer_uses_vnorm(cfg->scorer) ? reinterpret_cast<float*>(A + L.off_vnorm) : nullptr;
   v.red = scorer_uses_red(cfg->scorer) ? reinterpret_cast<float*>(A + L.off_red) : nullptr;
   v.lastk = scorer_uses_red(cfg->scorer) ? reinterpret_cast<uint16_t*>(A + L.off_lastk) : nullptr;
+  v.snap = scorer_uses_window(cfg->scorer) ? reinterpret_cast<float*>(A + L.off_snap) : nullptr;
+  v.pool = scorer_uses_window(cfg->scorer) ? reinterpret_cast<float*>(A + L.off_pool) : nullptr;
+  v.interval = cfg->manage_interval;
   v.hot_base = A + L.hot_begin;
   v.hot_bytes = L.total - L.hot_begin;
   v.moves = reinterpret_cast<int4*>(A + L.off_moves);
@@ -417,6 +475,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.c0_load = std::max(0, cap0 - delta_slack(*cfg));
   v.scratch = reinterpret_cast<int*>(A + L.off_scratch);
   v.mtemp = reinterpret_cast<__nv_bfloat16*>(A + L.off_mtemp);
+  v.gbar = reinterpret_cast<unsigned*>(A + L.off_uctr);
   v.fS = reinterpret_cast<float*>(A + L.off_fS);
   v.st = reinterpret_cast<DevState*>(A + L.off_st);
   // pinned, mapped host stores (NUMA placement follows the calling thread's node)
@@ -500,7 +559,39 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   ctx->loaded_layers.assign(v.L, 0);
   ctx->prefetched_step.assign(v.L, -1);
   ctx->appended_step.assign(v.L, -1);
+  if (nccl_unique_id) {
+    // sequence sharding: a library-owned communicator and its exchange buffers (the layer
+    // partials of one rank; every rank's; the global (M, L) per layer; all ranks' S_part)
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof(id));
+    const ncclResult_t r = nccl_api().comm_init_rank(&ctx->comm, cfg->world, id, cfg->rank);
+    if (r != ncclSuccess) {
+      ctx->comm = nullptr;
+      kv_tier_destroy(ctx);
+      return fail(nullptr, KV_TIER_E_NCCL, "ncclCommInitRank: %s", nccl_api().error_string(r));
+    }
+    const size_t rows = (size_t)v.B * v.Hq, W = (size_t)cfg->world;
+    e = cudaMalloc(&ctx->x_send, rows * (v.D + 2) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->x_recv, W * rows * (v.D + 2) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->x_lse, (size_t)v.L * rows * 2 * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->x_scores, W * v.B * v.Hkv * (size_t)v.Nmax * 4);
+    if (e != cudaSuccess) {
+      kv_tier_destroy(ctx);
+      return fail(nullptr, KV_TIER_E_OOM, "sequence-shard exchange buffers: %s", cudaGetErrorString(e));
+    }
+  }
   *out = ctx;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_nccl_unique_id(void* out, size_t bytes) {
+  if (!out || bytes < sizeof(ncclUniqueId))
+    return fail(nullptr, KV_TIER_E_INVAL, "need %zu bytes for the NCCL unique id", sizeof(ncclUniqueId));
+  if (!nccl_api().ok) return fail(nullptr, KV_TIER_E_NCCL, "libnccl.so.2 not found in the process or on the loader path");
+  ncclUniqueId id;
+  const ncclResult_t r = nccl_api().get_unique_id(&id);
+  if (r != ncclSuccess) return fail(nullptr, KV_TIER_E_NCCL, "ncclGetUniqueId: %s", nccl_api().error_string(r));
+  memcpy(out, &id, sizeof(id));
   return KV_TIER_OK;
 }
 
@@ -531,6 +622,9 @@ kv_tier_status kv_tier_destroy(kv_tier_ctx* ctx) {
   if (ctx->h1_o) cudaFreeHost(ctx->h1_o);
   if (ctx->d1_parts) cudaFree(ctx->d1_parts);
   if (ctx->ev_q) cudaEventDestroy(ctx->ev_q);
+  if (ctx->comm) nccl_api().comm_destroy(ctx->comm);
+  for (float* p : {ctx->x_send, ctx->x_recv, ctx->x_lse, ctx->x_scores})
+    if (p) cudaFree(p);
   delete ctx;
   return KV_TIER_OK;
 }
@@ -808,6 +902,15 @@ static kv_tier_status classify_impl(kv_tier_ctx* ctx, const float* Sx, int parts
 
 kv_tier_status kv_tier_classify(kv_tier_ctx* ctx, void* stream) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (ctx->comm) {
+    // sequence shards: every rank classifies the sum of all ranks' S_part (one owner per
+    // position, so the sum is exact), all-gathered here over the library's communicator
+    const DevView& v = ctx->v;
+    const ncclResult_t r = nccl_api().all_gather(v.S, ctx->x_scores, (size_t)v.B * v.Hkv * v.Nmax, ncclFloat32,
+                                                 ctx->comm, reinterpret_cast<cudaStream_t>(stream));
+    if (r != ncclSuccess) return fail(ctx, KV_TIER_E_NCCL, "all-gather of S_part: %s", nccl_api().error_string(r));
+    return classify_impl(ctx, ctx->x_scores, ctx->cfg.world, stream);
+  }
   if ((ctx->cfg.shard == KV_TIER_SHARD_KVHEAD || ctx->cfg.shard == KV_TIER_SHARD_SEQUENCE) && ctx->cfg.world > 1)
     return fail(ctx, KV_TIER_E_STATE, "KV-head sharding: classify needs every shard's scores (kv_tier_classify_gathered)");
   return classify_impl(ctx, nullptr, 1, stream);
@@ -819,6 +922,8 @@ kv_tier_status kv_tier_classify_gathered(kv_tier_ctx* ctx, const float* S_all, i
   if (((uintptr_t)S_all) & 3) return fail(ctx, KV_TIER_E_INVAL, "S_all must be 4-B aligned");
   if (scorer_uses_red(ctx->v.scorer))
     return fail(ctx, KV_TIER_E_STATE, "redundancy scorers classify from the ctx's own R_part (kv_tier_classify)");
+  if (scorer_uses_window(ctx->v.scorer))
+    return fail(ctx, KV_TIER_E_STATE, "windowed scorers classify from the ctx's own S_part snapshot (kv_tier_classify)");
   return classify_impl(ctx, S_all, parts, stream);
 }
 
@@ -860,12 +965,13 @@ kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side) 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(main_stream);
   (void)side;                                // the offload runs in stream order with its chunk (mtemp reuse)
   ctx->mig_epoch += 1;                       // host-T1 mode re-reads the T1 lists
-  // plan the new row layout, then move only the rows that change, in place, one chunk of
-  // (layer, kv head) pairs at a time (gather -> scatter -> offload of rows entering T1/T2)
+  // plan the new row layout, then move only the rows that change, in place: one cooperative
+  // launch over chunks of (layer, kv head) pairs (gather + offload of rows entering T1/T2 ->
+  // grid barrier -> scatter)
   cudaError_t e = launch_plan(ctx->v, s);
   const int npairs = ctx->v.L * ctx->v.Hkv;
-  for (int lg0 = 0; lg0 < npairs && e == cudaSuccess; lg0 += ctx->v.mchunk)
-    e = launch_move_chunk(ctx->v, ctx->cur, lg0, std::min(ctx->v.mchunk, npairs - lg0), s);
+  (void)npairs;
+  if (e == cudaSuccess) e = launch_migrate_rows(ctx->v, s);
   if (e == cudaSuccess) e = launch_commit(ctx->v, s);
   if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_migrated, s);
   if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_offload_done, s);
@@ -890,10 +996,55 @@ kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side) 
   return KV_TIER_OK;
 }
 
+// One decode step of a sequence shard with the library's communicator: per
+// layer, this rank's partial softmax (o normalised by its own sum, (m, l) in the log2 domain) ->
+// ncclAllGather of every rank's partial -> LSE combine in rank order (deterministic, Eq. 3 over
+// the union of the shards) -> the score update rescaled by the global (M, L) (Eq. 1).  Every
+// call is stream-ordered, so the whole step captures into one CUDA graph.
+static kv_tier_status seq_step(kv_tier_ctx* ctx, const void* q, const void* k_new, const void* v_new, void* o,
+                               int32_t fuse_score_update, void* stream, void* side) {
+  if (!q || !k_new || !v_new || !o) return fail(ctx, KV_TIER_E_INVAL, "null step buffer");
+  if (!fuse_score_update) return fail(ctx, KV_TIER_E_INVAL, "sequence shards fuse the score update (the combine rescales it)");
+  const DevView& v = ctx->v;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t rows = (size_t)v.B * v.Hq, W = (size_t)ctx->cfg.world;
+  const size_t qs = rows * v.D, ks = (size_t)v.B * v.Hkv * v.D;
+  const char* qb = reinterpret_cast<const char*>(q);
+  const char* kb = reinterpret_cast<const char*>(k_new);
+  const char* vb = reinterpret_cast<const char*>(v_new);
+  float* ob = reinterpret_cast<float*>(o);
+  float* o_send = ctx->x_send;
+  float* l_send = ctx->x_send + rows * v.D;
+  float* o_recv = ctx->x_recv;
+  float* l_recv = ctx->x_recv + W * rows * v.D;
+  kv_tier_status st = kv_tier_begin_step(ctx, stream);
+  if (v.stream_mode)
+    for (int l = 0; l < std::min(2, v.L) && !st; ++l) st = kv_tier_prefetch(ctx, l, side);
+  for (int l = 0; l < v.L && !st; ++l) {
+    st = decode_attention_impl(ctx, l, qb + l * qs * 2, kb + l * ks * 2, vb + l * ks * 2, o_send, 1, stream, 0, l_send);
+    if (st) break;
+    const NcclApi& nc = nccl_api();
+    ncclResult_t r = nc.group_start();
+    if (r == ncclSuccess) r = nc.all_gather(o_send, o_recv, rows * v.D, ncclFloat32, ctx->comm, s);
+    if (r == ncclSuccess) r = nc.all_gather(l_send, l_recv, rows * 2, ncclFloat32, ctx->comm, s);
+    const ncclResult_t r2 = nc.group_end();
+    if (r == ncclSuccess) r = r2;
+    if (r != ncclSuccess) return fail(ctx, KV_TIER_E_NCCL, "layer %d all-gather: %s", l, nc.error_string(r));
+    float* lse_l = ctx->x_lse + (size_t)l * rows * 2;
+    st = cuda_check(ctx, launch_lse_combine(o_recv, l_recv, (int)W, (int)rows, v.D, ob + (size_t)l * qs, lse_l, s),
+                    "lse_combine");
+    if (!st) st = kv_tier_score_update_lse(ctx, lse_l, stream);
+    if (!st && v.stream_mode && l + 2 < v.L) st = kv_tier_prefetch(ctx, l + 2, side);
+  }
+  if (st) return st;
+  return kv_tier_end_step(ctx, stream);
+}
+
 kv_tier_status kv_tier_step(kv_tier_ctx* ctx, const void* q, const void* k_new, const void* v_new, void* o,
                             int32_t fuse_score_update, void* stream, void* side) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
-  if (ctx->v.seq_w > 1) return fail(ctx, KV_TIER_E_STATE, "sequence shards combine every layer: drive decode_attention_lse per layer");
+  if (ctx->comm) return seq_step(ctx, q, k_new, v_new, o, fuse_score_update, stream, side);
+  if (ctx->v.seq_w > 1) return fail(ctx, KV_TIER_E_STATE, "sequence shards without a communicator combine every layer: drive decode_attention_lse per layer");
   if (!q || !k_new || !v_new || !o) return fail(ctx, KV_TIER_E_INVAL, "null step buffer");
   const DevView& v = ctx->v;
   const size_t qs = (size_t)v.B * v.Hq * v.D, ks = (size_t)v.B * v.Hkv * v.D;
@@ -988,6 +1139,7 @@ kv_tier_status kv_tier_sync(kv_tier_ctx* ctx) {
   e = cudaMemcpy(&h, ctx->v.st, sizeof(h), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return fail(ctx, KV_TIER_E_CUDA, "state read: %s", cudaGetErrorString(e));
   if (h.err & 2) return fail(ctx, KV_TIER_E_CAPACITY, "a tier store of this sequence shard overflowed at classify (its share of T1/T2 exceeded 1.25x the fair share)");
+  if (h.err & 4) return fail(ctx, KV_TIER_E_CUDA, "a device-side wait timed out (2 s watchdog: a co-scheduled CTA never arrived)");
   if (h.err) return fail(ctx, KV_TIER_E_NUMERIC, "non-finite probability or score detected on device");
   if (h.n != ctx->n || h.cur != ctx->cur)
     return fail(ctx, KV_TIER_E_STATE, "device/host state diverged (n %d/%d cur %d/%d)", h.n, ctx->n, h.cur, ctx->cur);
@@ -1041,7 +1193,7 @@ static kv_tier_status req_counts(kv_tier_ctx* ctx, std::vector<int>& cb) {
 static size_t export_bytes_req(const kv_tier_ctx* ctx, int32_t what, const int* c) {
   const size_t H = ctx->v.Hkv, D = ctx->v.D, n = ctx->n;
   switch (what) {
-    case KV_TIER_X_SCORES: case KV_TIER_X_REDUNDANCY: return H * n * 4;
+    case KV_TIER_X_SCORES: case KV_TIER_X_REDUNDANCY: case KV_TIER_X_SNAPSHOT: return H * n * 4;
     case KV_TIER_X_TIERS: return n;
     case KV_TIER_X_IDX_T0: return (size_t)c[0] * 4;
     case KV_TIER_X_IDX_T1: return (size_t)c[1] * 4;
@@ -1112,6 +1264,9 @@ kv_tier_status kv_tier_export(kv_tier_ctx* ctx, int32_t what, int32_t layer, voi
     } else if (what == KV_TIER_X_REDUNDANCY) {
       if (!v.red) memset(ob, 0, H * n * 4);
       for (size_t g = 0; g < H && v.red && e == cudaSuccess; ++g) e = d2h(ob + g * n * 4, v.red + (b * H + g) * N, n * 4);
+    } else if (what == KV_TIER_X_SNAPSHOT) {
+      if (!v.snap) memset(ob, 0, H * n * 4);
+      for (size_t g = 0; g < H && v.snap && e == cudaSuccess; ++g) e = d2h(ob + g * n * 4, v.snap + (b * H + g) * N, n * 4);
     } else if (what == KV_TIER_X_TIERS) {
       e = d2h(ob, v.tier[cur] + b * N, n);
     } else if (what >= KV_TIER_X_IDX_T0 && what <= KV_TIER_X_IDX_T2) {

@@ -17,7 +17,11 @@ constexpr int ZBATCH = 1;         // launches whose score updates one score kern
 // kv_tier_scorer: VATP (1) and combined (3) weight increments by ||v||; redundancy (2) and
 // combined (3) rank by I - rho (DESIGN AMB-30/31)
 __host__ __device__ constexpr bool scorer_uses_vnorm(int s) { return s == 1 || s == 3; }
-__host__ __device__ constexpr bool scorer_uses_red(int s) { return s == 2 || s == 3; }
+__host__ __device__ constexpr bool scorer_uses_red(int s) { return s == 2 || s == 3 || s == 5; }
+// windowed (4) and R-KV (5): classify ranks the max-pooled score of the last w steps (AMB-32)
+__host__ __device__ constexpr bool scorer_uses_window(int s) { return s == 4 || s == 5; }
+constexpr int RKV_ALPHA = 8;        // observation steps
+constexpr int RKV_HALF_POOL = 3;    // max-pool kernel 7
 
 // Mutable device state (graph-static kernels read it instead of taking args).
 struct DevState {
@@ -25,7 +29,8 @@ struct DevState {
   int t;            // decode step
   int cur;          // ping-pong buffer holding the live stores / lists
   int n_event;      // n at the last committed manage event
-  int err;          // sticky error bits: 1 = non-finite probability/score, 2 = tier store overflow (shard)
+  int err;          // sticky error bits: 1 = non-finite probability/score, 2 = tier store overflow (shard),
+                    // 4 = a device-side wait hit its 2 s watchdog
   int scur;         // row-store buffer (always 0: the stores are single-buffered, migrate works in place)
   int pad0, pad1;
   unsigned long long d2h_rows;   // rows written to the pinned host stores
@@ -42,6 +47,9 @@ struct DevView {
   float* vnorm;         // VATP / combined: [L][B][Hkv][Nmax] fp32 L2 norm of each token's V row (else null)
   float* red;           // redundancy / combined: [B][Hkv][Nmax] fp32 R_part = sum_l cos(k_i, k_{i-1})
   uint16_t* lastk;      // redundancy / combined: [L][B][Hkv][D] bf16 key of the last appended token
+  float* snap;          // windowed / R-KV: [B][Hkv][Nmax] S_part at the start of the observation window
+  float* pool;          // windowed / R-KV: [B][Nmax] classify scratch (max-pooled scores)
+  int interval;         // Delta (kv_tier_config::manage_interval; binding for windowed scorers)
   int* zlayer;          // [ZRING] layer of the launch that filled each logit slot
   int zring;            // logit ring slots in use (2..ZRING): the ring stays inside the L2 carve-out
   unsigned policy_seed;
@@ -71,10 +79,11 @@ struct DevView {
   int4* moves;          // [B][mcap] {src tier, src row, dst tier | dst row << 2, position}
   int* mcount;          // [B] moves of the last plan (<= mcap)
   int mcap;             // moves per request (>= N: an event never overflows)
-  int mchunk;           // (layer, kv head) pairs per migrate chunk (mtemp holds one chunk)
+  int mchunk;           // mtemp holds B * mcap * mchunk rows: mchunk pairs at the worst-case move count
+  unsigned* gbar;       // grid barrier counter of k_migrate_rows (zeroed by k_plan)
   int c0_load;          // prefix positions loaded into T0 (the rest start in T1, AMB-26)
   int* scratch;         // [B][Nmax] plan scratch (hole rows)
-  __nv_bfloat16* mtemp; // [B][mcap][mchunk][2][D] rows in flight during a migrate chunk
+  __nv_bfloat16* mtemp; // [B * mcap * mchunk][2][D] rows in flight during a migrate chunk
   __nv_bfloat16* k0[2]; __nv_bfloat16* v0[2];        // T0 store  [L][B][Hkv][cap0][D]
   __nv_bfloat16* k1[2]; __nv_bfloat16* v1[2];        // T1 staging [L][B][Hkv][cap1][D] (stream: [2][B][Hkv][cap1][D] in k1[0]/v1[0])
   int8_t* c2k[2]; int8_t* c2v[2];                      // T2 codes  [L][B][Hkv][cap2][D]
@@ -90,6 +99,12 @@ struct DevView {
   __nv_bfloat16* hk1; __nv_bfloat16* hv1;            // pinned host T1 [L][B][Hkv][hN][D] (mapped; host_row)
   int8_t* hc2k; int8_t* hc2v; float* hs2k; float* hs2v;   // pinned host T2 (mapped, may be null)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {   // %globaltimer (ns): watchdogs, debug traces
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // RANDOM tier policy: rank key of (request, position) = high 32 bits of
 // splitmix64(splitmix64(seed << 32 | req) ^ pos) (the oracle implements the same generator).
@@ -253,7 +268,7 @@ cudaError_t launch_score_update(const DevView& v, int layer, const float* probs,
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);
 cudaError_t launch_classify(const DevView& v, const float* Sx, int parts, cudaStream_t s);
 cudaError_t launch_plan(const DevView& v, cudaStream_t s);
-cudaError_t launch_move_chunk(const DevView& v, int cur, int lg0, int nlg, cudaStream_t s);
+cudaError_t launch_migrate_rows(const DevView& v, cudaStream_t s);
 cudaError_t launch_commit(const DevView& v, cudaStream_t s);
 cudaError_t launch_prefetch(const DevView& v, int layer, cudaStream_t s);
 size_t attn_smem_bytes(const DevView& v);

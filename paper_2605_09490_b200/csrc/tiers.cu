@@ -37,6 +37,19 @@ __global__ void k_begin_step(const DevView v) {
   }
 }
 
+// Windowed / R-KV scorers (AMB-32): at the start of step t with (t + w - 1) % Delta == 0,
+// w = min(8, Delta), S_snap = S_part over positions [0, n), so that the event of step t + w - 1
+// ranks S(after that step) - S_snap = the probability mass of its last w steps.
+// Launched before k_begin_step on the step's stream (graph-static: t is read from the device).
+__global__ void k_snapshot(const DevView v) {
+  const int t = v.st->t, n = v.st->n;
+  const int w = v.interval < RKV_ALPHA ? v.interval : RKV_ALPHA;
+  if ((t + w - 1) % v.interval != 0) return;
+  const size_t base = (size_t)blockIdx.y * v.Nmax;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    v.snap[base + i] = v.S[base + i];
+}
+
 __global__ void k_end_step(const DevView v) {
   if (threadIdx.x == 0) v.st->t += 1;
 }
@@ -212,6 +225,8 @@ __global__ void k_init_meta(const DevView v, const int n0) {
       else v.idx[0][0][(size_t)b * v.cap0 + j] = pos;
     }
     for (int g = 0; g < v.Hkv; ++g) v.S[((size_t)b * v.Hkv + g) * v.Nmax + pos] = 0.f;
+    if (v.snap)                                  // windowed scorers: no window before step 0
+      for (int g = 0; g < v.Hkv; ++g) v.snap[((size_t)b * v.Hkv + g) * v.Nmax + pos] = 0.f;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int buf = 0; buf < 2; ++buf) {
@@ -294,11 +309,18 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
   int c_live = 0, c_t3 = 0;
   unsigned smax = 0u;                      // max S over the live set (bits; S >= 0)
   bool bad = false;
+  const bool win = v.snap != nullptr;      // windowed / R-KV (AMB-32); parts == 1 (classify_gathered refuses)
   for (int pos = tid; pos < n; pos += CLS_THREADS) {
     float s = Sx[((size_t)b * v.Hkv) * v.Nmax + pos];
     for (int gg = 1; gg < parts * v.Hkv; ++gg) {     // ascending global kv head
       const int part = gg / v.Hkv, g = gg - part * v.Hkv;
       s = __fadd_rn(s, Sx[(((size_t)part * v.B + b) * v.Hkv + g) * v.Nmax + pos]);
+    }
+    if (win) {                             // W_i = fp32(sum_g S) - fp32(sum_g S_snap)
+      const float* sn = v.snap + (size_t)b * v.Hkv * v.Nmax + pos;
+      float s0 = sn[0];
+      for (int g = 1; g < v.Hkv; ++g) s0 = __fadd_rn(s0, sn[(size_t)g * v.Nmax]);
+      s = __fsub_rn(s, s0);
     }
     fS[pos] = s;
     bad |= !(s >= 0.f) || isinf(s);
@@ -317,9 +339,34 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
     atomicAdd(&s_cnt[0], c_live);
     atomicAdd(&s_cnt[1], c_t3);
   }
-  if (v.red) atomicMax(&s_smax, smax);
+  if (v.red && !win) atomicMax(&s_smax, smax);
   if (bad) atomicOr(&v.st->err, 1);
   __syncthreads();
+  if (win) {
+    // max-pool (kernel 7, stride 1) over the non-T3 positions in ascending order: the visible
+    // list of the last event followed by the positions appended since (all T0), P:976 / AMB-32
+    const int nve = v.cnt[cur][b * CNT_STRIDE + 4];
+    const int nvis = nve + (n - v.st->n_event);
+    const int* vl = v.idxvis[cur] + (size_t)b * v.Nmax;
+    const int ne = v.st->n_event;
+    float* pl = v.pool + (size_t)b * v.Nmax;
+    auto vpos = [&](int j) { return j < nve ? vl[j] : ne + (j - nve); };
+    for (int j = tid; j < nvis; j += CLS_THREADS) {
+      float m = fS[vpos(j)];
+      for (int x = max(0, j - RKV_HALF_POOL); x <= min(nvis - 1, j + RKV_HALF_POOL); ++x) m = fmaxf(m, fS[vpos(x)]);
+      pl[vpos(j)] = m;
+    }
+    __syncthreads();
+    unsigned pmax = 0u;
+    for (int j = tid; j < nvis; j += CLS_THREADS) {
+      const int pos = vpos(j);
+      const float m = pl[pos];
+      fS[pos] = m;
+      if (pos >= prot_lo && pos < prot_hi) pmax = max(pmax, __float_as_uint(m));
+    }
+    if (v.red) atomicMax(&s_smax, pmax);
+    __syncthreads();
+  }
   if (v.red) {
     // redundancy / combined (AMB-31): rank by I - rho, I = S / S_max, rho = mean_{l,g} cos
     const float fmax = __uint_as_float(s_smax);
@@ -329,7 +376,9 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
       float rs = r[0];
       for (int g = 1; g < v.Hkv; ++g) rs = __fadd_rn(rs, r[(size_t)g * v.Nmax]);
       const float I = fmax > 0.f ? __fdiv_rn(fS[pos], fmax) : 0.f;
-      fS[pos] = __fsub_rn(I, __fdiv_rn(rs, lh));
+      const float rho = __fdiv_rn(rs, lh);
+      fS[pos] = v.scorer == 5 ? __fsub_rn(__fmul_rn(0.07f, I), __fmul_rn(0.93f, rho))   // R-KV (AMB-33)
+                              : __fsub_rn(I, rho);
     }
     __syncthreads();
   }
@@ -633,118 +682,135 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(const DevView v) {
   for (int p = tid; p < n; p += PLAN_THREADS)
     if (tnew[p] == T3) rnew[p] = -1;
   if (tid == 0) {
+    if (b == 0) *v.gbar = 0u;                                 // k_migrate_rows' grid barrier
     v.mcount[b] = min(s_nm, v.mcap);
     if (s_nm > v.mcap) atomicOr(&v.st->err, 2);              // cannot happen: moves <= n <= mcap
   }
 }
 
-// Migrate, phase 1: every moved row of the (layer, kv head) pairs [lg0, lg0 + gridDim.y), K and V
-// -> the staging buffer mtemp in the destination's format (bf16 canonical, or int8 codes + scale
-// for T2).  The stores are updated in place, so a chunk's rows are all gathered before any is
-// scattered; pairs are independent (a move never crosses layers or heads).
+// Migrate (a6) in ONE cooperative launch: every moved row of every (layer, kv head) pair.  The
+// stores are updated in place, so the moved rows of a chunk of pairs are all gathered into
+// mtemp (destination format: bf16 canonical, or int8 codes + scale for T2) before any is
+// scattered; the chunk holds as many pairs as mtemp fits at this event's largest move count
+// (pairs are independent: a move never crosses layers or heads).  Rows newly in T1 / T2 are
+// written to the pinned host stores in the gather phase (zero-copy stores over the host link:
+// "Offload T1 entries").  Work items = (pair, request, move), one warp each; grid-wide
+// barriers between the phases (all CTAs co-resident: cudaLaunchAttributeCooperative).
+__device__ __forceinline__ bool grid_barrier(unsigned* ctr, unsigned target) {
+  bool ok = true;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    const unsigned long long t0 = gtimer();
+    for (;;) {
+      unsigned x;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(x) : "l"(ctr) : "memory");
+      if (x >= target) break;
+      if (gtimer() - t0 > 2000000000ull) { ok = false; break; }   // watchdog: report, never hang
+      __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  return ok;
+}
+
 template <int D>
-__global__ void __launch_bounds__(256) k_move_gather(const DevView v, const int cur, const int lg0) {
+__global__ void __launch_bounds__(256) k_migrate_rows(const DevView v) {
   constexpr int E = D / 32;
-  const int b = blockIdx.z, lg = lg0 + blockIdx.y, l = lg / v.Hkv, g = lg % v.Hkv;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m = blockIdx.x * 8 + w;
-  if (m >= v.mcount[b]) return;
-  const int4 mv = v.moves[(size_t)b * v.mcap + m];
-  const int st = mv.x, srow = mv.y, dt = mv.z & 3, pos = mv.w;
-  if (st == T1 && dt == T1 && v.stream_mode) return;       // list-only move (rows live on the host)
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int B = v.B, npairs = v.L * v.Hkv;
+  int mmax = 0;
+  for (int b = 0; b < B; ++b) mmax = max(mmax, v.mcount[b]);
+  if (mmax == 0) return;                                      // uniform over the grid: no barrier reached
+  const long long cap_rows = (long long)B * v.mcap * v.mchunk;
+  const int K = (int)max(1ll, min((long long)npairs, cap_rows / ((long long)B * mmax)));
   const int sb = v.st->scur;
-  const size_t grp = grp_of(v, l, b, g);
-  uint16_t* tmp = reinterpret_cast<uint16_t*>(v.mtemp) + (((size_t)b * v.mcap + m) * v.mchunk + blockIdx.y) * 2 * D;
-  for (int kv = 0; kv < 2; ++kv) {
-    uint16_t* tk = tmp + kv * D;
-    if (dt == T2 && st == T2) {       // T2 -> T2: codes and scale verbatim
-      const int8_t* c = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + srow) * D + lane * E;
-      int8_t* o = reinterpret_cast<int8_t*>(tk) + lane * E;
+  unsigned gen = 0;
+  bool ok = true;
+  for (int c0 = 0; c0 < npairs; c0 += K) {
+    const long long items = (long long)min(K, npairs - c0) * B * mmax;
+    // ---- phase 1: gather (+ host offload)
+    for (long long i = gw; i < items; i += nw) {
+      const int m = (int)(i % mmax);
+      const long long r = i / mmax;
+      const int b = (int)(r % B), lg = c0 + (int)(r / B), l = lg / v.Hkv, g = lg % v.Hkv;
+      if (m >= v.mcount[b]) continue;
+      const int4 mv = v.moves[(size_t)b * v.mcap + m];
+      const int st = mv.x, srow = mv.y, dt = mv.z & 3, pos = mv.w;
+      if (st == T1 && dt == T1 && v.stream_mode) continue;   // list-only move (rows live on the host)
+      const size_t grp = grp_of(v, l, b, g);
+      const bool off = st != dt && (dt == T1 || (dt == T2 && v.hc2k != nullptr));
+      uint16_t* tmp = reinterpret_cast<uint16_t*>(v.mtemp) + (size_t)i * 2 * D;
+      for (int kv = 0; kv < 2; ++kv) {
+        uint16_t* tk = tmp + kv * D;
+        if (dt == T2 && st == T2) {       // T2 -> T2: codes and scale verbatim
+          const int8_t* c = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + srow) * D + lane * E;
+          int8_t* o = reinterpret_cast<int8_t*>(tk) + lane * E;
 #pragma unroll
-      for (int k = 0; k < E; ++k) o[k] = c[k];
-      if (lane == 0) *reinterpret_cast<float*>(reinterpret_cast<int8_t*>(tk) + D) = (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + srow];
-    } else {
-      uint16_t x[E];
-      source_row<D>(v, sb, kv, grp, st, srow, pos, lane, x);
-      if (dt == T2) {
-        int8_t codes[E];
-        float sc;
-        quantize_row<D>(x, codes, &sc, lane);
-        int8_t* o = reinterpret_cast<int8_t*>(tk) + lane * E;
+          for (int k = 0; k < E; ++k) o[k] = c[k];
+          if (lane == 0) *reinterpret_cast<float*>(reinterpret_cast<int8_t*>(tk) + D) = (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + srow];
+          continue;
+        }
+        uint16_t x[E];
+        source_row<D>(v, sb, kv, grp, st, srow, pos, lane, x);
+        if (dt == T2) {
+          int8_t codes[E];
+          float sc;
+          quantize_row<D>(x, codes, &sc, lane);
+          int8_t* o = reinterpret_cast<int8_t*>(tk) + lane * E;
 #pragma unroll
-        for (int k = 0; k < E; ++k) o[k] = codes[k];
-        if (lane == 0) *reinterpret_cast<float*>(reinterpret_cast<int8_t*>(tk) + D) = sc;
-      } else {
-        store_bits(tk + lane * E, x, E);
+          for (int k = 0; k < E; ++k) o[k] = codes[k];
+          if (lane == 0) *reinterpret_cast<float*>(reinterpret_cast<int8_t*>(tk) + D) = sc;
+          if (off) {
+            int8_t* dc = (kv ? v.hc2v : v.hc2k) + host_row(v, grp, pos) * D + lane * E;
+#pragma unroll
+            for (int k = 0; k < E; ++k) dc[k] = codes[k];
+            if (lane == 0) (kv ? v.hs2v : v.hs2k)[host_row(v, grp, pos)] = sc;
+          }
+        } else {
+          store_bits(tk + lane * E, x, E);
+          if (off) store_bits(reinterpret_cast<uint16_t*>(kv ? v.hv1 : v.hk1) + host_row(v, grp, pos) * D + lane * E, x, E);
+        }
+      }
+      if (off && lane == 0) atomicAdd(&v.st->d2h_rows, 2ull);
+    }
+    ok &= grid_barrier(v.gbar, ++gen * gridDim.x);
+    // ---- phase 2: scatter into the destination rows
+    for (long long i = gw; i < items; i += nw) {
+      const int m = (int)(i % mmax);
+      const long long r = i / mmax;
+      const int b = (int)(r % B), lg = c0 + (int)(r / B), l = lg / v.Hkv, g = lg % v.Hkv;
+      if (m >= v.mcount[b]) continue;
+      const int4 mv = v.moves[(size_t)b * v.mcap + m];
+      const int dt = mv.z & 3, drow = mv.z >> 2;
+      if (dt == T1 && v.stream_mode) continue;               // T1 rows live on the host
+      const size_t grp = grp_of(v, l, b, g);
+      const uint16_t* tmp = reinterpret_cast<const uint16_t*>(v.mtemp) + (size_t)i * 2 * D;
+      for (int kv = 0; kv < 2; ++kv) {
+        const uint16_t* tk = tmp + kv * D;
+        if (dt == T2) {
+          const int8_t* c = reinterpret_cast<const int8_t*>(tk) + lane * E;
+          int8_t* o = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + drow) * D + lane * E;
+#pragma unroll
+          for (int k = 0; k < E; ++k) o[k] = c[k];
+          if (lane == 0) (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + drow] = *reinterpret_cast<const float*>(reinterpret_cast<const int8_t*>(tk) + D);
+        } else {
+          uint16_t x[E];
+          load_bits(x, tk + lane * E, E);
+          uint16_t* dst = dt == T0
+              ? reinterpret_cast<uint16_t*>(kv ? v.v0[sb] : v.k0[sb]) + (grp * v.cap0 + drow) * D
+              : reinterpret_cast<uint16_t*>(kv ? v.v1[sb] : v.k1[sb]) + (grp * v.cap1 + drow) * D;
+          store_bits(dst + swz_off(drow, lane * E, D), x, E);
+        }
       }
     }
+    if (c0 + K < npairs) ok &= grid_barrier(v.gbar, ++gen * gridDim.x);   // mtemp is reused
   }
-}
-
-// Migrate, phase 2: staging buffer -> destination rows of the same chunk.
-template <int D>
-__global__ void __launch_bounds__(256) k_move_scatter(const DevView v, const int cur, const int lg0) {
-  constexpr int E = D / 32;
-  const int b = blockIdx.z, lg = lg0 + blockIdx.y, l = lg / v.Hkv, g = lg % v.Hkv;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m = blockIdx.x * 8 + w;
-  if (m >= v.mcount[b]) return;
-  const int4 mv = v.moves[(size_t)b * v.mcap + m];
-  const int dt = mv.z & 3, drow = mv.z >> 2;
-  if (dt == T1 && v.stream_mode) return;                     // T1 rows live on the host
-  const int sb = v.st->scur;
-  const size_t grp = grp_of(v, l, b, g);
-  const uint16_t* tmp = reinterpret_cast<const uint16_t*>(v.mtemp) + (((size_t)b * v.mcap + m) * v.mchunk + blockIdx.y) * 2 * D;
-  for (int kv = 0; kv < 2; ++kv) {
-    const uint16_t* tk = tmp + kv * D;
-    if (dt == T2) {
-      const int8_t* c = reinterpret_cast<const int8_t*>(tk) + lane * E;
-      int8_t* o = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + drow) * D + lane * E;
-#pragma unroll
-      for (int k = 0; k < E; ++k) o[k] = c[k];
-      if (lane == 0) (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + drow] = *reinterpret_cast<const float*>(reinterpret_cast<const int8_t*>(tk) + D);
-    } else {
-      uint16_t x[E];
-      load_bits(x, tk + lane * E, E);
-      uint16_t* dst = dt == T0
-          ? reinterpret_cast<uint16_t*>(kv ? v.v0[sb] : v.k0[sb]) + (grp * v.cap0 + drow) * D
-          : reinterpret_cast<uint16_t*>(kv ? v.v1[sb] : v.k1[sb]) + (grp * v.cap1 + drow) * D;
-      store_bits(dst + swz_off(drow, lane * E, D), x, E);
-    }
-  }
-}
-
-// Offload to the pinned host stores (zero-copy stores over the host link) of a chunk's moves:
-// rows newly in T1 (paper: "Offload T1 entries") and new T2 codes, from mtemp.
-template <int D>
-__global__ void __launch_bounds__(256) k_offload_moves(const DevView v, const int cur, const int lg0) {
-  constexpr int E = D / 32;
-  const int b = blockIdx.z, lg = lg0 + blockIdx.y, l = lg / v.Hkv, g = lg % v.Hkv;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m = blockIdx.x * 8 + w;
-  if (m >= v.mcount[b]) return;
-  const int4 mv = v.moves[(size_t)b * v.mcap + m];
-  const int st = mv.x, dt = mv.z & 3, pos = mv.w;
-  if (st == dt || dt == T0) return;
-  if (dt == T2 && v.hc2k == nullptr) return;
-  const size_t grp = grp_of(v, l, b, g);
-  const uint16_t* tmp = reinterpret_cast<const uint16_t*>(v.mtemp) + (((size_t)b * v.mcap + m) * v.mchunk + blockIdx.y) * 2 * D;
-  for (int kv = 0; kv < 2; ++kv) {
-    const uint16_t* tk = tmp + kv * D;
-    if (dt == T1) {
-      uint16_t x[E];
-      load_bits(x, tk + lane * E, E);
-      uint16_t* dst = reinterpret_cast<uint16_t*>(kv ? v.hv1 : v.hk1) + host_row(v, grp, pos) * D;
-      store_bits(dst + lane * E, x, E);
-    } else {
-      const int8_t* c = reinterpret_cast<const int8_t*>(tk) + lane * E;
-      int8_t* dc = (kv ? v.hc2v : v.hc2k) + host_row(v, grp, pos) * D + lane * E;
-#pragma unroll
-      for (int k = 0; k < E; ++k) dc[k] = c[k];
-      if (lane == 0) (kv ? v.hs2v : v.hs2k)[host_row(v, grp, pos)] = *reinterpret_cast<const float*>(reinterpret_cast<const int8_t*>(tk) + D);
-    }
-  }
-  if (lane == 0) atomicAdd(&v.st->d2h_rows, 2ull);
+  if (!ok && threadIdx.x == 0) atomicOr(&v.st->err, 4);
 }
 
 __global__ void k_commit(const DevView v) {
@@ -782,6 +848,11 @@ __global__ void __launch_bounds__(256) k_prefetch(const DevView v, const int lay
 
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_begin_step(const DevView& v, cudaStream_t s) {
+  if (v.snap) {                                  // windowed / R-KV scorers: the window may start here
+    k_snapshot<<<dim3(64, v.B * v.Hkv), 256, 0, s>>>(v);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   k_begin_step<<<1, ((v.B + 31) / 32) * 32, 0, s>>>(v);
   return cudaGetLastError();
 }
@@ -818,19 +889,31 @@ cudaError_t launch_plan(const DevView& v, cudaStream_t s) {
   k_plan<<<v.B, PLAN_THREADS, 0, s>>>(v);
   return cudaGetLastError();
 }
-// one chunk of (layer, kv head) pairs [lg0, lg0 + nlg): gather, scatter, host offload
-cudaError_t launch_move_chunk(const DevView& v, int cur, int lg0, int nlg, cudaStream_t s) {
-  dim3 grid((v.mcap + 7) / 8, nlg, v.B);
-  if (v.D == 128) {
-    k_move_gather<128><<<grid, 256, 0, s>>>(v, cur, lg0);
-    k_move_scatter<128><<<grid, 256, 0, s>>>(v, cur, lg0);
-    k_offload_moves<128><<<grid, 256, 0, s>>>(v, cur, lg0);
-  } else {
-    k_move_gather<64><<<grid, 256, 0, s>>>(v, cur, lg0);
-    k_move_scatter<64><<<grid, 256, 0, s>>>(v, cur, lg0);
-    k_offload_moves<64><<<grid, 256, 0, s>>>(v, cur, lg0);
+// every moved row of the event: one cooperative launch, as many CTAs as are co-resident (<= 2 per SM)
+template <int D>
+static cudaError_t migrate_rows_t(const DevView& v, cudaStream_t s) {
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_migrate_rows<D>, 256, 0);
+    if (e != cudaSuccess) return e;
+    grid = sms * std::max(1, std::min(per, 2));
   }
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_migrate_rows<D>, v);
+}
+cudaError_t launch_migrate_rows(const DevView& v, cudaStream_t s) {
+  return v.D == 128 ? migrate_rows_t<128>(v, s) : migrate_rows_t<64>(v, s);
 }
 cudaError_t launch_commit(const DevView& v, cudaStream_t s) {
   k_commit<<<1, 32, 0, s>>>(v);

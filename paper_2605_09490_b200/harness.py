@@ -30,10 +30,12 @@ class TieredDecode:
     first manage event (t = 0) sees exactly N tokens (reading AMB-22)."""
 
     def __init__(self, w, device="cuda:0", out_fp32=True, split=0, seed_offset=0, keep_inputs=False, variant=0,
-                 heads=None, classify_fn=None, shard=kt.SHARD_REQUEST, rank=0, world=1):
+                 heads=None, classify_fn=None, shard=kt.SHARD_REQUEST, rank=0, world=1, nccl_id=None):
         """heads = (first kv head, count): this ctx holds only those kv heads and their q
         heads (KV-head sharding); classify_fn(run, stream) replaces kv.classify at events
-        (e.g. dist.kvhead_classify, or a single-process gather over several ctxs)."""
+        (e.g. dist.kvhead_classify, or a single-process gather over several ctxs); nccl_id:
+        sequence sharding on the library's own communicator (kv_tier_step / the step graph
+        run the per-layer exchange, kv_tier_classify the event's all-gather)."""
         self.w = w
         self.dev = torch.device(device)
         torch.cuda.set_device(self.dev)
@@ -53,7 +55,7 @@ class TieredDecode:
                                   policy_seed=w.get("policy_seed", 0), scorer=w.get("scorer", 0))
         hs = slice(h0, h0 + hl)
         qs = slice(h0 * G, (h0 + hl) * G)
-        self.kv = kt.KvTier(self.cfg)
+        self.kv = kt.KvTier(self.cfg, nccl_id=nccl_id)
         self.main = torch.cuda.Stream(self.dev)
         self.side = torch.cuda.Stream(self.dev)
         with torch.cuda.stream(self.main):

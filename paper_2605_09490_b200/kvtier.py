@@ -20,10 +20,10 @@ STATUS = {0: "OK", -1: "E_INVAL", -2: "E_CUDA", -3: "E_NCCL", -4: "E_STATE", -5:
 EVICT_TOTAL, EVICT_PER_EVENT = 0, 1
 SHARD_REQUEST, SHARD_KVHEAD, SHARD_SEQUENCE = 0, 1, 2
 POLICY_HIERARCHY, POLICY_STREAMING, POLICY_H2O, POLICY_RANDOM = 0, 1, 2, 3
-SCORER_ATTENTION, SCORER_VATP, SCORER_REDUNDANCY, SCORER_COMBINED = 0, 1, 2, 3
+SCORER_ATTENTION, SCORER_VATP, SCORER_REDUNDANCY, SCORER_COMBINED, SCORER_WINDOW, SCORER_RKV = 0, 1, 2, 3, 4, 5
 STAGING_ALL = 0xFFFFFFFF
 (X_SCORES, X_TIERS, X_IDX_T0, X_IDX_T1, X_IDX_T2, X_T0_ROWS, X_T1_ROWS, X_STAGING, X_T2_CODES, X_T2_SCALES,
- X_REDUNDANCY) = range(11)
+ X_REDUNDANCY, X_SNAPSHOT) = range(12)
 
 
 class KvTierError(RuntimeError):
@@ -58,6 +58,7 @@ _SIGS = {
     "kv_tier_query_sizes": [C.POINTER(Config), C.POINTER(Sizes)],
     "kv_tier_init": [C.POINTER(Config), C.POINTER(Buffers), C.c_void_p, C.POINTER(C.c_void_p)],
     "kv_tier_destroy": [C.c_void_p],
+    "kv_tier_nccl_unique_id": [C.c_void_p, C.c_size_t],
     "kv_tier_load_prefix": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p],
     "kv_tier_begin_step": [C.c_void_p, C.c_void_p],
     "kv_tier_append": [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p],
@@ -146,6 +147,16 @@ def make_config(B, L, Hq, Hkv, d, max_tokens, prompt_len, hbm_bp=5000, evict_bp=
                   policy_seed=policy_seed, scorer=scorer)
 
 
+NCCL_ID_BYTES = 128
+
+
+def nccl_unique_id():
+    """A fresh ncclUniqueId (bytes) for kv_tier_init: rank 0 draws it, every rank passes it."""
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    _check(load().kv_tier_nccl_unique_id(buf, NCCL_ID_BYTES))
+    return buf.raw
+
+
 def query_sizes(cfg):
     s = Sizes()
     _check(load().kv_tier_query_sizes(C.byref(cfg), C.byref(s)))
@@ -155,14 +166,17 @@ def query_sizes(cfg):
 class KvTier:
     """One ctx.  The device arena is a torch uint8 tensor owned by this object."""
 
-    def __init__(self, cfg: Config):
+    def __init__(self, cfg: Config, nccl_id: bytes = None):
+        """nccl_id: sequence sharding with the library's own communicator (kv_tier_nccl_unique_id
+        bytes, identical on every rank); None: no collective inside the library."""
         import torch
         self.cfg = cfg
         self.sizes = query_sizes(cfg)
         self.arena = torch.empty(self.sizes.device_arena, dtype=torch.uint8, device=f"cuda:{cfg.device}")
         buf = Buffers(device_arena=C.c_void_p(self.arena.data_ptr()))
         h = C.c_void_p()
-        _check(load().kv_tier_init(C.byref(cfg), C.byref(buf), None, C.byref(h)))
+        idb = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), NCCL_ID_BYTES)
+        _check(load().kv_tier_init(C.byref(cfg), C.byref(buf), idb, C.byref(h)))
         self.ctx = h
 
     def close(self):
@@ -315,7 +329,7 @@ class KvTier:
         buf = np.zeros(nbytes.value, dtype=np.uint8)
         _check(load().kv_tier_export(self.ctx, what, layer, buf.ctypes.data_as(C.c_void_p), nbytes.value), self.ctx)
         B, H, D = self.cfg.num_requests, self.cfg.num_kv_heads, self.cfg.head_dim
-        if what in (X_SCORES, X_REDUNDANCY):
+        if what in (X_SCORES, X_REDUNDANCY, X_SNAPSHOT):
             return buf.view(np.float32).reshape(B, H, -1)
         if what == X_TIERS:
             return buf.reshape(B, -1)

@@ -120,7 +120,7 @@ def test_lse_combine_rejects_bad_arguments():
         assert st == -1                                            # E_INVAL
 
 
-@pytest.mark.parametrize("field,value", [("policy", 9), ("scorer", 4), ("budget", 0)])
+@pytest.mark.parametrize("field,value", [("policy", 9), ("scorer", 6), ("scorer", -1), ("budget", 0)])
 def test_policy_and_scorer_validation(field, value):
     kw = dict(policy=kt.POLICY_H2O, budget=100)
     kw[field] = value
@@ -131,7 +131,9 @@ def test_policy_and_scorer_validation(field, value):
 
 def test_redundancy_scorers_refused_under_sequence_sharding():
     # neighbour cosine needs position i-1, which another sequence shard owns (AMB-31)
-    for sc, want in ((kt.SCORER_REDUNDANCY, -1), (kt.SCORER_COMBINED, -1), (kt.SCORER_VATP, 0)):
+    # the windowed scorers pool over the whole cache order (AMB-32): also refused
+    for sc, want in ((kt.SCORER_REDUNDANCY, -1), (kt.SCORER_COMBINED, -1), (kt.SCORER_VATP, 0),
+                     (kt.SCORER_WINDOW, -1), (kt.SCORER_RKV, -1)):
         cfg = kt.make_config(2, 1, 4, 2, 64, 300, 16, scorer=sc, shard=kt.SHARD_SEQUENCE, world=2, rank=0)
         s = kt.Sizes()
         assert kt.load().kv_tier_query_sizes(C.byref(cfg), C.byref(s)) == want
@@ -147,6 +149,39 @@ def test_redundancy_scorers_size_their_buffers():
         sz[sc] = s.device_arena
     extra = sz[kt.SCORER_REDUNDANCY] - sz[kt.SCORER_ATTENTION]
     assert 2 * 2 * 300 * 4 + 3 * 2 * 2 * 64 * 2 <= extra <= 2 * 2 * 300 * 4 + 3 * 2 * 2 * 64 * 2 + 2 * 256
+
+
+def test_window_scorers_size_their_buffers():
+    # windowed: the snapshot [B][H_kv][N] + the pool scratch [B][N] fp32; R-KV adds R-KV's
+    # redundancy buffers on top (R_part + previous keys)
+    sz = {}
+    for sc in (kt.SCORER_ATTENTION, kt.SCORER_WINDOW, kt.SCORER_RKV, kt.SCORER_REDUNDANCY):
+        cfg = kt.make_config(2, 3, 4, 2, 64, 300, 16, scorer=sc)
+        s = kt.Sizes()
+        assert kt.load().kv_tier_query_sizes(C.byref(cfg), C.byref(s)) == 0
+        sz[sc] = s.device_arena
+    win = 2 * 2 * 300 * 4 + 2 * 300 * 4
+    assert win <= sz[kt.SCORER_WINDOW] - sz[kt.SCORER_ATTENTION] <= win + 2 * 256
+    red = sz[kt.SCORER_REDUNDANCY] - sz[kt.SCORER_ATTENTION]
+    assert win + red <= sz[kt.SCORER_RKV] - sz[kt.SCORER_ATTENTION] <= win + red + 4 * 256
+    cfg = kt.make_config(2, 3, 4, 2, 64, 300, 16, scorer=kt.SCORER_WINDOW, manage_interval=0)
+    assert kt.load().kv_tier_query_sizes(C.byref(cfg), C.byref(kt.Sizes())) == -1
+
+
+def test_nccl_unique_id_and_init_guards():
+    # the library resolves NCCL at run time: an id is 128 bytes and differs per call; an id is
+    # refused for shard modes without a collective, and for bf16 o (the combine is fp32)
+    a, b = kt.nccl_unique_id(), kt.nccl_unique_id()
+    assert len(a) == kt.NCCL_ID_BYTES and a != b
+    lib = kt.load()
+    assert lib.kv_tier_nccl_unique_id(None, 128) == -1
+    idb = C.create_string_buffer(a, kt.NCCL_ID_BYTES)
+    h = C.c_void_p()
+    buf = kt.Buffers(device_arena=C.c_void_p(1 << 20))
+    for kw in (dict(shard=kt.SHARD_REQUEST), dict(shard=kt.SHARD_KVHEAD, world=2),
+               dict(shard=kt.SHARD_SEQUENCE, world=2, out_fp32=0)):
+        cfg = kt.make_config(2, 1, 4, 2, 64, 300, 16, **kw)
+        assert lib.kv_tier_init(C.byref(cfg), C.byref(buf), idb, C.byref(h)) == -1
 
 
 def test_host_t1_entry_points_reject_null_ctx():

@@ -70,8 +70,9 @@ def _check_event_state(run, orc, reqs_gpu, layers=(0,)):
                 assert np.array_equal(scales[bg][:, :, 1], st.scaleV[l, bo, hs][:, pos])
 
 
-def _run_pair(w, reqs=None, graph=False, check_every=1, layers_api=False, split=0, variant=0, out_fp32=True):
-    run = H.TieredDecode(w, split=split, variant=variant, out_fp32=out_fp32)
+def _run_pair(w, reqs=None, graph=False, check_every=1, layers_api=False, split=0, variant=0, out_fp32=True,
+              **run_kw):
+    run = H.TieredDecode(w, split=split, variant=variant, out_fp32=out_fp32, **run_kw)
     orc = OracleRun(w, reqs=reqs)
     reqs_gpu = orc.reqs
     if graph:
@@ -93,6 +94,9 @@ def _run_pair(w, reqs=None, graph=False, check_every=1, layers_api=False, split=
                 R_gpu = run.kv.export(kt.X_REDUNDANCY)[reqs_gpu]
                 err = np.abs(R_gpu - orc.st.R_part[:, :, :orc.st.n]).max()
                 assert err <= 2e-6 * w["L"], f"redundancy mismatch at step {t}: {err}"
+            if orc.st.S_snap is not None:          # windowed scorers: the window's start snapshot (AMB-32)
+                ok, mrel = s_close(run.kv.export(kt.X_SNAPSHOT)[reqs_gpu], orc.st.S_snap[:, :, :orc.st.n])
+                assert ok, f"snapshot mismatch at step {t}: max rel {mrel}"
             if run.is_event(t):
                 _check_event_state(run, orc, reqs_gpu)
     run.close()
@@ -482,6 +486,26 @@ def test_sequence_shard_refuses_plain_paths():
     run.close()
 
 
+@pytest.mark.parametrize("graph,staging", [(True, kt.STAGING_ALL), (False, kt.STAGING_ALL), (True, 0)])
+def test_sequence_shard_library_communicator(graph, staging):
+    # kv_tier_init with an nccl_unique_id: kv_tier_step runs every layer's all-gather of (o, m, l)
+    # on the library's NCCL communicator, the LSE combine and the rescaled score update -- the
+    # whole step captured as ONE CUDA graph -- and kv_tier_classify all-gathers S_part itself.
+    # world = 1 (one GPU): the collective is the identity, the path and its state machine are
+    # the multi-rank ones
+    w = H.workload("tiny", B=2, L=3, Hq=8, Hkv=2, d=64, N=400, P=16, interval=8, steps=26,
+                   hbm_bp=4000, evict_bp=800, t2_bp=3000, staging=staging)
+    _run_pair(w, graph=graph, check_every=4, shard=kt.SHARD_SEQUENCE, rank=0, world=1,
+              nccl_id=kt.nccl_unique_id())
+
+
+def test_sequence_shard_library_communicator_7b_sampled():
+    # 7B-shaped (28 layers, G = 7, d = 128) through the communicator path, requests 2 and 7
+    w = H.workload("7b", steps=10, interval=4)
+    _run_pair(w, reqs=[2, 7], graph=True, check_every=3, shard=kt.SHARD_SEQUENCE, rank=0, world=1,
+              nccl_id=kt.nccl_unique_id())
+
+
 def _seq_proc_worker(rank, world, port, q):
     import os
     import torch.distributed as tdist
@@ -566,6 +590,32 @@ def test_redundancy_scorer_parity(scorer, api):
     w = H.workload("tiny", B=3, L=3, Hq=8, Hkv=2, d=128, N=600, P=32, interval=8, steps=26,
                    hbm_bp=4000, evict_bp=1200, t2_bp=3000, scorer=sc)
     _run_pair(w, graph=api == "graph", layers_api=api == "layers", check_every=4)
+
+
+@pytest.mark.parametrize("scorer", ["window", "rkv"])
+@pytest.mark.parametrize("api,interval", [("graph", 16), ("layers", 8), ("step", 4)])
+def test_window_scorer_parity(scorer, api, interval):
+    # windowed attention (last w = min(8, Delta) steps, max-pooled over the cache) and
+    # R-KV's Z = 0.07 I - 0.93 R (App. E): S_part, the window snapshot, tiers, index
+    # lists and rows at every event equal the oracle's (AMB-32/33); T2 on
+    sc = kt.SCORER_WINDOW if scorer == "window" else kt.SCORER_RKV
+    w = H.workload("tiny", B=3, L=3, Hq=8, Hkv=2, d=128, N=600, P=32, interval=interval, steps=2 * interval + 10,
+                   hbm_bp=4000, evict_bp=1200, t2_bp=3000, scorer=sc)
+    _run_pair(w, graph=api == "graph", layers_api=api == "layers", check_every=4)
+
+
+def test_window_scorer_refused_in_classify_gathered():
+    w = H.workload("tiny", Hq=4, Hkv=2, steps=2, scorer=kt.SCORER_WINDOW)
+    sh = H.KvHeadShardedDecode(w, 2)
+    with pytest.raises(kt.KvTierError):
+        sh.step()                                    # t = 0 is an event
+    sh.close()
+
+
+def test_rkv_scorer_sampled_7b_requests():
+    # the 7B-shaped config (d = 128, 28 layers, G = 7) with R-KV's scorer, requests 1 and 6
+    w = H.workload("7b", steps=18, interval=8, scorer=kt.SCORER_RKV)
+    _run_pair(w, reqs=[1, 6], check_every=4)
 
 
 def test_redundancy_scorer_sampled_7b_requests():
@@ -730,7 +780,8 @@ def test_randomized_configs(seed):
                    staging=int(rng.choice([kt.STAGING_ALL, kt.STAGING_ALL, 0])),
                    policy=pol, budget=int(rng.integers(P + 140, N + 50)) if pol in (2, 3) else 0,
                    policy_seed=seed, scorer=int(rng.choice([0, 0, kt.SCORER_VATP, kt.SCORER_REDUNDANCY,
-                                                             kt.SCORER_COMBINED])))
+                                                             kt.SCORER_COMBINED, kt.SCORER_WINDOW,
+                                                             kt.SCORER_RKV])))
     api = int(rng.integers(0, 3))             # step graph / kv_tier_step (whole-step kernel) / per-layer ABI
     _run_pair(w, graph=api == 0, layers_api=api == 2, check_every=3)
 
