@@ -80,6 +80,9 @@ def _args():
                          "positions split over the ranks with a per-layer LSE combine (strong scaling)")
     ap.add_argument("--scorer", default="attention", choices=list(SCORERS),
                     help="token scorer: Eq. 1 attention, VATP (P:712), redundancy (P:713), combined (P:714)")
+    ap.add_argument("--positions", type=int, default=0,
+                    help="chain length N per request (0: the config's); e.g. --config 70b --positions 2048 = "
+                         "the positions ONE rank of configs[4]'s 8-way sequence split attends")
     ap.add_argument("--no-extras", action="store_true", help="skip control/e2e/stream/N1/N4/cpu legs")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -341,6 +344,8 @@ def main():
     E = 0 if args.no_extras else 64                    # e2e window: exactly one Delta (one event)
     pol = POLICIES[args.policy]
     over = {"B": args.batch} if args.batch else {}
+    if args.positions:
+        over["N"] = args.positions
     # steps the longest leg needs (+ the event chase after the window)
     w = H.workload(args.config, hbm_bp=args.hbm, evict_bp=args.evict, steps=W + K + E + 66, policy=pol, **over,
                    budget=args.budget if pol in (2, 3) else 0, policy_seed=7, scorer=SCORERS[args.scorer])
@@ -552,7 +557,11 @@ def main():
                                    f"r={args.evict}bp Delta={itv} differential staging"
                                    + ("" if pol == 0 else f" policy={args.policy}"
                                       + (f" budget={args.budget}" if pol in (2, 3) else ""))
-                                   + ("" if args.scorer == "attention" else f" scorer={args.scorer}"),
+                                   + ("" if args.scorer == "attention" else f" scorer={args.scorer}")
+                                   + ("" if not args.positions else
+                                      f" (N overridden: {args.positions} positions per request"
+                                      + (", one rank's share of the 8-way sequence split; the per-layer "
+                                         "exchange is not in this number" if args.config == "70b" else "") + ")"),
                        "global_batch": B * world, "parallelism": f"request-sharded x{world}",
                        "l2": "no flush: per-step K/V traffic > 126 MB L2",
                        "step_kernel": {"ctas": shape[0], "ctas_per_kv_head": shape[1], "kv_heads_per_cta": shape[2],

@@ -176,6 +176,14 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + NST);
   const uint32_t nfull0 = smem_u32(bars + 2 * NST), nempty0 = smem_u32(bars + 2 * NST + 2);
   const uint32_t rxb0 = smem_u32(bars + 2 * NST + 4);
+  // S > 1: q(l) of the head reaches shared memory in ONE bulk copy issued by the new-token warp
+  // once the layer dependency holds; its completion (phase l & 1) is also the consumers' signal
+  // that q(l) may be used.  The copy lands in the receive half rx[(l + 1) & 1], which is idle
+  // during layer l: its last reader was merge(l - 1) (done before the dependency of layer l can
+  // hold) and its next writers are the peers' pushes of layer l + 1 (after they read q(l + 1),
+  // i.e. after every CTA finished o(l)).
+  const uint32_t qbar = smem_u32(bars + 2 * NST + 6);
+  auto qsm = [&](int l) { return rx + ((l + 1) & 1) * S * (16 + SL); };
   // q(l) and the new token's K/V of layer l are projections of o(l-1) of the same request: wait
   // until every CTA of the request has finished its part of o(l-1) (relaxed polling: the counter
   // orders the computation; no data produced by another CTA is read after it)
@@ -202,6 +210,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
       mbar_init(nempty0 + 8 * x, 1);
       mbar_init(rxb0 + 8 * x, 1);               // the owner's arrive.expect_tx; peers complete tx
     }
+    mbar_init(qbar, 1);
     *sc_done = 0;
     *ml_done = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -318,6 +327,14 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
         if (lane == 0) wait_layer(l);
         __syncwarp();
       }
+      if (S > 1) {                                           // q(l) of the head -> shared memory
+        if (lane == 0) {
+          const uint32_t qb = (uint32_t)(G * D * 2);
+          mbar_expect_tx(qbar, qb);
+          bulk_g2s(smem_u32(qsm(l)), io.q + (((size_t)l * B + b) * v.Hq + part(0).g * G) * D, qb, qbar);
+        }
+        mbar_sleep_wait(qbar, l & 1);
+      }
       float* zl = v.zbuf + (size_t)(l % ZS) * U * v.zrows * 8;
       for (int k = 0; k < npart; ++k) {
         const StepPart pp = part(k);
@@ -328,13 +345,15 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
         const uint16_t* vin = reinterpret_cast<const uint16_t*>(io.vnew) + (((size_t)l * B + b) * Hkv + g) * D;
         const uint16_t* qb0 = reinterpret_cast<const uint16_t*>(io.q) + (((size_t)l * B + b) * v.Hq + g * G) * D;
         uint16_t kb[EL], vb[EL], qb[8][EL];
+        const uint16_t* qsrc = S > 1 ? reinterpret_cast<const uint16_t*>(qsm(l)) : qb0;
 #pragma unroll
         for (int e2 = 0; e2 < EL; ++e2) {
           const int e = lane + 32 * e2;
           kb[e2] = __ldcg(kin + e);
           vb[e2] = __ldcg(vin + e);
 #pragma unroll
-          for (int h = 0; h < 8; ++h) qb[h][e2] = h < G ? __ldcg(qb0 + (size_t)h * D + e) : (uint16_t)0;
+          for (int h = 0; h < 8; ++h)
+            qb[h][e2] = h >= G ? (uint16_t)0 : S > 1 ? qsrc[(size_t)h * D + e] : __ldcg(qsrc + (size_t)h * D + e);
         }
         float dot[8];
 #pragma unroll
@@ -569,23 +588,33 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
         if (kpart == 0) {
           // q(l) is a projection of o(l-1): every CTA of this request has stored its part
           if (tid == 0) ctrace(l, 12);
+          if (S > 1) mbar_sleep_wait(qbar, l & 1);          // the dependency held and q(l) landed
           if (lane == 0) {
-            if (l > 0) wait_layer(l);
+            if (S == 1 && l > 0) wait_layer(l);
             if (io.score)
               while (*sc_done < l - ZS + 1) __nanosleep(128);   // logit slot of layer l - ZS consumed
           }
           __syncwarp();
           if (tid == 0) { trace(l, 1); ctrace(l, 13); }
         }
-        const __nv_bfloat16* qh = io.q + (((size_t)l * B + b) * v.Hq + g * G + gq) * D;
+        if (S > 1) {
+          const uint32_t* qw = reinterpret_cast<const uint32_t*>(qsm(l)) + (gq * D + 2 * tq) / 2;
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          if (gq < G) {
-            qf[ks][0] = __ldcg(reinterpret_cast<const unsigned int*>(qh + ks * 16 + 2 * tq));
-            qf[ks][1] = __ldcg(reinterpret_cast<const unsigned int*>(qh + ks * 16 + 8 + 2 * tq));
-          } else {
-            qf[ks][0] = 0u;
-            qf[ks][1] = 0u;
+          for (int ks = 0; ks < KS; ++ks) {
+            qf[ks][0] = gq < G ? qw[ks * 8] : 0u;
+            qf[ks][1] = gq < G ? qw[ks * 8 + 4] : 0u;
+          }
+        } else {
+          const __nv_bfloat16* qh = io.q + (((size_t)l * B + b) * v.Hq + g * G + gq) * D;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            if (gq < G) {
+              qf[ks][0] = __ldcg(reinterpret_cast<const unsigned int*>(qh + ks * 16 + 2 * tq));
+              qf[ks][1] = __ldcg(reinterpret_cast<const unsigned int*>(qh + ks * 16 + 8 + 2 * tq));
+            } else {
+              qf[ks][0] = 0u;
+              qf[ks][1] = 0u;
+            }
           }
         }
         mxa = mxb = -INFINITY;

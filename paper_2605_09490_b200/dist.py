@@ -125,30 +125,24 @@ def seq_owned_positions(n, world, rank):
 
 
 def lse_combine(o_parts, lse_parts):
-    """Combine per-rank partial attention results (rank order, deterministic).  CUDA tensors run
-    the library kernel (kv_tier_lse_combine); CPU tensors (gloo host-logic tests only) the same
-    arithmetic in torch.
-
-    o_parts [W][B][H][d]: each rank's o normalised by its own partial sum; lse_parts
-    [W][B][H][2]: (m, l) per head, m in the log2 domain, l = sum 2^(z - m) (a rank without
-    visible tokens has m = -inf, l = 0, o = 0).  Returns (o [B][H][d], lse [B][H][2]) with
-    M = max_r m_r, w_r = 2^(m_r - M) l_r, L = sum_r w_r, o = sum_r w_r o_r / L."""
-    if o_parts.is_cuda:
-        from . import kvtier as kt
-        return kt.lse_combine(o_parts, lse_parts)
-    m, l = lse_parts[..., 0], lse_parts[..., 1]
-    M = m.max(dim=0).values
-    w = torch.where(torch.isinf(m), torch.zeros_like(l), torch.exp2(m - M) * l)
-    L = w.sum(dim=0)
-    o = (w.unsqueeze(-1) * o_parts).sum(dim=0) / L.unsqueeze(-1)
-    return o, torch.stack([M, L], dim=-1)
+    """Combine per-rank partial attention results in rank order (deterministic) with the library
+    kernel kv_tier_lse_combine.  o_parts [W][B][H][d] fp32 CUDA: each rank's o normalised by its
+    own partial sum; lse_parts [W][B][H][2]: (m, l) per head, m in the log2 domain, l = sum
+    2^(z - m) (a rank without visible tokens has m = -inf, l = 0, o = 0).  Returns (o [B][H][d],
+    lse [B][H][2]) with M = max_r m_r, w_r = 2^(m_r - M) l_r, L = sum_r w_r, o = sum_r w_r o_r / L.
+    No CPU path: host tensors raise."""
+    if not o_parts.is_cuda:
+        raise RuntimeError("lse_combine runs the CUDA kernel (kv_tier_lse_combine): CUDA tensors only")
+    from . import kvtier as kt
+    return kt.lse_combine(o_parts, lse_parts)
 
 
-def seq_combine(o_local, lse_local, group=None):
-    """All-gather (o, lse) over the group (NCCL on CUDA tensors, gloo on CPU) and combine."""
+def seq_combine(o_local, lse_local, group=None, combine=None):
+    """All-gather (o, lse) over the group (NCCL on CUDA tensors, gloo on CPU) and combine them
+    (``combine`` defaults to the CUDA kernel; host-logic tests pass their own)."""
     og = gather_scores(o_local.float(), group)
     lg = gather_scores(lse_local, group)
-    return lse_combine(og, lg)
+    return (combine or lse_combine)(og, lg)
 
 
 def seq_classify(kv, stream=None, group=None):
