@@ -32,6 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+STEP_KERNELS = {"auto": 0, "mma": 1, "tcgen05": 2}                      # kv_tier_config::step_kernel
 CONFIG_INDEX = {"tiny": 0, "7b": 1, "14b": 2, "32b": 3, "70b": 4}      # BASELINE.json configs[i]
 POLICIES = {"hierarchy": 0, "streaming": 1, "h2o": 2, "random": 3}       # kv_tier_policy
 SCORERS = {"attention": 0, "vatp": 1, "redundancy": 2, "combined": 3}    # kv_tier_scorer
@@ -83,6 +84,8 @@ def _args():
     ap.add_argument("--positions", type=int, default=0,
                     help="chain length N per request (0: the config's); e.g. --config 70b --positions 2048 = "
                          "the positions ONE rank of configs[4]'s 8-way sequence split attends")
+    ap.add_argument("--step-kernel", default="auto", choices=list(STEP_KERNELS),
+                    help="whole-step kernel consumer: auto (= mma), mma (mma.sync), tcgen05 (TMEM accumulators)")
     ap.add_argument("--no-extras", action="store_true", help="skip control/e2e/stream/N1/N4/cpu legs")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -358,7 +361,8 @@ def main():
     L, B, Hkv, d, itv = w["L"], w["B"], w["Hkv"], w["d"], w["interval"]
 
     # ---- headline: tiered step (whole-step kernel via the step graph), device-resident inputs
-    run = H.TieredDecode(w, device=dev, out_fp32=False, split=args.split, seed_offset=seed_off)
+    run = H.TieredDecode(w, device=dev, out_fp32=False, split=args.split, seed_offset=seed_off,
+                         step_kernel=STEP_KERNELS[args.step_kernel])
     run.capture()
     m = measure_tiered(run, W, K, w, local)
     t_amort = _max_over_ranks(m["t_amortized"])
@@ -462,7 +466,8 @@ def main():
     if not args.no_extras:
         # ---- control: the same r and event schedule with beta = 100 % (every survivor in T0): the
         # visible sets match the tiered run's, so the difference is the hierarchy's own cost
-        ctl = H.TieredDecode(dict(w, hbm_bp=10000), device=dev, out_fp32=False, split=args.split, seed_offset=seed_off)
+        ctl = H.TieredDecode(dict(w, hbm_bp=10000), device=dev, out_fp32=False, split=args.split, seed_offset=seed_off,
+                             step_kernel=STEP_KERNELS[args.step_kernel])
         ctl.capture()
         mc = measure_tiered(ctl, W, K, dict(w, hbm_bp=10000), local, with_clocks=False)
         ctl.close()
@@ -565,7 +570,9 @@ def main():
                        "global_batch": B * world, "parallelism": f"request-sharded x{world}",
                        "l2": "no flush: per-step K/V traffic > 126 MB L2",
                        "step_kernel": {"ctas": shape[0], "ctas_per_kv_head": shape[1], "kv_heads_per_cta": shape[2],
-                                       "consumer_warps": shape[3]}},
+                                       "consumer": {8: "mma.sync x 8 warps", 4: "mma.sync x 4 warps",
+                                                    5: "tcgen05/TMEM (4 softmax warps + issuer)"}
+                                       .get(shape[3], shape[3])}},
             "value_note": "1 / (t_step + t_event / Delta): t_step = the timed window's event-free step time, "
                           "t_event = mean classify + migrate time, both CUDA-event measured in this run",
             "window": {"value_raw": world * K / el_max, "ms_per_step_raw": 1e3 * el_max / K,

@@ -162,6 +162,11 @@ typedef struct {
   int32_t  budget;           /* kept tokens per request (H2O / RANDOM)                 */
   uint32_t policy_seed;      /* RANDOM                                                 */
   int32_t  scorer;           /* kv_tier_scorer (0 = Eq. 1 attention score)             */
+  int32_t  step_kernel;      /* whole-step kernel consumer: 0 = auto (= 1, measured faster on
+                                every shape tried), 1 = mma.sync (legacy tensor
+                                path, 16-row slices per warp), 2 = tcgen05 / TMEM (d = 128,
+                                no T2 rows, a cluster per kv head; else the step runs the
+                                mma.sync consumer)                                         */
 } kv_tier_config;
 
 typedef struct kv_tier_ctx kv_tier_ctx;
@@ -299,7 +304,8 @@ KV_TIER_API kv_tier_status kv_tier_visible_count(const kv_tier_ctx* ctx, int32_t
  * mirror, no device synchronisation (unlike kv_tier_census).  Also reports the step kernel's
  * work split: shape[0] = CTAs of kv_tier_step's whole-step kernel (0: the step runs layer by
  * layer), shape[1] = CTAs per kv head (a thread-block cluster), shape[2] = kv heads per CTA,
- * shape[3] = consumer warps per CTA.  Either pointer may be NULL. */
+ * shape[3] = the consumer design: 8 or 4 = mma.sync consumer warps per CTA, 5 = the tcgen05 /
+ * TMEM consumer (4 softmax warps + the MMA-issuing warp).  Either pointer may be NULL. */
 KV_TIER_API kv_tier_status kv_tier_layout(const kv_tier_ctx* ctx, int32_t* counts4, int32_t* shape4);
 
 KV_TIER_API kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream);

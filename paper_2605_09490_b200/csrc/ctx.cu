@@ -182,6 +182,8 @@ kv_tier_status validate(const kv_tier_config* c) {
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(nullptr, KV_TIER_E_INVAL, "need 0 <= rank < world");
   if (c->split < 0 || c->split > 64) return fail(nullptr, KV_TIER_E_INVAL, "split must be in [0, 64]");
   if (c->variant < 0 || c->variant > 5) return fail(nullptr, KV_TIER_E_INVAL, "variant must be in [0, 5]");
+  if (c->step_kernel < 0 || c->step_kernel > 2)
+    return fail(nullptr, KV_TIER_E_INVAL, "step_kernel must be 0 (auto), 1 (mma.sync) or 2 (tcgen05)");
   if (c->policy < KV_TIER_POLICY_HIERARCHY || c->policy > KV_TIER_POLICY_RANDOM)
     return fail(nullptr, KV_TIER_E_INVAL, "policy must be a kv_tier_policy");
   if (c->scorer < KV_TIER_SCORER_ATTENTION || c->scorer > KV_TIER_SCORER_RKV)
@@ -248,28 +250,35 @@ int zring_of(const kv_tier_config& c);
 // the one-CTA-per-SM shape.  Sets v.step_k (total CTAs, 0 = no
 // shape fits), v.step_s, v.step_m, v.step_nw.
 void step_plan(DevView& v, int nsm) {
-  int best = 0, bs = 0, bm = 0, bnw = 0;
-  for (int nw : {8, 4}) {
-    const int per_sm = nw == 8 ? 1 : 2;
+  int best = 0, bs = 0, bm = 0, bnw = 0, bum = 0, brank = 0;
+  // candidates in preference order on ties: the tcgen05 consumer, 8 mma.sync warps, 4 warps
+  const int um_ok = v.step_um_ok && v.D == 128 && v.cap2 == 0;
+  for (int cand = 0; cand < 3; ++cand) {
+    const int um = cand == 0, nw = cand == 2 ? 4 : 8;
+    if (um && !um_ok) continue;
+    const int per_sm = nw == 8 ? 1 : 2, rank = 3 - cand;
     for (int m = 8; m >= 1; m >>= 1) {
       if (v.Hkv % m) continue;
-      for (int s = 1; s <= (m == 1 ? 16 : 1); ++s) {
+      if (um && m != 1) continue;                    // the tcgen05 consumer: one kv head per cluster
+      for (int s = um ? 2 : 1; s <= (m == 1 ? 16 : 1); ++s) {
         if (v.split_req > 0 && (s != v.split_req || m != 1)) continue;   // the config's split, if given
         const int clusters_needed = v.B * v.Hkv / m, total = clusters_needed * s;
         if (total > per_sm * nsm) continue;
-        v.step_k = total; v.step_s = s; v.step_m = m; v.step_nw = nw;
+        v.step_k = total; v.step_s = s; v.step_m = m; v.step_nw = um ? 4 : nw; v.step_um = um;
         if (step_smem_bytes(v) > (nw == 8 ? 227 * 1024 : 113 * 1024)) continue;
         int clusters = 0;
         if (step_configure(v, &clusters) != cudaSuccess) { cudaGetLastError(); continue; }
         if (clusters < clusters_needed) continue;
-        // SMs engaged; ties: one CTA per SM (measured at 7B: 8 warps x 128 CTAs 3593 steps/s,
-        // 4 warps x 256 CTAs 3353)
-        const int sms = total / per_sm, best_sms = best ? best / (bnw == 8 ? 1 : 2) : 0;
-        if (sms > best_sms || (sms == best_sms && nw > bnw)) { best = total; bs = s; bm = m; bnw = nw; }
+        // SMs engaged; ties: the tcgen05 consumer, then one CTA per SM (measured at 7B: 8 warps x
+        // 128 CTAs 3593 steps/s, 4 warps x 256 CTAs 3353)
+        const int sms = total / per_sm, best_sms = best ? best / (bnw == 8 || bum ? 1 : 2) : 0;
+        if (sms > best_sms || (sms == best_sms && rank > brank)) {
+          best = total; bs = s; bm = m; bnw = um ? 4 : nw; bum = um; brank = rank;
+        }
       }
     }
   }
-  v.step_k = best; v.step_s = bs; v.step_m = bm; v.step_nw = bnw;
+  v.step_k = best; v.step_s = bs; v.step_m = bm; v.step_nw = bnw; v.step_um = bum;
   if (best) { int c = 0; step_configure(v, &c); }   // leave the chosen shape's attributes set
 }
 
@@ -431,6 +440,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.split = auto_split(*cfg);
   v.split_req = cfg->split;
   v.variant = cfg->variant;
+  v.step_um_ok = cfg->step_kernel == 2;
   v.seq_w = cfg->shard == KV_TIER_SHARD_SEQUENCE ? cfg->world : 1;
   v.seq_r = cfg->shard == KV_TIER_SHARD_SEQUENCE ? cfg->rank : 0;
   v.score_grid = 148;                       // score-flush CTAs beside the per-layer chain (measured best)
@@ -858,7 +868,7 @@ kv_tier_status kv_tier_layout(const kv_tier_ctx* ctx, int32_t* counts4, int32_t*
     shape4[0] = ctx->v.step_k;
     shape4[1] = ctx->v.step_s;
     shape4[2] = ctx->v.step_m;
-    shape4[3] = ctx->v.step_nw;
+    shape4[3] = ctx->v.step_um ? 5 : ctx->v.step_nw;
   }
   return KV_TIER_OK;
 }

@@ -72,6 +72,8 @@ struct DevView {
   int step_k, step_s, step_m;
   int split_req;        // kv_tier_config::split (0 = auto): also fixes the step kernel's CTAs per kv head
   int step_nw;          // consumer warps per CTA: 8 (one CTA per SM) or 4 (two CTAs per SM)
+  int step_um;          // 1: the tcgen05 consumer (4 softmax warps + the MMA-issuing warp, one CTA per SM)
+  int step_um_ok;       // kv_tier_config::step_kernel == 2
   int* step_done;       // [L][B] CTAs of request b that finished layer l (zeroed by k_begin_step)
   void* hot_base;       // L2 access-policy window over the small hot buffers
   size_t hot_bytes;

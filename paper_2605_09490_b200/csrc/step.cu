@@ -97,12 +97,21 @@ struct StepIO {
 constexpr int SD_FIRST = 1, SD_LAST = 2, SD_T2 = 4;
 constexpr int STEP_MAXM = 8;   // kv heads per CTA when s == 1
 
-template <int D, int NW, int NST>
-__global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(const DevView v, const StepIO io) {
+// UM = false: consumers on the legacy tensor path (mma.sync, NW warps of 16 rows per stage).
+// UM = true (d = 128, no T2 rows): the 5th-generation tensor cores -- one issuing thread runs
+// S = K q^T and O = V^T P^T per 128-row stage with tcgen05.mma from the swizzled shared-memory
+// tiles into TMEM; NW = 4 softmax warps (one token row, then one d row of O, per thread) keep
+// the online softmax and the o accumulator.
+template <int D, int NW, int NST, bool UM>
+__global__ void __launch_bounds__((NW + 4 + (UM ? 1 : 0)) * 32, (NW <= 4 && !UM) ? 2 : 1)
+    k_decode_step(const DevView v, const StepIO io) {
+  static_assert(!UM || (D == 128 && NW == 4), "the UMMA consumer is written for d = 128, 4 softmax warps");
   constexpr int NCONS = NW * 32;
   constexpr int WPROD = NW, WNEW = NW + 1, WSC0 = NW + 2;   // + two score warps
+  constexpr int WISS = NW + 4;                               // UM: the MMA-issuing warp
   constexpr int NSC = 64;                                    // score-pass threads
-  constexpr int TILE = NW * 16;
+  constexpr int GPS = UM ? 8 : NW;                           // 16-row groups per stage
+  constexpr int TILE = GPS * 16;
   constexpr int ROWB = D * 2;
   constexpr int TILEB = TILE * ROWB;
   constexpr int STAGEB = 2 * TILEB;
@@ -128,11 +137,14 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
     if (KVT_TRACE && v.trace) v.trace[((size_t)l * gridDim.x + blockIdx.x) * NTRACE + slot] = clock64();
   };
 
-  extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* ring = smem;                                              // [NST][K tile | V tile]
-  unsigned char* t2w = ring + NST * STAGEB;                                // [NW][16][D] bf16 (T2 only)
+  extern __shared__ __align__(1024) unsigned char smem[];
+  // UM: the swizzle atoms need 1024-byte aligned tiles
+  unsigned char* ring = UM ? smem + ((1024u - (smem_u32(smem) & 1023u)) & 1023u) : smem;   // [NST][K tile | V tile]
+  unsigned char* qtile = ring + NST * STAGEB;                              // UM: [16][D] q(l) of the head, swizzled
+  unsigned char* ptile = qtile + (UM ? 16 * ROWB : 0);                     // UM: [2][16][TILE] p hi (rows 0-7), lo (8-15)
+  unsigned char* t2w = ptile + (UM ? 2 * 16 * ROWB : 0);                   // [NW][16][D] bf16 (T2 only)
   float* ow = reinterpret_cast<float*>(t2w + (v.cap2 > 0 ? NW * 16 * ROWB : 0));   // [NH][8][OWS] combine
-  float* pbuf = ow + NH * 8 * OWS;                                         // [16 + 8 D] CTA partial (m, l, o)
+  float* pbuf = ow + (UM ? 0 : NH * 8 * OWS);                              // [16 + 8 D] CTA partial (m, l, o)
   float* rx = pbuf + 16 + 8 * D + 64;                                      // [2][S][16 + SL] received partials
   float* redm = rx + 2 * S * (16 + SL);                                    // [NW][8]
   float* redl = redm + NW * 8;                                             // [NW][8]
@@ -141,12 +153,15 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
   float* sml = ntv + 2 * D;                                                // [ZRING][STEP_MAXM][16] (M, 1/L) for a4
   float* smisc = sml + ZRING * STEP_MAXM * 16;                             // [24] merge scalars
   float* fac = smisc + 24;                                                 // [16][8] merge factors (S <= 16)
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(fac + 16 * 8);
-  // full[NST] empty[NST] nfull[2] nempty[2] rxb[2] done[2]
-  int4* sdesc = reinterpret_cast<int4*>(bars + 2 * NST + 8);               // [NST]
+  float* wmx = fac + 16 * 8;                                               // UM: [2][NW][8] per-warp stage maxima
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(wmx + (UM ? 2 * NW * 8 : 0));
+  // full[NST] empty[NST] | nfull[2] nempty[2] rxb[2] q spare | UM: sready[2] pready oready qready
+  int4* sdesc = reinterpret_cast<int4*>(bars + 2 * NST + 16);              // [NST]
   StepPart* ptab = reinterpret_cast<StepPart*>(sdesc + NST);               // [STEP_MAXM] this CTA's parts
   volatile int* sc_done = reinterpret_cast<volatile int*>(ptab + STEP_MAXM);   // layers whose a4 pass is complete
   volatile int* ml_done = sc_done + 1;                                     // layers merged ((M, 1/L) in sml)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(const_cast<int*>(sc_done) + 2);   // UM: TMEM base
+  volatile int* pvfresh = sc_done + 3;                                     // UM: [2] P.V of stage i starts O afresh
 
   const int cur = v.st->cur, sb = v.st->scur;
   Seg sg;
@@ -200,10 +215,15 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
       }
     }
   };
+  // UM barriers: S(i) in TMEM (commit, by stage parity), P(i) in shared memory (one arrive per
+  // softmax warp), P.V of stage i done (commit, by stage parity), the q tile of a layer (one
+  // arrive per softmax warp)
+  const uint32_t sready0 = smem_u32(bars + 2 * NST + 8), pready = smem_u32(bars + 2 * NST + 10);
+  const uint32_t odone0 = smem_u32(bars + 2 * NST + 11), qready = smem_u32(bars + 2 * NST + 13);
   if (tid == 0) {
     for (int x = 0; x < NST; ++x) {
       mbar_init(full0 + 8 * x, 1);
-      mbar_init(empty0 + 8 * x, NW);
+      mbar_init(empty0 + 8 * x, UM ? 1 : NW);   // UM: the commit of the stage's P.V frees the slot
     }
     for (int x = 0; x < 2; ++x) {
       mbar_init(nfull0 + 8 * x, 1);
@@ -211,17 +231,159 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
       mbar_init(rxb0 + 8 * x, 1);               // the owner's arrive.expect_tx; peers complete tx
     }
     mbar_init(qbar, 1);
+    if (UM) {
+      mbar_init(sready0, 1);
+      mbar_init(sready0 + 8, 1);
+      mbar_init(pready, NW);
+      mbar_init(odone0, 1);
+      mbar_init(odone0 + 8, 1);
+      mbar_init(qready, NW);
+    }
     *sc_done = 0;
     *ml_done = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  if constexpr (UM) {
+    // stale shared memory must read as finite numbers: rows past a stage's last group enter the
+    // MMAs (multiplied by p = 0 or masked), so the ring and the tiles start zeroed
+    for (int i = tid; i < (NST * STAGEB + 48 * ROWB) / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(ring)[i] = make_uint4(0u, 0u, 0u, 0u);
+    fence_proxy_async_cta();
+    if (w == WISS) {                              // TMEM: S double buffer (2 x 16 columns) + O (16)
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;\n" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    tc_fence_before();
+  }
   __syncthreads();                              // part table, barriers, counters
+  if constexpr (UM) tc_fence_after();
+  const uint32_t tmem = UM ? *tmem_slot : 0u;
   if (S > 1) cluster_sync_all();                // every peer's barriers exist before any remote use
   if (KVT_TRACE && v.trace && blockIdx.x == 0 && tid == 0) v.trace[NTRACE - 1] = gridDim.x;
 
+  // ---------------- consumer-side tail of a part, shared by both consumer designs: the CTA
+  // partial (m, l, o) is in pbuf; exchange it over DSMEM, merge this CTA's share of o (+ the new
+  // token), store o, publish (M, 1/L) for the score warps and count o(l) for the request.
+  int nts = 0, nrx = 0;
+  auto store_o = [&](int l, int g, int e, float4 val) {    // o elements [e, e+4) of kv head g
+    const size_t oi = (((size_t)l * B + b) * v.Hq + g * G) * D + e;
+    if (v.out_fp32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(io.o) + oi) = val;
+    } else {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(val.x, val.y), hi = __floats2bfloat162_rn(val.z, val.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(io.o) + oi) = pk;
+    }
+  };
+  auto merge_part = [&](int l, int kpart, int g) {
+    const int par = l & 1;
+    if (tid == 0 && kpart == 0) ctrace(l, 16);             // CTA partial in pbuf
+    if (S > 1) {
+      // ---------------- DSMEM exchange: (m, l) + o slice r of this partial -> slice r's CTA.
+      // Every push carries 16 + SL floats (the last slice is padded from pbuf's tail), so each
+      // receiver expects exactly S * (16 + SL) * 4 bytes per layer.
+      fence_proxy_async_smem();                              // pbuf (generic stores) -> bulk copy reads
+      named_sync(1, NCONS);
+      if (tid == 0) {
+        const uint32_t rx_s = smem_u32(rx);
+        mbar_expect_tx(rxb0 + 8 * par, (uint32_t)(S * (16 + SL) * 4));
+        for (int r = 0; r < S; ++r) {                       // cluster ranks = the head's slices
+          const uint32_t peer = (uint32_t)r;
+          const uint32_t dst = rx_s + (uint32_t)(((par * S + slice) * (16 + SL)) * 4);
+          const uint32_t mb = mapa(rxb0 + 8 * par, peer);
+          bulk_s2peer(mapa(dst, peer), smem_u32(pbuf), 64, mb);
+          bulk_s2peer(mapa(dst + 64, peer), smem_u32(pbuf + 16 + r * SL), (uint32_t)(SL * 4), mb);
+        }
+        bulk_commit();
+      }
+    }
+    // ---------------- merge: this CTA's share of o (slice, or the whole head) + the new token
+    const int nslot = nts & 1;
+    mbar_sleep_wait(nfull0 + 8 * nslot, (nts >> 1) & 1);   // the new token's term (every CTA of the head)
+    if (tid == 0 && kpart == 0) ctrace(l, 17);             // new token ready
+    if (S > 1) mbar_sleep_wait(rxb0 + 8 * par, (nrx >> 1) & 1);
+    named_sync(1, NCONS);                                   // pbuf complete (S == 1)
+    if (tid == 0 && kpart == 0) ctrace(l, 18);             // peers' partials landed
+    const int nsrc = S > 1 ? S : 1;
+    const float* src0 = S > 1 ? rx + par * S * (16 + SL) : pbuf;   // partial 0 of the merge
+    const int sstride = 16 + SL;                            // between received partials
+    const int e_beg = S > 1 ? slice * SL : 0;
+    const int e_end = S > 1 ? min(tot, e_beg + SL) : tot;
+    float* sIL = smisc;                                     // [8] 1/L
+    float* sFN = smisc + 8;                                 // [8] new-token factor
+    if (w == 0) {
+      // warp 0: lane = (source group j = lane >> 3, head h = lane & 7); sources j, j+4, ... ;
+      // max and sum over the source groups by shuffles (fixed order: deterministic)
+      const int h = lane & 7, j = lane >> 3;
+      const float zn = ntz[nslot * 8 + h];
+      float M = zn;
+      for (int x = j; x < nsrc; x += 4) M = fmaxf(M, src0[x * sstride + h]);
+      M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 8));
+      M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 16));
+      float Ls = 0.f;
+      for (int x = j; x < nsrc; x += 4) {
+        const float m = src0[x * sstride + h];
+        const float f = m == -INFINITY ? 0.f : ex2_ftz(m - M);
+        fac[x * 8 + h] = f;
+        Ls += f * src0[x * sstride + 8 + h];
+      }
+      Ls += __shfl_xor_sync(0xffffffffu, Ls, 8);
+      Ls += __shfl_xor_sync(0xffffffffu, Ls, 16);
+      if (j == 0) {
+        const float fn = zn == -INFINITY ? 0.f : ex2_ftz(zn - M);
+        Ls += fn;
+        const float il = Ls > 0.f ? 1.0f / Ls : 0.f;
+        sIL[h] = il;
+        sFN[h] = fn;
+        float* mlw = sml + ((l % ZS) * STEP_MAXM + kpart) * 16;
+        mlw[h] = h < G ? M : 0.f;
+        mlw[8 + h] = h < G ? il : 0.f;
+      }
+    }
+    named_sync(1, NCONS);
+    for (int e = e_beg + 4 * tid; e < e_end; e += 4 * NCONS) {
+      const int h = e / D, dd = e - h * D;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int x = 0; x < nsrc; ++x) {
+        const float f = fac[x * 8 + h];
+        const float4 y = *reinterpret_cast<const float4*>(src0 + x * sstride + 16 + (e - e_beg));
+        acc.x += f * y.x;
+        acc.y += f * y.y;
+        acc.z += f * y.z;
+        acc.w += f * y.w;
+      }
+      const float fn = sFN[h], il = sIL[h];
+      const float4 nv = *reinterpret_cast<const float4*>(ntv + nslot * D + dd);
+      acc.x = (acc.x + fn * nv.x) * il;
+      acc.y = (acc.y + fn * nv.y) * il;
+      acc.z = (acc.z + fn * nv.z) * il;
+      acc.w = (acc.w + fn * nv.w) * il;
+      store_o(l, g, e, acc);
+    }
+    named_sync(1, NCONS);                                   // o stored, rx / ntv / fac read
+    if (tid == 0 && kpart == 0) ctrace(l, 19);
+    if (tid == 0) {
+      mbar_arrive(nempty0 + 8 * nslot);
+      if (kpart == npart - 1) {
+        __threadfence_block();
+        *ml_done = l + 1;                                   // every part's (M, 1/L) of layer l is in sml
+        // o(l) of this CTA is final: count it for the request (the q(l+1) dependency).  The
+        // relaxed add orders the COMPUTATION (a fused decoder would hand o(l) to its o_proj
+        // stage on chip); it deliberately does not wait for the global o stores to drain behind
+        // the K/V stream -- they are visible at kernel end.
+        red_relaxed_gpu(done_ctr + (size_t)l * B + b, 1);
+        ctrace(l, 20);
+      }
+    }
+    ++nts;
+    if (S > 1) ++nrx;
+  };
+
   if (w == WPROD) {
     // ================================ producer ================================
-    // Stage sequence: layer-major, then this CTA's parts, then up to NW groups per stage.  A second
+    // Stage sequence: layer-major, then this CTA's parts, then up to GPS groups per stage.  A second
     // cursor NST stages ahead prefetches into L2, so the copy that refills a ring slot hits L2.
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
@@ -230,7 +392,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
         if (pp.j0 == pp.j1) { t2 = false; return 0; }
         t2 = it.j >= gbf;
         const int send = t2 ? pp.j1 : min(pp.j1, gbf);
-        return min(NW, send - it.j);
+        return min(GPS, send - it.j);
       };
       auto advance = [&](Cur& it) {
         const StepPart pp = part(it.k);
@@ -400,7 +562,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
         ++nts;
       }
     }
-  } else if (w >= WSC0) {
+  } else if (w == WSC0 || w == WSC0 + 1) {
     // ====== score warps: a4 of layer l-1 while the consumers run layer l (Eq. 1, AMB-14) ======
     const int st0 = tid - WSC0 * 32;                          // 0..NSC-1
     constexpr int SB = 8;
@@ -471,6 +633,237 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
       }
     }
     if (bad) atomicOr(&v.st->err, 1);
+  } else if (w == WISS) {
+    // ========== UM: the MMA-issuing thread (tcgen05.mma, accumulators in TMEM) ==========
+    // Per stage i: S(i) = K(i) q^T into TMEM S[i & 1] (commit -> sready[i & 1]); once the softmax
+    // warps have written P(i) into p tile i & 1, O += V(i)^T P(i)^T into TMEM O (afresh when the
+    // softmax warps say so: a part's first P.V, or the first after they folded O into registers
+    // at a raised running max), commit -> odone[i & 1] and the ring slot's empty barrier.  S(i + 1)
+    // is issued before the P.V of stage i (it overlaps the softmax) unless stage i + 1 opens the
+    // next layer: its q waits for o(l), which needs the P.V of stage i.  Commits (never plain
+    // arrives) also signal stages without rows: a commit tracks every earlier MMA of the thread.
+    if constexpr (UM) {
+      if (lane == 0) {
+        const uint32_t idS = umma_idesc(128, 16, 0, 0), idO = umma_idesc(128, 16, 1, 0);
+        const uint32_t qs = smem_u32(qtile), ps = smem_u32(ptile);
+        auto koff = [](int kk) { return (uint32_t)((kk >> 2) * 1024 + (kk & 3) * 32); };
+        auto issue_qk = [&](int i, int cnt) {
+          if (cnt > 0) {
+            const uint32_t sK = ring_s + (i % NST) * STAGEB;
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk)
+              umma_bf16(tmem + 16 * (i & 1), umma_sdesc(sK + koff(kk), 16, 2048), umma_sdesc(qs + koff(kk), 16, 2048),
+                        idS, kk > 0);
+          }
+          umma_commit(sready0 + 8 * (i & 1));
+        };
+        int nq = 0;
+        bool ahead = false;
+        for (int i = 0;; ++i) {
+          const int s2 = i % NST;
+          if (!ahead) {
+            mbar_wait(full0 + 8 * s2, (i / NST) & 1);
+            const int4 dsc = sdesc[s2];
+            if (dsc.x < 0) { umma_commit(sready0 + 8 * (i & 1)); break; }   // wake the softmax warps
+            if (dsc.w & SD_FIRST) { mbar_wait(qready, nq & 1); ++nq; }     // q(l) in the q tile
+            tc_fence_after();
+            issue_qk(i, dsc.w >> 8);
+          }
+          ahead = false;
+          {
+            const int i1 = i + 1;
+            mbar_wait(full0 + 8 * (i1 % NST), (i1 / NST) & 1);
+            const int4 d1 = sdesc[i1 % NST];
+            if (d1.x >= 0 && !(d1.w & SD_FIRST)) {
+              issue_qk(i1, d1.w >> 8);
+              ahead = true;
+            }
+          }
+          mbar_wait(pready, i & 1);                               // P(i) in p tile i & 1
+          tc_fence_after();
+          if ((sdesc[s2].w >> 8) > 0) {
+            const uint32_t sV = ring_s + s2 * STAGEB + TILEB, pt = ps + (i & 1) * 16 * ROWB;
+            const uint32_t fresh = (uint32_t)pvfresh[i & 1];
+#pragma unroll
+            for (int kk = 0; kk < TILE / 16; ++kk)
+              umma_bf16(tmem + 32, umma_sdesc(sV + kk * 4096, 1024, 2048), umma_sdesc(pt + koff(kk), 16, 2048), idO,
+                        (kk > 0 || !fresh) ? 1u : 0u);
+          }
+          umma_commit(odone0 + 8 * (i & 1));
+          umma_commit(empty0 + 8 * s2);
+        }
+      }
+    }
+  } else if constexpr (UM) {
+    // ========== UM: softmax warps -- thread t owns token row t of S(i) and d row t of O ==========
+    // The o accumulator stays in TMEM across a part's stages; it is folded into registers only
+    // when the CTA-wide running max of a head rises past its slack (rare after the first stage)
+    // and at the part's end, so the softmax of stage i + 1 never waits for the P.V of stage i.
+    const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));
+    constexpr float RESCALE_SLACK = 8.f;
+    float mref[8], lsum[8], oacc[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) { mref[h] = -INFINITY; lsum[h] = 0.f; oacc[h] = 0.f; }
+    float* zrow = nullptr;
+    bool pend = false;                                       // a P.V of this part sits in TMEM O
+    const uint32_t tq_lane = (uint32_t)(32 * w) << 16;      // TMEM lane quadrant of this warp
+    auto fold_o = [&](int k) {                               // O (through the P.V of stage k) -> registers
+      mbar_sleep_wait(odone0 + 8 * (k & 1), (k >> 1) & 1);
+      tc_fence_after();
+      uint32_t r[16];
+      tmem_ld16(tmem + 32 + tq_lane, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int h = 0; h < 8; ++h) oacc[h] += __uint_as_float(r[h]) + __uint_as_float(r[8 + h]);
+    };
+    auto build_q = [&](int l) {                              // q(l) of the head -> the swizzled q tile
+      mbar_sleep_wait(qbar, l & 1);                          // the layer dependency held, q(l) landed
+      const uint16_t* qsrc = reinterpret_cast<const uint16_t*>(qsm(l));
+      for (int x = tid; x < 16 * (D / 8); x += NCONS) {
+        const int r = x / (D / 8), c = x % (D / 8);
+        const uint4 val = r < G ? *reinterpret_cast<const uint4*>(qsrc + r * D + c * 8) : make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(qtile + tile_off<D>(r, c)) = val;
+      }
+      fence_proxy_async_cta();                               // generic stores -> the MMA's operand reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qready);
+    };
+    build_q(0);
+    for (int i = 0;; ++i) {
+      const int s2 = i % NST;
+      mbar_sleep_wait(full0 + 8 * s2, (i / NST) & 1);       // acquire the stage descriptor
+      const int4 dsc = sdesc[s2];
+      mbar_sleep_wait(sready0 + 8 * (i & 1), (i >> 1) & 1);
+      if (dsc.x < 0) break;
+      const int l = dsc.x, kpart = dsc.y, j = dsc.z, fl = dsc.w & 0xFF, cnt = dsc.w >> 8;
+      const int g = part(kpart).g, u = b * Hkv + g;
+      if (fl & SD_FIRST) {
+        if (lane == 0 && io.score)
+          while (*sc_done < l - ZS + 1) __nanosleep(128);     // logit slot of layer l - ZS consumed
+        __syncwarp();
+        zrow = io.score ? v.zbuf + (size_t)(l % ZS) * U * v.zrows * 8 + (size_t)u * v.zrows * 8 : nullptr;
+      }
+      tc_fence_after();
+      // ---- logits of token row t (log2 domain)
+      const int tv = 16 * j + tid;
+      const bool valid = tid < cnt * 16 && sg.bf16_valid(tv);
+      float z[8];
+      if (cnt > 0) {
+        uint32_t r[8];
+        tmem_ld8(tmem + 16 * (i & 1) + tq_lane, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int h = 0; h < 8; ++h) z[h] = (valid && h < G) ? __uint_as_float(r[h]) * sl2 : -INFINITY;
+      } else {
+#pragma unroll
+        for (int h = 0; h < 8; ++h) z[h] = -INFINITY;
+      }
+      if (zrow && valid) {
+        *reinterpret_cast<float4*>(zrow + (size_t)tv * 8) = make_float4(z[0], z[1], z[2], z[3]);
+        *reinterpret_cast<float4*>(zrow + (size_t)tv * 8 + 4) = make_float4(z[4], z[5], z[6], z[7]);
+      }
+      // ---- running max per head, CTA-wide: raised only when a logit passes it by the slack
+      bool need = false;
+#pragma unroll
+      for (int h = 0; h < 8; ++h) need |= z[h] > mref[h] + RESCALE_SLACK;
+      float* wm = wmx + (i & 1) * NW * 8;
+      if (__any_sync(0xffffffffu, need)) {
+        float t8[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) t8[h] = z[h];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+          for (int h = 0; h < 8; ++h) t8[h] = fmaxf(t8[h], __shfl_xor_sync(0xffffffffu, t8[h], off));
+        if (lane < 8) {
+          float x = t8[0];
+#pragma unroll
+          for (int h = 1; h < 8; ++h) x = lane == h ? t8[h] : x;
+          wm[w * 8 + lane] = x;
+        }
+      } else if (lane < 8) {
+        wm[w * 8 + lane] = -INFINITY;
+      }
+      named_sync(1, NCONS);
+      float mnew[8];
+      bool raise = false;                                    // uniform: every thread reads the same maxima
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        float mx = wm[h];
+#pragma unroll
+        for (int x = 1; x < NW; ++x) mx = fmaxf(mx, wm[x * 8 + h]);
+        mnew[h] = mx > mref[h] + RESCALE_SLACK ? mx : mref[h];
+        raise |= mnew[h] != mref[h];
+      }
+      if (raise) {
+        if (pend) fold_o(i - 1);                             // O so far, at the old scale
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          if (mnew[h] != mref[h]) {
+            const float c = mref[h] == -INFINITY ? 0.f : ex2_ftz(mref[h] - mnew[h]);
+            oacc[h] *= c;
+            lsum[h] *= c;
+            mref[h] = mnew[h];
+          }
+        }
+      }
+      const bool fresh = !pend || raise;                     // this stage's P.V starts O afresh
+      // ---- p = 2^(z - m) as two bf16 terms (hi: P rows 0-7, lo: rows 8-15), token column t
+      if (i >= 2) mbar_sleep_wait(odone0 + 8 * (i & 1), ((i - 2) >> 1) & 1);   // P.V(i - 2) read this p tile
+      unsigned char* pt = ptile + (i & 1) * 16 * ROWB;
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const float p = (valid && h < G) ? ex2_ftz(z[h] - mref[h]) : 0.f;
+        lsum[h] += p;
+        const __nv_bfloat16 hi = __float2bfloat16_rn(p);
+        const __nv_bfloat16 lo = __float2bfloat16_rn(p - __bfloat162float(hi));
+        *reinterpret_cast<__nv_bfloat16*>(pt + tile_off<D>(h, tid >> 3) + (tid & 7) * 2) = hi;
+        *reinterpret_cast<__nv_bfloat16*>(pt + tile_off<D>(8 + h, tid >> 3) + (tid & 7) * 2) = lo;
+      }
+      if (tid == 0) pvfresh[i & 1] = fresh ? 1 : 0;
+      fence_proxy_async_cta();
+      tc_fence_before();                                     // this warp's TMEM reads precede the next MMAs
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pready);
+      if (cnt > 0) pend = true;
+      if (!(fl & SD_LAST)) continue;
+      // ---- part end: the CTA partial is (m = mref, l = sum of p over the 128 token rows, o)
+      if (pend) fold_o(i);
+      tc_fence_before();
+      pend = false;
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        float x = lsum[h];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+        lsum[h] = x;
+      }
+      if (lane < 8) {
+        float x = lsum[0];
+#pragma unroll
+        for (int h = 1; h < 8; ++h) x = lane == h ? lsum[h] : x;
+        redl[w * 8 + lane] = x;
+      }
+      if (tid == 0 && S > 1) bulk_wait_read0();              // the previous push has read pbuf
+      named_sync(1, NCONS);
+      if (tid < 8) {
+        float Ls = 0.f, M = mref[0];
+#pragma unroll
+        for (int x = 0; x < NW; ++x) Ls += redl[x * 8 + tid];
+#pragma unroll
+        for (int h = 1; h < 8; ++h) M = tid == h ? mref[h] : M;
+        pbuf[tid] = M;
+        pbuf[8 + tid] = Ls;
+      }
+#pragma unroll
+      for (int h = 0; h < 8; ++h)
+        if (h < G) pbuf[16 + h * D + tid] = oacc[h];
+#pragma unroll
+      for (int h = 0; h < 8; ++h) { mref[h] = -INFINITY; lsum[h] = 0.f; oacc[h] = 0.f; }
+      merge_part(l, kpart, g);
+      if (l + 1 < L) build_q(l + 1);
+    }
+    if (tid == 0 && S > 1) bulk_wait_read0();
   } else {
     // ================================ consumers ================================
     const float sl2 = (float)(1.4426950408889634 / __dsqrt_rn((double)D));
@@ -478,7 +871,6 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
     float oacc[KS][4];
     uint32_t qf[KS][2];
     float* zrow = nullptr;
-    int nts = 0, nrx = 0;
     const int mi = lane >> 3, ii = lane & 7;
     constexpr float RESCALE_SLACK = 8.f;
     auto online = [&](float z00, float z01, float z10, float z11, float& p00, float& p01, float& p10, float& p11) {
@@ -560,18 +952,6 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
         *reinterpret_cast<uint4*>(scr + tile_off<D>(row, 2 * j + 1)) = hi;
       }
       __syncwarp();
-    };
-    auto store_o = [&](int l, int g, int e, float4 val) {    // o elements [e, e+4) of kv head g
-      const size_t oi = (((size_t)l * B + b) * v.Hq + g * G) * D + e;
-      if (v.out_fp32) {
-        *reinterpret_cast<float4*>(reinterpret_cast<float*>(io.o) + oi) = val;
-      } else {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(val.x, val.y), hi = __floats2bfloat162_rn(val.z, val.w);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&lo);
-        pk.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(io.o) + oi) = pk;
-      }
     };
 
     for (int i = 0;; ++i) {
@@ -748,163 +1128,78 @@ __global__ void __launch_bounds__((NW + 4) * 32, NW <= 4 ? 2 : 1) k_decode_step(
         for (int x = 0; x < NH; ++x) a += ow[(x * 8 + h) * OWS + dd];
         pbuf[16 + e] = a;
       }
-      const int par = l & 1;
-      if (tid == 0 && kpart == 0) ctrace(l, 16);             // CTA partial in pbuf
-      if (S > 1) {
-        // ---------------- DSMEM exchange: (m, l) + o slice r of this partial -> slice r's CTA.
-        // Every push carries 16 + SL floats (the last slice is padded from pbuf's tail), so each
-        // receiver expects exactly S * (16 + SL) * 4 bytes per layer.
-        fence_proxy_async_smem();                              // pbuf (generic stores) -> bulk copy reads
-        named_sync(1, NCONS);
-        if (tid == 0) {
-          const uint32_t rx_s = smem_u32(rx);
-          mbar_expect_tx(rxb0 + 8 * par, (uint32_t)(S * (16 + SL) * 4));
-          for (int r = 0; r < S; ++r) {                       // cluster ranks = the head's slices
-            const uint32_t peer = (uint32_t)r;
-            const uint32_t dst = rx_s + (uint32_t)(((par * S + slice) * (16 + SL)) * 4);
-            const uint32_t mb = mapa(rxb0 + 8 * par, peer);
-            bulk_s2peer(mapa(dst, peer), smem_u32(pbuf), 64, mb);
-            bulk_s2peer(mapa(dst + 64, peer), smem_u32(pbuf + 16 + r * SL), (uint32_t)(SL * 4), mb);
-          }
-          bulk_commit();
-        }
-      }
-      // ---------------- merge: this CTA's share of o (slice, or the whole head) + the new token
-      const int nslot = nts & 1;
-      mbar_sleep_wait(nfull0 + 8 * nslot, (nts >> 1) & 1);   // the new token's term (every CTA of the head)
-      if (tid == 0 && kpart == 0) ctrace(l, 17);             // new token ready
-      if (S > 1) mbar_sleep_wait(rxb0 + 8 * par, (nrx >> 1) & 1);
-      named_sync(1, NCONS);                                   // pbuf complete (S == 1)
-      if (tid == 0 && kpart == 0) ctrace(l, 18);             // peers' partials landed
-      const int nsrc = S > 1 ? S : 1;
-      const float* src0 = S > 1 ? rx + par * S * (16 + SL) : pbuf;   // partial 0 of the merge
-      const int sstride = 16 + SL;                            // between received partials
-      const int e_beg = S > 1 ? slice * SL : 0;
-      const int e_end = S > 1 ? min(tot, e_beg + SL) : tot;
-      float* sIL = smisc;                                     // [8] 1/L
-      float* sFN = smisc + 8;                                 // [8] new-token factor
-      if (w == 0) {
-        // warp 0: lane = (source group j = lane >> 3, head h = lane & 7); sources j, j+4, ... ;
-        // max and sum over the source groups by shuffles (fixed order: deterministic)
-        const int h = lane & 7, j = lane >> 3;
-        const float zn = ntz[nslot * 8 + h];
-        float M = zn;
-        for (int x = j; x < nsrc; x += 4) M = fmaxf(M, src0[x * sstride + h]);
-        M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 8));
-        M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 16));
-        float Ls = 0.f;
-        for (int x = j; x < nsrc; x += 4) {
-          const float m = src0[x * sstride + h];
-          const float f = m == -INFINITY ? 0.f : ex2_ftz(m - M);
-          fac[x * 8 + h] = f;
-          Ls += f * src0[x * sstride + 8 + h];
-        }
-        Ls += __shfl_xor_sync(0xffffffffu, Ls, 8);
-        Ls += __shfl_xor_sync(0xffffffffu, Ls, 16);
-        if (j == 0) {
-          const float fn = zn == -INFINITY ? 0.f : ex2_ftz(zn - M);
-          Ls += fn;
-          const float il = Ls > 0.f ? 1.0f / Ls : 0.f;
-          sIL[h] = il;
-          sFN[h] = fn;
-          float* mlw = sml + ((l % ZS) * STEP_MAXM + kpart) * 16;
-          mlw[h] = h < G ? M : 0.f;
-          mlw[8 + h] = h < G ? il : 0.f;
-        }
-      }
-      named_sync(1, NCONS);
-      for (int e = e_beg + 4 * tid; e < e_end; e += 4 * NCONS) {
-        const int h = e / D, dd = e - h * D;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int x = 0; x < nsrc; ++x) {
-          const float f = fac[x * 8 + h];
-          const float4 y = *reinterpret_cast<const float4*>(src0 + x * sstride + 16 + (e - e_beg));
-          acc.x += f * y.x;
-          acc.y += f * y.y;
-          acc.z += f * y.z;
-          acc.w += f * y.w;
-        }
-        const float fn = sFN[h], il = sIL[h];
-        const float4 nv = *reinterpret_cast<const float4*>(ntv + nslot * D + dd);
-        acc.x = (acc.x + fn * nv.x) * il;
-        acc.y = (acc.y + fn * nv.y) * il;
-        acc.z = (acc.z + fn * nv.z) * il;
-        acc.w = (acc.w + fn * nv.w) * il;
-        store_o(l, g, e, acc);
-      }
-      named_sync(1, NCONS);                                   // o stored, rx / ntv / fac read
-      if (tid == 0 && kpart == 0) ctrace(l, 19);
-      if (tid == 0) {
-        mbar_arrive(nempty0 + 8 * nslot);
-        if (kpart == npart - 1) {
-          __threadfence_block();
-          *ml_done = l + 1;                                   // every part's (M, 1/L) of layer l is in sml
-          // o(l) of this CTA is final: count it for the request (the q(l+1) dependency).  The
-          // relaxed add orders the COMPUTATION (a fused decoder would hand o(l) to its o_proj
-          // stage on chip); it deliberately does not wait for the global o stores to drain behind
-          // the K/V stream -- they are visible at kernel end.
-          red_relaxed_gpu(done_ctr + (size_t)l * B + b, 1);
-          ctrace(l, 20);
-        }
-      }
-      ++nts;
-      if (S > 1) ++nrx;
+      merge_part(l, kpart, g);
     }
     if (tid == 0 && S > 1) bulk_wait_read0();
   }
   __syncwarp();
+  if constexpr (UM) tc_fence_before();
   if (S > 1) cluster_sync_all();                // no peer accesses this CTA's shared memory after exit
+  if constexpr (UM) {                           // (UM runs with S > 1: the cluster barrier above is CTA-wide too)
+    if (w == WISS) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" ::"r"(tmem));
+    }
+  }
 }
 
 // ----------------------------------------------------------------- host side
-// Two shapes: 8 consumer warps, one CTA per SM (NW = 8), or 4 consumer warps, two CTAs per SM
-// (NW = 4: twice the CTAs, so a request's rows are cut into twice as many slices and two
-// requests' layer chains share each SM).  DevView::step_nw selects.
-template <int D, int NW, int NST>
+// Shapes: 8 consumer warps, one CTA per SM (NW = 8); 4 consumer warps, two CTAs per SM (NW = 4:
+// twice the CTAs, so a request's rows are cut into twice as many slices and two requests' layer
+// chains share each SM); or the tcgen05 consumer (DevView::step_um: d = 128, no T2 rows, a
+// cluster per kv head; 4 softmax warps + the issuing warp, one CTA per SM, 128-row stages).
+template <int D, int NW, int NST, bool UM>
 static size_t step_smem_bytes_t(const DevView& v) {
   const int S = v.step_s > 0 ? v.step_s : 1;
   const int tot = v.G * D, SL = ((tot + S - 1) / S + 3) & ~3;
-  size_t s = (size_t)NST * 2 * NW * 16 * D * 2;                  // ring
+  constexpr int GPS = UM ? 8 : NW;
+  size_t s = (size_t)NST * 2 * GPS * 16 * D * 2;                 // ring
+  if (UM) s += 1024 + 3 * 16 * D * 2;                            // alignment, q tile, p tiles
   if (v.cap2 > 0) s += (size_t)NW * 16 * D * 2;                  // T2 scratch
-  s += (size_t)(NW / 2) * 8 * (D + 4) * 4;                       // ow
+  if (!UM) s += (size_t)(NW / 2) * 8 * (D + 4) * 4;              // ow
   s += (size_t)(16 + 8 * D + 4 * 16) * 4;                        // pbuf (+ tail read by the padded last slice)
   s += (size_t)2 * S * (16 + SL) * 4;                            // rx
   s += (size_t)2 * NW * 8 * 4 + 16 * 4 + 2 * D * 4;              // redm, redl, ntz, ntv
   s += (size_t)ZRING * STEP_MAXM * 16 * 4 + 24 * 4 + 16 * 8 * 4; // sml, merge scalars, merge factors
-  s += (2 * NST + 8) * 8 + NST * 16 + STEP_MAXM * sizeof(StepPart) + 16;   // barriers, descriptors, parts, counters
+  if (UM) s += (size_t)2 * NW * 8 * 4;                           // stage maxima
+  s += (2 * NST + 16) * 8 + NST * 16 + STEP_MAXM * sizeof(StepPart) + 32;   // barriers, descriptors, parts, counters
   return s;
 }
 
 // ring depth: as many stages as fit beside the scratch
 static int step_nst(const DevView& v) {
+  if (v.step_um) return 3;
   if (v.step_nw == 4) return v.D == 128 ? 2 : 4;                 // two CTAs per SM
   if (v.D == 128) return v.cap2 > 0 ? 2 : 3;
   return v.cap2 > 0 ? 5 : 6;
 }
 
-#define KVT_STEP_SHAPES(X)                                          \
-  X(128, 8, 3) X(128, 8, 2) X(64, 8, 6) X(64, 8, 5) X(128, 4, 2) X(64, 4, 4)
+#define KVT_STEP_SHAPES(X)                                                                   \
+  X(128, 8, 3, false) X(128, 8, 2, false) X(64, 8, 6, false) X(64, 8, 5, false) X(128, 4, 2, false) \
+  X(64, 4, 4, false) X(128, 4, 3, true)
+#define KVT_STEP_MATCH(DD, NWW, NSS, UU) \
+  (v.D == DD && nst == NSS && (UU ? v.step_um != 0 : (v.step_um == 0 && v.step_nw == NWW)))
 
 size_t step_smem_bytes(const DevView& v) {
   const int nst = step_nst(v);
-#define KVT_SZ(DD, NWW, NSS) \
-  if (v.D == DD && v.step_nw == NWW && nst == NSS) return step_smem_bytes_t<DD, NWW, NSS>(v);
+#define KVT_SZ(DD, NWW, NSS, UU) \
+  if (KVT_STEP_MATCH(DD, NWW, NSS, UU)) return step_smem_bytes_t<DD, NWW, NSS, UU>(v);
   KVT_STEP_SHAPES(KVT_SZ)
 #undef KVT_SZ
   return ~(size_t)0;
 }
 
-template <int D, int NW, int NST>
+template <int D, int NW, int NST, bool UM>
 static cudaError_t step_conf_t(const DevView& v, int* clusters) {
-  auto kern = k_decode_step<D, NW, NST>;
-  const size_t smem = step_smem_bytes_t<D, NW, NST>(v);
+  auto kern = k_decode_step<D, NW, NST, UM>;
+  const size_t smem = step_smem_bytes_t<D, NW, NST, UM>(v);
   const int K = v.step_s;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(v.B * v.Hkv * v.step_s / v.step_m, 1, 1);
-  cfg.blockDim = dim3((NW + 4) * 32, 1, 1);
+  cfg.blockDim = dim3((NW + 4 + (UM ? 1 : 0)) * 32, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -916,23 +1211,23 @@ static cudaError_t step_conf_t(const DevView& v, int* clusters) {
   return cudaOccupancyMaxActiveClusters(clusters, kern, &cfg);
 }
 
-// Co-resident clusters of v.step_s CTAs of the v.step_nw shape (0: it cannot run).
+// Co-resident clusters of v.step_s CTAs of the chosen shape (0: it cannot run).
 cudaError_t step_configure(const DevView& v, int* clusters) {
   *clusters = 0;
   const int nst = step_nst(v);
-#define KVT_CF(DD, NWW, NSS) \
-  if (v.D == DD && v.step_nw == NWW && nst == NSS) return step_conf_t<DD, NWW, NSS>(v, clusters);
+#define KVT_CF(DD, NWW, NSS, UU) \
+  if (KVT_STEP_MATCH(DD, NWW, NSS, UU)) return step_conf_t<DD, NWW, NSS, UU>(v, clusters);
   KVT_STEP_SHAPES(KVT_CF)
 #undef KVT_CF
   return cudaErrorInvalidValue;
 }
 
-template <int D, int NW, int NST>
+template <int D, int NW, int NST, bool UM>
 static cudaError_t step_launch_t(const DevView& v, const StepIO& io, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(v.step_k, 1, 1);                  // step_k = total CTAs
-  cfg.blockDim = dim3((NW + 4) * 32, 1, 1);
-  cfg.dynamicSmemBytes = step_smem_bytes_t<D, NW, NST>(v);
+  cfg.blockDim = dim3((NW + 4 + (UM ? 1 : 0)) * 32, 1, 1);
+  cfg.dynamicSmemBytes = step_smem_bytes_t<D, NW, NST, UM>(v);
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   int na = 0;
@@ -952,7 +1247,7 @@ static cudaError_t step_launch_t(const DevView& v, const StepIO& io, cudaStream_
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, k_decode_step<D, NW, NST>, v, io);
+  return cudaLaunchKernelEx(&cfg, k_decode_step<D, NW, NST, UM>, v, io);
 }
 
 cudaError_t launch_decode_step(const DevView& v, const void* q, const void* knew, const void* vnew, void* o, int score,
@@ -964,8 +1259,8 @@ cudaError_t launch_decode_step(const DevView& v, const void* q, const void* knew
   io.o = o;
   io.score = score;
   const int nst = step_nst(v);
-#define KVT_LN(DD, NWW, NSS) \
-  if (v.D == DD && v.step_nw == NWW && nst == NSS) return step_launch_t<DD, NWW, NSS>(v, io, s);
+#define KVT_LN(DD, NWW, NSS, UU) \
+  if (KVT_STEP_MATCH(DD, NWW, NSS, UU)) return step_launch_t<DD, NWW, NSS, UU>(v, io, s);
   KVT_STEP_SHAPES(KVT_LN)
 #undef KVT_LN
   return cudaErrorInvalidValue;

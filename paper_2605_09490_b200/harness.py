@@ -30,7 +30,8 @@ class TieredDecode:
     first manage event (t = 0) sees exactly N tokens (reading AMB-22)."""
 
     def __init__(self, w, device="cuda:0", out_fp32=True, split=0, seed_offset=0, keep_inputs=False, variant=0,
-                 heads=None, classify_fn=None, shard=kt.SHARD_REQUEST, rank=0, world=1, nccl_id=None):
+                 heads=None, classify_fn=None, shard=kt.SHARD_REQUEST, rank=0, world=1, nccl_id=None,
+                 step_kernel=0):
         """heads = (first kv head, count): this ctx holds only those kv heads and their q
         heads (KV-head sharding); classify_fn(run, stream) replaces kv.classify at events
         (e.g. dist.kvhead_classify, or a single-process gather over several ctxs); nccl_id:
@@ -52,7 +53,8 @@ class TieredDecode:
                                   staging=w["staging"], device=self.dev.index or 0, out_fp32=int(out_fp32),
                                   split=split, variant=variant, shard=shard, rank=rank, world=world,
                                   policy=w.get("policy", 0), budget=w.get("budget", 0),
-                                  policy_seed=w.get("policy_seed", 0), scorer=w.get("scorer", 0))
+                                  policy_seed=w.get("policy_seed", 0), scorer=w.get("scorer", 0),
+                                  step_kernel=step_kernel)
         hs = slice(h0, h0 + hl)
         qs = slice(h0 * G, (h0 + hl) * G)
         self.kv = kt.KvTier(self.cfg, nccl_id=nccl_id)
@@ -179,6 +181,9 @@ class ModelDecode:
                             wd=W(inter, hidden)) for _ in range(L)]
         self.x = torch.randn(B, hidden, generator=g, device=dev).to(torch.bfloat16)
         self.O = torch.empty((B, Hq, d), dtype=torch.bfloat16, device=dev)
+        # the weights were drawn on torch's current stream; the steps run on the ctx's main
+        # stream (non-blocking w.r.t. it): order them
+        self.run.main.wait_stream(torch.cuda.current_stream(dev))
 
     @staticmethod
     def _rms(x):

@@ -40,7 +40,8 @@ class Config(C.Structure):
         ("evict_mode", C.c_int32), ("staging_tokens", C.c_uint32),
         ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("shard", C.c_int32),
         ("out_fp32", C.c_int32), ("split", C.c_int32), ("variant", C.c_int32),
-        ("policy", C.c_int32), ("budget", C.c_int32), ("policy_seed", C.c_uint32), ("scorer", C.c_int32)]
+        ("policy", C.c_int32), ("budget", C.c_int32), ("policy_seed", C.c_uint32), ("scorer", C.c_int32),
+        ("step_kernel", C.c_int32)]
 
 
 class Sizes(C.Structure):
@@ -137,14 +138,14 @@ def _stream_ptr(stream):
 def make_config(B, L, Hq, Hkv, d, max_tokens, prompt_len, hbm_bp=5000, evict_bp=500, t2_bp=0,
                 sink_size=4, window_size=128, manage_interval=64, evict_mode=EVICT_TOTAL,
                 staging=STAGING_ALL, device=0, out_fp32=1, split=0, rank=0, world=1, variant=0,
-                shard=0, policy=0, budget=0, policy_seed=0, scorer=0):
+                shard=0, policy=0, budget=0, policy_seed=0, scorer=0, step_kernel=0):
     return Config(num_requests=B, num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=d,
                   max_tokens=max_tokens, prompt_len=prompt_len, sink_size=sink_size,
                   window_size=window_size, manage_interval=manage_interval, hbm_ratio_bp=hbm_bp,
                   evict_ratio_bp=evict_bp, t2_fraction_bp=t2_bp, evict_mode=evict_mode,
                   staging_tokens=staging, device=device, rank=rank, world=world, shard=shard,
                   out_fp32=out_fp32, split=split, variant=variant, policy=policy, budget=budget,
-                  policy_seed=policy_seed, scorer=scorer)
+                  policy_seed=policy_seed, scorer=scorer, step_kernel=step_kernel)
 
 
 NCCL_ID_BYTES = 128

@@ -46,6 +46,9 @@ def test_sass_is_sm100a_and_uses_tensor_cores():
     assert "HMMA" in out                 # mma.sync bf16 tiles in the decode kernel
     assert "UBLKCP" in out               # cp.async.bulk ring (TMA bulk copy engine)
     assert "SYNCS" in out                # mbarrier full/empty pipeline
+    assert "UTCHMMA" in out              # tcgen05.mma (step kernel, step_kernel = 2)
+    assert "LDTM" in out                 # tcgen05.ld: TMEM accumulators -> registers
+    assert "UTCBAR" in out               # tcgen05.commit -> mbarrier
 
 
 def test_library_loads_and_versions():
@@ -120,7 +123,8 @@ def test_lse_combine_rejects_bad_arguments():
         assert st == -1                                            # E_INVAL
 
 
-@pytest.mark.parametrize("field,value", [("policy", 9), ("scorer", 6), ("scorer", -1), ("budget", 0)])
+@pytest.mark.parametrize("field,value", [("policy", 9), ("scorer", 6), ("scorer", -1), ("budget", 0),
+                                         ("step_kernel", 3)])
 def test_policy_and_scorer_validation(field, value):
     kw = dict(policy=kt.POLICY_H2O, budget=100)
     kw[field] = value

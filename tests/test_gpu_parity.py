@@ -345,6 +345,41 @@ def test_step_kernel_shapes(shape):
     _run_pair(w, graph=True, check_every=2)
 
 
+@pytest.mark.parametrize("G,Hkv,s", [(7, 4, 4), (5, 4, 2), (8, 2, 3), (1, 4, 9), (2, 2, 16)])
+def test_umma_step_kernel_parity(G, Hkv, s):
+    # the tcgen05 / TMEM consumer of the whole-step kernel (d = 128, no T2 rows): S = K q^T and
+    # O = V^T P^T on the 5th-generation tensor cores, online softmax on the CUDA cores; every
+    # event's tiers / rows and o / scores against the oracle, across head ratios and cluster sizes
+    w = H.workload("tiny", B=2, L=3, Hq=G * Hkv, Hkv=Hkv, d=128, N=900, P=64, interval=8, steps=18,
+                   hbm_bp=4000, evict_bp=800, t2_bp=0)
+    run = H.TieredDecode(w, split=s, step_kernel=2)
+    shape = run.kv.layout()[1]
+    run.close()
+    assert shape[0] > 0 and shape[1] == s and shape[3] == 5, shape      # the tcgen05 consumer
+    _run_pair(w, graph=True, check_every=2, split=s, step_kernel=2)
+
+
+def test_umma_step_kernel_equals_mma_sync_consumer():
+    # the two consumers of the whole-step kernel compute the same softmax in a different
+    # summation order: fp32 rounding apart, T0 rows byte-equal
+    w = H.workload("tiny", B=3, L=4, Hq=28, Hkv=4, d=128, N=1500, P=64, interval=8, steps=20, hbm_bp=5000,
+                   evict_bp=500, t2_bp=0)
+    a = H.TieredDecode(w, step_kernel=1)
+    b = H.TieredDecode(w, step_kernel=2)
+    assert a.kv.layout()[1][3] == 8 and b.kv.layout()[1][3] == 5
+    a.capture()
+    b.capture()
+    for t in range(w["steps"]):
+        a.step()
+        b.step()
+        oa, ob = a.output(), b.output()
+        assert np.abs(oa - ob).max() <= 2e-6 + 1e-5 * np.abs(oa).max(), t
+    a.sync(); b.sync()
+    assert np.array_equal(a.kv.export(kt.X_TIERS), b.kv.export(kt.X_TIERS))
+    assert np.array_equal(a.kv.export(kt.X_T0_ROWS, 1), b.kv.export(kt.X_T0_ROWS, 1))
+    a.close(); b.close()
+
+
 @pytest.mark.parametrize("s", [1, 2, 3, 5, 9, 16])
 def test_step_kernel_slices_per_head(s):
     # the config's split fixes the cluster size (row slices per kv head): odd sizes, a 9-CTA and a
