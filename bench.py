@@ -526,12 +526,19 @@ def main():
             hidden, inter = MODEL_DIMS[args.config]
             Km, Wm = 64, 3                      # one Delta: exactly one classify/migrate event (t = 64)
             model_leg = {"hidden": hidden, "intermediate": inter,
-                         "note": "random bf16 weights, RMSNorm + GEMMs + SiLU in torch/cuBLAS, no RoPE / LM head"}
-            for name, extra in (("all_hbm_no_eviction", dict(hbm_bp=10000, evict_bp=0)), ("hierarchy", {}),
-                                ("hierarchy_stream_mode", dict(staging=0))):
+                         "note": "random bf16 weights, RMSNorm + GEMMs + SiLU in torch/cuBLAS, no RoPE / LM head; "
+                                 "each decoder step is ONE CUDA graph (torch.cuda.graph around the library's "
+                                 "kv_tier_capture_begin/_end, kv_tier_graph_advance per replay) except "
+                                 "hierarchy_eager; the Delta-step window holds one classify/migrate event"}
+            for name, extra, graph in (("all_hbm_no_eviction", dict(hbm_bp=10000, evict_bp=0), True),
+                                       ("hierarchy", {}, True), ("hierarchy_eager", {}, False),
+                                       ("hierarchy_stream_mode", dict(staging=0), True)):
                 md = H.ModelDecode(dict(w, **extra), hidden=hidden, inter=inter, device=dev,
                                    split=args.split, seed_offset=seed_off)
                 for _ in range(Wm):
+                    md.step()
+                if graph:
+                    md.capture()
                     md.step()
                 md.sync()
                 _barrier_sync()
@@ -541,7 +548,7 @@ def main():
                 del md
                 torch.cuda.empty_cache()
             b0 = model_leg["all_hbm_no_eviction"]["ms_per_step"]
-            for name in ("hierarchy", "hierarchy_stream_mode"):
+            for name in ("hierarchy", "hierarchy_eager", "hierarchy_stream_mode"):
                 model_leg[name]["overhead_pct_vs_all_hbm"] = 100.0 * (model_leg[name]["ms_per_step"] / b0 - 1.0)
 
     cpu = None

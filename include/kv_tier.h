@@ -324,6 +324,18 @@ KV_TIER_API kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const vo
                                                       void* stream, void* side);
 KV_TIER_API kv_tier_status kv_tier_step_graph_launch(kv_tier_ctx* ctx, void* stream);
 
+/* A whole decoder step in the CALLER's CUDA graph: kv_tier_capture_begin before
+ * the caller begins its stream capture, the step's calls (begin_step, prefetch,
+ * decode_attention per layer, end_step; no classify / migrate) on the capturing stream, and
+ * kv_tier_capture_end after the capture ends: the host state machine runs once during the
+ * capture and is restored.  After each replay of that graph, kv_tier_graph_advance moves the
+ * host mirror on by one step (the kernels read the step and tier counters from device memory,
+ * so one graph serves every step, events included).  E_STATE out of order; E_CAPACITY as
+ * begin_step. */
+KV_TIER_API kv_tier_status kv_tier_capture_begin(kv_tier_ctx* ctx);
+KV_TIER_API kv_tier_status kv_tier_capture_end(kv_tier_ctx* ctx);
+KV_TIER_API kv_tier_status kv_tier_graph_advance(kv_tier_ctx* ctx);
+
 /* a5: per request, protected set P = [0,P) u [P,P+k_s) u [n-k_w,n); the live
  * non-protected tokens ordered by the unique key (fp32 bits of S_i, i) ascending
  * (AMB-7); n_new = bottom -> T3 (AMB-8/9), top floor(beta|surv|) -> T0, lowest

@@ -80,6 +80,7 @@ struct kv_tier_ctx {
   bool slot_busy[ZRING] = {};              // a score kernel may still read the slot
   bool scores_pending = false;             // score kernels not yet joined back into the main stream
   cudaStream_t score_stream = nullptr;     // a4 score updates run here, off the attention chain
+  cudaStream_t offload_stream = nullptr;   // differential staging: rows entering T1/T2 -> pinned host
   cudaEvent_t ev_merged[ZRING] = {}, ev_scored[ZRING] = {}, ev_score_tail = nullptr;
   bool slot_recorded[2] = {false, false};   // ev_slot_free[x] recorded within the open step
   int lse_pending = -1;                    // score slot of a decode_attention_lse awaiting the global (M, L)
@@ -559,6 +560,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_score_tail, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->score_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->offload_stream, cudaStreamNonBlocking);
   ctx->ev_prefetched.assign(v.L, nullptr);
   for (int l = 0; l < v.L && e == cudaSuccess; ++l) e = cudaEventCreateWithFlags(&ctx->ev_prefetched[l], cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -624,6 +626,7 @@ kv_tier_status kv_tier_destroy(kv_tier_ctx* ctx) {
   }
   if (ctx->ev_score_tail) cudaEventDestroy(ctx->ev_score_tail);
   if (ctx->score_stream) cudaStreamDestroy(ctx->score_stream);
+  if (ctx->offload_stream) cudaStreamDestroy(ctx->offload_stream);
   for (int i = 0; i < 2; ++i) {
     if (ctx->h1_inc[i]) cudaFreeHost(ctx->h1_inc[i]);
     if (ctx->ev_inc[i]) cudaEventDestroy(ctx->ev_inc[i]);
@@ -973,7 +976,7 @@ kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side) 
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (!ctx->classified) return fail(ctx, KV_TIER_E_STATE, "migrate without a preceding classify");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(main_stream);
-  (void)side;                                // the offload runs in stream order with its chunk (mtemp reuse)
+  (void)side;          // differential staging offloads on the ctx's own stream, stream mode in the migrate kernel
   ctx->mig_epoch += 1;                       // host-T1 mode re-reads the T1 lists
   // plan the new row layout, then move only the rows that change, in place: one cooperative
   // launch over chunks of (layer, kv head) pairs (gather + offload of rows entering T1/T2 ->
@@ -984,7 +987,13 @@ kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side) 
   if (e == cudaSuccess) e = launch_migrate_rows(ctx->v, s);
   if (e == cudaSuccess) e = launch_commit(ctx->v, s);
   if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_migrated, s);
-  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_offload_done, s);
+  if (ctx->v.stream_mode) {                  // rows entering T1/T2 already written by the migrate kernel
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_offload_done, s);
+  } else {                                   // copy them out beside the next steps (P:643's overlap)
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->offload_stream, ctx->ev_migrated, 0);
+    if (e == cudaSuccess) e = launch_offload_rows(ctx->v, ctx->offload_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_offload_done, ctx->offload_stream);
+  }
   kv_tier_status st = cuda_check(ctx, e, "migrate");
   if (st) return st;
   ctx->offload_pending = true;
@@ -1086,34 +1095,68 @@ kv_tier_status kv_tier_step(kv_tier_ctx* ctx, const void* q, const void* k_new, 
   return kv_tier_end_step(ctx, stream);
 }
 
-kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const void* k_new, const void* v_new,
-                                          void* o, int32_t fuse_score_update, void* stream, void* side) {
+// External capture of a whole decoder step (the caller's CUDA graph holds this ctx's step calls
+// between its own kernels): the host state machine runs once during the capture and is restored
+// afterwards; kv_tier_graph_advance then advances it once per replay (kernels read the step and
+// tier counters from device memory, so one graph serves every step).
+struct CaptureSave {
+  int n, t, c0;
+  bool classified;
+  std::vector<int> pstep, astep;
+};
+static thread_local CaptureSave g_cap;
+kv_tier_status kv_tier_capture_begin(kv_tier_ctx* ctx) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "capture inside a step");
   if (!ctx->loaded) return fail(ctx, KV_TIER_E_STATE, "no prefix loaded");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (s == nullptr) return fail(ctx, KV_TIER_E_INVAL, "capture needs a non-default stream");
-  if (ctx->graph_exec) { cudaGraphExecDestroy(ctx->graph_exec); ctx->graph_exec = nullptr; }
-  if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
-  // the capture runs the host state machine once; restore it afterwards
-  const int n = ctx->n, t = ctx->t, c0 = ctx->c[0];
-  const bool classified = ctx->classified;
-  const std::vector<int> pstep = ctx->prefetched_step;
-  const std::vector<int> astep = ctx->appended_step;
-  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
-  if (e != cudaSuccess) return cuda_check(ctx, e, "begin capture");
+  if (ctx->capturing) return fail(ctx, KV_TIER_E_STATE, "capture already open");
+  g_cap = CaptureSave{ctx->n, ctx->t, ctx->c[0], ctx->classified, ctx->prefetched_step, ctx->appended_step};
   ctx->capturing = true;
-  kv_tier_status st = kv_tier_step(ctx, q, k_new, v_new, o, fuse_score_update, stream, side);
+  ctx->pdl_ok = false;
+  return KV_TIER_OK;
+}
+kv_tier_status kv_tier_capture_end(kv_tier_ctx* ctx) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!ctx->capturing) return fail(ctx, KV_TIER_E_STATE, "no capture open");
   ctx->capturing = false;
-  cudaGraph_t g = nullptr;
-  e = cudaStreamEndCapture(s, &g);
-  ctx->n = n; ctx->t = t; ctx->c[0] = c0; ctx->classified = classified; ctx->step_open = false;
-  ctx->prefetched_step = pstep;
-  ctx->appended_step = astep;
+  ctx->pdl_ok = false;
+  ctx->n = g_cap.n; ctx->t = g_cap.t; ctx->c[0] = g_cap.c0; ctx->classified = g_cap.classified;
+  ctx->step_open = false;
+  ctx->prefetched_step = g_cap.pstep;
+  ctx->appended_step = g_cap.astep;
   ctx->zslot_next = 0;
   ctx->zpend_n = 0;
   for (auto& b : ctx->slot_busy) b = false;
   ctx->scores_pending = false;
+  return KV_TIER_OK;
+}
+kv_tier_status kv_tier_graph_advance(kv_tier_ctx* ctx) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (ctx->step_open || ctx->capturing) return fail(ctx, KV_TIER_E_STATE, "advance inside a step or a capture");
+  if (ctx->n + 1 > ctx->v.Nmax) return fail(ctx, KV_TIER_E_CAPACITY, "N_max=%d reached", ctx->v.Nmax);
+  if (ctx->c[0] + 1 > ctx->v.cap0) return fail(ctx, KV_TIER_E_CAPACITY, "T0 store full (%d rows)", ctx->v.cap0);
+  ctx->c[0] += seq_own(ctx->v.seq_w, ctx->v.seq_r, ctx->n) ? 1 : 0;
+  ctx->n += 1;
+  ctx->t += 1;
+  ctx->classified = false;
+  return KV_TIER_OK;
+}
+
+kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const void* k_new, const void* v_new,
+                                          void* o, int32_t fuse_score_update, void* stream, void* side) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (s == nullptr) return fail(ctx, KV_TIER_E_INVAL, "capture needs a non-default stream");
+  kv_tier_status st = kv_tier_capture_begin(ctx);
+  if (st) return st;
+  if (ctx->graph_exec) { cudaGraphExecDestroy(ctx->graph_exec); ctx->graph_exec = nullptr; }
+  if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) { kv_tier_capture_end(ctx); return cuda_check(ctx, e, "begin capture"); }
+  st = kv_tier_step(ctx, q, k_new, v_new, o, fuse_score_update, stream, side);
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(s, &g);
+  kv_tier_capture_end(ctx);
   if (st) { if (g) cudaGraphDestroy(g); return st; }
   if (e != cudaSuccess) return cuda_check(ctx, e, "end capture");
   e = cudaGraphInstantiate(&ctx->graph_exec, g, 0);
@@ -1121,7 +1164,6 @@ kv_tier_status kv_tier_step_graph_capture(kv_tier_ctx* ctx, const void* q, const
   ctx->graph = g;
   return KV_TIER_OK;
 }
-
 kv_tier_status kv_tier_step_graph_launch(kv_tier_ctx* ctx, void* stream) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (!ctx->graph_exec) return fail(ctx, KV_TIER_E_STATE, "no step graph captured");

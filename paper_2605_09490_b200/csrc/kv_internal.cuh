@@ -271,6 +271,7 @@ cudaError_t launch_end_step(const DevView& v, cudaStream_t s);
 cudaError_t launch_classify(const DevView& v, const float* Sx, int parts, cudaStream_t s);
 cudaError_t launch_plan(const DevView& v, cudaStream_t s);
 cudaError_t launch_migrate_rows(const DevView& v, cudaStream_t s);
+cudaError_t launch_offload_rows(const DevView& v, cudaStream_t s);
 cudaError_t launch_commit(const DevView& v, cudaStream_t s);
 cudaError_t launch_prefetch(const DevView& v, int layer, cudaStream_t s);
 size_t attn_smem_bytes(const DevView& v);

@@ -743,7 +743,9 @@ __global__ void __launch_bounds__(256) k_migrate_rows(const DevView v) {
       const int st = mv.x, srow = mv.y, dt = mv.z & 3, pos = mv.w;
       if (st == T1 && dt == T1 && v.stream_mode) continue;   // list-only move (rows live on the host)
       const size_t grp = grp_of(v, l, b, g);
-      const bool off = st != dt && (dt == T1 || (dt == T2 && v.hc2k != nullptr));
+      // stream mode: the pinned store is T1's only home, so a row entering T1/T2 is written there
+      // now; differential staging keeps it in HBM and k_offload_rows copies it out afterwards
+      const bool off = v.stream_mode && st != dt && (dt == T1 || (dt == T2 && v.hc2k != nullptr));
       uint16_t* tmp = reinterpret_cast<uint16_t*>(v.mtemp) + (size_t)i * 2 * D;
       for (int kv = 0; kv < 2; ++kv) {
         uint16_t* tk = tmp + kv * D;
@@ -889,6 +891,53 @@ cudaError_t launch_plan(const DevView& v, cudaStream_t s) {
   k_plan<<<v.B, PLAN_THREADS, 0, s>>>(v);
   return cudaGetLastError();
 }
+// Differential staging: the rows that entered T1 / T2 at the last migrate, from their new HBM rows
+// (staging / T2 store) to the pinned host stores ("Offload T1 entries"), on the ctx's
+// offload stream while the next steps run: the next classify waits for it (the move list and the
+// rows may change then), and every host-side reader of the pinned stores synchronises first.
+template <int D>
+__global__ void __launch_bounds__(256) k_offload_rows(const DevView v) {
+  constexpr int E = D / 32;
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int B = v.B, npairs = v.L * v.Hkv, sb = v.st->scur;
+  int mmax = 0;
+  for (int b = 0; b < B; ++b) mmax = max(mmax, v.mcount[b]);
+  const long long items = (long long)npairs * B * mmax;
+  for (long long i = gw; i < items; i += nw) {
+    const int m = (int)(i % mmax);
+    const long long r = i / mmax;
+    const int b = (int)(r % B), lg = (int)(r / B), l = lg / v.Hkv, g = lg % v.Hkv;
+    if (m >= v.mcount[b]) continue;
+    const int4 mv = v.moves[(size_t)b * v.mcap + m];
+    const int st = mv.x, dt = mv.z & 3, drow = mv.z >> 2, pos = mv.w;
+    if (st == dt || !(dt == T1 || (dt == T2 && v.hc2k != nullptr))) continue;
+    const size_t grp = grp_of(v, l, b, g);
+    const size_t hr = host_row(v, grp, pos);
+    for (int kv = 0; kv < 2; ++kv) {
+      if (dt == T1) {
+        uint16_t x[E];
+        const uint16_t* s = reinterpret_cast<const uint16_t*>(kv ? v.v1[sb] : v.k1[sb]) + (grp * v.cap1 + drow) * D;
+        load_bits(x, s + swz_off(drow, lane * E, D), E);
+        store_bits(reinterpret_cast<uint16_t*>(kv ? v.hv1 : v.hk1) + hr * D + lane * E, x, E);
+      } else {
+        const int8_t* c = (kv ? v.c2v[sb] : v.c2k[sb]) + (grp * v.cap2 + drow) * D + lane * E;
+        int8_t* dc = (kv ? v.hc2v : v.hc2k) + hr * D + lane * E;
+#pragma unroll
+        for (int k = 0; k < E; ++k) dc[k] = c[k];
+        if (lane == 0) (kv ? v.hs2v : v.hs2k)[hr] = (kv ? v.s2v[sb] : v.s2k[sb])[grp * v.cap2 + drow];
+      }
+    }
+    if (lane == 0) atomicAdd(&v.st->d2h_rows, 2ull);
+  }
+}
+cudaError_t launch_offload_rows(const DevView& v, cudaStream_t s) {
+  if (v.D == 128) k_offload_rows<128><<<32, 256, 0, s>>>(v);
+  else k_offload_rows<64><<<32, 256, 0, s>>>(v);
+  return cudaGetLastError();
+}
+
 // every moved row of the event: one cooperative launch, as many CTAs as are co-resident (<= 2 per SM)
 template <int D>
 static cudaError_t migrate_rows_t(const DevView& v, cudaStream_t s) {

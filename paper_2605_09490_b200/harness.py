@@ -190,9 +190,60 @@ class ModelDecode:
         xf = x.float()
         return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-6)).to(torch.bfloat16)
 
+    def capture(self):
+        """The whole decoder step -- RMSNorm, GEMMs, the library's begin_step / prefetch /
+        decode_attention per layer / end_step -- as ONE CUDA graph (torch.cuda.graph around the
+        library's kv_tier_capture_begin / _end); step() then replays it and advances the
+        library's host state (kv_tier_graph_advance).  Manage events stay eager between replays."""
+        r = self.run
+        self.xin = self.x.clone()
+        torch.cuda.synchronize(self.run.dev)
+        self.graph = torch.cuda.CUDAGraph()
+        r.kv.capture_begin()
+        try:
+            with torch.cuda.graph(self.graph, stream=r.main):
+                self.xout = self._body(self.xin)
+        finally:
+            r.kv.capture_end()
+
+    def _body(self, x):
+        r, w = self.run, self.w
+        kv, s = r.kv, torch.cuda.current_stream(r.dev)
+        B, L, Hq, Hkv, d = w["B"], w["L"], w["Hq"], w["Hkv"], w["d"]
+        stream_mode = w["staging"] == 0
+        kv.begin_step(stream=s)
+        if stream_mode:
+            for l in range(min(2, L)):
+                kv.prefetch(l, side=r.side)
+        for l, p in enumerate(self.layers):
+            qkv = self._rms(x) @ p["wqkv"]
+            q = qkv[:, :Hq * d].reshape(B, Hq, d).contiguous()
+            k = qkv[:, Hq * d:(Hq + Hkv) * d].reshape(B, Hkv, d).contiguous()
+            v = qkv[:, (Hq + Hkv) * d:].reshape(B, Hkv, d).contiguous()
+            kv.decode_attention(l, q, self.O, 1, stream=s, k_new=k, v_new=v)
+            if stream_mode and l + 2 < L:
+                kv.prefetch(l + 2, side=r.side)
+            x = x + self.O.reshape(B, Hq * d) @ p["wo"]
+            gu = self._rms(x) @ p["wgu"]
+            x = x + (torch.nn.functional.silu(gu[:, :self.inter]) * gu[:, self.inter:]) @ p["wd"]
+        kv.end_step(stream=s)
+        return self._rms(x)
+
     def step(self):
         r, w = self.run, self.w
         kv, s, t = r.kv, r.main, r.t
+        if getattr(self, "graph", None) is not None:
+            with torch.cuda.stream(s):
+                self.xin.copy_(self.x)
+                self.graph.replay()
+                kv.graph_advance()
+                if r.is_event(t):
+                    r.classify()
+                    kv.migrate(stream=s, side=r.side)
+                self.x = self.xout.clone()
+            r.t += 1
+            torch.cuda.current_stream(r.dev).wait_stream(s)   # the caller reads x on its own stream
+            return self.x
         B, L, Hq, Hkv, d = w["B"], w["L"], w["Hq"], w["Hkv"], w["d"]
         stream_mode = w["staging"] == 0
         with torch.cuda.stream(s):
@@ -218,6 +269,7 @@ class ModelDecode:
                 kv.migrate(stream=s, side=r.side)
             self.x = self._rms(x)
         r.t += 1
+        torch.cuda.current_stream(r.dev).wait_stream(s)       # the caller reads x on its own stream
         return self.x
 
     def sync(self):

@@ -82,6 +82,9 @@ _SIGS = {
     "kv_tier_step": [C.c_void_p] + [C.c_void_p] * 4 + [C.c_int32, C.c_void_p, C.c_void_p],
     "kv_tier_step_graph_capture": [C.c_void_p] + [C.c_void_p] * 4 + [C.c_int32, C.c_void_p, C.c_void_p],
     "kv_tier_step_graph_launch": [C.c_void_p, C.c_void_p],
+    "kv_tier_capture_begin": [C.c_void_p],
+    "kv_tier_capture_end": [C.c_void_p],
+    "kv_tier_graph_advance": [C.c_void_p],
     "kv_tier_classify": [C.c_void_p, C.c_void_p],
     "kv_tier_classify_gathered": [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p],
     "kv_tier_scores_device": [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)],
@@ -284,6 +287,17 @@ class KvTier:
 
     def step_graph_launch(self, stream=None):
         _check(load().kv_tier_step_graph_launch(self.ctx, _stream_ptr(stream)), self.ctx)
+
+    def capture_begin(self):
+        """Open an external capture (the caller's CUDA graph records this ctx's step calls)."""
+        _check(load().kv_tier_capture_begin(self.ctx), self.ctx)
+
+    def capture_end(self):
+        _check(load().kv_tier_capture_end(self.ctx), self.ctx)
+
+    def graph_advance(self):
+        """Advance the host state machine by the one step a replay of the caller's graph ran."""
+        _check(load().kv_tier_graph_advance(self.ctx), self.ctx)
 
     def classify(self, stream=None):
         _check(load().kv_tier_classify(self.ctx, _stream_ptr(stream)), self.ctx)

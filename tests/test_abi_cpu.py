@@ -188,6 +188,13 @@ def test_nccl_unique_id_and_init_guards():
         assert lib.kv_tier_init(C.byref(cfg), C.byref(buf), idb, C.byref(h)) == -1
 
 
+def test_capture_entry_points_reject_null_ctx():
+    lib = kt.load()
+    assert lib.kv_tier_capture_begin(None) == -1
+    assert lib.kv_tier_capture_end(None) == -1
+    assert lib.kv_tier_graph_advance(None) == -1
+
+
 def test_host_t1_entry_points_reject_null_ctx():
     # N1 entry points check their arguments before touching a device
     lib = kt.load()

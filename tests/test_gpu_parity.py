@@ -591,6 +591,68 @@ def test_sequence_sharding_two_processes():
         assert status == "ok", (rank, status)
 
 
+# --------------------------------------------------------------------- negative controls,
+# determinism (item 6): the parity checks must fail on an injected fault
+def test_negative_control_flipped_tier_is_caught():
+    # one live token's score is raised on the GPU side only (kv_tier_import_scores): at the next
+    # event it lands in T0 on the GPU but not in the oracle, and the event-state check must fail
+    w = H.workload("tiny", interval=8, steps=9)
+    run = H.TieredDecode(w)
+    orc = OracleRun(w)
+    for t in range(8):
+        run.step()
+        orc.step()
+    run.sync()
+    S = run.kv.export(kt.X_SCORES).copy()
+    t1 = O.export_index(orc.st, 0, O.T1)
+    assert t1.size > 0
+    S[0, :, t1[0]] += 1e3                                   # a T1 token becomes the heaviest hitter
+    run.kv.import_scores(S)
+    run.step()
+    orc.step()
+    run.sync()
+    with pytest.raises(AssertionError):
+        _check_event_state(run, orc, orc.reqs)
+    run.close()
+
+
+def test_negative_control_missing_token_is_caught():
+    # the GPU evicts one token more than the oracle (r one step higher at the first event): the
+    # tier / index / census checks must fail even when the attention outputs stay within tolerance
+    w = H.workload("tiny", interval=8, steps=1)
+    run = H.TieredDecode(dict(w, evict_bp=w["evict_bp"] + 100))      # floor(6.48) = 6 vs floor(5.4) = 5 of |U| = 108
+    orc = OracleRun(w)
+    run.step()
+    orc.step()
+    run.sync()
+    assert run.kv.census()[0][0][3] == O.census(orc.st, 0)[3] + 1
+    with pytest.raises(AssertionError):
+        _check_event_state(run, orc, orc.reqs)
+    run.close()
+
+
+def test_two_runs_export_identical_bytes():
+    # determinism: two runs of the same seeded workload give byte-identical outputs and exports
+    w = H.workload("tiny", B=2, L=2, interval=8, steps=20, t2_bp=3000, evict_bp=800)
+    res = []
+    for _ in range(2):
+        run = H.TieredDecode(w)
+        run.capture()
+        outs = []
+        for _ in range(w["steps"]):
+            run.step()
+            outs.append(run.output())
+        run.sync()
+        res.append((np.stack(outs), [run.kv.export(x) for x in (kt.X_SCORES, kt.X_TIERS, kt.X_IDX_T1)],
+                    run.kv.export(kt.X_T0_ROWS, 1), run.kv.export(kt.X_T2_CODES, 0)))
+        run.close()
+    a, b = res
+    assert np.array_equal(a[0], b[0])
+    for x, y in zip(a[1], b[1]):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
+
+
 # --------------------------------------------------------------------- tier policies (§8f N3)
 @pytest.mark.parametrize("policy,budget", [(kt.POLICY_STREAMING, 0), (kt.POLICY_H2O, 300), (kt.POLICY_RANDOM, 300)])
 def test_tier_policy_parity(policy, budget):
@@ -761,6 +823,31 @@ def test_model_decode_stream_mode_equals_differential_and_prop1():
     a, b = xs["diff50"].astype(np.float64), xs["hbm100"].astype(np.float64)
     rel = np.linalg.norm(a - b) / np.linalg.norm(b)
     assert rel <= 2e-2, rel
+
+
+@pytest.mark.parametrize("staging", [kt.STAGING_ALL, 0])
+def test_model_decode_graph_equals_eager(staging):
+    # the whole decoder step as one CUDA graph (torch.cuda.graph around kv_tier_capture_begin /
+    # _end, kv_tier_graph_advance per replay; events eager between replays) runs the same kernels
+    # on the same data as the eager step: identical hidden states, scores and tiers
+    base = dict(B=2, L=3, Hq=8, Hkv=2, d=64, N=400, P=16, interval=4, steps=14, evict_bp=800, hbm_bp=5000,
+                staging=staging)
+    outs, tiers, scores = [], [], []
+    for graph in (False, True):
+        m = H.ModelDecode(H.workload("tiny", **base), hidden=256, inter=512)
+        seq = []
+        for t in range(base["steps"]):
+            if graph and t == 2:
+                m.capture()
+            seq.append(m.step().float().cpu().numpy())
+        m.sync()
+        outs.append(np.stack(seq))
+        tiers.append(m.run.kv.export(kt.X_TIERS))
+        scores.append(m.run.kv.export(kt.X_SCORES))
+        m.close()
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(tiers[0], tiers[1])
+    assert np.array_equal(scores[0], scores[1])
 
 
 def test_lse_combine_kernel_matches_full_softmax():
