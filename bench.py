@@ -35,9 +35,9 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
 STEP_KERNELS = {"auto": 0, "mma": 1, "tcgen05": 2}                      # kv_tier_config::step_kernel
 CONFIG_INDEX = {"tiny": 0, "7b": 1, "14b": 2, "32b": 3, "70b": 4}      # BASELINE.json configs[i]
 POLICIES = {"hierarchy": 0, "streaming": 1, "h2o": 2, "random": 3}       # kv_tier_policy
-SCORERS = {"attention": 0, "vatp": 1, "redundancy": 2, "combined": 3}    # kv_tier_scorer
+SCORERS = {"attention": 0, "vatp": 1, "redundancy": 2, "combined": 3, "window": 4, "rkv": 5}   # kv_tier_scorer
 MODEL_DIMS = {"tiny": (256, 512), "7b": (3584, 18944)}                    # (hidden, intermediate): Qwen2-7B
-EVENT_LAUNCHES = 8          # classify, plan, move gather/scatter, rebuild, commit, offload moves/host
+EVENT_LAUNCHES = 5          # classify, plan, cooperative migrate, commit, offload (side stream)
 
 
 def _metric():
@@ -80,7 +80,8 @@ def _args():
                     help="N>1 partitioning: requests per rank (weak scaling, default) or one batch's "
                          "positions split over the ranks with a per-layer LSE combine (strong scaling)")
     ap.add_argument("--scorer", default="attention", choices=list(SCORERS),
-                    help="token scorer: Eq. 1 attention, VATP (P:712), redundancy (P:713), combined (P:714)")
+                    help="token scorer: Eq. 1 attention, VATP (P:712), redundancy (P:713), combined (P:714), "
+                         "windowed attention (P:137, P:976), R-KV's 0.07 I - 0.93 R (P:972-978)")
     ap.add_argument("--positions", type=int, default=0,
                     help="chain length N per request (0: the config's); e.g. --config 70b --positions 2048 = "
                          "the positions ONE rank of configs[4]'s 8-way sequence split attends")
