@@ -708,7 +708,7 @@ __global__ void __launch_bounds__((NW + 4 + (UM ? 1 : 0)) * 32, (NW <= 4 && !UM)
     bool pend = false;                                       // a P.V of this part sits in TMEM O
     const uint32_t tq_lane = (uint32_t)(32 * w) << 16;      // TMEM lane quadrant of this warp
     auto fold_o = [&](int k) {                               // O (through the P.V of stage k) -> registers
-      mbar_sleep_wait(odone0 + 8 * (k & 1), (k >> 1) & 1);
+      mbar_wait(odone0 + 8 * (k & 1), (k >> 1) & 1);
       tc_fence_after();
       uint32_t r[16];
       tmem_ld16(tmem + 32 + tq_lane, r);
@@ -717,7 +717,9 @@ __global__ void __launch_bounds__((NW + 4 + (UM ? 1 : 0)) * 32, (NW <= 4 && !UM)
       for (int h = 0; h < 8; ++h) oacc[h] += __uint_as_float(r[h]) + __uint_as_float(r[8 + h]);
     };
     auto build_q = [&](int l) {                              // q(l) of the head -> the swizzled q tile
-      mbar_sleep_wait(qbar, l & 1);                          // the layer dependency held, q(l) landed
+      if (tid == 0) ctrace(l, 12);
+      mbar_wait(qbar, l & 1);                          // the layer dependency held, q(l) landed
+      if (tid == 0) { trace(l, 1); ctrace(l, 13); }
       const uint16_t* qsrc = reinterpret_cast<const uint16_t*>(qsm(l));
       for (int x = tid; x < 16 * (D / 8); x += NCONS) {
         const int r = x / (D / 8), c = x % (D / 8);
@@ -731,13 +733,14 @@ __global__ void __launch_bounds__((NW + 4 + (UM ? 1 : 0)) * 32, (NW <= 4 && !UM)
     build_q(0);
     for (int i = 0;; ++i) {
       const int s2 = i % NST;
-      mbar_sleep_wait(full0 + 8 * s2, (i / NST) & 1);       // acquire the stage descriptor
+      mbar_wait(full0 + 8 * s2, (i / NST) & 1);       // acquire the stage descriptor
       const int4 dsc = sdesc[s2];
-      mbar_sleep_wait(sready0 + 8 * (i & 1), (i >> 1) & 1);
+      mbar_wait(sready0 + 8 * (i & 1), (i >> 1) & 1);
       if (dsc.x < 0) break;
       const int l = dsc.x, kpart = dsc.y, j = dsc.z, fl = dsc.w & 0xFF, cnt = dsc.w >> 8;
       const int g = part(kpart).g, u = b * Hkv + g;
       if (fl & SD_FIRST) {
+        if (tid == 0) ctrace(l, 14);                         // S of the layer's first stage is in TMEM
         if (lane == 0 && io.score)
           while (*sc_done < l - ZS + 1) __nanosleep(128);     // logit slot of layer l - ZS consumed
         __syncwarp();
@@ -809,7 +812,7 @@ __global__ void __launch_bounds__((NW + 4 + (UM ? 1 : 0)) * 32, (NW <= 4 && !UM)
       }
       const bool fresh = !pend || raise;                     // this stage's P.V starts O afresh
       // ---- p = 2^(z - m) as two bf16 terms (hi: P rows 0-7, lo: rows 8-15), token column t
-      if (i >= 2) mbar_sleep_wait(odone0 + 8 * (i & 1), ((i - 2) >> 1) & 1);   // P.V(i - 2) read this p tile
+      if (i >= 2) mbar_wait(odone0 + 8 * (i & 1), ((i - 2) >> 1) & 1);   // P.V(i - 2) read this p tile
       unsigned char* pt = ptile + (i & 1) * 16 * ROWB;
 #pragma unroll
       for (int h = 0; h < 8; ++h) {
@@ -829,6 +832,7 @@ __global__ void __launch_bounds__((NW + 4 + (UM ? 1 : 0)) * 32, (NW <= 4 && !UM)
       if (!(fl & SD_LAST)) continue;
       // ---- part end: the CTA partial is (m = mref, l = sum of p over the 128 token rows, o)
       if (pend) fold_o(i);
+      if (tid == 0) ctrace(l, 15);
       tc_fence_before();
       pend = false;
 #pragma unroll

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--t2", type=int, default=0)
     ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--step-kernel", type=int, default=0, help="kv_tier_config::step_kernel (2 = tcgen05)")
     a = ap.parse_args()
     if a.trace:
         os.environ["KVTIER_TRACE"] = "1"
@@ -27,7 +28,7 @@ def main():
     over = {"B": a.batch} if a.batch else {}
     for fuse in (1, 0):
         w = H.workload(a.config, steps=a.steps + 10, t2_bp=a.t2, **over)
-        run = H.TieredDecode(w, out_fp32=False)
+        run = H.TieredDecode(w, out_fp32=False, step_kernel=a.step_kernel)
         with torch.cuda.stream(run.main):
             run.kv.step_graph_capture(run.qbuf, run.kbuf, run.vbuf, run.O, fuse, stream=run.main, side=run.side)
         run.graph = True
