@@ -60,8 +60,9 @@ typedef enum {
  * PER_EVENT: literal Alg. 1, n_evict = floor(r * |U|) at every event. */
 typedef enum { KV_TIER_EVICT_TOTAL = 0, KV_TIER_EVICT_PER_EVENT = 1 } kv_tier_evict_mode;
 
-/* Multi-GPU partitioning.  The library itself runs no collective; the caller
- * (paper_2605_09490_b200/dist.py, torch.distributed over NCCL) moves the bytes.
+/* Multi-GPU partitioning.  Without an nccl_unique_id the library runs no collective
+ * and the caller (paper_2605_09490_b200/dist.py, torch.distributed over NCCL) moves the bytes;
+ * with one (sequence sharding only) the library owns the communicator (see SEQUENCE below).
  *   REQUEST  each rank owns B requests; no collective anywhere on the path.
  *   KVHEAD   each rank owns H_kv / world kv heads (num_q_heads / num_kv_heads in the config
  *            are the rank's LOCAL counts; its global kv heads are rank*H_kv .. +H_kv-1).
@@ -107,7 +108,7 @@ typedef enum { KV_TIER_POLICY_HIERARCHY = 0, KV_TIER_POLICY_STREAMING = 1, KV_TI
  *   ATTENTION  Eq. 1: S_i += sum_h p_{l,h,i}.
  *   VATP       value-aware attention: S_i += fp32(sum_h p_{l,h,i}) * ||v_{l,g,i}||_2, the
  *              fp32 L2 norm of the token's bf16 V row of layer l, kv head g, fixed when the row
- *              is loaded / appended.  Split decode kernel only (not KVTIER_FLAT / KVTIER_CLUSTER).
+ *              is loaded / appended.
  *   REDUNDANCY "attn - redundancy" (R-KV): S as ATTENTION; classify ranks by
  *              I_i - rho_i, I_i = fp32(S_i / S_max over the live set), rho_i the mean over layers
  *              and kv heads of c_i = cos(k_i, k_{i-1}) of the original key rows (DESIGN AMB-30/31).
