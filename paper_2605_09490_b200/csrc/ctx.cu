@@ -70,6 +70,11 @@ struct kv_tier_ctx {
   std::vector<int> appended_step;          // step in which layer l's new row was written
   bool offload_pending = false;
   bool capturing = false;
+  struct {                                 // host state saved by kv_tier_capture_begin
+    int n, t, c0;
+    bool classified;
+    std::vector<int> pstep, astep;
+  } cap;
   // per-layer ABI: may decode_attention chain to the previous library launch with programmatic
   // dependent launch?  Only when that launch was this step's decode_attention / append on the
   // same stream (begin_step, score flushes and migrate change state the kernel's prologue reads).
@@ -1099,18 +1104,17 @@ kv_tier_status kv_tier_step(kv_tier_ctx* ctx, const void* q, const void* k_new, 
 // between its own kernels): the host state machine runs once during the capture and is restored
 // afterwards; kv_tier_graph_advance then advances it once per replay (kernels read the step and
 // tier counters from device memory, so one graph serves every step).
-struct CaptureSave {
-  int n, t, c0;
-  bool classified;
-  std::vector<int> pstep, astep;
-};
-static thread_local CaptureSave g_cap;
 kv_tier_status kv_tier_capture_begin(kv_tier_ctx* ctx) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "capture inside a step");
   if (!ctx->loaded) return fail(ctx, KV_TIER_E_STATE, "no prefix loaded");
   if (ctx->capturing) return fail(ctx, KV_TIER_E_STATE, "capture already open");
-  g_cap = CaptureSave{ctx->n, ctx->t, ctx->c[0], ctx->classified, ctx->prefetched_step, ctx->appended_step};
+  ctx->cap.n = ctx->n;
+  ctx->cap.t = ctx->t;
+  ctx->cap.c0 = ctx->c[0];
+  ctx->cap.classified = ctx->classified;
+  ctx->cap.pstep = ctx->prefetched_step;
+  ctx->cap.astep = ctx->appended_step;
   ctx->capturing = true;
   ctx->pdl_ok = false;
   return KV_TIER_OK;
@@ -1120,10 +1124,10 @@ kv_tier_status kv_tier_capture_end(kv_tier_ctx* ctx) {
   if (!ctx->capturing) return fail(ctx, KV_TIER_E_STATE, "no capture open");
   ctx->capturing = false;
   ctx->pdl_ok = false;
-  ctx->n = g_cap.n; ctx->t = g_cap.t; ctx->c[0] = g_cap.c0; ctx->classified = g_cap.classified;
+  ctx->n = ctx->cap.n; ctx->t = ctx->cap.t; ctx->c[0] = ctx->cap.c0; ctx->classified = ctx->cap.classified;
   ctx->step_open = false;
-  ctx->prefetched_step = g_cap.pstep;
-  ctx->appended_step = g_cap.astep;
+  ctx->prefetched_step = ctx->cap.pstep;
+  ctx->appended_step = ctx->cap.astep;
   ctx->zslot_next = 0;
   ctx->zpend_n = 0;
   for (auto& b : ctx->slot_busy) b = false;

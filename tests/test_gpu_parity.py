@@ -905,7 +905,8 @@ def test_randomized_configs(seed):
                                                              kt.SCORER_COMBINED, kt.SCORER_WINDOW,
                                                              kt.SCORER_RKV])))
     api = int(rng.integers(0, 3))             # step graph / kv_tier_step (whole-step kernel) / per-layer ABI
-    _run_pair(w, graph=api == 0, layers_api=api == 2, check_every=3)
+    sk = int(rng.choice([0, 2]))              # whole-step kernel consumer: mma.sync / tcgen05 (where it applies)
+    _run_pair(w, graph=api == 0, layers_api=api == 2, check_every=3, step_kernel=sk)
 
 
 @pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVT_FUZZ_SEEDS_SEQ", "24"))))
