@@ -341,13 +341,20 @@ KV_TIER_API kv_tier_status kv_tier_graph_advance(kv_tier_ctx* ctx);
  * non-protected tokens ordered by the unique key (fp32 bits of S_i, i) ascending
  * (AMB-7); n_new = bottom -> T3 (AMB-8/9), top floor(beta|surv|) -> T0, lowest
  * floor(f2 * rest) -> T2, remainder -> T1 (Alg. 1).  Idempotent until migrate.
- * E_STATE under KV-head sharding with world > 1 (use kv_tier_classify_gathered). */
+ * The ranking key is the scorer's (kv_tier_scorer; WINDOW / RKV: the max-pooled windowed
+ * score, AMB-32/33).  Waits (on `stream`) for the previous event's host offload.
+ * E_STATE under KV-head or sequence sharding with world > 1 (use kv_tier_classify_gathered),
+ * except a sequence-shard ctx that owns a communicator: it all-gathers S_part itself (NCCL on
+ * `stream`) and classifies the sum (one owner per position: exact). */
 KV_TIER_API kv_tier_status kv_tier_classify(kv_tier_ctx* ctx, void* stream);
 
 /* a6: apply the transitions of the last classify: T0<->T1 copies, ->T2 int8
  * quantisation (AMB-12), T2-> bf16 of the dequantised row, ->T3 dropped.
- * Newly offloaded rows are written to the pinned host store on `side`.  E_STATE
- * without a preceding classify. */
+ * Rows entering T1/T2 reach the pinned host store inside the migrate kernel (stream mode) or,
+ * with differential staging, from their new HBM rows on the ctx's own offload stream beside the
+ * following steps (the next classify waits for it; host-side readers synchronise).  One
+ * cooperative launch moves every row (grid barriers; a 2 s watchdog reports E_CUDA at the next
+ * sync instead of hanging).  `side` is unused.  E_STATE without a preceding classify. */
 KV_TIER_API kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side);
 
 /* Synchronise the device and report async errors (E_CUDA, E_NUMERIC). */
