@@ -258,10 +258,10 @@ int zring_of(const kv_tier_config& c);
 void step_plan(DevView& v, int nsm) {
   int best = 0, bs = 0, bm = 0, bnw = 0, bum = 0, brank = 0;
   // candidates in preference order on ties: the tcgen05 consumer, 8 mma.sync warps, 4 warps
-  const int um_ok = v.step_um_ok && v.D == 128 && v.cap2 == 0;
+  const int um_ok = (v.D == 128 && v.cap2 == 0) ? v.step_um_ok : 0;   // the tcgen05 consumer applies
   for (int cand = 0; cand < 3; ++cand) {
-    const int um = cand == 0, nw = cand == 2 ? 4 : 8;
-    if (um && !um_ok) continue;
+    const int um = cand == 0 ? um_ok : 0, nw = cand == 2 ? 4 : 8;
+    if (cand == 0 && !um_ok) continue;
     const int per_sm = nw == 8 ? 1 : 2, rank = 3 - cand;
     for (int m = 8; m >= 1; m >>= 1) {
       if (v.Hkv % m) continue;
@@ -446,7 +446,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
   v.split = auto_split(*cfg);
   v.split_req = cfg->split;
   v.variant = cfg->variant;
-  v.step_um_ok = cfg->step_kernel == 2;
+  v.step_um_ok = cfg->step_kernel == 2 ? 1 : 0;
   v.seq_w = cfg->shard == KV_TIER_SHARD_SEQUENCE ? cfg->world : 1;
   v.seq_r = cfg->shard == KV_TIER_SHARD_SEQUENCE ? cfg->rank : 0;
   v.score_grid = 148;                       // score-flush CTAs beside the per-layer chain (measured best)
