@@ -932,9 +932,12 @@ __global__ void __launch_bounds__(256) k_offload_rows(const DevView v) {
     if (lane == 0) atomicAdd(&v.st->d2h_rows, 2ull);
   }
 }
+// 16 CTAs: the whole-step kernel holds one CTA per SM on 128 of the 148 SMs and needs every
+// cluster resident; an offload that stays under the 20 free SMs never displaces it, and 16 SMs of
+// zero-copy stores already fill the host link
 cudaError_t launch_offload_rows(const DevView& v, cudaStream_t s) {
-  if (v.D == 128) k_offload_rows<128><<<32, 256, 0, s>>>(v);
-  else k_offload_rows<64><<<32, 256, 0, s>>>(v);
+  if (v.D == 128) k_offload_rows<128><<<16, 256, 0, s>>>(v);
+  else k_offload_rows<64><<<16, 256, 0, s>>>(v);
   return cudaGetLastError();
 }
 
