@@ -206,9 +206,9 @@ __global__ void __launch_bounds__((NW + 4 + (UM ? 1 : 0)) * 32, (NW <= 4 && !UM)
     const int* p = done_ctr + (size_t)(l - 1) * B + b;
     if (ld_relaxed_gpu(p) < R) {
       const unsigned long long t0 = gtimer();
-      while (ld_relaxed_gpu(p) < R) {
+      for (unsigned it = 1; ld_relaxed_gpu(p) < R; ++it) {
         __nanosleep(64);
-        if (gtimer() - t0 > 2000000000ull) {       // watchdog: report, never hang the device
+        if ((it & 255u) == 0 && gtimer() - t0 > 2000000000ull) {   // watchdog: report, never hang the device
           atomicOr(&v.st->err, 4);
           break;
         }
@@ -958,9 +958,12 @@ __global__ void __launch_bounds__((NW + 4 + (UM ? 1 : 0)) * 32, (NW <= 4 && !UM)
       __syncwarp();
     };
 
+    long long wfull = 0;                                     // debug: cycles warp 0 waited for stage data
     for (int i = 0;; ++i) {
       const int s2 = i % NST;
+      const long long tw = KVT_TRACE ? clock64() : 0;
       mbar_sleep_wait(full0 + 8 * s2, (i / NST) & 1);
+      if (KVT_TRACE) wfull += clock64() - tw;
       const int4 dsc = sdesc[s2];
       const int l = dsc.x;
       if (l < 0) break;
@@ -1055,6 +1058,10 @@ __global__ void __launch_bounds__((NW + 4 + (UM ? 1 : 0)) * 32, (NW <= 4 && !UM)
 
       // ---------------- part end: warps -> CTA partial (m, l, o) in pbuf
       if (tid == 0 && kpart == 0) ctrace(l, 15);
+      if (KVT_TRACE && v.trace && tid == 0 && kpart == 0) {
+        v.trace[((size_t)l * gridDim.x + blockIdx.x) * NTRACE + 21] = (unsigned long long)wfull;
+        wfull = 0;
+      }
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) {
         la += __shfl_xor_sync(0xffffffffu, la, off);

@@ -13,3 +13,9 @@ for a, b, nm in names:
     tot += d.mean()
 cyc = (tr[2:L - 1, :, 12] - tr[1:L - 2, :, 12]).astype(np.float64)
 print(f"{'layer (12->12)':18s} mean {cyc.mean():8.0f} cyc; sum of segments {tot:.0f}")
+
+if tr.shape[2] > 21:
+    wf = tr[1:L - 1, :, 21].astype(np.float64)
+    wf = wf[wf > 0]
+    if wf.size:
+        print(f"{'stage data waits':18s} mean {wf.mean():8.0f} cyc per layer (warp 0, inside the stage loop)")
