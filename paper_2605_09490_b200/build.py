@@ -15,6 +15,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-X
          "-Xcompiler", "-fopenmp", "-lgomp"]     # OpenMP: host-T1 attention (N1) on the host cores
 if os.environ.get("KVT_TRACE"):             # debug builds: per-(layer, CTA) timeline buffer
     FLAGS += ["-DKVT_TRACE=1"]
+if os.environ.get("KVT_INLINE_OFFLOAD"):    # A/B builds: the event's host offload inside the migrate kernel
+    FLAGS += ["-DKVT_INLINE_OFFLOAD=1"]
 
 TARGETS = {
     "libkvtier.so": ["csrc/ctx.cu", "csrc/attn.cu", "csrc/tiers.cu", "csrc/step.cu"],

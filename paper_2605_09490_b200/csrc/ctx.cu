@@ -992,7 +992,7 @@ kv_tier_status kv_tier_migrate(kv_tier_ctx* ctx, void* main_stream, void* side) 
   if (e == cudaSuccess) e = launch_migrate_rows(ctx->v, s);
   if (e == cudaSuccess) e = launch_commit(ctx->v, s);
   if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_migrated, s);
-  if (ctx->v.stream_mode) {                  // rows entering T1/T2 already written by the migrate kernel
+  if (ctx->v.stream_mode || KVT_INLINE_OFFLOAD) {   // rows entering T1/T2 already written by the migrate kernel
     if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_offload_done, s);
   } else {                                   // copy them out beside the next steps (P:643's overlap)
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->offload_stream, ctx->ev_migrated, 0);

@@ -102,6 +102,10 @@ struct DevView {
   int8_t* hc2k; int8_t* hc2v; float* hs2k; float* hs2v;   // pinned host T2 (mapped, may be null)
 };
 
+#ifndef KVT_INLINE_OFFLOAD
+#define KVT_INLINE_OFFLOAD 0   // A/B builds only (-DKVT_INLINE_OFFLOAD=1): offload inside the migrate kernel
+#endif
+
 __device__ __forceinline__ unsigned long long gtimer() {   // %globaltimer (ns): watchdogs, debug traces
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -745,7 +745,7 @@ __global__ void __launch_bounds__(256) k_migrate_rows(const DevView v) {
       const size_t grp = grp_of(v, l, b, g);
       // stream mode: the pinned store is T1's only home, so a row entering T1/T2 is written there
       // now; differential staging keeps it in HBM and k_offload_rows copies it out afterwards
-      const bool off = v.stream_mode && st != dt && (dt == T1 || (dt == T2 && v.hc2k != nullptr));
+      const bool off = (v.stream_mode || KVT_INLINE_OFFLOAD) && st != dt && (dt == T1 || (dt == T2 && v.hc2k != nullptr));
       uint16_t* tmp = reinterpret_cast<uint16_t*>(v.mtemp) + (size_t)i * 2 * D;
       for (int kv = 0; kv < 2; ++kv) {
         uint16_t* tk = tmp + kv * D;
