@@ -61,16 +61,26 @@ class TieredDecode:
         self.main = torch.cuda.Stream(self.dev)
         self.side = torch.cuda.Stream(self.dev)
         with torch.cuda.stream(self.main):
-            K = SG.gen_kv(self.seed, "k", L, B, Hkv, d, 0, self.n0, P, S.SINK_SIZE, self.dev, stream=self.main)
-            V = SG.gen_kv(self.seed, "v", L, B, Hkv, d, 0, self.n0, P, S.SINK_SIZE, self.dev, stream=self.main)
-            if heads is not None:
-                K, V = K[:, :, hs].contiguous(), V[:, :, hs].contiguous()
-            for l in range(L):
-                self.kv.load_prefix(l, K[l], V[l], self.n0, stream=self.main)
-            self.main.synchronize()
             if keep_inputs:
+                K = SG.gen_kv(self.seed, "k", L, B, Hkv, d, 0, self.n0, P, S.SINK_SIZE, self.dev, stream=self.main)
+                V = SG.gen_kv(self.seed, "v", L, B, Hkv, d, 0, self.n0, P, S.SINK_SIZE, self.dev, stream=self.main)
+                if heads is not None:
+                    K, V = K[:, :, hs].contiguous(), V[:, :, hs].contiguous()
+                for l in range(L):
+                    self.kv.load_prefix(l, K[l], V[l], self.n0, stream=self.main)
                 self.K0, self.V0 = K, V
-            del K, V
+            else:                       # one layer at a time: the full prefix of a large config never sits in HBM
+                for l in range(L):
+                    Kl = SG.gen_kv_layer(self.seed, "k", l, B, Hkv, d, 0, self.n0, P, S.SINK_SIZE, self.dev,
+                                         stream=self.main)
+                    Vl = SG.gen_kv_layer(self.seed, "v", l, B, Hkv, d, 0, self.n0, P, S.SINK_SIZE, self.dev,
+                                         stream=self.main)
+                    if heads is not None:
+                        Kl, Vl = Kl[:, hs].contiguous(), Vl[:, hs].contiguous()
+                    self.kv.load_prefix(l, Kl, Vl, self.n0, stream=self.main)
+                    self.main.synchronize()     # the layer's buffers are freed before the next is drawn
+                    del Kl, Vl
+            self.main.synchronize()
             kn = SG.gen_kv(self.seed, "k", L, B, Hkv, d, self.n0, T, P, S.SINK_SIZE, self.dev, stream=self.main)
             vn = SG.gen_kv(self.seed, "v", L, B, Hkv, d, self.n0, T, P, S.SINK_SIZE, self.dev, stream=self.main)
             # [L][B][Hkv][T][d] -> [T][L][B][Hkv][d] (per-step append rows)

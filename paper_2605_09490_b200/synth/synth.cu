@@ -47,7 +47,7 @@ __device__ __forceinline__ float direction(uint64_t seed, int l, int g, int dim)
 }
 
 __global__ void k_gen_kv(uint64_t seed, int which, int L, int B, int Hkv, int d, int pos0, int npos, int P,
-                         int ks, float sig_a, uint16_t* out) {
+                         int ks, float sig_a, uint16_t* out, int l0) {
   const size_t total = (size_t)L * B * Hkv * npos * d;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     size_t r = e;
@@ -55,7 +55,7 @@ __global__ void k_gen_kv(uint64_t seed, int which, int L, int B, int Hkv, int d,
     const int p = (int)(r % npos); r /= npos;
     const int h = (int)(r % Hkv); r /= Hkv;
     const int b = (int)(r % B); r /= B;
-    const int l = (int)r;
+    const int l = l0 + (int)r;                  // layers [l0, l0 + L)
     const int pos = pos0 + p;
     const uint64_t key = row_key(seed, which == 0 ? TID_K : TID_V, l, b, h, pos);
     const float x = gauss(sm64(key + (uint64_t)dim));
@@ -91,7 +91,15 @@ extern "C" int kv_synth_kv(uint64_t seed, int which, int L, int B, int Hkv, int 
   const size_t total = (size_t)L * B * Hkv * npos * d;
   if (total == 0) return 0;
   k_gen_kv<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(seed, which, L, B, Hkv, d, pos0, npos, prompt_len,
-                                                            sink_size, sig_a, (uint16_t*)out);
+                                                            sink_size, sig_a, (uint16_t*)out, 0);
+  return (int)cudaGetLastError();
+}
+extern "C" int kv_synth_kv_layer(uint64_t seed, int which, int layer, int B, int Hkv, int d, int pos0, int npos,
+                                 int prompt_len, int sink_size, float sig_a, void* out, void* stream) {
+  const size_t total = (size_t)B * Hkv * npos * d;
+  if (total == 0) return 0;
+  k_gen_kv<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(seed, which, 1, B, Hkv, d, pos0, npos, prompt_len,
+                                                            sink_size, sig_a, (uint16_t*)out, layer);
   return (int)cudaGetLastError();
 }
 extern "C" int kv_synth_q(uint64_t seed, int t0, int T, int L, int B, int Hq, int Hkv, int d, void* out,

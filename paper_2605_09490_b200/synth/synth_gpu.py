@@ -19,6 +19,9 @@ def load():
         lib.kv_synth_q.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.c_void_p, C.c_void_p]
         lib.kv_synth_kv.restype = C.c_int
+        lib.kv_synth_kv_layer.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_void_p]
+        lib.kv_synth_kv_layer.restype = C.c_int
         lib.kv_synth_q.restype = C.c_int
         _lib = lib
     return _lib
@@ -38,6 +41,18 @@ def gen_kv(seed, which, L, B, Hkv, d, pos0, npos, prompt_len, sink_size, device,
                             float(sig_a), C.c_void_p(out.data_ptr()), _stream(stream))
     if rc:
         raise RuntimeError(f"kv_synth_kv failed: cuda error {rc}")
+    return out
+
+
+def gen_kv_layer(seed, which, layer, B, Hkv, d, pos0, npos, prompt_len, sink_size, device, sig_a=SIG_A_DEFAULT,
+                 stream=None):
+    """torch.bfloat16 [B][Hkv][npos][d]: layer `layer` of gen_kv's tensor (same bytes)."""
+    import torch
+    out = torch.empty((B, Hkv, npos, d), dtype=torch.bfloat16, device=device)
+    rc = load().kv_synth_kv_layer(seed, 0 if which == "k" else 1, layer, B, Hkv, d, pos0, npos, prompt_len,
+                                  sink_size, float(sig_a), C.c_void_p(out.data_ptr()), _stream(stream))
+    if rc:
+        raise RuntimeError(f"kv_synth_kv_layer failed: cuda error {rc}")
     return out
 
 

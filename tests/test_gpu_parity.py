@@ -115,6 +115,9 @@ def test_synth_gpu_matches_cpu():
         assert np.array_equal(g, c)
     g = SG.gen_q(9, 5, 3, 2, 2, 8, 2, 128, dev).view(torch.int16).cpu().numpy().view(np.uint16)
     assert np.array_equal(g, S.gen_q(9, 5, 3, 2, 2, 8, 2, 128))
+    full = SG.gen_kv(7, "k", 3, 2, 2, 64, 100, 40, 16, 4, dev)
+    for l in range(3):                          # one layer at a time: the same bytes
+        assert torch.equal(SG.gen_kv_layer(7, "k", l, 2, 2, 64, 100, 40, 16, 4, dev), full[l])
 
 
 # --------------------------------------------------------------------- tiny end to end
