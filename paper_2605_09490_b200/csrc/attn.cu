@@ -751,8 +751,11 @@ __global__ void k_set_ml(const DevView v, const int zslot, const float* __restri
 
 // Rank combine of sequence-shard partials (kv_tier_lse_combine): one thread per (row, 4 lanes
 // of d), ranks in order.
+// ml (optional): the score pass's (M, 1/L) ring slot [B*H_kv][16], written here instead of by a
+// separate k_set_ml (rows = b * H_q + h, kv head h / G)
 __global__ void k_lse_combine(const float* __restrict__ op, const float* __restrict__ lp, const int world,
-                              const int rows, const int d, float* __restrict__ oo, float* __restrict__ lo) {
+                              const int rows, const int d, float* __restrict__ oo, float* __restrict__ lo,
+                              float* __restrict__ ml, const int G) {
   const int d4 = d / 4;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)rows * d4) return;
@@ -776,13 +779,21 @@ __global__ void k_lse_combine(const float* __restrict__ op, const float* __restr
   if (j == 0) {
     lo[(size_t)row * 2] = M;
     lo[(size_t)row * 2 + 1] = L;
+    if (ml) {
+      const int unit = row / G, hh = row - unit * G;     // rows of one kv head are consecutive
+      float* m = ml + (size_t)unit * 16;
+      m[hh] = M;
+      m[8 + hh] = 1.0f / L;
+      if (hh == 0)
+        for (int x = G; x < 8; ++x) { m[x] = -INFINITY; m[8 + x] = 0.f; }
+    }
   }
 }
 
 cudaError_t launch_lse_combine(const float* op, const float* lp, int world, int rows, int d, float* oo, float* lo,
-                               cudaStream_t s) {
+                               cudaStream_t s, float* ml, int G) {
   const long long n = (long long)rows * (d / 4);
-  k_lse_combine<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(op, lp, world, rows, d, oo, lo);
+  k_lse_combine<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(op, lp, world, rows, d, oo, lo, ml, G);
   return cudaGetLastError();
 }
 

@@ -842,13 +842,11 @@ kv_tier_status kv_tier_lse_combine(const float* o_parts, const float* lse_parts,
                                                 reinterpret_cast<cudaStream_t>(stream)), "lse_combine");
 }
 
-kv_tier_status kv_tier_score_update_lse(kv_tier_ctx* ctx, const float* lse_global, void* stream) {
-  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
-  if (!lse_global || ((uintptr_t)lse_global & 7)) return fail(ctx, KV_TIER_E_INVAL, "lse_global must be an 8-B aligned device pointer");
-  if (ctx->lse_pending < 0) return fail(ctx, KV_TIER_E_STATE, "no decode_attention_lse awaits its score update");
+// ml_set: the slot's (M, 1/L) were already written (seq_step's combine kernel writes them)
+static kv_tier_status score_update_lse_impl(kv_tier_ctx* ctx, const float* lse_global, void* stream, bool ml_set) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int z = ctx->lse_pending;
-  cudaError_t e = launch_set_ml(ctx->v, z, lse_global, s);
+  cudaError_t e = ml_set ? cudaSuccess : launch_set_ml(ctx->v, z, lse_global, s);
   if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_merged[z], s);
   if (e == cudaSuccess) {
     if (ctx->zpend_n == 0) ctx->zpend_first = z;
@@ -857,6 +855,12 @@ kv_tier_status kv_tier_score_update_lse(kv_tier_ctx* ctx, const float* lse_globa
   }
   if (e == cudaSuccess) ctx->lse_pending = -1;
   return cuda_check(ctx, e, "score_update_lse");
+}
+kv_tier_status kv_tier_score_update_lse(kv_tier_ctx* ctx, const float* lse_global, void* stream) {
+  if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
+  if (!lse_global || ((uintptr_t)lse_global & 7)) return fail(ctx, KV_TIER_E_INVAL, "lse_global must be an 8-B aligned device pointer");
+  if (ctx->lse_pending < 0) return fail(ctx, KV_TIER_E_STATE, "no decode_attention_lse awaits its score update");
+  return score_update_lse_impl(ctx, lse_global, stream, false);
 }
 
 kv_tier_status kv_tier_visible_count(const kv_tier_ctx* ctx, int32_t* n_vis) {
@@ -1045,19 +1049,31 @@ static kv_tier_status seq_step(kv_tier_ctx* ctx, const void* q, const void* k_ne
   if (v.stream_mode)
     for (int l = 0; l < std::min(2, v.L) && !st; ++l) st = kv_tier_prefetch(ctx, l, side);
   for (int l = 0; l < v.L && !st; ++l) {
-    st = decode_attention_impl(ctx, l, qb + l * qs * 2, kb + l * ks * 2, vb + l * ks * 2, o_send, 1, stream, 0, l_send);
+    // PDL: the decode's prologue (barriers, first K/V tiles) overlaps the previous layer's combine;
+    // q and the new rows are read after griddepcontrol.wait
+    st = decode_attention_impl(ctx, l, qb + l * qs * 2, kb + l * ks * 2, vb + l * ks * 2, o_send, 1, stream,
+                               l > 0 && !v.stream_mode ? 1 : 0, l_send);
     if (st) break;
-    const NcclApi& nc = nccl_api();
-    ncclResult_t r = nc.group_start();
-    if (r == ncclSuccess) r = nc.all_gather(o_send, o_recv, rows * v.D, ncclFloat32, ctx->comm, s);
-    if (r == ncclSuccess) r = nc.all_gather(l_send, l_recv, rows * 2, ncclFloat32, ctx->comm, s);
-    const ncclResult_t r2 = nc.group_end();
-    if (r == ncclSuccess) r = r2;
-    if (r != ncclSuccess) return fail(ctx, KV_TIER_E_NCCL, "layer %d all-gather: %s", l, nc.error_string(r));
+    const float* o_src = o_recv;
+    const float* l_src = l_recv;
+    if (W == 1) {                            // a one-rank all-gather is the identity: combine in place
+      o_src = o_send;
+      l_src = l_send;
+    } else {
+      const NcclApi& nc = nccl_api();
+      ncclResult_t r = nc.group_start();
+      if (r == ncclSuccess) r = nc.all_gather(o_send, o_recv, rows * v.D, ncclFloat32, ctx->comm, s);
+      if (r == ncclSuccess) r = nc.all_gather(l_send, l_recv, rows * 2, ncclFloat32, ctx->comm, s);
+      const ncclResult_t r2 = nc.group_end();
+      if (r == ncclSuccess) r = r2;
+      if (r != ncclSuccess) return fail(ctx, KV_TIER_E_NCCL, "layer %d all-gather: %s", l, nc.error_string(r));
+    }
     float* lse_l = ctx->x_lse + (size_t)l * rows * 2;
-    st = cuda_check(ctx, launch_lse_combine(o_recv, l_recv, (int)W, (int)rows, v.D, ob + (size_t)l * qs, lse_l, s),
-                    "lse_combine");
-    if (!st) st = kv_tier_score_update_lse(ctx, lse_l, stream);
+    // the combine also writes the pending score slot's (M, 1/L): no separate set_ml launch
+    float* mlz = v.ml + (size_t)ctx->lse_pending * v.B * v.Hkv * 16;
+    st = cuda_check(ctx, launch_lse_combine(o_src, l_src, (int)W, (int)rows, v.D, ob + (size_t)l * qs, lse_l, s,
+                                            mlz, v.G), "lse_combine");
+    if (!st) st = score_update_lse_impl(ctx, lse_l, stream, true);
     if (!st && v.stream_mode && l + 2 < v.L) st = kv_tier_prefetch(ctx, l + 2, side);
   }
   if (st) return st;
