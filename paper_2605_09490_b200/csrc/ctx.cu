@@ -1054,20 +1054,16 @@ static kv_tier_status seq_step(kv_tier_ctx* ctx, const void* q, const void* k_ne
     st = decode_attention_impl(ctx, l, qb + l * qs * 2, kb + l * ks * 2, vb + l * ks * 2, o_send, 1, stream,
                                l > 0 && !v.stream_mode ? 1 : 0, l_send);
     if (st) break;
+    // (also at world 1, where it is a copy: the one-GPU tests then run the multi-rank code path)
+    const NcclApi& nc = nccl_api();
+    ncclResult_t r = nc.group_start();
+    if (r == ncclSuccess) r = nc.all_gather(o_send, o_recv, rows * v.D, ncclFloat32, ctx->comm, s);
+    if (r == ncclSuccess) r = nc.all_gather(l_send, l_recv, rows * 2, ncclFloat32, ctx->comm, s);
+    const ncclResult_t r2 = nc.group_end();
+    if (r == ncclSuccess) r = r2;
+    if (r != ncclSuccess) return fail(ctx, KV_TIER_E_NCCL, "layer %d all-gather: %s", l, nc.error_string(r));
     const float* o_src = o_recv;
     const float* l_src = l_recv;
-    if (W == 1) {                            // a one-rank all-gather is the identity: combine in place
-      o_src = o_send;
-      l_src = l_send;
-    } else {
-      const NcclApi& nc = nccl_api();
-      ncclResult_t r = nc.group_start();
-      if (r == ncclSuccess) r = nc.all_gather(o_send, o_recv, rows * v.D, ncclFloat32, ctx->comm, s);
-      if (r == ncclSuccess) r = nc.all_gather(l_send, l_recv, rows * 2, ncclFloat32, ctx->comm, s);
-      const ncclResult_t r2 = nc.group_end();
-      if (r == ncclSuccess) r = r2;
-      if (r != ncclSuccess) return fail(ctx, KV_TIER_E_NCCL, "layer %d all-gather: %s", l, nc.error_string(r));
-    }
     float* lse_l = ctx->x_lse + (size_t)l * rows * 2;
     // the combine also writes the pending score slot's (M, 1/L): no separate set_ml launch
     float* mlz = v.ml + (size_t)ctx->lse_pending * v.B * v.Hkv * 16;
