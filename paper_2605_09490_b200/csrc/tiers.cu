@@ -944,11 +944,15 @@ cudaError_t launch_offload_rows(const DevView& v, cudaStream_t s) {
 // every moved row of the event: one cooperative launch, as many CTAs as are co-resident (<= 2 per SM)
 template <int D>
 static cudaError_t migrate_rows_t(const DevView& v, cudaStream_t s) {
-  static int grid = 0;
-  if (grid == 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  constexpr int MAXDEV = 64;
+  static int grids[MAXDEV] = {};                 // per device: co-resident CTAs (<= 2 per SM)
+  int dev = 0;
+  cudaError_t e0 = cudaGetDevice(&dev);
+  if (e0 != cudaSuccess) return e0;
+  int& grid = grids[dev < MAXDEV ? dev : MAXDEV - 1];
+  if (grid == 0 || dev >= MAXDEV) {
+    int sms = 0, per = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_migrate_rows<D>, 256, 0);
     if (e != cudaSuccess) return e;
     grid = sms * std::max(1, std::min(per, 2));
