@@ -127,7 +127,9 @@ typedef enum { KV_TIER_POLICY_HIERARCHY = 0, KV_TIER_POLICY_STREAMING = 1, KV_TI
  *              R_i = rho_i as REDUNDANCY; Z = fp32(0.07f * I) - fp32(0.93f * rho) (AMB-33).
  *   REDUNDANCY / COMBINED / RKV: request or KV-head sharding without classify_gathered (E_INVAL
  *   for sequence sharding; kv_tier_classify_gathered returns E_STATE).  WINDOW / RKV: no
- *   sequence sharding (E_INVAL), no classify_gathered (E_STATE). */
+ *   classify_gathered (E_STATE); WINDOW on sequence shards only with the library's communicator
+ *   (kv_tier_init E_INVAL without an nccl_unique_id): its kv_tier_classify all-gathers every
+ *   shard's S_part and snapshot and pools over the global cache order of the tier array. */
 typedef enum { KV_TIER_SCORER_ATTENTION = 0, KV_TIER_SCORER_VATP = 1, KV_TIER_SCORER_REDUNDANCY = 2,
                KV_TIER_SCORER_COMBINED = 3, KV_TIER_SCORER_WINDOW = 4, KV_TIER_SCORER_RKV = 5 } kv_tier_scorer;
 

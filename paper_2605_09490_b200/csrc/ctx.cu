@@ -113,6 +113,7 @@ struct kv_tier_ctx {
   float* x_recv = nullptr;                 // [W][B][H_q][d] o parts, then [W][B][H_q][2] lse parts
   float* x_lse = nullptr;                  // [L][B][H_q][2] global (M, L) per layer
   float* x_scores = nullptr;               // [W][B][H_kv][N_max] all-gathered S_part (events)
+  float* x_snaps = nullptr;                // [W][B][H_kv][N_max] all-gathered S_part snapshots (windowed scorers)
   std::string err;
 };
 
@@ -194,8 +195,7 @@ kv_tier_status validate(const kv_tier_config* c) {
     return fail(nullptr, KV_TIER_E_INVAL, "policy must be a kv_tier_policy");
   if (c->scorer < KV_TIER_SCORER_ATTENTION || c->scorer > KV_TIER_SCORER_RKV)
     return fail(nullptr, KV_TIER_E_INVAL, "scorer must be a kv_tier_scorer");
-  if (scorer_uses_window(c->scorer) && c->shard == KV_TIER_SHARD_SEQUENCE && c->world > 1)
-    return fail(nullptr, KV_TIER_E_INVAL, "windowed scorers pool over the whole cache order: not with sequence sharding");
+
   if (scorer_uses_window(c->scorer) && c->manage_interval < 1)
     return fail(nullptr, KV_TIER_E_INVAL, "windowed scorers need manage_interval >= 1 (the observation window follows it)");
   if (scorer_uses_red(c->scorer) && c->shard == KV_TIER_SHARD_SEQUENCE && c->world > 1)
@@ -352,7 +352,7 @@ Layout make_layout(const kv_tier_config& c, int cap0, int cap1, int cap2) {
   L.off_red = take(scorer_uses_red(c.scorer) ? BH * N * 4 : 0);          // redundancy partials R_part
   L.off_lastk = take(scorer_uses_red(c.scorer) ? LBH * D * 2 : 0);       // previous key per (layer, kv head)
   L.off_snap = take(scorer_uses_window(c.scorer) ? BH * N * 4 : 0);      // windowed: S_part snapshot
-  L.off_pool = take(scorer_uses_window(c.scorer) ? B * N * 4 : 0);       // windowed: pooled scores
+  L.off_pool = take(scorer_uses_window(c.scorer) ? 2 * B * N * 4 : 0);   // windowed: compacted scores + indices
   L.b_scores = o - s0; s0 = o;
   for (int i = 0; i < 2; ++i) {
     L.off_idx[i][0] = take(B * cap0 * 4);
@@ -419,6 +419,9 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     return fail(nullptr, KV_TIER_E_INVAL, "an nccl_unique_id is only used by sequence sharding (the other splits have no collective on the step)");
   if (nccl_unique_id && !cfg->out_fp32)
     return fail(nullptr, KV_TIER_E_INVAL, "sequence sharding with a communicator combines o in fp32: out_fp32 must be 1");
+  if (scorer_uses_window(cfg->scorer) && cfg->shard == KV_TIER_SHARD_SEQUENCE && cfg->world > 1 && !nccl_unique_id)
+    return fail(nullptr, KV_TIER_E_INVAL, "windowed scorers on sequence shards need the library's communicator "
+                "(their classify all-gathers every shard's S_part and snapshot)");
   if (nccl_unique_id && !nccl_api().ok)
     return fail(nullptr, KV_TIER_E_NCCL, "libnccl.so.2 not found in the process or on the loader path");
   if (((uintptr_t)buf->device_arena) & 255) return fail(nullptr, KV_TIER_E_INVAL, "device_arena must be 256-B aligned");
@@ -592,6 +595,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     if (e == cudaSuccess) e = cudaMalloc(&ctx->x_recv, W * rows * (v.D + 2) * 4);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->x_lse, (size_t)v.L * rows * 2 * 4);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->x_scores, W * v.B * v.Hkv * (size_t)v.Nmax * 4);
+    if (e == cudaSuccess && v.snap) e = cudaMalloc(&ctx->x_snaps, W * v.B * v.Hkv * (size_t)v.Nmax * 4);
     if (e != cudaSuccess) {
       kv_tier_destroy(ctx);
       return fail(nullptr, KV_TIER_E_OOM, "sequence-shard exchange buffers: %s", cudaGetErrorString(e));
@@ -641,7 +645,7 @@ kv_tier_status kv_tier_destroy(kv_tier_ctx* ctx) {
   if (ctx->d1_parts) cudaFree(ctx->d1_parts);
   if (ctx->ev_q) cudaEventDestroy(ctx->ev_q);
   if (ctx->comm) nccl_api().comm_destroy(ctx->comm);
-  for (float* p : {ctx->x_send, ctx->x_recv, ctx->x_lse, ctx->x_scores})
+  for (float* p : {ctx->x_send, ctx->x_recv, ctx->x_lse, ctx->x_scores, ctx->x_snaps})
     if (p) cudaFree(p);
   delete ctx;
   return KV_TIER_OK;
@@ -920,7 +924,8 @@ kv_tier_status kv_tier_end_step(kv_tier_ctx* ctx, void* stream) {
   return KV_TIER_OK;
 }
 
-static kv_tier_status classify_impl(kv_tier_ctx* ctx, const float* Sx, int parts, void* stream);
+static kv_tier_status classify_impl(kv_tier_ctx* ctx, const float* Sx, int parts, void* stream,
+                                    const float* snapx = nullptr);
 
 kv_tier_status kv_tier_classify(kv_tier_ctx* ctx, void* stream) {
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
@@ -928,10 +933,17 @@ kv_tier_status kv_tier_classify(kv_tier_ctx* ctx, void* stream) {
     // sequence shards: every rank classifies the sum of all ranks' S_part (one owner per
     // position, so the sum is exact), all-gathered here over the library's communicator
     const DevView& v = ctx->v;
-    const ncclResult_t r = nccl_api().all_gather(v.S, ctx->x_scores, (size_t)v.B * v.Hkv * v.Nmax, ncclFloat32,
-                                                 ctx->comm, reinterpret_cast<cudaStream_t>(stream));
-    if (r != ncclSuccess) return fail(ctx, KV_TIER_E_NCCL, "all-gather of S_part: %s", nccl_api().error_string(r));
-    return classify_impl(ctx, ctx->x_scores, ctx->cfg.world, stream);
+    const size_t cnt = (size_t)v.B * v.Hkv * v.Nmax;
+    const NcclApi& nc = nccl_api();
+    ncclResult_t r = nc.group_start();
+    if (r == ncclSuccess)
+      r = nc.all_gather(v.S, ctx->x_scores, cnt, ncclFloat32, ctx->comm, reinterpret_cast<cudaStream_t>(stream));
+    if (r == ncclSuccess && v.snap)            // windowed scorers: every shard's snapshot too (AMB-32)
+      r = nc.all_gather(v.snap, ctx->x_snaps, cnt, ncclFloat32, ctx->comm, reinterpret_cast<cudaStream_t>(stream));
+    const ncclResult_t r2 = nc.group_end();
+    if (r == ncclSuccess) r = r2;
+    if (r != ncclSuccess) return fail(ctx, KV_TIER_E_NCCL, "all-gather of S_part: %s", nc.error_string(r));
+    return classify_impl(ctx, ctx->x_scores, ctx->cfg.world, stream, v.snap ? ctx->x_snaps : nullptr);
   }
   if ((ctx->cfg.shard == KV_TIER_SHARD_KVHEAD || ctx->cfg.shard == KV_TIER_SHARD_SEQUENCE) && ctx->cfg.world > 1)
     return fail(ctx, KV_TIER_E_STATE, "KV-head sharding: classify needs every shard's scores (kv_tier_classify_gathered)");
@@ -956,7 +968,7 @@ kv_tier_status kv_tier_scores_device(kv_tier_ctx* ctx, void** ptr, size_t* bytes
   return KV_TIER_OK;
 }
 
-static kv_tier_status classify_impl(kv_tier_ctx* ctx, const float* Sx, int parts, void* stream) {
+static kv_tier_status classify_impl(kv_tier_ctx* ctx, const float* Sx, int parts, void* stream, const float* snapx) {
   if (!ctx->loaded) return fail(ctx, KV_TIER_E_STATE, "no prefix loaded");
   if (ctx->step_open) return fail(ctx, KV_TIER_E_STATE, "classify inside a step (call after the last layer's score update)");
   const kv_tier_config& c = ctx->cfg;
@@ -973,7 +985,7 @@ static kv_tier_status classify_impl(kv_tier_ctx* ctx, const float* Sx, int parts
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
   if (ctx->offload_pending) e = cudaStreamWaitEvent(s, ctx->ev_offload_done, 0);
-  if (e == cudaSuccess) e = launch_classify(ctx->v, Sx, parts, s);
+  if (e == cudaSuccess) e = launch_classify(ctx->v, Sx, parts, s, snapx);
   kv_tier_status st = cuda_check(ctx, e, "classify");
   if (st) return st;
   ctx->pend[0] = p0; ctx->pend[1] = p1; ctx->pend[2] = p2; ctx->pend[3] = p3;

@@ -48,7 +48,7 @@ struct DevView {
   float* red;           // redundancy / combined: [B][Hkv][Nmax] fp32 R_part = sum_l cos(k_i, k_{i-1})
   uint16_t* lastk;      // redundancy / combined: [L][B][Hkv][D] bf16 key of the last appended token
   float* snap;          // windowed / R-KV: [B][Hkv][Nmax] S_part at the start of the observation window
-  float* pool;          // windowed / R-KV: [B][Nmax] classify scratch (max-pooled scores)
+  float* pool;          // windowed / R-KV: classify scratch [B][Nmax] compacted scores + [B][Nmax] int indices
   int interval;         // Delta (kv_tier_config::manage_interval; binding for windowed scorers)
   int* zlayer;          // [ZRING] layer of the launch that filled each logit slot
   int zring;            // logit ring slots in use (2..ZRING): the ring stays inside the L2 carve-out
@@ -272,7 +272,8 @@ cudaError_t launch_lse_combine(const float* op, const float* lp, int world, int 
 cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_t s);
 cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s);
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);
-cudaError_t launch_classify(const DevView& v, const float* Sx, int parts, cudaStream_t s);
+cudaError_t launch_classify(const DevView& v, const float* Sx, int parts, cudaStream_t s,
+                            const float* snapx = nullptr);
 cudaError_t launch_plan(const DevView& v, cudaStream_t s);
 cudaError_t launch_migrate_rows(const DevView& v, cudaStream_t s);
 cudaError_t launch_offload_rows(const DevView& v, cudaStream_t s);

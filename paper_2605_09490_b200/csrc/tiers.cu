@@ -284,7 +284,10 @@ __device__ __forceinline__ unsigned ord_bits(float f) {
 
 // Sx: per-kv-head partial scores [parts][B][H_kv][N_max] -- the ctx's own S_part (parts = 1)
 // or the all-gathered S_part of `parts` KV-head shards (global kv head = part * H_kv + g).
-__global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const float* __restrict__ Sx, const int parts) {
+// snapx (windowed scorers): the S_part snapshots in Sx's layout (the all-gathered ones of every
+// sequence shard), or the ctx's own (parts = 1)
+__global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const float* __restrict__ Sx, const int parts,
+                                                          const float* __restrict__ snapx) {
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int cur = v.st->cur, nxt = cur ^ 1, n = v.st->n;
   const uint8_t* told = v.tier[cur] + (size_t)b * v.Nmax;
@@ -316,10 +319,12 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
       const int part = gg / v.Hkv, g = gg - part * v.Hkv;
       s = __fadd_rn(s, Sx[(((size_t)part * v.B + b) * v.Hkv + g) * v.Nmax + pos]);
     }
-    if (win) {                             // W_i = fp32(sum_g S) - fp32(sum_g S_snap)
-      const float* sn = v.snap + (size_t)b * v.Hkv * v.Nmax + pos;
-      float s0 = sn[0];
-      for (int g = 1; g < v.Hkv; ++g) s0 = __fadd_rn(s0, sn[(size_t)g * v.Nmax]);
+    if (win) {                             // W_i = fp32(sum_g S) - fp32(sum_g S_snap), same summation order
+      float s0 = snapx[((size_t)b * v.Hkv) * v.Nmax + pos];
+      for (int gg = 1; gg < parts * v.Hkv; ++gg) {
+        const int part = gg / v.Hkv, g = gg - part * v.Hkv;
+        s0 = __fadd_rn(s0, snapx[(((size_t)part * v.B + b) * v.Hkv + g) * v.Nmax + pos]);
+      }
       s = __fsub_rn(s, s0);
     }
     fS[pos] = s;
@@ -343,24 +348,47 @@ __global__ void __launch_bounds__(CLS_THREADS) k_classify(const DevView v, const
   if (bad) atomicOr(&v.st->err, 1);
   __syncthreads();
   if (win) {
-    // max-pool (kernel 7, stride 1) over the non-T3 positions in ascending order: the visible
-    // list of the last event followed by the positions appended since (all T0), P:976 / AMB-32
-    const int nve = v.cnt[cur][b * CNT_STRIDE + 4];
-    const int nvis = nve + (n - v.st->n_event);
-    const int* vl = v.idxvis[cur] + (size_t)b * v.Nmax;
-    const int ne = v.st->n_event;
-    float* pl = v.pool + (size_t)b * v.Nmax;
-    auto vpos = [&](int j) { return j < nve ? vl[j] : ne + (j - nve); };
-    for (int j = tid; j < nvis; j += CLS_THREADS) {
-      float m = fS[vpos(j)];
-      for (int x = max(0, j - RKV_HALF_POOL); x <= min(nvis - 1, j + RKV_HALF_POOL); ++x) m = fmaxf(m, fS[vpos(x)]);
-      pl[vpos(j)] = m;
-    }
+    // max-pool (kernel 7, stride 1) over the non-T3 positions in ascending order (P:976 / AMB-32).
+    // The order is built from the tier array, which every sequence shard holds for all positions:
+    // compact W into pool[0..nvis) (prefix sums over the block), keep each position's index.
+    float* cw = v.pool + (size_t)b * v.Nmax;
+    int* cix = reinterpret_cast<int*>(v.pool + (size_t)v.B * v.Nmax) + (size_t)b * v.Nmax;
+    if (tid == 0) s_base[0] = 0;
     __syncthreads();
+    for (int base = 0; base < n; base += CLS_THREADS) {
+      const int pos = base + tid;
+      const bool f = pos < n && told[pos] != T3;
+      const unsigned m = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) s_wsum[0][w] = __popc(m);
+      __syncthreads();
+      if (w == 0) {
+        const int x = s_wsum[0][lane];
+        int inc = x;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, inc, off);
+          if (lane >= off) inc += y;
+        }
+        s_wsum[0][lane] = inc - x;
+        if (lane == 31) s_tot[0] = inc;
+      }
+      __syncthreads();
+      if (f) {
+        const int k = s_base[0] + s_wsum[0][w] + __popc(m & ((1u << lane) - 1u));
+        cw[k] = fS[pos];
+        cix[pos] = k;
+      }
+      __syncthreads();
+      if (tid == 0) s_base[0] += s_tot[0];
+      __syncthreads();
+    }
+    const int nvis = s_base[0];
     unsigned pmax = 0u;
-    for (int j = tid; j < nvis; j += CLS_THREADS) {
-      const int pos = vpos(j);
-      const float m = pl[pos];
+    for (int pos = tid; pos < n; pos += CLS_THREADS) {
+      if (told[pos] == T3) continue;
+      const int k = cix[pos];
+      float m = cw[k];
+      for (int x = max(0, k - RKV_HALF_POOL); x <= min(nvis - 1, k + RKV_HALF_POOL); ++x) m = fmaxf(m, cw[x]);
       fS[pos] = m;
       if (pos >= prot_lo && pos < prot_hi) pmax = max(pmax, __float_as_uint(m));
     }
@@ -883,8 +911,8 @@ cudaError_t launch_score_update(const DevView& v, int layer, const float* probs,
   k_score_update<<<grid, 256, 0, s>>>(v, layer, probs);
   return cudaGetLastError();
 }
-cudaError_t launch_classify(const DevView& v, const float* Sx, int parts, cudaStream_t s) {
-  k_classify<<<v.B, CLS_THREADS, 0, s>>>(v, Sx ? Sx : v.S, Sx ? parts : 1);
+cudaError_t launch_classify(const DevView& v, const float* Sx, int parts, cudaStream_t s, const float* snapx) {
+  k_classify<<<v.B, CLS_THREADS, 0, s>>>(v, Sx ? Sx : v.S, Sx ? parts : 1, snapx ? snapx : v.snap);
   return cudaGetLastError();
 }
 cudaError_t launch_plan(const DevView& v, cudaStream_t s) {

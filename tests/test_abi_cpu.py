@@ -137,7 +137,7 @@ def test_redundancy_scorers_refused_under_sequence_sharding():
     # neighbour cosine needs position i-1, which another sequence shard owns (AMB-31)
     # the windowed scorers pool over the whole cache order (AMB-32): also refused
     for sc, want in ((kt.SCORER_REDUNDANCY, -1), (kt.SCORER_COMBINED, -1), (kt.SCORER_VATP, 0),
-                     (kt.SCORER_WINDOW, -1), (kt.SCORER_RKV, -1)):
+                     (kt.SCORER_WINDOW, 0), (kt.SCORER_RKV, -1)):
         cfg = kt.make_config(2, 1, 4, 2, 64, 300, 16, scorer=sc, shard=kt.SHARD_SEQUENCE, world=2, rank=0)
         s = kt.Sizes()
         assert kt.load().kv_tier_query_sizes(C.byref(cfg), C.byref(s)) == want
@@ -156,15 +156,15 @@ def test_redundancy_scorers_size_their_buffers():
 
 
 def test_window_scorers_size_their_buffers():
-    # windowed: the snapshot [B][H_kv][N] + the pool scratch [B][N] fp32; R-KV adds R-KV's
-    # redundancy buffers on top (R_part + previous keys)
+    # windowed: the snapshot [B][H_kv][N] + the pool scratch [B][N] fp32 + [B][N] int32; R-KV adds
+    # R-KV's redundancy buffers on top (R_part + previous keys)
     sz = {}
     for sc in (kt.SCORER_ATTENTION, kt.SCORER_WINDOW, kt.SCORER_RKV, kt.SCORER_REDUNDANCY):
         cfg = kt.make_config(2, 3, 4, 2, 64, 300, 16, scorer=sc)
         s = kt.Sizes()
         assert kt.load().kv_tier_query_sizes(C.byref(cfg), C.byref(s)) == 0
         sz[sc] = s.device_arena
-    win = 2 * 2 * 300 * 4 + 2 * 300 * 4
+    win = 2 * 2 * 300 * 4 + 2 * 2 * 300 * 4
     assert win <= sz[kt.SCORER_WINDOW] - sz[kt.SCORER_ATTENTION] <= win + 2 * 256
     red = sz[kt.SCORER_REDUNDANCY] - sz[kt.SCORER_ATTENTION]
     assert win + red <= sz[kt.SCORER_RKV] - sz[kt.SCORER_ATTENTION] <= win + red + 4 * 256
@@ -186,6 +186,15 @@ def test_nccl_unique_id_and_init_guards():
                dict(shard=kt.SHARD_SEQUENCE, world=2, out_fp32=0)):
         cfg = kt.make_config(2, 1, 4, 2, 64, 300, 16, **kw)
         assert lib.kv_tier_init(C.byref(cfg), C.byref(buf), idb, C.byref(h)) == -1
+
+
+def test_window_scorer_on_sequence_shards_needs_the_communicator():
+    # WINDOW pools over the global cache order: a sequence shard without the library's
+    # communicator cannot see the other shards' scores, so kv_tier_init refuses it (before any GPU use)
+    cfg = kt.make_config(2, 1, 4, 2, 64, 300, 16, scorer=kt.SCORER_WINDOW, shard=kt.SHARD_SEQUENCE, world=2, rank=0)
+    buf = kt.Buffers(device_arena=C.c_void_p(1 << 20))
+    h = C.c_void_p()
+    assert kt.load().kv_tier_init(C.byref(cfg), C.byref(buf), None, C.byref(h)) == -1
 
 
 def test_capture_entry_points_reject_null_ctx():

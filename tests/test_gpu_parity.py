@@ -524,15 +524,16 @@ def test_sequence_shard_refuses_plain_paths():
     run.close()
 
 
-@pytest.mark.parametrize("graph,staging", [(True, kt.STAGING_ALL), (False, kt.STAGING_ALL), (True, 0)])
-def test_sequence_shard_library_communicator(graph, staging):
+@pytest.mark.parametrize("graph,staging,scorer", [(True, kt.STAGING_ALL, 0), (False, kt.STAGING_ALL, 0), (True, 0, 0),
+                                                  (True, kt.STAGING_ALL, kt.SCORER_WINDOW)])
+def test_sequence_shard_library_communicator(graph, staging, scorer):
     # kv_tier_init with an nccl_unique_id: kv_tier_step runs every layer's all-gather of (o, m, l)
     # on the library's NCCL communicator, the LSE combine and the rescaled score update -- the
     # whole step captured as ONE CUDA graph -- and kv_tier_classify all-gathers S_part itself.
     # world = 1 (one GPU): the collective is the identity, the path and its state machine are
     # the multi-rank ones
     w = H.workload("tiny", B=2, L=3, Hq=8, Hkv=2, d=64, N=400, P=16, interval=8, steps=26,
-                   hbm_bp=4000, evict_bp=800, t2_bp=3000, staging=staging)
+                   hbm_bp=4000, evict_bp=800, t2_bp=3000, staging=staging, scorer=scorer)
     _run_pair(w, graph=graph, check_every=4, shard=kt.SHARD_SEQUENCE, rank=0, world=1,
               nccl_id=kt.nccl_unique_id())
 
