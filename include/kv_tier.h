@@ -125,9 +125,11 @@ typedef enum { KV_TIER_POLICY_HIERARCHY = 0, KV_TIER_POLICY_STREAMING = 1, KV_TI
  *   RKV        R-KV's Z = lambda I - (1 - lambda) R (App. E), lambda = 0.07:
  *              I_i = fp32(Wpool_i / max of Wpool over the live set) (0 if that max is 0),
  *              R_i = rho_i as REDUNDANCY; Z = fp32(0.07f * I) - fp32(0.93f * rho) (AMB-33).
- *   REDUNDANCY / COMBINED / RKV: request or KV-head sharding without classify_gathered (E_INVAL
- *   for sequence sharding; kv_tier_classify_gathered returns E_STATE).  WINDOW / RKV: no
- *   classify_gathered (E_STATE); WINDOW on sequence shards only with the library's communicator
+ *   REDUNDANCY / COMBINED / RKV: every sequence shard appends every new key to its previous-key
+ *   state and R_part covers all positions on every shard (identical copies), so sequence shards
+ *   classify from their own R_part (also through kv_tier_classify_gathered); under KV-head
+ *   sharding R_part is per shard and kv_tier_classify_gathered returns E_STATE.  WINDOW / RKV: no
+ *   classify_gathered (E_STATE); on sequence shards only with the library's communicator
  *   (kv_tier_init E_INVAL without an nccl_unique_id): its kv_tier_classify all-gathers every
  *   shard's S_part and snapshot and pools over the global cache order of the tier array. */
 typedef enum { KV_TIER_SCORER_ATTENTION = 0, KV_TIER_SCORER_VATP = 1, KV_TIER_SCORER_REDUNDANCY = 2,

@@ -246,6 +246,10 @@ __global__ void __launch_bounds__((NW + 2) * 32, (NW == 4 ? 2 : 1))
     if (r == 0 && !sg.nn) {     // sequence shard without the new token: neutral partial C
       float* part = v.part + ((size_t)unit * (C + 1) + C) * v.part_stride;
       for (int e = lane; e < 16 + G * D; e += 32) part[e] = e < 8 ? -INFINITY : 0.f;
+      // redundancy: every shard tracks the globally previous key and R_part of every position
+      // (identical on all shards, so each classifies from its own copy)
+      if (v.red && knew) redund_append(v, layer, unit, v.st->n - 1,
+                                       reinterpret_cast<const uint16_t*>(knew) + ((size_t)b * v.Hkv + g) * D);
     }
     return;
   }

@@ -198,8 +198,7 @@ kv_tier_status validate(const kv_tier_config* c) {
 
   if (scorer_uses_window(c->scorer) && c->manage_interval < 1)
     return fail(nullptr, KV_TIER_E_INVAL, "windowed scorers need manage_interval >= 1 (the observation window follows it)");
-  if (scorer_uses_red(c->scorer) && c->shard == KV_TIER_SHARD_SEQUENCE && c->world > 1)
-    return fail(nullptr, KV_TIER_E_INVAL, "redundancy scorers need each position's predecessor: not with sequence sharding");
+
   if ((c->policy == KV_TIER_POLICY_H2O || c->policy == KV_TIER_POLICY_RANDOM) && c->budget < 1)
     return fail(nullptr, KV_TIER_E_INVAL, "H2O / RANDOM need budget >= 1 kept tokens per request");
   return KV_TIER_OK;
@@ -954,7 +953,7 @@ kv_tier_status kv_tier_classify_gathered(kv_tier_ctx* ctx, const float* S_all, i
   if (!ctx) return fail(nullptr, KV_TIER_E_INVAL, "null ctx");
   if (!S_all || parts < 1) return fail(ctx, KV_TIER_E_INVAL, "S_all must be a device pointer and parts >= 1");
   if (((uintptr_t)S_all) & 3) return fail(ctx, KV_TIER_E_INVAL, "S_all must be 4-B aligned");
-  if (scorer_uses_red(ctx->v.scorer))
+  if (scorer_uses_red(ctx->v.scorer) && ctx->v.seq_w <= 1)   // KV-head shards: R_part is per shard
     return fail(ctx, KV_TIER_E_STATE, "redundancy scorers classify from the ctx's own R_part (kv_tier_classify)");
   if (scorer_uses_window(ctx->v.scorer))
     return fail(ctx, KV_TIER_E_STATE, "windowed scorers classify from the ctx's own S_part snapshot (kv_tier_classify)");

@@ -60,6 +60,8 @@ __global__ void k_append(const DevView v, const int layer, const uint16_t* __res
   const int unit = blockIdx.x;               // b * Hkv + g
   const int b = unit / v.Hkv, g = unit % v.Hkv;
   const int cur = v.st->cur;
+  if (v.red && threadIdx.x >= 32 && threadIdx.x < 64)   // redundancy: cos with the previous key (every shard)
+    redund_append(v, layer, unit, v.st->n - 1, k + (size_t)unit * v.D);
   if (!v.st->nn) return;                     // another sequence shard holds the new token
   const int row = v.cnt[cur][b * CNT_STRIDE + 0] - 1;
   const size_t dst = (grp_of(v, layer, b, g) * v.cap0 + row) * v.D;
@@ -70,8 +72,6 @@ __global__ void k_append(const DevView v, const int layer, const uint16_t* __res
     K[dst + swz_off(row, e, v.D)] = k[(size_t)unit * v.D + e];
     V[dst + swz_off(row, e, v.D)] = vv[(size_t)unit * v.D + e];
   }
-  if (v.red && threadIdx.x >= 32 && threadIdx.x < 64)   // redundancy: cos with the previous key
-    redund_append(v, layer, unit, v.st->n - 1, k + (size_t)unit * v.D);
   if (scorer_uses_vnorm(v.scorer) && threadIdx.x < 32) {   // VATP: V-row norm of the appended token
     float ss = 0.f;
     for (int e = threadIdx.x; e < v.D; e += 32) {

@@ -133,11 +133,11 @@ def test_policy_and_scorer_validation(field, value):
     assert kt.load().kv_tier_query_sizes(C.byref(cfg), C.byref(s)) == -1
 
 
-def test_redundancy_scorers_refused_under_sequence_sharding():
-    # neighbour cosine needs position i-1, which another sequence shard owns (AMB-31)
-    # the windowed scorers pool over the whole cache order (AMB-32): also refused
-    for sc, want in ((kt.SCORER_REDUNDANCY, -1), (kt.SCORER_COMBINED, -1), (kt.SCORER_VATP, 0),
-                     (kt.SCORER_WINDOW, 0), (kt.SCORER_RKV, -1)):
+def test_scorers_accepted_under_sequence_sharding():
+    # every shard tracks the global previous key (R_part complete on each): accepted; the windowed
+    # scorers are checked at kv_tier_init (they need the library's communicator)
+    for sc, want in ((kt.SCORER_REDUNDANCY, 0), (kt.SCORER_COMBINED, 0), (kt.SCORER_VATP, 0),
+                     (kt.SCORER_WINDOW, 0), (kt.SCORER_RKV, 0)):
         cfg = kt.make_config(2, 1, 4, 2, 64, 300, 16, scorer=sc, shard=kt.SHARD_SEQUENCE, world=2, rank=0)
         s = kt.Sizes()
         assert kt.load().kv_tier_query_sizes(C.byref(cfg), C.byref(s)) == want
@@ -191,10 +191,11 @@ def test_nccl_unique_id_and_init_guards():
 def test_window_scorer_on_sequence_shards_needs_the_communicator():
     # WINDOW pools over the global cache order: a sequence shard without the library's
     # communicator cannot see the other shards' scores, so kv_tier_init refuses it (before any GPU use)
-    cfg = kt.make_config(2, 1, 4, 2, 64, 300, 16, scorer=kt.SCORER_WINDOW, shard=kt.SHARD_SEQUENCE, world=2, rank=0)
-    buf = kt.Buffers(device_arena=C.c_void_p(1 << 20))
-    h = C.c_void_p()
-    assert kt.load().kv_tier_init(C.byref(cfg), C.byref(buf), None, C.byref(h)) == -1
+    for sc in (kt.SCORER_WINDOW, kt.SCORER_RKV):
+        cfg = kt.make_config(2, 1, 4, 2, 64, 300, 16, scorer=sc, shard=kt.SHARD_SEQUENCE, world=2, rank=0)
+        buf = kt.Buffers(device_arena=C.c_void_p(1 << 20))
+        h = C.c_void_p()
+        assert kt.load().kv_tier_init(C.byref(cfg), C.byref(buf), None, C.byref(h)) == -1
 
 
 def test_capture_entry_points_reject_null_ctx():

@@ -475,13 +475,17 @@ def _check_seq_event_state(sh, orc, layers=(0, 1)):
                     assert np.array_equal(codes[bg][:, :, 0, :], st.codeK[l, bo][:, pos])
 
 
-@pytest.mark.parametrize("world,staging", [(2, kt.STAGING_ALL), (3, kt.STAGING_ALL), (2, 0)])
-def test_sequence_sharding_matches_unsharded_oracle(world, staging):
+@pytest.mark.parametrize("world,staging,scorer", [(2, kt.STAGING_ALL, 0), (3, kt.STAGING_ALL, 0), (2, 0, 0),
+                                                  (2, kt.STAGING_ALL, kt.SCORER_REDUNDANCY),
+                                                  (3, kt.STAGING_ALL, kt.SCORER_COMBINED)])
+def test_sequence_sharding_matches_unsharded_oracle(world, staging, scorer):
     # world ctxs on one GPU, block-cyclic 64-position ownership; per-layer LSE combine of the
     # ranks' partials, global (M, L) back into the fused score update, summed scores at events;
     # staging 0: each shard re-fetches its own T1 rows from pinned host memory every step
+    # redundancy / combined: every shard appends every new key to its previous-key state, so R_part
+    # is complete on each shard and the gathered classify ranks I - rho exactly as unsharded
     w = H.workload("tiny", B=2, L=2, Hq=8, Hkv=2, d=64, N=400, P=16, interval=8, steps=26,
-                   hbm_bp=4000, evict_bp=800, t2_bp=3000, staging=staging)
+                   hbm_bp=4000, evict_bp=800, t2_bp=3000, staging=staging, scorer=scorer)
     sh = H.SeqShardedDecode(w, world)
     orc = OracleRun(w)
     for t in range(w["steps"]):
@@ -525,7 +529,8 @@ def test_sequence_shard_refuses_plain_paths():
 
 
 @pytest.mark.parametrize("graph,staging,scorer", [(True, kt.STAGING_ALL, 0), (False, kt.STAGING_ALL, 0), (True, 0, 0),
-                                                  (True, kt.STAGING_ALL, kt.SCORER_WINDOW)])
+                                                  (True, kt.STAGING_ALL, kt.SCORER_WINDOW),
+                                                  (True, kt.STAGING_ALL, kt.SCORER_RKV)])
 def test_sequence_shard_library_communicator(graph, staging, scorer):
     # kv_tier_init with an nccl_unique_id: kv_tier_step runs every layer's all-gather of (o, m, l)
     # on the library's NCCL communicator, the LSE combine and the rescaled score update -- the
