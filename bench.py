@@ -552,6 +552,29 @@ def main():
             for name in ("hierarchy", "hierarchy_eager", "hierarchy_stream_mode"):
                 model_leg[name]["overhead_pct_vs_all_hbm"] = 100.0 * (model_leg[name]["ms_per_step"] / b0 - 1.0)
 
+    # ---- configs[3] strong scaling (N > 1): the 32B-shaped batch (B = 32) split over the ranks, so the
+    # whole-job work is fixed as N grows; the driver's SCALE lines stay request-sharded weak scaling
+    strong_leg = None
+    if world > 1 and not args.no_extras:
+        w32 = H.workload("32b", steps=W + K + 66)
+        if w32["B"] % world == 0:
+            w32 = dict(w32, B=w32["B"] // world)
+            sr32 = H.TieredDecode(w32, device=dev, out_fp32=False, split=args.split, seed_offset=seed_off,
+                                  step_kernel=STEP_KERNELS[args.step_kernel])
+            sr32.capture()
+            m32 = measure_tiered(sr32, W, K, w32, local, with_clocks=False)
+            sr32.close()
+            del sr32
+            torch.cuda.empty_cache()
+            t32 = _max_over_ranks(m32["t_amortized"])
+            strong_leg = {"workload": "32b-shaped (BASELINE.json configs[3]): global B=32 split over the ranks, "
+                                      f"B={w32['B']}/GPU L={w32['L']} N={w32['N']}",
+                          "scaling": "strong", "steps_per_s": 1.0 / t32, "ms_per_step": 1e3 * t32,
+                          "tokens_per_s": 32.0 / t32,
+                          "note": "one decode step of the whole 32-request batch = every rank's step; time = max over ranks"}
+        else:
+            strong_leg = {"skipped": f"B=32 does not split over {world} ranks"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_extras:
         cpu = cpu_oracle_sample(w, args.cpu_seconds)
@@ -605,7 +628,7 @@ def main():
                          "algorithmic_bytes_per_launch": int(step_bytes), "peak_src": peaks["src"]},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K * 3 + m["n_events"] * EVENT_LAUNCHES,
             "clocks": m["clocks"],
-            "stream_mode": stream_leg, "host_t1": host_t1_leg, "model_decode": model_leg,
+            "stream_mode": stream_leg, "host_t1": host_t1_leg, "model_decode": model_leg, "strong_32b": strong_leg,
             "context": "paper: 5-7% transfer overhead on RTX 5080 PCIe Gen5, unpinned, 7B int8, batch 1 (P:642)",
         }
         tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
