@@ -32,7 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
-STEP_KERNELS = {"auto": 0, "mma": 1, "tcgen05": 2}                      # kv_tier_config::step_kernel
+STEP_KERNELS = {"auto": 0, "mma": 1, "tcgen05": 2, "layers": 3}                      # kv_tier_config::step_kernel
 CONFIG_INDEX = {"tiny": 0, "7b": 1, "14b": 2, "32b": 3, "70b": 4}      # BASELINE.json configs[i]
 POLICIES = {"hierarchy": 0, "streaming": 1, "h2o": 2, "random": 3}       # kv_tier_policy
 SCORERS = {"attention": 0, "vatp": 1, "redundancy": 2, "combined": 3, "window": 4, "rkv": 5}   # kv_tier_scorer
@@ -678,6 +678,21 @@ def run_sequence_sharded(args, w, world, rank, local, dev, peaks):
     L = w["L"]
     step_bytes = _sum_over_ranks(L * attn_bytes(w, own, n_vis_own))
     sps = K / el_max
+    sr.close()
+    # the same batch request-sharded on one GPU, the same events: per-layer kernels (step_kernel = 3,
+    # the kernels the sequence step runs plus the exchange) and the whole-step kernel
+    ref_rates = None
+    if world == 1 and not args.no_extras:
+        ref_rates = {}
+        for name, sk in (("request_per_layer_kernels", 3), ("request_whole_step_kernel", 0)):
+            rr = H.TieredDecode(w, device=dev, out_fp32=True, step_kernel=sk)
+            rr.capture()
+            for _ in range(W):
+                rr.step()
+            rr.sync()
+            el_r = timed(rr.step, rr.main, K)
+            rr.close()
+            ref_rates[name] = {"steps_per_s": K / el_r, "sequence_over_this": sps / (K / el_r)}
     if rank == 0:
         hbm = step_bytes * sps / 1e9
         print(json.dumps({
@@ -692,12 +707,11 @@ def run_sequence_sharded(args, w, world, rank, local, dev, peaks):
                                                             f"step graph)"},
             "hbm_gbs": hbm, "hbm_frac_of_measured_peak": hbm / (peaks["hbm_gbs"] * world),
             "bytes_per_step": int(step_bytes), "census_rank0_b0": own,
-            "clocks": clk.summary(), "gpu_launches": K * (4 * L + 2),
+            "clocks": clk.summary(), "gpu_launches": K * (4 * L + 2), "request_sharded_n1": ref_rates,
             "note": "one CUDA graph per step: per layer decode + merge + NCCL all-gather + LSE combine + "
                     "score rescale on the library's communicator; events (classify all-gathers S_part) "
                     "inside the window",
         }), flush=True)
-    sr.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

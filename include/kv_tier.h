@@ -171,7 +171,9 @@ typedef struct {
                                 every shape tried), 1 = mma.sync (legacy tensor
                                 path, 16-row slices per warp), 2 = tcgen05 / TMEM (d = 128,
                                 no T2 rows, a cluster per kv head; else the step runs the
-                                mma.sync consumer)                                         */
+                                mma.sync consumer), 3 = none: kv_tier_step / the step graph
+                                run the per-layer kernels (k_decode_attn + merge, chained
+                                with PDL) as sequence shards always do                     */
 } kv_tier_config;
 
 typedef struct kv_tier_ctx kv_tier_ctx;

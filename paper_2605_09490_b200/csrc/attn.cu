@@ -759,19 +759,23 @@ __global__ void k_set_ml(const DevView v, const int zslot, const float* __restri
 // separate k_set_ml (rows = b * H_q + h, kv head h / G)
 __global__ void k_lse_combine(const float* __restrict__ op, const float* __restrict__ lp, const int world,
                               const int rows, const int d, float* __restrict__ oo, float* __restrict__ lo,
-                              float* __restrict__ ml, const int G) {
+                              float* __restrict__ ml, const int G, const size_t rs_o, const size_t rs_l) {
+  // PDL (sequence step): the next layer's decode may launch now (its K/V prologue does not read o);
+  // the parts are read after the producer grid (merge or the all-gather) has completed
+  pdl_trigger();
+  pdl_wait();
   const int d4 = d / 4;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)rows * d4) return;
   const int row = (int)(i / d4), j = (int)(i - (long long)row * d4);
   float M = -INFINITY;
-  for (int r = 0; r < world; ++r) M = fmaxf(M, lp[((size_t)r * rows + row) * 2]);
+  for (int r = 0; r < world; ++r) M = fmaxf(M, lp[r * rs_l + (size_t)row * 2]);
   float L = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int r = 0; r < world; ++r) {
-    const float m = lp[((size_t)r * rows + row) * 2], l = lp[((size_t)r * rows + row) * 2 + 1];
+    const float m = lp[r * rs_l + (size_t)row * 2], l = lp[r * rs_l + (size_t)row * 2 + 1];
     const float wr = m == -INFINITY ? 0.f : ex2_ftz(m - M) * l;
-    const float4 x = reinterpret_cast<const float4*>(op + ((size_t)r * rows + row) * d)[j];
+    const float4 x = reinterpret_cast<const float4*>(op + r * rs_o + (size_t)row * d)[j];
     L += wr;
     acc.x += wr * x.x;
     acc.y += wr * x.y;
@@ -795,9 +799,21 @@ __global__ void k_lse_combine(const float* __restrict__ op, const float* __restr
 }
 
 cudaError_t launch_lse_combine(const float* op, const float* lp, int world, int rows, int d, float* oo, float* lo,
-                               cudaStream_t s, float* ml, int G) {
+                               cudaStream_t s, float* ml, int G, size_t rs_o, size_t rs_l, int pdl) {
   const long long n = (long long)rows * (d / 4);
-  k_lse_combine<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(op, lp, world, rows, d, oo, lo, ml, G);
+  if (!rs_o) rs_o = (size_t)rows * d;
+  if (!rs_l) rs_l = (size_t)rows * 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((n + 255) / 256), 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_lse_combine, op, lp, world, rows, d, oo, lo, ml, G, rs_o, rs_l);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -109,8 +109,8 @@ struct kv_tier_ctx {
   // every layer's (o, m, l) all-gather + LSE combine + score rescale run inside kv_tier_step /
   // the step graph; events all-gather S_part inside kv_tier_classify
   ncclComm_t comm = nullptr;
-  float* x_send = nullptr;                 // [B][H_q][d] o partial, then [B][H_q][2] (m, l)
-  float* x_recv = nullptr;                 // [W][B][H_q][d] o parts, then [W][B][H_q][2] lse parts
+  float* x_recv = nullptr;                 // [W] slots of x_slot floats: [B][H_q][d] o part, then [B][H_q][2] (m, l)
+  size_t x_slot = 0;                       // floats per rank slot (rounded up to 16 B)
   float* x_lse = nullptr;                  // [L][B][H_q][2] global (M, L) per layer
   float* x_scores = nullptr;               // [W][B][H_kv][N_max] all-gathered S_part (events)
   float* x_snaps = nullptr;                // [W][B][H_kv][N_max] all-gathered S_part snapshots (windowed scorers)
@@ -189,8 +189,8 @@ kv_tier_status validate(const kv_tier_config* c) {
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(nullptr, KV_TIER_E_INVAL, "need 0 <= rank < world");
   if (c->split < 0 || c->split > 64) return fail(nullptr, KV_TIER_E_INVAL, "split must be in [0, 64]");
   if (c->variant < 0 || c->variant > 5) return fail(nullptr, KV_TIER_E_INVAL, "variant must be in [0, 5]");
-  if (c->step_kernel < 0 || c->step_kernel > 2)
-    return fail(nullptr, KV_TIER_E_INVAL, "step_kernel must be 0 (auto), 1 (mma.sync) or 2 (tcgen05)");
+  if (c->step_kernel < 0 || c->step_kernel > 3)
+    return fail(nullptr, KV_TIER_E_INVAL, "step_kernel must be 0 (auto), 1 (mma.sync), 2 (tcgen05) or 3 (per-layer kernels)");
   if (c->policy < KV_TIER_POLICY_HIERARCHY || c->policy > KV_TIER_POLICY_RANDOM)
     return fail(nullptr, KV_TIER_E_INVAL, "policy must be a kv_tier_policy");
   if (c->scorer < KV_TIER_SCORER_ATTENTION || c->scorer > KV_TIER_SCORER_RKV)
@@ -551,7 +551,7 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
     cudaGetLastError();                  // persistence is an optimisation: ignore if unsupported
   }
   if (e == cudaSuccess) e = attn_configure(v);
-  if (e == cudaSuccess && !v.stream_mode && v.seq_w <= 1) {
+  if (e == cudaSuccess && !v.stream_mode && v.seq_w <= 1 && cfg->step_kernel != 3) {
     // kv_tier_step / the step graph: all layers in one launch, one thread-block cluster per request
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device);
@@ -590,8 +590,8 @@ kv_tier_status kv_tier_init(const kv_tier_config* cfg, const kv_tier_buffers* bu
       return fail(nullptr, KV_TIER_E_NCCL, "ncclCommInitRank: %s", nccl_api().error_string(r));
     }
     const size_t rows = (size_t)v.B * v.Hq, W = (size_t)cfg->world;
-    e = cudaMalloc(&ctx->x_send, rows * (v.D + 2) * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&ctx->x_recv, W * rows * (v.D + 2) * 4);
+    ctx->x_slot = (rows * (v.D + 2) + 3) & ~(size_t)3;
+    e = cudaMalloc(&ctx->x_recv, W * ctx->x_slot * 4);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->x_lse, (size_t)v.L * rows * 2 * 4);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->x_scores, W * v.B * v.Hkv * (size_t)v.Nmax * 4);
     if (e == cudaSuccess && v.snap) e = cudaMalloc(&ctx->x_snaps, W * v.B * v.Hkv * (size_t)v.Nmax * 4);
@@ -644,7 +644,7 @@ kv_tier_status kv_tier_destroy(kv_tier_ctx* ctx) {
   if (ctx->d1_parts) cudaFree(ctx->d1_parts);
   if (ctx->ev_q) cudaEventDestroy(ctx->ev_q);
   if (ctx->comm) nccl_api().comm_destroy(ctx->comm);
-  for (float* p : {ctx->x_send, ctx->x_recv, ctx->x_lse, ctx->x_scores, ctx->x_snaps})
+  for (float* p : {ctx->x_recv, ctx->x_lse, ctx->x_scores, ctx->x_snaps})
     if (p) cudaFree(p);
   delete ctx;
   return KV_TIER_OK;
@@ -1052,10 +1052,11 @@ static kv_tier_status seq_step(kv_tier_ctx* ctx, const void* q, const void* k_ne
   const char* kb = reinterpret_cast<const char*>(k_new);
   const char* vb = reinterpret_cast<const char*>(v_new);
   float* ob = reinterpret_cast<float*>(o);
-  float* o_send = ctx->x_send;
-  float* l_send = ctx->x_send + rows * v.D;
-  float* o_recv = ctx->x_recv;
-  float* l_recv = ctx->x_recv + W * rows * v.D;
+  // in-place all-gather: this rank's partial is written straight into its own slot of the receive
+  // buffer, one packed (o, m, l) slot per rank -> one ncclAllGather per layer, no send copy
+  const size_t slot = ctx->x_slot;
+  float* o_send = ctx->x_recv + (size_t)ctx->cfg.rank * slot;
+  float* l_send = o_send + rows * v.D;
   kv_tier_status st = kv_tier_begin_step(ctx, stream);
   if (v.stream_mode)
     for (int l = 0; l < std::min(2, v.L) && !st; ++l) st = kv_tier_prefetch(ctx, l, side);
@@ -1067,19 +1068,14 @@ static kv_tier_status seq_step(kv_tier_ctx* ctx, const void* q, const void* k_ne
     if (st) break;
     // (also at world 1, where it is a copy: the one-GPU tests then run the multi-rank code path)
     const NcclApi& nc = nccl_api();
-    ncclResult_t r = nc.group_start();
-    if (r == ncclSuccess) r = nc.all_gather(o_send, o_recv, rows * v.D, ncclFloat32, ctx->comm, s);
-    if (r == ncclSuccess) r = nc.all_gather(l_send, l_recv, rows * 2, ncclFloat32, ctx->comm, s);
-    const ncclResult_t r2 = nc.group_end();
-    if (r == ncclSuccess) r = r2;
+    const ncclResult_t r = nc.all_gather(o_send, ctx->x_recv, slot, ncclFloat32, ctx->comm, s);
     if (r != ncclSuccess) return fail(ctx, KV_TIER_E_NCCL, "layer %d all-gather: %s", l, nc.error_string(r));
-    const float* o_src = o_recv;
-    const float* l_src = l_recv;
     float* lse_l = ctx->x_lse + (size_t)l * rows * 2;
     // the combine also writes the pending score slot's (M, 1/L): no separate set_ml launch
     float* mlz = v.ml + (size_t)ctx->lse_pending * v.B * v.Hkv * 16;
-    st = cuda_check(ctx, launch_lse_combine(o_src, l_src, (int)W, (int)rows, v.D, ob + (size_t)l * qs, lse_l, s,
-                                            mlz, v.G), "lse_combine");
+    st = cuda_check(ctx, launch_lse_combine(ctx->x_recv, ctx->x_recv + rows * v.D, (int)W, (int)rows, v.D,
+                                            ob + (size_t)l * qs, lse_l, s, mlz, v.G, slot, slot,
+                                            v.stream_mode ? 0 : 1), "lse_combine");
     if (!st) st = score_update_lse_impl(ctx, lse_l, stream, true);
     if (!st && v.stream_mode && l + 2 < v.L) st = kv_tier_prefetch(ctx, l + 2, side);
   }

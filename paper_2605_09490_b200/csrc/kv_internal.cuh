@@ -268,7 +268,9 @@ cudaError_t launch_vnorm_prefix(const DevView& v, int layer, const void* vv, int
 cudaError_t launch_t1_score_add(const DevView& v, const float* inc, cudaStream_t s);
 cudaError_t launch_redund_prefix(const DevView& v, int layer, const void* k, int n0, cudaStream_t s);
 cudaError_t launch_lse_combine(const float* op, const float* lp, int world, int rows, int d, float* oo, float* lo,
-                               cudaStream_t s, float* ml = nullptr, int G = 1);
+                               cudaStream_t s, float* ml = nullptr, int G = 1, size_t rs_o = 0, size_t rs_l = 0,
+                               int pdl = 0);
+// rs_o / rs_l: floats between consecutive ranks' o / (m, l) parts (0 = packed: rows * d, rows * 2)
 cudaError_t launch_score_flush(const DevView& v, int zfirst, int nz, cudaStream_t s);
 cudaError_t launch_score_update(const DevView& v, int layer, const float* probs, cudaStream_t s);
 cudaError_t launch_end_step(const DevView& v, cudaStream_t s);

@@ -124,7 +124,7 @@ def test_lse_combine_rejects_bad_arguments():
 
 
 @pytest.mark.parametrize("field,value", [("policy", 9), ("scorer", 6), ("scorer", -1), ("budget", 0),
-                                         ("step_kernel", 3)])
+                                         ("step_kernel", 4), ("step_kernel", -1)])
 def test_policy_and_scorer_validation(field, value):
     kw = dict(policy=kt.POLICY_H2O, budget=100)
     kw[field] = value

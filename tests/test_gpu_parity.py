@@ -276,6 +276,23 @@ def test_step_kernel_matches_layer_kernel():
     a.close(); b.close()
 
 
+def test_step_kernel_none_runs_the_layer_kernels():
+    # step_kernel = 3: kv_tier_step / the step graph run the per-layer kernels -> bit-identical to
+    # driving decode_attention layer by layer (same kernels, same split, same order)
+    w = H.workload("tiny", interval=8, B=3, L=3, t2_bp=3000, Hq=12, Hkv=2, d=128, N=700, P=40)
+    a = H.TieredDecode(w)
+    b = H.TieredDecode(w, step_kernel=3)
+    assert b.kv.layout()[1][0] == 0            # no whole-step kernel shape
+    b.capture()
+    for t in range(w["steps"]):
+        a.step_layers()
+        b.step()
+        assert np.array_equal(a.output(), b.output()), t
+    a.sync(); b.sync()
+    assert np.array_equal(a.kv.export(kt.X_SCORES), b.kv.export(kt.X_SCORES))
+    a.close(); b.close()
+
+
 def test_stream_mode_equals_differential_bitwise():   # same rows, same order -> same bits
     # both through the per-layer kernels (stream mode always runs them; the differential run
     # uses the per-layer ABI so the work split is the same)
@@ -914,7 +931,7 @@ def test_randomized_configs(seed):
                                                              kt.SCORER_COMBINED, kt.SCORER_WINDOW,
                                                              kt.SCORER_RKV])))
     api = int(rng.integers(0, 3))             # step graph / kv_tier_step (whole-step kernel) / per-layer ABI
-    sk = int(rng.choice([0, 2]))              # whole-step kernel consumer: mma.sync / tcgen05 (where it applies)
+    sk = int(rng.choice([0, 2, 3]))           # whole-step consumer: mma.sync / tcgen05 (where it applies) / none
     _run_pair(w, graph=api == 0, layers_api=api == 2, check_every=3, step_kernel=sk)
 
 
