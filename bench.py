@@ -530,12 +530,14 @@ def main():
                          "note": "random bf16 weights, RMSNorm + GEMMs + SiLU in torch/cuBLAS, no RoPE / LM head; "
                                  "each decoder step is ONE CUDA graph (torch.cuda.graph around the library's "
                                  "kv_tier_capture_begin/_end, kv_tier_graph_advance per replay) except "
-                                 "hierarchy_eager; the Delta-step window holds one classify/migrate event"}
+                                 "hierarchy_eager; the Delta-step window holds one classify/migrate event; the "
+                                 "prefix K/V come from the decoder's own causal prefill over N-1 random prompt "
+                                 "embeddings (Alg. 1 line 1), the first decode input is the prompt's last output"}
             for name, extra, graph in (("all_hbm_no_eviction", dict(hbm_bp=10000, evict_bp=0), True),
                                        ("hierarchy", {}, True), ("hierarchy_eager", {}, False),
                                        ("hierarchy_stream_mode", dict(staging=0), True)):
                 md = H.ModelDecode(dict(w, **extra), hidden=hidden, inter=inter, device=dev,
-                                   split=args.split, seed_offset=seed_off)
+                                   split=args.split, seed_offset=seed_off, prefill=True)
                 for _ in range(Wm):
                     md.step()
                 if graph:

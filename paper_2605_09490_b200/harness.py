@@ -31,12 +31,14 @@ class TieredDecode:
 
     def __init__(self, w, device="cuda:0", out_fp32=True, split=0, seed_offset=0, keep_inputs=False, variant=0,
                  heads=None, classify_fn=None, shard=kt.SHARD_REQUEST, rank=0, world=1, nccl_id=None,
-                 step_kernel=0):
+                 step_kernel=0, prefix_fn=None):
         """heads = (first kv head, count): this ctx holds only those kv heads and their q
         heads (KV-head sharding); classify_fn(run, stream) replaces kv.classify at events
         (e.g. dist.kvhead_classify, or a single-process gather over several ctxs); nccl_id:
         sequence sharding on the library's own communicator (kv_tier_step / the step graph
-        run the per-layer exchange, kv_tier_classify the event's all-gather)."""
+        run the per-layer exchange, kv_tier_classify the event's all-gather); prefix_fn(l) ->
+        (K, V) [B][H_kv][N-1][d] bf16 on the device: the prefix of layer l from a prefill (called
+        in layer order) instead of the synthetic generator."""
         self.w = w
         self.dev = torch.device(device)
         torch.cuda.set_device(self.dev)
@@ -61,7 +63,14 @@ class TieredDecode:
         self.main = torch.cuda.Stream(self.dev)
         self.side = torch.cuda.Stream(self.dev)
         with torch.cuda.stream(self.main):
-            if keep_inputs:
+            if prefix_fn is not None:        # Alg. 1 line 1: C <- Prefill(M, x_1:P), layer by layer
+                assert heads is None and not keep_inputs
+                for l in range(L):
+                    Kl, Vl = prefix_fn(l)
+                    self.kv.load_prefix(l, Kl, Vl, self.n0, stream=self.main)
+                    self.main.synchronize()
+                    del Kl, Vl
+            elif keep_inputs:
                 K = SG.gen_kv(self.seed, "k", L, B, Hkv, d, 0, self.n0, P, S.SINK_SIZE, self.dev, stream=self.main)
                 V = SG.gen_kv(self.seed, "v", L, B, Hkv, d, 0, self.n0, P, S.SINK_SIZE, self.dev, stream=self.main)
                 if heads is not None:
@@ -174,14 +183,17 @@ class ModelDecode:
     per-layer dependency: q/k/v come from this layer's projections of the previous layer's
     output, and the T1 prefetch of layer l+2 (stream mode) overlaps layer l's MLP.
     Non-attention layers are plain torch/cuBLAS (RMSNorm, GEMMs, SiLU; no RoPE, no LM head):
-    they are the context, not the product.  The prefix K/V are the synthetic generator's."""
+    they are the context, not the product.  The prefix K/V are the synthetic generator's, or with
+    prefill=True the model's own: Alg. 1 line 1, C <- Prefill(M, x_1:P) -- a causal
+    forward (torch SDPA, GQA) over N-1 random prompt embeddings, each layer's K/V loaded as that
+    layer's prefix, and the last prompt position's output is the first decode input."""
 
-    def __init__(self, w, hidden=3584, inter=18944, device="cuda:0", **kw):
+    def __init__(self, w, hidden=3584, inter=18944, device="cuda:0", prefill=False, keep_prefill=False, **kw):
         import math
         self.w, self.hidden, self.inter = w, hidden, inter
-        self.run = TieredDecode(w, device=device, out_fp32=False, **kw)
         B, L, Hq, Hkv, d = w["B"], w["L"], w["Hq"], w["Hkv"], w["d"]
-        dev = self.run.dev
+        dev = torch.device(device)
+        torch.cuda.set_device(dev)
         g = torch.Generator(device=dev).manual_seed(w["seed"] + 17)
 
         def W(i, o):
@@ -190,10 +202,37 @@ class ModelDecode:
         self.layers = [dict(wqkv=W(hidden, (Hq + 2 * Hkv) * d), wo=W(Hq * d, hidden), wgu=W(hidden, 2 * inter),
                             wd=W(inter, hidden)) for _ in range(L)]
         self.x = torch.randn(B, hidden, generator=g, device=dev).to(torch.bfloat16)
+        self.prefill_kv = [] if keep_prefill else None
+        if prefill:
+            self._H = torch.randn(B, w["N"] - 1, hidden, generator=g, device=dev).to(torch.bfloat16)
+            torch.cuda.synchronize(dev)              # weights and prompt drawn on torch's stream
+            self.run = TieredDecode(w, device=device, out_fp32=False, prefix_fn=self._prefill_layer, **kw)
+            self.x = self._rms(self._H[:, -1])
+            self._H = None
+        else:
+            self.run = TieredDecode(w, device=device, out_fp32=False, **kw)
         self.O = torch.empty((B, Hq, d), dtype=torch.bfloat16, device=dev)
         # the weights were drawn on torch's current stream; the steps run on the ctx's main
         # stream (non-blocking w.r.t. it): order them
         self.run.main.wait_stream(torch.cuda.current_stream(dev))
+
+    def _prefill_layer(self, l):
+        """Layer l of the prefill over the prompt's hidden states (causal attention over the
+        prompt); returns the layer's K, V [B][H_kv][n][d] and advances the hidden states."""
+        w, p, Hs = self.w, self.layers[l], self._H
+        B, n = Hs.shape[0], Hs.shape[1]
+        Hq, Hkv, d = w["Hq"], w["Hkv"], w["d"]
+        qkv = self._rms(Hs) @ p["wqkv"]
+        q = qkv[..., :Hq * d].reshape(B, n, Hq, d).transpose(1, 2)
+        k = qkv[..., Hq * d:(Hq + Hkv) * d].reshape(B, n, Hkv, d).transpose(1, 2).contiguous()
+        v = qkv[..., (Hq + Hkv) * d:].reshape(B, n, Hkv, d).transpose(1, 2).contiguous()
+        a = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+        Hs = Hs + a.transpose(1, 2).reshape(B, n, Hq * d) @ p["wo"]
+        gu = self._rms(Hs) @ p["wgu"]
+        self._H = Hs + (torch.nn.functional.silu(gu[..., :self.inter]) * gu[..., self.inter:]) @ p["wd"]
+        if self.prefill_kv is not None:
+            self.prefill_kv.append((k.clone(), v.clone()))
+        return k, v
 
     @staticmethod
     def _rms(x):

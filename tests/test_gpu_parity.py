@@ -851,6 +851,67 @@ def test_model_decode_stream_mode_equals_differential_and_prop1():
     assert rel <= 2e-2, rel
 
 
+def _ref_decoder_step(m, x, caches):
+    """Plain torch decoder step over whole K/V caches (no tiers): the model's own prefill K/V
+    plus every appended row, fp32 softmax over all positions (Eq. 3 with nothing evicted)."""
+    w = m.w
+    B, Hq, Hkv, d = w["B"], w["Hq"], w["Hkv"], w["d"]
+    G = Hq // Hkv
+    for l, p in enumerate(m.layers):
+        qkv = m._rms(x) @ p["wqkv"]
+        q = qkv[:, :Hq * d].reshape(B, Hq, d).float()
+        k = qkv[:, Hq * d:(Hq + Hkv) * d].reshape(B, Hkv, 1, d)
+        v = qkv[:, (Hq + Hkv) * d:].reshape(B, Hkv, 1, d)
+        K = torch.cat([caches[l][0], k], dim=2)
+        V = torch.cat([caches[l][1], v], dim=2)
+        caches[l] = (K, V)
+        Kq = K.float().repeat_interleave(G, dim=1)                  # [B][Hq][n][d]
+        Vq = V.float().repeat_interleave(G, dim=1)
+        a = torch.softmax(torch.einsum("bhd,bhnd->bhn", q, Kq) / np.sqrt(d), dim=-1)
+        o = torch.einsum("bhn,bhnd->bhd", a, Vq).to(torch.bfloat16)
+        x = x + o.reshape(B, Hq * d) @ p["wo"]
+        gu = m._rms(x) @ p["wgu"]
+        x = x + (torch.nn.functional.silu(gu[:, :m.inter]) * gu[:, m.inter:]) @ p["wd"]
+    return m._rms(x)
+
+
+def test_model_prefill_initial_tiers_and_decode():
+    # Alg. 1 line 1 (P:173): C <- Prefill(M, x_1:P).  The decoder's own causal prefill produces
+    # every layer's prefix K/V, the library loads them as the initial cache, and the decode
+    # continues from the last prompt position.  With beta = 100 %, r = 0 (nothing leaves T0, Prop. 1)
+    # the tiered decoder equals a plain torch decoder over the whole caches, step after step,
+    # across the manage events; the t = 0 event classifies exactly the prefill's positions.
+    base = dict(B=2, L=3, Hq=8, Hkv=2, d=64, N=300, P=16, interval=4, steps=9, evict_bp=0, hbm_bp=10000)
+    m = H.ModelDecode(H.workload("tiny", **base), hidden=256, inter=512, prefill=True, keep_prefill=True)
+    caches = list(m.prefill_kv)
+    assert len(caches) == base["L"] and caches[0][0].shape == (2, 2, base["N"] - 1, 64)
+    x = m.x.clone()
+    for t in range(base["steps"]):
+        got = m.step()
+        x = _ref_decoder_step(m, x, caches)
+        a, b = got.float().cpu().numpy().astype(np.float64), x.float().cpu().numpy().astype(np.float64)
+        rel = np.linalg.norm(a - b) / np.linalg.norm(b)
+        assert rel <= 2e-2, (t, rel)
+        x = got.clone()                      # both continue from the library's hidden state
+    m.sync()
+    counts, _ = m.run.kv.layout()
+    assert counts[3] == 0 and counts[0] == base["N"] - 1 + base["steps"]
+    m.close()
+
+
+def test_model_prefill_tiers_with_eviction():
+    # the same prefill at beta 50 %, r 5 %: the t = 0 event splits the prefill's positions by
+    # their step-0 scores (Alg. 1 lines 17-25); the census adds up and the decode stays finite
+    base = dict(B=2, L=3, Hq=8, Hkv=2, d=64, N=300, P=16, interval=4, steps=6, evict_bp=500, hbm_bp=5000)
+    m = H.ModelDecode(H.workload("tiny", **base), hidden=256, inter=512, prefill=True)
+    outs = [m.step().float().cpu().numpy() for _ in range(base["steps"])]
+    m.sync()
+    counts, _ = m.run.kv.layout()
+    assert sum(counts) == base["N"] - 1 + base["steps"] and counts[1] > 0 and counts[3] > 0
+    assert np.all(np.isfinite(np.stack(outs)))
+    m.close()
+
+
 @pytest.mark.parametrize("staging", [kt.STAGING_ALL, 0])
 def test_model_decode_graph_equals_eager(staging):
     # the whole decoder step as one CUDA graph (torch.cuda.graph around kv_tier_capture_begin /
