@@ -681,6 +681,9 @@ def run_sequence_sharded(args, w, world, rank, local, dev, peaks):
     step_bytes = _sum_over_ranks(L * attn_bytes(w, own, n_vis_own))
     sps = K / el_max
     sr.close()
+    del sr, run
+    import torch
+    torch.cuda.empty_cache()
     # the same batch request-sharded on one GPU, the same events: per-layer kernels (step_kernel = 3,
     # the kernels the sequence step runs plus the exchange) and the whole-step kernel
     ref_rates = None
@@ -694,6 +697,8 @@ def run_sequence_sharded(args, w, world, rank, local, dev, peaks):
             rr.sync()
             el_r = timed(rr.step, rr.main, K)
             rr.close()
+            del rr
+            torch.cuda.empty_cache()
             ref_rates[name] = {"steps_per_s": K / el_r, "sequence_over_this": sps / (K / el_r)}
     if rank == 0:
         hbm = step_bytes * sps / 1e9
