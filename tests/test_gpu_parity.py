@@ -1004,7 +1004,8 @@ def test_randomized_sequence_shards(seed):
                    Hkv=Hkv, d=int(rng.choice([64, 128])), N=int(rng.integers(100, 700)), P=int(rng.integers(0, 40)),
                    interval=int(rng.choice([4, 8])), steps=int(rng.integers(8, 18)), hbm_bp=int(rng.integers(0, 10001)),
                    evict_bp=int(rng.integers(0, 1500)), t2_bp=int(rng.choice([0, 3000])),
-                   staging=int(rng.choice([kt.STAGING_ALL, 0])))
+                   staging=int(rng.choice([kt.STAGING_ALL, 0])),
+                   scorer=int(rng.choice([0, 0, kt.SCORER_VATP, kt.SCORER_REDUNDANCY, kt.SCORER_COMBINED])))
     sh = H.SeqShardedDecode(w, int(rng.integers(2, 5)))
     orc = OracleRun(w)
     for t in range(w["steps"]):
