@@ -87,7 +87,8 @@ typedef enum { KV_TIER_EVICT_TOTAL = 0, KV_TIER_EVICT_PER_EVENT = 1 } kv_tier_ev
  *            WITH a communicator (kv_tier_init given an nccl_unique_id from
  *            kv_tier_nccl_unique_id, one per job, every rank passing the same bytes): kv_tier_step
  *            and the step graph run the whole step on the library's NCCL communicator -- per
- *            layer decode_attention_lse -> ncclAllGather of every rank's (o, m, l) -> the LSE
+ *            layer decode_attention_lse (the rank's (o, m, l) written straight into its own slot
+ *            of a packed receive buffer) -> ONE in-place ncclAllGather of the slots -> the LSE
  *            combine (rank order, deterministic) into o -> kv_tier_score_update_lse -- captured
  *            as one CUDA graph; kv_tier_classify all-gathers S_part itself.  out_fp32 must be 1. */
 typedef enum { KV_TIER_SHARD_REQUEST = 0, KV_TIER_SHARD_KVHEAD = 1, KV_TIER_SHARD_SEQUENCE = 2 } kv_tier_shard;
