@@ -17,6 +17,8 @@ if os.environ.get("KVT_TRACE"):             # debug builds: per-(layer, CTA) tim
     FLAGS += ["-DKVT_TRACE=1"]
 if os.environ.get("KVT_INLINE_OFFLOAD"):    # A/B builds: the event's host offload inside the migrate kernel
     FLAGS += ["-DKVT_INLINE_OFFLOAD=1"]
+if os.environ.get("KVT_SLEEP_CHAIN"):       # A/B builds: suspend (not spin) on the step kernel's layer chain
+    FLAGS += ["-DKVT_SPIN_CHAIN=0"]
 
 TARGETS = {
     "libkvtier.so": ["csrc/ctx.cu", "csrc/attn.cu", "csrc/tiers.cu", "csrc/step.cu"],

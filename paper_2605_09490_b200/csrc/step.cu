@@ -71,7 +71,17 @@ __device__ __forceinline__ void red_relaxed_gpu(int* p, int x) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(x) : "memory");
 }
 // CTA-local mbarrier wait that suspends until the phase completes (no issue slots while waiting)
-__device__ __forceinline__ void mbar_sleep_wait(uint32_t a, uint32_t parity) { mbar_wait_hint(a, parity, 1000000u); }
+#ifndef KVT_SPIN_CHAIN
+// the layer chain's barriers and counter are polled without suspending: the hand-offs sit on the
+// step's critical path (7B, same box: 254.4 vs 257.7 us/step with a 1 us suspend hint and a 64 ns
+// sleep per counter poll; profiles/r02/spin_ab_r02.md).  -DKVT_SPIN_CHAIN=0 builds the suspending
+// variant for A/B runs.
+#define KVT_SPIN_CHAIN 1
+#endif
+__device__ __forceinline__ void mbar_sleep_wait(uint32_t a, uint32_t parity) {
+  if (KVT_SPIN_CHAIN) mbar_wait(a, parity);
+  else mbar_wait_hint(a, parity, 1000000u);
+}
 
 // ----------------------------------------------------------------- work split
 // Geometry (host side, step_plan in ctx.cu): R = H_kv * s / m CTAs per request; s > 1: a
@@ -207,7 +217,7 @@ __global__ void __launch_bounds__((NW + 4 + (UM ? 1 : 0)) * 32, (NW <= 4 && !UM)
     if (ld_relaxed_gpu(p) < R) {
       const unsigned long long t0 = gtimer();
       for (unsigned it = 1; ld_relaxed_gpu(p) < R; ++it) {
-        __nanosleep(64);
+        if (!KVT_SPIN_CHAIN) __nanosleep(64);
         if ((it & 255u) == 0 && gtimer() - t0 > 2000000000ull) {   // watchdog: report, never hang the device
           atomicOr(&v.st->err, 4);
           break;
