@@ -16,11 +16,12 @@ def main():
     ap.add_argument("--config", default="7b")
     ap.add_argument("--steps", type=int, default=56)
     ap.add_argument("--splits", default="0,2,3,4,5,6,7,8,9,10,12")
+    ap.add_argument("--positions", type=int, default=0, help="override N (positions per request)")
     a = ap.parse_args()
     import torch
     from paper_2605_09490_b200 import harness as H
     for s in (int(x) for x in a.splits.split(",")):
-        w = H.workload(a.config, steps=a.steps + 12)
+        w = H.workload(a.config, steps=a.steps + 12, **({"N": a.positions} if a.positions else {}))
         try:
             run = H.TieredDecode(w, out_fp32=False, split=s)
         except Exception as e:      # noqa: BLE001 - report the shape as not placeable
