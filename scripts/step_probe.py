@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--config", default="7b")
     ap.add_argument("--steps", type=int, default=32)
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--positions", type=int, default=0, help="override N (positions per request)")
     ap.add_argument("--t2", type=int, default=0)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--step-kernel", type=int, default=0, help="kv_tier_config::step_kernel (2 = tcgen05)")
@@ -26,6 +27,8 @@ def main():
     import torch
     from paper_2605_09490_b200 import harness as H
     over = {"B": a.batch} if a.batch else {}
+    if a.positions:
+        over["N"] = a.positions
     for fuse in (1, 0):
         w = H.workload(a.config, steps=a.steps + 10, t2_bp=a.t2, **over)
         run = H.TieredDecode(w, out_fp32=False, step_kernel=a.step_kernel)
