@@ -266,9 +266,8 @@ def _event_step(run, timing):
     import torch
     t = run.t
     with torch.cuda.stream(run.main):
-        run.qbuf.copy_(run.Q[t], non_blocking=True)
-        run.kbuf.copy_(run.Kn[t], non_blocking=True)
-        run.vbuf.copy_(run.Vn[t], non_blocking=True)
+        # the step's inputs into the graph's fixed buffers: one multi-tensor copy launch
+        torch._foreach_copy_([run.qbuf, run.kbuf, run.vbuf], [run.Q[t], run.Kn[t], run.Vn[t]], non_blocking=True)
         run.kv.step_graph_launch(stream=run.main)
         if run.is_event(t):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

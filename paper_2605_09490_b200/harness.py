@@ -127,9 +127,8 @@ class TieredDecode:
         t = self.t
         with torch.cuda.stream(self.main):
             if self.graph:
-                self.qbuf.copy_(self.Q[t], non_blocking=True)
-                self.kbuf.copy_(self.Kn[t], non_blocking=True)
-                self.vbuf.copy_(self.Vn[t], non_blocking=True)
+                torch._foreach_copy_([self.qbuf, self.kbuf, self.vbuf], [self.Q[t], self.Kn[t], self.Vn[t]],
+                                     non_blocking=True)          # one multi-tensor copy launch
                 self.kv.step_graph_launch(stream=self.main)
             else:
                 self.kv.step(self.Q[t], self.Kn[t], self.Vn[t], self.O, 1, stream=self.main, side=self.side)
